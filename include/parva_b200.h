@@ -1,0 +1,231 @@
+/*
+ * parva_b200.h — C ABI of the B200-native ParvaGPU scheduling hot path.
+ *
+ * The reference (arXiv 2409.14447's `migplan`, pure Python) has no FFI; its
+ * drop-in boundary is the Python API in pkg/src/migplan/__init__.py:12-74.
+ * Each entry point below replaces a batch of calls to that API:
+ *
+ *   parva_configure_sweep  <- configure_service(service, table) per query
+ *                             (configurator.py:189-191 = decide_best_triplets
+ *                             :93-124 + select_optimal_segment :127-139 +
+ *                             match_demand :142-186)
+ *   parva_build_index      <- (no reference equivalent) latency-sorted
+ *                             prefix-argmax index of prepared tables, so
+ *                             many queries per table cost O(log n)
+ *   parva_plan_batch       <- plan_services(services, tables, options) per
+ *                             scenario, timed region pipeline.py:95-103:
+ *                             configure -> relocate_segments
+ *                             (allocator.py:292-316) -> optimize_allocation
+ *                             (allocator.py:362-443)
+ *   parva_plan_general     <- relocate_segments / optimize_allocation on
+ *                             arbitrary service sets and DeploymentMaps
+ *                             (no size limits; also the overflow path of
+ *                             parva_plan_batch)
+ *
+ * All pointers named d_* are device pointers; `stream` is a cudaStream_t
+ * (void* here so the header needs no CUDA include).  Calls are
+ * stream-ordered and asynchronous; they return a parva_status for argument
+ * errors and launch failures only — per-row results are in the records.
+ * parva_plan_host is the host-buffer convenience entry (copies inside).
+ * No entry allocates device memory except through the caller's workspace.
+ */
+#ifndef PARVA_B200_H
+#define PARVA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PARVA_ABI_VERSION 1
+
+/* instance sizes by size class c: 1, 2, 3, 4, 7 GPCs (mig.py:19) */
+#define PARVA_NUM_SIZES 5
+
+/* per-row status codes */
+enum parva_status {
+  PARVA_OK = 0,
+  PARVA_INFEASIBLE_SLO = 1,        /* InfeasibleSLOError (configurator.py:110-111)   */
+  PARVA_RESIDUAL_UNCOVERABLE = 2,  /* ResidualUncoverableError (configurator.py:173)  */
+  PARVA_COUNT_OVERFLOW = 3,        /* rate/throughput not a finite int64 (math.floor)   */
+  PARVA_CAPACITY = 4,              /* fast-path record limits exceeded: re-plan general */
+  PARVA_BAD_INPUT = 5,
+  PARVA_COVERAGE_ASSERT = 6,       /* optimize coverage assert (allocator.py:437-442)   */
+  PARVA_LAUNCH_ERROR = 7
+};
+
+/* diagnostic reasons (allocator.py:394,401,410-412,432-434) */
+enum parva_diag_reason {
+  PARVA_DIAG_SMALL_UNAVAILABLE = 0, /* "service 'x' has no size-1 or size-2 triplet"      */
+  PARVA_DIAG_NEED_NEW_GPU = 1,      /* "replacements for GPU g would need a new GPU; ..." */
+  PARVA_DIAG_UNKNOWN_SERVICE = 2,   /* "unknown service 'x'"                               */
+  PARVA_DIAG_REGRESSED = 3          /* "optimization regressed GPU count or ..."          */
+};
+
+/* Prepared profile tables (filter_feasible + optional restrict applied,
+ * pipeline.py:70-80), structure of arrays grouped by (table, size class):
+ * segment s = t*5 + c holds points [seg_start[s], seg_start[s] + seg_count[s])
+ * in key order (batch asc, procs asc; profiles.py:98-100).  Within a segment
+ * the point's position is its tie-break rank, so no key array is read. */
+typedef struct {
+  const double*  d_tp;        /* throughput, rps        [n_points] */
+  const double*  d_lat;       /* latency, ms            [n_points] */
+  const int64_t* d_seg_start; /* [n_tables * 5]                    */
+  const int32_t* d_seg_count; /* [n_tables * 5]                    */
+  int32_t n_tables;
+  int64_t n_points;
+} parva_tables;
+
+/* Latency-sorted prefix-argmax index over the same segments (same offsets).
+ * lat_sorted[seg_start[s] + j] ascending; best[seg_start[s] + j] is the
+ * within-segment position of the argmax of the first j+1 sorted points under
+ * (tp desc, lat asc, position asc). */
+typedef struct {
+  double*   d_lat_sorted;     /* [n_points]                      */
+  uint16_t* d_best;           /* [n_points]                      */
+} parva_index;
+
+/* 32-byte per-service configuration record (a Service after match_demand). */
+typedef struct {
+  int16_t best[PARVA_NUM_SIZES]; /* within-segment point position, -1 = size absent */
+  int8_t  opt_sc;                /* optimal_segment size class, -1 = none           */
+  int8_t  last_sc;               /* last_segment size class, -1 = none              */
+  uint8_t status;                /* parva_status                                    */
+  uint8_t flags;
+  int16_t reserved;
+  int64_t count;                 /* optimal_segment_count                           */
+  double  coverage;              /* Service.coverage (Python 3.12 sum, Neumaier)    */
+} parva_config_record;
+
+/* 128-byte per-scenario plan record (fast path: <=32 services, <=32 GPUs,
+ * <=40 final placements, <=20 diagnostics; else status PARVA_CAPACITY).
+ *   place[i] = gpu << 11 | cat << 3 | slot,  cat = service * 5 + size class
+ *   diag[i]  = gpu << 7 | reason << 5 | service
+ * GPU ids equal relocation indices (allocator.py:280-281 on a fresh map);
+ * placements are listed GPU by GPU in final-map order, each GPU's list in
+ * list order (the order optimize_allocation leaves them in). */
+#define PARVA_PLAN_MAX_PLACE 40
+#define PARVA_PLAN_MAX_DIAG 20
+#define PARVA_PLAN_MAX_GPUS 32
+#define PARVA_PLAN_MAX_SERVICES 32
+#define PARVA_FLAG_FALLBACK 1u   /* regression fallback: map = relocation result */
+
+typedef struct {
+  uint8_t  status;
+  uint8_t  err_service;   /* scenario-local index of the first failing service */
+  uint8_t  n_gpus;        /* final map                                         */
+  uint8_t  n_gpus_unopt;  /* PlanResult.unoptimized_gpu_count (pipeline.py:98) */
+  uint8_t  n_place;
+  uint8_t  n_diag;
+  uint8_t  flags;
+  uint8_t  total_gpcs;
+  uint16_t place[PARVA_PLAN_MAX_PLACE];
+  uint16_t diag[PARVA_PLAN_MAX_DIAG];
+} parva_plan_record;
+
+/* ---------------------------------------------------------------- entries */
+
+int parva_abi_version(void);
+
+/* Device bytes of workspace parva_plan_batch needs (0 today; reserved). */
+size_t parva_plan_batch_workspace(int32_t n_scenarios, int32_t n_services);
+
+/* Build the prefix-argmax index of `tables` into `index` (both device). */
+int parva_build_index(const parva_tables* tables, parva_index* index, void* stream);
+
+/* One query per row: table id, request rate, internal latency bound
+ * (Service.internal_latency = slo / 2 by default, configurator.py:87-89).
+ * Streams each queried table once from HBM; HBM-bound. */
+int parva_configure_sweep(const parva_tables* tables, int32_t n_queries,
+                          const int32_t* d_q_table, const double* d_q_rate,
+                          const double* d_q_bound, parva_config_record* d_out,
+                          void* stream);
+
+/* Plan n_scenarios independent scenarios.  Scenario k owns services
+ * [d_scen_off[k], d_scen_off[k+1]); service i queries table d_svc_table[i].
+ * Writes one config record per service and one plan record per scenario;
+ * d_ledger_val / d_ledger_order (optional, may be NULL) receive the
+ * freed_rate ledger per service (order 0 = key absent, else 1-based
+ * insertion rank).  index must have been built from tables. */
+int parva_plan_batch(const parva_tables* tables, const parva_index* index,
+                     int32_t n_scenarios, const int32_t* d_scen_off,
+                     const int32_t* d_svc_table, const double* d_svc_rate,
+                     const double* d_svc_bound, int32_t optimize, int32_t threshold,
+                     parva_config_record* d_cfg, parva_plan_record* d_plan,
+                     double* d_ledger_val, uint8_t* d_ledger_order, void* stream);
+
+/* Host-buffer entry for one batch: copies inputs to the device, plans, and
+ * copies records back, all on `stream`, then synchronizes.  Tables and index
+ * are device-resident (built once).  Device scratch comes from `d_scratch`
+ * (parva_plan_host_scratch bytes). */
+size_t parva_plan_host_scratch(int32_t n_scenarios, int32_t n_services);
+int parva_plan_host(const parva_tables* tables, const parva_index* index,
+                    int32_t n_scenarios, const int32_t* h_scen_off,
+                    const int32_t* h_svc_table, const double* h_svc_rate,
+                    const double* h_svc_bound, int32_t optimize, int32_t threshold,
+                    parva_config_record* h_cfg, parva_plan_record* h_plan,
+                    void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* ------------------------------------------------------ general problems */
+/* One problem = a catalogue of segment kinds, a service list, an optional
+ * initial DeploymentMap and ledger.  Names (service ids) are indices
+ * 0..n_names-1; services are names 0..n_services-1, other names only occur
+ * in placements or the initial ledger (unknown services).  All arrays are
+ * device arrays. */
+typedef struct {
+  /* catalogue of segment kinds: instance size (1,2,3,4,7), throughput, name */
+  int32_t n_cat;
+  const uint8_t* d_cat_size;
+  const double*  d_cat_tp;
+  const int32_t* d_cat_name;
+  /* services: small-segment kinds for propose_small_segments (cat or -1),
+   * and the relocation queue input: opt kind x count, then last kind */
+  int32_t n_services;
+  int32_t n_names;
+  const int32_t* d_svc_t1;
+  const int32_t* d_svc_t2;
+  const int32_t* d_svc_opt;
+  const int64_t* d_svc_count;
+  const int32_t* d_svc_last;
+  const double*  d_svc_rate;     /* for the optimize coverage assert          */
+  /* initial map: n_gpus GPUs with ids; placements [pl_off[g], pl_off[g+1]) */
+  int32_t n_gpus;
+  const int64_t* d_gpu_id;
+  const int32_t* d_pl_off;
+  const int32_t* d_pl_cat;
+  const uint8_t* d_pl_slot;
+  /* initial ledger over names (order 0 = absent) */
+  const double*  d_ledger_val;
+  const int32_t* d_ledger_order;
+  int32_t relocate;              /* run relocate_segments into the map       */
+  int32_t optimize;              /* run optimize_allocation afterwards        */
+  int32_t threshold;
+} parva_general_problem;
+
+typedef struct {
+  int32_t gpu_cap;               /* capacity of the GPU arrays                */
+  int32_t place_cap;             /* capacity of the placement arrays          */
+  int32_t diag_cap;
+  int32_t* d_status;             /* [1] parva_status                          */
+  int32_t* d_counts;             /* [4] n_gpus, n_place, n_diag, n_gpus_unopt */
+  int64_t* d_gpu_id;             /* [gpu_cap]                                 */
+  int32_t* d_pl_off;             /* [gpu_cap + 1]                             */
+  int32_t* d_pl_cat;             /* [place_cap]                               */
+  uint8_t* d_pl_slot;            /* [place_cap]                               */
+  int64_t* d_diag;               /* [diag_cap*3]: reason, gpu id, name        */
+  double*  d_ledger_val;         /* [n_names]                                 */
+  int32_t* d_ledger_order;       /* [n_names]                                 */
+  int32_t* d_fallback;           /* [1]                                       */
+} parva_general_result;
+
+/* Device workspace for parva_plan_general (GPU state + lists + queues). */
+size_t parva_plan_general_workspace(const parva_general_problem* p, int32_t gpu_cap);
+int parva_plan_general(const parva_general_problem* p, parva_general_result* r,
+                       void* d_workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARVA_B200_H */

@@ -1,0 +1,204 @@
+"""Pin the C oracle against golden vectors rendered from the reference.
+
+CPU-only: these tests never touch CUDA.  They are what makes the oracle a
+trustworthy checker for the GPU parity tests (tests/test_gpu_parity.py).
+"""
+
+import hashlib
+import math
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import canon, golden, oracle_plan_canon, map_canon, service_canon
+from paper_2409_14447_b200 import workloads as W
+from paper_2409_14447_b200.profiles import ProfilePoint, ProfileTable, serialize_profile_table
+from paper_2409_14447_b200.tables import pack_tables, pack_dense
+
+
+@pytest.fixture(scope="module")
+def fx():
+    return W.load_fixtures()
+
+
+def _pack(fx, options):
+    mm = options.get("memory_map")
+    if mm is not None:
+        mm = {int(s): float(v) for s, v in mm}
+    return pack_tables(fx.tables, memory_map=mm, single_process=options.get("single_process", False))
+
+
+def test_fixture_tables_match_reference_csv(fx):
+    g = golden("fixture_tables.json")
+    for m in fx.models:
+        sha = hashlib.sha256(serialize_profile_table(fx.tables[m], "csv").encode()).hexdigest()[:16]
+        assert sha == g["csv_sha256"][m]
+    assert g["csv_sha256"]["inceptionv3"] == "a34f57a6f81f9392"
+    assert g["csv_sha256"]["resnet50"] == "c5082c21144f5b1b"
+
+
+def test_pysum_is_python312_sum():
+    rng = random.Random(5)
+    for _ in range(3000):
+        n = rng.randint(0, 40)
+        xs = [rng.choice([0.1, 1e16, -1e16, 3.3, rng.uniform(-1e6, 1e6), 1e-9]) for _ in range(n)]
+        assert oracle.pysum(xs) == sum(xs), xs
+    assert oracle.pysum([0.1] * 10) == 1.0
+
+
+OPTS = {"default": {}, "noopt": {"optimize": False}, "single": {"single_process": True}}
+
+
+def test_fixture_plans(fx):
+    for case in golden("fixture_plans.json"):
+        opts = OPTS[case["options"]]
+        pt = _pack(fx, opts)
+        inputs = [[m, m, r, s] for m, r, s in case["inputs"]]
+        got = oracle_plan_canon(oracle, pt, inputs, opts)
+        assert got == case["plan"], (case["scenario"], case["options"])
+
+
+def test_fixture_gpu_counts(fx):
+    counts = {(c["scenario"], c["options"]): len(c["plan"]["gpus"]) for c in golden("fixture_plans.json")}
+    assert [counts[(f"S{i}", "default")] for i in range(1, 7)] == [1, 2, 3, 4, 8, 9]
+    assert [counts[(f"S{i}", "single")] for i in range(1, 7)] == [1, 2, 3, 4, 8, 10]
+
+
+def test_fuzz_plans(fx):
+    packs = {}
+    for i, case in enumerate(golden("fuzz_plans.json")):
+        opts = case["options"]
+        key = (repr(opts.get("memory_map")), opts.get("single_process", False))
+        if key not in packs:
+            packs[key] = _pack(fx, opts)
+        got = oracle_plan_canon(oracle, packs[key], case["inputs"], opts)
+        assert got == case["result"], i
+
+
+def _single_table(points):
+    t = ProfileTable("m", tuple(ProfilePoint("m", s, b, p, tp, lat) for s, b, p, tp, lat in points))
+    return pack_tables([t], prepared=True)
+
+
+def test_unit_configure():
+    for i, case in enumerate(golden("unit_cases.json")["configure"]):
+        pt = _single_table(case["points"])
+        rec = oracle.configure_batch(pt, [0], [case["rate"]], [case["bound"]])[0]
+        res = case["result"]
+        if "error" in res:
+            assert rec["status"] == 1 and res["error"] == "InfeasibleSLOError", i
+            continue
+        got = service_canon("s", "m", case["rate"], 1.0, case["bound"], pt, 0, rec)
+        assert got == res, i
+
+
+def test_unit_select_optimal():
+    for case in golden("unit_cases.json")["select"]:
+        trips = [(t[0], t[3]) for t in case["triplets"]]
+        assert oracle.select_optimal(trips) == case["index"], case
+
+
+def test_unit_propose():
+    for case in golden("unit_cases.json")["propose"]:
+        got = oracle.propose(case["tp1"], case["tp2"], case["freed"])
+        res = case["result"]
+        if isinstance(res, dict):
+            assert got is None and res["error"] == "SmallSegmentsUnavailableError", case
+        else:
+            assert list(got) == res, case
+
+
+def _services_general(svcs):
+    out = []
+    for s in svcs:
+        out.append({"best": {t[0]: t[:4] + [0.0] for t in s["best"]}, "opt": s["opt"], "count": s["count"],
+                    "last": s["last"], "rate": s["rate"]})
+    return out
+
+
+def _general_case(svcs, dmap_in, relocate, optimize, threshold):
+    names = [s["id"] for s in svcs]
+    extra = []
+    for _, pls in (dmap_in["gpus"] if dmap_in else []):
+        for p in pls:
+            if p[0] not in names and p[0] not in extra:
+                extra.append(p[0])
+    for k, _ in (dmap_in["freed"] if dmap_in else []):
+        if k not in names and k not in extra:
+            extra.append(k)
+    allnames = names + extra
+    nid = {n: i for i, n in enumerate(allnames)}
+    gpus = [(gid, [(nid[p[0]], p[1:5], p[5]) for p in pls]) for gid, pls in (dmap_in["gpus"] if dmap_in else [])]
+    ledger = {nid[k]: (v, r + 1) for r, (k, v) in enumerate(dmap_in["freed"] if dmap_in else [])}
+    res = oracle.plan_general(len(allnames), _services_general(svcs), gpus, ledger, relocate, optimize, threshold)
+    return res, allnames
+
+
+def test_alloc_relocate():
+    for i, case in enumerate(golden("alloc_cases.json")["relocate"]):
+        res, names = _general_case(case["services"], None, 1, 0, 4)
+        assert map_canon(res, names) == case["result"], i
+
+
+def test_alloc_optimize():
+    for i, case in enumerate(golden("alloc_cases.json")["optimize"]):
+        res, names = _general_case(case["services"], case["map"], 0, 1, case["threshold"])
+        exp = case["result"]
+        if "error" in exp:
+            assert exp["error"] == "AssertionError" and res["status"] == 6, (i, case["tag"])
+            continue
+        assert res["status"] == 0, (i, case["tag"])
+        got = map_canon(res, names, prior_diags=case["map"]["diags"])
+        if res["fallback"]:
+            # fallback returns the input clone: its ledger, not the optimize pass's
+            got["freed"] = case["map"]["freed"]
+        assert got == exp, (i, case["tag"])
+
+
+def test_c2_digests(fx):
+    g = golden("c2_digests.json")
+    sb = W.scenario_batch(fx, g["n"], seed=g["seed"])
+    assert hashlib.sha256(sb.rate.tobytes() + sb.slo.tobytes()).hexdigest()[:16] == g["input_sha256"]
+    pt = pack_tables(fx.tables)
+    bad = []
+    for k in range(g["n"]):
+        inputs = [[m, m, float(sb.rate[k, j]), float(sb.slo[k, j])] for j, m in enumerate(sb.models)]
+        got = oracle_plan_canon(oracle, pt, inputs, {})
+        if k < len(g["full"]):
+            assert got == g["full"][k], k
+        if canon.digest(got) != g["digests"][k]:
+            bad.append(k)
+    assert not bad, bad[:10]
+
+
+def test_c3_sample():
+    g = golden("c3_sample.json")
+    dt = W.dense_tables(g["n"], seed=g["seed"])
+    pt = pack_dense(dt)
+    n = g["n"]
+    recs = oracle.configure_batch(pt, np.arange(n), dt.rate, dt.slo / 2.0)
+    for w in range(n):
+        row = g["rows"][w]
+        assert int(dt.seg_count[w * 5:(w + 1) * 5].sum()) == row["points"]
+        if "error" in row["result"]:
+            assert recs[w]["status"] == 1
+            continue
+        sid = f"w{w:05d}"
+        got = service_canon(sid, sid, dt.rate[w], dt.slo[w], dt.slo[w] / 2.0, pt, w, recs[w])
+        assert got == row["result"], w
+
+
+@pytest.mark.slow
+def test_c5_large_cluster(fx):
+    g = golden("c5_summary.json")
+    pt = pack_tables(fx.tables)
+    t = pt.index_of()[W.C5_MODEL]
+    rates = W.c5_rates()
+    n = rates.shape[0]
+    cfg, res = oracle.plan_scenario(pt, np.full(n, t), rates, np.full(n, W.C5_SLO / 2.0), True, 4,
+                                    gcap=200_000)
+    assert res["unopt"] == g["unopt_gpus"] and len(res["gpus"]) == g["gpus"]
+    names = [f"d121#{i}" for i in range(n)]
+    assert canon.digest(map_canon(res, names)) == g["optimized_sha256"]
