@@ -1,0 +1,367 @@
+#!/usr/bin/env python3
+"""Benchmark: scenarios scheduled/sec (configurator + allocator) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], "C2"): the 11 fixture models x 10^4
+synthetic (SLO, request-rate) scenarios per GPU (SURVEY §8d C2 generator,
+seed = rank).  One step = one pass of the hot path over that batch: the
+fused K2 launch that configures every service, relocates and optimizes
+every scenario (pipeline.py:95-103 semantics), inputs resident in HBM, L2
+flushed between steps.  N>1 (torchrun): every rank plans its own 10^4
+scenarios (weak scaling) and the step ends with one NCCL all-gather of the
+128-byte plan records.  Also reported: e2e through the host-buffer C-ABI
+entry (parva_plan_host: H2D inputs, plan, D2H records), the C3 configurator
+sweep (10^4 dense tables, the HBM-roofline kernel), and the CPU oracle
+(C restatement of the reference, all host threads) as cpu_baseline.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+PEAKS_PATH = REPO / "MEASURED_PEAKS.json"
+METRIC = "scenarios scheduled/sec (configurator+allocator)"
+UNIT = "scenarios/s"
+
+
+def peaks():
+    try:
+        p = json.loads(PEAKS_PATH.read_text())
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def c2_inputs(fx, n, seed):
+    from paper_2409_14447_b200 import workloads as W
+    sb = W.scenario_batch(fx, n, seed=seed)
+    M = len(sb.models)
+    off = (np.arange(n + 1, dtype=np.int32) * M)
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    return off, tab, np.ascontiguousarray(sb.rate.ravel()), np.ascontiguousarray(sb.bound.ravel())
+
+
+def cpu_baseline_c2(fx, n, min_seconds=3.0):
+    """The oracle (C port of the reference) on all host threads, bounded sample."""
+    import oracle
+    from paper_2409_14447_b200.tables import pack_tables
+    pt = pack_tables(fx.tables)
+    off, tab, rate, bound = c2_inputs(fx, n, 0)
+    threads = os.cpu_count() or 1
+    oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)  # warm
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
+        done += n
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"C2 batch of {n} scenarios x 11 services, repeated {done // n}x ({el:.1f} s), "
+                      f"oracle/migplan_oracle.c via OpenMP"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2409_14447_b200 import workloads as W
+    fx = W.load_fixtures()
+    import oracle
+    from paper_2409_14447_b200.tables import pack_tables
+    pt = pack_tables(fx.tables)
+    n = 10_000
+    off, tab, rate, bound = c2_inputs(fx, n, 0)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
+    el = time.perf_counter() - t0
+    v = n * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (C2 generator seed 0)",
+            "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios",
+                       "scenarios_per_step": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"full C2 batch ({n} scenarios) per step on {threads} host threads; "
+                                       "the reference itself is pure Python (see DESIGN.md)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scenarios", type=int, default=10_000, help="scenarios per GPU per step")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C3 configurator-sweep measurement")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sweep-workloads", type=int, default=10_000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2409_14447_b200 import _native as N
+    from paper_2409_14447_b200 import batch as B
+    from paper_2409_14447_b200 import workloads as W
+    from paper_2409_14447_b200.records import PLAN_DTYPE
+
+    fx = W.load_fixtures()
+    dt = N.device_tables_for(fx.tables)
+    n = args.scenarios
+    off, tab, rate, bound = c2_inputs(fx, n, rank)
+    d_off, d_tab = N.to_device(off), N.to_device(tab)
+    d_rate, d_bound = N.to_device(rate), N.to_device(bound)
+    stream = torch.cuda.current_stream()
+    res = B.plan_batch(dt, d_off, d_tab, d_rate, d_bound)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    gathered = torch.empty((world, n, PLAN_DTYPE.itemsize), dtype=torch.uint8, device="cuda") if world > 1 else None
+
+    def step():
+        B.plan_batch(dt, d_off, d_tab, d_rate, d_bound, out=res)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered.view(world, -1), res.plan[:n].reshape(-1))
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            kev[i][0].record(stream)
+            B.plan_batch(dt, d_off, d_tab, d_rate, d_bound, out=res)
+            kev[i][1].record(stream)
+            if world > 1:
+                dist.all_gather_into_tensor(gathered.view(world, -1), res.plan[:n].reshape(-1))
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        # keep the GPU busy a little longer so the sampler sees the loaded clocks
+        t_end = time.perf_counter() + 1.0
+        while time.perf_counter() < t_end:
+            for _ in range(50):
+                B.plan_batch(dt, d_off, d_tab, d_rate, d_bound, out=res)
+            torch.cuda.synchronize()
+    step_ms = sum(a.elapsed_time(b) for a, b in ev)
+    kern_ms = sum(a.elapsed_time(b) for a, b in kev)
+    t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, kern_ms = float(t[0]), float(t[1])
+
+    # parity spot check of what was timed (oracle = test infrastructure, checker only)
+    parity = None
+    if rank == 0:
+        import oracle
+        from paper_2409_14447_b200.tables import pack_tables
+        cfg, plan, _, _ = res.host()
+        k = min(n, 2000)
+        ocfg, oplan, _, _ = oracle.plan_batch_records(pack_tables(fx.tables), off[:k + 1], tab[:off[k]],
+                                                      rate[:off[k]], bound[:off[k]])
+        parity = bool(cfg[:off[k]].tobytes() == ocfg.tobytes() and plan[:k].tobytes() == oplan.tobytes())
+
+    # ---- e2e through the host-buffer C ABI (pinned host memory)
+    L = N.lib()
+    n_svc = int(off[-1])
+    h_off = torch.from_numpy(off).pin_memory(); h_tab = torch.from_numpy(tab).pin_memory()
+    h_rate = torch.from_numpy(rate).pin_memory(); h_bound = torch.from_numpy(bound).pin_memory()
+    h_cfg = torch.empty((n_svc, 32), dtype=torch.uint8).pin_memory()
+    h_plan = torch.empty((n, 128), dtype=torch.uint8).pin_memory()
+    scratch_b = int(L.parva_plan_host_scratch(C.c_int32(n), C.c_int32(n_svc)))
+    scratch = torch.empty(scratch_b, dtype=torch.uint8, device="cuda")
+    sh = N.stream_handle()
+
+    def e2e_call():
+        rc = L.parva_plan_host(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n), N.ptr(h_off), N.ptr(h_tab),
+                               N.ptr(h_rate), N.ptr(h_bound), C.c_int32(1), C.c_int32(4), N.ptr(h_cfg),
+                               N.ptr(h_plan), N.ptr(scratch), C.c_size_t(scratch_b), sh)
+        N.check(rc, "parva_plan_host")
+
+    for _ in range(args.warmup):
+        e2e_call()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_call()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te[0])
+
+    hbm, peak_src = peaks()
+    # algorithmic bytes per K2 launch: per service 20 B in
+    # (table id, rate, bound) + 32 B config record + 9 B ledger out; per scenario
+    # 4 B offset + 128 B plan record; tables+index once (18 B / point).
+    bytes_per_launch = n_svc * (20 + 32 + 9) + n * (4 + 128) + dt.packed.n_points * 18
+    kern_s = kern_ms / 1000.0 / args.steps
+    achieved = bytes_per_launch / kern_s / 1e9
+    value = n * world * args.steps / (step_ms / 1000.0)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY C2 generator, seed = rank; fixture tables rendered from the reference)",
+        "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU",
+                   "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n * world,
+                   "l2": "flushed between steps (512 MiB write, outside the events)",
+                   "parallelism": f"scenario-sharded x{world}" + (" + NCCL all-gather of plan records" if world > 1 else ""),
+                   "optimize": True, "threshold": 4},
+        "gpu_launches": args.steps,
+        "kernel_ms_per_step": kern_ms / args.steps,
+        "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
+        "e2e": {"value": n * world * args.steps / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": int((n + 1) * 4 + n_svc * 20),
+                "d2h_bytes_per_step": int(n_svc * 32 + n * 128),
+                "api": "parva_plan_host (C ABI, pinned host buffers)"},
+        "parity_vs_oracle_first_2000": parity,
+    }
+    clk_summary = clk.summary()
+    line["clocks"] = clk_summary
+
+    # ---- C3 configurator sweep (HBM-roofline kernel), rank 0
+    if not args.no_sweep and rank == 0:
+        line["configurator_sweep"] = sweep_measure(args, torch, N, B, W, hbm, peak_src, local)
+    if not args.no_cpu and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline_c2(fx, n)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sweep_measure(args, torch, N, B, W, hbm, peak_src, local):
+    from paper_2409_14447_b200.tables import pack_dense
+    nw = args.sweep_workloads
+    t0 = time.perf_counter()
+    dth = W.dense_tables(nw, seed=3)
+    gen_s = time.perf_counter() - t0
+    pt = pack_dense(dth)
+    dt = N.DeviceTables(pt, build_index=False)
+    q_table = N.to_device(np.arange(nw, dtype=np.int32))
+    q_rate = N.to_device(dth.rate)
+    q_bound = N.to_device(dth.slo / 2.0)
+    out = B.configure_sweep(dt, q_table, q_rate, q_bound)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    steps = max(10, min(args.steps, 50))
+    for _ in range(5):
+        B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            flush.zero_()
+            ev[i][0].record(s)
+            B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
+            ev[i][1].record(s)
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    points = pt.n_points
+    alg = points * 16 + nw * (4 + 8 + 8) + nw * 32
+    achieved = alg / (ms / 1000.0) / 1e9
+    import oracle
+    recs = N.records_to_numpy(out, nw, N.CONFIG_DTYPE)
+    k = min(nw, 1000)
+    orec = oracle.configure_batch(pt, np.arange(k), dth.rate[:k], dth.slo[:k] / 2.0)
+    return {"workload": "C3: 10^4 dense tables (5 sizes x batch 1-128 x procs 1-8), 1 query each",
+            "workloads": nw, "points": points, "ms_per_launch": ms, "value": nw / (ms / 1000.0),
+            "unit": "workloads/s", "points_per_s": points / (ms / 1000.0),
+            "roofline": {"bound": "hbm", "kernel": "configure_sweep_kernel", "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg},
+            "parity_vs_oracle_first_1000": bool(recs[:k].tobytes() == orec.tobytes()),
+            "generation_s": gen_s, "clocks": clk.summary()}
+
+
+if __name__ == "__main__":
+    main()

@@ -156,6 +156,14 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index,
                      parva_config_record* d_cfg, parva_plan_record* d_plan,
                      double* d_ledger_val, uint8_t* d_ledger_order, void* stream);
 
+/* parva_plan_batch for tables too large for the shared-memory index: the
+ * config records in d_cfg were produced by parva_configure_sweep. */
+int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios,
+                                   const int32_t* d_scen_off, const int32_t* d_svc_table,
+                                   int32_t optimize, int32_t threshold,
+                                   parva_config_record* d_cfg, parva_plan_record* d_plan,
+                                   double* d_ledger_val, uint8_t* d_ledger_order, void* stream);
+
 /* Host-buffer entry for one batch: copies inputs to the device, plans, and
  * copies records back, all on `stream`, then synchronizes.  Tables and index
  * are device-resident (built once).  Device scratch comes from `d_scratch`
@@ -224,6 +232,28 @@ typedef struct {
 size_t parva_plan_general_workspace(const parva_general_problem* p, int32_t gpu_cap);
 int parva_plan_general(const parva_general_problem* p, parva_general_result* r,
                        void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------ fine-grained API kernels */
+/* Lists k = [d_off[k], d_off[k+1]) of (instance size, throughput) triplets in
+ * caller order (one thread per list). */
+
+/* select_optimal_segment (configurator.py:127-139): absolute index of the
+ * chosen triplet, -1 for an empty list. */
+int parva_select_optimal_lists(int32_t n_lists, const int32_t* d_off, const int32_t* d_size,
+                               const double* d_tp, int32_t* d_out, void* stream);
+
+/* match_demand (configurator.py:142-186) on best_triplets lists: absolute
+ * indices of optimal/last triplet (-1 none), count, coverage, status. */
+int parva_match_demand_lists(int32_t n_lists, const int32_t* d_off, const int32_t* d_size,
+                             const double* d_tp, const double* d_rate, int32_t* d_opt,
+                             int32_t* d_last, int64_t* d_count, double* d_coverage,
+                             uint8_t* d_status, void* stream);
+
+/* propose_small_segments (allocator.py:319-359): tp == 0 marks an absent
+ * size-1 / size-2 triplet; ok = 0 is SmallSegmentsUnavailableError. */
+int parva_propose_small_batch(int32_t n, const double* d_tp1, const double* d_tp2,
+                              const double* d_freed, int64_t* d_k2, int64_t* d_k1,
+                              uint8_t* d_ok, void* stream);
 
 #ifdef __cplusplus
 }

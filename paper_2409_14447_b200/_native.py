@@ -1,0 +1,205 @@
+"""Loader of the sm_100a CUDA library and device-side containers.
+
+There is no CPU implementation of the planner in this package: every
+planning entry point calls into `_build/libparva_b200.so` through the C ABI
+declared in include/parva_b200.h.  If the library or a CUDA device is
+missing, `lib()` / `require_cuda()` raise NativeLibraryError.
+
+PyTorch is used only as the device-memory and stream provider: tensors hold
+the device buffers, `torch.cuda.current_stream()` orders the launches.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from collections import OrderedDict
+
+import numpy as np
+
+from .errors import NativeLibraryError
+from .records import CONFIG_DTYPE, PLAN_DTYPE
+
+_LIB = None
+_LOCK = threading.Lock()
+
+
+class ParvaTables(C.Structure):
+    _fields_ = [("d_tp", C.c_void_p), ("d_lat", C.c_void_p), ("d_seg_start", C.c_void_p),
+                ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32), ("n_points", C.c_int64)]
+
+
+class ParvaIndex(C.Structure):
+    _fields_ = [("d_lat_sorted", C.c_void_p), ("d_best", C.c_void_p)]
+
+
+class GeneralProblem(C.Structure):
+    _fields_ = [("n_cat", C.c_int32), ("d_cat_size", C.c_void_p), ("d_cat_tp", C.c_void_p),
+                ("d_cat_name", C.c_void_p), ("n_services", C.c_int32), ("n_names", C.c_int32),
+                ("d_svc_t1", C.c_void_p), ("d_svc_t2", C.c_void_p), ("d_svc_opt", C.c_void_p),
+                ("d_svc_count", C.c_void_p), ("d_svc_last", C.c_void_p), ("d_svc_rate", C.c_void_p),
+                ("n_gpus", C.c_int32), ("d_gpu_id", C.c_void_p), ("d_pl_off", C.c_void_p),
+                ("d_pl_cat", C.c_void_p), ("d_pl_slot", C.c_void_p), ("d_ledger_val", C.c_void_p),
+                ("d_ledger_order", C.c_void_p), ("relocate", C.c_int32), ("optimize", C.c_int32),
+                ("threshold", C.c_int32)]
+
+
+class GeneralResult(C.Structure):
+    _fields_ = [("gpu_cap", C.c_int32), ("place_cap", C.c_int32), ("diag_cap", C.c_int32),
+                ("d_status", C.c_void_p), ("d_counts", C.c_void_p), ("d_gpu_id", C.c_void_p),
+                ("d_pl_off", C.c_void_p), ("d_pl_cat", C.c_void_p), ("d_pl_slot", C.c_void_p),
+                ("d_diag", C.c_void_p), ("d_ledger_val", C.c_void_p), ("d_ledger_order", C.c_void_p),
+                ("d_fallback", C.c_void_p)]
+
+
+EXPORTS = (
+    "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
+    "parva_plan_batch", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
+    "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
+    "parva_match_demand_lists", "parva_propose_small_batch",
+)
+
+
+def lib_path():
+    from .build import LIB
+    return LIB
+
+
+def load_library(build_if_missing: bool = True):
+    """dlopen the library (no CUDA device needed to load it)."""
+    global _LIB
+    with _LOCK:
+        if _LIB is None:
+            from . import build as _build
+            path = _build.LIB
+            if build_if_missing and _build.stale():
+                try:
+                    _build.build()
+                except Exception as exc:  # noqa: BLE001
+                    raise NativeLibraryError(f"cannot build {path}: {exc}") from exc
+            if not path.exists():
+                raise NativeLibraryError(f"CUDA library {path} is missing; run __graft_entry__.build()")
+            try:
+                _LIB = C.CDLL(str(path))
+            except OSError as exc:
+                raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+            _LIB.parva_plan_batch_workspace.restype = C.c_size_t
+            _LIB.parva_plan_host_scratch.restype = C.c_size_t
+            _LIB.parva_plan_general_workspace.restype = C.c_size_t
+        return _LIB
+
+
+def lib():
+    return load_library()
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device: the planner runs only on the GPU (sm_100a); there is no CPU path")
+    lib()
+    return torch
+
+
+def stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        raise NativeLibraryError(f"{what} failed with parva status {rc}")
+
+
+def ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def to_device(a: np.ndarray, pad: int = 0):
+    torch = require_cuda()
+    a = np.ascontiguousarray(a)
+    if pad:
+        a = np.concatenate([a, np.zeros(pad, dtype=a.dtype)])
+    return torch.from_numpy(a).to("cuda", non_blocking=False)
+
+
+def empty_records(n: int, dtype: np.dtype):
+    torch = require_cuda()
+    return torch.empty((max(n, 1), dtype.itemsize), dtype=torch.uint8, device="cuda")
+
+
+def records_to_numpy(t, n: int, dtype: np.dtype) -> np.ndarray:
+    return t[:n].cpu().numpy().view(dtype).reshape(n)
+
+
+class DeviceTables:
+    """Prepared tables resident in HBM + their prefix-argmax index.
+
+    Layout: tp f64[P], lat f64[P] (+2 pad so 16-byte bulk copies
+    may round the last chunk up), seg_start i64[T*5], seg_count i32[T*5];
+    index: lat_sorted f64[P], best u16[P].  batch/procs stay on the host for
+    decoding winners.
+    """
+
+    def __init__(self, packed, build_index: bool = True):
+        torch = require_cuda()
+        self.packed = packed
+        self.tp = to_device(packed.tp, pad=2)
+        self.lat = to_device(packed.lat, pad=2)
+        self.seg_start = to_device(packed.seg_start.astype(np.int64))
+        self.seg_count = to_device(packed.seg_count.astype(np.int32))
+        self.struct = ParvaTables(self.tp.data_ptr(), self.lat.data_ptr(), self.seg_start.data_ptr(),
+                                  self.seg_count.data_ptr(), packed.n_tables, packed.n_points)
+        self.index = None
+        self.index_struct = None
+        if build_index and packed.n_points and int(packed.seg_count.max(initial=0)) <= 4096:
+            self.lat_sorted = torch.empty(packed.n_points + 2, dtype=torch.float64, device="cuda")
+            self.best = torch.empty(packed.n_points + 8, dtype=torch.int16, device="cuda")
+            self.index_struct = ParvaIndex(self.lat_sorted.data_ptr(), self.best.data_ptr())
+            check(lib().parva_build_index(C.byref(self.struct), C.byref(self.index_struct), stream_handle()),
+                  "parva_build_index")
+            self.index = True
+
+    @property
+    def n_tables(self) -> int:
+        return self.packed.n_tables
+
+
+class _LRU:
+    def __init__(self, n=8):
+        self.n = n
+        self.d: OrderedDict = OrderedDict()
+
+    def get(self, key, make):
+        if key in self.d:
+            self.d.move_to_end(key)
+            return self.d[key][1]
+        val = make()
+        self.d[key] = val
+        if len(self.d) > self.n:
+            self.d.popitem(last=False)
+        return val[1]
+
+
+_TABLE_CACHE = _LRU(8)
+
+
+def device_tables_for(tables, memory_map=None, single_process=False, prepared=False) -> DeviceTables:
+    """Cached DeviceTables for a {model: ProfileTable} mapping (or sequence)."""
+    from .tables import pack_tables
+    items = list(tables.items()) if hasattr(tables, "items") else [(t.model_id, t) for t in tables]
+    mm = None if memory_map is None else tuple(sorted((int(k), float(v)) for k, v in dict(memory_map).items()))
+    key = (tuple((n, id(t)) for n, t in items), mm, bool(single_process), bool(prepared))
+
+    def make():
+        pt = pack_tables(dict(items) if hasattr(tables, "items") else [t for _, t in items],
+                         memory_map=memory_map, single_process=single_process, prepared=prepared)
+        # keep the table objects alive so their ids stay unique for the key
+        return ([t for _, t in items], DeviceTables(pt))
+
+    return _TABLE_CACHE.get(key, make)
+
+
+__all__ = ["CONFIG_DTYPE", "PLAN_DTYPE", "DeviceTables", "device_tables_for", "lib", "load_library",
+           "require_cuda", "EXPORTS"]

@@ -1,0 +1,238 @@
+"""Batched device entry points (the product's hot path).
+
+    configure_sweep(dt, q_table, q_rate, q_bound)       K1, HBM-bound sweep
+    plan_batch(dt, scen_off, svc_table, rate, bound)    K2, fused planner
+    plan_general(GeneralInput)                          KG, unbounded problems
+
+All of them enqueue sm_100a kernels on the current torch CUDA stream through
+the C ABI (include/parva_b200.h); nothing here computes a plan on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .records import CAPACITY, CONFIG_DTYPE, PLAN_DTYPE
+from .tables import PackedTables
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def configure_sweep(dt: N.DeviceTables, q_table, q_rate, q_bound, out=None, stream=None):
+    """Device config records (uint8 [nq, 32]) for one query per row."""
+    torch = N.require_cuda()
+    q_table = q_table if isinstance(q_table, torch.Tensor) else N.to_device(_i32(q_table))
+    q_rate = q_rate if isinstance(q_rate, torch.Tensor) else N.to_device(_f64(q_rate))
+    q_bound = q_bound if isinstance(q_bound, torch.Tensor) else N.to_device(_f64(q_bound))
+    nq = int(q_table.shape[0])
+    if out is None:
+        out = N.empty_records(nq, CONFIG_DTYPE)
+    N.check(N.lib().parva_configure_sweep(C.byref(dt.struct), C.c_int32(nq), N.ptr(q_table), N.ptr(q_rate),
+                                          N.ptr(q_bound), N.ptr(out), N.stream_handle(stream)),
+            "parva_configure_sweep")
+    return out
+
+
+@dataclass
+class BatchResult:
+    cfg: object            # device uint8 [n_services, 32]
+    plan: object           # device uint8 [n_scenarios, 128]
+    ledger_val: object     # device f64 [n_services] or None
+    ledger_order: object   # device u8 [n_services] or None
+    n_scenarios: int
+    n_services: int
+
+    def host(self):
+        cfg = N.records_to_numpy(self.cfg, self.n_services, CONFIG_DTYPE)
+        plan = N.records_to_numpy(self.plan, self.n_scenarios, PLAN_DTYPE)
+        lv = self.ledger_val[:self.n_services].cpu().numpy() if self.ledger_val is not None else None
+        lo = self.ledger_order[:self.n_services].cpu().numpy() if self.ledger_order is not None else None
+        return cfg, plan, lv, lo
+
+
+def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, optimize: bool = True,
+               threshold: int = 4, ledger: bool = True, stream=None, out: BatchResult | None = None) -> BatchResult:
+    """Plan independent scenarios; scenario k owns services [scen_off[k], scen_off[k+1])."""
+    torch = N.require_cuda()
+    dev = lambda a, f: a if isinstance(a, torch.Tensor) else N.to_device(f(a))  # noqa: E731
+    scen_off = dev(scen_off, _i32)
+    svc_table = dev(svc_table, _i32)
+    svc_rate = dev(svc_rate, _f64)
+    svc_bound = dev(svc_bound, _f64)
+    n_scen = int(scen_off.shape[0]) - 1
+    n_svc = int(svc_table.shape[0])
+    if out is None:
+        out = BatchResult(N.empty_records(n_svc, CONFIG_DTYPE), N.empty_records(n_scen, PLAN_DTYPE),
+                          torch.empty(max(n_svc, 1), dtype=torch.float64, device="cuda") if ledger else None,
+                          torch.empty(max(n_svc, 1), dtype=torch.uint8, device="cuda") if ledger else None,
+                          n_scen, n_svc)
+    s = N.stream_handle(stream)
+    L = N.lib()
+    if dt.index_struct is not None:
+        rc = L.parva_plan_batch(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), N.ptr(scen_off),
+                                N.ptr(svc_table), N.ptr(svc_rate), N.ptr(svc_bound), C.c_int32(int(optimize)),
+                                C.c_int32(int(threshold)), N.ptr(out.cfg), N.ptr(out.plan),
+                                N.ptr(out.ledger_val), N.ptr(out.ledger_order), s)
+        N.check(rc, "parva_plan_batch")
+    else:
+        configure_sweep(dt, svc_table, svc_rate, svc_bound, out=out.cfg, stream=stream)
+        rc = L.parva_plan_batch_preconfigured(C.byref(dt.struct), C.c_int32(n_scen), N.ptr(scen_off),
+                                              N.ptr(svc_table), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
+                                              N.ptr(out.cfg), N.ptr(out.plan), N.ptr(out.ledger_val),
+                                              N.ptr(out.ledger_order), s)
+        N.check(rc, "parva_plan_batch_preconfigured")
+    return out
+
+
+# ----------------------------------------------------------------- general
+@dataclass
+class GeneralInput:
+    """One allocator problem for the general kernel (see parva_general_problem).
+
+    names: service ids first (n_services of them), then other ids that occur
+    only in placements or the initial ledger."""
+
+    names: list
+    n_services: int
+    cat_size: list = field(default_factory=list)
+    cat_tp: list = field(default_factory=list)
+    cat_name: list = field(default_factory=list)
+    svc_t1: list = field(default_factory=list)
+    svc_t2: list = field(default_factory=list)
+    svc_opt: list = field(default_factory=list)
+    svc_count: list = field(default_factory=list)
+    svc_last: list = field(default_factory=list)
+    svc_rate: list = field(default_factory=list)
+    gpu_id: list = field(default_factory=list)
+    pl_off: list = field(default_factory=lambda: [0])
+    pl_cat: list = field(default_factory=list)
+    pl_slot: list = field(default_factory=list)
+    ledger_val: list = field(default_factory=list)
+    ledger_order: list = field(default_factory=list)
+    relocate: bool = False
+    optimize: bool = False
+    threshold: int = 4
+    cat_key: list = field(default_factory=list)   # host-side decode key per catalogue entry
+
+    def add_cat(self, size: int, tp: float, name: int, memo: dict, key) -> int:
+        if key in memo:
+            return memo[key]
+        self.cat_size.append(size); self.cat_tp.append(tp); self.cat_name.append(name)
+        self.cat_key.append(key)
+        memo[key] = len(self.cat_size) - 1
+        return memo[key]
+
+
+@dataclass
+class GeneralOutput:
+    status: int
+    gpu_id: np.ndarray
+    pl_off: np.ndarray
+    pl_cat: np.ndarray
+    pl_slot: np.ndarray
+    diags: list            # (reason, gpu id, name index)
+    ledger_val: np.ndarray
+    ledger_order: np.ndarray
+    fallback: bool
+    n_gpus_unopt: int
+
+
+def plan_general(g: GeneralInput, stream=None) -> GeneralOutput:
+    torch = N.require_cuda()
+    n_names = max(len(g.names), 1)
+    total_new = sum(int(c) for c in g.svc_count) + sum(1 for x in g.svc_last if x >= 0) if g.relocate else 0
+    gpu_cap = len(g.gpu_id) + total_new + 1
+    place_cap = gpu_cap * 7
+    diag_cap = gpu_cap + 1
+
+    def d(a, dt, n=1):
+        arr = np.asarray(a if len(a) else [0] * n, dtype=dt)
+        return N.to_device(arr)
+
+    cat_size = d(g.cat_size, np.uint8); cat_tp = d(g.cat_tp, np.float64); cat_name = d(g.cat_name, np.int32)
+    svc_t1 = d(g.svc_t1, np.int32); svc_t2 = d(g.svc_t2, np.int32); svc_opt = d(g.svc_opt, np.int32)
+    svc_count = d(g.svc_count, np.int64); svc_last = d(g.svc_last, np.int32); svc_rate = d(g.svc_rate, np.float64)
+    gpu_id = d(g.gpu_id, np.int64); pl_off = d(g.pl_off, np.int32); pl_cat = d(g.pl_cat, np.int32)
+    pl_slot = d(g.pl_slot, np.uint8)
+    lv = np.zeros(n_names); lo = np.zeros(n_names, dtype=np.int32)
+    lv[:len(g.ledger_val)] = g.ledger_val
+    lo[:len(g.ledger_order)] = g.ledger_order
+    ledger_val = N.to_device(lv); ledger_order = N.to_device(lo)
+    P = N.GeneralProblem(len(g.cat_size), cat_size.data_ptr(), cat_tp.data_ptr(), cat_name.data_ptr(),
+                         g.n_services, len(g.names), svc_t1.data_ptr(), svc_t2.data_ptr(), svc_opt.data_ptr(),
+                         svc_count.data_ptr(), svc_last.data_ptr(), svc_rate.data_ptr(), len(g.gpu_id),
+                         gpu_id.data_ptr(), pl_off.data_ptr(), pl_cat.data_ptr(), pl_slot.data_ptr(),
+                         ledger_val.data_ptr(), ledger_order.data_ptr(), int(g.relocate), int(g.optimize),
+                         int(g.threshold))
+    o_status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    o_counts = torch.zeros(4, dtype=torch.int32, device="cuda")
+    o_gid = torch.zeros(gpu_cap, dtype=torch.int64, device="cuda")
+    o_off = torch.zeros(gpu_cap + 1, dtype=torch.int32, device="cuda")
+    o_cat = torch.zeros(place_cap, dtype=torch.int32, device="cuda")
+    o_slot = torch.zeros(place_cap, dtype=torch.uint8, device="cuda")
+    o_diag = torch.zeros(diag_cap * 3, dtype=torch.int64, device="cuda")
+    o_lv = torch.zeros(n_names, dtype=torch.float64, device="cuda")
+    o_lo = torch.zeros(n_names, dtype=torch.int32, device="cuda")
+    o_fb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    R = N.GeneralResult(gpu_cap, place_cap, diag_cap, o_status.data_ptr(), o_counts.data_ptr(), o_gid.data_ptr(),
+                        o_off.data_ptr(), o_cat.data_ptr(), o_slot.data_ptr(), o_diag.data_ptr(), o_lv.data_ptr(),
+                        o_lo.data_ptr(), o_fb.data_ptr())
+    L = N.lib()
+    ws_bytes = L.parva_plan_general_workspace(C.byref(P), C.c_int32(gpu_cap))
+    ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device="cuda")
+    N.check(L.parva_plan_general(C.byref(P), C.byref(R), N.ptr(ws), C.c_size_t(ws_bytes), N.stream_handle(stream)),
+            "parva_plan_general")
+    counts = o_counts.cpu().numpy()
+    ng, npl, nd, nun = (int(x) for x in counts)
+    diag = o_diag.cpu().numpy()[:3 * min(nd, diag_cap)].reshape(-1, 3)
+    return GeneralOutput(
+        status=int(o_status.item()), gpu_id=o_gid[:ng].cpu().numpy(), pl_off=o_off[:ng + 1].cpu().numpy(),
+        pl_cat=o_cat[:npl].cpu().numpy(), pl_slot=o_slot[:npl].cpu().numpy(),
+        diags=[tuple(int(v) for v in row) for row in diag], ledger_val=o_lv.cpu().numpy(),
+        ledger_order=o_lo.cpu().numpy(), fallback=bool(o_fb.item()), n_gpus_unopt=nun)
+
+
+def general_from_configs(pt: PackedTables, svc_table, cfg, optimize: bool, threshold: int) -> GeneralInput:
+    """General problem for one scenario from its config records (CAPACITY path)."""
+    n = len(svc_table)
+    g = GeneralInput(names=list(range(n)), n_services=n, relocate=True, optimize=optimize, threshold=threshold)
+    memo: dict = {}
+    for s in range(n):
+        t = int(svc_table[s]); r = cfg[s]
+        cats = [-1] * 5
+        for c in range(5):
+            if r["best"][c] >= 0:
+                cats[c] = g.add_cat((1, 2, 3, 4, 7)[c], float(pt.tp[pt.point(t, c, int(r["best"][c]))]), s, memo,
+                                    (s, c))
+        g.svc_t1.append(cats[0]); g.svc_t2.append(cats[1])
+        g.svc_opt.append(cats[int(r["opt_sc"])] if r["opt_sc"] >= 0 else -1)
+        g.svc_count.append(int(r["count"]))
+        g.svc_last.append(cats[int(r["last_sc"])] if r["last_sc"] >= 0 else -1)
+        g.svc_rate.append(0.0)
+    return g
+
+
+def resolve_capacity(pt: PackedTables, scen_off, svc_table, cfg, plan, optimize=True, threshold=4) -> dict:
+    """Re-plan every PARVA_CAPACITY scenario with the general kernel.
+
+    Returns {scenario index: (GeneralInput, GeneralOutput)}; config records
+    are valid for all scenarios."""
+    out = {}
+    for k in np.nonzero(plan["status"] == CAPACITY)[0].tolist():
+        a, b = int(scen_off[k]), int(scen_off[k + 1])
+        recs = cfg[a:b]
+        if (recs["status"] != 0).any():
+            continue  # configuration error: reported from the config records
+        g = general_from_configs(pt, svc_table[a:b], recs, optimize, threshold)
+        out[k] = (g, plan_general(g))
+    return out

@@ -1,0 +1,53 @@
+"""Build the sm_100a CUDA library (nvcc, in-tree) -> _build/libparva_b200.so.
+
+    python -m paper_2409_14447_b200.build
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT_DIR = PKG / "_build"
+LIB = OUT_DIR / "libparva_b200.so"
+SOURCES = ["configure.cu", "plan_batch.cu", "plan_general.cu", "unit_ops.cu", "capi.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "--fmad=false",                  # no FMA contraction: bit-exact with CPython
+    "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+    "-Xcompiler", "-fPIC", "-shared",
+    "-Xptxas", "-v",
+]
+
+
+def stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = list(CSRC.glob("*")) + [PKG.parent / "include" / "parva_b200.h", Path(__file__)]
+    return any(p.stat().st_mtime > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not stale():
+        return LIB
+    OUT_DIR.mkdir(exist_ok=True)
+    cmd = [NVCC, *FLAGS, "-o", str(LIB), *[str(CSRC / s) for s in SOURCES], "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    (OUT_DIR / "ptxas.log").write_text(res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libparva_b200.so")
+    if verbose:
+        print(res.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,42 @@
+// parva_kernels.cuh — launcher interfaces between the kernels and capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/parva_b200.h"
+
+namespace parva {
+
+struct PlanArgs {
+  const double* tp;              // prepared points (global)
+  const double* idx_lat;         // prefix-argmax index (global; copied to smem)
+  const uint16_t* idx_best;
+  const int64_t* seg_start;
+  const int32_t* seg_count;
+  int n_tables;
+  int64_t n_points;
+  int n_scen;
+  const int32_t* scen_off;
+  const int32_t* svc_table;
+  const double* svc_rate;
+  const double* svc_bound;
+  int optimize, threshold;
+  int cfg_given;                 // config records precomputed by K1
+  int smem_index;                // index resident in shared memory
+  parva_config_record* cfg;
+  parva_plan_record* plan;
+  double* ledger_val;
+  uint8_t* ledger_order;
+};
+
+int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
+                           const double* q_bound, parva_config_record* out, cudaStream_t stream);
+int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cudaStream_t stream);
+size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index);
+int launch_plan_batch(const PlanArgs& A, cudaStream_t stream);
+size_t general_workspace(const parva_general_problem* p, int64_t cap);
+int launch_plan_general(const parva_general_problem* p, parva_general_result* r, void* ws, size_t ws_bytes,
+                        cudaStream_t stream);
+
+}  // namespace parva

@@ -1,0 +1,407 @@
+// plan_batch.cu — K2: fused per-scenario planner (sm_100a).
+//
+// Replaces plan_services' timed region (pipeline.py:95-103) for a batch of
+// independent scenarios: configure_service x N (configurator.py:189-191),
+// relocate_segments (allocator.py:292-316), optimize_allocation
+// (allocator.py:362-443).  One warp plans one scenario:
+//   * configure: lane = service; per size class a binary search over the
+//     latency-sorted prefix-argmax index held in shared memory (exact:
+//     the points with lat < bound are a prefix of the sorted order and the
+//     argmax under a total order is prefix-decomposable);
+//   * relocate / optimize: lane = GPU; a GPU is a 7-bit slot mask; first-fit
+//     is one ballot over find_start(mask) (cursorless first-fit is
+//     equivalent to the reference's cursors); the
+//     freed_rate ledger lives in lane = service registers, snapshot/restore
+//     is a register copy.
+// Scenarios beyond the 128-byte record's limits report PARVA_CAPACITY and
+// are re-planned by the general kernel (plan_general.cu).
+#include <cuda_runtime.h>
+
+#include "parva_common.cuh"
+#include "parva_kernels.cuh"
+
+namespace parva {
+
+constexpr int PB_WARPS = 8;
+constexpr int PB_THREADS = PB_WARPS * 32;
+constexpr int QCAP = 224;                 // > 31 GPUs x 7 slots: longer queues cannot fit
+
+struct WarpScratch {
+  double cat_tp[32 * 5];                  // best tp per (service, size class); 0 = absent
+  long long count[32];
+  int8_t opt_sc[32];
+  int8_t last_sc[32];
+  uint16_t lst[32][8];                    // per GPU placement list: cat << 3 | slot
+  uint16_t bak[32][8];                    // relocation result (regression fallback)
+  uint8_t q2[QCAP];
+  uint8_t q1[QCAP];
+  uint8_t undo[2 * QCAP];
+  parva_plan_record rec;
+};
+
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double unallocated(int total, int n) {
+  if (n == 0) return 0.0;
+  return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
+}
+
+// configure one service from the index (binary search per size class)
+__device__ __forceinline__ void configure_indexed(const double* lat_s, const uint16_t* best_s,
+                                                  const double* tp, const int* seg_s,
+                                                  const int* seg_n, int t, double bound,
+                                                  double rate, parva_config_record& r,
+                                                  double tpc[5]) {
+#pragma unroll
+  for (int c = 0; c < 5; c++) {
+    const int s0 = seg_s[t * 5 + c], n = seg_n[t * 5 + c];
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (lat_s[s0 + mid] < bound) lo = mid + 1;
+      else hi = mid;
+    }
+    const int b = lo ? (int)best_s[s0 + lo - 1] : -1;
+    r.best[c] = (int16_t)b;
+    tpc[c] = b >= 0 ? tp[s0 + b] : 0.0;
+  }
+  match_demand(tpc, rate, r);
+  if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
+}
+
+__global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  uint8_t* idx_base = smem_raw + sizeof(WarpScratch) * PB_WARPS;
+  const int T5 = A.n_tables * 5;
+  int* seg_s = reinterpret_cast<int*>(idx_base);
+  int* seg_n = seg_s + T5;
+  const double* lat_s = A.idx_lat;
+  const uint16_t* best_s = A.idx_best;
+  const double* tp_s = A.tp;
+  if (A.smem_index) {
+    double* lat_w = reinterpret_cast<double*>(idx_base + ((size_t(T5) * 8 + 15) & ~size_t(15)));
+    double* tp_w = lat_w + A.n_points;
+    uint16_t* best_w = reinterpret_cast<uint16_t*>(tp_w + A.n_points);
+    for (int i = threadIdx.x; i < T5; i += blockDim.x) {
+      seg_s[i] = (int)A.seg_start[i];
+      seg_n[i] = A.seg_count[i];
+    }
+    for (int64_t i = threadIdx.x; i < A.n_points; i += blockDim.x) {
+      lat_w[i] = A.idx_lat[i];
+      tp_w[i] = A.tp[i];
+      best_w[i] = A.idx_best[i];
+    }
+    lat_s = lat_w; tp_s = tp_w; best_s = best_w;
+  } else {
+    for (int i = threadIdx.x; i < T5; i += blockDim.x) {
+      seg_s[i] = (int)A.seg_start[i];
+      seg_n[i] = A.seg_count[i];
+    }
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpScratch& W = scratch[warp];
+  const int gwarps = gridDim.x * PB_WARPS;
+
+  for (int k = blockIdx.x * PB_WARPS + warp; k < A.n_scen; k += gwarps) {
+    const int a0 = A.scen_off[k];
+    const int n = A.scen_off[k + 1] - a0;
+    reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
+
+    // ------------------------------------------------------------ configure
+    int err_status = 0, err_svc = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      parva_config_record r;
+      double tpc[5] = {0, 0, 0, 0, 0};
+      if (i < n) {
+        if (A.cfg_given) {
+          r = A.cfg[a0 + i];
+          const int t = A.svc_table[a0 + i];
+          for (int c = 0; c < 5; c++)
+            tpc[c] = r.best[c] >= 0 ? A.tp[A.seg_start[t * 5 + c] + r.best[c]] : 0.0;
+        } else {
+          r = {};
+          const int t = A.svc_table[a0 + i];
+          if (t < 0 || t >= A.n_tables) {
+            for (int c = 0; c < 5; c++) r.best[c] = -1;
+            r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
+          } else {
+            configure_indexed(lat_s, best_s, tp_s, seg_s, seg_n, t, A.svc_bound[a0 + i],
+                              A.svc_rate[a0 + i], r, tpc);
+          }
+          A.cfg[a0 + i] = r;
+        }
+        if (base == 0) {
+          W.opt_sc[lane] = r.opt_sc;
+          W.last_sc[lane] = r.last_sc;
+          W.count[lane] = r.count;
+#pragma unroll
+          for (int c = 0; c < 5; c++) W.cat_tp[lane * 5 + c] = tpc[c];
+        }
+      }
+      const unsigned bad = __ballot_sync(0xffffffffu, i < n && r.status != PARVA_OK);
+      const int st = __shfl_sync(0xffffffffu, (int)r.status, bad ? __ffs(bad) - 1 : 0);
+      if (err_status == 0 && bad) { err_status = st; err_svc = base + __ffs(bad) - 1; }
+    }
+    __syncwarp();
+
+    int status = PARVA_OK;
+    if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
+    else if (err_status) status = err_status;
+    else {
+      const long long segs = warp_sum_ll(lane < n ? W.count[lane] + (W.last_sc[lane] >= 0) : 0);
+      if (segs > 32 * 7) status = PARVA_CAPACITY;
+    }
+
+    // per-lane GPU state (lane = GPU index) and ledger state (lane = service)
+    uint32_t mask = 0;
+    int ngpc = 0, len = 0, ngpus = 0;
+    double freed = 0.0;
+    int order = 0;
+    bool fallback = false;
+    int nd = 0, n_before = 0;
+
+    if (status == PARVA_OK) {
+      // --------------------------------------------- relocate_segments
+      for (int c = 4; c >= 0 && status == PARVA_OK; c--) {
+        const int size = size_of_class(c);
+        for (int s = 0; s < n && status == PARVA_OK; s++) {
+          const long long reps = (W.opt_sc[s] == c ? W.count[s] : 0) + (W.last_sc[s] == c ? 1 : 0);
+          const uint16_t cat = (uint16_t)(s * 5 + c);
+          for (long long r = 0; r < reps; r++) {
+            int st = lane < ngpus ? find_start(mask, c) : -1;
+            const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
+            int g;
+            if (b) g = __ffs(b) - 1;
+            else {
+              if (ngpus >= PARVA_PLAN_MAX_GPUS) { status = PARVA_CAPACITY; break; }
+              g = ngpus++;
+              st = find_start(0u, c);
+            }
+            if (lane == g) {
+              mask |= footprint(c, st);
+              ngpc += size;
+              W.lst[g][len++] = (uint16_t)(cat << 3 | st);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+
+    if (status == PARVA_OK) {
+      n_before = ngpus;
+      const int total_before = warp_sum_i(lane < ngpus ? ngpc : 0);
+      *reinterpret_cast<uint4*>(W.bak[lane]) = *reinterpret_cast<const uint4*>(W.lst[lane]);
+      const int bak_len = len, bak_ngpc = ngpc;
+      const uint32_t bak_mask = mask;
+
+      if (A.optimize) {
+        // ----------------------------------------- optimize_allocation
+        int next = 0;
+        for (int index = ngpus - 1; index >= 0; index--) {
+          const int nl = __shfl_sync(0xffffffffu, len, index);
+          const int ng = __shfl_sync(0xffffffffu, ngpc, index);
+          if (nl == 0 || ng > A.threshold) continue;
+          const double sv_freed = freed;
+          const int sv_order = order, sv_next = next;
+          int q2n = 0, q1n = 0, fail = -1, fsvc = 0, rot = nl;
+          bool qover = false;
+          for (int kk = 0; kk < nl; kk++) {
+            const int cat = W.lst[index][kk] >> 3;
+            const int s = cat / 5;
+            const double tpp = W.cat_tp[cat];
+            const bool newkey = __shfl_sync(0xffffffffu, order, s) == 0;
+            if (newkey) next++;
+            if (lane == s) {
+              if (newkey) { order = next; freed = __dadd_rn(0.0, tpp); }
+              else freed = __dadd_rn(freed, tpp);
+            }
+            const double f = __shfl_sync(0xffffffffu, freed, s);
+            const double t1 = W.cat_tp[s * 5 + 0], t2 = W.cat_tp[s * 5 + 1];
+            long long k2, k1;
+            if (!propose_small(t1, t2, f, k2, k1)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fsvc = s; rot = kk + 1; break; }
+            if (lane == s) {
+              for (long long j = 0; j < k2; j++) freed = __dsub_rn(freed, t2);
+              for (long long j = 0; j < k1; j++) freed = __dsub_rn(freed, t1);
+            }
+            if (qover || q2n + k2 > QCAP || q1n + k1 > QCAP) qover = true;
+            else {
+              for (int j = lane; j < k2; j += 32) W.q2[q2n + j] = (uint8_t)(s * 5 + 1);
+              for (int j = lane; j < k1; j += 32) W.q1[q1n + j] = (uint8_t)(s * 5 + 0);
+              q2n += (int)k2; q1n += (int)k1;
+            }
+          }
+          __syncwarp();
+          if (fail < 0) {
+            if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
+            else {
+              int nu = 0;
+              for (int j = 0; j < q2n + q1n; j++) {
+                const int cat = j < q2n ? W.q2[j] : W.q1[j - q2n];
+                const int c = cat % 5;
+                const int st = (lane < ngpus && lane != index) ? find_start(mask, c) : -1;
+                const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
+                if (!b) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
+                const int g = __ffs(b) - 1;
+                if (lane == g) {
+                  mask |= footprint(c, st);
+                  ngpc += size_of_class(c);
+                  W.lst[g][len++] = (uint16_t)(cat << 3 | st);
+                }
+                if (lane == 0) W.undo[nu] = (uint8_t)g;
+                nu++;
+              }
+              __syncwarp();
+              if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
+                for (int j = nu - 1; j >= 0; j--) {
+                  const int g = W.undo[j];
+                  if (lane == g) {
+                    const int e = W.lst[g][--len];
+                    mask &= ~footprint((e >> 3) % 5, e & 7);
+                    ngpc -= size_of_class((e >> 3) % 5);
+                  }
+                }
+              }
+            }
+          }
+          if (fail >= 0) {
+            // restore drained placements (allocator.py:415-417): the ones not yet
+            // removed keep their order, the removed ones are re-appended
+            if (lane == index && rot != nl) {
+              uint16_t e[8];
+#pragma unroll
+              for (int j = 0; j < 8; j++) e[j] = W.lst[index][j];
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                if (j < nl) {
+                  int src = j + rot;
+                  if (src >= nl) src -= nl;
+                  uint16_t v = e[0];
+#pragma unroll
+                  for (int u = 1; u < 8; u++) if (u == src) v = e[u];
+                  W.lst[index][j] = v;
+                }
+              }
+            }
+            freed = sv_freed; order = sv_order; next = sv_next;
+            if (nd < PARVA_PLAN_MAX_DIAG && lane == 0)
+              W.rec.diag[nd] = (uint16_t)(index << 7 | fail << 5 | (fail == PARVA_DIAG_SMALL_UNAVAILABLE ? fsvc : 0));
+            nd++;
+          } else if (lane == index) {
+            len = 0; mask = 0; ngpc = 0;
+          }
+          __syncwarp();
+        }
+        // compaction + regression check (allocator.py:423-435)
+        const int n_after = __popc(__ballot_sync(0xffffffffu, lane < ngpus && len > 0));
+        const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0);
+        const double ua_before = unallocated(total_before, n_before);
+        const double ua_after = unallocated(total_after, n_after);
+        if (n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12)) {
+          fallback = true;
+          *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
+          len = bak_len; ngpc = bak_ngpc; mask = bak_mask;
+          freed = 0.0; order = 0; nd = 0;
+        }
+      }
+      __syncwarp();
+
+      // ------------------------------------------------------- emit record
+      const bool good = lane < ngpus && len > 0;
+      const int mine = good ? len : 0;
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int n_place = __shfl_sync(0xffffffffu, incl, 31);
+      const int n_final = __popc(__ballot_sync(0xffffffffu, good));
+      const int tot = warp_sum_i(good ? ngpc : 0);
+      if (n_place > PARVA_PLAN_MAX_PLACE || nd > PARVA_PLAN_MAX_DIAG) {
+        status = PARVA_CAPACITY;
+      } else {
+        for (int j = 0; j < mine; j++) W.rec.place[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+        if (lane == 0) {
+          W.rec.n_gpus = (uint8_t)n_final;
+          W.rec.n_gpus_unopt = (uint8_t)n_before;
+          W.rec.n_place = (uint8_t)n_place;
+          W.rec.n_diag = (uint8_t)nd;
+          W.rec.flags = fallback ? PARVA_FLAG_FALLBACK : 0;
+          W.rec.total_gpcs = (uint8_t)tot;
+        }
+      }
+      // reset this lane's GPU list slots for the next scenario
+      *reinterpret_cast<uint4*>(W.lst[lane]) = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    if (status != PARVA_OK) {
+      reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
+      __syncwarp();
+      if (lane == 0) {
+        W.rec.status = (uint8_t)status;
+        W.rec.err_service = (uint8_t)(status == PARVA_CAPACITY ? 0 : err_svc);
+      }
+    }
+    __syncwarp();
+    if (lane < 8)
+      reinterpret_cast<uint4*>(A.plan + k)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    if (A.ledger_val) {
+      const bool keep = status == PARVA_OK && !fallback;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        if (i < n) {
+          const bool on = keep && base == 0 && order != 0;
+          A.ledger_val[a0 + i] = on ? freed : 0.0;
+          A.ledger_order[a0 + i] = (uint8_t)(on ? order : 0);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index) {
+  size_t b = sizeof(WarpScratch) * PB_WARPS + ((size_t(n_tables) * 5 * 8 + 15) & ~size_t(15));
+  if (smem_index) b += size_t(n_points) * (8 + 8 + 2);
+  return (b + 15) & ~size_t(15);
+}
+
+int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
+  if (A.n_scen <= 0) return PARVA_OK;
+  const size_t smem = plan_smem_bytes(A.n_tables, A.n_points, A.smem_index);
+  static size_t configured = 0;
+  static int n_sm = 0;
+  if (smem > configured) {
+    cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  if (!n_sm) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_batch_kernel, PB_THREADS, smem);
+  if (per_sm < 1) return PARVA_LAUNCH_ERROR;
+  int grid = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  if (grid > n_sm * per_sm) grid = n_sm * per_sm;
+  plan_batch_kernel<<<grid, PB_THREADS, smem, stream>>>(A);
+  return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+}  // namespace parva

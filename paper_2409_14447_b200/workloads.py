@@ -142,8 +142,8 @@ def dense_params(n_workloads: int, seed: int = 3, first: int = 0) -> dict[str, n
     """Per-workload SyntheticModelParams fields and the query, C3 stream."""
     W_all = first + n_workloads
     rng = np.random.default_rng(seed)
-    u = rng.random((W_all, 6))[first:]
-    q = rng.random((W_all, 2))[first:]
+    u = rng.random((W_all, 8))[first:]     # one row per workload: 6 params + query
+    q = u[:, 6:8]
     ln = math.log
     gexp = 0.95 + (1.4 - 0.95) * u[:, 1]
     return {

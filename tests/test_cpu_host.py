@@ -1,0 +1,130 @@
+"""CPU-only checks: the C ABI library loads and exports every declared
+symbol; host-side data model mirrors the reference; no silent CPU path."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2409_14447_b200 as P
+from paper_2409_14447_b200 import _native as N
+from paper_2409_14447_b200 import workloads as W
+from paper_2409_14447_b200.records import CONFIG_DTYPE, PLAN_DTYPE
+from paper_2409_14447_b200.tables import pack_tables
+
+REPO = Path(__file__).resolve().parent.parent
+
+
+def _declared():
+    text = (REPO / "include" / "parva_b200.h").read_text()
+    return sorted(set(re.findall(r"^(?:int|size_t)\s+(parva_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load_library()
+    declared = _declared()
+    assert len(declared) >= 13
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(N.EXPORTS)
+    assert lib.parva_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(N.lib_path())],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_record_layouts():
+    assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128
+
+
+def test_no_cpu_fallback_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    fx = W.load_fixtures()
+    with pytest.raises(P.NativeLibraryError):
+        P.plan_services([P.make_service("resnet50", "resnet50", 100.0, 200.0)], fx.tables)
+    with pytest.raises(P.NativeLibraryError):
+        P.configure_service(P.make_service("resnet50", "resnet50", 100.0, 200.0), fx.tables["resnet50"])
+
+
+def test_enumerate_full_configs_is_19():
+    cfgs = P.enumerate_full_configs()
+    assert len(cfgs) == 19
+    assert ((0, 1), (1, 1), (2, 1), (3, 1), (4, 1), (5, 1), (6, 1)) in cfgs
+
+
+def test_greedy_copies_on_empty_gpu():
+    for size, n in ((1, 7), (2, 3), (3, 2), (4, 1), (7, 1)):
+        g = P.GpuState(0)
+        k = 0
+        while g.place("s", size, 1, 1, 1.0) is not None:
+            k += 1
+        assert k == n
+    g = P.GpuState(0)
+    assert g.place("s", 3, 1, 1, 1.0).start_slot == 4
+    assert g.place("s", 3, 1, 1, 1.0).start_slot == 0
+    assert g.find_start(1) is None            # slot 3 blocked
+
+
+def test_make_service_and_errors():
+    s = P.make_service("a", "m", 10, 200)
+    assert s.internal_latency == 100.0 and isinstance(s.request_rate, float)
+    with pytest.raises(P.MigplanError):
+        P.make_service("a", "m", -1, 200)
+    with pytest.raises(P.MigplanError):
+        P.make_service("a", "m", 1, 0)
+    e = P.InfeasibleSLOError("x", 12.5)
+    assert str(e) == "service 'x': no profile point has latency below 12.5 ms"
+    assert str(P.SmallSegmentsUnavailableError("y")) == "service 'y' has no size-1 or size-2 triplet"
+
+
+def test_profile_csv_round_trip():
+    fx = W.load_fixtures()
+    for m in fx.models:
+        t = fx.tables[m]
+        assert P.load_profile_table(P.serialize_profile_table(t, "csv")) == t
+        assert P.load_profile_table(P.serialize_profile_table(t, "json"), format="json") == t
+    with pytest.raises(P.ValidationError):
+        P.ProfileTable("m", (P.ProfilePoint("m", 1, 1, 1, 1.0, 1.0), P.ProfilePoint("m", 1, 1, 1, 2.0, 1.0)))
+
+
+def test_pack_tables_layout():
+    fx = W.load_fixtures()
+    pt = pack_tables(fx.tables)
+    assert pt.n_tables == 11 and pt.n_points == 1311
+    single = pack_tables(fx.tables, single_process=True)
+    assert (single.procs == 1).all()
+    # segments in key order: batch asc then procs asc within each size class
+    for t in range(pt.n_tables):
+        for c in range(5):
+            a, n = int(pt.seg_start[t * 5 + c]), int(pt.seg_count[t * 5 + c])
+            keys = list(zip(pt.batch[a:a + n], pt.procs[a:a + n]))
+            assert keys == sorted(keys)
+
+
+def test_workload_generators_deterministic():
+    fx = W.load_fixtures()
+    a = W.scenario_batch(fx, 300, seed=0)
+    b = W.scenario_batch(fx, 300, seed=0)
+    assert a.rate.tobytes() == b.rate.tobytes() and a.slo.tobytes() == b.slo.tobytes()
+    d1 = W.dense_tables(5, seed=3)
+    d2 = W.dense_tables(3, seed=3, first=2)
+    s1 = int(d1.seg_start[10])
+    assert d1.tp[s1:].tobytes() == d2.tp.tobytes()
+    assert d1.rate[2:].tobytes() == d2.rate.tobytes() and d1.slo[2:].tobytes() == d2.slo.tobytes()
+    assert W.c5_rates(3).tolist() == W.c5_rates(5)[:3].tolist()
+
+
+def test_deployment_map_json_round_trip():
+    d = P.DeploymentMap(gpus=[P.GpuState(3, [P.Placement("a", 4, 8, 2, 1695.0, 0), P.Placement("b", 3, 1, 1, 9.5, 4)])])
+    e = P.DeploymentMap.from_json(d.to_json())
+    assert e.to_json() == d.to_json()
+    with pytest.raises(P.ValidationError):
+        P.DeploymentMap.from_json('{"gpus":[{"id":0,"segments":[{"service":"a","instance_size":2,'
+                                  '"batch_size":1,"process_count":1,"start_slot":5,"throughput_rps":1.0}]}]}')
