@@ -17,22 +17,57 @@
 
 namespace parva {
 
-constexpr int SW_WARPS = 8;                    // consumer warps
-constexpr int SW_THREADS = (SW_WARPS + 1) * 32;
-constexpr int SW_CH = 2048;                    // points per chunk
-constexpr int SW_STAGES = 3;
+constexpr int SW_WARPS = 12;                   // warps per CTA, one table each at a time
+constexpr int SW_THREADS = SW_WARPS * 32;
+constexpr int SW_CH = 384;                     // points per chunk (2 x 3 KB)
+constexpr int SW_STAGES = 3;                   // chunks in flight per warp
 
-struct SweepSmem {
+struct alignas(128) SweepWarpSmem {
   double tp[SW_STAGES][SW_CH + 2];
   double lat[SW_STAGES][SW_CH + 2];
   uint64_t full[SW_STAGES];
-  uint64_t empty[SW_STAGES];
-  Cand wbest[SW_WARPS][5];
-  Cand fin[5];
 };
 
-struct ChunkIter {
-  int64_t a, b, s0;  // chunk [a, b) of segment starting at s0
+// Walks (query, size class, chunk) for one warp: queries q0, q0+stride, ...
+// The current table's 5 segment offsets/counts live in lanes 0..4.
+struct ChunkCursor {
+  int q, c, off, n;
+  int64_t s0;
+  int64_t lane_start;   // lane c: seg_start of the current table, class c
+  int lane_count;       // lane c: seg_count
+  bool valid;           // current q has a valid table
+
+  __device__ void load_table(const int32_t* q_table, const int64_t* seg_start, const int32_t* seg_count,
+                             int n_tables, int lane) {
+    const int t = q_table[q];
+    valid = t >= 0 && t < n_tables;
+    lane_start = 0; lane_count = 0;
+    if (valid && lane < 5) { lane_start = seg_start[t * 5 + lane]; lane_count = seg_count[t * 5 + lane]; }
+  }
+  __device__ void select(int cc) {
+    c = cc;
+    s0 = __shfl_sync(0xffffffffu, lane_start, cc);
+    n = __shfl_sync(0xffffffffu, lane_count, cc);
+  }
+  // move to the next non-empty chunk at or after (q, c, off); false when done
+  __device__ bool settle(const int32_t* q_table, const int64_t* seg_start, const int32_t* seg_count,
+                         int n_tables, int nq, int stride, int lane) {
+    while (q < nq) {
+      if (valid) {
+        while (c < 5) {
+          if (off < n) return true;
+          off = 0;
+          if (c + 1 < 5) select(c + 1); else c = 5;
+        }
+      }
+      q += stride;
+      if (q >= nq) break;
+      load_table(q_table, seg_start, seg_count, n_tables, lane);
+      off = 0;
+      select(0);
+    }
+    return false;
+  }
 };
 
 __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
@@ -41,105 +76,124 @@ __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
     int nq, const int32_t* __restrict__ q_table, const double* __restrict__ q_rate,
     const double* __restrict__ q_bound, parva_config_record* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  SweepSmem& S = *reinterpret_cast<SweepSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SweepWarpSmem& S = reinterpret_cast<SweepWarpSmem*>(smem_raw)[warp];
+  const int gw = blockIdx.x * SW_WARPS + warp;
+  const int stride = gridDim.x * SW_WARPS;
+  if (gw >= nq) return;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < SW_STAGES; s++) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], SW_WARPS);
-    }
+  if (lane == 0) {
+    for (int s = 0; s < SW_STAGES; s++) mbar_init(&S.full[s], 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  __syncwarp();
+  const uint64_t pol = policy_evict_first();
 
-  if (warp == SW_WARPS) {
-    // ---------------------------------------------------------- producer
+  // producer cursor: up to SW_STAGES chunks ahead of the consumer
+  ChunkCursor P;
+  P.q = gw; P.off = 0;
+  P.load_table(q_table, seg_start, seg_count, n_tables, lane);
+  P.select(0);
+  bool p_ok = P.settle(q_table, seg_start, seg_count, n_tables, nq, stride, lane);
+  uint32_t issued = 0;
+  auto issue = [&]() {
+    const int64_t a = P.s0 + P.off;
+    const int64_t b = P.s0 + min(P.n, P.off + SW_CH);
+    const int64_t a2 = a & ~int64_t(1), b2 = (b + 1) & ~int64_t(1);
+    const uint32_t bytes = uint32_t(b2 - a2) * 8u;
+    const int st = issued % SW_STAGES;
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
-      for (int q = blockIdx.x; q < nq; q += gridDim.x) {
-        const int t = q_table[q];
-        if (t < 0 || t >= n_tables) continue;
-        for (int c = 0; c < 5; c++) {
-          const int64_t s0 = seg_start[t * 5 + c];
-          const int n = seg_count[t * 5 + c];
-          for (int off = 0; off < n; off += SW_CH, it++) {
-            const int64_t a = s0 + off, b = s0 + min(n, off + SW_CH);
-            const int64_t a2 = a & ~int64_t(1), b2 = (b + 1) & ~int64_t(1);
-            const uint32_t bytes = uint32_t(b2 - a2) * 8u;
-            const int st = it % SW_STAGES;
-            mbar_wait(&S.empty[st], ((it / SW_STAGES) & 1) ^ 1);
-            mbar_arrive_expect_tx(&S.full[st], 2 * bytes);
-            bulk_g2s(S.tp[st], tp + a2, bytes, &S.full[st], pol);
-            bulk_g2s(S.lat[st], lat + a2, bytes, &S.full[st], pol);
-          }
-        }
-      }
+      mbar_arrive_expect_tx(&S.full[st], 2 * bytes);
+      bulk_g2s(S.tp[st], tp + a2, bytes, &S.full[st], pol);
+      bulk_g2s(S.lat[st], lat + a2, bytes, &S.full[st], pol);
     }
-    return;
-  }
+    issued++;
+    P.off += SW_CH;
+    p_ok = P.settle(q_table, seg_start, seg_count, n_tables, nq, stride, lane);
+  };
+  for (int k = 0; k < SW_STAGES && p_ok; k++) issue();
 
-  // ------------------------------------------------------------ consumers
-  const int tid = threadIdx.x;  // 0 .. 255
-  uint32_t it = 0;
-  for (int q = blockIdx.x; q < nq; q += gridDim.x) {
-    const int t = q_table[q];
-    if (t < 0 || t >= n_tables) {
-      if (tid == 0) {
+  // deferred epilogue: lane L holds the per-size winners of the L-th pending query
+  int pend_q = -1;
+  int p_idx0 = -1, p_idx1 = -1, p_idx2 = -1, p_idx3 = -1, p_idx4 = -1;
+  double p_tp0 = 0, p_tp1 = 0, p_tp2 = 0, p_tp3 = 0, p_tp4 = 0;
+  int npend = 0;
+  auto flush = [&]() {
+    if (pend_q >= 0) {
+      parva_config_record r = {};
+      r.best[0] = (int16_t)p_idx0; r.best[1] = (int16_t)p_idx1; r.best[2] = (int16_t)p_idx2;
+      r.best[3] = (int16_t)p_idx3; r.best[4] = (int16_t)p_idx4;
+      double tpc[5] = {p_idx0 >= 0 ? p_tp0 : 0.0, p_idx1 >= 0 ? p_tp1 : 0.0, p_idx2 >= 0 ? p_tp2 : 0.0,
+                       p_idx3 >= 0 ? p_tp3 : 0.0, p_idx4 >= 0 ? p_tp4 : 0.0};
+      match_demand(tpc, q_rate[pend_q], r);
+      const uint4* src = reinterpret_cast<const uint4*>(&r);
+      uint4* dst = reinterpret_cast<uint4*>(out + pend_q);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    }
+    pend_q = -1; p_idx0 = p_idx1 = p_idx2 = p_idx3 = p_idx4 = -1;
+    npend = 0;
+  };
+
+  // consumer cursor over the same sequence
+  ChunkCursor Q;
+  uint32_t consumed = 0;
+  for (Q.q = gw; Q.q < nq; Q.q += stride) {
+    Q.load_table(q_table, seg_start, seg_count, n_tables, lane);
+    if (!Q.valid) {
+      if (lane == 0) {
         parva_config_record r = {};
         for (int c = 0; c < 5; c++) r.best[c] = -1;
         r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
-        out[q] = r;
+        out[Q.q] = r;
       }
       continue;
     }
-    const double bound = q_bound[q];
+    const double bound = q_bound[Q.q];
+    const int slot = npend++;
+#pragma unroll 1
     for (int c = 0; c < 5; c++) {
-      const int64_t s0 = seg_start[t * 5 + c];
-      const int n = seg_count[t * 5 + c];
+      Q.select(c);
       Cand best{0.0, 0.0, -1};
-      for (int off = 0; off < n; off += SW_CH, it++) {
-        const int64_t a = s0 + off, b = s0 + min(n, off + SW_CH);
+      for (int off = 0; off < Q.n; off += SW_CH) {
+        const int64_t a = Q.s0 + off, b = Q.s0 + min(Q.n, off + SW_CH);
         const int64_t a2 = a & ~int64_t(1);
-        const int st = it % SW_STAGES;
-        mbar_wait(&S.full[st], (it / SW_STAGES) & 1);
+        const int st = consumed % SW_STAGES;
+        mbar_wait(&S.full[st], (consumed / SW_STAGES) & 1);
         const double* stp = S.tp[st];
         const double* slat = S.lat[st];
         const int lo = int(a - a2), hi = int(b - a2);
-#pragma unroll 4
-        for (int j = lo + tid; j < hi; j += SW_WARPS * 32) {
-          const double l = slat[j];
-          if (l < bound) {
-            Cand cnd{stp[j], l, int(a2 - s0) + j};
-            if (better(cnd, best)) best = cnd;
+        const int base = int(a2 - Q.s0);
+#pragma unroll
+        for (int j0 = 0; j0 < SW_CH + 2; j0 += 32) {
+          const int j = j0 + lane;
+          if (j >= lo && j < hi) {
+            const double l = slat[j];
+            if (l < bound) {
+              Cand cnd{stp[j], l, base + j};
+              if (better(cnd, best)) best = cnd;
+            }
           }
         }
+        consumed++;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[st]);
+        if (p_ok) issue();
       }
       best = warp_argmax(best);
-      if (lane == 0) S.wbest[warp][c] = best;
-    }
-    named_bar_sync(1, SW_WARPS * 32);
-    if (tid < 5) {
-      Cand b = S.wbest[0][tid];
-      for (int w = 1; w < SW_WARPS; w++)
-        if (better(S.wbest[w][tid], b)) b = S.wbest[w][tid];
-      S.fin[tid] = b;
-    }
-    named_bar_sync(1, SW_WARPS * 32);
-    if (tid == 0) {
-      parva_config_record r = {};
-      double tpc[5];
-      for (int c = 0; c < 5; c++) {
-        r.best[c] = (int16_t)S.fin[c].idx;
-        tpc[c] = S.fin[c].idx >= 0 ? S.fin[c].tp : 0.0;
+      if (lane == slot) {
+        switch (c) {
+          case 0: p_idx0 = best.idx; p_tp0 = best.tp; break;
+          case 1: p_idx1 = best.idx; p_tp1 = best.tp; break;
+          case 2: p_idx2 = best.idx; p_tp2 = best.tp; break;
+          case 3: p_idx3 = best.idx; p_tp3 = best.tp; break;
+          default: p_idx4 = best.idx; p_tp4 = best.tp; break;
+        }
+        pend_q = Q.q;
       }
-      match_demand(tpc, q_rate[q], r);
-      out[q] = r;
     }
+    if (npend == 32) flush();
   }
+  flush();
 }
 
 // ------------------------------------------------------------------- K0
@@ -193,7 +247,7 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
                            parva_config_record* out, cudaStream_t stream) {
   if (nq <= 0) return PARVA_OK;
   static int blocks_per_sm = -1, n_sm = 0;
-  const size_t smem = sizeof(SweepSmem);
+  const size_t smem = sizeof(SweepWarpSmem) * SW_WARPS;
   if (blocks_per_sm < 0) {
     cudaFuncSetAttribute(configure_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev;
@@ -203,7 +257,8 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   int grid = n_sm * blocks_per_sm;
-  if (grid > nq) grid = nq;
+  const int need = (nq + SW_WARPS - 1) / SW_WARPS;
+  if (grid > need) grid = need;
   configure_sweep_kernel<<<grid, SW_THREADS, smem, stream>>>(
       t->d_tp, t->d_lat, t->d_seg_start, t->d_seg_count, t->n_tables, nq, q_table, q_rate, q_bound, out);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;

@@ -22,15 +22,12 @@
 
 namespace parva {
 
-constexpr int PB_WARPS = 8;
+constexpr int PB_WARPS = 16;
 constexpr int PB_THREADS = PB_WARPS * 32;
 constexpr int QCAP = 224;                 // > 31 GPUs x 7 slots: longer queues cannot fit
 
 struct WarpScratch {
   double cat_tp[32 * 5];                  // best tp per (service, size class); 0 = absent
-  long long count[32];
-  int8_t opt_sc[32];
-  int8_t last_sc[32];
   uint16_t lst[32][8];                    // per GPU placement list: cat << 3 | slot
   uint16_t bak[32][8];                    // relocation result (regression fallback)
   uint8_t q2[QCAP];
@@ -79,7 +76,7 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
   if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
 }
 
-__global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
+__global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   uint8_t* idx_base = smem_raw + sizeof(WarpScratch) * PB_WARPS;
@@ -122,6 +119,8 @@ __global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
 
     // ------------------------------------------------------------ configure
     int err_status = 0, err_svc = 0;
+    int my_opt = -1, my_last = -1;
+    long long my_count = 0;
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       parva_config_record r;
@@ -145,9 +144,9 @@ __global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
           A.cfg[a0 + i] = r;
         }
         if (base == 0) {
-          W.opt_sc[lane] = r.opt_sc;
-          W.last_sc[lane] = r.last_sc;
-          W.count[lane] = r.count;
+          my_opt = r.opt_sc;
+          my_last = r.last_sc;
+          my_count = r.count;
 #pragma unroll
           for (int c = 0; c < 5; c++) W.cat_tp[lane * 5 + c] = tpc[c];
         }
@@ -162,7 +161,7 @@ __global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
     if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
     else if (err_status) status = err_status;
     else {
-      const long long segs = warp_sum_ll(lane < n ? W.count[lane] + (W.last_sc[lane] >= 0) : 0);
+      const long long segs = warp_sum_ll(lane < n ? my_count + (my_last >= 0) : 0);
       if (segs > 32 * 7) status = PARVA_CAPACITY;
     }
 
@@ -176,12 +175,19 @@ __global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
 
     if (status == PARVA_OK) {
       // --------------------------------------------- relocate_segments
+      // queue order (allocator.py:284-289, 46-51): size classes 7,4,3,2,1; within
+      // a class services in input order, opt copies then last.  Services with
+      // nothing of this class are skipped with one ballot.
       for (int c = 4; c >= 0 && status == PARVA_OK; c--) {
         const int size = size_of_class(c);
-        for (int s = 0; s < n && status == PARVA_OK; s++) {
-          const long long reps = (W.opt_sc[s] == c ? W.count[s] : 0) + (W.last_sc[s] == c ? 1 : 0);
+        const int my_reps = lane < n ? (my_opt == c ? (int)my_count : 0) + (my_last == c ? 1 : 0) : 0;
+        unsigned pending = __ballot_sync(0xffffffffu, my_reps > 0);
+        while (pending && status == PARVA_OK) {
+          const int s = __ffs(pending) - 1;
+          pending &= pending - 1;
+          const int reps = __shfl_sync(0xffffffffu, my_reps, s);
           const uint16_t cat = (uint16_t)(s * 5 + c);
-          for (long long r = 0; r < reps; r++) {
+          for (int r = 0; r < reps; r++) {
             int st = lane < ngpus ? find_start(mask, c) : -1;
             const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
             int g;
@@ -316,6 +322,7 @@ __global__ void __launch_bounds__(PB_THREADS) plan_batch_kernel(PlanArgs A) {
           *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
           len = bak_len; ngpc = bak_ngpc; mask = bak_mask;
           freed = 0.0; order = 0; nd = 0;
+          if (lane < PARVA_PLAN_MAX_DIAG / 2) reinterpret_cast<uint32_t*>(W.rec.diag)[lane] = 0u;
         }
       }
       __syncwarp();
