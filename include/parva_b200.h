@@ -68,10 +68,12 @@ enum parva_diag_reason {
  * pipeline.py:70-80), structure of arrays grouped by (table, size class):
  * segment s = t*5 + c holds points [seg_start[s], seg_start[s] + seg_count[s])
  * in key order (batch asc, procs asc; profiles.py:98-100).  Within a segment
- * the point's position is its tie-break rank, so no key array is read. */
+ * the point's position is its tie-break rank, so no key array is read.  A
+ * point is 16 bytes: (throughput rps, latency ms) interleaved, so every point
+ * starts 16-byte aligned and a segment streams as one contiguous range.
+ * d_pts must hold 2 extra doubles of padding. */
 typedef struct {
-  const double*  d_tp;        /* throughput, rps        [n_points] */
-  const double*  d_lat;       /* latency, ms            [n_points] */
+  const double*  d_pts;       /* (tp, lat) pairs        [2 * n_points] */
   const int64_t* d_seg_start; /* [n_tables * 5]                    */
   const int32_t* d_seg_count; /* [n_tables * 5]                    */
   int32_t n_tables;

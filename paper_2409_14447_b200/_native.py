@@ -25,7 +25,7 @@ _LOCK = threading.Lock()
 
 
 class ParvaTables(C.Structure):
-    _fields_ = [("d_tp", C.c_void_p), ("d_lat", C.c_void_p), ("d_seg_start", C.c_void_p),
+    _fields_ = [("d_pts", C.c_void_p), ("d_seg_start", C.c_void_p),
                 ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32), ("n_points", C.c_int64)]
 
 
@@ -136,8 +136,8 @@ def records_to_numpy(t, n: int, dtype: np.dtype) -> np.ndarray:
 class DeviceTables:
     """Prepared tables resident in HBM + their prefix-argmax index.
 
-    Layout: tp f64[P], lat f64[P] (+2 pad so 16-byte bulk copies
-    may round the last chunk up), seg_start i64[T*5], seg_count i32[T*5];
+    Layout: (tp, lat) f64 pairs [2P] (+2 pad), seg_start i64[T*5],
+    seg_count i32[T*5];
     index: lat_sorted f64[P], best u16[P].  batch/procs stay on the host for
     decoding winners.
     """
@@ -145,11 +145,13 @@ class DeviceTables:
     def __init__(self, packed, build_index: bool = True):
         torch = require_cuda()
         self.packed = packed
-        self.tp = to_device(packed.tp, pad=2)
-        self.lat = to_device(packed.lat, pad=2)
+        inter = np.empty(2 * packed.n_points, dtype=np.float64)
+        inter[0::2] = packed.tp
+        inter[1::2] = packed.lat
+        self.pts = to_device(inter, pad=2)
         self.seg_start = to_device(packed.seg_start.astype(np.int64))
         self.seg_count = to_device(packed.seg_count.astype(np.int32))
-        self.struct = ParvaTables(self.tp.data_ptr(), self.lat.data_ptr(), self.seg_start.data_ptr(),
+        self.struct = ParvaTables(self.pts.data_ptr(), self.seg_start.data_ptr(),
                                   self.seg_count.data_ptr(), packed.n_tables, packed.n_points)
         self.index = None
         self.index_struct = None

@@ -41,7 +41,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
                            parva_config_record* d_cfg, parva_plan_record* d_plan, double* d_ledger_val,
                            uint8_t* d_ledger_order, int cfg_given, cudaStream_t stream) {
   parva::PlanArgs A;
-  A.tp = tables->d_tp;
+  A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
   A.idx_best = index ? index->d_best : nullptr;
   A.seg_start = tables->d_seg_start;

@@ -17,14 +17,22 @@
 
 namespace parva {
 
-constexpr int SW_WARPS = 12;                   // warps per CTA, one table each at a time
+#ifndef PARVA_SW_WARPS
+#define PARVA_SW_WARPS 14
+#endif
+#ifndef PARVA_SW_CH
+#define PARVA_SW_CH 256
+#endif
+#ifndef PARVA_SW_STAGES
+#define PARVA_SW_STAGES 4
+#endif
+constexpr int SW_WARPS = PARVA_SW_WARPS;       // warps per CTA, one table each at a time
 constexpr int SW_THREADS = SW_WARPS * 32;
-constexpr int SW_CH = 384;                     // points per chunk (2 x 3 KB)
-constexpr int SW_STAGES = 3;                   // chunks in flight per warp
+constexpr int SW_CH = PARVA_SW_CH;             // points per chunk (16 B each)
+constexpr int SW_STAGES = PARVA_SW_STAGES;     // chunks in flight per warp
 
 struct alignas(128) SweepWarpSmem {
-  double tp[SW_STAGES][SW_CH + 2];
-  double lat[SW_STAGES][SW_CH + 2];
+  double2 pts[SW_STAGES][SW_CH];   // (tp, lat)
   uint64_t full[SW_STAGES];
 };
 
@@ -71,7 +79,7 @@ struct ChunkCursor {
 };
 
 __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
-    const double* __restrict__ tp, const double* __restrict__ lat,
+    const double2* __restrict__ pts,
     const int64_t* __restrict__ seg_start, const int32_t* __restrict__ seg_count, int n_tables,
     int nq, const int32_t* __restrict__ q_table, const double* __restrict__ q_rate,
     const double* __restrict__ q_bound, parva_config_record* __restrict__ out) {
@@ -98,14 +106,11 @@ __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
   uint32_t issued = 0;
   auto issue = [&]() {
     const int64_t a = P.s0 + P.off;
-    const int64_t b = P.s0 + min(P.n, P.off + SW_CH);
-    const int64_t a2 = a & ~int64_t(1), b2 = (b + 1) & ~int64_t(1);
-    const uint32_t bytes = uint32_t(b2 - a2) * 8u;
+    const uint32_t bytes = uint32_t(min(P.n - P.off, SW_CH)) * 16u;
     const int st = issued % SW_STAGES;
     if (lane == 0) {
-      mbar_arrive_expect_tx(&S.full[st], 2 * bytes);
-      bulk_g2s(S.tp[st], tp + a2, bytes, &S.full[st], pol);
-      bulk_g2s(S.lat[st], lat + a2, bytes, &S.full[st], pol);
+      mbar_arrive_expect_tx(&S.full[st], bytes);
+      bulk_g2s(S.pts[st], pts + a, bytes, &S.full[st], pol);
     }
     issued++;
     P.off += SW_CH;
@@ -156,21 +161,17 @@ __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
       Q.select(c);
       Cand best{0.0, 0.0, -1};
       for (int off = 0; off < Q.n; off += SW_CH) {
-        const int64_t a = Q.s0 + off, b = Q.s0 + min(Q.n, off + SW_CH);
-        const int64_t a2 = a & ~int64_t(1);
+        const int hi = min(Q.n - off, SW_CH);
         const int st = consumed % SW_STAGES;
         mbar_wait(&S.full[st], (consumed / SW_STAGES) & 1);
-        const double* stp = S.tp[st];
-        const double* slat = S.lat[st];
-        const int lo = int(a - a2), hi = int(b - a2);
-        const int base = int(a2 - Q.s0);
+        const double2* sp = S.pts[st];
 #pragma unroll
-        for (int j0 = 0; j0 < SW_CH + 2; j0 += 32) {
+        for (int j0 = 0; j0 < SW_CH; j0 += 32) {
           const int j = j0 + lane;
-          if (j >= lo && j < hi) {
-            const double l = slat[j];
-            if (l < bound) {
-              Cand cnd{stp[j], l, base + j};
+          if (j < hi) {
+            const double2 v = sp[j];
+            if (v.y < bound) {
+              Cand cnd{v.x, v.y, off + j};
               if (better(cnd, best)) best = cnd;
             }
           }
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
 constexpr int IDX_MAX = 4096;
 
 __global__ void __launch_bounds__(256) build_index_kernel(
-    const double* __restrict__ tp, const double* __restrict__ lat,
+    const double2* __restrict__ pts,
     const int64_t* __restrict__ seg_start, const int32_t* __restrict__ seg_count,
     double* __restrict__ lat_sorted, uint16_t* __restrict__ best_out, int* __restrict__ err) {
   __shared__ double sl[IDX_MAX];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256) build_index_kernel(
     if (threadIdx.x == 0) atomicExch(err, 1);
     return;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sl[i] = lat[s0 + i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sl[i] = pts[s0 + i].y;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double li = sl[i];
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(256) build_index_kernel(
     Cand b{0.0, 0.0, -1};
     for (int r = 0; r < n; r++) {
       const int i = order[r];
-      Cand c{tp[s0 + i], sl[i], i};
+      Cand c{pts[s0 + i].x, sl[i], i};
       if (better(c, b)) b = c;
       lat_sorted[s0 + r] = sl[i];
       best_out[s0 + r] = (uint16_t)b.idx;
@@ -260,14 +261,14 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
   const int need = (nq + SW_WARPS - 1) / SW_WARPS;
   if (grid > need) grid = need;
   configure_sweep_kernel<<<grid, SW_THREADS, smem, stream>>>(
-      t->d_tp, t->d_lat, t->d_seg_start, t->d_seg_count, t->n_tables, nq, q_table, q_rate, q_bound, out);
+      reinterpret_cast<const double2*>(t->d_pts), t->d_seg_start, t->d_seg_count, t->n_tables, nq, q_table, q_rate, q_bound, out);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
 int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cudaStream_t stream) {
   const int nseg = t->n_tables * 5;
   if (nseg <= 0) return PARVA_OK;
-  build_index_kernel<<<nseg, 256, 0, stream>>>(t->d_tp, t->d_lat, t->d_seg_start, t->d_seg_count,
+  build_index_kernel<<<nseg, 256, 0, stream>>>(reinterpret_cast<const double2*>(t->d_pts), t->d_seg_start, t->d_seg_count,
                                                idx->d_lat_sorted, idx->d_best, d_err);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }

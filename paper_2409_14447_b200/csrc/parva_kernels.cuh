@@ -9,7 +9,7 @@
 namespace parva {
 
 struct PlanArgs {
-  const double* tp;              // prepared points (global)
+  const double* pts;             // prepared (tp, lat) pairs (global)
   const double* idx_lat;         // prefix-argmax index (global; copied to smem)
   const uint16_t* idx_best;
   const int64_t* seg_start;

@@ -55,7 +55,7 @@ __device__ __forceinline__ double unallocated(int total, int n) {
 
 // configure one service from the index (binary search per size class)
 __device__ __forceinline__ void configure_indexed(const double* lat_s, const uint16_t* best_s,
-                                                  const double* tp, const int* seg_s,
+                                                  const double* tp, int tp_stride, const int* seg_s,
                                                   const int* seg_n, int t, double bound,
                                                   double rate, parva_config_record& r,
                                                   double tpc[5]) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
     }
     const int b = lo ? (int)best_s[s0 + lo - 1] : -1;
     r.best[c] = (int16_t)b;
-    tpc[c] = b >= 0 ? tp[s0 + b] : 0.0;
+    tpc[c] = b >= 0 ? tp[(s0 + b) * tp_stride] : 0.0;
   }
   match_demand(tpc, rate, r);
   if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   int* seg_n = seg_s + T5;
   const double* lat_s = A.idx_lat;
   const uint16_t* best_s = A.idx_best;
-  const double* tp_s = A.tp;
+  const double* tp_s = A.pts;   // stride 2 in global, 1 in smem
+  int tp_stride = 2;
   if (A.smem_index) {
     double* lat_w = reinterpret_cast<double*>(idx_base + ((size_t(T5) * 8 + 15) & ~size_t(15)));
     double* tp_w = lat_w + A.n_points;
@@ -96,10 +97,10 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
     }
     for (int64_t i = threadIdx.x; i < A.n_points; i += blockDim.x) {
       lat_w[i] = A.idx_lat[i];
-      tp_w[i] = A.tp[i];
+      tp_w[i] = A.pts[2 * i];
       best_w[i] = A.idx_best[i];
     }
-    lat_s = lat_w; tp_s = tp_w; best_s = best_w;
+    lat_s = lat_w; tp_s = tp_w; best_s = best_w; tp_stride = 1;
   } else {
     for (int i = threadIdx.x; i < T5; i += blockDim.x) {
       seg_s[i] = (int)A.seg_start[i];
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
           r = A.cfg[a0 + i];
           const int t = A.svc_table[a0 + i];
           for (int c = 0; c < 5; c++)
-            tpc[c] = r.best[c] >= 0 ? A.tp[A.seg_start[t * 5 + c] + r.best[c]] : 0.0;
+            tpc[c] = r.best[c] >= 0 ? A.pts[2 * (A.seg_start[t * 5 + c] + r.best[c])] : 0.0;
         } else {
           r = {};
           const int t = A.svc_table[a0 + i];
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
             for (int c = 0; c < 5; c++) r.best[c] = -1;
             r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
           } else {
-            configure_indexed(lat_s, best_s, tp_s, seg_s, seg_n, t, A.svc_bound[a0 + i],
+            configure_indexed(lat_s, best_s, tp_s, tp_stride, seg_s, seg_n, t, A.svc_bound[a0 + i],
                               A.svc_rate[a0 + i], r, tpc);
           }
           A.cfg[a0 + i] = r;
