@@ -85,8 +85,9 @@ typedef struct {
  * within-segment position of the argmax of the first j+1 sorted points under
  * (tp desc, lat asc, position asc). */
 typedef struct {
-  double*   d_lat_sorted;     /* [n_points]                      */
-  uint16_t* d_best;           /* [n_points]                      */
+  double*   d_lat_sorted;     /* [n_points + 2]                  */
+  uint16_t* d_best;           /* [n_points + 8]                  */
+  double*   d_tp;             /* [n_points + 2] tp in key order  */
 } parva_index;
 
 /* 32-byte per-service configuration record (a Service after match_demand). */

@@ -30,7 +30,7 @@ class ParvaTables(C.Structure):
 
 
 class ParvaIndex(C.Structure):
-    _fields_ = [("d_lat_sorted", C.c_void_p), ("d_best", C.c_void_p)]
+    _fields_ = [("d_lat_sorted", C.c_void_p), ("d_best", C.c_void_p), ("d_tp", C.c_void_p)]
 
 
 class GeneralProblem(C.Structure):
@@ -158,7 +158,8 @@ class DeviceTables:
         if build_index and packed.n_points and int(packed.seg_count.max(initial=0)) <= 4096:
             self.lat_sorted = torch.empty(packed.n_points + 2, dtype=torch.float64, device="cuda")
             self.best = torch.empty(packed.n_points + 8, dtype=torch.int16, device="cuda")
-            self.index_struct = ParvaIndex(self.lat_sorted.data_ptr(), self.best.data_ptr())
+            self.idx_tp = torch.empty(packed.n_points + 2, dtype=torch.float64, device="cuda")
+            self.index_struct = ParvaIndex(self.lat_sorted.data_ptr(), self.best.data_ptr(), self.idx_tp.data_ptr())
             check(lib().parva_build_index(C.byref(self.struct), C.byref(self.index_struct), stream_handle()),
                   "parva_build_index")
             self.index = True

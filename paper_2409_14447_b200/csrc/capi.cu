@@ -44,6 +44,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
   A.idx_best = index ? index->d_best : nullptr;
+  A.idx_tp = index ? index->d_tp : nullptr;
   A.seg_start = tables->d_seg_start;
   A.seg_count = tables->d_seg_count;
   A.n_tables = tables->n_tables;

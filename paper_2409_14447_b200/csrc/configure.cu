@@ -159,27 +159,39 @@ __global__ void __launch_bounds__(SW_THREADS) configure_sweep_kernel(
 #pragma unroll 1
     for (int c = 0; c < 5; c++) {
       Q.select(c);
-      Cand best{0.0, 0.0, -1};
+      // lane-local running best: a lane sees its points in increasing
+      // position, so (tp desc, lat asc) decides and later equal points lose
+      // on position; tp > 0, so btp = 0 means "none yet"
+      double btp = 0.0, blat = 0.0;
+      int bidx = -1;
       for (int off = 0; off < Q.n; off += SW_CH) {
         const int hi = min(Q.n - off, SW_CH);
         const int st = consumed % SW_STAGES;
         mbar_wait(&S.full[st], (consumed / SW_STAGES) & 1);
         const double2* sp = S.pts[st];
+        if (hi == SW_CH) {
 #pragma unroll
-        for (int j0 = 0; j0 < SW_CH; j0 += 32) {
-          const int j = j0 + lane;
-          if (j < hi) {
+          for (int j0 = 0; j0 < SW_CH; j0 += 32) {
+            const double2 v = sp[j0 + lane];
+            const bool take = v.y < bound && (v.x > btp || (v.x == btp && v.y < blat));
+            btp = take ? v.x : btp;
+            blat = take ? v.y : blat;
+            bidx = take ? off + j0 + lane : bidx;
+          }
+        } else {
+          for (int j = lane; j < hi; j += 32) {
             const double2 v = sp[j];
-            if (v.y < bound) {
-              Cand cnd{v.x, v.y, off + j};
-              if (better(cnd, best)) best = cnd;
-            }
+            const bool take = v.y < bound && (v.x > btp || (v.x == btp && v.y < blat));
+            btp = take ? v.x : btp;
+            blat = take ? v.y : blat;
+            bidx = take ? off + j : bidx;
           }
         }
         consumed++;
         __syncwarp();
         if (p_ok) issue();
       }
+      Cand best{btp, blat, bidx};
       best = warp_argmax(best);
       if (lane == slot) {
         switch (c) {
@@ -204,7 +216,8 @@ constexpr int IDX_MAX = 4096;
 __global__ void __launch_bounds__(256) build_index_kernel(
     const double2* __restrict__ pts,
     const int64_t* __restrict__ seg_start, const int32_t* __restrict__ seg_count,
-    double* __restrict__ lat_sorted, uint16_t* __restrict__ best_out, int* __restrict__ err) {
+    double* __restrict__ lat_sorted, uint16_t* __restrict__ best_out, double* __restrict__ tp_out,
+    int* __restrict__ err) {
   __shared__ double sl[IDX_MAX];
   __shared__ uint16_t order[IDX_MAX];
   const int s = blockIdx.x;
@@ -214,7 +227,10 @@ __global__ void __launch_bounds__(256) build_index_kernel(
     if (threadIdx.x == 0) atomicExch(err, 1);
     return;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sl[i] = pts[s0 + i].y;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sl[i] = pts[s0 + i].y;
+    tp_out[s0 + i] = pts[s0 + i].x;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double li = sl[i];
@@ -269,7 +285,7 @@ int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cuda
   const int nseg = t->n_tables * 5;
   if (nseg <= 0) return PARVA_OK;
   build_index_kernel<<<nseg, 256, 0, stream>>>(reinterpret_cast<const double2*>(t->d_pts), t->d_seg_start, t->d_seg_count,
-                                               idx->d_lat_sorted, idx->d_best, d_err);
+                                               idx->d_lat_sorted, idx->d_best, idx->d_tp, d_err);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 

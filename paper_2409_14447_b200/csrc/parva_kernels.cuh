@@ -12,6 +12,7 @@ struct PlanArgs {
   const double* pts;             // prepared (tp, lat) pairs (global)
   const double* idx_lat;         // prefix-argmax index (global; copied to smem)
   const uint16_t* idx_best;
+  const double* idx_tp;          // tp in key order (index copy, 16-B padded)
   const int64_t* seg_start;
   const int32_t* seg_count;
   int n_tables;

@@ -17,6 +17,7 @@
 // are re-planned by the general kernel (plan_general.cu).
 #include <cuda_runtime.h>
 
+#include "parva_async.cuh"
 #include "parva_common.cuh"
 #include "parva_kernels.cuh"
 
@@ -53,27 +54,71 @@ __device__ __forceinline__ double unallocated(int total, int n) {
   return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
 }
 
-// configure one service from the index (binary search per size class)
+// configure one service from the index: for each size class, count = number
+// of points with lat < bound (binary search over the latency-sorted
+// segment), winner = prefix argmax at count-1.  The five searches advance in
+// lockstep (branch-free power-of-two steps) so their loads overlap.
 __device__ __forceinline__ void configure_indexed(const double* lat_s, const uint16_t* best_s,
                                                   const double* tp, int tp_stride, const int* seg_s,
                                                   const int* seg_n, int t, double bound,
                                                   double rate, parva_config_record& r,
                                                   double tpc[5]) {
+  int s0[5], n[5], lo[5];
+  int nmax = 0;
 #pragma unroll
   for (int c = 0; c < 5; c++) {
-    const int s0 = seg_s[t * 5 + c], n = seg_n[t * 5 + c];
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (lat_s[s0 + mid] < bound) lo = mid + 1;
-      else hi = mid;
+    s0[c] = seg_s[t * 5 + c];
+    n[c] = seg_n[t * 5 + c];
+    lo[c] = 0;
+    nmax = max(nmax, n[c]);
+  }
+  for (int step = nmax ? 1 << (31 - __clz(nmax)) : 0; step > 0; step >>= 1) {
+#pragma unroll
+    for (int c = 0; c < 5; c++) {
+      const int probe = lo[c] + step;
+      if (probe <= n[c] && lat_s[s0[c] + probe - 1] < bound) lo[c] = probe;
     }
-    const int b = lo ? (int)best_s[s0 + lo - 1] : -1;
+  }
+#pragma unroll
+  for (int c = 0; c < 5; c++) {
+    const int b = lo[c] ? (int)best_s[s0[c] + lo[c] - 1] : -1;
     r.best[c] = (int16_t)b;
-    tpc[c] = b >= 0 ? tp[(s0 + b) * tp_stride] : 0.0;
+    tpc[c] = b >= 0 ? tp[(s0[c] + b) * tp_stride] : 0.0;
   }
   match_demand(tpc, rate, r);
   if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
+}
+
+// one relocation size class (allocator.py:284-289): services in input order,
+// opt copies then last; c is a compile-time constant in each instantiation
+template <int c>
+__device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, int my_opt, long long my_count,
+                                               int my_last, uint32_t& mask, int& ngpc, int& len, int& ngpus,
+                                               int& status) {
+  const int my_reps = lane < n ? (my_opt == c ? (int)my_count : 0) + (my_last == c ? 1 : 0) : 0;
+  unsigned pending = __ballot_sync(0xffffffffu, my_reps > 0);
+  while (pending && status == PARVA_OK) {
+    const int s = __ffs(pending) - 1;
+    pending &= pending - 1;
+    const int reps = __shfl_sync(0xffffffffu, my_reps, s);
+    const uint16_t cat3 = (uint16_t)((s * 5 + c) << 3);
+    for (int r = 0; r < reps; r++) {
+      int st = lane < ngpus ? find_start(mask, c) : -1;
+      const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
+      int g;
+      if (b) g = __ffs(b) - 1;
+      else {
+        if (ngpus >= PARVA_PLAN_MAX_GPUS) { status = PARVA_CAPACITY; break; }
+        g = ngpus++;
+        st = find_start(0u, c);
+      }
+      if (lane == g) {
+        mask |= footprint(c, st);
+        ngpc += size_of_class(c);
+        W.lst[g][len++] = (uint16_t)(cat3 | st);
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
@@ -87,25 +132,31 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   const uint16_t* best_s = A.idx_best;
   const double* tp_s = A.pts;   // stride 2 in global, 1 in smem
   int tp_stride = 2;
+  for (int i = threadIdx.x; i < T5; i += blockDim.x) {
+    seg_s[i] = (int)A.seg_start[i];
+    seg_n[i] = A.seg_count[i];
+  }
   if (A.smem_index) {
-    double* lat_w = reinterpret_cast<double*>(idx_base + ((size_t(T5) * 8 + 15) & ~size_t(15)));
-    double* tp_w = lat_w + A.n_points;
-    uint16_t* best_w = reinterpret_cast<uint16_t*>(tp_w + A.n_points);
-    for (int i = threadIdx.x; i < T5; i += blockDim.x) {
-      seg_s[i] = (int)A.seg_start[i];
-      seg_n[i] = A.seg_count[i];
+    // three 1-D bulk copies (TMA) into shared memory, one mbarrier
+    const size_t off_lat = (size_t(T5) * 8 + 15) & ~size_t(15);
+    const uint32_t b_dbl = uint32_t((A.n_points * 8 + 15) & ~int64_t(15));
+    const uint32_t b_u16 = uint32_t((A.n_points * 2 + 15) & ~int64_t(15));
+    double* lat_w = reinterpret_cast<double*>(idx_base + off_lat);
+    double* tp_w = reinterpret_cast<double*>(idx_base + off_lat + b_dbl);
+    uint16_t* best_w = reinterpret_cast<uint16_t*>(idx_base + off_lat + 2 * size_t(b_dbl));
+    __shared__ uint64_t idx_bar;
+    if (threadIdx.x == 0) {
+      mbar_init(&idx_bar, 1);
+      fence_mbar_init();
+      mbar_arrive_expect_tx(&idx_bar, 2 * b_dbl + b_u16);
+      const uint64_t pol = policy_evict_last();
+      bulk_g2s(lat_w, A.idx_lat, b_dbl, &idx_bar, pol);
+      bulk_g2s(tp_w, A.idx_tp, b_dbl, &idx_bar, pol);
+      bulk_g2s(best_w, A.idx_best, b_u16, &idx_bar, pol);
     }
-    for (int64_t i = threadIdx.x; i < A.n_points; i += blockDim.x) {
-      lat_w[i] = A.idx_lat[i];
-      tp_w[i] = A.pts[2 * i];
-      best_w[i] = A.idx_best[i];
-    }
+    __syncthreads();
+    mbar_wait(&idx_bar, 0);
     lat_s = lat_w; tp_s = tp_w; best_s = best_w; tp_stride = 1;
-  } else {
-    for (int i = threadIdx.x; i < T5; i += blockDim.x) {
-      seg_s[i] = (int)A.seg_start[i];
-      seg_n[i] = A.seg_count[i];
-    }
   }
   __syncthreads();
 
@@ -142,7 +193,9 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
             configure_indexed(lat_s, best_s, tp_s, tp_stride, seg_s, seg_n, t, A.svc_bound[a0 + i],
                               A.svc_rate[a0 + i], r, tpc);
           }
-          A.cfg[a0 + i] = r;
+          uint4* dst = reinterpret_cast<uint4*>(A.cfg + a0 + i);
+          dst[0] = reinterpret_cast<const uint4*>(&r)[0];
+          dst[1] = reinterpret_cast<const uint4*>(&r)[1];
         }
         if (base == 0) {
           my_opt = r.opt_sc;
@@ -176,36 +229,12 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
 
     if (status == PARVA_OK) {
       // --------------------------------------------- relocate_segments
-      // queue order (allocator.py:284-289, 46-51): size classes 7,4,3,2,1; within
-      // a class services in input order, opt copies then last.  Services with
-      // nothing of this class are skipped with one ballot.
-      for (int c = 4; c >= 0 && status == PARVA_OK; c--) {
-        const int size = size_of_class(c);
-        const int my_reps = lane < n ? (my_opt == c ? (int)my_count : 0) + (my_last == c ? 1 : 0) : 0;
-        unsigned pending = __ballot_sync(0xffffffffu, my_reps > 0);
-        while (pending && status == PARVA_OK) {
-          const int s = __ffs(pending) - 1;
-          pending &= pending - 1;
-          const int reps = __shfl_sync(0xffffffffu, my_reps, s);
-          const uint16_t cat = (uint16_t)(s * 5 + c);
-          for (int r = 0; r < reps; r++) {
-            int st = lane < ngpus ? find_start(mask, c) : -1;
-            const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
-            int g;
-            if (b) g = __ffs(b) - 1;
-            else {
-              if (ngpus >= PARVA_PLAN_MAX_GPUS) { status = PARVA_CAPACITY; break; }
-              g = ngpus++;
-              st = find_start(0u, c);
-            }
-            if (lane == g) {
-              mask |= footprint(c, st);
-              ngpc += size;
-              W.lst[g][len++] = (uint16_t)(cat << 3 | st);
-            }
-          }
-        }
-      }
+      // queue order (allocator.py:46-51): size classes 7,4,3,2,1
+      relocate_class<4>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
+      if (status == PARVA_OK) relocate_class<3>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
+      if (status == PARVA_OK) relocate_class<2>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
+      if (status == PARVA_OK) relocate_class<1>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
+      if (status == PARVA_OK) relocate_class<0>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
     }
     __syncwarp();
 
@@ -385,7 +414,7 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
 
 size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index) {
   size_t b = sizeof(WarpScratch) * PB_WARPS + ((size_t(n_tables) * 5 * 8 + 15) & ~size_t(15));
-  if (smem_index) b += size_t(n_points) * (8 + 8 + 2);
+  if (smem_index) b += 2 * size_t((n_points * 8 + 15) & ~int64_t(15)) + size_t((n_points * 2 + 15) & ~int64_t(15));
   return (b + 15) & ~size_t(15);
 }
 
