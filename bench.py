@@ -158,7 +158,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scenarios", type=int, default=10_000, help="scenarios per GPU per step")
+    ap.add_argument("--scenarios", type=int, default=10_000,
+                    help="scenarios per GPU per step (weak) or in total (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-sweep", action="store_true", help="skip the C3 configurator-sweep measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--sweep-workloads", type=int, default=10_000)
@@ -184,21 +186,28 @@ def main():
     from paper_2409_14447_b200 import workloads as W
     from paper_2409_14447_b200.records import PLAN_DTYPE
 
+    from paper_2409_14447_b200.distributed import gather_records, make_shard
+
     fx = W.load_fixtures()
     dt = N.device_tables_for(fx.tables)
-    n = args.scenarios
-    off, tab, rate, bound = c2_inputs(fx, n, rank)
+    n_global = args.scenarios * (world if args.scaling == "weak" else 1)
+    g_off, g_tab, g_rate, g_bound = c2_inputs(fx, n_global, 0)   # N=1 weak: exactly C2
+    shard = make_shard(g_off, rank, world)
+    off = shard.off
+    tab = g_tab[shard.svc_a:shard.svc_b]
+    rate = np.ascontiguousarray(g_rate[shard.svc_a:shard.svc_b])
+    bound = np.ascontiguousarray(g_bound[shard.svc_a:shard.svc_b])
+    n = shard.scen_b - shard.scen_a
     d_off, d_tab = N.to_device(off), N.to_device(tab)
     d_rate, d_bound = N.to_device(rate), N.to_device(bound)
     stream = torch.cuda.current_stream()
     res = B.plan_batch(dt, d_off, d_tab, d_rate, d_bound)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    gathered = torch.empty((world, n, PLAN_DTYPE.itemsize), dtype=torch.uint8, device="cuda") if world > 1 else None
 
     def step():
         B.plan_batch(dt, d_off, d_tab, d_rate, d_bound, out=res)
         if world > 1:
-            dist.all_gather_into_tensor(gathered.view(world, -1), res.plan[:n].reshape(-1))
+            gather_records(res.cfg, res.plan, shard, g_off)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -217,7 +226,7 @@ def main():
             B.plan_batch(dt, d_off, d_tab, d_rate, d_bound, out=res)
             kev[i][1].record(stream)
             if world > 1:
-                dist.all_gather_into_tensor(gathered.view(world, -1), res.plan[:n].reshape(-1))
+                gather_records(res.cfg, res.plan, shard, g_off)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         # keep the GPU busy a little longer so the sampler sees the loaded clocks
@@ -281,17 +290,18 @@ def main():
     bytes_per_launch = n_svc * (20 + 32 + 9) + n * (4 + 128) + dt.packed.n_points * 18
     kern_s = kern_ms / 1000.0 / args.steps
     achieved = bytes_per_launch / kern_s / 1e9
-    value = n * world * args.steps / (step_ms / 1000.0)
+    value = n_global * args.steps / (step_ms / 1000.0)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY C2 generator, seed = rank; fixture tables rendered from the reference)",
-        "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU",
-                   "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n * world,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY C2 generator, seed 0, sharded contiguously; fixture tables rendered from the reference)",
+        "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU"
+                               if args.scaling == "weak" else f"C2/C4 generator, {n_global} scenarios total",
+                   "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n_global,
                    "l2": "flushed between steps (512 MiB write, outside the events)",
-                   "parallelism": f"scenario-sharded x{world}" + (" + NCCL all-gather of plan records" if world > 1 else ""),
+                   "parallelism": f"scenario-sharded x{world}" + (" + NCCL all-gather of plan+config records" if world > 1 else ""),
                    "optimize": True, "threshold": 4},
         "gpu_launches": args.steps,
         "kernel_ms_per_step": kern_ms / args.steps,
@@ -299,7 +309,7 @@ def main():
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
-        "e2e": {"value": n * world * args.steps / e2e_s, "unit": UNIT,
+        "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int((n + 1) * 4 + n_svc * 20),
                 "d2h_bytes_per_step": int(n_svc * 32 + n * 128),
                 "api": "parva_plan_host (C ABI, pinned host buffers)"},

@@ -1,0 +1,86 @@
+"""Scenario sharding across GPUs: one process per GPU, torch.distributed.
+
+Scenarios are independent, so a batch shards into contiguous
+scenario blocks, one per rank, with no exchange during planning.  The only
+collective is the gather of the fixed-size results at the end:
+one all-gather of the 128-byte plan records and one of the 32-byte config
+records, each padded to the largest shard so every rank contributes the
+same byte count (NCCL over NVLink on the GPU box; gloo in the CPU tests).
+
+`plan_fn(off, tab, rate, bound) -> (cfg_u8[n_svc,32], plan_u8[n_scen,128])`
+is the per-rank planner: batch.plan_batch on the GPU; the tests inject the
+CPU oracle to check the sharding/gather logic without a GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [a, b) of n items for `rank` (sizes differ by at most 1)."""
+    base, extra = divmod(n, world)
+    a = rank * base + min(rank, extra)
+    return a, a + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class Shard:
+    scen_a: int
+    scen_b: int
+    off: np.ndarray     # local scenario offsets (start at 0)
+    svc_a: int
+    svc_b: int
+
+
+def make_shard(scen_off: np.ndarray, rank: int, world: int) -> Shard:
+    n = len(scen_off) - 1
+    a, b = shard_bounds(n, rank, world)
+    sa, sb = int(scen_off[a]), int(scen_off[b])
+    return Shard(a, b, (scen_off[a:b + 1] - sa).astype(np.int32), sa, sb)
+
+
+def gather_records(local_cfg, local_plan, shard: Shard, scen_off, group=None, device=None):
+    """All-gather padded per-rank record blocks and reassemble in global order.
+
+    local_cfg / local_plan: torch uint8 tensors [n, 32] / [n, 128] on the
+    collective's device.  Returns (cfg [N_svc, 32], plan [N_scen, 128]) as
+    torch tensors on that device."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n_scen = len(scen_off) - 1
+    sizes_s = [shard_bounds(n_scen, r, world) for r in range(world)]
+    max_s = max(b - a for a, b in sizes_s)
+    sizes_v = [(int(scen_off[a]), int(scen_off[b])) for a, b in sizes_s]
+    max_v = max(b - a for a, b in sizes_v)
+    dev = local_plan.device if device is None else device
+
+    def padded(t, rows, width):
+        out = torch.zeros((max(rows, 1), width), dtype=torch.uint8, device=dev)
+        out[:t.shape[0]] = t
+        return out
+
+    pl = padded(local_plan[:shard.scen_b - shard.scen_a], max_s, 128)
+    cf = padded(local_cfg[:shard.svc_b - shard.svc_a], max_v, 32)
+    all_pl = torch.empty((world * max(max_s, 1), 128), dtype=torch.uint8, device=dev)
+    all_cf = torch.empty((world * max(max_v, 1), 32), dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(all_pl, pl, group=group)
+    dist.all_gather_into_tensor(all_cf, cf, group=group)
+    plan = torch.cat([all_pl[r * max(max_s, 1): r * max(max_s, 1) + (b - a)] for r, (a, b) in enumerate(sizes_s)])
+    cfg = torch.cat([all_cf[r * max(max_v, 1): r * max(max_v, 1) + (b - a)] for r, (a, b) in enumerate(sizes_v)])
+    return cfg, plan
+
+
+def plan_sharded(scen_off, svc_table, svc_rate, svc_bound, plan_fn, group=None, device=None):
+    """Plan this rank's contiguous shard with plan_fn, then all-gather every
+    rank's records.  All ranks return the full (cfg, plan) record arrays."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    scen_off = np.asarray(scen_off, dtype=np.int32)
+    sh = make_shard(scen_off, rank, world)
+    cfg, plan = plan_fn(sh.off, np.asarray(svc_table)[sh.svc_a:sh.svc_b],
+                        np.asarray(svc_rate)[sh.svc_a:sh.svc_b], np.asarray(svc_bound)[sh.svc_a:sh.svc_b])
+    return gather_records(cfg, plan, sh, scen_off, group=group, device=device)
