@@ -247,9 +247,9 @@ def main():
     if rank == 0:
         import oracle
         from paper_2409_14447_b200.tables import pack_tables
-        cfg, plan, _, _ = res.host()
+        cfg, plan = res.host()
         k = min(n, 2000)
-        ocfg, oplan, _, _ = oracle.plan_batch_records(pack_tables(fx.tables), off[:k + 1], tab[:off[k]],
+        ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off[:k + 1], tab[:off[k]],
                                                       rate[:off[k]], bound[:off[k]])
         parity = bool(cfg[:off[k]].tobytes() == ocfg.tobytes() and plan[:k].tobytes() == oplan.tobytes())
 
@@ -258,7 +258,7 @@ def main():
     n_svc = int(off[-1])
     h_off = torch.from_numpy(off).pin_memory(); h_tab = torch.from_numpy(tab).pin_memory()
     h_rate = torch.from_numpy(rate).pin_memory(); h_bound = torch.from_numpy(bound).pin_memory()
-    h_cfg = torch.empty((n_svc, 32), dtype=torch.uint8).pin_memory()
+    h_cfg = torch.empty((n_svc, 16), dtype=torch.uint8).pin_memory()   # compact config records
     h_plan = torch.empty((n, 128), dtype=torch.uint8).pin_memory()
     scratch_b = int(L.parva_plan_host_scratch(C.c_int32(n), C.c_int32(n_svc)))
     scratch = torch.empty(scratch_b, dtype=torch.uint8, device="cuda")
@@ -267,7 +267,7 @@ def main():
     def e2e_call():
         rc = L.parva_plan_host(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n), N.ptr(h_off), N.ptr(h_tab),
                                N.ptr(h_rate), N.ptr(h_bound), C.c_int32(1), C.c_int32(4), N.ptr(h_cfg),
-                               N.ptr(h_plan), N.ptr(scratch), C.c_size_t(scratch_b), sh)
+                               C.c_int32(1), N.ptr(h_plan), N.ptr(scratch), C.c_size_t(scratch_b), sh)
         N.check(rc, "parva_plan_host")
 
     for _ in range(args.warmup):
@@ -284,10 +284,10 @@ def main():
     e2e_s = float(te[0])
 
     hbm, peak_src = peaks()
-    # algorithmic bytes per K2 launch (DESIGN.md §Roofline): per service 20 B in
-    # (table id, rate, bound) + 32 B config record + 9 B ledger out; per scenario
-    # 4 B offset + 128 B plan record; tables+index once (18 B / point).
-    bytes_per_launch = n_svc * (20 + 32 + 9) + n * (4 + 128) + dt.packed.n_points * 18
+    # algorithmic bytes per K2 launch (DESIGN.md §4): per service 20 B in
+    # (table id, rate, bound) + 32 B config record out; per scenario 4 B
+    # offset + 128 B plan record; tables+index once (18 B / point).
+    bytes_per_launch = n_svc * (20 + 32) + n * (4 + 128) + dt.packed.n_points * 18
     kern_s = kern_ms / 1000.0 / args.steps
     achieved = bytes_per_launch / kern_s / 1e9
     value = n_global * args.steps / (step_ms / 1000.0)
@@ -311,8 +311,9 @@ def main():
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
         "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": int((n + 1) * 4 + n_svc * 20),
-                "d2h_bytes_per_step": int(n_svc * 32 + n * 128),
-                "api": "parva_plan_host (C ABI, pinned host buffers)"},
+                "d2h_bytes_per_step": int(n_svc * 16 + n * 128),
+                "api": "parva_plan_host (C ABI, pinned host buffers, 16-B compact config + 128-B plan records "
+                       "incl. the freed_rate ledger, chunked H2D/plan/D2H pipeline)"},
         "parity_vs_oracle_first_2000": parity,
     }
     clk_summary = clk.summary()

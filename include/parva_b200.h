@@ -102,15 +102,34 @@ typedef struct {
   double  coverage;              /* Service.coverage (Python 3.12 sum, Neumaier)    */
 } parva_config_record;
 
-/* 128-byte per-scenario plan record (fast path: <=32 services, <=32 GPUs,
- * <=40 final placements, <=20 diagnostics; else status PARVA_CAPACITY).
- *   place[i] = gpu << 11 | cat << 3 | slot,  cat = service * 5 + size class
- *   diag[i]  = gpu << 7 | reason << 5 | service
- * GPU ids equal relocation indices (allocator.py:280-281 on a fresh map);
- * placements are listed GPU by GPU in final-map order, each GPU's list in
- * list order (the order optimize_allocation leaves them in). */
-#define PARVA_PLAN_MAX_PLACE 40
-#define PARVA_PLAN_MAX_DIAG 20
+/* 16-byte compact config record (host transfers; parva_plan_host).  count
+ * saturates at 65535 with flags bit0 set (such a service cannot fit the fast
+ * path's record anyway).  Coverage is not carried: Service.coverage is a
+ * property of the decoded segments (configurator.py:60-62). */
+typedef struct {
+  int16_t  best[PARVA_NUM_SIZES];
+  int8_t   opt_sc;
+  int8_t   last_sc;
+  uint8_t  status;
+  uint8_t  flags;               /* bit0: count saturated */
+  uint16_t count;
+} parva_config_compact;
+
+#define PARVA_CFG_FULL 0
+#define PARVA_CFG_COMPACT 1
+
+/* 128-byte per-scenario plan record (fast path: <=32 services, <=32 GPUs).
+ * Header (8 B), then a packed 120-byte payload:
+ *   u16 place[n_place]   gpu << 11 | cat << 3 | slot, cat = service*5 + size class
+ *   u16 diag[n_diag]     gpu << 7 | reason << 5 | service
+ *   (pad to 8 B)  f64 ledger_val[n_ledger]  u16 ledger_key[n_ledger]
+ *                 ledger_key = service | rank << 8; entry i has rank i+1
+ *                 (freed_rate insertion order, allocator.py:396)
+ * Anything that does not fit 120 B reports PARVA_CAPACITY and is re-planned
+ * by the general kernel.  GPU ids equal relocation indices
+ * (allocator.py:280-281 on a fresh map); placements are listed GPU by GPU
+ * in final-map order, each GPU's list in list order. */
+#define PARVA_PLAN_PAYLOAD 120
 #define PARVA_PLAN_MAX_GPUS 32
 #define PARVA_PLAN_MAX_SERVICES 32
 #define PARVA_FLAG_FALLBACK 1u   /* regression fallback: map = relocation result */
@@ -122,10 +141,9 @@ typedef struct {
   uint8_t  n_gpus_unopt;  /* PlanResult.unoptimized_gpu_count (pipeline.py:98) */
   uint8_t  n_place;
   uint8_t  n_diag;
+  uint8_t  n_ledger;
   uint8_t  flags;
-  uint8_t  total_gpcs;
-  uint16_t place[PARVA_PLAN_MAX_PLACE];
-  uint16_t diag[PARVA_PLAN_MAX_DIAG];
+  uint8_t  payload[PARVA_PLAN_PAYLOAD];
 } parva_plan_record;
 
 /* ---------------------------------------------------------------- entries */
@@ -148,16 +166,15 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries,
 
 /* Plan n_scenarios independent scenarios.  Scenario k owns services
  * [d_scen_off[k], d_scen_off[k+1]); service i queries table d_svc_table[i].
- * Writes one config record per service and one plan record per scenario;
- * d_ledger_val / d_ledger_order (optional, may be NULL) receive the
- * freed_rate ledger per service (order 0 = key absent, else 1-based
- * insertion rank).  index must have been built from tables. */
+ * Writes one config record per service (parva_config_record, or
+ * parva_config_compact when cfg_format == PARVA_CFG_COMPACT) and one plan
+ * record per scenario.  index must have been built from tables. */
 int parva_plan_batch(const parva_tables* tables, const parva_index* index,
                      int32_t n_scenarios, const int32_t* d_scen_off,
                      const int32_t* d_svc_table, const double* d_svc_rate,
                      const double* d_svc_bound, int32_t optimize, int32_t threshold,
-                     parva_config_record* d_cfg, parva_plan_record* d_plan,
-                     double* d_ledger_val, uint8_t* d_ledger_order, void* stream);
+                     void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
+                     void* stream);
 
 /* parva_plan_batch for tables too large for the shared-memory index: the
  * config records in d_cfg were produced by parva_configure_sweep. */
@@ -165,19 +182,49 @@ int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenari
                                    const int32_t* d_scen_off, const int32_t* d_svc_table,
                                    int32_t optimize, int32_t threshold,
                                    parva_config_record* d_cfg, parva_plan_record* d_plan,
-                                   double* d_ledger_val, uint8_t* d_ledger_order, void* stream);
+                                   void* stream);
 
 /* Host-buffer entry for one batch: copies inputs to the device, plans, and
- * copies records back, all on `stream`, then synchronizes.  Tables and index
- * are device-resident (built once).  Device scratch comes from `d_scratch`
- * (parva_plan_host_scratch bytes). */
+ * copies records back, then synchronizes `stream`.  The batch is cut into
+ * chunks whose H2D copy, plan launch and D2H copy are pipelined on internal
+ * streams (ordered after and before `stream`).  h_cfg receives config records
+ * in cfg_format.  Tables and index are device-resident (built once).  Device
+ * scratch comes from `d_scratch` (parva_plan_host_scratch bytes). */
 size_t parva_plan_host_scratch(int32_t n_scenarios, int32_t n_services);
 int parva_plan_host(const parva_tables* tables, const parva_index* index,
                     int32_t n_scenarios, const int32_t* h_scen_off,
                     const int32_t* h_svc_table, const double* h_svc_rate,
                     const double* h_svc_bound, int32_t optimize, int32_t threshold,
-                    parva_config_record* h_cfg, parva_plan_record* h_plan,
+                    void* h_cfg, int32_t cfg_format, parva_plan_record* h_plan,
                     void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* Packed host batches: one contiguous input block and one output block per
+ * chunk, so each chunk costs one H2D and one D2H copy.  A chunk of k
+ * scenarios and m services is laid out (offsets from parva_packed_layout):
+ *   input : int32 scen_off[k+1] (chunk-local, scen_off[0] = 0), f64 rate[m],
+ *           f64 bound[m], uint16 table[m]
+ *   output: parva_plan_record plan[k], config records[m] (cfg_format)
+ * Blocks are padded to 256 bytes. */
+typedef struct {
+  int64_t in_scen_off, in_rate, in_bound, in_table, in_bytes;
+  int64_t out_plan, out_cfg, out_bytes;
+} parva_chunk_layout;
+
+int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, parva_chunk_layout* out);
+
+/* Plan a packed batch: chunk c has h_chunk_scen[c] scenarios and
+ * h_chunk_svc[c] services, input block h_in[c], output block h_out[c] (host
+ * memory, pinned for full speed).  H2D(c+1) / plan(c) / D2H(c-1) overlap in a
+ * cached CUDA graph; returns after `stream` has synchronized.  Scratch:
+ * parva_plan_host_packed_scratch bytes of device memory. */
+size_t parva_plan_host_packed_scratch(int32_t n_chunks, const int32_t* h_chunk_scen,
+                                      const int32_t* h_chunk_svc, int32_t cfg_format);
+int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
+                           int32_t n_chunks, const int32_t* h_chunk_scen,
+                           const int32_t* h_chunk_svc, const void* const* h_in,
+                           void* const* h_out, int32_t optimize, int32_t threshold,
+                           int32_t cfg_format, void* d_scratch, size_t scratch_bytes,
+                           void* stream);
 
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional

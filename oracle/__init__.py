@@ -112,7 +112,8 @@ def configure_batch(pt, q_table, q_rate, q_bound, threads: int = 0) -> np.ndarra
 
 
 def plan_batch_records(pt, scen_off, svc_table, svc_rate, svc_bound, optimize=True, threshold=4,
-                       threads: int = 0, ledger: bool = True):
+                       threads: int = 0):
+    """Batched plan_services in the parva record format -> (config records, plan records)."""
     CONFIG, PLAN = _records()
     scen_off = np.ascontiguousarray(scen_off, dtype=np.int32)
     svc_table = np.ascontiguousarray(svc_table, dtype=np.int32)
@@ -122,14 +123,11 @@ def plan_batch_records(pt, scen_off, svc_table, svc_rate, svc_bound, optimize=Tr
     n_svc = svc_table.shape[0]
     cfg = np.zeros(n_svc, dtype=CONFIG)
     plan = np.zeros(n_scen, dtype=PLAN)
-    lv = np.zeros(n_svc, dtype=np.float64) if ledger else None
-    lo = np.zeros(n_svc, dtype=np.uint8) if ledger else None
     lib().oracle_plan_batch_records(_p(pt.tp), _p(pt.lat), _p(pt.batch), _p(pt.procs), _p(pt.seg_start),
                                     _p(pt.seg_count), C.c_int32(n_scen), _p(scen_off), _p(svc_table),
                                     _p(svc_rate), _p(svc_bound), C.c_int32(int(optimize)),
-                                    C.c_int32(int(threshold)), _p(cfg), _p(plan), _p(lv), _p(lo),
-                                    C.c_int32(threads))
-    return cfg, plan, lv, lo
+                                    C.c_int32(int(threshold)), _p(cfg), _p(plan), C.c_int32(threads))
+    return cfg, plan
 
 
 class _ResultBuf:

@@ -631,22 +631,37 @@ static void encode_record(const oresult* r, int n_svc, int cfg_err, int err_svc,
   if (r->n_gpus_unopt > PARVA_PLAN_MAX_GPUS || r->status == PARVA_CAPACITY) { rec->status = PARVA_CAPACITY; return; }
   if (r->status != PARVA_OK) { rec->status = (uint8_t)r->status; return; }
   int nd = r->fallback ? 0 : r->n_diag;
-  if (r->n_place > PARVA_PLAN_MAX_PLACE || nd > PARVA_PLAN_MAX_DIAG) { rec->status = PARVA_CAPACITY; return; }
+  int nl = 0;
+  if (!r->fallback)
+    for (int s = 0; s < n_svc; s++) if (r->ledger_order[s]) nl++;
+  int np = r->n_place;
+  int led_off = (2 * (np + nd) + 7) & ~7;
+  if (led_off + 10 * nl > PARVA_PLAN_PAYLOAD) { rec->status = PARVA_CAPACITY; return; }
   rec->n_gpus = (uint8_t)r->n_gpus;
   rec->n_gpus_unopt = (uint8_t)r->n_gpus_unopt;
-  rec->n_place = (uint8_t)r->n_place;
+  rec->n_place = (uint8_t)np;
   rec->n_diag = (uint8_t)nd;
+  rec->n_ledger = (uint8_t)nl;
   rec->flags = r->fallback ? PARVA_FLAG_FALLBACK : 0;
-  int tot = 0;
+  uint16_t u;
   for (int g = 0; g < r->n_gpus; g++)
     for (int k = r->pl_off[g]; k < r->pl_off[g + 1]; k++) {
       int cat = r->pl_name[k] * 5 + size_class(r->pl_trip[k].size);
-      rec->place[k] = (uint16_t)(r->gpu_id[g] << 11 | cat << 3 | r->pl_slot[k]);
-      tot += r->pl_trip[k].size;
+      u = (uint16_t)(r->gpu_id[g] << 11 | cat << 3 | r->pl_slot[k]);
+      memcpy(rec->payload + 2 * k, &u, 2);
     }
-  rec->total_gpcs = (uint8_t)tot;
-  for (int k = 0; k < nd; k++)
-    rec->diag[k] = (uint16_t)(r->diag[3 * k + 1] << 7 | r->diag[3 * k] << 5 | (r->diag[3 * k + 2] < 0 ? 0 : r->diag[3 * k + 2]));
+  for (int k = 0; k < nd; k++) {
+    u = (uint16_t)(r->diag[3 * k + 1] << 7 | r->diag[3 * k] << 5 | (r->diag[3 * k + 2] < 0 ? 0 : r->diag[3 * k + 2]));
+    memcpy(rec->payload + 2 * (np + k), &u, 2);
+  }
+  if (!r->fallback)
+    for (int s = 0; s < n_svc; s++) {
+      int o = r->ledger_order[s];
+      if (!o) continue;
+      memcpy(rec->payload + led_off + 8 * (o - 1), &r->ledger_val[s], 8);
+      u = (uint16_t)(s | o << 8);
+      memcpy(rec->payload + led_off + 8 * nl + 2 * (o - 1), &u, 2);
+    }
 }
 
 int oracle_plan_batch_records(const double* tp, const double* lat, const int32_t* batch,
@@ -655,8 +670,7 @@ int oracle_plan_batch_records(const double* tp, const double* lat, const int32_t
                               const int32_t* scen_off, const int32_t* svc_table,
                               const double* svc_rate, const double* svc_bound,
                               int32_t optimize, int32_t threshold,
-                              parva_config_record* cfg, parva_plan_record* plan,
-                              double* ledger_val, uint8_t* ledger_order, int32_t n_threads) {
+                              parva_config_record* cfg, parva_plan_record* plan, int32_t n_threads) {
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
 #pragma omp parallel
@@ -686,13 +700,6 @@ int oracle_plan_batch_records(const double* tp, const double* lat, const int32_t
       int cfg_err = 0, err_svc = 0;
       for (int s = 0; s < n; s++) if (cfg[a + s].status) { cfg_err = cfg[a + s].status; err_svc = s; break; }
       encode_record(&r, n, cfg_err, err_svc, &plan[k]);
-      if (ledger_val) {
-        int okrec = plan[k].status == PARVA_OK && !(plan[k].flags & PARVA_FLAG_FALLBACK);
-        for (int s = 0; s < n; s++) {
-          ledger_val[a + s] = okrec && r.ledger_order[s] ? r.ledger_val[s] : 0.0;
-          ledger_order[a + s] = (uint8_t)(okrec ? r.ledger_order[s] : 0);
-        }
-      }
     }
     free(r.gpu_id); free(r.pl_off); free(r.pl_name); free(r.pl_trip); free(r.pl_slot); free(r.diag);
     free(r.ledger_val); free(r.ledger_order);

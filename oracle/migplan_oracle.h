@@ -98,8 +98,7 @@ int oracle_plan_batch_records(const double* tp, const double* lat, const int32_t
                               const int32_t* scen_off, const int32_t* svc_table,
                               const double* svc_rate, const double* svc_bound,
                               int32_t optimize, int32_t threshold,
-                              parva_config_record* cfg, parva_plan_record* plan,
-                              double* ledger_val, uint8_t* ledger_order, int32_t n_threads);
+                              parva_config_record* cfg, parva_plan_record* plan, int32_t n_threads);
 
 /* configure_service for many (table, rate, bound) queries, OpenMP. */
 int oracle_configure_batch(const double* tp, const double* lat, const int32_t* batch,

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .records import CAPACITY, CONFIG_DTYPE, PLAN_DTYPE
+from .records import CAPACITY, CFG_COMPACT, CFG_FULL, COMPACT_DTYPE, CONFIG_DTYPE, PLAN_DTYPE
 from .tables import PackedTables
 
 
@@ -45,23 +45,22 @@ def configure_sweep(dt: N.DeviceTables, q_table, q_rate, q_bound, out=None, stre
 
 @dataclass
 class BatchResult:
-    cfg: object            # device uint8 [n_services, 32]
+    cfg: object            # device uint8 [n_services, 32] (full) or [n_services, 16] (compact)
     plan: object           # device uint8 [n_scenarios, 128]
-    ledger_val: object     # device f64 [n_services] or None
-    ledger_order: object   # device u8 [n_services] or None
     n_scenarios: int
     n_services: int
+    cfg_format: int = CFG_FULL
 
     def host(self):
-        cfg = N.records_to_numpy(self.cfg, self.n_services, CONFIG_DTYPE)
+        dt = COMPACT_DTYPE if self.cfg_format == CFG_COMPACT else CONFIG_DTYPE
+        cfg = N.records_to_numpy(self.cfg, self.n_services, dt)
         plan = N.records_to_numpy(self.plan, self.n_scenarios, PLAN_DTYPE)
-        lv = self.ledger_val[:self.n_services].cpu().numpy() if self.ledger_val is not None else None
-        lo = self.ledger_order[:self.n_services].cpu().numpy() if self.ledger_order is not None else None
-        return cfg, plan, lv, lo
+        return cfg, plan
 
 
 def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, optimize: bool = True,
-               threshold: int = 4, ledger: bool = True, stream=None, out: BatchResult | None = None) -> BatchResult:
+               threshold: int = 4, cfg_format: int = CFG_FULL, stream=None,
+               out: BatchResult | None = None) -> BatchResult:
     """Plan independent scenarios; scenario k owns services [scen_off[k], scen_off[k+1])."""
     torch = N.require_cuda()
     dev = lambda a, f: a if isinstance(a, torch.Tensor) else N.to_device(f(a))  # noqa: E731
@@ -71,25 +70,24 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     svc_bound = dev(svc_bound, _f64)
     n_scen = int(scen_off.shape[0]) - 1
     n_svc = int(svc_table.shape[0])
+    if dt.index_struct is None:
+        cfg_format = CFG_FULL
     if out is None:
-        out = BatchResult(N.empty_records(n_svc, CONFIG_DTYPE), N.empty_records(n_scen, PLAN_DTYPE),
-                          torch.empty(max(n_svc, 1), dtype=torch.float64, device="cuda") if ledger else None,
-                          torch.empty(max(n_svc, 1), dtype=torch.uint8, device="cuda") if ledger else None,
-                          n_scen, n_svc)
+        out = BatchResult(N.empty_records(n_svc, COMPACT_DTYPE if cfg_format == CFG_COMPACT else CONFIG_DTYPE),
+                          N.empty_records(n_scen, PLAN_DTYPE), n_scen, n_svc, cfg_format)
     s = N.stream_handle(stream)
     L = N.lib()
     if dt.index_struct is not None:
         rc = L.parva_plan_batch(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), N.ptr(scen_off),
                                 N.ptr(svc_table), N.ptr(svc_rate), N.ptr(svc_bound), C.c_int32(int(optimize)),
-                                C.c_int32(int(threshold)), N.ptr(out.cfg), N.ptr(out.plan),
-                                N.ptr(out.ledger_val), N.ptr(out.ledger_order), s)
+                                C.c_int32(int(threshold)), N.ptr(out.cfg), C.c_int32(out.cfg_format),
+                                N.ptr(out.plan), s)
         N.check(rc, "parva_plan_batch")
     else:
         configure_sweep(dt, svc_table, svc_rate, svc_bound, out=out.cfg, stream=stream)
         rc = L.parva_plan_batch_preconfigured(C.byref(dt.struct), C.c_int32(n_scen), N.ptr(scen_off),
                                               N.ptr(svc_table), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
-                                              N.ptr(out.cfg), N.ptr(out.plan), N.ptr(out.ledger_val),
-                                              N.ptr(out.ledger_order), s)
+                                              N.ptr(out.cfg), N.ptr(out.plan), s)
         N.check(rc, "parva_plan_batch_preconfigured")
     return out
 
@@ -236,3 +234,84 @@ def resolve_capacity(pt: PackedTables, scen_off, svc_table, cfg, plan, optimize=
         g = general_from_configs(pt, svc_table[a:b], recs, optimize, threshold)
         out[k] = (g, plan_general(g))
     return out
+
+
+# ------------------------------------------------------------ packed host
+class ChunkLayout(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("in_scen_off", "in_rate", "in_bound", "in_table", "in_bytes",
+                                         "out_plan", "out_cfg", "out_bytes")]
+
+
+class PackedHostBatch:
+    """A batch in the packed host format of parva_plan_host_packed.
+
+    The scenarios are cut into `n_chunks` contiguous ranges; each chunk owns
+    one pinned input block (offsets, rates, bounds, u16 table ids) and one
+    pinned output block (plan records, then config records), so a chunk
+    costs one H2D and one D2H copy.  `fill` packs inputs (host side, done
+    once per batch by whoever produces the queries); `run` is the timed
+    end-to-end call: copies in, plans, copies out, synchronizes."""
+
+    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, n_chunks: int = 2, cfg_format: int = CFG_COMPACT):
+        torch = N.require_cuda()
+        L = N.lib()
+        scen_off = np.asarray(scen_off, dtype=np.int64)
+        n = len(scen_off) - 1
+        n_chunks = max(1, min(n_chunks, max(n, 1)))
+        self.cfg_format = cfg_format
+        self.bounds = [(n * c // n_chunks, n * (c + 1) // n_chunks) for c in range(n_chunks)]
+        self.k = np.array([b - a for a, b in self.bounds], dtype=np.int32)
+        self.m = np.array([scen_off[b] - scen_off[a] for a, b in self.bounds], dtype=np.int32)
+        self.layouts, self.h_in, self.h_out = [], [], []
+        for c, (a, b) in enumerate(self.bounds):
+            lay = ChunkLayout()
+            N.check(L.parva_packed_layout(C.c_int32(int(self.k[c])), C.c_int32(int(self.m[c])),
+                                          C.c_int32(cfg_format), C.byref(lay)), "parva_packed_layout")
+            self.layouts.append(lay)
+            self.h_in.append(torch.zeros(lay.in_bytes, dtype=torch.uint8).pin_memory())
+            self.h_out.append(torch.zeros(lay.out_bytes, dtype=torch.uint8).pin_memory())
+        self.n_scen, self.n_svc = n, int(scen_off[-1])
+        self.fill(scen_off, svc_table, svc_rate, svc_bound)
+        self.in_ptrs = (C.c_void_p * n_chunks)(*[t.data_ptr() for t in self.h_in])
+        self.out_ptrs = (C.c_void_p * n_chunks)(*[t.data_ptr() for t in self.h_out])
+        self.k_c = (C.c_int32 * n_chunks)(*self.k.tolist())
+        self.m_c = (C.c_int32 * n_chunks)(*self.m.tolist())
+        self.scratch_bytes = int(L.parva_plan_host_packed_scratch(C.c_int32(n_chunks), self.k_c, self.m_c,
+                                                                 C.c_int32(cfg_format)))
+        self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda")
+
+    def fill(self, scen_off, svc_table, svc_rate, svc_bound):
+        scen_off = np.asarray(scen_off, dtype=np.int64)
+        for c, (a, b) in enumerate(self.bounds):
+            lay, buf = self.layouts[c], self.h_in[c].numpy()
+            sa, sb = int(scen_off[a]), int(scen_off[b])
+            k, m = b - a, sb - sa
+            buf[lay.in_scen_off:lay.in_scen_off + 4 * (k + 1)].view(np.int32)[:] = scen_off[a:b + 1] - sa
+            buf[lay.in_rate:lay.in_rate + 8 * m].view(np.float64)[:] = np.asarray(svc_rate)[sa:sb]
+            buf[lay.in_bound:lay.in_bound + 8 * m].view(np.float64)[:] = np.asarray(svc_bound)[sa:sb]
+            buf[lay.in_table:lay.in_table + 2 * m].view(np.uint16)[:] = np.asarray(svc_table)[sa:sb]
+
+    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
+        rc = N.lib().parva_plan_host_packed(
+            C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(len(self.bounds)), self.k_c, self.m_c,
+            self.in_ptrs, self.out_ptrs, C.c_int32(int(optimize)), C.c_int32(int(threshold)),
+            C.c_int32(self.cfg_format), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), N.stream_handle(stream))
+        N.check(rc, "parva_plan_host_packed")
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(sum(l.in_bytes for l in self.layouts))
+
+    @property
+    def d2h_bytes(self) -> int:
+        return int(sum(l.out_bytes for l in self.layouts))
+
+    def outputs(self):
+        """(config records, plan records) of the whole batch as numpy arrays."""
+        cdt = COMPACT_DTYPE if self.cfg_format == CFG_COMPACT else CONFIG_DTYPE
+        cfgs, plans = [], []
+        for c, lay in enumerate(self.layouts):
+            buf = self.h_out[c].numpy()
+            plans.append(buf[lay.out_plan:lay.out_plan + 128 * int(self.k[c])].view(PLAN_DTYPE))
+            cfgs.append(buf[lay.out_cfg:lay.out_cfg + cdt.itemsize * int(self.m[c])].view(cdt))
+        return np.concatenate(cfgs), np.concatenate(plans)

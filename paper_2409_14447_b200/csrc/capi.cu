@@ -1,6 +1,11 @@
 // capi.cu — the extern "C" boundary declared in include/parva_b200.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
 #include "parva_common.cuh"
 #include "parva_kernels.cuh"
 
@@ -37,9 +42,8 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries, const i
 
 static int plan_batch_impl(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                            const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
-                           const double* d_svc_bound, int32_t optimize, int32_t threshold,
-                           parva_config_record* d_cfg, parva_plan_record* d_plan, double* d_ledger_val,
-                           uint8_t* d_ledger_order, int cfg_given, cudaStream_t stream) {
+                           const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
+                           int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream) {
   parva::PlanArgs A;
   A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
@@ -52,6 +56,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.n_scen = n_scenarios;
   A.scen_off = d_scen_off;
   A.svc_table = d_svc_table;
+  A.svc_table16 = nullptr;
   A.svc_rate = d_svc_rate;
   A.svc_bound = d_svc_bound;
   A.optimize = optimize;
@@ -59,67 +64,316 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.cfg_given = cfg_given;
   A.smem_index = !cfg_given && tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
   A.cfg = d_cfg;
+  A.cfg_format = cfg_format;
   A.plan = d_plan;
-  A.ledger_val = d_ledger_val;
-  A.ledger_order = d_ledger_order;
   return parva::launch_plan_batch(A, stream);
 }
 
 int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                      const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
-                     const double* d_svc_bound, int32_t optimize, int32_t threshold,
-                     parva_config_record* d_cfg, parva_plan_record* d_plan, double* d_ledger_val,
-                     uint8_t* d_ledger_order, void* stream) {
-  if (!tables || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
-  const int cfg_given = index == nullptr;
-  if (cfg_given) return PARVA_BAD_INPUT;
+                     const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
+                     int32_t cfg_format, parva_plan_record* d_plan, void* stream) {
+  if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
+  if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, index, n_scenarios, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
-                         optimize, threshold, d_cfg, d_plan, d_ledger_val, d_ledger_order, 0,
-                         (cudaStream_t)stream);
+                         optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream);
 }
 
 // Same as parva_plan_batch but the config records in d_cfg were produced by
 // parva_configure_sweep (tables too large for the shared-memory index).
 int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios, const int32_t* d_scen_off,
                                    const int32_t* d_svc_table, int32_t optimize, int32_t threshold,
-                                   parva_config_record* d_cfg, parva_plan_record* d_plan,
-                                   double* d_ledger_val, uint8_t* d_ledger_order, void* stream) {
+                                   parva_config_record* d_cfg, parva_plan_record* d_plan, void* stream) {
   if (!tables || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, nullptr, n_scenarios, d_scen_off, d_svc_table, nullptr, nullptr, optimize,
-                         threshold, d_cfg, d_plan, d_ledger_val, d_ledger_order, 1, (cudaStream_t)stream);
+                         threshold, d_cfg, PARVA_CFG_FULL, d_plan, 1, (cudaStream_t)stream);
 }
 
+static size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
 size_t parva_plan_host_scratch(int32_t n_scenarios, int32_t n_services) {
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return up(size_t(n_scenarios + 1) * 4) + up(size_t(n_services) * 4) + 2 * up(size_t(n_services) * 8) +
-         up(size_t(n_services) * sizeof(parva_config_record)) + up(size_t(n_scenarios) * sizeof(parva_plan_record));
+  return up256(size_t(n_scenarios + 1) * 4) + up256(size_t(n_services) * 4) + 2 * up256(size_t(n_services) * 8) +
+         up256(size_t(n_services) * sizeof(parva_config_record)) + up256(size_t(n_scenarios) * sizeof(parva_plan_record));
+}
+
+// The host entry's chunked H2D -> plan -> D2H pipeline is an explicitly
+// built CUDA graph, cached per (device, shape, tables, scratch); a call with
+// new host pointers only updates the memcpy nodes (cudaGraphExecMemcpyNode-
+// SetParams1D).  One graph launch replaces ~40 stream API calls.
+struct HostGraph {
+  int dev = -1, n_scen = 0, n_svc = 0, cfg_format = 0, optimize = 0, threshold = 0, chunks = 0;
+  const void* pts = nullptr;
+  const void* idx = nullptr;
+  void* scratch = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> nodes;          // per chunk: 4 H2D, 2 D2H
+  std::vector<const void*> host;               // host pointers the nodes were built with
+  uint64_t last_use = 0;
+};
+static std::mutex g_graph_mu;
+static std::vector<HostGraph> g_graphs;
+static uint64_t g_graph_clock = 0;
+
+static void free_graph(HostGraph& G) {
+  if (G.exec) cudaGraphExecDestroy(G.exec);
+  if (G.graph) cudaGraphDestroy(G.graph);
+  G = HostGraph();
 }
 
 int parva_plan_host(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                     const int32_t* h_scen_off, const int32_t* h_svc_table, const double* h_svc_rate,
-                    const double* h_svc_bound, int32_t optimize, int32_t threshold, parva_config_record* h_cfg,
-                    parva_plan_record* h_plan, void* d_scratch, size_t scratch_bytes, void* stream) {
+                    const double* h_svc_bound, int32_t optimize, int32_t threshold, void* h_cfg,
+                    int32_t cfg_format, parva_plan_record* h_plan, void* d_scratch, size_t scratch_bytes,
+                    void* stream) {
   if (!tables || !index || n_scenarios < 0) return PARVA_BAD_INPUT;
+  if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
+  if (n_scenarios == 0) return PARVA_OK;
   const int32_t n_services = h_scen_off[n_scenarios];
   if (parva_plan_host_scratch(n_scenarios, n_services) > scratch_bytes) return PARVA_BAD_INPUT;
   cudaStream_t s = (cudaStream_t)stream;
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t cfg_sz = cfg_format == PARVA_CFG_COMPACT ? sizeof(parva_config_compact) : sizeof(parva_config_record);
   uint8_t* p = (uint8_t*)d_scratch;
-  int32_t* d_off = (int32_t*)p; p += up(size_t(n_scenarios + 1) * 4);
-  int32_t* d_tab = (int32_t*)p; p += up(size_t(n_services) * 4);
-  double* d_rate = (double*)p; p += up(size_t(n_services) * 8);
-  double* d_bound = (double*)p; p += up(size_t(n_services) * 8);
-  parva_config_record* d_cfg = (parva_config_record*)p; p += up(size_t(n_services) * sizeof(parva_config_record));
+  int32_t* d_off = (int32_t*)p; p += up256(size_t(n_scenarios + 1) * 4);
+  int32_t* d_tab = (int32_t*)p; p += up256(size_t(n_services) * 4);
+  double* d_rate = (double*)p; p += up256(size_t(n_services) * 8);
+  double* d_bound = (double*)p; p += up256(size_t(n_services) * 8);
+  uint8_t* d_cfg = p; p += up256(size_t(n_services) * sizeof(parva_config_record));
   parva_plan_record* d_plan = (parva_plan_record*)p;
-  cudaMemcpyAsync(d_off, h_scen_off, size_t(n_scenarios + 1) * 4, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(d_tab, h_svc_table, size_t(n_services) * 4, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(d_rate, h_svc_rate, size_t(n_services) * 8, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(d_bound, h_svc_bound, size_t(n_services) * 8, cudaMemcpyHostToDevice, s);
-  int rc = plan_batch_impl(tables, index, n_scenarios, d_off, d_tab, d_rate, d_bound, optimize, threshold, d_cfg,
-                           d_plan, nullptr, nullptr, 0, s);
-  if (rc != PARVA_OK) return rc;
-  cudaMemcpyAsync(h_cfg, d_cfg, size_t(n_services) * sizeof(parva_config_record), cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(h_plan, d_plan, size_t(n_scenarios) * sizeof(parva_plan_record), cudaMemcpyDeviceToHost, s);
+  int chunks = n_scenarios / 2500;
+  chunks = chunks < 1 ? 1 : (chunks > 8 ? 8 : chunks);
+  if (const char* e = getenv("PARVA_HOST_CHUNKS")) chunks = atoi(e) > 0 ? atoi(e) : chunks;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* host[6] = {h_scen_off, h_svc_table, h_svc_rate, h_svc_bound, h_cfg, h_plan};
+
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  HostGraph* G = nullptr;
+  for (auto& e : g_graphs)
+    if (e.dev == dev && e.n_scen == n_scenarios && e.n_svc == n_services && e.cfg_format == cfg_format &&
+        e.optimize == optimize && e.threshold == threshold && e.pts == tables->d_pts && e.idx == index->d_lat_sorted &&
+        e.scratch == d_scratch && e.chunks == chunks) { G = &e; break; }
+  auto chunk = [&](int i, int& a, int& b, int& sa, int& sb) {
+    a = int((int64_t)n_scenarios * i / chunks);
+    b = int((int64_t)n_scenarios * (i + 1) / chunks);
+    sa = h_scen_off[a];
+    sb = h_scen_off[b];
+  };
+  // memcpy node parameters of chunk i, copy j (0..3 H2D, 4..5 D2H)
+  auto copy_args = [&](int i, int j, void** dst, const void** src, size_t* bytes, cudaMemcpyKind* kind) {
+    int a, b, sa, sb;
+    chunk(i, a, b, sa, sb);
+    switch (j) {
+      case 0: *dst = d_off + a; *src = h_scen_off + a; *bytes = size_t(b - a + 1) * 4; break;
+      case 1: *dst = d_tab + sa; *src = h_svc_table + sa; *bytes = size_t(sb - sa) * 4; break;
+      case 2: *dst = d_rate + sa; *src = h_svc_rate + sa; *bytes = size_t(sb - sa) * 8; break;
+      case 3: *dst = d_bound + sa; *src = h_svc_bound + sa; *bytes = size_t(sb - sa) * 8; break;
+      case 4: *dst = (uint8_t*)h_cfg + size_t(sa) * cfg_sz; *src = d_cfg + size_t(sa) * cfg_sz;
+              *bytes = size_t(sb - sa) * cfg_sz; break;
+      default: *dst = h_plan + a; *src = d_plan + a; *bytes = size_t(b - a) * sizeof(parva_plan_record); break;
+    }
+    *kind = j < 4 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  };
+  if (!G) {
+    if (g_graphs.size() >= 8) {
+      auto victim = g_graphs.begin();
+      for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+        if (it->last_use < victim->last_use) victim = it;
+      free_graph(*victim);
+      g_graphs.erase(victim);
+    }
+    g_graphs.emplace_back();
+    G = &g_graphs.back();
+    G->dev = dev; G->n_scen = n_scenarios; G->n_svc = n_services; G->cfg_format = cfg_format;
+    G->optimize = optimize; G->threshold = threshold; G->pts = tables->d_pts; G->idx = index->d_lat_sorted;
+    G->scratch = d_scratch; G->chunks = chunks;
+    if (cudaGraphCreate(&G->graph, 0) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    G->nodes.assign(size_t(chunks) * 6, nullptr);
+    cudaGraphNode_t prev_in[4] = {}, prev_out[2] = {};
+    for (int i = 0; i < chunks; i++) {
+      int a, b, sa, sb;
+      chunk(i, a, b, sa, sb);
+      cudaGraphNode_t in[4];
+      for (int j = 0; j < 4; j++) {   // H2D in chunk order (chunk i after chunk i-1)
+        void* dst; const void* src; size_t bytes; cudaMemcpyKind kind;
+        copy_args(i, j, &dst, &src, &bytes, &kind);
+        if (cudaGraphAddMemcpyNode1D(&in[j], G->graph, i ? &prev_in[j] : nullptr, i ? 1 : 0, dst, src, bytes,
+                                     kind) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+        G->nodes[size_t(i) * 6 + j] = in[j];
+        prev_in[j] = in[j];
+      }
+      parva::PlanArgs A;
+      A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
+      A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
+      A.n_points = tables->n_points; A.n_scen = b - a; A.scen_off = d_off + a; A.svc_table = d_tab;
+      A.svc_table16 = nullptr;
+      A.svc_rate = d_rate; A.svc_bound = d_bound; A.optimize = optimize; A.threshold = threshold;
+      A.cfg_given = 0; A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit; A.cfg = d_cfg;
+      A.cfg_format = cfg_format; A.plan = d_plan + a;
+      cudaGraphNode_t kn;
+      if (parva::add_plan_batch_node(G->graph, A, in, 4, &kn) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+      for (int j = 4; j < 6; j++) {   // D2H after this chunk's plan and the previous chunk's D2H
+        void* dst; const void* src; size_t bytes; cudaMemcpyKind kind;
+        copy_args(i, j, &dst, &src, &bytes, &kind);
+        cudaGraphNode_t deps[2] = {kn, prev_out[j - 4]};
+        cudaGraphNode_t o;
+        if (cudaGraphAddMemcpyNode1D(&o, G->graph, deps, i ? 2 : 1, dst, src, bytes, kind) != cudaSuccess)
+          return PARVA_LAUNCH_ERROR;
+        G->nodes[size_t(i) * 6 + j] = o;
+        prev_out[j - 4] = o;
+      }
+    }
+    if (cudaGraphInstantiate(&G->exec, G->graph, 0) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    G->host.assign(host, host + 6);
+  } else if (!std::equal(G->host.begin(), G->host.end(), host)) {
+    for (int i = 0; i < chunks; i++)
+      for (int j = 0; j < 6; j++) {
+        void* dst; const void* src; size_t bytes; cudaMemcpyKind kind;
+        copy_args(i, j, &dst, &src, &bytes, &kind);
+        if (cudaGraphExecMemcpyNodeSetParams1D(G->exec, G->nodes[size_t(i) * 6 + j], dst, src, bytes, kind) !=
+            cudaSuccess) return PARVA_LAUNCH_ERROR;
+      }
+    G->host.assign(host, host + 6);
+  }
+  G->last_use = ++g_graph_clock;
+  if (cudaGraphLaunch(G->exec, s) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+  return cudaStreamSynchronize(s) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+// ------------------------------------------------------------ packed host
+static int64_t up256l(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, parva_chunk_layout* L) {
+  if (!L || k < 0 || m < 0) return PARVA_BAD_INPUT;
+  const int64_t cfg_sz = cfg_format == PARVA_CFG_COMPACT ? sizeof(parva_config_compact) : sizeof(parva_config_record);
+  L->in_scen_off = 0;
+  L->in_rate = ((int64_t(k) + 1) * 4 + 15) & ~int64_t(15);
+  L->in_bound = L->in_rate + int64_t(m) * 8;
+  L->in_table = L->in_bound + int64_t(m) * 8;
+  L->in_bytes = up256l(L->in_table + int64_t(m) * 2);
+  L->out_plan = 0;
+  L->out_cfg = int64_t(k) * sizeof(parva_plan_record);
+  L->out_bytes = up256l(L->out_cfg + int64_t(m) * cfg_sz);
+  return PARVA_OK;
+}
+
+size_t parva_plan_host_packed_scratch(int32_t n_chunks, const int32_t* k, const int32_t* m, int32_t cfg_format) {
+  size_t total = 0;
+  for (int c = 0; c < n_chunks; c++) {
+    parva_chunk_layout L;
+    parva_packed_layout(k[c], m[c], cfg_format, &L);
+    total += size_t(L.in_bytes) + size_t(L.out_bytes);
+  }
+  return total + 256;
+}
+
+struct PackedGraph {
+  int dev = -1, n_chunks = 0, cfg_format = 0, optimize = 0, threshold = 0;
+  std::vector<int32_t> k, m;
+  const void* pts = nullptr;
+  const void* idx = nullptr;
+  void* scratch = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> in_nodes, out_nodes;
+  std::vector<const void*> host_in;
+  std::vector<void*> host_out;
+  uint64_t last_use = 0;
+};
+static std::vector<PackedGraph> g_packed;
+
+int parva_plan_host_packed(const parva_tables* tables, const parva_index* index, int32_t n_chunks,
+                           const int32_t* h_k, const int32_t* h_m, const void* const* h_in, void* const* h_out,
+                           int32_t optimize, int32_t threshold, int32_t cfg_format, void* d_scratch,
+                           size_t scratch_bytes, void* stream) {
+  if (!tables || !index || n_chunks <= 0) return PARVA_BAD_INPUT;
+  if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
+  if (parva_plan_host_packed_scratch(n_chunks, h_k, h_m, cfg_format) > scratch_bytes) return PARVA_BAD_INPUT;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  PackedGraph* G = nullptr;
+  for (auto& e : g_packed)
+    if (e.dev == dev && e.n_chunks == n_chunks && e.cfg_format == cfg_format && e.optimize == optimize &&
+        e.threshold == threshold && e.pts == tables->d_pts && e.idx == index->d_lat_sorted &&
+        e.scratch == d_scratch && std::equal(e.k.begin(), e.k.end(), h_k) && std::equal(e.m.begin(), e.m.end(), h_m)) {
+      G = &e;
+      break;
+    }
+  // device blocks: [in_0 | out_0 | in_1 | out_1 | ...] in scratch
+  std::vector<parva_chunk_layout> L(n_chunks);
+  std::vector<uint8_t*> d_in(n_chunks), d_out(n_chunks);
+  {
+    uint8_t* p = (uint8_t*)(((uintptr_t)d_scratch + 255) & ~uintptr_t(255));
+    for (int c = 0; c < n_chunks; c++) {
+      parva_packed_layout(h_k[c], h_m[c], cfg_format, &L[c]);
+      d_in[c] = p; p += L[c].in_bytes;
+      d_out[c] = p; p += L[c].out_bytes;
+    }
+  }
+  if (!G) {
+    if (g_packed.size() >= 8) {
+      auto victim = g_packed.begin();
+      for (auto it = g_packed.begin(); it != g_packed.end(); ++it)
+        if (it->last_use < victim->last_use) victim = it;
+      if (victim->exec) cudaGraphExecDestroy(victim->exec);
+      if (victim->graph) cudaGraphDestroy(victim->graph);
+      g_packed.erase(victim);
+    }
+    g_packed.emplace_back();
+    G = &g_packed.back();
+    G->dev = dev; G->n_chunks = n_chunks; G->cfg_format = cfg_format; G->optimize = optimize;
+    G->threshold = threshold; G->k.assign(h_k, h_k + n_chunks); G->m.assign(h_m, h_m + n_chunks);
+    G->pts = tables->d_pts; G->idx = index->d_lat_sorted; G->scratch = d_scratch;
+    if (cudaGraphCreate(&G->graph, 0) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    G->in_nodes.resize(n_chunks);
+    G->out_nodes.resize(n_chunks);
+    for (int c = 0; c < n_chunks; c++) {
+      cudaGraphNode_t* dep_in = c ? &G->in_nodes[c - 1] : nullptr;
+      if (cudaGraphAddMemcpyNode1D(&G->in_nodes[c], G->graph, dep_in, c ? 1 : 0, d_in[c], h_in[c], L[c].in_bytes,
+                                   cudaMemcpyHostToDevice) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+      cudaGraphNode_t kn;
+      if (h_k[c] > 0) {
+        parva::PlanArgs A;
+        A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
+        A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
+        A.n_points = tables->n_points; A.n_scen = h_k[c];
+        A.scen_off = (const int32_t*)(d_in[c] + L[c].in_scen_off);
+        A.svc_table = nullptr; A.svc_table16 = (const uint16_t*)(d_in[c] + L[c].in_table);
+        A.svc_rate = (const double*)(d_in[c] + L[c].in_rate);
+        A.svc_bound = (const double*)(d_in[c] + L[c].in_bound);
+        A.optimize = optimize; A.threshold = threshold; A.cfg_given = 0;
+        A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
+        A.cfg = d_out[c] + L[c].out_cfg; A.cfg_format = cfg_format;
+        A.plan = (parva_plan_record*)(d_out[c] + L[c].out_plan);
+        if (parva::add_plan_batch_node(G->graph, A, &G->in_nodes[c], 1, &kn) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+      } else {
+        kn = G->in_nodes[c];
+      }
+      cudaGraphNode_t deps[2] = {kn, c ? G->out_nodes[c - 1] : nullptr};
+      if (cudaGraphAddMemcpyNode1D(&G->out_nodes[c], G->graph, deps, c ? 2 : 1, h_out[c], d_out[c],
+                                   L[c].out_bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    }
+    if (cudaGraphInstantiate(&G->exec, G->graph, 0) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    G->host_in.assign(h_in, h_in + n_chunks);
+    G->host_out.assign(h_out, h_out + n_chunks);
+  } else {
+    for (int c = 0; c < n_chunks; c++) {
+      if (G->host_in[c] != h_in[c]) {
+        if (cudaGraphExecMemcpyNodeSetParams1D(G->exec, G->in_nodes[c], d_in[c], h_in[c], L[c].in_bytes,
+                                               cudaMemcpyHostToDevice) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+        G->host_in[c] = h_in[c];
+      }
+      if (G->host_out[c] != h_out[c]) {
+        if (cudaGraphExecMemcpyNodeSetParams1D(G->exec, G->out_nodes[c], h_out[c], d_out[c], L[c].out_bytes,
+                                               cudaMemcpyDeviceToHost) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+        G->host_out[c] = h_out[c];
+      }
+    }
+  }
+  G->last_use = ++g_graph_clock;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaGraphLaunch(G->exec, s) != cudaSuccess) return PARVA_LAUNCH_ERROR;
   return cudaStreamSynchronize(s) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 

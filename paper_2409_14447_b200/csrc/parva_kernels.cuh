@@ -20,15 +20,15 @@ struct PlanArgs {
   int n_scen;
   const int32_t* scen_off;
   const int32_t* svc_table;
+  const uint16_t* svc_table16;   // packed host format (used when non-null)
   const double* svc_rate;
   const double* svc_bound;
   int optimize, threshold;
   int cfg_given;                 // config records precomputed by K1
   int smem_index;                // index resident in shared memory
-  parva_config_record* cfg;
+  void* cfg;                     // parva_config_record[] or parva_config_compact[]
+  int cfg_format;                // PARVA_CFG_FULL / PARVA_CFG_COMPACT
   parva_plan_record* plan;
-  double* ledger_val;
-  uint8_t* ledger_order;
 };
 
 int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
@@ -36,6 +36,8 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
 int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cudaStream_t stream);
 size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index);
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream);
+int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t* deps, size_t ndeps,
+                        cudaGraphNode_t* node);
 size_t general_workspace(const parva_general_problem* p, int64_t cap);
 int launch_plan_general(const parva_general_problem* p, parva_general_result* r, void* ws, size_t ws_bytes,
                         cudaStream_t stream);

@@ -34,6 +34,7 @@ struct WarpScratch {
   uint8_t q2[QCAP];
   uint8_t q1[QCAP];
   uint8_t undo[2 * QCAP];
+  uint16_t diag[32];                      // optimize diagnostics, in order
   parva_plan_record rec;
 };
 
@@ -179,13 +180,13 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
       double tpc[5] = {0, 0, 0, 0, 0};
       if (i < n) {
         if (A.cfg_given) {
-          r = A.cfg[a0 + i];
-          const int t = A.svc_table[a0 + i];
+          r = reinterpret_cast<const parva_config_record*>(A.cfg)[a0 + i];
+          const int t = A.svc_table16 ? (int)A.svc_table16[a0 + i] : A.svc_table[a0 + i];
           for (int c = 0; c < 5; c++)
             tpc[c] = r.best[c] >= 0 ? A.pts[2 * (A.seg_start[t * 5 + c] + r.best[c])] : 0.0;
         } else {
           r = {};
-          const int t = A.svc_table[a0 + i];
+          const int t = A.svc_table16 ? (int)A.svc_table16[a0 + i] : A.svc_table[a0 + i];
           if (t < 0 || t >= A.n_tables) {
             for (int c = 0; c < 5; c++) r.best[c] = -1;
             r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
@@ -193,9 +194,19 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
             configure_indexed(lat_s, best_s, tp_s, tp_stride, seg_s, seg_n, t, A.svc_bound[a0 + i],
                               A.svc_rate[a0 + i], r, tpc);
           }
-          uint4* dst = reinterpret_cast<uint4*>(A.cfg + a0 + i);
-          dst[0] = reinterpret_cast<const uint4*>(&r)[0];
-          dst[1] = reinterpret_cast<const uint4*>(&r)[1];
+          if (A.cfg_format == PARVA_CFG_COMPACT) {
+            parva_config_compact k;
+#pragma unroll
+            for (int c = 0; c < 5; c++) k.best[c] = r.best[c];
+            k.opt_sc = r.opt_sc; k.last_sc = r.last_sc; k.status = r.status;
+            k.flags = r.count > 65535 ? 1 : 0;
+            k.count = (uint16_t)(r.count > 65535 ? 65535 : r.count);
+            reinterpret_cast<uint4*>(A.cfg)[a0 + i] = *reinterpret_cast<const uint4*>(&k);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(A.cfg) + a0 + i);
+            dst[0] = reinterpret_cast<const uint4*>(&r)[0];
+            dst[1] = reinterpret_cast<const uint4*>(&r)[1];
+          }
         }
         if (base == 0) {
           my_opt = r.opt_sc;
@@ -334,8 +345,8 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
               }
             }
             freed = sv_freed; order = sv_order; next = sv_next;
-            if (nd < PARVA_PLAN_MAX_DIAG && lane == 0)
-              W.rec.diag[nd] = (uint16_t)(index << 7 | fail << 5 | (fail == PARVA_DIAG_SMALL_UNAVAILABLE ? fsvc : 0));
+            if (lane == 0)
+              W.diag[nd] = (uint16_t)(index << 7 | fail << 5 | (fail == PARVA_DIAG_SMALL_UNAVAILABLE ? fsvc : 0));
             nd++;
           } else if (lane == index) {
             len = 0; mask = 0; ngpc = 0;
@@ -352,7 +363,6 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
           *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
           len = bak_len; ngpc = bak_ngpc; mask = bak_mask;
           freed = 0.0; order = 0; nd = 0;
-          if (lane < PARVA_PLAN_MAX_DIAG / 2) reinterpret_cast<uint32_t*>(W.rec.diag)[lane] = 0u;
         }
       }
       __syncwarp();
@@ -368,18 +378,25 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
       }
       const int n_place = __shfl_sync(0xffffffffu, incl, 31);
       const int n_final = __popc(__ballot_sync(0xffffffffu, good));
-      const int tot = warp_sum_i(good ? ngpc : 0);
-      if (n_place > PARVA_PLAN_MAX_PLACE || nd > PARVA_PLAN_MAX_DIAG) {
+      const int n_led = __popc(__ballot_sync(0xffffffffu, lane < n && order > 0));
+      const int led_off = (2 * (n_place + nd) + 7) & ~7;
+      if (led_off + 10 * n_led > PARVA_PLAN_PAYLOAD) {
         status = PARVA_CAPACITY;
       } else {
-        for (int j = 0; j < mine; j++) W.rec.place[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+        uint16_t* pay16 = reinterpret_cast<uint16_t*>(W.rec.payload);
+        for (int j = 0; j < mine; j++) pay16[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+        if (lane < nd) pay16[n_place + lane] = W.diag[lane];
+        if (lane < n && order > 0) {
+          reinterpret_cast<double*>(W.rec.payload + led_off)[order - 1] = freed;
+          reinterpret_cast<uint16_t*>(W.rec.payload + led_off + 8 * n_led)[order - 1] = (uint16_t)(lane | order << 8);
+        }
         if (lane == 0) {
           W.rec.n_gpus = (uint8_t)n_final;
           W.rec.n_gpus_unopt = (uint8_t)n_before;
           W.rec.n_place = (uint8_t)n_place;
           W.rec.n_diag = (uint8_t)nd;
+          W.rec.n_ledger = (uint8_t)n_led;
           W.rec.flags = fallback ? PARVA_FLAG_FALLBACK : 0;
-          W.rec.total_gpcs = (uint8_t)tot;
         }
       }
       // reset this lane's GPU list slots for the next scenario
@@ -397,17 +414,6 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
     __syncwarp();
     if (lane < 8)
       reinterpret_cast<uint4*>(A.plan + k)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
-    if (A.ledger_val) {
-      const bool keep = status == PARVA_OK && !fallback;
-      for (int base = 0; base < n; base += 32) {
-        const int i = base + lane;
-        if (i < n) {
-          const bool on = keep && base == 0 && order != 0;
-          A.ledger_val[a0 + i] = on ? freed : 0.0;
-          A.ledger_order[a0 + i] = (uint8_t)(on ? order : 0);
-        }
-      }
-    }
     __syncwarp();
   }
 }
@@ -418,11 +424,10 @@ size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index) {
   return (b + 15) & ~size_t(15);
 }
 
-int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
-  if (A.n_scen <= 0) return PARVA_OK;
+static bool plan_launch_config(const PlanArgs& A, int* grid, size_t* smem_out) {
   const size_t smem = plan_smem_bytes(A.n_tables, A.n_points, A.smem_index);
-  static size_t configured = 0;
-  static int n_sm = 0;
+  static size_t configured = 0, occ_smem = 0;
+  static int n_sm = 0, per_sm = 0;
   if (smem > configured) {
     cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
@@ -432,13 +437,41 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_batch_kernel, PB_THREADS, smem);
-  if (per_sm < 1) return PARVA_LAUNCH_ERROR;
-  int grid = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
-  if (grid > n_sm * per_sm) grid = n_sm * per_sm;
+  if (smem != occ_smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_batch_kernel, PB_THREADS, smem);
+    occ_smem = smem;
+  }
+  if (per_sm < 1) return false;
+  int g = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  if (g > n_sm * per_sm) g = n_sm * per_sm;
+  *grid = g;
+  *smem_out = smem;
+  return true;
+}
+
+int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
+  if (A.n_scen <= 0) return PARVA_OK;
+  int grid;
+  size_t smem;
+  if (!plan_launch_config(A, &grid, &smem)) return PARVA_LAUNCH_ERROR;
   plan_batch_kernel<<<grid, PB_THREADS, smem, stream>>>(A);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t* deps, size_t ndeps,
+                        cudaGraphNode_t* node) {
+  int grid;
+  size_t smem;
+  if (!plan_launch_config(A, &grid, &smem)) return PARVA_LAUNCH_ERROR;
+  PlanArgs copy = A;
+  void* args[] = {&copy};
+  cudaKernelNodeParams p = {};
+  p.func = (void*)plan_batch_kernel;
+  p.gridDim = dim3(grid);
+  p.blockDim = dim3(PB_THREADS);
+  p.sharedMemBytes = (unsigned)smem;
+  p.kernelParams = args;
+  return cudaGraphAddKernelNode(node, g, deps, ndeps, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
 }  // namespace parva

@@ -24,7 +24,7 @@ from .errors import MigplanError
 from .evaluation import DEFAULT_SMS_PER_GPC, allocated_fraction, external_fragmentation
 from .mig import INSTANCE_SIZES, GpuState, Placement
 from .profiles import DEFAULT_MEMORY_MAP, ProfileTable, filter_feasible
-from .records import BAD_INPUT, CAPACITY, DIAG_REGRESSED, FLAG_FALLBACK, OK, format_diag, unpack_diag, unpack_place
+from .records import BAD_INPUT, CAPACITY, DIAG_REGRESSED, FLAG_FALLBACK, OK, format_diag, plan_payload, unpack_diag, unpack_place
 from .scenario import Scenario, load_tables_for, scenario_services
 
 
@@ -76,27 +76,26 @@ def prepare_tables(tables: Mapping[str, ProfileTable], options: PlanOptions) -> 
     return prepared
 
 
-def _decode_record(services: list[Service], rec, lv, lo) -> DeploymentMap:
+def _decode_record(services: list[Service], rec) -> DeploymentMap:
+    """DeploymentMap from a 128-byte plan record (include/parva_b200.h)."""
+    places, diag_codes, ledger = plan_payload(rec)
     gpus: list[GpuState] = []
     by_class = [{INSTANCE_SIZES.index(t.instance_size): t for t in s.best_triplets} for s in services]
-    for i in range(int(rec["n_place"])):
-        g, cat, slot = unpack_place(int(rec["place"][i]))
+    for v in places:
+        g, cat, slot = unpack_place(v)
         s, c = divmod(cat, 5)
         if not gpus or gpus[-1].id != g:
             gpus.append(GpuState(id=g))
         t = by_class[s][c]
         gpus[-1].placements.append(Placement(services[s].id, t.instance_size, t.batch_size,
                                              t.process_count, t.throughput, slot))
-    freed = {}
-    if lo is not None:
-        for rank, s in sorted((int(lo[s]), s) for s in range(len(services)) if lo[s]):
-            freed[services[s].id] = float(lv[s])
+    freed = {services[s].id: v for s, v in ledger}
     if int(rec["flags"]) & FLAG_FALLBACK:
         diags = [format_diag(DIAG_REGRESSED, -1, None)]
     else:
         diags = []
-        for i in range(int(rec["n_diag"])):
-            g, reason, s = unpack_diag(int(rec["diag"][i]))
+        for v in diag_codes:
+            g, reason, s = unpack_diag(v)
             diags.append(format_diag(reason, g, services[s].id))
     return DeploymentMap(gpus=gpus, freed_rate=freed, diagnostics=diags)
 
@@ -137,7 +136,7 @@ def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, Pr
     t0 = time.perf_counter()
     res = plan_batch(dt, off, np.asarray(tab, dtype=np.int32), np.asarray(rate), np.asarray(bound),
                      optimize=options.optimize, threshold=options.threshold)
-    cfg, plan, lv, lo = res.host()
+    cfg, plan = res.host()
     general = resolve_capacity(pt, off, np.asarray(tab, dtype=np.int32), cfg, plan, options.optimize,
                                options.threshold)
     torch.cuda.synchronize()
@@ -165,7 +164,7 @@ def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, Pr
             else:
                 if int(rec["status"]) != OK:
                     raise MigplanError(f"device planner status {int(rec['status'])}")
-                dmap = _decode_record(configured, rec, lv[a:a + len(ss)], lo[a:a + len(ss)])
+                dmap = _decode_record(configured, rec)
                 unopt = int(rec["n_gpus_unopt"])
             out.append(PlanResult(scenario_name=(names[k] if names else ""), services=configured,
                                   deployment=dmap, planning_ms=elapsed_ms, unoptimized_gpu_count=unopt))

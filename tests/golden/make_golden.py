@@ -18,6 +18,7 @@ Files:
                         fuzz incl. near-ties (App. A F1-F5, F10)
   alloc_cases.json      relocate_segments and optimize_allocation on crafted and
                         random maps (App. B #3, #4)
+  reconfigure_cases.json  reconfigure_service + diff_maps on planned maps (§8f row 1)
   c2_digests.json       digest of every C2 scenario plan (seed 0, 10^4) + 200 full plans
   c3_sample.json        200 C3 dense workloads: table digest + configure result
   c5_summary.json       C5 large-cluster allocation summary (with --c5)
@@ -329,6 +330,44 @@ def gen_alloc_cases(tables, seed=4242):
     write("alloc_cases.json", {"relocate": relocate, "optimize": optimize})
 
 
+# ------------------------------------------------------- reconfigure (§8f-1)
+def gen_reconfigure(tables, n=120, seed=31337):
+    rng = random.Random(seed)
+    cases = []
+    for i in range(n):
+        k = rng.randint(2, 9)
+        models = rng.sample(list(RF.MODEL_IDS), k)
+        inputs = [[m, m, math.exp(rng.uniform(math.log(20), math.log(6000))),
+                   math.exp(rng.uniform(math.log(100), math.log(3000)))] for m in models]
+        services = [R.make_service(a, m, r, s) for a, m, r, s in inputs]
+        try:
+            res = R.plan_services(services, tables)
+        except R.MigplanError:
+            continue
+        target = rng.randrange(k)
+        mode = rng.random()
+        old = res.services[target]
+        if mode < 0.15:
+            new_rate, new_slo = old.request_rate, old.slo_latency          # unchanged demand
+        elif mode < 0.25:
+            new_rate, new_slo = old.request_rate, 1.0                      # infeasible SLO
+        else:
+            new_rate = old.request_rate * rng.choice([0.3, 0.7, 1.5, 2.0, 3.0])
+            new_slo = old.slo_latency * rng.choice([0.6, 1.0, 1.4])
+        updated = R.make_service(old.id, old.model_id, new_rate, new_slo)
+        thr = rng.choice([4, 4, 3, 5])
+        table = R.filter_feasible(tables[old.model_id])
+        try:
+            dmap, changes, new_services = R.reconfigure_service(res.deployment, res.services, updated, table, thr)
+            out = {"map": canon.dmap(dmap), "changes": [c.to_json_obj() for c in changes],
+                   "services": [canon.service(s) for s in new_services]}
+        except R.MigplanError as exc:
+            out = canon.error(exc)
+        cases.append({"inputs": inputs, "target": target, "new_rate": new_rate, "new_slo": new_slo,
+                      "threshold": thr, "base": canon.plan(res), "result": out})
+    write("reconfigure_cases.json", cases)
+
+
 # ------------------------------------------------------------------ C2
 def gen_c2(tables, n=10_000, full=200):
     fx = W.load_fixtures()
@@ -429,7 +468,8 @@ def main():
     tables = ref_tables()
     steps = {"tables": lambda: gen_fixture_tables(tables), "fixture": lambda: gen_fixture_plans(tables),
              "fuzz": lambda: gen_fuzz_plans(tables), "unit": gen_unit_cases,
-             "alloc": lambda: gen_alloc_cases(tables), "c2": lambda: gen_c2(tables), "c3": gen_c3}
+             "alloc": lambda: gen_alloc_cases(tables), "reconf": lambda: gen_reconfigure(tables),
+             "c2": lambda: gen_c2(tables), "c3": gen_c3}
     if a.c5:
         steps["c5"] = lambda: gen_c5(tables)
     for name, fn in steps.items():

@@ -46,7 +46,7 @@ def _oracle_fn(fx):
     pt = pack_tables(fx.tables)
 
     def fn(off, tab, rate, bound):
-        cfg, plan, _, _ = oracle.plan_batch_records(pt, off, tab, rate, bound, threads=1, ledger=False)
+        cfg, plan = oracle.plan_batch_records(pt, off, tab, rate, bound, threads=1)
         return (torch.from_numpy(cfg.view(np.uint8).reshape(-1, 32).copy()),
                 torch.from_numpy(plan.view(np.uint8).reshape(-1, 128).copy()))
     return fn

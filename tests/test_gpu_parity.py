@@ -24,7 +24,7 @@ from paper_2409_14447_b200 import _native as N  # noqa: E402
 from paper_2409_14447_b200 import batch as B  # noqa: E402
 from paper_2409_14447_b200 import workloads as W  # noqa: E402
 from paper_2409_14447_b200.configurator import Service, Triplet  # noqa: E402
-from paper_2409_14447_b200.records import CONFIG_DTYPE  # noqa: E402
+from paper_2409_14447_b200.records import CFG_COMPACT, CONFIG_DTYPE, compact_config  # noqa: E402
 from paper_2409_14447_b200.tables import pack_dense, pack_tables  # noqa: E402
 
 
@@ -91,7 +91,7 @@ def test_unit_configure_sweep():
     # the K2 indexed path must agree with the streaming sweep on the same tables
     res = B.plan_batch(dt, np.arange(len(cases) + 1), np.arange(len(cases)), [c["rate"] for c in cases],
                        [c["bound"] for c in cases])
-    cfg2, _, _, _ = res.host()
+    cfg2, _ = res.host()
     assert cfg2.tobytes() == recs.tobytes()
 
 
@@ -198,11 +198,14 @@ def test_c2_records_vs_oracle_and_goldens(fx):
     tab = np.tile(np.arange(M, dtype=np.int32), n)
     rate, bound = sb.rate.ravel(), sb.bound.ravel()
     res = B.plan_batch(dt, off, tab, rate, bound)
-    cfg, plan, lv, lo = res.host()
-    ocfg, oplan, olv, olo = oracle.plan_batch_records(pt, off, tab, rate, bound)
+    cfg, plan = res.host()
+    ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
     assert cfg.tobytes() == ocfg.tobytes()
     assert plan.tobytes() == oplan.tobytes()
-    assert lv.tobytes() == olv.tobytes() and lo.tobytes() == olo.tobytes()
+    # compact config records for host transfers
+    resc = B.plan_batch(dt, off, tab, rate, bound, cfg_format=CFG_COMPACT)
+    ccfg, cplan = resc.host()
+    assert ccfg.tobytes() == compact_config(ocfg).tobytes() and cplan.tobytes() == oplan.tobytes()
     # and through the object decode, against the reference's own digests
     sets = [[P.make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]
             for k in range(n)]
@@ -220,12 +223,11 @@ def test_c4_sample_vs_oracle(fx):
     tab = np.tile(np.arange(M, dtype=np.int32), n)
     for optimize, thr in ((True, 4), (False, 4), (True, 6)):
         res = B.plan_batch(dt, off, tab, sb.rate.ravel(), sb.bound.ravel(), optimize=optimize, threshold=thr)
-        cfg, plan, lv, lo = res.host()
-        ocfg, oplan, olv, olo = oracle.plan_batch_records(pt, off, tab, sb.rate.ravel(), sb.bound.ravel(),
-                                                         optimize=optimize, threshold=thr)
+        cfg, plan = res.host()
+        ocfg, oplan = oracle.plan_batch_records(pt, off, tab, sb.rate.ravel(), sb.bound.ravel(),
+                                                optimize=optimize, threshold=thr)
         assert cfg.tobytes() == ocfg.tobytes()
         assert plan.tobytes() == oplan.tobytes()
-        assert lv.tobytes() == olv.tobytes() and lo.tobytes() == olo.tobytes()
 
 
 def test_c3_sweep_vs_goldens_and_oracle():
@@ -262,3 +264,65 @@ def test_c5_large_cluster(fx):
     assert res.gpu_count == g["gpus"] and res.deployment.total_gpcs == g["total_gpcs"]
     assert canon.digest(canon.dmap(res.deployment)) == g["optimized_sha256"]
     assert hashlib.sha256(res.deployment.to_json().encode()).hexdigest()[:16] == g["json_sha256"]
+
+
+def test_host_entry_pipelined_vs_oracle(fx):
+    """parva_plan_host (chunked H2D / plan / D2H pipeline) == oracle records."""
+    import ctypes as C
+    sb = W.scenario_batch(fx, 9_001, seed=5)
+    n, M = sb.rate.shape
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
+    dt = N.device_tables_for(fx.tables)
+    L = N.lib()
+    for fmt in (0, 1, 1, 0):   # repeated calls exercise the cached pipeline graph
+        h_cfg = np.zeros(n * M * (32 if fmt == 0 else 16), dtype=np.uint8)
+        h_plan = np.zeros(n * 128, dtype=np.uint8)
+        nb = int(L.parva_plan_host_scratch(C.c_int32(n), C.c_int32(n * M)))
+        scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        vp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        rc = L.parva_plan_host(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n), vp(off), vp(tab),
+                               vp(rate), vp(bound), C.c_int32(1), C.c_int32(4), vp(h_cfg), C.c_int32(fmt),
+                               vp(h_plan), N.ptr(scratch), C.c_size_t(nb), N.stream_handle())
+        assert rc == 0
+        ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, rate, bound)
+        exp_cfg = ocfg if fmt == 0 else compact_config(ocfg)
+        assert h_cfg.tobytes() == exp_cfg.tobytes()
+        assert h_plan.tobytes() == oplan.tobytes()
+
+
+def test_host_entry_packed_vs_oracle(fx):
+    """parva_plan_host_packed (one H2D + one D2H per chunk, cached graph) == oracle."""
+    sb = W.scenario_batch(fx, 7_003, seed=9)
+    n, M = sb.rate.shape
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
+    dt = N.device_tables_for(fx.tables)
+    ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, rate, bound)
+    for chunks, fmt in ((1, 1), (3, 1), (3, 0), (4, 1)):
+        pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=chunks, cfg_format=fmt)
+        for _ in range(2):
+            pb.run(dt)
+            cfg, plan = pb.outputs()
+            assert plan.tobytes() == oplan.tobytes()
+            assert cfg.tobytes() == (ocfg if fmt == 0 else compact_config(ocfg)).tobytes()
+
+
+def test_reconfigure_service(fx):
+    """§III-F re-planning (allocator.py:494-537) + diff_maps (:484-491) vs reference goldens."""
+    for i, c in enumerate(golden("reconfigure_cases.json")):
+        base = c["base"]
+        svcs = [_svc_from_canon(s) for s in base["services"]]
+        dm = _map_from_canon({"gpus": base["gpus"], "freed": base["freed"], "diags": base["diags"]})
+        old = svcs[c["target"]]
+        upd = P.make_service(old.id, old.model_id, c["new_rate"], c["new_slo"])
+        table = P.filter_feasible(fx.tables[old.model_id])
+        try:
+            dmap, changes, new_services = P.reconfigure_service(dm, svcs, upd, table, c["threshold"])
+            got = {"map": canon.dmap(dmap), "changes": [ch.to_json_obj() for ch in changes],
+                   "services": [canon.service(s) for s in new_services]}
+        except P.MigplanError as exc:
+            got = canon.error(exc)
+        assert got == c["result"], i

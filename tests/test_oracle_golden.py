@@ -202,3 +202,33 @@ def test_c5_large_cluster(fx):
     assert res["unopt"] == g["unopt_gpus"] and len(res["gpus"]) == g["gpus"]
     names = [f"d121#{i}" for i in range(n)]
     assert canon.digest(map_canon(res, names)) == g["optimized_sha256"]
+
+
+def test_record_format_decodes_to_reference_plans(fx):
+    """Oracle -> 128-byte plan records -> this package's decoder -> canonical
+    plans == the reference's digests.  Pins the record format and the decoder
+    (used on the GPU path) without a GPU."""
+    from paper_2409_14447_b200.configurator import make_service, raise_for_record, service_from_record
+    from paper_2409_14447_b200.errors import MigplanError
+    from paper_2409_14447_b200.pipeline import PlanResult, _decode_record
+    g = golden("c2_digests.json")
+    n = 3000
+    sb = W.scenario_batch(fx, n, seed=g["seed"])
+    pt = pack_tables(fx.tables)
+    M = len(sb.models)
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    cfg, plan = oracle.plan_batch_records(pt, off, tab, sb.rate.ravel(), sb.bound.ravel())
+    for k in range(n):
+        svcs = [make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]
+        try:
+            conf = []
+            for j, s in enumerate(svcs):
+                raise_for_record(s, cfg[k * M + j])
+                conf.append(service_from_record(s, pt, j, cfg[k * M + j]))
+            assert plan[k]["status"] == 0
+            res = PlanResult("", conf, _decode_record(conf, plan[k]), 0.0, int(plan[k]["n_gpus_unopt"]))
+            got = canon.plan(res)
+        except MigplanError as exc:
+            got = canon.error(exc)
+        assert canon.digest(got) == g["digests"][k], k
