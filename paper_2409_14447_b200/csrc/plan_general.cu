@@ -37,6 +37,9 @@ struct GenWs {
   int32_t* undo;    // [qcap]
   double* after;    // [n_services]
   uint8_t* seen;    // [n_services]
+  int64_t* svc_pos; // [n_services + 1] relocation queue offsets of one size class
+  int64_t* gpu_pos; // [cap + 1] cumulative capacity of one size class
+  int64_t* hdr;     // [8]: G, max_id, status, next (ledger rank counter)
   int64_t words, qcap, cap;
 };
 
@@ -55,6 +58,8 @@ __host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_se
   t.acc = (uint64_t*)take(5 * words * 8);
   t.q = (int32_t*)take(qcap * 4); t.q1 = (int32_t*)take(qcap * 4); t.undo = (int32_t*)take(qcap * 4);
   t.after = (double*)take((size_t)(n_services + 1) * 8); t.seen = take(n_services + 1);
+  t.svc_pos = (int64_t*)take((size_t)(n_services + 2) * 8); t.gpu_pos = (int64_t*)take((size_t)(cap + 2) * 8);
+  t.hdr = (int64_t*)take(8 * 8);
   t.words = words; t.qcap = qcap; t.cap = cap;
   if (w) *w = t;
   return off;
@@ -145,58 +150,219 @@ struct Gen {
   }
 };
 
-__device__ inline double unalloc_g(int64_t total, int64_t n) {
-  if (n == 0) return 0.0;
-  return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
+// ------------------------------------------------------------------ helpers
+// successive greedy placements of size class c on a GPU with mask m
+__device__ __forceinline__ int fill_cap(uint32_t m, int c) {
+  int k = 0, st;
+  while ((st = find_start(m, c)) >= 0) { m |= footprint(c, st); k++; }
+  return k;
+}
+__device__ __forceinline__ int fill_start(uint32_t m, int c, int j) {
+  for (int k = 0;; k++) {
+    const int st = find_start(m, c);
+    if (k == j) return st;
+    m |= footprint(c, st);
+  }
+}
+__device__ __forceinline__ uint32_t fill_mask(uint32_t m, int c, int used) {
+  for (int k = 0; k < used; k++) m |= footprint(c, find_start(m, c));
+  return m;
 }
 
-__global__ void plan_general_kernel(parva_general_problem P, parva_general_result R, uint8_t* ws_base,
-                                    int64_t cap, int64_t qcap) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  Gen S{P, {}, 0, -1, {0, 0, 0, 0, 0}};
-  gen_layout(cap, qcap, P.n_services, ws_base, &S.w);
-  GenWs& w = S.w;
-  int status = PARVA_OK;
+// exclusive block scan (1024 threads) of f(i), i < n, into out[0..n]; returns the total
+template <class F>
+__device__ int64_t block_scan(int64_t n, F f, int64_t* out, int64_t* sh /*[33]*/) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + tid;
+    const int64_t v = i < n ? f(i) : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) sh[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0, wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += u;
+      }
+      sh[lane] = wi - w;        // exclusive warp offsets
+      if (lane == 31) sh[32] = wi;
+    }
+    __syncthreads();
+    if (i < n) out[i] = carry + sh[warp] + incl - v;
+    carry += sh[32];
+    __syncthreads();
+  }
+  if (tid == 0) out[n] = carry;
+  __syncthreads();
+  return carry;
+}
 
-  // ---- initial map
-  for (int64_t k = 0; k < 5 * w.words; k++) w.acc[k] = 0;
-  S.G = P.n_gpus;
-  for (int64_t g = 0; g < P.n_gpus; g++) {
+__device__ __forceinline__ int64_t upper_bound64(const int64_t* a, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;   // first index with a[idx] > x
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int class_of_size(int size) {
+  return size == 7 ? 4 : size - 1;
+}
+
+// Initial map, ledger, and relocate_segments (allocator.py:292-316) in
+// parallel.  Within one size class, first-fit fills GPUs strictly in list
+// order -- a placement changes only the GPU it lands on, so every earlier
+// GPU keeps rejecting the class -- and each GPU receives its greedy capacity
+// for the class before the next one gets anything; GPUs appended when none
+// accepts fill the same way.  So a class phase is: scan the per-service
+// queue lengths, scan the per-GPU capacities, scatter queue entry i to the
+// GPU whose capacity range holds i.
+__global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem P, parva_general_result R,
+                                                            uint8_t* ws_base, int64_t cap, int64_t qcap) {
+  GenWs w;
+  gen_layout(cap, qcap, P.n_services, ws_base, &w);
+  __shared__ int64_t sh[33];
+  __shared__ unsigned long long s_max;
+  __shared__ int s_next;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_max = 0; s_next = 0; }
+  __syncthreads();
+  for (int64_t g = tid; g < P.n_gpus; g += blockDim.x) {
     w.id[g] = P.d_gpu_id[g];
-    if (P.d_gpu_id[g] > S.max_id) S.max_id = P.d_gpu_id[g];
+    atomicMax(&s_max, (unsigned long long)(P.d_gpu_id[g] + (1ll << 62)));
     uint32_t m = 0;
     int ng = 0, n = 0;
     for (int k = P.d_pl_off[g]; k < P.d_pl_off[g + 1]; k++, n++) {
-      const int cat = P.d_pl_cat[k], c = S.class_of(cat);
+      const int cat = P.d_pl_cat[k], c = class_of_size(P.d_cat_size[cat]);
       m |= footprint(c, P.d_pl_slot[k]);
       ng += size_of_class(c);
       w.lcat[g * 7 + n] = cat;
       w.lslot[g * 7 + n] = P.d_pl_slot[k];
     }
     w.mask[g] = (uint8_t)m; w.len[g] = (uint8_t)n; w.ngpc[g] = (uint8_t)ng;
-    S.set_acc(g);
   }
-  for (int c = 0; c < 5; c++) S.hint[c] = 0;
-  int32_t next = 0;
-  for (int k = 0; k < P.n_names; k++) {
+  for (int k = tid; k < P.n_names; k += blockDim.x) {
     R.d_ledger_val[k] = P.d_ledger_val[k];
     R.d_ledger_order[k] = P.d_ledger_order[k];
-    if (P.d_ledger_order[k] > next) next = P.d_ledger_order[k];
+    atomicMax(&s_next, P.d_ledger_order[k]);
   }
+  __syncthreads();
+  int64_t G = P.n_gpus;
+  int64_t max_id = P.n_gpus ? (int64_t)s_max - (1ll << 62) : -1;   // _next_id (allocator.py:280-281)
+  int status = PARVA_OK;
 
-  // ---- relocate_segments (allocator.py:292-316): sizes 7,4,3,2,1; FIFO by service
   if (P.relocate) {
     for (int c = 4; c >= 0 && status == PARVA_OK; c--) {
-      for (int s = 0; s < P.n_services && status == PARVA_OK; s++) {
+      const int size = size_of_class(c);
+      const int64_t L = block_scan(P.n_services, [&](int64_t s) -> int64_t {
         const int oc = P.d_svc_opt[s], lc = P.d_svc_last[s];
-        const long long reps = (oc >= 0 && S.class_of(oc) == c ? P.d_svc_count[s] : 0);
-        for (long long r = 0; r < reps; r++)
-          if (S.place(oc, -1, true) == -2) { status = PARVA_CAPACITY; break; }
-        if (status == PARVA_OK && lc >= 0 && S.class_of(lc) == c)
-          if (S.place(lc, -1, true) == -2) status = PARVA_CAPACITY;
+        return (oc >= 0 && class_of_size(P.d_cat_size[oc]) == c ? P.d_svc_count[s] : 0) +
+               (lc >= 0 && class_of_size(P.d_cat_size[lc]) == c ? 1 : 0);
+      }, w.svc_pos, sh);
+      if (L == 0) continue;
+      const int64_t S = block_scan(G, [&](int64_t g) -> int64_t { return fill_cap(w.mask[g], c); }, w.gpu_pos, sh);
+      const int cap_e = fill_cap(0u, c);
+      const int64_t rem = L > S ? L - S : 0;
+      const int64_t n_new = (rem + cap_e - 1) / cap_e;
+      if (G + n_new > w.cap) { status = PARVA_CAPACITY; break; }
+      // scatter: thread t owns a contiguous run of queue entries
+      const int64_t per = (L + blockDim.x - 1) / blockDim.x;
+      const int64_t i0 = tid * per, i1 = min(L, i0 + per);
+      if (i0 < i1) {
+        int64_t s = upper_bound64(w.svc_pos, P.n_services + 1, i0) - 1;
+        int64_t g = i0 < S ? upper_bound64(w.gpu_pos, G + 1, i0) - 1 : -1;
+        for (int64_t i = i0; i < i1; i++) {
+          while (w.svc_pos[s + 1] <= i) s++;
+          const int oc = P.d_svc_opt[s];
+          const int64_t r = i - w.svc_pos[s];
+          const bool is_opt = oc >= 0 && class_of_size(P.d_cat_size[oc]) == c && r < P.d_svc_count[s];
+          const int cat = is_opt ? oc : P.d_svc_last[s];
+          if (i < S) {
+            while (w.gpu_pos[g + 1] <= i) g++;
+            const int j = (int)(i - w.gpu_pos[g]);
+            w.lcat[g * 7 + w.len[g] + j] = cat;
+            w.lslot[g * 7 + w.len[g] + j] = (uint8_t)fill_start(w.mask[g], c, j);
+          } else {
+            const int64_t k = i - S, gn = G + k / cap_e;
+            const int j = (int)(k % cap_e);
+            w.lcat[gn * 7 + j] = cat;
+            w.lslot[gn * 7 + j] = (uint8_t)fill_start(0u, c, j);
+          }
+        }
       }
+      __syncthreads();
+      for (int64_t g = tid; g < G; g += blockDim.x) {
+        const int64_t got = L - w.gpu_pos[g];
+        const int capg = (int)(w.gpu_pos[g + 1] - w.gpu_pos[g]);
+        const int used = got <= 0 ? 0 : (got < capg ? (int)got : capg);
+        if (used) {
+          w.mask[g] = (uint8_t)fill_mask(w.mask[g], c, used);
+          w.len[g] += (uint8_t)used;
+          w.ngpc[g] += (uint8_t)(used * size);
+        }
+      }
+      for (int64_t k = tid; k < n_new; k += blockDim.x) {
+        const int64_t g = G + k;
+        const int used = (int)min((int64_t)cap_e, rem - k * cap_e);
+        w.id[g] = max_id + 1 + k;
+        w.mask[g] = (uint8_t)fill_mask(0u, c, used);
+        w.len[g] = (uint8_t)used;
+        w.ngpc[g] = (uint8_t)(used * size);
+      }
+      G += n_new;
+      max_id += n_new;
+      __syncthreads();
     }
   }
+  if (tid == 0) {
+    w.hdr[0] = G;
+    w.hdr[1] = max_id;
+    w.hdr[2] = status;
+    w.hdr[3] = s_next;
+  }
+}
+
+__device__ inline double unalloc_g(int64_t total, int64_t n) {
+  if (n == 0) return 0.0;
+  return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
+}
+
+__global__ void __launch_bounds__(1024) plan_general_kernel(parva_general_problem P, parva_general_result R,
+                                                             uint8_t* ws_base, int64_t cap, int64_t qcap) {
+  GenWs wsh;
+  gen_layout(cap, qcap, P.n_services, ws_base, &wsh);
+  const int64_t G0 = wsh.hdr[0];
+  // accepts-bitmaps and the optimize-input backup, in parallel
+  for (int64_t k = threadIdx.x; k < (G0 + 63) / 64; k += blockDim.x) {
+    uint64_t b[5] = {0, 0, 0, 0, 0};
+    for (int j = 0; j < 64 && k * 64 + j < G0; j++) {
+      const uint32_t m = wsh.mask[k * 64 + j];
+#pragma unroll
+      for (int c = 0; c < 5; c++) if (find_start(m, c) >= 0) b[c] |= 1ull << j;
+    }
+#pragma unroll
+    for (int c = 0; c < 5; c++) wsh.acc[c * wsh.words + k] = b[c];
+  }
+  if (P.optimize && wsh.hdr[2] == PARVA_OK)
+    for (int64_t g = threadIdx.x; g < G0; g += blockDim.x) {
+      wsh.b_id[g] = wsh.id[g]; wsh.b_mask[g] = wsh.mask[g]; wsh.b_len[g] = wsh.len[g]; wsh.b_ngpc[g] = wsh.ngpc[g];
+      for (int k = 0; k < wsh.len[g]; k++) { wsh.b_lcat[g * 7 + k] = wsh.lcat[g * 7 + k]; wsh.b_lslot[g * 7 + k] = wsh.lslot[g * 7 + k]; }
+    }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  Gen S{P, wsh, G0, wsh.hdr[1], {0, 0, 0, 0, 0}};
+  GenWs& w = S.w;
+  int status = (int)w.hdr[2];
+  int32_t next = (int32_t)w.hdr[3];
   const int64_t n_before = S.G;
   int64_t total_before = 0;
   for (int64_t g = 0; g < S.G; g++) total_before += w.ngpc[g];
@@ -205,10 +371,6 @@ __global__ void plan_general_kernel(parva_general_problem P, parva_general_resul
   int64_t nd = 0;
 
   if (status == PARVA_OK && P.optimize) {
-    for (int64_t g = 0; g < S.G; g++) {
-      w.b_id[g] = w.id[g]; w.b_mask[g] = w.mask[g]; w.b_len[g] = w.len[g]; w.b_ngpc[g] = w.ngpc[g];
-      for (int k = 0; k < w.len[g]; k++) { w.b_lcat[g * 7 + k] = w.lcat[g * 7 + k]; w.b_lslot[g * 7 + k] = w.lslot[g * 7 + k]; }
-    }
     // ---- optimize_allocation (allocator.py:362-443)
     for (int64_t index = S.G - 1; index >= 0; index--) {
       const int nl = w.len[index];
@@ -348,7 +510,8 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
                         cudaStream_t stream) {
   const int64_t cap = r->gpu_cap;
   if (general_workspace(p, cap) > ws_bytes) return PARVA_BAD_INPUT;
-  plan_general_kernel<<<1, 32, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
+  gen_prepare_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
+  plan_general_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
