@@ -165,12 +165,14 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries,
                           void* stream);
 
 /* Plan n_scenarios independent scenarios.  Scenario k owns services
- * [d_scen_off[k], d_scen_off[k+1]); service i queries table d_svc_table[i].
+ * [d_scen_off[k], d_scen_off[k+1]); service i queries table d_svc_table[i];
+ * n_services = d_scen_off[n_scenarios] - d_scen_off[0].  Two launches: every
+ * service is configured by one thread, then one warp plans each scenario.
  * Writes one config record per service (parva_config_record, or
  * parva_config_compact when cfg_format == PARVA_CFG_COMPACT) and one plan
  * record per scenario.  index must have been built from tables. */
 int parva_plan_batch(const parva_tables* tables, const parva_index* index,
-                     int32_t n_scenarios, const int32_t* d_scen_off,
+                     int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,
                      const int32_t* d_svc_table, const double* d_svc_rate,
                      const double* d_svc_bound, int32_t optimize, int32_t threshold,
                      void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
@@ -179,7 +181,7 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index,
 /* parva_plan_batch for tables too large for the shared-memory index: the
  * config records in d_cfg were produced by parva_configure_sweep. */
 int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios,
-                                   const int32_t* d_scen_off, const int32_t* d_svc_table,
+                                   int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table,
                                    int32_t optimize, int32_t threshold,
                                    parva_config_record* d_cfg, parva_plan_record* d_plan,
                                    void* stream);

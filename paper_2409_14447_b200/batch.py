@@ -78,14 +78,15 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     s = N.stream_handle(stream)
     L = N.lib()
     if dt.index_struct is not None:
-        rc = L.parva_plan_batch(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), N.ptr(scen_off),
+        rc = L.parva_plan_batch(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), C.c_int32(n_svc),
+                                N.ptr(scen_off),
                                 N.ptr(svc_table), N.ptr(svc_rate), N.ptr(svc_bound), C.c_int32(int(optimize)),
                                 C.c_int32(int(threshold)), N.ptr(out.cfg), C.c_int32(out.cfg_format),
                                 N.ptr(out.plan), s)
         N.check(rc, "parva_plan_batch")
     else:
         configure_sweep(dt, svc_table, svc_rate, svc_bound, out=out.cfg, stream=stream)
-        rc = L.parva_plan_batch_preconfigured(C.byref(dt.struct), C.c_int32(n_scen), N.ptr(scen_off),
+        rc = L.parva_plan_batch_preconfigured(C.byref(dt.struct), C.c_int32(n_scen), C.c_int32(n_svc), N.ptr(scen_off),
                                               N.ptr(svc_table), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
                                               N.ptr(out.cfg), N.ptr(out.plan), s)
         N.check(rc, "parva_plan_batch_preconfigured")

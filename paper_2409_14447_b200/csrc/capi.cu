@@ -41,7 +41,7 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries, const i
 }
 
 static int plan_batch_impl(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
-                           const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
+                           int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
                            const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
                            int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream) {
   parva::PlanArgs A;
@@ -54,6 +54,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.n_tables = tables->n_tables;
   A.n_points = tables->n_points;
   A.n_scen = n_scenarios;
+  A.n_svc = n_services;
   A.scen_off = d_scen_off;
   A.svc_table = d_svc_table;
   A.svc_table16 = nullptr;
@@ -70,22 +71,23 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
 }
 
 int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
-                     const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
+                     int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
                      const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
                      int32_t cfg_format, parva_plan_record* d_plan, void* stream) {
   if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
   if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
-  return plan_batch_impl(tables, index, n_scenarios, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
+  return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
                          optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream);
 }
 
 // Same as parva_plan_batch but the config records in d_cfg were produced by
 // parva_configure_sweep (tables too large for the shared-memory index).
-int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios, const int32_t* d_scen_off,
+int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios, int32_t n_services,
+                                   const int32_t* d_scen_off,
                                    const int32_t* d_svc_table, int32_t optimize, int32_t threshold,
                                    parva_config_record* d_cfg, parva_plan_record* d_plan, void* stream) {
   if (!tables || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
-  return plan_batch_impl(tables, nullptr, n_scenarios, d_scen_off, d_svc_table, nullptr, nullptr, optimize,
+  return plan_batch_impl(tables, nullptr, n_scenarios, n_services, d_scen_off, d_svc_table, nullptr, nullptr, optimize,
                          threshold, d_cfg, PARVA_CFG_FULL, d_plan, 1, (cudaStream_t)stream);
 }
 
@@ -205,7 +207,7 @@ int parva_plan_host(const parva_tables* tables, const parva_index* index, int32_
       parva::PlanArgs A;
       A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
       A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
-      A.n_points = tables->n_points; A.n_scen = b - a; A.scen_off = d_off + a; A.svc_table = d_tab;
+      A.n_points = tables->n_points; A.n_scen = b - a; A.n_svc = sb - sa; A.scen_off = d_off + a; A.svc_table = d_tab;
       A.svc_table16 = nullptr;
       A.svc_rate = d_rate; A.svc_bound = d_bound; A.optimize = optimize; A.threshold = threshold;
       A.cfg_given = 0; A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit; A.cfg = d_cfg;
@@ -337,7 +339,7 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
         parva::PlanArgs A;
         A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
         A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
-        A.n_points = tables->n_points; A.n_scen = h_k[c];
+        A.n_points = tables->n_points; A.n_scen = h_k[c]; A.n_svc = h_m[c];
         A.scen_off = (const int32_t*)(d_in[c] + L[c].in_scen_off);
         A.svc_table = nullptr; A.svc_table16 = (const uint16_t*)(d_in[c] + L[c].in_table);
         A.svc_rate = (const double*)(d_in[c] + L[c].in_rate);

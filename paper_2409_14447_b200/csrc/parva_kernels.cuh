@@ -18,6 +18,7 @@ struct PlanArgs {
   int n_tables;
   int64_t n_points;
   int n_scen;
+  int n_svc;                     // services [scen_off[0], scen_off[0] + n_svc)
   const int32_t* scen_off;
   const int32_t* svc_table;
   const uint16_t* svc_table16;   // packed host format (used when non-null)
@@ -34,7 +35,6 @@ struct PlanArgs {
 int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
                            const double* q_bound, parva_config_record* out, cudaStream_t stream);
 int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cudaStream_t stream);
-size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index);
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream);
 int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t* deps, size_t ndeps,
                         cudaGraphNode_t* node);

@@ -122,44 +122,99 @@ __device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, 
   }
 }
 
-__global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
-  uint8_t* idx_base = smem_raw + sizeof(WarpScratch) * PB_WARPS;
+// Index view: segment tables always in shared memory; latency-sorted
+// index + tp either bulk-copied into shared memory or read from global.
+struct IndexView {
+  const int* seg_s;
+  const int* seg_n;
+  const double* lat;
+  const uint16_t* best;
+  const double* tp;
+  int tp_stride;
+};
+
+__device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base, bool need_lat_best,
+                                                uint64_t* bar) {
   const int T5 = A.n_tables * 5;
-  int* seg_s = reinterpret_cast<int*>(idx_base);
+  int* seg_s = reinterpret_cast<int*>(base);
   int* seg_n = seg_s + T5;
-  const double* lat_s = A.idx_lat;
-  const uint16_t* best_s = A.idx_best;
-  const double* tp_s = A.pts;   // stride 2 in global, 1 in smem
-  int tp_stride = 2;
   for (int i = threadIdx.x; i < T5; i += blockDim.x) {
     seg_s[i] = (int)A.seg_start[i];
     seg_n[i] = A.seg_count[i];
   }
+  IndexView V{seg_s, seg_n, A.idx_lat, A.idx_best, A.pts, 2};
   if (A.smem_index) {
-    // three 1-D bulk copies (TMA) into shared memory, one mbarrier
-    const size_t off_lat = (size_t(T5) * 8 + 15) & ~size_t(15);
+    const size_t off = (size_t(T5) * 8 + 15) & ~size_t(15);
     const uint32_t b_dbl = uint32_t((A.n_points * 8 + 15) & ~int64_t(15));
     const uint32_t b_u16 = uint32_t((A.n_points * 2 + 15) & ~int64_t(15));
-    double* lat_w = reinterpret_cast<double*>(idx_base + off_lat);
-    double* tp_w = reinterpret_cast<double*>(idx_base + off_lat + b_dbl);
-    uint16_t* best_w = reinterpret_cast<uint16_t*>(idx_base + off_lat + 2 * size_t(b_dbl));
-    __shared__ uint64_t idx_bar;
+    double* tp_w = reinterpret_cast<double*>(base + off);
+    double* lat_w = reinterpret_cast<double*>(base + off + b_dbl);
+    uint16_t* best_w = reinterpret_cast<uint16_t*>(base + off + 2 * size_t(b_dbl));
     if (threadIdx.x == 0) {
-      mbar_init(&idx_bar, 1);
+      mbar_init(bar, 1);
       fence_mbar_init();
-      mbar_arrive_expect_tx(&idx_bar, 2 * b_dbl + b_u16);
+      mbar_arrive_expect_tx(bar, b_dbl + (need_lat_best ? b_dbl + b_u16 : 0u));
       const uint64_t pol = policy_evict_last();
-      bulk_g2s(lat_w, A.idx_lat, b_dbl, &idx_bar, pol);
-      bulk_g2s(tp_w, A.idx_tp, b_dbl, &idx_bar, pol);
-      bulk_g2s(best_w, A.idx_best, b_u16, &idx_bar, pol);
+      bulk_g2s(tp_w, A.idx_tp, b_dbl, bar, pol);
+      if (need_lat_best) {
+        bulk_g2s(lat_w, A.idx_lat, b_dbl, bar, pol);
+        bulk_g2s(best_w, A.idx_best, b_u16, bar, pol);
+      }
     }
     __syncthreads();
-    mbar_wait(&idx_bar, 0);
-    lat_s = lat_w; tp_s = tp_w; best_s = best_w; tp_stride = 1;
+    mbar_wait(bar, 0);
+    V.tp = tp_w;
+    V.tp_stride = 1;
+    if (need_lat_best) { V.lat = lat_w; V.best = best_w; }
   }
   __syncthreads();
+  return V;
+}
+
+__device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
+  if (A.cfg_format == PARVA_CFG_COMPACT) {
+    parva_config_compact k;
+#pragma unroll
+    for (int c = 0; c < 5; c++) k.best[c] = r.best[c];
+    k.opt_sc = r.opt_sc; k.last_sc = r.last_sc; k.status = r.status;
+    k.flags = r.count > 65535 ? 1 : 0;
+    k.count = (uint16_t)(r.count > 65535 ? 65535 : r.count);
+    reinterpret_cast<uint4*>(A.cfg)[i] = *reinterpret_cast<const uint4*>(&k);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(A.cfg) + i);
+    dst[0] = reinterpret_cast<const uint4*>(&r)[0];
+    dst[1] = reinterpret_cast<const uint4*>(&r)[1];
+  }
+}
+
+// K2a: configure_service for every service of the batch, one thread each
+// (configurator.py:189-191 via the prefix-argmax index).
+constexpr int CF_THREADS = 256;
+__global__ void __launch_bounds__(CF_THREADS) configure_services_kernel(PlanArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __shared__ uint64_t bar;
+  const IndexView V = load_index(A, smem_raw, true, &bar);
+  const int64_t lo = A.scen_off[0], hi = lo + A.n_svc;
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+    parva_config_record r = {};
+    double tpc[5];
+    const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
+    if (t < 0 || t >= A.n_tables) {
+      for (int c = 0; c < 5; c++) r.best[c] = -1;
+      r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
+    } else {
+      configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, A.svc_bound[i], A.svc_rate[i], r, tpc);
+    }
+    store_config(A, i, r);
+  }
+}
+
+// K2b: relocate + optimize, one warp per scenario, from the config records.
+__global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  __shared__ uint64_t bar;
+  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS, false, &bar);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpScratch& W = scratch[warp];
@@ -170,55 +225,37 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
     const int n = A.scen_off[k + 1] - a0;
     reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
 
-    // ------------------------------------------------------------ configure
+    // ------------------------------------------------ configured services
     int err_status = 0, err_svc = 0;
     int my_opt = -1, my_last = -1;
     long long my_count = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      parva_config_record r;
-      double tpc[5] = {0, 0, 0, 0, 0};
-      if (i < n) {
-        if (A.cfg_given) {
-          r = reinterpret_cast<const parva_config_record*>(A.cfg)[a0 + i];
-          const int t = A.svc_table16 ? (int)A.svc_table16[a0 + i] : A.svc_table[a0 + i];
-          for (int c = 0; c < 5; c++)
-            tpc[c] = r.best[c] >= 0 ? A.pts[2 * (A.seg_start[t * 5 + c] + r.best[c])] : 0.0;
+    if (n <= PARVA_PLAN_MAX_SERVICES) {
+      int st = PARVA_OK;
+      if (lane < n) {
+        const int i = a0 + lane;
+        int16_t best[5];
+        if (A.cfg_format == PARVA_CFG_COMPACT) {
+          const parva_config_compact r = reinterpret_cast<const parva_config_compact*>(A.cfg)[i];
+#pragma unroll
+          for (int c = 0; c < 5; c++) best[c] = r.best[c];
+          my_opt = r.opt_sc; my_last = r.last_sc; my_count = r.count; st = r.status;
         } else {
-          r = {};
-          const int t = A.svc_table16 ? (int)A.svc_table16[a0 + i] : A.svc_table[a0 + i];
-          if (t < 0 || t >= A.n_tables) {
-            for (int c = 0; c < 5; c++) r.best[c] = -1;
-            r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
-          } else {
-            configure_indexed(lat_s, best_s, tp_s, tp_stride, seg_s, seg_n, t, A.svc_bound[a0 + i],
-                              A.svc_rate[a0 + i], r, tpc);
-          }
-          if (A.cfg_format == PARVA_CFG_COMPACT) {
-            parva_config_compact k;
+          const parva_config_record r = reinterpret_cast<const parva_config_record*>(A.cfg)[i];
 #pragma unroll
-            for (int c = 0; c < 5; c++) k.best[c] = r.best[c];
-            k.opt_sc = r.opt_sc; k.last_sc = r.last_sc; k.status = r.status;
-            k.flags = r.count > 65535 ? 1 : 0;
-            k.count = (uint16_t)(r.count > 65535 ? 65535 : r.count);
-            reinterpret_cast<uint4*>(A.cfg)[a0 + i] = *reinterpret_cast<const uint4*>(&k);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(A.cfg) + a0 + i);
-            dst[0] = reinterpret_cast<const uint4*>(&r)[0];
-            dst[1] = reinterpret_cast<const uint4*>(&r)[1];
-          }
+          for (int c = 0; c < 5; c++) best[c] = r.best[c];
+          my_opt = r.opt_sc; my_last = r.last_sc; my_count = r.count; st = r.status;
         }
-        if (base == 0) {
-          my_opt = r.opt_sc;
-          my_last = r.last_sc;
-          my_count = r.count;
+        const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
 #pragma unroll
-          for (int c = 0; c < 5; c++) W.cat_tp[lane * 5 + c] = tpc[c];
-        }
+        for (int c = 0; c < 5; c++)
+          W.cat_tp[lane * 5 + c] =
+              (st != PARVA_BAD_INPUT && best[c] >= 0) ? V.tp[(V.seg_s[t * 5 + c] + best[c]) * V.tp_stride] : 0.0;
       }
-      const unsigned bad = __ballot_sync(0xffffffffu, i < n && r.status != PARVA_OK);
-      const int st = __shfl_sync(0xffffffffu, (int)r.status, bad ? __ffs(bad) - 1 : 0);
-      if (err_status == 0 && bad) { err_status = st; err_svc = base + __ffs(bad) - 1; }
+      const unsigned bad = __ballot_sync(0xffffffffu, lane < n && st != PARVA_OK);
+      if (bad) {
+        err_svc = __ffs(bad) - 1;
+        err_status = __shfl_sync(0xffffffffu, st, err_svc);
+      }
     }
     __syncwarp();
 
@@ -418,60 +455,95 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   }
 }
 
-size_t plan_smem_bytes(int n_tables, int64_t n_points, bool smem_index) {
-  size_t b = sizeof(WarpScratch) * PB_WARPS + ((size_t(n_tables) * 5 * 8 + 15) & ~size_t(15));
-  if (smem_index) b += 2 * size_t((n_points * 8 + 15) & ~int64_t(15)) + size_t((n_points * 2 + 15) & ~int64_t(15));
+
+size_t index_smem_bytes(int n_tables, int64_t n_points, bool smem_index, bool lat_best) {
+  size_t b = (size_t(n_tables) * 5 * 8 + 15) & ~size_t(15);
+  if (smem_index) {
+    b += size_t((n_points * 8 + 15) & ~int64_t(15));
+    if (lat_best) b += size_t((n_points * 8 + 15) & ~int64_t(15)) + size_t((n_points * 2 + 15) & ~int64_t(15));
+  }
   return (b + 15) & ~size_t(15);
 }
 
-static bool plan_launch_config(const PlanArgs& A, int* grid, size_t* smem_out) {
-  const size_t smem = plan_smem_bytes(A.n_tables, A.n_points, A.smem_index);
-  static size_t configured = 0, occ_smem = 0;
-  static int n_sm = 0, per_sm = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
+struct LaunchCfg {
+  int grid_a, grid_b;
+  size_t smem_a, smem_b;
+};
+
+static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
+  const size_t smem_b = sizeof(WarpScratch) * PB_WARPS + index_smem_bytes(A.n_tables, A.n_points, A.smem_index, false);
+  const size_t smem_a = index_smem_bytes(A.n_tables, A.n_points, A.smem_index, true);
+  static size_t conf_a = 0, conf_b = 0, occ_a = 0, occ_b = 0;
+  static int n_sm = 0, per_a = 0, per_b = 0;
+  if (smem_b > conf_b) {
+    cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+    conf_b = smem_b;
+  }
+  if (smem_a > conf_a) {
+    cudaFuncSetAttribute(configure_services_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+    conf_a = smem_a;
   }
   if (!n_sm) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (smem != occ_smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_batch_kernel, PB_THREADS, smem);
-    occ_smem = smem;
+  if (smem_b != occ_b) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, plan_batch_kernel, PB_THREADS, smem_b);
+    occ_b = smem_b;
   }
-  if (per_sm < 1) return false;
-  int g = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
-  if (g > n_sm * per_sm) g = n_sm * per_sm;
-  *grid = g;
-  *smem_out = smem;
+  if (smem_a != occ_a) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_a, configure_services_kernel, CF_THREADS, smem_a);
+    occ_a = smem_a;
+  }
+  if (per_b < 1 || per_a < 1) return false;
+  int gb = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  if (gb > n_sm * per_b) gb = n_sm * per_b;
+  int ga = (int)((A.n_svc + CF_THREADS - 1) / CF_THREADS);
+  if (ga > n_sm * per_a) ga = n_sm * per_a;
+  L->grid_a = ga < 1 ? 1 : ga;
+  L->grid_b = gb < 1 ? 1 : gb;
+  L->smem_a = smem_a;
+  L->smem_b = smem_b;
   return true;
 }
 
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.n_scen <= 0) return PARVA_OK;
-  int grid;
-  size_t smem;
-  if (!plan_launch_config(A, &grid, &smem)) return PARVA_LAUNCH_ERROR;
-  plan_batch_kernel<<<grid, PB_THREADS, smem, stream>>>(A);
+  LaunchCfg L;
+  if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
+  if (!A.cfg_given && A.n_svc > 0)
+    configure_services_kernel<<<L.grid_a, CF_THREADS, L.smem_a, stream>>>(A);
+  plan_batch_kernel<<<L.grid_b, PB_THREADS, L.smem_b, stream>>>(A);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
 int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t* deps, size_t ndeps,
                         cudaGraphNode_t* node) {
-  int grid;
-  size_t smem;
-  if (!plan_launch_config(A, &grid, &smem)) return PARVA_LAUNCH_ERROR;
+  LaunchCfg L;
+  if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
   PlanArgs copy = A;
   void* args[] = {&copy};
   cudaKernelNodeParams p = {};
+  cudaGraphNode_t na;
+  const cudaGraphNode_t* d = deps;
+  size_t nd = ndeps;
+  if (!A.cfg_given && A.n_svc > 0) {
+    p.func = (void*)configure_services_kernel;
+    p.gridDim = dim3(L.grid_a);
+    p.blockDim = dim3(CF_THREADS);
+    p.sharedMemBytes = (unsigned)L.smem_a;
+    p.kernelParams = args;
+    if (cudaGraphAddKernelNode(&na, g, deps, ndeps, &p) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    d = &na;
+    nd = 1;
+  }
   p.func = (void*)plan_batch_kernel;
-  p.gridDim = dim3(grid);
+  p.gridDim = dim3(L.grid_b);
   p.blockDim = dim3(PB_THREADS);
-  p.sharedMemBytes = (unsigned)smem;
+  p.sharedMemBytes = (unsigned)L.smem_b;
   p.kernelParams = args;
-  return cudaGraphAddKernelNode(node, g, deps, ndeps, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+  return cudaGraphAddKernelNode(node, g, d, nd, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
 }  // namespace parva

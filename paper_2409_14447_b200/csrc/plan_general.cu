@@ -39,6 +39,7 @@ struct GenWs {
   uint8_t* seen;    // [n_services]
   int64_t* svc_pos; // [n_services + 1] relocation queue offsets of one size class
   int64_t* gpu_pos; // [cap + 1] cumulative capacity of one size class
+  int64_t* gpu_pos2;// [cap + 1] second scan buffer
   int64_t* hdr;     // [8]: G, max_id, status, next (ledger rank counter)
   int64_t words, qcap, cap;
 };
@@ -59,6 +60,7 @@ __host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_se
   t.q = (int32_t*)take(qcap * 4); t.q1 = (int32_t*)take(qcap * 4); t.undo = (int32_t*)take(qcap * 4);
   t.after = (double*)take((size_t)(n_services + 1) * 8); t.seen = take(n_services + 1);
   t.svc_pos = (int64_t*)take((size_t)(n_services + 2) * 8); t.gpu_pos = (int64_t*)take((size_t)(cap + 2) * 8);
+  t.gpu_pos2 = (int64_t*)take((size_t)(cap + 2) * 8);
   t.hdr = (int64_t*)take(8 * 8);
   t.words = words; t.qcap = qcap; t.cap = cap;
   if (w) *w = t;
@@ -164,10 +166,20 @@ __device__ __forceinline__ int fill_start(uint32_t m, int c, int j) {
     m |= footprint(c, st);
   }
 }
-__device__ __forceinline__ uint32_t fill_mask(uint32_t m, int c, int used) {
-  for (int k = 0; k < used; k++) m |= footprint(c, find_start(m, c));
-  return m;
+// 8-bit GPU state: bits 0-6 occupied-or-blocked slots, bit 7 = a size-3
+// segment sits at slot 0 (its blocked slot 3 is not a GPC), so
+// num_gpcs = popc(bits 0-6) - bit 7.
+constexpr uint32_t kFlag30 = 0x80u;
+__device__ __forceinline__ uint32_t fill_mask8(uint32_t m8, int c, int used) {
+  uint32_t m = m8 & 0x7Fu, f = m8 & kFlag30;
+  for (int k = 0; k < used; k++) {
+    const int st = find_start(m, c);
+    m |= footprint(c, st);
+    if (c == 2 && st == 0) f = kFlag30;
+  }
+  return m | f;
 }
+__device__ __forceinline__ int gpcs8(uint32_t m8) { return __popc(m8 & 0x7Fu) - (int)(m8 >> 7); }
 
 // exclusive block scan (1024 threads) of f(i), i < n, into out[0..n]; returns the total
 template <class F>
@@ -243,7 +255,7 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
     int ng = 0, n = 0;
     for (int k = P.d_pl_off[g]; k < P.d_pl_off[g + 1]; k++, n++) {
       const int cat = P.d_pl_cat[k], c = class_of_size(P.d_cat_size[cat]);
-      m |= footprint(c, P.d_pl_slot[k]);
+      m |= footprint(c, P.d_pl_slot[k]) | (c == 2 && P.d_pl_slot[k] == 0 ? kFlag30 : 0u);
       ng += size_of_class(c);
       w.lcat[g * 7 + n] = cat;
       w.lslot[g * 7 + n] = P.d_pl_slot[k];
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
                (lc >= 0 && class_of_size(P.d_cat_size[lc]) == c ? 1 : 0);
       }, w.svc_pos, sh);
       if (L == 0) continue;
-      const int64_t S = block_scan(G, [&](int64_t g) -> int64_t { return fill_cap(w.mask[g], c); }, w.gpu_pos, sh);
+      const int64_t S = block_scan(G, [&](int64_t g) -> int64_t { return fill_cap(w.mask[g] & 0x7Fu, c); }, w.gpu_pos, sh);
       const int cap_e = fill_cap(0u, c);
       const int64_t rem = L > S ? L - S : 0;
       const int64_t n_new = (rem + cap_e - 1) / cap_e;
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
             while (w.gpu_pos[g + 1] <= i) g++;
             const int j = (int)(i - w.gpu_pos[g]);
             w.lcat[g * 7 + w.len[g] + j] = cat;
-            w.lslot[g * 7 + w.len[g] + j] = (uint8_t)fill_start(w.mask[g], c, j);
+            w.lslot[g * 7 + w.len[g] + j] = (uint8_t)fill_start(w.mask[g] & 0x7Fu, c, j);
           } else {
             const int64_t k = i - S, gn = G + k / cap_e;
             const int j = (int)(k % cap_e);
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
         const int capg = (int)(w.gpu_pos[g + 1] - w.gpu_pos[g]);
         const int used = got <= 0 ? 0 : (got < capg ? (int)got : capg);
         if (used) {
-          w.mask[g] = (uint8_t)fill_mask(w.mask[g], c, used);
+          w.mask[g] = (uint8_t)fill_mask8(w.mask[g], c, used);
           w.len[g] += (uint8_t)used;
           w.ngpc[g] += (uint8_t)(used * size);
         }
@@ -314,7 +326,7 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
         const int64_t g = G + k;
         const int used = (int)min((int64_t)cap_e, rem - k * cap_e);
         w.id[g] = max_id + 1 + k;
-        w.mask[g] = (uint8_t)fill_mask(0u, c, used);
+        w.mask[g] = (uint8_t)fill_mask8(0u, c, used);
         w.len[g] = (uint8_t)used;
         w.ngpc[g] = (uint8_t)(used * size);
       }
@@ -336,170 +348,323 @@ __device__ inline double unalloc_g(int64_t total, int64_t n) {
   return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
 }
 
-__global__ void __launch_bounds__(1024) plan_general_kernel(parva_general_problem P, parva_general_result R,
-                                                             uint8_t* ws_base, int64_t cap, int64_t qcap) {
-  GenWs wsh;
-  gen_layout(cap, qcap, P.n_services, ws_base, &wsh);
-  const int64_t G0 = wsh.hdr[0];
-  // accepts-bitmaps and the optimize-input backup, in parallel
-  for (int64_t k = threadIdx.x; k < (G0 + 63) / 64; k += blockDim.x) {
+// Optimize (allocator.py:362-443) as a warp-cooperative serial chain.  GPU
+// state (8-bit mask + list length) and the per-size accepts bitmaps sit in
+// shared memory when they fit (up to ~85k GPUs), else in global memory.  Warp
+// 0 walks the chain: the next drain candidate (0 < num_gpcs <= threshold) is
+// found 32 GPUs per ballot, first-fit scans 32 bitmap words per ballot from a
+// lowest-nonzero-word hint, undo entries carry (gpu, class, slot) so a
+// rollback reads no lists, and the freed_rate ledger rolls back from a log.
+constexpr int OPT_THREADS = 512;
+
+struct OptState {
+  uint8_t* M;        // mask | flag, per GPU
+  uint8_t* Ln;       // list length, per GPU
+  uint64_t* A;       // accepts bitmaps [5][words]
+  int64_t words, G;
+  int64_t hint[5];
+
+  __device__ void set_bits(int64_t g, int lane) {
+    const uint32_t m = M[g] & 0x7Fu;
+    const int64_t k = g >> 6;
+    const uint64_t bit = 1ull << (g & 63);
+#pragma unroll
+    for (int c = 0; c < 5; c++) {
+      const bool acc = find_start(m, c) >= 0;
+      if (lane == 0) {
+        uint64_t* a = &A[c * words + k];
+        *a = acc ? (*a | bit) : (*a & ~bit);
+      }
+      if (acc && k < hint[c]) hint[c] = k;
+    }
+    __syncwarp();
+  }
+
+  // first GPU in list order accepting class c, skipping `excl` (warp-wide)
+  __device__ int64_t first_fit(int c, int64_t excl, int lane) {
+    const uint64_t* a = &A[c * words];
+    const int64_t nw = (G + 63) >> 6;
+    for (int64_t k = hint[c]; k < nw; k += 32) {
+      const int64_t kk = k + lane;
+      const uint64_t raw = kk < nw ? a[kk] : 0ull;
+      uint64_t v = raw;
+      if (excl >= 0 && kk == (excl >> 6)) v &= ~(1ull << (excl & 63));
+      const unsigned rb = __ballot_sync(0xffffffffu, raw != 0ull);
+      if (k == hint[c]) hint[c] = rb ? k + __ffs(rb) - 1 : k + 32;
+      const unsigned b = __ballot_sync(0xffffffffu, v != 0ull);
+      if (b) {
+        const int src = __ffs(b) - 1;
+        const uint64_t word = __shfl_sync(0xffffffffu, v, src);
+        return (k + src) * 64 + __ffsll((long long)word) - 1;
+      }
+    }
+    return -1;
+  }
+};
+
+__global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general_problem P, parva_general_result R,
+                                                                   uint8_t* ws_base, int64_t cap, int64_t qcap,
+                                                                   int64_t smem_gpus) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ int64_t sh[33];
+  __shared__ int s_fallback, s_status;
+  __shared__ int64_t s_nd;
+  GenWs w;
+  gen_layout(cap, qcap, P.n_services, ws_base, &w);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t G0 = w.hdr[0];
+  int status = (int)w.hdr[2];
+  const bool in_smem = G0 <= smem_gpus;
+  const int64_t words = (G0 + 63) / 64;
+  const int64_t gpad = (G0 + 15) & ~int64_t(15);
+  OptState S;
+  S.M = in_smem ? dsm : w.mask;
+  S.Ln = in_smem ? dsm + gpad : w.len;
+  S.A = in_smem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
+  S.words = words;
+  S.G = G0;
+  for (int c = 0; c < 5; c++) S.hint[c] = 0;
+  if (in_smem)
+    for (int64_t g = tid; g < G0; g += blockDim.x) { S.M[g] = w.mask[g]; S.Ln[g] = w.len[g]; }
+  __syncthreads();
+  for (int64_t k = tid; k < words; k += blockDim.x) {
     uint64_t b[5] = {0, 0, 0, 0, 0};
     for (int j = 0; j < 64 && k * 64 + j < G0; j++) {
-      const uint32_t m = wsh.mask[k * 64 + j];
+      const uint32_t m = S.M[k * 64 + j] & 0x7Fu;
 #pragma unroll
       for (int c = 0; c < 5; c++) if (find_start(m, c) >= 0) b[c] |= 1ull << j;
     }
 #pragma unroll
-    for (int c = 0; c < 5; c++) wsh.acc[c * wsh.words + k] = b[c];
+    for (int c = 0; c < 5; c++) S.A[c * words + k] = b[c];
   }
-  if (P.optimize && wsh.hdr[2] == PARVA_OK)
-    for (int64_t g = threadIdx.x; g < G0; g += blockDim.x) {
-      wsh.b_id[g] = wsh.id[g]; wsh.b_mask[g] = wsh.mask[g]; wsh.b_len[g] = wsh.len[g]; wsh.b_ngpc[g] = wsh.ngpc[g];
-      for (int k = 0; k < wsh.len[g]; k++) { wsh.b_lcat[g * 7 + k] = wsh.lcat[g * 7 + k]; wsh.b_lslot[g * 7 + k] = wsh.lslot[g * 7 + k]; }
+  const bool run = P.optimize && status == PARVA_OK;
+  if (run)
+    for (int64_t g = tid; g < G0; g += blockDim.x) {
+      w.b_mask[g] = w.mask[g]; w.b_len[g] = w.len[g];
+      for (int k = 0; k < w.len[g]; k++) { w.b_lcat[g * 7 + k] = w.lcat[g * 7 + k]; w.b_lslot[g * 7 + k] = w.lslot[g * 7 + k]; }
     }
+  if (tid == 0) { s_fallback = 0; s_status = status; s_nd = 0; }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  Gen S{P, wsh, G0, wsh.hdr[1], {0, 0, 0, 0, 0}};
-  GenWs& w = S.w;
-  int status = (int)w.hdr[2];
-  int32_t next = (int32_t)w.hdr[3];
-  const int64_t n_before = S.G;
-  int64_t total_before = 0;
-  for (int64_t g = 0; g < S.G; g++) total_before += w.ngpc[g];
-  R.d_counts[3] = (int32_t)n_before;
-  int fallback = 0;
-  int64_t nd = 0;
 
-  if (status == PARVA_OK && P.optimize) {
-    // ---- optimize_allocation (allocator.py:362-443)
-    for (int64_t index = S.G - 1; index >= 0; index--) {
-      const int nl = w.len[index];
-      if (nl == 0 || (int)w.ngpc[index] > P.threshold) continue;
-      int32_t lg_name[7];
-      double lg_val[7];
-      int32_t lg_ord[7];
-      int nlog = 0;
+  if (run && warp == 0) {
+    int32_t next = (int32_t)w.hdr[3];
+    int64_t nd = 0;
+    int64_t idx = G0 - 1;
+    while (true) {
+      // next drain candidate at or below idx
+      int64_t index = -1;
+      while (idx >= 0) {
+        const int64_t g = idx - lane;
+        const int ng = g >= 0 ? gpcs8(S.M[g]) : 0;
+        const unsigned b = __ballot_sync(0xffffffffu, ng > 0 && ng <= P.threshold);
+        if (b) { index = idx - (__ffs(b) - 1); break; }
+        idx -= 32;
+      }
+      if (index < 0) break;
+      idx = index - 1;
+      const int nl = S.Ln[index];
+      // the drained list and what it needs, one entry per lane
+      int e_cat = 0, e_slot = 0, e_name = 0, e_t1 = -1, e_t2 = -1;
+      double e_tp = 0.0;
+      if (lane < nl) {
+        e_cat = w.lcat[index * 7 + lane];
+        e_slot = w.lslot[index * 7 + lane];
+        e_name = P.d_cat_name[e_cat];
+        e_tp = P.d_cat_tp[e_cat];
+        if (e_name < P.n_services) { e_t1 = P.d_svc_t1[e_name]; e_t2 = P.d_svc_t2[e_name]; }
+      }
+      const double tp1s = lane < nl && e_t1 >= 0 ? P.d_cat_tp[e_t1] : 0.0;
+      const double tp2s = lane < nl && e_t2 >= 0 ? P.d_cat_tp[e_t2] : 0.0;
+      int32_t lg_name = -1, lg_ord = 0;   // lane k logs the k-th ledger change
+      double lg_val = 0.0;
+      double st_v = 0.0;                  // lane 0 staging of the log entry
+      int32_t st_o = 0;
       const int32_t sv_next = next;
       int64_t q2n = 0, q1n = 0;
       int fail = -1, rot = nl;
       int64_t fname = -1;
       bool qover = false;
       for (int k = 0; k < nl; k++) {
-        const int cat = w.lcat[index * 7 + k];
-        const int name = P.d_cat_name[cat];
-        const int s = name < P.n_services ? name : -1;   // services_by_id.get
-        if (s < 0) { fail = PARVA_DIAG_UNKNOWN_SERVICE; fname = name; rot = k; break; }
-        lg_name[nlog] = s; lg_val[nlog] = R.d_ledger_val[s]; lg_ord[nlog] = R.d_ledger_order[s]; nlog++;
-        const double tpp = P.d_cat_tp[cat];
-        if (R.d_ledger_order[s] == 0) { R.d_ledger_order[s] = ++next; R.d_ledger_val[s] = __dadd_rn(0.0, tpp); }
-        else R.d_ledger_val[s] = __dadd_rn(R.d_ledger_val[s], tpp);
-        const int c1 = P.d_svc_t1[s], c2 = P.d_svc_t2[s];
-        const double t1 = c1 >= 0 ? P.d_cat_tp[c1] : 0.0, t2 = c2 >= 0 ? P.d_cat_tp[c2] : 0.0;
-        long long k2, k1;
-        if (!propose_small(t1, t2, R.d_ledger_val[s], k2, k1)) {
-          fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break;
+        const int name = __shfl_sync(0xffffffffu, e_name, k);
+        if (name >= P.n_services) { fail = PARVA_DIAG_UNKNOWN_SERVICE; fname = name; rot = k; break; }
+        const int s = name;
+        const double tpp = __shfl_sync(0xffffffffu, e_tp, k);
+        const int c1 = __shfl_sync(0xffffffffu, e_t1, k), c2 = __shfl_sync(0xffffffffu, e_t2, k);
+        const double t1 = __shfl_sync(0xffffffffu, tp1s, k), t2 = __shfl_sync(0xffffffffu, tp2s, k);
+        double f = 0.0;
+        if (lane == 0) {
+          const double ov = R.d_ledger_val[s];
+          const int32_t oo = R.d_ledger_order[s];
+          f = oo == 0 ? __dadd_rn(0.0, tpp) : __dadd_rn(ov, tpp);
+          if (oo == 0) R.d_ledger_order[s] = ++next;
+          R.d_ledger_val[s] = f;
+          st_v = ov; st_o = oo;
         }
-        double v = R.d_ledger_val[s];
-        for (long long j = 0; j < k2; j++) v = __dsub_rn(v, t2);
-        for (long long j = 0; j < k1; j++) v = __dsub_rn(v, t1);
-        R.d_ledger_val[s] = v;
+        // move lane 0's staged log entry to lane k (k < nl <= 7)
+        const double mv = __shfl_sync(0xffffffffu, st_v, 0);
+        const int32_t mo = __shfl_sync(0xffffffffu, st_o, 0);
+        if (lane == k) { lg_name = s; lg_val = mv; lg_ord = mo; }
+        next = __shfl_sync(0xffffffffu, next, 0);
+        f = __shfl_sync(0xffffffffu, f, 0);
+        long long k2, k1;
+        if (!propose_small(t1, t2, f, k2, k1)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break; }
+        if (lane == 0) {
+          double v = f;
+          for (long long j = 0; j < k2; j++) v = __dsub_rn(v, t2);
+          for (long long j = 0; j < k1; j++) v = __dsub_rn(v, t1);
+          R.d_ledger_val[s] = v;
+        }
         if (qover || q2n + k2 > w.qcap || q1n + k1 > w.qcap) qover = true;
         else {
-          for (long long j = 0; j < k2; j++) w.q[q2n++] = c2;
-          for (long long j = 0; j < k1; j++) w.q1[q1n++] = c1;
+          for (long long j = lane; j < k2; j += 32) w.q[q2n + j] = c2;
+          for (long long j = lane; j < k1; j += 32) w.q1[q1n + j] = c1;
+          q2n += k2; q1n += k1;
         }
+        __syncwarp();
       }
+      __threadfence_block();
+      int64_t nu = 0;
       if (fail < 0) {
         if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
         else {
-          int64_t nu = 0;
-          for (int64_t j = 0; j < q2n + q1n; j++) {
-            const int cat = j < q2n ? w.q[j] : w.q1[j - q2n];
-            const int64_t g = S.place(cat, index, false);
-            if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
-            w.undo[nu++] = (int32_t)g;
+          for (int64_t base = 0; base < q2n + q1n && fail < 0; base += 32) {
+            const int64_t jl = base + lane;
+            const int my_cat = jl < q2n ? w.q[jl] : (jl < q2n + q1n ? w.q1[jl - q2n] : 0);
+            const int cnt = (int)min((int64_t)32, q2n + q1n - base);
+            for (int u = 0; u < cnt; u++) {
+              const int cat = __shfl_sync(0xffffffffu, my_cat, u);
+              const int c = base + u < q2n ? 1 : 0;   // t2 kinds are size 2, t1 kinds size 1
+              const int64_t g = S.first_fit(c, index, lane);
+              if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
+              const uint32_t m8 = S.M[g];
+              const int st = find_start(m8 & 0x7Fu, c);
+              const int ln = S.Ln[g];
+              if (lane == 0) {
+                S.M[g] = (uint8_t)(m8 | footprint(c, st));
+                S.Ln[g] = (uint8_t)(ln + 1);
+                w.lcat[g * 7 + ln] = cat;
+                w.lslot[g * 7 + ln] = (uint8_t)st;
+                w.undo[nu] = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
+              }
+              __syncwarp();
+              nu++;
+              S.set_bits(g, lane);
+            }
           }
-          if (fail >= 0)
-            for (int64_t j = nu - 1; j >= 0; j--) S.pop(w.undo[j]);
+          if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
+            for (int64_t j = nu - 1; j >= 0; j--) {
+              const int32_t u = w.undo[j];
+              const int64_t g = u >> 4;
+              const int c = (u >> 3) & 1, st = u & 7;
+              if (lane == 0) {
+                S.M[g] = (uint8_t)(S.M[g] & ~footprint(c, st));
+                S.Ln[g] = (uint8_t)(S.Ln[g] - 1);
+              }
+              __syncwarp();
+              S.set_bits(g, lane);
+            }
+          }
         }
       }
       if (fail >= 0) {
-        if (rot != nl) {   // allocator.py:415-417: removed ones re-appended
-          int32_t tc[7];
-          uint8_t ts[7];
-          for (int k = 0; k < nl; k++) { tc[k] = w.lcat[index * 7 + k]; ts[k] = w.lslot[index * 7 + k]; }
-          for (int k = 0; k < nl; k++) {
-            const int src = (k + rot) % nl;
-            w.lcat[index * 7 + k] = tc[src];
-            w.lslot[index * 7 + k] = ts[src];
-          }
+        if (rot != nl) {   // allocator.py:415-417: the removed ones are re-appended
+          int src = lane + rot;
+          if (src >= nl) src -= nl;
+          const int nc = __shfl_sync(0xffffffffu, e_cat, src & 31);
+          const int ns = __shfl_sync(0xffffffffu, e_slot, src & 31);
+          if (lane < nl) { w.lcat[index * 7 + lane] = nc; w.lslot[index * 7 + lane] = (uint8_t)ns; }
         }
-        for (int k = nlog - 1; k >= 0; k--) {
-          R.d_ledger_val[lg_name[k]] = lg_val[k];
-          R.d_ledger_order[lg_name[k]] = lg_ord[k];
+        // ledger rollback in reverse log order
+        for (int k = nl - 1; k >= 0; k--) {
+          const int32_t nm = __shfl_sync(0xffffffffu, lg_name, k);
+          const double v = __shfl_sync(0xffffffffu, lg_val, k);
+          const int32_t o = __shfl_sync(0xffffffffu, lg_ord, k);
+          if (nm >= 0 && lane == 0) { R.d_ledger_val[nm] = v; R.d_ledger_order[nm] = o; }
         }
         next = sv_next;
-        if (nd < R.diag_cap) {
+        if (lane == 0 && nd < R.diag_cap) {
           R.d_diag[3 * nd] = fail;
           R.d_diag[3 * nd + 1] = w.id[index];
           R.d_diag[3 * nd + 2] = fname;
         }
         nd++;
       } else {
-        w.len[index] = 0; w.mask[index] = 0; w.ngpc[index] = 0;
-        S.set_acc(index);
+        if (lane == 0) { S.M[index] = 0; S.Ln[index] = 0; }
+        __syncwarp();
+        S.set_bits(index, lane);
       }
+      __syncwarp();
     }
-    int64_t n_after = 0, total_after = 0;
-    for (int64_t g = 0; g < S.G; g++) if (w.len[g]) { n_after++; total_after += w.ngpc[g]; }
-    if (n_after > n_before ||
-        unalloc_g(total_after, n_after) > __dadd_rn(unalloc_g(total_before, n_before), 1e-12)) {
-      fallback = 1;
-      for (int64_t g = 0; g < S.G; g++) {
-        w.id[g] = w.b_id[g]; w.mask[g] = w.b_mask[g]; w.len[g] = w.b_len[g]; w.ngpc[g] = w.b_ngpc[g];
-        for (int k = 0; k < w.len[g]; k++) { w.lcat[g * 7 + k] = w.b_lcat[g * 7 + k]; w.lslot[g * 7 + k] = w.b_lslot[g * 7 + k]; }
-      }
-      for (int k = 0; k < P.n_names; k++) { R.d_ledger_val[k] = P.d_ledger_val[k]; R.d_ledger_order[k] = P.d_ledger_order[k]; }
-      nd = 1;
-      if (R.diag_cap >= 1) { R.d_diag[0] = PARVA_DIAG_REGRESSED; R.d_diag[1] = -1; R.d_diag[2] = -1; }
-    }
+    if (lane == 0) s_nd = nd;
   }
+  __syncthreads();
 
-  // ---- emit (compaction drops empty GPUs, ids kept; the fallback map is the
-  // optimize input as is)
-  int64_t ng = 0, np = 0;
-  if (status == PARVA_OK) {
-    const bool compact = P.optimize && !fallback;
-    for (int64_t g = 0; g < S.G; g++) {
-      if (compact && w.len[g] == 0) continue;
-      if (ng >= R.gpu_cap || np + w.len[g] > R.place_cap) { status = PARVA_CAPACITY; break; }
-      R.d_gpu_id[ng] = w.id[g];
-      R.d_pl_off[ng] = (int32_t)np;
-      for (int k = 0; k < w.len[g]; k++, np++) {
-        R.d_pl_cat[np] = w.lcat[g * 7 + k];
-        R.d_pl_slot[np] = w.lslot[g * 7 + k];
+  // ---- compaction + regression check (allocator.py:423-435), parallel
+  int64_t nd = s_nd;
+  if (run) {
+    const int64_t n_after = block_scan(G0, [&](int64_t g) -> int64_t { return S.Ln[g] ? 1 : 0; }, w.gpu_pos, sh);
+    const int64_t tot_after = block_scan(G0, [&](int64_t g) -> int64_t { return S.Ln[g] ? gpcs8(S.M[g]) : 0; },
+                                         w.gpu_pos2, sh);
+    const int64_t tot_before = block_scan(G0, [&](int64_t g) -> int64_t { return gpcs8(w.b_mask[g]); },
+                                          w.gpu_pos2, sh);
+    const double ua_b = unalloc_g(tot_before, G0), ua_a = unalloc_g(tot_after, n_after);
+    if (tid == 0 && (n_after > G0 || ua_a > __dadd_rn(ua_b, 1e-12))) s_fallback = 1;
+    __syncthreads();
+    if (s_fallback) {
+      for (int64_t g = tid; g < G0; g += blockDim.x) {
+        S.M[g] = w.b_mask[g]; S.Ln[g] = w.b_len[g];
+        for (int k = 0; k < w.b_len[g]; k++) { w.lcat[g * 7 + k] = w.b_lcat[g * 7 + k]; w.lslot[g * 7 + k] = w.b_lslot[g * 7 + k]; }
       }
-      ng++;
+      for (int k = tid; k < P.n_names; k += blockDim.x) { R.d_ledger_val[k] = P.d_ledger_val[k]; R.d_ledger_order[k] = P.d_ledger_order[k]; }
+      nd = 1;
+      if (tid == 0 && R.diag_cap >= 1) { R.d_diag[0] = PARVA_DIAG_REGRESSED; R.d_diag[1] = -1; R.d_diag[2] = -1; }
+      __syncthreads();
     }
-    R.d_pl_off[ng] = (int32_t)np;
-    if (nd > R.diag_cap) status = PARVA_CAPACITY;
   }
-  // ---- coverage assert (allocator.py:437-442), service_throughput in map order
-  if (status == PARVA_OK && P.optimize && !fallback) {
-    for (int s = 0; s < P.n_services; s++) { w.after[s] = 0.0; w.seen[s] = 0; }
-    for (int64_t k = 0; k < np; k++) {
-      const int name = P.d_cat_name[R.d_pl_cat[k]];
-      if (name < P.n_services) { w.after[name] = __dadd_rn(w.after[name], P.d_cat_tp[R.d_pl_cat[k]]); w.seen[name] = 1; }
+  // ---- emit: GPUs in order (compacted unless fallback / no optimize), lists
+  if (status == PARVA_OK) {
+    const bool compact = run && !s_fallback;
+    const int64_t ng = block_scan(G0, [&](int64_t g) -> int64_t { return !compact || S.Ln[g] ? 1 : 0; }, w.gpu_pos, sh);
+    const int64_t np = block_scan(G0, [&](int64_t g) -> int64_t { return !compact || S.Ln[g] ? S.Ln[g] : 0; },
+                                  w.gpu_pos2, sh);
+    if (ng > R.gpu_cap || np > R.place_cap || nd > R.diag_cap) {
+      status = PARVA_CAPACITY;
+    } else {
+      for (int64_t g = tid; g < G0; g += blockDim.x) {
+        if (compact && !S.Ln[g]) continue;
+        const int64_t o = w.gpu_pos[g], po = w.gpu_pos2[g];
+        R.d_gpu_id[o] = w.id[g];
+        R.d_pl_off[o] = (int32_t)po;
+        for (int k = 0; k < S.Ln[g]; k++) { R.d_pl_cat[po + k] = w.lcat[g * 7 + k]; R.d_pl_slot[po + k] = w.lslot[g * 7 + k]; }
+      }
+      if (tid == 0) R.d_pl_off[ng] = (int32_t)np;
     }
-    for (int s = 0; s < P.n_services; s++)
-      if (P.d_svc_rate[s] > 0.0 && w.seen[s] && !(w.after[s] >= __dmul_rn(P.d_svc_rate[s], 1.0 - 1e-9)))
-        status = PARVA_COVERAGE_ASSERT;
+    __syncthreads();
+    // ---- coverage assert (allocator.py:437-442): service_throughput in map order
+    if (status == PARVA_OK && compact) {
+      for (int s = tid; s < P.n_services; s += blockDim.x) { w.after[s] = 0.0; w.seen[s] = 0; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int64_t k = 0; k < np; k++) {
+          const int name = P.d_cat_name[R.d_pl_cat[k]];
+          if (name < P.n_services) { w.after[name] = __dadd_rn(w.after[name], P.d_cat_tp[R.d_pl_cat[k]]); w.seen[name] = 1; }
+        }
+      }
+      __syncthreads();
+      for (int s = tid; s < P.n_services; s += blockDim.x)
+        if (P.d_svc_rate[s] > 0.0 && w.seen[s] && !(w.after[s] >= __dmul_rn(P.d_svc_rate[s], 1.0 - 1e-9)))
+          atomicExch(&s_status, PARVA_COVERAGE_ASSERT);
+      __syncthreads();
+      if (s_status == PARVA_COVERAGE_ASSERT) status = PARVA_COVERAGE_ASSERT;
+    }
+    if (tid == 0) { R.d_counts[0] = (int32_t)ng; R.d_counts[1] = (int32_t)np; }
   }
-  R.d_counts[0] = (int32_t)ng;
-  R.d_counts[1] = (int32_t)np;
-  R.d_counts[2] = (int32_t)nd;
-  *R.d_fallback = fallback;
-  *R.d_status = status;
+  if (tid == 0) {
+    R.d_counts[2] = (int32_t)nd;
+    R.d_counts[3] = (int32_t)G0;
+    *R.d_fallback = s_fallback;
+    *R.d_status = status;
+  }
 }
 
 size_t general_workspace(const parva_general_problem* p, int64_t cap) {
@@ -511,7 +676,20 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
   const int64_t cap = r->gpu_cap;
   if (general_workspace(p, cap) > ws_bytes) return PARVA_BAD_INPUT;
   gen_prepare_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
-  plan_general_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
+  // shared-memory state when it fits: 2 B per GPU + 5 bitmap bits per GPU
+  static int smem_max = 0;
+  if (!smem_max) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    smem_max -= 2048;   // static shared memory of the kernel
+    cudaFuncSetAttribute(plan_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+  }
+  // largest G with 2 * pad16(G) + 40 * ceil(G / 64) <= smem_max
+  int64_t smem_gpus = (int64_t)smem_max * 8 / 21;
+  while (smem_gpus > 0 && 2 * ((smem_gpus + 15) & ~int64_t(15)) + 40 * ((smem_gpus + 63) / 64) > smem_max) smem_gpus--;
+  const size_t smem = (size_t)smem_max;
+  plan_general_kernel<<<1, OPT_THREADS, smem, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8, smem_gpus);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
