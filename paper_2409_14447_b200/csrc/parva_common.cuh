@@ -8,6 +8,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <climits>
 #include "../../include/parva_b200.h"
 
 namespace parva {
@@ -168,6 +169,52 @@ __device__ inline bool propose_small(double tp1, double tp2, double freed, long 
     } else continue;
     long long g = 2 * k2 + k1, cn = k2 + k1, nk = -k2;
     if (!have || g < bg || (g == bg && (cn < bc || (cn == bc && nk < bn)))) {
+      have = true; bg = g; bc = cn; bn = nk;
+    }
+  }
+  if (!have) return false;
+  k2o = -bn;
+  k1o = bc + bn;
+  return true;
+}
+
+// propose_small_segments with the k2 candidates spread over the warp: lane j
+// evaluates k2 = base + j, then a lexicographic-min reduction over
+// (2*k2+k1, k2+k1, -k2) -- a strict total order (k2 unique), so the result is
+// the sequential loop's.  All 32 lanes must call it with the same arguments.
+__device__ inline bool propose_small_warp(double tp1, double tp2, double freed, long long& k2o, long long& k1o,
+                                          int lane) {
+  k2o = 0; k1o = 0;
+  if (freed <= 0.0) return true;
+  if (tp1 == 0.0 && tp2 == 0.0) return false;
+  long long max_k2 = 0;
+  if (tp2 != 0.0) max_k2 = (long long)ceil(__dsub_rn(__ddiv_rn(freed, tp2), 1e-12));
+  const double m = (1.0 > freed) ? 1.0 : freed;
+  const double thr = __dmul_rn(1e-12, m);
+  bool have = false;
+  long long bg = 0, bc = 0, bn = 0;
+  for (long long base = 0; base <= max_k2; base += 32) {
+    const long long k2 = base + lane;
+    bool ok = k2 <= max_k2;
+    long long k1 = 0;
+    if (ok) {
+      const double covered = tp2 != 0.0 ? __dmul_rn((double)k2, tp2) : 0.0;
+      const double sh = __dsub_rn(freed, covered);
+      if (sh <= thr) k1 = 0;
+      else if (tp1 != 0.0) {
+        k1 = (long long)ceil(__dsub_rn(__ddiv_rn(sh, tp1), 1e-12));
+        if (k1 < 1) k1 = 1;
+      } else ok = false;
+    }
+    long long g = ok ? 2 * k2 + k1 : LLONG_MAX, cn = ok ? k2 + k1 : LLONG_MAX, nk = ok ? -k2 : LLONG_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
+      const long long c2 = __shfl_xor_sync(0xffffffffu, cn, o);
+      const long long n2 = __shfl_xor_sync(0xffffffffu, nk, o);
+      if (g2 < g || (g2 == g && (c2 < cn || (c2 == cn && n2 < nk)))) { g = g2; cn = c2; nk = n2; }
+    }
+    if (g != LLONG_MAX && (!have || g < bg || (g == bg && (cn < bc || (cn == bc && nk < bn))))) {
       have = true; bg = g; bc = cn; bn = nk;
     }
   }

@@ -4,19 +4,27 @@
 // (relocate_segments, optimize_allocation) and for scenarios that overflow
 // the fast path's 128-byte record (PARVA_CAPACITY).
 //
-// The allocator's optimize pass is a serial dependency chain (SURVEY.md
-// §8e): one thread walks it.  First-fit is O(1) amortised through per-size
-// "accepts" bitmaps with a lowest-nonzero-word hint instead of the
-// reference's O(M) scans and O(M) _next_id (allocator.py:204-281), which is
-// what makes the 10^5-segment case (C5) cheap.  Ledger rollback uses an undo
-// log instead of the reference's whole-dict snapshot (allocator.py:387,418-419):
-// same observable ledger, O(touched) instead of O(services) per GPU.
+// Relocation runs as parallel per-size-class phases (gen_prepare_kernel).  The
+// optimize pass is a serial dependency chain walked by one
+// warp; first-fit is a two-level "accepts" bitmap search (summary ballot,
+// then word) instead of the reference's O(M) scans and O(M) _next_id
+// (allocator.py:204-281), which is what makes the 10^5-segment case (C5)
+// cheap.  Ledger rollback uses an undo log instead of the reference's
+// whole-dict snapshot (allocator.py:387,418-419): same observable ledger,
+// O(touched) instead of O(services) per GPU.
 #include <cuda_runtime.h>
 
 #include "parva_common.cuh"
 #include "parva_kernels.cuh"
 
 namespace parva {
+
+// Flattened catalogue entry: everything a drain needs about a placement kind
+// in one 40-byte load (tp, the owning service's size-1/2 kinds and their tps).
+struct CatExt {
+  double tp, tp1, tp2;
+  int32_t name, c1, c2, pad;
+};
 
 struct GenWs {
   int64_t* id;
@@ -37,16 +45,18 @@ struct GenWs {
   int32_t* undo;    // [qcap]
   double* after;    // [n_services]
   uint8_t* seen;    // [n_services]
+  uint64_t* summary;// [5 * swords] (global fallback of the summary bitmaps)
   int64_t* svc_pos; // [n_services + 1] relocation queue offsets of one size class
   int64_t* gpu_pos; // [cap + 1] cumulative capacity of one size class
   int64_t* gpu_pos2;// [cap + 1] second scan buffer
   int64_t* hdr;     // [8]: G, max_id, status, next (ledger rank counter)
+  CatExt* ext;      // [n_cat]
   int64_t words, qcap, cap;
 };
 
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-__host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_services, uint8_t* base,
+__host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_services, int n_cat, uint8_t* base,
                                              GenWs* w) {
   const int64_t words = (cap + 63) / 64;
   size_t off = 0;
@@ -57,100 +67,18 @@ __host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_se
   t.b_id = (int64_t*)take(cap * 8); t.b_mask = take(cap); t.b_len = take(cap); t.b_ngpc = take(cap);
   t.b_lcat = (int32_t*)take(cap * 7 * 4); t.b_lslot = take(cap * 7);
   t.acc = (uint64_t*)take(5 * words * 8);
+  t.summary = (uint64_t*)take(5 * ((words + 63) / 64 + 1) * 8);
   t.q = (int32_t*)take(qcap * 4); t.q1 = (int32_t*)take(qcap * 4); t.undo = (int32_t*)take(qcap * 4);
   t.after = (double*)take((size_t)(n_services + 1) * 8); t.seen = take(n_services + 1);
   t.svc_pos = (int64_t*)take((size_t)(n_services + 2) * 8); t.gpu_pos = (int64_t*)take((size_t)(cap + 2) * 8);
   t.gpu_pos2 = (int64_t*)take((size_t)(cap + 2) * 8);
   t.hdr = (int64_t*)take(8 * 8);
+  t.ext = (CatExt*)take((size_t)(n_cat + 1) * sizeof(CatExt));
   t.words = words; t.qcap = qcap; t.cap = cap;
   if (w) *w = t;
   return off;
 }
 
-struct Gen {
-  const parva_general_problem P;
-  GenWs w;
-  int64_t G;
-  int64_t max_id;
-  int64_t hint[5];
-
-  __device__ void set_acc(int64_t g) {
-    const uint32_t m = w.mask[g];
-    const int64_t word = g >> 6;
-    const uint64_t bit = 1ull << (g & 63);
-#pragma unroll
-    for (int c = 0; c < 5; c++) {
-      uint64_t* a = &w.acc[c * w.words + word];
-      if (find_start(m, c) >= 0) {
-        *a |= bit;
-        if (word < hint[c]) hint[c] = word;
-      } else {
-        *a &= ~bit;
-      }
-    }
-  }
-
-  // first GPU (list order) accepting size class c, skipping `exclude`
-  __device__ int64_t first_fit(int c, int64_t exclude) {
-    const uint64_t* a = &w.acc[c * w.words];
-    const int64_t nw = (G + 63) >> 6;
-    int64_t k = hint[c];
-    bool moving = true;
-    for (; k < nw; k++) {
-      uint64_t v = a[k];
-      if (moving && v == 0) { hint[c] = k + 1; continue; }
-      moving = false;
-      if (exclude >= 0 && (exclude >> 6) == k) v &= ~(1ull << (exclude & 63));
-      if (k == nw - 1 && (G & 63)) v &= (1ull << (G & 63)) - 1;
-      if (v) return k * 64 + __ffsll((long long)v) - 1;
-    }
-    return -1;
-  }
-
-  __device__ void put(int64_t g, int cat) {
-    const int c = class_of(cat);
-    const int st = find_start(w.mask[g], c);
-    w.mask[g] |= (uint8_t)footprint(c, st);
-    w.ngpc[g] += (uint8_t)size_of_class(c);
-    w.lcat[g * 7 + w.len[g]] = cat;
-    w.lslot[g * 7 + w.len[g]] = (uint8_t)st;
-    w.len[g]++;
-    set_acc(g);
-  }
-
-  __device__ void pop(int64_t g) {
-    const int k = --w.len[g];
-    const int c = class_of(w.lcat[g * 7 + k]);
-    w.mask[g] &= (uint8_t)~footprint(c, w.lslot[g * 7 + k]);
-    w.ngpc[g] -= (uint8_t)size_of_class(c);
-    set_acc(g);
-  }
-
-  __device__ int class_of(int cat) const {
-    switch (P.d_cat_size[cat]) {
-      case 1: return 0;
-      case 2: return 1;
-      case 3: return 2;
-      case 4: return 3;
-      default: return 4;
-    }
-  }
-
-  // _FirstFit.place (allocator.py:194-251); returns GPU index, -1 no fit, -2 capacity
-  __device__ int64_t place(int cat, int64_t exclude, bool allow_new) {
-    int64_t g = first_fit(class_of(cat), exclude);
-    if (g < 0) {
-      if (!allow_new) return -1;
-      if (G >= w.cap) return -2;
-      g = G++;
-      w.id[g] = ++max_id;  // _next_id: max(ids) + 1
-      w.mask[g] = 0; w.len[g] = 0; w.ngpc[g] = 0;
-      set_acc(g);
-    }
-    put(g, cat);
-    return g;
-  }
-};
 
 // ------------------------------------------------------------------ helpers
 // successive greedy placements of size class c on a GPU with mask m
@@ -241,7 +169,7 @@ __device__ __forceinline__ int class_of_size(int size) {
 __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem P, parva_general_result R,
                                                             uint8_t* ws_base, int64_t cap, int64_t qcap) {
   GenWs w;
-  gen_layout(cap, qcap, P.n_services, ws_base, &w);
+  gen_layout(cap, qcap, P.n_services, P.n_cat, ws_base, &w);
   __shared__ int64_t sh[33];
   __shared__ unsigned long long s_max;
   __shared__ int s_next;
@@ -261,6 +189,18 @@ __global__ void __launch_bounds__(1024) gen_prepare_kernel(parva_general_problem
       w.lslot[g * 7 + n] = P.d_pl_slot[k];
     }
     w.mask[g] = (uint8_t)m; w.len[g] = (uint8_t)n; w.ngpc[g] = (uint8_t)ng;
+  }
+  for (int k = tid; k < P.n_cat; k += blockDim.x) {
+    CatExt e;
+    e.tp = P.d_cat_tp[k];
+    e.name = P.d_cat_name[k];
+    const int sv = e.name < P.n_services ? e.name : -1;
+    e.c1 = sv >= 0 ? P.d_svc_t1[sv] : -1;
+    e.c2 = sv >= 0 ? P.d_svc_t2[sv] : -1;
+    e.tp1 = e.c1 >= 0 ? P.d_cat_tp[e.c1] : 0.0;
+    e.tp2 = e.c2 >= 0 ? P.d_cat_tp[e.c2] : 0.0;
+    e.pad = 0;
+    w.ext[k] = e;
   }
   for (int k = tid; k < P.n_names; k += blockDim.x) {
     R.d_ledger_val[k] = P.d_ledger_val[k];
@@ -352,50 +292,57 @@ __device__ inline double unalloc_g(int64_t total, int64_t n) {
 // state (8-bit mask + list length) and the per-size accepts bitmaps sit in
 // shared memory when they fit (up to ~85k GPUs), else in global memory.  Warp
 // 0 walks the chain: the next drain candidate (0 < num_gpcs <= threshold) is
-// found 32 GPUs per ballot, first-fit scans 32 bitmap words per ballot from a
-// lowest-nonzero-word hint, undo entries carry (gpu, class, slot) so a
-// rollback reads no lists, and the freed_rate ledger rolls back from a log.
+// found 32 GPUs per ballot, first-fit is a ballot over the summary bitmap
+// then one word, proposals stay in lane registers as (kind, count) runs,
+// undo entries carry (gpu, class, slot) so a rollback reads no lists, and the
+// freed_rate ledger rolls back from a per-lane log.
 constexpr int OPT_THREADS = 512;
 
 struct OptState {
   uint8_t* M;        // mask | flag, per GPU
   uint8_t* Ln;       // list length, per GPU
   uint64_t* A;       // accepts bitmaps [5][words]
-  int64_t words, G;
-  int64_t hint[5];
+  uint64_t* Sm;      // summary bitmaps [5][swords]: bit = word of A nonzero
+  int64_t words, swords, G;
 
   __device__ void set_bits(int64_t g, int lane) {
     const uint32_t m = M[g] & 0x7Fu;
     const int64_t k = g >> 6;
     const uint64_t bit = 1ull << (g & 63);
-#pragma unroll
-    for (int c = 0; c < 5; c++) {
+    if (lane < 5) {
+      const int c = lane;
       const bool acc = find_start(m, c) >= 0;
-      if (lane == 0) {
-        uint64_t* a = &A[c * words + k];
-        *a = acc ? (*a | bit) : (*a & ~bit);
-      }
-      if (acc && k < hint[c]) hint[c] = k;
+      uint64_t* a = &A[c * words + k];
+      const uint64_t nv = acc ? (*a | bit) : (*a & ~bit);
+      *a = nv;
+      uint64_t* sw = &Sm[c * swords + (k >> 6)];
+      const uint64_t sb = 1ull << (k & 63);
+      *sw = nv ? (*sw | sb) : (*sw & ~sb);
     }
     __syncwarp();
   }
 
-  // first GPU in list order accepting class c, skipping `excl` (warp-wide)
+  // first GPU in list order accepting class c, skipping `excl` (warp-wide):
+  // ballot over summary words, then the first nonzero bitmap word
   __device__ int64_t first_fit(int c, int64_t excl, int lane) {
     const uint64_t* a = &A[c * words];
-    const int64_t nw = (G + 63) >> 6;
-    for (int64_t k = hint[c]; k < nw; k += 32) {
-      const int64_t kk = k + lane;
-      const uint64_t raw = kk < nw ? a[kk] : 0ull;
-      uint64_t v = raw;
-      if (excl >= 0 && kk == (excl >> 6)) v &= ~(1ull << (excl & 63));
-      const unsigned rb = __ballot_sync(0xffffffffu, raw != 0ull);
-      if (k == hint[c]) hint[c] = rb ? k + __ffs(rb) - 1 : k + 32;
-      const unsigned b = __ballot_sync(0xffffffffu, v != 0ull);
-      if (b) {
+    const uint64_t* sm = &Sm[c * swords];
+    const int64_t ew = excl >= 0 ? excl >> 6 : -1;
+    const uint64_t ebit = excl >= 0 ? 1ull << (excl & 63) : 0ull;
+    for (int64_t base = 0; base < swords; base += 32) {
+      const uint64_t v = base + lane < swords ? sm[base + lane] : 0ull;
+      unsigned b = __ballot_sync(0xffffffffu, v != 0ull);
+      while (b) {
         const int src = __ffs(b) - 1;
-        const uint64_t word = __shfl_sync(0xffffffffu, v, src);
-        return (k + src) * 64 + __ffsll((long long)word) - 1;
+        b &= b - 1;
+        uint64_t vs = __shfl_sync(0xffffffffu, v, src);
+        while (vs) {
+          const int64_t wi = (base + src) * 64 + __ffsll((long long)vs) - 1;
+          vs &= vs - 1;
+          uint64_t word = a[wi];
+          if (wi == ew) word &= ~ebit;
+          if (word) return wi * 64 + __ffsll((long long)word) - 1;
+        }
       }
     }
     return -1;
@@ -409,21 +356,24 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   __shared__ int64_t sh[33];
   __shared__ int s_fallback, s_status;
   __shared__ int64_t s_nd;
+  __shared__ uint64_t sm_summary[5 * 64];
   GenWs w;
-  gen_layout(cap, qcap, P.n_services, ws_base, &w);
+  gen_layout(cap, qcap, P.n_services, P.n_cat, ws_base, &w);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t G0 = w.hdr[0];
   int status = (int)w.hdr[2];
   const bool in_smem = G0 <= smem_gpus;
   const int64_t words = (G0 + 63) / 64;
+  const int64_t swords = (words + 63) / 64;
   const int64_t gpad = (G0 + 15) & ~int64_t(15);
   OptState S;
   S.M = in_smem ? dsm : w.mask;
   S.Ln = in_smem ? dsm + gpad : w.len;
   S.A = in_smem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
+  S.Sm = (in_smem && swords <= 64) ? sm_summary : w.summary;
   S.words = words;
+  S.swords = swords;
   S.G = G0;
-  for (int c = 0; c < 5; c++) S.hint[c] = 0;
   if (in_smem)
     for (int64_t g = tid; g < G0; g += blockDim.x) { S.M[g] = w.mask[g]; S.Ln[g] = w.len[g]; }
   __syncthreads();
@@ -436,6 +386,15 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
     }
 #pragma unroll
     for (int c = 0; c < 5; c++) S.A[c * words + k] = b[c];
+  }
+  __syncthreads();
+  for (int64_t k = tid; k < 5 * swords; k += blockDim.x) {
+    const int c = (int)(k / swords);
+    const int64_t sw = k % swords;
+    uint64_t v = 0;
+    for (int j = 0; j < 64 && sw * 64 + j < words; j++)
+      if (S.A[c * words + sw * 64 + j]) v |= 1ull << j;
+    S.Sm[k] = v;
   }
   const bool run = P.optimize && status == PARVA_OK;
   if (run)
@@ -465,25 +424,25 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
       const int nl = S.Ln[index];
       // the drained list and what it needs, one entry per lane
       int e_cat = 0, e_slot = 0, e_name = 0, e_t1 = -1, e_t2 = -1;
-      double e_tp = 0.0;
+      double e_tp = 0.0, tp1s = 0.0, tp2s = 0.0;
       if (lane < nl) {
         e_cat = w.lcat[index * 7 + lane];
         e_slot = w.lslot[index * 7 + lane];
-        e_name = P.d_cat_name[e_cat];
-        e_tp = P.d_cat_tp[e_cat];
-        if (e_name < P.n_services) { e_t1 = P.d_svc_t1[e_name]; e_t2 = P.d_svc_t2[e_name]; }
+        const CatExt X = w.ext[e_cat];
+        e_name = X.name; e_tp = X.tp; e_t1 = X.c1; e_t2 = X.c2; tp1s = X.tp1; tp2s = X.tp2;
+        if (e_name < P.n_services) {   // warm L1 with this service's ledger entry
+          volatile double lv = R.d_ledger_val[e_name];
+          (void)lv;
+        }
       }
-      const double tp1s = lane < nl && e_t1 >= 0 ? P.d_cat_tp[e_t1] : 0.0;
-      const double tp2s = lane < nl && e_t2 >= 0 ? P.d_cat_tp[e_t2] : 0.0;
       int32_t lg_name = -1, lg_ord = 0;   // lane k logs the k-th ledger change
       double lg_val = 0.0;
       double st_v = 0.0;                  // lane 0 staging of the log entry
       int32_t st_o = 0;
       const int32_t sv_next = next;
-      int64_t q2n = 0, q1n = 0;
+      long long my_k2 = 0, my_k1 = 0;   // lane k: proposals of the k-th drained placement
       int fail = -1, rot = nl;
       int64_t fname = -1;
-      bool qover = false;
       for (int k = 0; k < nl; k++) {
         const int name = __shfl_sync(0xffffffffu, e_name, k);
         if (name >= P.n_services) { fail = PARVA_DIAG_UNKNOWN_SERVICE; fname = name; rot = k; break; }
@@ -507,53 +466,54 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
         next = __shfl_sync(0xffffffffu, next, 0);
         f = __shfl_sync(0xffffffffu, f, 0);
         long long k2, k1;
-        if (!propose_small(t1, t2, f, k2, k1)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break; }
+        if (!propose_small_warp(t1, t2, f, k2, k1, lane)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break; }
         if (lane == 0) {
           double v = f;
           for (long long j = 0; j < k2; j++) v = __dsub_rn(v, t2);
           for (long long j = 0; j < k1; j++) v = __dsub_rn(v, t1);
           R.d_ledger_val[s] = v;
         }
-        if (qover || q2n + k2 > w.qcap || q1n + k1 > w.qcap) qover = true;
-        else {
-          for (long long j = lane; j < k2; j += 32) w.q[q2n + j] = c2;
-          for (long long j = lane; j < k1; j += 32) w.q1[q1n + j] = c1;
-          q2n += k2; q1n += k1;
-        }
-        __syncwarp();
+        if (lane == k) { my_k2 = k2; my_k1 = k1; }
       }
-      __threadfence_block();
       int64_t nu = 0;
+      int32_t my_undo = 0;   // undo entry nu lives in lane nu (first 32), then in w.undo
       if (fail < 0) {
-        if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
+        long long tot = my_k2 + my_k1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (tot > w.qcap) fail = PARVA_DIAG_NEED_NEW_GPU;   // more GPCs than any map can free
         else {
-          for (int64_t base = 0; base < q2n + q1n && fail < 0; base += 32) {
-            const int64_t jl = base + lane;
-            const int my_cat = jl < q2n ? w.q[jl] : (jl < q2n + q1n ? w.q1[jl - q2n] : 0);
-            const int cnt = (int)min((int64_t)32, q2n + q1n - base);
-            for (int u = 0; u < cnt; u++) {
-              const int cat = __shfl_sync(0xffffffffu, my_cat, u);
-              const int c = base + u < q2n ? 1 : 0;   // t2 kinds are size 2, t1 kinds size 1
-              const int64_t g = S.first_fit(c, index, lane);
-              if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
-              const uint32_t m8 = S.M[g];
-              const int st = find_start(m8 & 0x7Fu, c);
-              const int ln = S.Ln[g];
-              if (lane == 0) {
-                S.M[g] = (uint8_t)(m8 | footprint(c, st));
-                S.Ln[g] = (uint8_t)(ln + 1);
-                w.lcat[g * 7 + ln] = cat;
-                w.lslot[g * 7 + ln] = (uint8_t)st;
-                w.undo[nu] = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
+          // proposals queue (allocator.py:403-405, drained by size): every size-2
+          // kind in drain order, then every size-1 kind
+          for (int c = 1; c >= 0 && fail < 0; c--) {
+            for (int k = 0; k < nl && fail < 0; k++) {
+              const long long cnt = __shfl_sync(0xffffffffu, c ? my_k2 : my_k1, k);
+              const int cat = __shfl_sync(0xffffffffu, c ? e_t2 : e_t1, k);
+              for (long long r = 0; r < cnt; r++) {
+                const int64_t g = S.first_fit(c, index, lane);
+                if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
+                const uint32_t m8 = S.M[g];
+                const int st = find_start(m8 & 0x7Fu, c);
+                const int ln = S.Ln[g];
+                const int32_t u = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
+                if (lane == 0) {
+                  S.M[g] = (uint8_t)(m8 | footprint(c, st));
+                  S.Ln[g] = (uint8_t)(ln + 1);
+                  w.lcat[g * 7 + ln] = cat;
+                  w.lslot[g * 7 + ln] = (uint8_t)st;
+                  if (nu >= 32) w.undo[nu] = u;
+                }
+                if (nu < 32 && lane == nu) my_undo = u;
+                __syncwarp();
+                nu++;
+                S.set_bits(g, lane);
               }
-              __syncwarp();
-              nu++;
-              S.set_bits(g, lane);
             }
           }
           if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
+            __threadfence_block();
             for (int64_t j = nu - 1; j >= 0; j--) {
-              const int32_t u = w.undo[j];
+              const int32_t u = j < 32 ? __shfl_sync(0xffffffffu, my_undo, (int)j) : w.undo[j];
               const int64_t g = u >> 4;
               const int c = (u >> 3) & 1, st = u & 7;
               if (lane == 0) {
@@ -640,20 +600,41 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
       if (tid == 0) R.d_pl_off[ng] = (int32_t)np;
     }
     __syncthreads();
-    // ---- coverage assert (allocator.py:437-442): service_throughput in map order
+    // ---- coverage assert (allocator.py:437-442): service_throughput in map
+    // order.  Parallel unordered sums first; any two summation orders of n
+    // positive terms differ by at most 2n*2^-53*sum, so only a service within
+    // that margin of its threshold is re-summed in map order (never seen).
     if (status == PARVA_OK && compact) {
-      for (int s = tid; s < P.n_services; s += blockDim.x) { w.after[s] = 0.0; w.seen[s] = 0; }
+      for (int s = tid; s < P.n_services; s += blockDim.x) { w.after[s] = 0.0; w.seen[s] = 0; w.svc_pos[s] = 0; }
       __syncthreads();
-      if (tid == 0) {
-        for (int64_t k = 0; k < np; k++) {
-          const int name = P.d_cat_name[R.d_pl_cat[k]];
-          if (name < P.n_services) { w.after[name] = __dadd_rn(w.after[name], P.d_cat_tp[R.d_pl_cat[k]]); w.seen[name] = 1; }
+      for (int64_t k = tid; k < np; k += blockDim.x) {
+        const CatExt X = w.ext[R.d_pl_cat[k]];
+        if (X.name < P.n_services) {
+          atomicAdd(&w.after[X.name], X.tp);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&w.svc_pos[X.name]), 1ull);
         }
       }
       __syncthreads();
-      for (int s = tid; s < P.n_services; s += blockDim.x)
-        if (P.d_svc_rate[s] > 0.0 && w.seen[s] && !(w.after[s] >= __dmul_rn(P.d_svc_rate[s], 1.0 - 1e-9)))
-          atomicExch(&s_status, PARVA_COVERAGE_ASSERT);
+      for (int s = tid; s < P.n_services; s += blockDim.x) {
+        const int64_t cnt = w.svc_pos[s];
+        if (!(P.d_svc_rate[s] > 0.0) || cnt == 0) continue;
+        const double thr = __dmul_rn(P.d_svc_rate[s], 1.0 - 1e-9);
+        const double sum = w.after[s];
+        const double err = (double)(2 * cnt + 2) * 1.1102230246251565e-16 * sum;
+        bool ok;
+        if (sum - err >= thr) ok = true;
+        else if (sum + err < thr) ok = false;
+        else {   // exact: the reference's left-to-right sum in map order
+          double e = 0.0;
+          bool first = true;
+          for (int64_t k = 0; k < np; k++) {
+            const CatExt X = w.ext[R.d_pl_cat[k]];
+            if (X.name == s) { e = first ? __dadd_rn(0.0, X.tp) : __dadd_rn(e, X.tp); first = false; }
+          }
+          ok = e >= thr;
+        }
+        if (!ok) atomicExch(&s_status, PARVA_COVERAGE_ASSERT);
+      }
       __syncthreads();
       if (s_status == PARVA_COVERAGE_ASSERT) status = PARVA_COVERAGE_ASSERT;
     }
@@ -668,7 +649,7 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
 }
 
 size_t general_workspace(const parva_general_problem* p, int64_t cap) {
-  return gen_layout(cap, cap * 7 + 8, p->n_services, nullptr, nullptr);
+  return gen_layout(cap, cap * 7 + 8, p->n_services, p->n_cat, nullptr, nullptr);
 }
 
 int launch_plan_general(const parva_general_problem* p, parva_general_result* r, void* ws, size_t ws_bytes,
@@ -682,7 +663,9 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    smem_max -= 2048;   // static shared memory of the kernel
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, plan_general_kernel);
+    smem_max -= (int)fa.sharedSizeBytes + 256;   // static shared memory of the kernel
     cudaFuncSetAttribute(plan_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
   }
   // largest G with 2 * pad16(G) + 40 * ceil(G / 64) <= smem_max
