@@ -178,9 +178,16 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # one process per GPU; PARVA_DIST_BACKEND=gloo lets the multi-rank path be
+    # smoke-tested with several ranks on one device (NCCL refuses that)
+    backend = os.environ.get("PARVA_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2409_14447_b200 import _native as N
     from paper_2409_14447_b200 import batch as B
