@@ -265,7 +265,7 @@ def main():
     # host blocks (inputs packed once by the producer, outside the timed loop);
     # every timed call copies the inputs in, plans, copies config + plan
     # records (freed_rate ledger included) out, and synchronizes.
-    pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=3)
+    pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=3, cfg_format=2, plan_bytes=64)
     for _ in range(args.warmup):
         pb.run(dt)
     if world > 1:
@@ -311,7 +311,8 @@ def main():
         "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": pb.h2d_bytes, "d2h_bytes_per_step": pb.d2h_bytes,
                 "api": "parva_plan_host_packed (C ABI, pinned host blocks, 3-chunk H2D/plan/D2H CUDA-graph "
-                       "pipeline; 16-B compact config + 128-B plan records incl. the freed_rate ledger)",
+                       "pipeline; 8-B config + 64-B plan records incl. the freed_rate ledger, full 128-B "
+                       "records of overflowing scenarios in a spill list)",
                 "plan_records_equal_device_path": e2e_parity},
         "parity_vs_oracle_first_2000": parity,
     }

@@ -53,7 +53,8 @@ enum parva_status {
   PARVA_CAPACITY = 4,              /* fast-path record limits exceeded: re-plan general */
   PARVA_BAD_INPUT = 5,
   PARVA_COVERAGE_ASSERT = 6,       /* optimize coverage assert (allocator.py:437-442)   */
-  PARVA_LAUNCH_ERROR = 7
+  PARVA_LAUNCH_ERROR = 7,
+  PARVA_SPILLED = 8                /* 64-byte record: full record is in the spill list */
 };
 
 /* diagnostic reasons (allocator.py:394,401,410-412,432-434) */
@@ -115,8 +116,20 @@ typedef struct {
   uint16_t count;
 } parva_config_compact;
 
+/* 8-byte tiny config record, for tables with at most 254 points per
+ * (table, size): best[c] = 255 if absent; opt_last = opt | last << 4 (15 =
+ * none); status_flags = status | 0x80 if count > 255 (count saturates at
+ * 255 -- more than 224 segments cannot fit the fast path anyway). */
+typedef struct {
+  uint8_t best[PARVA_NUM_SIZES];
+  uint8_t opt_last;
+  uint8_t status_flags;
+  uint8_t count;
+} parva_config_tiny;
+
 #define PARVA_CFG_FULL 0
 #define PARVA_CFG_COMPACT 1
+#define PARVA_CFG_TINY 2
 
 /* 128-byte per-scenario plan record (fast path: <=32 services, <=32 GPUs).
  * Header (8 B), then a packed 120-byte payload:
@@ -205,14 +218,22 @@ int parva_plan_host(const parva_tables* tables, const parva_index* index,
  * scenarios and m services is laid out (offsets from parva_packed_layout):
  *   input : int32 scen_off[k+1] (chunk-local, scen_off[0] = 0), f64 rate[m],
  *           f64 bound[m], uint16 table[m]
- *   output: parva_plan_record plan[k], config records[m] (cfg_format)
- * Blocks are padded to 256 bytes. */
+ *   output: plan records[k] (plan_bytes = 128, or 64 with a spill list),
+ *           config records[m] (cfg_format), then for 64-byte records
+ *           int32 spill_count (+pad to 16 B) and spill_cap entries of
+ *           {int32 scenario (chunk-local), int32 pad, parva_plan_record}.
+ * A 64-byte plan record is the 128-byte record truncated to 56 payload bytes;
+ * a scenario whose payload does not fit has status PARVA_SPILLED and its full
+ * record in the spill list (PARVA_CAPACITY if the list is full).  Blocks are
+ * padded to 256 bytes. */
 typedef struct {
   int64_t in_scen_off, in_rate, in_bound, in_table, in_bytes;
-  int64_t out_plan, out_cfg, out_bytes;
+  int64_t out_plan, out_cfg, out_spill, out_bytes;
+  int32_t plan_bytes, spill_cap;
 } parva_chunk_layout;
 
-int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, parva_chunk_layout* out);
+int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes,
+                        parva_chunk_layout* out);
 
 /* Plan a packed batch: chunk c has h_chunk_scen[c] scenarios and
  * h_chunk_svc[c] services, input block h_in[c], output block h_out[c] (host
@@ -220,13 +241,14 @@ int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, parva_chunk_la
  * cached CUDA graph; returns after `stream` has synchronized.  Scratch:
  * parva_plan_host_packed_scratch bytes of device memory. */
 size_t parva_plan_host_packed_scratch(int32_t n_chunks, const int32_t* h_chunk_scen,
-                                      const int32_t* h_chunk_svc, int32_t cfg_format);
+                                      const int32_t* h_chunk_svc, int32_t cfg_format,
+                                      int32_t plan_bytes);
 int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
                            int32_t n_chunks, const int32_t* h_chunk_scen,
                            const int32_t* h_chunk_svc, const void* const* h_in,
                            void* const* h_out, int32_t optimize, int32_t threshold,
-                           int32_t cfg_format, void* d_scratch, size_t scratch_bytes,
-                           void* stream);
+                           int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
+                           size_t scratch_bytes, void* stream);
 
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional

@@ -16,7 +16,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .records import CAPACITY, CFG_COMPACT, CFG_FULL, COMPACT_DTYPE, CONFIG_DTYPE, PLAN_DTYPE
+from .records import (CAPACITY, CFG_COMPACT, CFG_FULL, CFG_TINY, COMPACT_DTYPE, CONFIG_DTYPE, PLAN64_DTYPE, PLAN_DTYPE,
+                      SPILL_DTYPE, SPILLED, TINY_DTYPE)
 from .tables import PackedTables
 
 
@@ -240,7 +241,11 @@ def resolve_capacity(pt: PackedTables, scen_off, svc_table, cfg, plan, optimize=
 # ------------------------------------------------------------ packed host
 class ChunkLayout(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("in_scen_off", "in_rate", "in_bound", "in_table", "in_bytes",
-                                         "out_plan", "out_cfg", "out_bytes")]
+                                         "out_plan", "out_cfg", "out_spill", "out_bytes")] + \
+               [("plan_bytes", C.c_int32), ("spill_cap", C.c_int32)]
+
+
+_CFG_DT = {CFG_FULL: CONFIG_DTYPE, CFG_COMPACT: COMPACT_DTYPE, CFG_TINY: TINY_DTYPE}
 
 
 class PackedHostBatch:
@@ -253,13 +258,15 @@ class PackedHostBatch:
     once per batch by whoever produces the queries); `run` is the timed
     end-to-end call: copies in, plans, copies out, synchronizes."""
 
-    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, n_chunks: int = 2, cfg_format: int = CFG_COMPACT):
+    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, n_chunks: int = 2, cfg_format: int = CFG_COMPACT,
+                 plan_bytes: int = 128):
         torch = N.require_cuda()
         L = N.lib()
         scen_off = np.asarray(scen_off, dtype=np.int64)
         n = len(scen_off) - 1
         n_chunks = max(1, min(n_chunks, max(n, 1)))
         self.cfg_format = cfg_format
+        self.plan_bytes = plan_bytes
         self.bounds = [(n * c // n_chunks, n * (c + 1) // n_chunks) for c in range(n_chunks)]
         self.k = np.array([b - a for a, b in self.bounds], dtype=np.int32)
         self.m = np.array([scen_off[b] - scen_off[a] for a, b in self.bounds], dtype=np.int32)
@@ -267,7 +274,8 @@ class PackedHostBatch:
         for c, (a, b) in enumerate(self.bounds):
             lay = ChunkLayout()
             N.check(L.parva_packed_layout(C.c_int32(int(self.k[c])), C.c_int32(int(self.m[c])),
-                                          C.c_int32(cfg_format), C.byref(lay)), "parva_packed_layout")
+                                          C.c_int32(cfg_format), C.c_int32(plan_bytes), C.byref(lay)),
+                    "parva_packed_layout")
             self.layouts.append(lay)
             self.h_in.append(torch.zeros(lay.in_bytes, dtype=torch.uint8).pin_memory())
             self.h_out.append(torch.zeros(lay.out_bytes, dtype=torch.uint8).pin_memory())
@@ -278,7 +286,7 @@ class PackedHostBatch:
         self.k_c = (C.c_int32 * n_chunks)(*self.k.tolist())
         self.m_c = (C.c_int32 * n_chunks)(*self.m.tolist())
         self.scratch_bytes = int(L.parva_plan_host_packed_scratch(C.c_int32(n_chunks), self.k_c, self.m_c,
-                                                                 C.c_int32(cfg_format)))
+                                                                 C.c_int32(cfg_format), C.c_int32(plan_bytes)))
         self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda")
 
     def fill(self, scen_off, svc_table, svc_rate, svc_bound):
@@ -296,7 +304,8 @@ class PackedHostBatch:
         rc = N.lib().parva_plan_host_packed(
             C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(len(self.bounds)), self.k_c, self.m_c,
             self.in_ptrs, self.out_ptrs, C.c_int32(int(optimize)), C.c_int32(int(threshold)),
-            C.c_int32(self.cfg_format), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), N.stream_handle(stream))
+            C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes),
+            N.stream_handle(stream))
         N.check(rc, "parva_plan_host_packed")
 
     @property
@@ -307,12 +316,35 @@ class PackedHostBatch:
     def d2h_bytes(self) -> int:
         return int(sum(l.out_bytes for l in self.layouts))
 
-    def outputs(self):
-        """(config records, plan records) of the whole batch as numpy arrays."""
-        cdt = COMPACT_DTYPE if self.cfg_format == CFG_COMPACT else CONFIG_DTYPE
-        cfgs, plans = [], []
+    def raw_outputs(self):
+        """Per chunk: (config records, plan records as written, spill entries)."""
+        cdt = _CFG_DT[self.cfg_format]
+        pdt = PLAN64_DTYPE if self.plan_bytes == 64 else PLAN_DTYPE
+        out = []
         for c, lay in enumerate(self.layouts):
             buf = self.h_out[c].numpy()
-            plans.append(buf[lay.out_plan:lay.out_plan + 128 * int(self.k[c])].view(PLAN_DTYPE))
-            cfgs.append(buf[lay.out_cfg:lay.out_cfg + cdt.itemsize * int(self.m[c])].view(cdt))
+            k, m = int(self.k[c]), int(self.m[c])
+            plan = buf[lay.out_plan:lay.out_plan + self.plan_bytes * k].view(pdt)
+            cfg = buf[lay.out_cfg:lay.out_cfg + cdt.itemsize * m].view(cdt)
+            spills = np.zeros(0, dtype=SPILL_DTYPE)
+            if self.plan_bytes == 64:
+                cnt = int(buf[lay.out_spill:lay.out_spill + 4].view(np.int32)[0])
+                cnt = min(cnt, lay.spill_cap)
+                spills = buf[lay.out_spill + 16:lay.out_spill + 16 + SPILL_DTYPE.itemsize * cnt].view(SPILL_DTYPE)
+            out.append((cfg, plan, spills))
+        return out
+
+    def outputs(self):
+        """(config records, 128-byte plan records) of the whole batch; 64-byte
+        records are widened and spilled scenarios restored from the spill list."""
+        cfgs, plans = [], []
+        for cfg, plan, spills in self.raw_outputs():
+            if self.plan_bytes == 64:
+                wide = np.zeros(plan.shape[0], dtype=PLAN_DTYPE)
+                wide.view(np.uint8).reshape(-1, 128)[:, :64] = plan.view(np.uint8).reshape(-1, 64)
+                for e in spills:
+                    wide[int(e["scenario"])] = e["record"]
+                plan = wide
+            cfgs.append(cfg)
+            plans.append(plan)
         return np.concatenate(cfgs), np.concatenate(plans)

@@ -67,6 +67,10 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.cfg = d_cfg;
   A.cfg_format = cfg_format;
   A.plan = d_plan;
+  A.plan_bytes = 128;
+  A.spill_cap = 0;
+  A.spill_count = nullptr;
+  A.spill = nullptr;
   return parva::launch_plan_batch(A, stream);
 }
 
@@ -75,7 +79,7 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32
                      const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
                      int32_t cfg_format, parva_plan_record* d_plan, void* stream) {
   if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
-  if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
+  if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
                          optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream);
 }
@@ -212,6 +216,7 @@ int parva_plan_host(const parva_tables* tables, const parva_index* index, int32_
       A.svc_rate = d_rate; A.svc_bound = d_bound; A.optimize = optimize; A.threshold = threshold;
       A.cfg_given = 0; A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit; A.cfg = d_cfg;
       A.cfg_format = cfg_format; A.plan = d_plan + a;
+      A.plan_bytes = 128; A.spill_cap = 0; A.spill_count = nullptr; A.spill = nullptr;
       cudaGraphNode_t kn;
       if (parva::add_plan_batch_node(G->graph, A, in, 4, &kn) != PARVA_OK) return PARVA_LAUNCH_ERROR;
       for (int j = 4; j < 6; j++) {   // D2H after this chunk's plan and the previous chunk's D2H
@@ -245,32 +250,41 @@ int parva_plan_host(const parva_tables* tables, const parva_index* index, int32_
 // ------------------------------------------------------------ packed host
 static int64_t up256l(int64_t x) { return (x + 255) & ~int64_t(255); }
 
-int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, parva_chunk_layout* L) {
-  if (!L || k < 0 || m < 0) return PARVA_BAD_INPUT;
-  const int64_t cfg_sz = cfg_format == PARVA_CFG_COMPACT ? sizeof(parva_config_compact) : sizeof(parva_config_record);
+static int64_t cfg_bytes(int32_t cfg_format) {
+  return cfg_format == PARVA_CFG_TINY ? sizeof(parva_config_tiny)
+         : cfg_format == PARVA_CFG_COMPACT ? sizeof(parva_config_compact) : sizeof(parva_config_record);
+}
+
+int parva_packed_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes, parva_chunk_layout* L) {
+  if (!L || k < 0 || m < 0 || (plan_bytes != 64 && plan_bytes != 128)) return PARVA_BAD_INPUT;
+  if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
   L->in_scen_off = 0;
   L->in_rate = ((int64_t(k) + 1) * 4 + 15) & ~int64_t(15);
   L->in_bound = L->in_rate + int64_t(m) * 8;
   L->in_table = L->in_bound + int64_t(m) * 8;
   L->in_bytes = up256l(L->in_table + int64_t(m) * 2);
+  L->plan_bytes = plan_bytes;
+  L->spill_cap = plan_bytes == 64 ? 16 + k / 256 : 0;
   L->out_plan = 0;
-  L->out_cfg = int64_t(k) * sizeof(parva_plan_record);
-  L->out_bytes = up256l(L->out_cfg + int64_t(m) * cfg_sz);
+  L->out_cfg = int64_t(k) * plan_bytes;
+  L->out_spill = (L->out_cfg + int64_t(m) * cfg_bytes(cfg_format) + 15) & ~int64_t(15);
+  L->out_bytes = up256l(L->out_spill + (plan_bytes == 64 ? 16 + int64_t(L->spill_cap) * parva::kSpillEntry : 0));
   return PARVA_OK;
 }
 
-size_t parva_plan_host_packed_scratch(int32_t n_chunks, const int32_t* k, const int32_t* m, int32_t cfg_format) {
+size_t parva_plan_host_packed_scratch(int32_t n_chunks, const int32_t* k, const int32_t* m, int32_t cfg_format,
+                                      int32_t plan_bytes) {
   size_t total = 0;
   for (int c = 0; c < n_chunks; c++) {
     parva_chunk_layout L;
-    parva_packed_layout(k[c], m[c], cfg_format, &L);
+    if (parva_packed_layout(k[c], m[c], cfg_format, plan_bytes, &L) != PARVA_OK) return 0;
     total += size_t(L.in_bytes) + size_t(L.out_bytes);
   }
   return total + 256;
 }
 
 struct PackedGraph {
-  int dev = -1, n_chunks = 0, cfg_format = 0, optimize = 0, threshold = 0;
+  int dev = -1, n_chunks = 0, cfg_format = 0, plan_bytes = 0, optimize = 0, threshold = 0;
   std::vector<int32_t> k, m;
   const void* pts = nullptr;
   const void* idx = nullptr;
@@ -286,17 +300,18 @@ static std::vector<PackedGraph> g_packed;
 
 int parva_plan_host_packed(const parva_tables* tables, const parva_index* index, int32_t n_chunks,
                            const int32_t* h_k, const int32_t* h_m, const void* const* h_in, void* const* h_out,
-                           int32_t optimize, int32_t threshold, int32_t cfg_format, void* d_scratch,
-                           size_t scratch_bytes, void* stream) {
+                           int32_t optimize, int32_t threshold, int32_t cfg_format, int32_t plan_bytes,
+                           void* d_scratch, size_t scratch_bytes, void* stream) {
   if (!tables || !index || n_chunks <= 0) return PARVA_BAD_INPUT;
-  if (cfg_format != PARVA_CFG_FULL && cfg_format != PARVA_CFG_COMPACT) return PARVA_BAD_INPUT;
-  if (parva_plan_host_packed_scratch(n_chunks, h_k, h_m, cfg_format) > scratch_bytes) return PARVA_BAD_INPUT;
+  const size_t need = parva_plan_host_packed_scratch(n_chunks, h_k, h_m, cfg_format, plan_bytes);
+  if (need == 0 || need > scratch_bytes) return PARVA_BAD_INPUT;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(g_graph_mu);
   PackedGraph* G = nullptr;
   for (auto& e : g_packed)
-    if (e.dev == dev && e.n_chunks == n_chunks && e.cfg_format == cfg_format && e.optimize == optimize &&
+    if (e.dev == dev && e.n_chunks == n_chunks && e.cfg_format == cfg_format && e.plan_bytes == plan_bytes &&
+        e.optimize == optimize &&
         e.threshold == threshold && e.pts == tables->d_pts && e.idx == index->d_lat_sorted &&
         e.scratch == d_scratch && std::equal(e.k.begin(), e.k.end(), h_k) && std::equal(e.m.begin(), e.m.end(), h_m)) {
       G = &e;
@@ -308,7 +323,7 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
   {
     uint8_t* p = (uint8_t*)(((uintptr_t)d_scratch + 255) & ~uintptr_t(255));
     for (int c = 0; c < n_chunks; c++) {
-      parva_packed_layout(h_k[c], h_m[c], cfg_format, &L[c]);
+      parva_packed_layout(h_k[c], h_m[c], cfg_format, plan_bytes, &L[c]);
       d_in[c] = p; p += L[c].in_bytes;
       d_out[c] = p; p += L[c].out_bytes;
     }
@@ -324,7 +339,7 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
     }
     g_packed.emplace_back();
     G = &g_packed.back();
-    G->dev = dev; G->n_chunks = n_chunks; G->cfg_format = cfg_format; G->optimize = optimize;
+    G->dev = dev; G->n_chunks = n_chunks; G->cfg_format = cfg_format; G->plan_bytes = plan_bytes; G->optimize = optimize;
     G->threshold = threshold; G->k.assign(h_k, h_k + n_chunks); G->m.assign(h_m, h_m + n_chunks);
     G->pts = tables->d_pts; G->idx = index->d_lat_sorted; G->scratch = d_scratch;
     if (cudaGraphCreate(&G->graph, 0) != cudaSuccess) return PARVA_LAUNCH_ERROR;
@@ -334,6 +349,15 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
       cudaGraphNode_t* dep_in = c ? &G->in_nodes[c - 1] : nullptr;
       if (cudaGraphAddMemcpyNode1D(&G->in_nodes[c], G->graph, dep_in, c ? 1 : 0, d_in[c], h_in[c], L[c].in_bytes,
                                    cudaMemcpyHostToDevice) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+      cudaGraphNode_t pre = G->in_nodes[c];
+      if (plan_bytes == 64) {   // zero the spill count before the chunk's plan
+        cudaMemsetParams mp = {};
+        mp.dst = d_out[c] + L[c].out_spill;
+        mp.value = 0; mp.elementSize = 4; mp.width = 4; mp.height = 1; mp.pitch = 0;
+        cudaGraphNode_t ms;
+        if (cudaGraphAddMemsetNode(&ms, G->graph, &G->in_nodes[c], 1, &mp) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+        pre = ms;
+      }
       cudaGraphNode_t kn;
       if (h_k[c] > 0) {
         parva::PlanArgs A;
@@ -348,9 +372,12 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
         A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
         A.cfg = d_out[c] + L[c].out_cfg; A.cfg_format = cfg_format;
         A.plan = (parva_plan_record*)(d_out[c] + L[c].out_plan);
-        if (parva::add_plan_batch_node(G->graph, A, &G->in_nodes[c], 1, &kn) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+        A.plan_bytes = plan_bytes; A.spill_cap = L[c].spill_cap;
+        A.spill_count = (int32_t*)(d_out[c] + L[c].out_spill);
+        A.spill = d_out[c] + L[c].out_spill + 16;
+        if (parva::add_plan_batch_node(G->graph, A, &pre, 1, &kn) != PARVA_OK) return PARVA_LAUNCH_ERROR;
       } else {
-        kn = G->in_nodes[c];
+        kn = pre;
       }
       cudaGraphNode_t deps[2] = {kn, c ? G->out_nodes[c - 1] : nullptr};
       if (cudaGraphAddMemcpyNode1D(&G->out_nodes[c], G->graph, deps, c ? 2 : 1, h_out[c], d_out[c],

@@ -27,10 +27,16 @@ struct PlanArgs {
   int optimize, threshold;
   int cfg_given;                 // config records precomputed by K1
   int smem_index;                // index resident in shared memory
-  void* cfg;                     // parva_config_record[] or parva_config_compact[]
-  int cfg_format;                // PARVA_CFG_FULL / PARVA_CFG_COMPACT
-  parva_plan_record* plan;
+  void* cfg;                     // config records in cfg_format
+  int cfg_format;                // PARVA_CFG_FULL / _COMPACT / _TINY
+  parva_plan_record* plan;       // byte stride plan_bytes (128, or 64 + spill list)
+  int plan_bytes;
+  int spill_cap;
+  int32_t* spill_count;          // 64-byte records: spill list header
+  uint8_t* spill;                // spill_cap entries of kSpillEntry bytes
 };
+
+constexpr int kSpillEntry = 144;   // int32 scenario, 12 B pad, 128-byte record
 
 int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
                            const double* q_bound, parva_config_record* out, cudaStream_t stream);

@@ -172,7 +172,15 @@ __device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base
 }
 
 __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
-  if (A.cfg_format == PARVA_CFG_COMPACT) {
+  if (A.cfg_format == PARVA_CFG_TINY) {
+    parva_config_tiny k;
+#pragma unroll
+    for (int c = 0; c < 5; c++) k.best[c] = r.best[c] < 0 ? 255 : (uint8_t)r.best[c];
+    k.opt_last = (uint8_t)((r.opt_sc < 0 ? 15 : r.opt_sc) | (r.last_sc < 0 ? 15 : r.last_sc) << 4);
+    k.status_flags = (uint8_t)(r.status | (r.count > 255 ? 0x80 : 0));
+    k.count = (uint8_t)(r.count > 255 ? 255 : r.count);
+    reinterpret_cast<uint2*>(A.cfg)[i] = *reinterpret_cast<const uint2*>(&k);
+  } else if (A.cfg_format == PARVA_CFG_COMPACT) {
     parva_config_compact k;
 #pragma unroll
     for (int c = 0; c < 5; c++) k.best[c] = r.best[c];
@@ -234,7 +242,15 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
       if (lane < n) {
         const int i = a0 + lane;
         int16_t best[5];
-        if (A.cfg_format == PARVA_CFG_COMPACT) {
+        if (A.cfg_format == PARVA_CFG_TINY) {
+          const parva_config_tiny r = reinterpret_cast<const parva_config_tiny*>(A.cfg)[i];
+#pragma unroll
+          for (int c = 0; c < 5; c++) best[c] = r.best[c] == 255 ? -1 : (int16_t)r.best[c];
+          my_opt = (r.opt_last & 15) == 15 ? -1 : (r.opt_last & 15);
+          my_last = (r.opt_last >> 4) == 15 ? -1 : (r.opt_last >> 4);
+          my_count = (r.status_flags & 0x80) ? (long long)1 << 40 : r.count;   // saturated: cannot fit
+          st = r.status_flags & 0x7F;
+        } else if (A.cfg_format == PARVA_CFG_COMPACT) {
           const parva_config_compact r = reinterpret_cast<const parva_config_compact*>(A.cfg)[i];
 #pragma unroll
           for (int c = 0; c < 5; c++) best[c] = r.best[c];
@@ -260,6 +276,7 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
     __syncwarp();
 
     int status = PARVA_OK;
+    bool spill = false;
     if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
     else if (err_status) status = err_status;
     else {
@@ -417,9 +434,11 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
       const int n_final = __popc(__ballot_sync(0xffffffffu, good));
       const int n_led = __popc(__ballot_sync(0xffffffffu, lane < n && order > 0));
       const int led_off = (2 * (n_place + nd) + 7) & ~7;
-      if (led_off + 10 * n_led > PARVA_PLAN_PAYLOAD) {
+      const int need = led_off + 10 * n_led;
+      if (need > PARVA_PLAN_PAYLOAD) {
         status = PARVA_CAPACITY;
       } else {
+        spill = A.plan_bytes == 64 && need > 64 - 8;
         uint16_t* pay16 = reinterpret_cast<uint16_t*>(W.rec.payload);
         for (int j = 0; j < mine; j++) pay16[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
         if (lane < nd) pay16[n_place + lane] = W.diag[lane];
@@ -449,8 +468,23 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
       }
     }
     __syncwarp();
-    if (lane < 8)
-      reinterpret_cast<uint4*>(A.plan + k)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    uint8_t* dst = reinterpret_cast<uint8_t*>(A.plan) + (size_t)k * A.plan_bytes;
+    if (status == PARVA_OK && spill) {
+      // 64-byte records: the full record goes to the spill list
+      int slot = 0;
+      if (lane == 0) slot = atomicAdd(A.spill_count, 1);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (slot < A.spill_cap) {
+        uint8_t* e = A.spill + (size_t)slot * kSpillEntry;
+        if (lane == 0) *reinterpret_cast<int4*>(e) = make_int4(k, 0, 0, 0);
+        if (lane < 8) reinterpret_cast<uint4*>(e + 16)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+        if (lane < 4) reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_SPILLED, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+      } else if (lane < 4) {
+        reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_CAPACITY, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+      }
+    } else if (lane < A.plan_bytes / 16) {
+      reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    }
     __syncwarp();
   }
 }

@@ -17,11 +17,19 @@ PLAN_DTYPE = np.dtype([
     ("n_place", "u1"), ("n_diag", "u1"), ("n_ledger", "u1"), ("flags", "u1"),
     ("payload", "u1", (120,)),
 ])
+TINY_DTYPE = np.dtype([("best", "u1", (5,)), ("opt_last", "u1"), ("status_flags", "u1"), ("count", "u1")])
+PLAN64_DTYPE = np.dtype([
+    ("status", "u1"), ("err_service", "u1"), ("n_gpus", "u1"), ("n_gpus_unopt", "u1"),
+    ("n_place", "u1"), ("n_diag", "u1"), ("n_ledger", "u1"), ("flags", "u1"),
+    ("payload", "u1", (56,)),
+])
+SPILL_DTYPE = np.dtype([("scenario", "<i4"), ("pad", "<i4", (3,)), ("record", PLAN_DTYPE)])
 assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128 and COMPACT_DTYPE.itemsize == 16
-CFG_FULL, CFG_COMPACT = 0, 1
+assert TINY_DTYPE.itemsize == 8 and PLAN64_DTYPE.itemsize == 64 and SPILL_DTYPE.itemsize == 144
+CFG_FULL, CFG_COMPACT, CFG_TINY = 0, 1, 2
 
 # parva_status
-OK, INFEASIBLE_SLO, RESIDUAL_UNCOVERABLE, COUNT_OVERFLOW, CAPACITY, BAD_INPUT, COVERAGE_ASSERT, LAUNCH_ERROR = range(8)
+OK, INFEASIBLE_SLO, RESIDUAL_UNCOVERABLE, COUNT_OVERFLOW, CAPACITY, BAD_INPUT, COVERAGE_ASSERT, LAUNCH_ERROR, SPILLED = range(9)
 # parva_diag_reason
 DIAG_SMALL_UNAVAILABLE, DIAG_NEED_NEW_GPU, DIAG_UNKNOWN_SERVICE, DIAG_REGRESSED = range(4)
 FLAG_FALLBACK = 1
@@ -76,3 +84,59 @@ def format_diag(reason: int, gpu_id: int, name: str | None) -> str:
     else:
         raise ValueError(f"unknown diagnostic reason {reason}")
     return f"GPU {gpu_id}: optimization skipped: {failure}"
+
+
+def tiny_config(full: np.ndarray) -> np.ndarray:
+    """Full 32-byte config records -> 8-byte tiny records (parva_config_tiny)."""
+    out = np.zeros(full.shape[0], dtype=TINY_DTYPE)
+    out["best"] = np.where(full["best"] < 0, 255, full["best"]).astype(np.uint8)
+    opt = np.where(full["opt_sc"] < 0, 15, full["opt_sc"]).astype(np.uint8)
+    last = np.where(full["last_sc"] < 0, 15, full["last_sc"]).astype(np.uint8)
+    out["opt_last"] = opt | (last << 4)
+    sat = full["count"] > 255
+    out["status_flags"] = full["status"].astype(np.uint8) | np.where(sat, 0x80, 0).astype(np.uint8)
+    out["count"] = np.where(sat, 255, full["count"]).astype(np.uint8)
+    return out
+
+
+def expand_config(cfg: np.ndarray) -> np.ndarray:
+    """Any config record format -> COMPACT_DTYPE fields (best i16, opt/last, status, count)."""
+    if cfg.dtype == COMPACT_DTYPE:
+        return cfg
+    out = np.zeros(cfg.shape[0], dtype=COMPACT_DTYPE)
+    if cfg.dtype == TINY_DTYPE:
+        out["best"] = np.where(cfg["best"] == 255, -1, cfg["best"]).astype(np.int16)
+        o, l = cfg["opt_last"] & 15, cfg["opt_last"] >> 4
+        out["opt_sc"] = np.where(o == 15, -1, o).astype(np.int8)
+        out["last_sc"] = np.where(l == 15, -1, l).astype(np.int8)
+        out["status"] = cfg["status_flags"] & 0x7F
+        out["flags"] = (cfg["status_flags"] >> 7).astype(np.uint8)
+        out["count"] = cfg["count"]
+        return out
+    for f in ("best", "opt_sc", "last_sc", "status"):
+        out[f] = cfg[f]
+    out["count"] = np.minimum(cfg["count"], 65535)
+    out["flags"] = (cfg["count"] > 65535).astype(np.uint8)
+    return out
+
+
+def plan64_view(plan128: np.ndarray, spill_cap: int):
+    """Expected 64-byte records + spill list for given 128-byte records
+    (what parva_plan_host_packed returns with plan_bytes = 64)."""
+    p64 = np.zeros(plan128.shape[0], dtype=PLAN64_DTYPE)
+    raw = plan128.view(np.uint8).reshape(-1, 128)
+    p64.view(np.uint8).reshape(-1, 64)[:] = raw[:, :64]
+    spills = []
+    for k in range(plan128.shape[0]):
+        r = plan128[k]
+        if r["status"] != OK:
+            continue
+        need = ((2 * (int(r["n_place"]) + int(r["n_diag"])) + 7) & ~7) + 10 * int(r["n_ledger"])
+        if need > 56:
+            p64.view(np.uint8).reshape(-1, 64)[k] = 0
+            if len(spills) < spill_cap:
+                p64[k]["status"] = SPILLED
+                spills.append(k)
+            else:
+                p64[k]["status"] = CAPACITY
+    return p64, spills

@@ -301,13 +301,22 @@ def test_host_entry_packed_vs_oracle(fx):
     rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
     dt = N.device_tables_for(fx.tables)
     ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, rate, bound)
-    for chunks, fmt in ((1, 1), (3, 1), (3, 0), (4, 1)):
-        pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=chunks, cfg_format=fmt)
+    from paper_2409_14447_b200.records import tiny_config
+    conv = {0: lambda c: c, 1: compact_config, 2: tiny_config}
+    for chunks, fmt, pbytes in ((1, 1, 128), (3, 1, 128), (3, 0, 128), (4, 1, 128), (3, 2, 64), (1, 2, 64)):
+        pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=chunks, cfg_format=fmt, plan_bytes=pbytes)
         for _ in range(2):
             pb.run(dt)
             cfg, plan = pb.outputs()
             assert plan.tobytes() == oplan.tobytes()
-            assert cfg.tobytes() == (ocfg if fmt == 0 else compact_config(ocfg)).tobytes()
+            assert cfg.tobytes() == conv[fmt](ocfg).tobytes()
+            if pbytes == 64:   # the 64-byte records themselves, and the spill list as a set
+                from paper_2409_14447_b200.records import plan64_view
+                for c, (ccfg, p64, spills) in enumerate(pb.raw_outputs()):
+                    a, b = pb.bounds[c]
+                    exp64, exp_sp = plan64_view(oplan[a:b], pb.layouts[c].spill_cap)
+                    assert p64.tobytes() == exp64.tobytes()
+                    assert sorted(int(x) for x in spills["scenario"]) == exp_sp
 
 
 def test_reconfigure_service(fx):
