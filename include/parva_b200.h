@@ -81,6 +81,19 @@ typedef struct {
   int64_t n_points;
 } parva_tables;
 
+/* Raw (unprepared) tables, same grouping: every point of the source
+ * ProfileTable, with the fields the preparation predicates read. */
+typedef struct {
+  const double*  d_tp;
+  const double*  d_lat;
+  const double*  d_mem;       /* memory_required, GB   [n_points] */
+  const int32_t* d_procs;     /* process_count         [n_points] */
+  const int64_t* d_seg_start; /* [n_tables * 5]                    */
+  const int32_t* d_seg_count; /* [n_tables * 5]                    */
+  int32_t n_tables;
+  int64_t n_points;
+} parva_raw_tables;
+
 /* Latency-sorted prefix-argmax index over the same segments (same offsets).
  * lat_sorted[seg_start[s] + j] ascending; best[seg_start[s] + j] is the
  * within-segment position of the argmax of the first j+1 sorted points under
@@ -165,6 +178,17 @@ int parva_abi_version(void);
 
 /* Device bytes of workspace parva_plan_batch needs (0 today; reserved). */
 size_t parva_plan_batch_workspace(int32_t n_scenarios, int32_t n_services);
+
+/* prepare_tables (pipeline.py:70-80) on the device: filter_feasible
+ * (profiles.py:260-271, memory_required <= h_memcap5[size class]) and, if
+ * single_process, restrict(process_counts=(1,)) (profiles.py:115-129).
+ * Writes the prepared layout into caller-allocated device arrays (capacity
+ * raw->n_points; d_pts 2*n_points + 2 doubles), d_src = raw index of each
+ * kept point; *h_n_points = prepared count (synchronizes `stream`). */
+int parva_prepare_tables(const parva_raw_tables* raw, const double* h_memcap5,
+                         int32_t single_process, double* d_pts, int64_t* d_seg_start,
+                         int32_t* d_seg_count, int32_t* d_src, int64_t* h_n_points,
+                         void* stream);
 
 /* Build the prefix-argmax index of `tables` into `index` (both device). */
 int parva_build_index(const parva_tables* tables, parva_index* index, void* stream);

@@ -29,6 +29,12 @@ class ParvaTables(C.Structure):
                 ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32), ("n_points", C.c_int64)]
 
 
+class ParvaRawTables(C.Structure):
+    _fields_ = [("d_tp", C.c_void_p), ("d_lat", C.c_void_p), ("d_mem", C.c_void_p), ("d_procs", C.c_void_p),
+                ("d_seg_start", C.c_void_p), ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32),
+                ("n_points", C.c_int64)]
+
+
 class ParvaIndex(C.Structure):
     _fields_ = [("d_lat_sorted", C.c_void_p), ("d_best", C.c_void_p), ("d_tp", C.c_void_p)]
 
@@ -57,7 +63,7 @@ EXPORTS = (
     "parva_plan_batch", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
-    "parva_plan_host_packed_scratch", "parva_plan_host_packed",
+    "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
 )
 
 
@@ -145,7 +151,7 @@ class DeviceTables:
     """
 
     def __init__(self, packed, build_index: bool = True):
-        torch = require_cuda()
+        require_cuda()
         self.packed = packed
         inter = np.empty(2 * packed.n_points, dtype=np.float64)
         inter[0::2] = packed.tp
@@ -153,6 +159,44 @@ class DeviceTables:
         self.pts = to_device(inter, pad=2)
         self.seg_start = to_device(packed.seg_start.astype(np.int64))
         self.seg_count = to_device(packed.seg_count.astype(np.int32))
+        self._finish(build_index)
+
+    @classmethod
+    def prepare_on_device(cls, raw, memory_map=None, single_process: bool = False, build_index: bool = True):
+        """prepare_tables (pipeline.py:70-80) on the GPU from raw packed tables
+        (tables.pack_raw): memory filter + single-process restriction as kernel
+        predicates (csrc/prepare.cu)."""
+        from .profiles import check_memory_map
+        from .tables import PackedTables
+        torch = require_cuda()
+        mm = check_memory_map(memory_map)
+        caps = np.array([mm[s] for s in (1, 2, 3, 4, 7)], dtype=np.float64)
+        P = raw.n_points
+        d = [to_device(a) for a in (raw.tp, raw.lat, raw.mem, raw.procs.astype(np.int32),
+                                    raw.seg_start.astype(np.int64), raw.seg_count.astype(np.int32))] \
+            if P else None
+        self = cls.__new__(cls)
+        self.pts = torch.zeros(2 * max(P, 1) + 2, dtype=torch.float64, device="cuda")
+        self.seg_start = torch.zeros(max(raw.n_tables * 5, 1), dtype=torch.int64, device="cuda")
+        self.seg_count = torch.zeros(max(raw.n_tables * 5, 1), dtype=torch.int32, device="cuda")
+        src = torch.zeros(max(P, 1), dtype=torch.int32, device="cuda")
+        n_out = C.c_int64(0)
+        if P:
+            R = ParvaRawTables(*[t.data_ptr() for t in d], raw.n_tables, P)
+            check(lib().parva_prepare_tables(C.byref(R), caps.ctypes.data_as(C.c_void_p), C.c_int32(int(single_process)),
+                                             ptr(self.pts), ptr(self.seg_start), ptr(self.seg_count), ptr(src),
+                                             C.byref(n_out), stream_handle()), "parva_prepare_tables")
+        n = int(n_out.value)
+        idx = src[:n].cpu().numpy()
+        self.packed = PackedTables(names=list(raw.names), tp=raw.tp[idx], lat=raw.lat[idx], batch=raw.batch[idx],
+                                   procs=raw.procs[idx], seg_start=self.seg_start[:raw.n_tables * 5].cpu().numpy(),
+                                   seg_count=self.seg_count[:raw.n_tables * 5].cpu().numpy())
+        self._finish(build_index)
+        return self
+
+    def _finish(self, build_index: bool):
+        import torch
+        packed = self.packed
         self.struct = ParvaTables(self.pts.data_ptr(), self.seg_start.data_ptr(),
                                   self.seg_count.data_ptr(), packed.n_tables, packed.n_points)
         self.index = None
@@ -190,18 +234,28 @@ class _LRU:
 _TABLE_CACHE = _LRU(8)
 
 
+_RAW_CACHE = _LRU(8)
+
+
 def device_tables_for(tables, memory_map=None, single_process=False, prepared=False) -> DeviceTables:
-    """Cached DeviceTables for a {model: ProfileTable} mapping (or sequence)."""
-    from .tables import pack_tables
+    """Cached DeviceTables for a {model: ProfileTable} mapping (or sequence).
+
+    The raw points are packed once per table set; the preparation for given
+    options (memory map, single process) runs on the GPU (csrc/prepare.cu)."""
+    from .tables import pack_raw
     items = list(tables.items()) if hasattr(tables, "items") else [(t.model_id, t) for t in tables]
     mm = None if memory_map is None else tuple(sorted((int(k), float(v)) for k, v in dict(memory_map).items()))
-    key = (tuple((n, id(t)) for n, t in items), mm, bool(single_process), bool(prepared))
+    tkey = tuple((n, id(t)) for n, t in items)
+    key = (tkey, mm, bool(single_process), bool(prepared))
+
+    def make_raw():
+        return ([t for _, t in items], pack_raw(dict(items) if hasattr(tables, "items") else [t for _, t in items]))
 
     def make():
-        pt = pack_tables(dict(items) if hasattr(tables, "items") else [t for _, t in items],
-                         memory_map=memory_map, single_process=single_process, prepared=prepared)
-        # keep the table objects alive so their ids stay unique for the key
-        return ([t for _, t in items], DeviceTables(pt))
+        raw = _RAW_CACHE.get(tkey, make_raw)
+        if prepared:
+            return ([t for _, t in items], DeviceTables(raw))
+        return ([t for _, t in items], DeviceTables.prepare_on_device(raw, memory_map, single_process))
 
     return _TABLE_CACHE.get(key, make)
 

@@ -33,6 +33,7 @@ class PackedTables:
     procs: np.ndarray       # i32 [P]
     seg_start: np.ndarray   # i64 [T*5]
     seg_count: np.ndarray   # i32 [T*5]
+    mem: np.ndarray | None = None   # f64 [P] memory_required (raw tables only)
 
     @property
     def n_tables(self) -> int:
@@ -58,7 +59,7 @@ def pack_tables(tables: Mapping[str, ProfileTable] | Sequence[ProfileTable],
     else:
         items = [(t.model_id, t) for t in tables]
     mm = check_memory_map(memory_map)
-    tp, lat, batch, procs = [], [], [], []
+    tp, lat, batch, procs, mem = [], [], [], [], []
     seg_start = np.zeros(len(items) * 5, dtype=np.int64)
     seg_count = np.zeros(len(items) * 5, dtype=np.int32)
     pos = 0
@@ -78,12 +79,18 @@ def pack_tables(tables: Mapping[str, ProfileTable] | Sequence[ProfileTable],
             pos += len(pts)
             for p in pts:
                 tp.append(p.throughput); lat.append(p.latency)
-                batch.append(p.batch_size); procs.append(p.process_count)
+                batch.append(p.batch_size); procs.append(p.process_count); mem.append(p.memory_required)
     return PackedTables(
         names=[n for n, _ in items],
         tp=np.asarray(tp, dtype=np.float64), lat=np.asarray(lat, dtype=np.float64),
         batch=np.asarray(batch, dtype=np.int32), procs=np.asarray(procs, dtype=np.int32),
-        seg_start=seg_start, seg_count=seg_count)
+        seg_start=seg_start, seg_count=seg_count, mem=np.asarray(mem, dtype=np.float64))
+
+
+def pack_raw(tables) -> PackedTables:
+    """Every point of the tables, unfiltered, in the device grouping (input of
+    the device-side preparation, csrc/prepare.cu)."""
+    return pack_tables(tables, prepared=True)
 
 
 def pack_dense(dt) -> PackedTables:

@@ -335,3 +335,36 @@ def test_reconfigure_service(fx):
         except P.MigplanError as exc:
             got = canon.error(exc)
         assert got == c["result"], i
+
+
+def test_prepare_tables_on_device(fx):
+    """§8f row 2: filter_feasible + restrict as kernel predicates == the host
+    preparation (profiles.py:260-271, pipeline.py:70-80), including memory
+    values exactly at, just below and just above the caps."""
+    import math
+    import random
+    from paper_2409_14447_b200.tables import pack_raw
+    rng = random.Random(3)
+    caps = {1: 10.0, 2: 20.0, 3: 40.0, 4: 40.0, 7: 80.0}
+    rand_tables = []
+    for t in range(40):
+        pts = []
+        for s in (1, 2, 3, 4, 7):
+            for b in rng.sample(range(1, 65), rng.randint(0, 40)):
+                for p in rng.sample([1, 2, 3, 4], rng.randint(1, 4)):
+                    c = caps[s]
+                    mem = rng.choice([c, math.nextafter(c, 0), math.nextafter(c, 99), rng.uniform(0, 2 * c), 0.0])
+                    pts.append(P.ProfilePoint(f"r{t}", s, b, p, rng.uniform(1, 999), rng.uniform(1, 99), mem))
+        rand_tables.append(P.ProfileTable(f"r{t}", tuple(pts)))
+    cases = [(fx.tables, None, False), (fx.tables, None, True),
+             (fx.tables, {1: 5.0, 2: 10.0, 3: 20.0, 4: 20.0, 7: 40.0}, False),
+             (rand_tables, None, False), (rand_tables, None, True), (rand_tables, {1: 3, 2: 7, 3: 11, 4: 11, 7: 30}, True)]
+    for tables, mm, single in cases:
+        host = pack_tables(tables, memory_map=mm, single_process=single)
+        dev = N.DeviceTables.prepare_on_device(pack_raw(tables), mm, single)
+        hp = dev.packed
+        for f in ("tp", "lat", "batch", "procs", "seg_start", "seg_count"):
+            assert np.asarray(getattr(hp, f)).tobytes() == np.asarray(getattr(host, f)).astype(
+                np.asarray(getattr(hp, f)).dtype).tobytes(), f
+        pts = dev.pts[:2 * host.n_points].cpu().numpy()
+        assert pts[0::2].tobytes() == host.tp.tobytes() and pts[1::2].tobytes() == host.lat.tobytes()
