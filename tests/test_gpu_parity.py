@@ -368,3 +368,53 @@ def test_prepare_tables_on_device(fx):
                 np.asarray(getattr(hp, f)).dtype).tobytes(), f
         pts = dev.pts[:2 * host.n_points].cpu().numpy()
         assert pts[0::2].tobytes() == host.tp.tobytes() and pts[1::2].tobytes() == host.lat.tobytes()
+
+
+def test_broad_fuzz_vs_oracle(fx):
+    """Random scenario sizes (0..40 services, so empty scenarios and the
+    CAPACITY path included), random options; K2 records == oracle records and
+    the decoded objects == the oracle's plans (capacity scenarios through KG)."""
+    import random
+    from helpers import oracle_plan_canon
+    rng = random.Random(2024)
+    models = list(fx.models)
+    for trial in range(6):
+        opts = {"optimize": rng.random() < 0.8, "threshold": rng.choice([0, 2, 3, 4, 4, 5, 7]),
+                "single_process": rng.random() < 0.3}
+        mm = {1: 6.0, 2: 12.0, 3: 24.0, 4: 24.0, 7: 60.0} if rng.random() < 0.3 else None
+        pt = pack_tables(fx.tables, memory_map=mm, single_process=opts["single_process"])
+        dt = N.device_tables_for(fx.tables, mm, opts["single_process"])
+        n_scen = 3000
+        sizes = [rng.choice([0, 1, 2, 5, 11, 11, 11, 17, 25, 33, 40]) for _ in range(n_scen)]
+        tab, rate, bound, names = [], [], [], []
+        for k, sz in enumerate(sizes):
+            row = []
+            for j in range(sz):
+                m = rng.randrange(len(models))
+                r = 0.0 if rng.random() < 0.03 else math_exp(rng.uniform(1.0, 9.5))
+                slo = math_exp(rng.uniform(3.0, 8.0))
+                tab.append(m); rate.append(r); bound.append(slo / 2.0)
+                row.append([f"s{j}", models[m], r, slo])
+            names.append(row)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        tab = np.array(tab, dtype=np.int32)
+        res = B.plan_batch(dt, off, tab, np.array(rate), np.array(bound), optimize=opts["optimize"],
+                           threshold=opts["threshold"])
+        cfg, plan = res.host()
+        ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound, optimize=opts["optimize"],
+                                                threshold=opts["threshold"])
+        assert cfg.tobytes() == ocfg.tobytes(), trial
+        assert plan.tobytes() == oplan.tobytes(), trial
+        # objects, incl. CAPACITY scenarios re-planned by the general kernel
+        sets = [[P.make_service(a, m, r, s) for a, m, r, s in row] for row in names[:400]]
+        popts = P.PlanOptions(optimize=opts["optimize"], threshold=opts["threshold"],
+                              single_process=opts["single_process"], **({"memory_map": mm} if mm else {}))
+        got = P.plan_many(sets, fx.tables, popts)
+        for k in range(400):
+            exp = oracle_plan_canon(oracle, pt, names[k], opts)
+            assert _canon_result(got[k]) == exp, (trial, k)
+
+
+def math_exp(x):
+    import math
+    return math.exp(x)
