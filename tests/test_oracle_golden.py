@@ -232,3 +232,25 @@ def test_record_format_decodes_to_reference_plans(fx):
         except MigplanError as exc:
             got = canon.error(exc)
         assert canon.digest(got) == g["digests"][k], k
+
+
+def test_plan_metrics_from_records(fx):
+    """§8f row 3: fragmentation / allocated fraction from the plan records equal
+    the reference's summary() values on S1-S6 (evaluation.py:65-82)."""
+    from paper_2409_14447_b200.evaluation import plan_metrics
+    cases = [c for c in golden("fixture_plans.json") if c["options"] == "default"]
+    pt = pack_tables(fx.tables)
+    idx = pt.index_of()
+    off = [0]
+    tab, rate, bound = [], [], []
+    for c in cases:
+        for m, r, s in c["inputs"]:
+            tab.append(idx[m]); rate.append(r); bound.append(s / 2.0)
+        off.append(len(tab))
+    _, plan = oracle.plan_batch_records(pt, np.array(off), np.array(tab), np.array(rate), np.array(bound))
+    met = plan_metrics(plan)
+    for k, c in enumerate(cases):
+        assert met["gpu_count"][k] == c["summary"]["gpu_count"]
+        assert met["total_gpcs"][k] == c["summary"]["total_gpcs"]
+        assert met["allocated_fraction"][k] == c["summary"]["allocated_fraction"]
+        assert met["external_fragmentation"][k] == c["summary"]["external_fragmentation"]
