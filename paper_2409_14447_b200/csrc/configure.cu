@@ -263,16 +263,20 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
                            const double* q_rate, const double* q_bound,
                            parva_config_record* out, cudaStream_t stream) {
   if (nq <= 0) return PARVA_OK;
-  static int blocks_per_sm = -1, n_sm = 0;
+  // per-device launch configuration (attributes are per device context)
+  static int s_bps[kMaxDevices], s_nsm[kMaxDevices];
   const size_t smem = sizeof(SweepWarpSmem) * SW_WARPS;
-  if (blocks_per_sm < 0) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= kMaxDevices - 1;
+  if (!s_nsm[dev]) {
     cudaFuncSetAttribute(configure_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, configure_sweep_kernel, SW_THREADS, smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    cudaDeviceGetAttribute(&s_nsm[dev], cudaDevAttrMultiProcessorCount, dev);
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, configure_sweep_kernel, SW_THREADS, smem);
+    s_bps[dev] = bps < 1 ? 1 : bps;
   }
+  const int blocks_per_sm = s_bps[dev], n_sm = s_nsm[dev];
   int grid = n_sm * blocks_per_sm;
   const int need = (nq + SW_WARPS - 1) / SW_WARPS;
   if (grid > need) grid = need;

@@ -36,7 +36,8 @@ struct PlanArgs {
   uint8_t* spill;                // spill_cap entries of kSpillEntry bytes
 };
 
-constexpr int kSpillEntry = 144;   // int32 scenario, 12 B pad, 128-byte record
+constexpr int kSpillEntry = 144;
+constexpr int kMaxDevices = 64;    // per-device launch-configuration caches   // int32 scenario, 12 B pad, 128-byte record
 
 int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
                            const double* q_bound, parva_config_record* out, cudaStream_t stream);

@@ -507,29 +507,30 @@ struct LaunchCfg {
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const size_t smem_b = sizeof(WarpScratch) * PB_WARPS + index_smem_bytes(A.n_tables, A.n_points, A.smem_index, false);
   const size_t smem_a = index_smem_bytes(A.n_tables, A.n_points, A.smem_index, true);
-  static size_t conf_a = 0, conf_b = 0, occ_a = 0, occ_b = 0;
-  static int n_sm = 0, per_a = 0, per_b = 0;
-  if (smem_b > conf_b) {
+  // per-device caches: smem attribute set, occupancy for the smem size used
+  struct DevCfg { size_t conf_a, conf_b, occ_a, occ_b; int n_sm, per_a, per_b; };
+  static DevCfg s_cfg[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)];
+  if (smem_b > D.conf_b) {
     cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    conf_b = smem_b;
+    D.conf_b = smem_b;
   }
-  if (smem_a > conf_a) {
+  if (smem_a > D.conf_a) {
     cudaFuncSetAttribute(configure_services_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
-    conf_a = smem_a;
+    D.conf_a = smem_a;
   }
-  if (!n_sm) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (!D.n_sm) cudaDeviceGetAttribute(&D.n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (smem_b != D.occ_b) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per_b, plan_batch_kernel, PB_THREADS, smem_b);
+    D.occ_b = smem_b;
   }
-  if (smem_b != occ_b) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, plan_batch_kernel, PB_THREADS, smem_b);
-    occ_b = smem_b;
+  if (smem_a != D.occ_a) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per_a, configure_services_kernel, CF_THREADS, smem_a);
+    D.occ_a = smem_a;
   }
-  if (smem_a != occ_a) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_a, configure_services_kernel, CF_THREADS, smem_a);
-    occ_a = smem_a;
-  }
+  const int n_sm = D.n_sm, per_a = D.per_a, per_b = D.per_b;
   if (per_b < 1 || per_a < 1) return false;
   int gb = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
   if (gb > n_sm * per_b) gb = n_sm * per_b;

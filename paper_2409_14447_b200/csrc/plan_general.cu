@@ -658,10 +658,11 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
   if (general_workspace(p, cap) > ws_bytes) return PARVA_BAD_INPUT;
   gen_prepare_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
   // shared-memory state when it fits: 2 B per GPU + 5 bitmap bits per GPU
-  static int smem_max = 0;
+  static int s_smem[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& smem_max = s_smem[dev & (kMaxDevices - 1)];
   if (!smem_max) {
-    int dev;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, plan_general_kernel);
