@@ -193,6 +193,9 @@ __device__ inline bool propose_small_warp(double tp1, double tp2, double freed, 
   const double thr = __dmul_rn(1e-12, m);
   bool have = false;
   long long bg = 0, bc = 0, bn = 0;
+  // (gpcs, count, -k2) packs order-preserving into one u64 when every field
+  // fits 21 bits: key = gpcs << 42 | count << 21 | (2^21 - 1 - k2)
+  const bool packed = max_k2 < (1ll << 19);
   for (long long base = 0; base <= max_k2; base += 32) {
     const long long k2 = base + lane;
     bool ok = k2 <= max_k2;
@@ -206,13 +209,33 @@ __device__ inline bool propose_small_warp(double tp1, double tp2, double freed, 
         if (k1 < 1) k1 = 1;
       } else ok = false;
     }
-    long long g = ok ? 2 * k2 + k1 : LLONG_MAX, cn = ok ? k2 + k1 : LLONG_MAX, nk = ok ? -k2 : LLONG_MAX;
+    long long g, cn, nk;
+    // warp-uniform choice (the reductions are collective)
+    if (packed && __all_sync(0xffffffffu, !ok || 2 * k2 + k1 < (1ll << 21))) {
+      unsigned long long key = ok ? ((unsigned long long)(2 * k2 + k1) << 42) |
+                                        ((unsigned long long)(k2 + k1) << 21) |
+                                        (unsigned long long)((1ll << 21) - 1 - k2)
+                                  : ~0ull;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
-      const long long c2 = __shfl_xor_sync(0xffffffffu, cn, o);
-      const long long n2 = __shfl_xor_sync(0xffffffffu, nk, o);
-      if (g2 < g || (g2 == g && (c2 < cn || (c2 == cn && n2 < nk)))) { g = g2; cn = c2; nk = n2; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k = __shfl_xor_sync(0xffffffffu, key, o);
+        key = k < key ? k : key;
+      }
+      if (key == ~0ull) { g = cn = nk = LLONG_MAX; }
+      else {
+        g = (long long)(key >> 42);
+        cn = (long long)((key >> 21) & ((1ull << 21) - 1));
+        nk = (long long)(key & ((1ull << 21) - 1)) - ((1ll << 21) - 1);
+      }
+    } else {
+      g = ok ? 2 * k2 + k1 : LLONG_MAX; cn = ok ? k2 + k1 : LLONG_MAX; nk = ok ? -k2 : LLONG_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long g2 = __shfl_xor_sync(0xffffffffu, g, o);
+        const long long c2 = __shfl_xor_sync(0xffffffffu, cn, o);
+        const long long n2 = __shfl_xor_sync(0xffffffffu, nk, o);
+        if (g2 < g || (g2 == g && (c2 < cn || (c2 == cn && n2 < nk)))) { g = g2; cn = c2; nk = n2; }
+      }
     }
     if (g != LLONG_MAX && (!have || g < bg || (g == bg && (cn < bc || (cn == bc && nk < bn))))) {
       have = true; bg = g; bc = cn; bn = nk;
