@@ -201,6 +201,9 @@ constexpr int CF_THREADS = 256;
 __global__ void __launch_bounds__(CF_THREADS) configure_services_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __shared__ uint64_t bar;
+  // let K2b's CTAs be scheduled now: they load their index while we work and
+  // wait for our records at griddepcontrol.wait (programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const IndexView V = load_index(A, smem_raw, true, &bar);
   const int64_t lo = A.scen_off[0], hi = lo + A.n_svc;
   for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
@@ -223,6 +226,8 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   __shared__ uint64_t bar;
   const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS, false, &bar);
+  // config records come from K2a (launched before us with PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpScratch& W = scratch[warp];
@@ -547,9 +552,19 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.n_scen <= 0) return PARVA_OK;
   LaunchCfg L;
   if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
-  if (!A.cfg_given && A.n_svc > 0)
-    configure_services_kernel<<<L.grid_a, CF_THREADS, L.smem_a, stream>>>(A);
-  plan_batch_kernel<<<L.grid_b, PB_THREADS, L.smem_b, stream>>>(A);
+  const bool two = !A.cfg_given && A.n_svc > 0;
+  if (two) configure_services_kernel<<<L.grid_a, CF_THREADS, L.smem_a, stream>>>(A);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid_b);
+  cfg.blockDim = dim3(PB_THREADS);
+  cfg.dynamicSmemBytes = L.smem_b;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = two ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, plan_batch_kernel, A) != cudaSuccess) return PARVA_LAUNCH_ERROR;
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
