@@ -593,6 +593,14 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
   p.blockDim = dim3(PB_THREADS);
   p.sharedMemBytes = (unsigned)L.smem_b;
   p.kernelParams = args;
+  if (d != deps) {
+    // K2a -> K2b as a programmatic edge (PDL inside the graph)
+    if (cudaGraphAddKernelNode(node, g, nullptr, 0, &p) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    cudaGraphEdgeData ed = {};
+    ed.from_port = cudaGraphKernelNodePortProgrammatic;
+    ed.type = cudaGraphDependencyTypeProgrammatic;
+    return cudaGraphAddDependencies_v2(g, &na, node, &ed, 1) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+  }
   return cudaGraphAddKernelNode(node, g, d, nd, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
