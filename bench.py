@@ -302,9 +302,9 @@ def main():
                    "l2": "flushed between steps (512 MiB write, outside the events)",
                    "parallelism": f"scenario-sharded x{world}" + (" + NCCL all-gather of plan+config records" if world > 1 else ""),
                    "optimize": True, "threshold": 4},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": args.steps,
         "kernel_ms_per_step": kern_ms / args.steps,
-        "roofline": {"bound": "hbm", "kernel": "configure_services_kernel + plan_batch_kernel", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel (fused configure + relocate + optimize)", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},

@@ -274,6 +274,25 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
                            int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
                            size_t scratch_bytes, void* stream);
 
+/* Zero-copy host entry (one batch, one launch): the kernel reads the packed
+ * input block straight from pinned, mapped host memory and writes the
+ * records straight into the pinned, mapped output block, so the PCIe reads,
+ * the planning and the PCIe writes overlap inside one kernel (no staging
+ * copies).  Scenarios are planned in tiles taken in order from a device
+ * counter.  Layout from parva_mapped_layout: the input block is the packed
+ * chunk layout; the output block holds plan records[k], config records[m],
+ * and for 64-byte plan records an overflow area of k full 128-byte records
+ * (a scenario with status PARVA_SPILLED has its full record at index k).
+ * d_work: 16 bytes of device memory, zeroed once before first use; it is
+ * left zeroed after every call (one call at a time per d_work).
+ * Synchronizes `stream` before returning. */
+int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes,
+                        parva_chunk_layout* out);
+int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
+                           int32_t n_scenarios, int32_t n_services, const void* h_in,
+                           void* h_out, int32_t optimize, int32_t threshold,
+                           int32_t cfg_format, int32_t plan_bytes, void* d_work, void* stream);
+
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional
  * initial DeploymentMap and ledger.  Names (service ids) are indices

@@ -64,6 +64,7 @@ EXPORTS = (
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
+    "parva_mapped_layout", "parva_plan_host_mapped",
 )
 
 

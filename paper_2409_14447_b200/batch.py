@@ -348,3 +348,78 @@ class PackedHostBatch:
             cfgs.append(cfg)
             plans.append(plan)
         return np.concatenate(cfgs), np.concatenate(plans)
+
+
+# ------------------------------------------------------------ mapped host
+class MappedHostBatch:
+    """A batch for the zero-copy host entry parva_plan_host_mapped.
+
+    One pinned input block (the packed chunk layout: offsets, rates, bounds,
+    u16 table ids) and one pinned output block (plan records, config
+    records, and for 64-byte plan records an overflow area of full records).
+    The planning kernel reads the inputs over PCIe straight from the input
+    block and writes the records straight into the output block; `run` is
+    one launch plus a stream synchronize."""
+
+    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64):
+        torch = N.require_cuda()
+        L = N.lib()
+        scen_off = np.asarray(scen_off, dtype=np.int64)
+        self.n_scen, self.n_svc = len(scen_off) - 1, int(scen_off[-1] - scen_off[0])
+        self.cfg_format, self.plan_bytes = cfg_format, plan_bytes
+        self.layout = ChunkLayout()
+        N.check(L.parva_mapped_layout(C.c_int32(self.n_scen), C.c_int32(self.n_svc), C.c_int32(cfg_format),
+                                      C.c_int32(plan_bytes), C.byref(self.layout)), "parva_mapped_layout")
+        self.h_in = torch.zeros(self.layout.in_bytes, dtype=torch.uint8).pin_memory()
+        self.h_out = torch.zeros(self.layout.out_bytes, dtype=torch.uint8).pin_memory()
+        self.work = torch.zeros(4, dtype=torch.int32, device="cuda")   # zeroed once; kernels leave it zeroed
+        self.fill(scen_off, svc_table, svc_rate, svc_bound)
+
+    def fill(self, scen_off, svc_table, svc_rate, svc_bound):
+        lay, buf = self.layout, self.h_in.numpy()
+        scen_off = np.asarray(scen_off, dtype=np.int64)
+        sa, sb = int(scen_off[0]), int(scen_off[-1])
+        k, m = self.n_scen, sb - sa
+        buf[lay.in_scen_off:lay.in_scen_off + 4 * (k + 1)].view(np.int32)[:] = scen_off - sa
+        buf[lay.in_rate:lay.in_rate + 8 * m].view(np.float64)[:] = np.asarray(svc_rate)[sa:sb]
+        buf[lay.in_bound:lay.in_bound + 8 * m].view(np.float64)[:] = np.asarray(svc_bound)[sa:sb]
+        buf[lay.in_table:lay.in_table + 2 * m].view(np.uint16)[:] = np.asarray(svc_table)[sa:sb]
+
+    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
+        rc = N.lib().parva_plan_host_mapped(
+            C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
+            C.c_void_p(self.h_in.data_ptr()), C.c_void_p(self.h_out.data_ptr()), C.c_int32(int(optimize)),
+            C.c_int32(int(threshold)), C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes),
+            N.ptr(self.work), N.stream_handle(stream))
+        N.check(rc, "parva_plan_host_mapped")
+
+    @property
+    def h2d_bytes(self) -> int:
+        """Bytes the kernel reads from the host block per call (the packed inputs)."""
+        lay = self.layout
+        return int(lay.in_table + 2 * self.n_svc)
+
+    @property
+    def d2h_bytes(self) -> int:
+        """Bytes written into the host block per call (records; overflow records only when used)."""
+        lay = self.layout
+        return int(lay.out_cfg + _CFG_DT[self.cfg_format].itemsize * self.n_svc)
+
+    def outputs(self):
+        """(config records, 128-byte plan records); spilled scenarios are
+        restored from the overflow area."""
+        lay, buf = self.layout, self.h_out.numpy()
+        cdt = _CFG_DT[self.cfg_format]
+        pdt = PLAN64_DTYPE if self.plan_bytes == 64 else PLAN_DTYPE
+        k, m = self.n_scen, self.n_svc
+        plan = buf[lay.out_plan:lay.out_plan + self.plan_bytes * k].view(pdt)
+        cfg = buf[lay.out_cfg:lay.out_cfg + cdt.itemsize * m].view(cdt)
+        if self.plan_bytes == 64:
+            wide = np.zeros(k, dtype=PLAN_DTYPE)
+            wide.view(np.uint8).reshape(-1, 128)[:, :64] = plan.view(np.uint8).reshape(-1, 64)
+            sp = np.nonzero(plan["status"] == SPILLED)[0]
+            if len(sp):
+                full = buf[lay.out_spill:lay.out_spill + 128 * k].view(PLAN_DTYPE)
+                wide[sp] = full[sp]
+            plan = wide
+        return cfg.copy(), plan

@@ -10,7 +10,7 @@
 #include "parva_kernels.cuh"
 
 
-static constexpr size_t kSmemIndexLimit = 150 * 1024;  // index bytes kept in shared memory
+static constexpr size_t kSmemIndexLimit = 120 * 1024;  // index bytes kept in shared memory (K2 tiles use ~85 KB)
 
 extern "C" {
 
@@ -403,6 +403,77 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
   G->last_use = ++g_graph_clock;
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaGraphLaunch(G->exec, s) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+  return cudaStreamSynchronize(s) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+// ------------------------------------------------------------ mapped host
+int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes, parva_chunk_layout* L) {
+  const int rc = parva_packed_layout(k, m, cfg_format, plan_bytes, L);
+  if (rc != PARVA_OK) return rc;
+  // the overflow area holds one full record per scenario (no spill list)
+  L->spill_cap = plan_bytes == 64 ? k : 0;
+  L->out_bytes = up256l(L->out_spill + (plan_bytes == 64 ? int64_t(k) * 128 : 0));
+  return PARVA_OK;
+}
+
+static int tile_scen_for(int n_scen, int grid_cap) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("PARVA_TILE_SCEN");
+    env = e ? std::max(0, std::atoi(e)) : 0;
+  }
+  if (env > 0) return env;
+  // about four tiles per resident CTA, 8..64 scenarios each
+  const int t = n_scen / std::max(1, 4 * grid_cap);
+  return std::min(64, std::max(8, t));
+}
+
+int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                           int32_t n_services, const void* h_in, void* h_out, int32_t optimize, int32_t threshold,
+                           int32_t cfg_format, int32_t plan_bytes, void* d_work, void* stream) {
+  if (!tables || !index || !h_in || !h_out || !d_work || n_scenarios < 0 || n_services < 0) return PARVA_BAD_INPUT;
+  parva_chunk_layout L;
+  if (parva_mapped_layout(n_scenarios, n_services, cfg_format, plan_bytes, &L) != PARVA_OK) return PARVA_BAD_INPUT;
+  // pinned host blocks are mapped to device addresses; device blocks are used as they are
+  auto dev_ptr = [](const void* p, void** d) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) { *d = const_cast<void*>(p); return true; }
+    if (at.type != cudaMemoryTypeHost) return false;          // pageable memory cannot be mapped
+    if (cudaHostGetDevicePointer(d, const_cast<void*>(p), 0) != cudaSuccess) { cudaGetLastError(); return false; }
+    return true;
+  };
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  if (!dev_ptr(h_in, &d_in) || !dev_ptr(h_out, &d_out)) return PARVA_BAD_INPUT;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_scenarios > 0) {
+    uint8_t* in = (uint8_t*)d_in;
+    uint8_t* out = (uint8_t*)d_out;
+    parva::PlanArgs A;
+    A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
+    A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
+    A.n_points = tables->n_points; A.n_scen = n_scenarios; A.n_svc = n_services;
+    A.scen_off = (const int32_t*)(in + L.in_scen_off);
+    A.svc_table = nullptr; A.svc_table16 = (const uint16_t*)(in + L.in_table);
+    A.svc_rate = (const double*)(in + L.in_rate);
+    A.svc_bound = (const double*)(in + L.in_bound);
+    A.optimize = optimize; A.threshold = threshold; A.cfg_given = 0;
+    A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
+    A.cfg = out + L.out_cfg; A.cfg_format = cfg_format;
+    A.plan = (parva_plan_record*)(out + L.out_plan);
+    A.plan_bytes = plan_bytes; A.spill_cap = L.spill_cap;
+    A.spill_count = nullptr;
+    A.spill = out + L.out_spill;
+    A.spill_direct = 1;
+    A.work = (uint32_t*)d_work;
+    A.tile_scen = 1;
+    const int cap = parva::plan_batch_grid(A);
+    if (cap < 1) return PARVA_LAUNCH_ERROR;
+    A.tile_scen = tile_scen_for(n_scenarios, cap);
+    const int rc = parva::launch_plan_batch(A, s);
+    if (rc != PARVA_OK) return rc;
+  }
   return cudaStreamSynchronize(s) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 

@@ -98,50 +98,53 @@ constexpr double kCountLimit = 1099511627776.0;  // 2^40 segments per service
 
 // select_optimal_segment + match_demand (configurator.py:127-186) given the
 // per-size-class best throughputs (tp[c] > 0 iff size class c present).
-// Fills opt_sc, last_sc, count, coverage, status of a config record.
+// Fills opt_sc, last_sc, count, coverage, status of a config record.  Only
+// constant indices into tp[] (after unrolling), so it stays in registers.
 __device__ inline void match_demand(const double tp[5], double rate, parva_config_record& r) {
   int o = -1;
+  double topt = 0.0;
 #pragma unroll
   for (int c = 0; c < 5; c++) {
     if (!(tp[c] > 0.0)) continue;
-    if (o < 0) { o = c; continue; }
+    if (o < 0) { o = c; topt = tp[c]; continue; }
     // ascending size order: t.size > best.size always, so lhs >= rhs wins
-    double lhs = __dmul_rn(tp[c], (double)size_of_class(o));
-    double rhs = __dmul_rn(tp[o], (double)size_of_class(c));
-    if (lhs > rhs || lhs == rhs) o = c;
+    const double lhs = __dmul_rn(tp[c], (double)size_of_class(o));
+    const double rhs = __dmul_rn(topt, (double)size_of_class(c));
+    if (lhs > rhs || lhs == rhs) { o = c; topt = tp[c]; }
   }
   r.opt_sc = (int8_t)o;
   r.last_sc = -1;
   r.count = 0;
   r.coverage = 0.0;
   if (o < 0) { r.status = PARVA_INFEASIBLE_SLO; r.opt_sc = -1; return; }
-  double topt = tp[o];
   long long count = 0;
   if (rate > 0.0) {
-    double q = floor(__ddiv_rn(rate, topt));
+    const double q = floor(__ddiv_rn(rate, topt));
     if (!(q <= kCountLimit)) { r.status = PARVA_COUNT_OVERFLOW; return; }
     count = (long long)q;
   }
   double remaining = __dsub_rn(rate, __dmul_rn((double)count, topt));
-  double m = (1.0 > rate) ? 1.0 : rate;
+  const double m = (1.0 > rate) ? 1.0 : rate;
   if (remaining <= __dmul_rn(1e-9, m)) remaining = 0.0;
   int last = -1;
+  double tlast = 0.0;
   if (remaining > 0.0) {
 #pragma unroll
     for (int c = 0; c < 5; c++)
-      if (last < 0 && tp[c] > 0.0 && tp[c] >= remaining) last = c;
+      if (last < 0 && tp[c] > 0.0 && tp[c] >= remaining) { last = c; tlast = tp[c]; }
     if (last < 0) {  // configurator.py:166-176 (unreachable in practice)
       int fb = -1;
+      double tfb = 0.0;
 #pragma unroll
       for (int c = 0; c < 5; c++)
-        if (tp[c] > 0.0 && (fb < 0 || tp[c] > tp[fb])) fb = c;
-      if (tp[fb] >= remaining) last = fb;
+        if (tp[c] > 0.0 && (fb < 0 || tp[c] > tfb)) { fb = c; tfb = tp[c]; }
+      if (tfb >= remaining) { last = fb; tlast = tfb; }
       else { r.status = PARVA_RESIDUAL_UNCOVERABLE; return; }
     }
   }
   r.last_sc = (int8_t)last;
   r.count = count;
-  r.coverage = coverage_sum(topt, count, last >= 0, last >= 0 ? tp[last] : 0.0);
+  r.coverage = coverage_sum(topt, count, last >= 0, tlast);
   r.status = PARVA_OK;
 }
 

@@ -34,6 +34,12 @@ struct PlanArgs {
   int spill_cap;
   int32_t* spill_count;          // 64-byte records: spill list header
   uint8_t* spill;                // spill_cap entries of kSpillEntry bytes
+  // streamed mode (zero-copy host entry): CTAs take tiles of tile_scen
+  // scenarios from work[0]; work[1] counts finished CTAs (the last one
+  // resets both, so the counters are zero between launches)
+  uint32_t* work = nullptr;
+  int tile_scen = 0;
+  int spill_direct = 0;          // 64-byte records: full record at spill + 128 * scenario
 };
 
 constexpr int kSpillEntry = 144;
@@ -43,6 +49,7 @@ int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table
                            const double* q_bound, parva_config_record* out, cudaStream_t stream);
 int launch_build_index(const parva_tables* t, parva_index* idx, int* d_err, cudaStream_t stream);
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream);
+int plan_batch_grid(const PlanArgs& A);
 int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t* deps, size_t ndeps,
                         cudaGraphNode_t* node);
 size_t general_workspace(const parva_general_problem* p, int64_t cap);

@@ -27,8 +27,7 @@ constexpr int PB_WARPS = 16;
 constexpr int PB_THREADS = PB_WARPS * 32;
 constexpr int QCAP = 224;                 // > 31 GPUs x 7 slots: longer queues cannot fit
 
-struct WarpScratch {
-  double cat_tp[32 * 5];                  // best tp per (service, size class); 0 = absent
+struct alignas(16) WarpScratch {
   uint16_t lst[32][8];                    // per GPU placement list: cat << 3 | slot
   uint16_t bak[32][8];                    // relocation result (regression fallback)
   uint8_t q2[QCAP];
@@ -90,36 +89,91 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
   if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
 }
 
-// one relocation size class (allocator.py:284-289): services in input order,
-// opt copies then last; c is a compile-time constant in each instantiation
+// Greedy capacity of a GPU (slot mask m) for size class c: how many
+// segments repeated find_start + place accept (mig.py:114-149).  The
+// preference-ordered footprints of one class are disjoint, so it is a count.
+__device__ __forceinline__ int class_capacity(uint32_t m, int c) {
+  switch (c) {
+    case 4: return m == 0;
+    case 3: return (m & 0x0Fu) == 0;
+    case 2: return ((m & 0x70u) == 0) + ((m & 0x0Fu) == 0);
+    case 1: return ((m & 0x03u) == 0) + ((m & 0x0Cu) == 0) + ((m & 0x30u) == 0);
+    default: return __popc(~m & 0x7Fu);
+  }
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// One relocation size class (allocator.py:284-289 queue order: services in
+// input order, opt copies then last; c is a compile-time constant).
+// First-fit within one class fills GPUs strictly in list order: a placement
+// changes only its own GPU, so the first accepting GPU keeps accepting until
+// it is full, and a new GPU is appended only when none accepts
+// (allocator.py:194-251, 280-281).  GPU g (lane g; lanes >= ngpus are the
+// GPUs that would be appended, mask 0) therefore takes queue items
+// [C_g - cap_g, min(C_g, R)), C = inclusive prefix of capacities -- the same
+// placements, in the same per-GPU list order, as R sequential first-fits.
+// The queue is walked service by service (warp-uniform); each lane places
+// its share of the service's items.  For the first three classes the
+// capacity prefix has a closed form: relocation starts from an empty map,
+// so when size 4 is queued every existing GPU holds one size-7 segment, and
+// when size 3 is queued the n7 first GPUs are full and the rest hold 4@0.
 template <int c>
 __device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, int my_opt, long long my_count,
                                                int my_last, uint32_t& mask, int& ngpc, int& len, int& ngpus,
-                                               int& status) {
+                                               int& n7, int& status) {
+  // total segments <= 224 was checked, so per-service counts fit an int
   const int my_reps = lane < n ? (my_opt == c ? (int)my_count : 0) + (my_last == c ? 1 : 0) : 0;
   unsigned pending = __ballot_sync(0xffffffffu, my_reps > 0);
-  while (pending && status == PARVA_OK) {
+  if (!pending) return;
+  int cap, incl;
+  if (c == 4) {                      // empty map
+    cap = 1; incl = lane + 1;
+  } else if (c == 3) {               // GPUs [0, ngpus) full
+    cap = lane >= ngpus; incl = max(0, lane + 1 - ngpus);
+  } else if (c == 2) {               // [0, n7) full, [n7, ngpus) hold 4@0 (slot 4 free), then empty
+    cap = lane < n7 ? 0 : lane < ngpus ? 1 : 2;
+    incl = lane < n7 ? 0 : lane < ngpus ? lane + 1 - n7 : ngpus - n7 + 2 * (lane + 1 - ngpus);
+  } else {
+    cap = class_capacity(mask, c);
+    incl = warp_incl_scan(cap, lane);
+  }
+  const int excl = incl - cap;
+  int e = 0;                         // queue position of the current service's first item
+  do {
     const int s = __ffs(pending) - 1;
     pending &= pending - 1;
     const int reps = __shfl_sync(0xffffffffu, my_reps, s);
+    const int hi = min(incl, e + reps);
     const uint16_t cat3 = (uint16_t)((s * 5 + c) << 3);
-    for (int r = 0; r < reps; r++) {
-      int st = lane < ngpus ? find_start(mask, c) : -1;
-      const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
-      int g;
-      if (b) g = __ffs(b) - 1;
-      else {
-        if (ngpus >= PARVA_PLAN_MAX_GPUS) { status = PARVA_CAPACITY; break; }
-        g = ngpus++;
-        st = find_start(0u, c);
+    int j = max(excl, e);
+    if (c >= 3) {                    // capacity 1: at most one item per GPU
+      if (j < hi) {
+        mask |= footprint(c, 0);
+        ngpc += size_of_class(c);
+        W.lst[lane][len++] = cat3;
       }
-      if (lane == g) {
+    } else {
+#pragma unroll 1
+      for (; j < hi; j++) {
+        const int st = find_start(mask, c);
         mask |= footprint(c, st);
         ngpc += size_of_class(c);
-        W.lst[g][len++] = (uint16_t)(cat3 | st);
+        W.lst[lane][len++] = (uint16_t)(cat3 | st);
       }
     }
-  }
+    e += reps;
+  } while (pending);
+  if (e > __shfl_sync(0xffffffffu, incl, 31)) { status = PARVA_CAPACITY; return; }  // needs GPU index >= 32
+  ngpus = max(ngpus, 32 - __clz(__ballot_sync(0xffffffffu, excl < e && cap > 0)));
+  if (c == 4) n7 = ngpus;
 }
 
 // Index view: segment tables always in shared memory; latency-sorted
@@ -171,327 +225,472 @@ __device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base
   return V;
 }
 
+// config record store, words assembled in registers (no local copy)
 __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
+  const uint32_t b01 = (uint16_t)r.best[0] | (uint32_t)(uint16_t)r.best[1] << 16;
+  const uint32_t b23 = (uint16_t)r.best[2] | (uint32_t)(uint16_t)r.best[3] << 16;
+  const uint32_t b4ol = (uint16_t)r.best[4] | (uint32_t)(uint8_t)r.opt_sc << 16 | (uint32_t)(uint8_t)r.last_sc << 24;
   if (A.cfg_format == PARVA_CFG_TINY) {
-    parva_config_tiny k;
+    uint32_t lo = 0, hi = 0;
 #pragma unroll
-    for (int c = 0; c < 5; c++) k.best[c] = r.best[c] < 0 ? 255 : (uint8_t)r.best[c];
-    k.opt_last = (uint8_t)((r.opt_sc < 0 ? 15 : r.opt_sc) | (r.last_sc < 0 ? 15 : r.last_sc) << 4);
-    k.status_flags = (uint8_t)(r.status | (r.count > 255 ? 0x80 : 0));
-    k.count = (uint8_t)(r.count > 255 ? 255 : r.count);
-    reinterpret_cast<uint2*>(A.cfg)[i] = *reinterpret_cast<const uint2*>(&k);
+    for (int c = 0; c < 4; c++) lo |= (uint32_t)(r.best[c] < 0 ? 255 : (uint8_t)r.best[c]) << (8 * c);
+    const uint32_t ol = (uint32_t)((r.opt_sc < 0 ? 15 : r.opt_sc) | (r.last_sc < 0 ? 15 : r.last_sc) << 4);
+    const uint32_t sf = (uint32_t)(r.status | (r.count > 255 ? 0x80 : 0));
+    const uint32_t cn = (uint32_t)(r.count > 255 ? 255 : r.count);
+    hi = (uint32_t)(r.best[4] < 0 ? 255 : (uint8_t)r.best[4]) | ol << 8 | sf << 16 | cn << 24;
+    reinterpret_cast<uint2*>(A.cfg)[i] = make_uint2(lo, hi);
   } else if (A.cfg_format == PARVA_CFG_COMPACT) {
-    parva_config_compact k;
-#pragma unroll
-    for (int c = 0; c < 5; c++) k.best[c] = r.best[c];
-    k.opt_sc = r.opt_sc; k.last_sc = r.last_sc; k.status = r.status;
-    k.flags = r.count > 65535 ? 1 : 0;
-    k.count = (uint16_t)(r.count > 65535 ? 65535 : r.count);
-    reinterpret_cast<uint4*>(A.cfg)[i] = *reinterpret_cast<const uint4*>(&k);
+    const uint32_t w3 = (uint32_t)r.status | (uint32_t)(r.count > 65535 ? 1 : 0) << 8 |
+                        (uint32_t)(r.count > 65535 ? 65535 : r.count) << 16;
+    reinterpret_cast<uint4*>(A.cfg)[i] = make_uint4(b01, b23, b4ol, w3);
   } else {
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(A.cfg) + i);
-    dst[0] = reinterpret_cast<const uint4*>(&r)[0];
-    dst[1] = reinterpret_cast<const uint4*>(&r)[1];
+    const unsigned long long cbits = (unsigned long long)r.count;
+    const unsigned long long vbits = (unsigned long long)__double_as_longlong(r.coverage);
+    dst[0] = make_uint4(b01, b23, b4ol, (uint32_t)r.status | (uint32_t)r.flags << 8);
+    dst[1] = make_uint4((uint32_t)cbits, (uint32_t)(cbits >> 32), (uint32_t)vbits, (uint32_t)(vbits >> 32));
   }
 }
 
-// K2a: configure_service for every service of the batch, one thread each
-// (configurator.py:189-191 via the prefix-argmax index).
-constexpr int CF_THREADS = 256;
-__global__ void __launch_bounds__(CF_THREADS) configure_services_kernel(PlanArgs A) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  __shared__ uint64_t bar;
-  // let K2b's CTAs be scheduled now: they load their index while we work and
-  // wait for our records at griddepcontrol.wait (programmatic dependent launch)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const IndexView V = load_index(A, smem_raw, true, &bar);
-  const int64_t lo = A.scen_off[0], hi = lo + A.n_svc;
-  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x) {
+// ------------------------------------------------------------------ K2
+// One kernel, tile by tile.  A CTA owns a contiguous block of scenarios and
+// walks it in tiles of at most kTileSvc services: all threads configure the
+// tile's services (thread per service, configurator.py:189-191 through the
+// prefix-argmax index in shared memory), the per-service results stay in
+// shared memory, then the CTA's warps plan the tile's scenarios (warp per
+// scenario, taken from a shared counter so that uneven scenarios balance
+// inside the CTA).
+constexpr int kTileSvc = 1024;
+
+#ifdef PARVA_PHASE_TIMING
+// development probe (tools/k2_probe.py): per-CTA phase timestamps and per-warp
+// finish times / scenario counts; not built into the product library
+__device__ unsigned long long g_phase[1024][4];
+__device__ unsigned long long g_warp_end[1024][PB_WARPS][2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PHASE(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_phase[blockIdx.x][i] = gtimer(); } while (0)
+__device__ unsigned long long g_warp_cyc[1024][PB_WARPS][4];
+#define WCYC_START long long wc_t = clock64();
+#define WCYC(i) do { const long long wc_n = clock64(); \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) g_warp_cyc[blockIdx.x][threadIdx.x >> 5][i] += wc_n - wc_t; \
+    wc_t = wc_n; } while (0)
+#else
+#define PHASE(i) do { } while (0)
+#define WCYC_START
+#define WCYC(i) do { } while (0)
+#endif
+
+struct alignas(16) TileSmem {
+  double tp[kTileSvc * 5];                // best tp per (tile service, size class); 0 = absent
+  uint64_t meta[kTileSvc];                // count | opt << 48 | last << 52 | status << 56 (15 = none)
+  int32_t off[PB_THREADS + 1];            // tile scenario offsets (absolute service index)
+  int32_t next;                           // next tile scenario to plan
+  int32_t tile;                           // streamed mode: tile taken from the device counter
+};
+
+__device__ __forceinline__ uint64_t pack_meta(int opt, int last, int status, long long count) {
+  const uint64_t c = (uint64_t)(count < 0 ? 0 : count > (1ll << 40) ? (1ll << 40) : count);
+  return c | (uint64_t)(opt < 0 ? 15 : opt) << 48 | (uint64_t)(last < 0 ? 15 : last) << 52 |
+         (uint64_t)(status & 0xFF) << 56;
+}
+
+// configure (or load the given config record of) absolute service i; returns
+// the per-size-class tp (0 = absent) and the packed meta word
+__device__ __forceinline__ uint64_t tile_service(const PlanArgs& A, const IndexView& V, int64_t i, double tpc[5]) {
+  const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
+  const bool bad_t = t < 0 || t >= A.n_tables;
+  if (!A.cfg_given) {
     parva_config_record r = {};
-    double tpc[5];
-    const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
-    if (t < 0 || t >= A.n_tables) {
-      for (int c = 0; c < 5; c++) r.best[c] = -1;
+    if (bad_t) {
+#pragma unroll
+      for (int c = 0; c < 5; c++) { r.best[c] = -1; tpc[c] = 0.0; }
       r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
     } else {
       configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, A.svc_bound[i], A.svc_rate[i], r, tpc);
     }
     store_config(A, i, r);
+    return pack_meta(r.opt_sc, r.last_sc, r.status, r.count);
   }
+  // preconfigured (K1 sweep records)
+  int16_t best[5];
+  int opt, last, st;
+  long long count;
+  if (A.cfg_format == PARVA_CFG_TINY) {
+    const parva_config_tiny r = reinterpret_cast<const parva_config_tiny*>(A.cfg)[i];
+#pragma unroll
+    for (int c = 0; c < 5; c++) best[c] = r.best[c] == 255 ? -1 : (int16_t)r.best[c];
+    opt = (r.opt_last & 15) == 15 ? -1 : (r.opt_last & 15);
+    last = (r.opt_last >> 4) == 15 ? -1 : (r.opt_last >> 4);
+    count = (r.status_flags & 0x80) ? (long long)1 << 40 : r.count;   // saturated: cannot fit
+    st = r.status_flags & 0x7F;
+  } else if (A.cfg_format == PARVA_CFG_COMPACT) {
+    const parva_config_compact r = reinterpret_cast<const parva_config_compact*>(A.cfg)[i];
+#pragma unroll
+    for (int c = 0; c < 5; c++) best[c] = r.best[c];
+    opt = r.opt_sc; last = r.last_sc; count = r.count; st = r.status;
+  } else {
+    const parva_config_record r = reinterpret_cast<const parva_config_record*>(A.cfg)[i];
+#pragma unroll
+    for (int c = 0; c < 5; c++) best[c] = r.best[c];
+    opt = r.opt_sc; last = r.last_sc; count = r.count; st = r.status;
+  }
+#pragma unroll
+  for (int c = 0; c < 5; c++)
+    tpc[c] = (!bad_t && st != PARVA_BAD_INPUT && best[c] >= 0) ? V.tp[(V.seg_s[t * 5 + c] + best[c]) * V.tp_stride]
+                                                               : 0.0;
+  return pack_meta(opt, last, st, count);
 }
 
-// K2b: relocate + optimize, one warp per scenario, from the config records.
+// relocate + optimize + emit for scenario k (scenario-local services [0, n),
+// their tile results at cat_tp / meta); one warp.
+__device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratch& W, int k, int n,
+                                                   const double* cat_tp, const uint64_t* meta, bool in_tile,
+                                                   int lane) {
+  WCYC_START
+  reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
+
+  // ------------------------------------------------ configured services
+  int err_status = 0, err_svc = 0;
+  int my_opt = -1, my_last = -1;
+  long long my_count = 0;
+  if (n <= PARVA_PLAN_MAX_SERVICES && in_tile) {
+    int st = PARVA_OK;
+    if (lane < n) {
+      const uint64_t m = meta[lane];
+      my_count = (long long)(m & ((1ull << 48) - 1));
+      my_opt = (int)(m >> 48 & 15); if (my_opt == 15) my_opt = -1;
+      my_last = (int)(m >> 52 & 15); if (my_last == 15) my_last = -1;
+      st = (int)(m >> 56);
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, lane < n && st != PARVA_OK);
+    if (bad) {
+      err_svc = __ffs(bad) - 1;
+      err_status = __shfl_sync(0xffffffffu, st, err_svc);
+    }
+  }
+
+  int status = PARVA_OK;
+  bool spill = false;
+  if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
+  else if (!in_tile) status = PARVA_BAD_INPUT;
+  else if (err_status) status = err_status;
+  else {
+    const long long segs = warp_sum_ll(lane < n ? my_count + (my_last >= 0) : 0);
+    if (segs > 32 * 7) status = PARVA_CAPACITY;
+  }
+
+  // per-lane GPU state (lane = GPU index) and ledger state (lane = service)
+  uint32_t mask = 0;
+  int ngpc = 0, len = 0, ngpus = 0;
+  double freed = 0.0;
+  int order = 0;
+  bool fallback = false;
+  int nd = 0, n_before = 0;
+
+  WCYC(0);
+  int n7 = 0;
+  if (status == PARVA_OK) {
+    // --------------------------------------------- relocate_segments
+    // queue order (allocator.py:46-51): size classes 7,4,3,2,1
+    relocate_class<4>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+    if (status == PARVA_OK) relocate_class<3>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+    if (status == PARVA_OK) relocate_class<2>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+    if (status == PARVA_OK) relocate_class<1>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+    if (status == PARVA_OK) relocate_class<0>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+  }
+  __syncwarp();
+  WCYC(1);
+
+  if (status == PARVA_OK) {
+    n_before = ngpus;
+    const int total_before = warp_sum_i(lane < ngpus ? ngpc : 0);
+    *reinterpret_cast<uint4*>(W.bak[lane]) = *reinterpret_cast<const uint4*>(W.lst[lane]);
+    const int bak_len = len, bak_ngpc = ngpc;
+    const uint32_t bak_mask = mask;
+
+    if (A.optimize) {
+      // ----------------------------------------- optimize_allocation
+      int next = 0;
+      for (int index = ngpus - 1; index >= 0; index--) {
+        const int nl = __shfl_sync(0xffffffffu, len, index);
+        const int ng = __shfl_sync(0xffffffffu, ngpc, index);
+        if (nl == 0 || ng > A.threshold) continue;
+        const double sv_freed = freed;
+        const int sv_order = order, sv_next = next;
+        int q2n = 0, q1n = 0, fail = -1, fsvc = 0, rot = nl;
+        bool qover = false;
+        for (int kk = 0; kk < nl; kk++) {
+          const int cat = W.lst[index][kk] >> 3;
+          const int s = cat / 5;
+          const double tpp = cat_tp[cat];
+          const bool newkey = __shfl_sync(0xffffffffu, order, s) == 0;
+          if (newkey) next++;
+          if (lane == s) {
+            if (newkey) { order = next; freed = __dadd_rn(0.0, tpp); }
+            else freed = __dadd_rn(freed, tpp);
+          }
+          const double f = __shfl_sync(0xffffffffu, freed, s);
+          const double t1 = cat_tp[s * 5 + 0], t2 = cat_tp[s * 5 + 1];
+          long long k2, k1;
+          if (!propose_small_warp(t1, t2, f, k2, k1, lane)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fsvc = s; rot = kk + 1; break; }
+          if (lane == s) {
+            for (long long j = 0; j < k2; j++) freed = __dsub_rn(freed, t2);
+            for (long long j = 0; j < k1; j++) freed = __dsub_rn(freed, t1);
+          }
+          if (qover || q2n + k2 > QCAP || q1n + k1 > QCAP) qover = true;
+          else {
+            for (int j = lane; j < k2; j += 32) W.q2[q2n + j] = (uint8_t)(s * 5 + 1);
+            for (int j = lane; j < k1; j += 32) W.q1[q1n + j] = (uint8_t)(s * 5 + 0);
+            q2n += (int)k2; q1n += (int)k1;
+          }
+        }
+        __syncwarp();
+        if (fail < 0) {
+          if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
+          else {
+            int nu = 0;
+            for (int j = 0; j < q2n + q1n; j++) {
+              const int cat = j < q2n ? W.q2[j] : W.q1[j - q2n];
+              const int c = cat % 5;
+              const int st = (lane < ngpus && lane != index) ? find_start(mask, c) : -1;
+              const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
+              if (!b) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
+              const int g = __ffs(b) - 1;
+              if (lane == g) {
+                mask |= footprint(c, st);
+                ngpc += size_of_class(c);
+                W.lst[g][len++] = (uint16_t)(cat << 3 | st);
+              }
+              if (lane == 0) W.undo[nu] = (uint8_t)g;
+              nu++;
+            }
+            __syncwarp();
+            if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
+              for (int j = nu - 1; j >= 0; j--) {
+                const int g = W.undo[j];
+                if (lane == g) {
+                  const int e = W.lst[g][--len];
+                  mask &= ~footprint((e >> 3) % 5, e & 7);
+                  ngpc -= size_of_class((e >> 3) % 5);
+                }
+              }
+            }
+          }
+        }
+        if (fail >= 0) {
+          // restore drained placements (allocator.py:415-417): the ones not yet
+          // removed keep their order, the removed ones are re-appended
+          if (lane == index && rot != nl) {
+            uint16_t e[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) e[j] = W.lst[index][j];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              if (j < nl) {
+                int src = j + rot;
+                if (src >= nl) src -= nl;
+                uint16_t v = e[0];
+#pragma unroll
+                for (int u = 1; u < 8; u++) if (u == src) v = e[u];
+                W.lst[index][j] = v;
+              }
+            }
+          }
+          freed = sv_freed; order = sv_order; next = sv_next;
+          if (lane == 0)
+            W.diag[nd] = (uint16_t)(index << 7 | fail << 5 | (fail == PARVA_DIAG_SMALL_UNAVAILABLE ? fsvc : 0));
+          nd++;
+        } else if (lane == index) {
+          len = 0; mask = 0; ngpc = 0;
+        }
+        __syncwarp();
+      }
+      // compaction + regression check (allocator.py:423-435)
+      const int n_after = __popc(__ballot_sync(0xffffffffu, lane < ngpus && len > 0));
+      const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0);
+      const double ua_before = unallocated(total_before, n_before);
+      const double ua_after = unallocated(total_after, n_after);
+      if (n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12)) {
+        fallback = true;
+        *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
+        len = bak_len; ngpc = bak_ngpc; mask = bak_mask;
+        freed = 0.0; order = 0; nd = 0;
+      }
+    }
+    __syncwarp();
+    WCYC(2);
+
+    // ------------------------------------------------------- emit record
+    const bool good = lane < ngpus && len > 0;
+    const int mine = good ? len : 0;
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int n_place = __shfl_sync(0xffffffffu, incl, 31);
+    const int n_final = __popc(__ballot_sync(0xffffffffu, good));
+    const int n_led = __popc(__ballot_sync(0xffffffffu, lane < n && order > 0));
+    const int led_off = (2 * (n_place + nd) + 7) & ~7;
+    const int need = led_off + 10 * n_led;
+    if (need > PARVA_PLAN_PAYLOAD) {
+      status = PARVA_CAPACITY;
+    } else {
+      spill = A.plan_bytes == 64 && need > 64 - 8;
+      uint16_t* pay16 = reinterpret_cast<uint16_t*>(W.rec.payload);
+      for (int j = 0; j < mine; j++) pay16[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+      if (lane < nd) pay16[n_place + lane] = W.diag[lane];
+      if (lane < n && order > 0) {
+        reinterpret_cast<double*>(W.rec.payload + led_off)[order - 1] = freed;
+        reinterpret_cast<uint16_t*>(W.rec.payload + led_off + 8 * n_led)[order - 1] = (uint16_t)(lane | order << 8);
+      }
+      if (lane == 0) {
+        W.rec.n_gpus = (uint8_t)n_final;
+        W.rec.n_gpus_unopt = (uint8_t)n_before;
+        W.rec.n_place = (uint8_t)n_place;
+        W.rec.n_diag = (uint8_t)nd;
+        W.rec.n_ledger = (uint8_t)n_led;
+        W.rec.flags = fallback ? PARVA_FLAG_FALLBACK : 0;
+      }
+    }
+    // reset this lane's GPU list slots for the next scenario
+    *reinterpret_cast<uint4*>(W.lst[lane]) = make_uint4(0, 0, 0, 0);
+  }
+  __syncwarp();
+  if (status != PARVA_OK) {
+    reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
+    __syncwarp();
+    if (lane == 0) {
+      W.rec.status = (uint8_t)status;
+      W.rec.err_service = (uint8_t)((status == PARVA_CAPACITY || (status == PARVA_BAD_INPUT && !in_tile)) ? 0 : err_svc);
+    }
+  }
+  __syncwarp();
+  uint8_t* dst = reinterpret_cast<uint8_t*>(A.plan) + (size_t)k * A.plan_bytes;
+  if (status == PARVA_OK && spill && A.spill_direct) {
+    // 64-byte records, streamed mode: the full record goes to its scenario's
+    // slot of the overflow area
+    if (lane < 8) reinterpret_cast<uint4*>(A.spill + (size_t)k * 128)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    if (lane < 4) reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_SPILLED, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+  } else if (status == PARVA_OK && spill) {
+    // 64-byte records: the full record goes to the spill list
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(A.spill_count, 1);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (slot < A.spill_cap) {
+      uint8_t* e = A.spill + (size_t)slot * kSpillEntry;
+      if (lane == 0) *reinterpret_cast<int4*>(e) = make_int4(k, 0, 0, 0);
+      if (lane < 8) reinterpret_cast<uint4*>(e + 16)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+      if (lane < 4) reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_SPILLED, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+    } else if (lane < 4) {
+      reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_CAPACITY, 0, 0, 0) : make_uint4(0, 0, 0, 0);
+    }
+  } else if (lane < A.plan_bytes / 16) {
+    reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+  }
+  __syncwarp();
+  WCYC(3);
+}
+
 __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
   __shared__ uint64_t bar;
-  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS, false, &bar);
-  // config records come from K2a (launched before us with PDL)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PHASE(0);
+  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem), !A.cfg_given,
+                                 &bar);
+  PHASE(1);
+#ifdef PARVA_PHASE_TIMING
+  int dbg_n = 0;
+  bool dbg_first = true;
+#endif
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   WarpScratch& W = scratch[warp];
-  const int gwarps = gridDim.x * PB_WARPS;
 
-  for (int k = blockIdx.x * PB_WARPS + warp; k < A.n_scen; k += gwarps) {
-    const int a0 = A.scen_off[k];
-    const int n = A.scen_off[k + 1] - a0;
-    reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
-
-    // ------------------------------------------------ configured services
-    int err_status = 0, err_svc = 0;
-    int my_opt = -1, my_last = -1;
-    long long my_count = 0;
-    if (n <= PARVA_PLAN_MAX_SERVICES) {
-      int st = PARVA_OK;
-      if (lane < n) {
-        const int i = a0 + lane;
-        int16_t best[5];
-        if (A.cfg_format == PARVA_CFG_TINY) {
-          const parva_config_tiny r = reinterpret_cast<const parva_config_tiny*>(A.cfg)[i];
-#pragma unroll
-          for (int c = 0; c < 5; c++) best[c] = r.best[c] == 255 ? -1 : (int16_t)r.best[c];
-          my_opt = (r.opt_last & 15) == 15 ? -1 : (r.opt_last & 15);
-          my_last = (r.opt_last >> 4) == 15 ? -1 : (r.opt_last >> 4);
-          my_count = (r.status_flags & 0x80) ? (long long)1 << 40 : r.count;   // saturated: cannot fit
-          st = r.status_flags & 0x7F;
-        } else if (A.cfg_format == PARVA_CFG_COMPACT) {
-          const parva_config_compact r = reinterpret_cast<const parva_config_compact*>(A.cfg)[i];
-#pragma unroll
-          for (int c = 0; c < 5; c++) best[c] = r.best[c];
-          my_opt = r.opt_sc; my_last = r.last_sc; my_count = r.count; st = r.status;
-        } else {
-          const parva_config_record r = reinterpret_cast<const parva_config_record*>(A.cfg)[i];
-#pragma unroll
-          for (int c = 0; c < 5; c++) best[c] = r.best[c];
-          my_opt = r.opt_sc; my_last = r.last_sc; my_count = r.count; st = r.status;
-        }
-        const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
-#pragma unroll
-        for (int c = 0; c < 5; c++)
-          W.cat_tp[lane * 5 + c] =
-              (st != PARVA_BAD_INPUT && best[c] >= 0) ? V.tp[(V.seg_s[t * 5 + c] + best[c]) * V.tp_stride] : 0.0;
-      }
-      const unsigned bad = __ballot_sync(0xffffffffu, lane < n && st != PARVA_OK);
-      if (bad) {
-        err_svc = __ffs(bad) - 1;
-        err_status = __shfl_sync(0xffffffffu, st, err_svc);
-      }
-    }
-    __syncwarp();
-
-    int status = PARVA_OK;
-    bool spill = false;
-    if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
-    else if (err_status) status = err_status;
-    else {
-      const long long segs = warp_sum_ll(lane < n ? my_count + (my_last >= 0) : 0);
-      if (segs > 32 * 7) status = PARVA_CAPACITY;
-    }
-
-    // per-lane GPU state (lane = GPU index) and ledger state (lane = service)
-    uint32_t mask = 0;
-    int ngpc = 0, len = 0, ngpus = 0;
-    double freed = 0.0;
-    int order = 0;
-    bool fallback = false;
-    int nd = 0, n_before = 0;
-
-    if (status == PARVA_OK) {
-      // --------------------------------------------- relocate_segments
-      // queue order (allocator.py:46-51): size classes 7,4,3,2,1
-      relocate_class<4>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
-      if (status == PARVA_OK) relocate_class<3>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
-      if (status == PARVA_OK) relocate_class<2>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
-      if (status == PARVA_OK) relocate_class<1>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
-      if (status == PARVA_OK) relocate_class<0>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, status);
-    }
-    __syncwarp();
-
-    if (status == PARVA_OK) {
-      n_before = ngpus;
-      const int total_before = warp_sum_i(lane < ngpus ? ngpc : 0);
-      *reinterpret_cast<uint4*>(W.bak[lane]) = *reinterpret_cast<const uint4*>(W.lst[lane]);
-      const int bak_len = len, bak_ngpc = ngpc;
-      const uint32_t bak_mask = mask;
-
-      if (A.optimize) {
-        // ----------------------------------------- optimize_allocation
-        int next = 0;
-        for (int index = ngpus - 1; index >= 0; index--) {
-          const int nl = __shfl_sync(0xffffffffu, len, index);
-          const int ng = __shfl_sync(0xffffffffu, ngpc, index);
-          if (nl == 0 || ng > A.threshold) continue;
-          const double sv_freed = freed;
-          const int sv_order = order, sv_next = next;
-          int q2n = 0, q1n = 0, fail = -1, fsvc = 0, rot = nl;
-          bool qover = false;
-          for (int kk = 0; kk < nl; kk++) {
-            const int cat = W.lst[index][kk] >> 3;
-            const int s = cat / 5;
-            const double tpp = W.cat_tp[cat];
-            const bool newkey = __shfl_sync(0xffffffffu, order, s) == 0;
-            if (newkey) next++;
-            if (lane == s) {
-              if (newkey) { order = next; freed = __dadd_rn(0.0, tpp); }
-              else freed = __dadd_rn(freed, tpp);
-            }
-            const double f = __shfl_sync(0xffffffffu, freed, s);
-            const double t1 = W.cat_tp[s * 5 + 0], t2 = W.cat_tp[s * 5 + 1];
-            long long k2, k1;
-            if (!propose_small(t1, t2, f, k2, k1)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fsvc = s; rot = kk + 1; break; }
-            if (lane == s) {
-              for (long long j = 0; j < k2; j++) freed = __dsub_rn(freed, t2);
-              for (long long j = 0; j < k1; j++) freed = __dsub_rn(freed, t1);
-            }
-            if (qover || q2n + k2 > QCAP || q1n + k1 > QCAP) qover = true;
-            else {
-              for (int j = lane; j < k2; j += 32) W.q2[q2n + j] = (uint8_t)(s * 5 + 1);
-              for (int j = lane; j < k1; j += 32) W.q1[q1n + j] = (uint8_t)(s * 5 + 0);
-              q2n += (int)k2; q1n += (int)k1;
-            }
-          }
-          __syncwarp();
-          if (fail < 0) {
-            if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
-            else {
-              int nu = 0;
-              for (int j = 0; j < q2n + q1n; j++) {
-                const int cat = j < q2n ? W.q2[j] : W.q1[j - q2n];
-                const int c = cat % 5;
-                const int st = (lane < ngpus && lane != index) ? find_start(mask, c) : -1;
-                const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
-                if (!b) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
-                const int g = __ffs(b) - 1;
-                if (lane == g) {
-                  mask |= footprint(c, st);
-                  ngpc += size_of_class(c);
-                  W.lst[g][len++] = (uint16_t)(cat << 3 | st);
-                }
-                if (lane == 0) W.undo[nu] = (uint8_t)g;
-                nu++;
-              }
-              __syncwarp();
-              if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
-                for (int j = nu - 1; j >= 0; j--) {
-                  const int g = W.undo[j];
-                  if (lane == g) {
-                    const int e = W.lst[g][--len];
-                    mask &= ~footprint((e >> 3) % 5, e & 7);
-                    ngpc -= size_of_class((e >> 3) % 5);
-                  }
-                }
-              }
-            }
-          }
-          if (fail >= 0) {
-            // restore drained placements (allocator.py:415-417): the ones not yet
-            // removed keep their order, the removed ones are re-appended
-            if (lane == index && rot != nl) {
-              uint16_t e[8];
-#pragma unroll
-              for (int j = 0; j < 8; j++) e[j] = W.lst[index][j];
-#pragma unroll
-              for (int j = 0; j < 8; j++) {
-                if (j < nl) {
-                  int src = j + rot;
-                  if (src >= nl) src -= nl;
-                  uint16_t v = e[0];
-#pragma unroll
-                  for (int u = 1; u < 8; u++) if (u == src) v = e[u];
-                  W.lst[index][j] = v;
-                }
-              }
-            }
-            freed = sv_freed; order = sv_order; next = sv_next;
-            if (lane == 0)
-              W.diag[nd] = (uint16_t)(index << 7 | fail << 5 | (fail == PARVA_DIAG_SMALL_UNAVAILABLE ? fsvc : 0));
-            nd++;
-          } else if (lane == index) {
-            len = 0; mask = 0; ngpc = 0;
-          }
-          __syncwarp();
-        }
-        // compaction + regression check (allocator.py:423-435)
-        const int n_after = __popc(__ballot_sync(0xffffffffu, lane < ngpus && len > 0));
-        const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0);
-        const double ua_before = unallocated(total_before, n_before);
-        const double ua_after = unallocated(total_after, n_after);
-        if (n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12)) {
-          fallback = true;
-          *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
-          len = bak_len; ngpc = bak_ngpc; mask = bak_mask;
-          freed = 0.0; order = 0; nd = 0;
-        }
-      }
-      __syncwarp();
-
-      // ------------------------------------------------------- emit record
-      const bool good = lane < ngpus && len > 0;
-      const int mine = good ? len : 0;
-      int incl = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int n_place = __shfl_sync(0xffffffffu, incl, 31);
-      const int n_final = __popc(__ballot_sync(0xffffffffu, good));
-      const int n_led = __popc(__ballot_sync(0xffffffffu, lane < n && order > 0));
-      const int led_off = (2 * (n_place + nd) + 7) & ~7;
-      const int need = led_off + 10 * n_led;
-      if (need > PARVA_PLAN_PAYLOAD) {
-        status = PARVA_CAPACITY;
-      } else {
-        spill = A.plan_bytes == 64 && need > 64 - 8;
-        uint16_t* pay16 = reinterpret_cast<uint16_t*>(W.rec.payload);
-        for (int j = 0; j < mine; j++) pay16[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
-        if (lane < nd) pay16[n_place + lane] = W.diag[lane];
-        if (lane < n && order > 0) {
-          reinterpret_cast<double*>(W.rec.payload + led_off)[order - 1] = freed;
-          reinterpret_cast<uint16_t*>(W.rec.payload + led_off + 8 * n_led)[order - 1] = (uint16_t)(lane | order << 8);
-        }
-        if (lane == 0) {
-          W.rec.n_gpus = (uint8_t)n_final;
-          W.rec.n_gpus_unopt = (uint8_t)n_before;
-          W.rec.n_place = (uint8_t)n_place;
-          W.rec.n_diag = (uint8_t)nd;
-          W.rec.n_ledger = (uint8_t)n_led;
-          W.rec.flags = fallback ? PARVA_FLAG_FALLBACK : 0;
-        }
-      }
-      // reset this lane's GPU list slots for the next scenario
-      *reinterpret_cast<uint4*>(W.lst[lane]) = make_uint4(0, 0, 0, 0);
-    }
-    __syncwarp();
-    if (status != PARVA_OK) {
-      reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
-      __syncwarp();
-      if (lane == 0) {
-        W.rec.status = (uint8_t)status;
-        W.rec.err_service = (uint8_t)(status == PARVA_CAPACITY ? 0 : err_svc);
-      }
-    }
-    __syncwarp();
-    uint8_t* dst = reinterpret_cast<uint8_t*>(A.plan) + (size_t)k * A.plan_bytes;
-    if (status == PARVA_OK && spill) {
-      // 64-byte records: the full record goes to the spill list
-      int slot = 0;
-      if (lane == 0) slot = atomicAdd(A.spill_count, 1);
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (slot < A.spill_cap) {
-        uint8_t* e = A.spill + (size_t)slot * kSpillEntry;
-        if (lane == 0) *reinterpret_cast<int4*>(e) = make_int4(k, 0, 0, 0);
-        if (lane < 8) reinterpret_cast<uint4*>(e + 16)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
-        if (lane < 4) reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_SPILLED, 0, 0, 0) : make_uint4(0, 0, 0, 0);
-      } else if (lane < 4) {
-        reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_CAPACITY, 0, 0, 0) : make_uint4(0, 0, 0, 0);
-      }
-    } else if (lane < A.plan_bytes / 16) {
-      reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
-    }
-    __syncwarp();
+  // this CTA's contiguous block of scenarios, or (streamed mode) tiles of
+  // tile_scen scenarios taken in order from a device counter
+  int k, k1;
+  if (A.work) {
+    k = 0; k1 = 0;
+  } else {
+    const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
+    k = blockIdx.x * per;
+    k1 = min(A.n_scen, k + per);
   }
+  for (;;) {
+  if (A.work) {
+    if (tid == 0) T.tile = (int)atomicAdd(&A.work[0], 1u);
+    __syncthreads();
+    const int t = T.tile;
+    if ((long long)t * A.tile_scen >= A.n_scen) break;
+    k = t * A.tile_scen;
+    k1 = min(A.n_scen, k + A.tile_scen);
+  }
+  while (k < k1) {
+    // tile = the longest run of scenarios from k with <= kTileSvc services
+    // (at least one scenario; offsets are non-decreasing)
+    const int a0 = A.scen_off[k];
+    const int e = k + 1 + tid;
+    const int off_e = e <= k1 ? A.scen_off[e] : 0;
+    const bool fits = e <= k1 && (tid == 0 || off_e - a0 <= kTileSvc);
+    if (e <= k1) T.off[tid + 1] = off_e;
+    if (tid == 0) { T.off[0] = a0; T.next = 0; }
+    const int n_tile = __syncthreads_count(fits);
+    const int a_end = T.off[n_tile];
+
+    // configure the tile's services
+    for (int i = a0 + tid; i < a_end; i += PB_THREADS) {
+      double tpc[5];
+      const uint64_t m = tile_service(A, V, i, tpc);
+      const int li = i - a0;
+      if (li < kTileSvc) {
+#pragma unroll
+        for (int c = 0; c < 5; c++) T.tp[li * 5 + c] = tpc[c];
+        T.meta[li] = m;
+      }
+    }
+    __syncthreads();
+#ifdef PARVA_PHASE_TIMING
+    if (dbg_first) PHASE(2);
+    dbg_first = false;
+#endif
+
+    // plan the tile's scenarios, warp per scenario
+    for (;;) {
+      int j = 0;
+      if (lane == 0) j = atomicAdd(&T.next, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      if (j >= n_tile) break;
+      const int b = T.off[j] - a0;
+      const int n = T.off[j + 1] - T.off[j];
+      const bool in_tile = b >= 0 && n >= 0 && b + n <= kTileSvc;
+      plan_scenario_warp(A, W, k + j, n, T.tp + (in_tile ? b * 5 : 0), T.meta + (in_tile ? b : 0), in_tile, lane);
+#ifdef PARVA_PHASE_TIMING
+      dbg_n++;
+#endif
+    }
+#ifdef PARVA_PHASE_TIMING
+    if (lane == 0 && blockIdx.x < 1024) { g_warp_end[blockIdx.x][warp][0] = gtimer(); g_warp_end[blockIdx.x][warp][1] = dbg_n; }
+#endif
+    __syncthreads();
+    k += n_tile;
+  }
+  if (!A.work) break;
+  }
+  if (A.work && tid == 0) {
+    __threadfence();
+    if (atomicAdd(&A.work[1], 1u) == gridDim.x - 1) {   // last CTA: reset for the next launch
+      atomicExch(&A.work[0], 0u);
+      atomicExch(&A.work[1], 0u);
+    }
+  }
+  PHASE(3);
 }
 
 
@@ -505,66 +704,48 @@ size_t index_smem_bytes(int n_tables, int64_t n_points, bool smem_index, bool la
 }
 
 struct LaunchCfg {
-  int grid_a, grid_b;
-  size_t smem_a, smem_b;
+  int grid;
+  size_t smem;
 };
 
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
-  const size_t smem_b = sizeof(WarpScratch) * PB_WARPS + index_smem_bytes(A.n_tables, A.n_points, A.smem_index, false);
-  const size_t smem_a = index_smem_bytes(A.n_tables, A.n_points, A.smem_index, true);
+  const size_t smem = sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem) +
+                      index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
-  struct DevCfg { size_t conf_a, conf_b, occ_a, occ_b; int n_sm, per_a, per_b; };
+  struct DevCfg { size_t conf, occ; int n_sm, per; };
   static DevCfg s_cfg[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
   DevCfg& D = s_cfg[dev & (kMaxDevices - 1)];
-  if (smem_b > D.conf_b) {
-    cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    D.conf_b = smem_b;
-  }
-  if (smem_a > D.conf_a) {
-    cudaFuncSetAttribute(configure_services_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
-    D.conf_a = smem_a;
+  if (smem > D.conf) {
+    if (cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return false;
+    D.conf = smem;
   }
   if (!D.n_sm) cudaDeviceGetAttribute(&D.n_sm, cudaDevAttrMultiProcessorCount, dev);
-  if (smem_b != D.occ_b) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per_b, plan_batch_kernel, PB_THREADS, smem_b);
-    D.occ_b = smem_b;
+  if (smem != D.occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per, plan_batch_kernel, PB_THREADS, smem);
+    D.occ = smem;
   }
-  if (smem_a != D.occ_a) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per_a, configure_services_kernel, CF_THREADS, smem_a);
-    D.occ_a = smem_a;
-  }
-  const int n_sm = D.n_sm, per_a = D.per_a, per_b = D.per_b;
-  if (per_b < 1 || per_a < 1) return false;
-  int gb = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
-  if (gb > n_sm * per_b) gb = n_sm * per_b;
-  int ga = (int)((A.n_svc + CF_THREADS - 1) / CF_THREADS);
-  if (ga > n_sm * per_a) ga = n_sm * per_a;
-  L->grid_a = ga < 1 ? 1 : ga;
-  L->grid_b = gb < 1 ? 1 : gb;
-  L->smem_a = smem_a;
-  L->smem_b = smem_b;
+  if (D.per < 1) return false;
+  int g = A.work ? (A.n_scen + A.tile_scen - 1) / A.tile_scen : (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  if (g > D.n_sm * D.per) g = D.n_sm * D.per;
+  L->grid = g < 1 ? 1 : g;
+  L->smem = smem;
   return true;
+}
+
+int plan_batch_grid(const PlanArgs& A) {
+  LaunchCfg L;
+  return plan_launch_config(A, &L) ? L.grid : 0;
 }
 
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.n_scen <= 0) return PARVA_OK;
+  if (A.work && A.tile_scen < 1) return PARVA_BAD_INPUT;
   LaunchCfg L;
   if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
-  const bool two = !A.cfg_given && A.n_svc > 0;
-  if (two) configure_services_kernel<<<L.grid_a, CF_THREADS, L.smem_a, stream>>>(A);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(L.grid_b);
-  cfg.blockDim = dim3(PB_THREADS);
-  cfg.dynamicSmemBytes = L.smem_b;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = two ? 1 : 0;
-  if (cudaLaunchKernelEx(&cfg, plan_batch_kernel, A) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+  plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
@@ -575,33 +756,20 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
   PlanArgs copy = A;
   void* args[] = {&copy};
   cudaKernelNodeParams p = {};
-  cudaGraphNode_t na;
-  const cudaGraphNode_t* d = deps;
-  size_t nd = ndeps;
-  if (!A.cfg_given && A.n_svc > 0) {
-    p.func = (void*)configure_services_kernel;
-    p.gridDim = dim3(L.grid_a);
-    p.blockDim = dim3(CF_THREADS);
-    p.sharedMemBytes = (unsigned)L.smem_a;
-    p.kernelParams = args;
-    if (cudaGraphAddKernelNode(&na, g, deps, ndeps, &p) != cudaSuccess) return PARVA_LAUNCH_ERROR;
-    d = &na;
-    nd = 1;
-  }
   p.func = (void*)plan_batch_kernel;
-  p.gridDim = dim3(L.grid_b);
+  p.gridDim = dim3(L.grid);
   p.blockDim = dim3(PB_THREADS);
-  p.sharedMemBytes = (unsigned)L.smem_b;
+  p.sharedMemBytes = (unsigned)L.smem;
   p.kernelParams = args;
-  if (d != deps) {
-    // K2a -> K2b as a programmatic edge (PDL inside the graph)
-    if (cudaGraphAddKernelNode(node, g, nullptr, 0, &p) != cudaSuccess) return PARVA_LAUNCH_ERROR;
-    cudaGraphEdgeData ed = {};
-    ed.from_port = cudaGraphKernelNodePortProgrammatic;
-    ed.type = cudaGraphDependencyTypeProgrammatic;
-    return cudaGraphAddDependencies_v2(g, &na, node, &ed, 1) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
-  }
-  return cudaGraphAddKernelNode(node, g, d, nd, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+  return cudaGraphAddKernelNode(node, g, deps, ndeps, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
 }  // namespace parva
+
+#ifdef PARVA_PHASE_TIMING
+extern "C" int parva_dbg_phase(unsigned long long* phase, unsigned long long* warp_end, unsigned long long* cyc) {
+  cudaMemcpyFromSymbol(phase, parva::g_phase, sizeof(parva::g_phase));
+  cudaMemcpyFromSymbol(cyc, parva::g_warp_cyc, sizeof(parva::g_warp_cyc));
+  return cudaMemcpyFromSymbol(warp_end, parva::g_warp_end, sizeof(parva::g_warp_end)) == cudaSuccess ? 0 : 1;
+}
+#endif
