@@ -274,24 +274,52 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
                            int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
                            size_t scratch_bytes, void* stream);
 
-/* Zero-copy host entry (one batch, one launch): the kernel reads the packed
- * input block straight from pinned, mapped host memory and writes the
- * records straight into the pinned, mapped output block, so the PCIe reads,
- * the planning and the PCIe writes overlap inside one kernel (no staging
- * copies).  Scenarios are planned in tiles taken in order from a device
- * counter.  Layout from parva_mapped_layout: the input block is the packed
- * chunk layout; the output block holds plan records[k], config records[m],
- * and for 64-byte plan records an overflow area of k full 128-byte records
- * (a scenario with status PARVA_SPILLED has its full record at index k).
- * d_work: 16 bytes of device memory, zeroed once before first use; it is
- * left zeroed after every call (one call at a time per d_work).
- * Synchronizes `stream` before returning. */
+/* Streamed input block (parva_plan_host_mapped): a header, then one packed
+ * chunk block (parva_packed_layout of the chunk, chunk-local offsets) per
+ * chunk of consecutive scenarios, so the data of the first scenarios arrives
+ * first.  Header: int32 n_chunks, int32 chunk_scen (scenarios per chunk, the
+ * last chunk may hold fewer), int32 pad[2], parva_stream_chunk[n_chunks];
+ * padded to 256 bytes. */
+typedef struct {
+  int32_t scen_lo;      /* first scenario of the chunk          */
+  int32_t svc_lo;       /* first service of the chunk           */
+  int32_t k, m;         /* scenarios, services                  */
+  int64_t offset;       /* byte offset of the chunk block       */
+} parva_stream_chunk;
+
+#define parva_stream_header_bytes(n_chunks) ((((int64_t)(n_chunks) * 24 + 16) + 255) & ~(int64_t)255)
+
+/* Bytes of the streamed input block for a batch (exact, for these offsets). */
+int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32_t chunk_scen);
+/* Pack a batch (services of scenario k: [h_scen_off[k], h_scen_off[k+1]),
+ * h_scen_off[0] = 0) into a streamed input block of `capacity` bytes;
+ * returns the bytes written, or -1. */
+int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const uint16_t* h_table,
+                          const double* h_rate, const double* h_bound, int32_t chunk_scen,
+                          void* h_block, int64_t capacity);
+
+/* Zero-copy host entry (the end-to-end path; one batch, one launch).  The
+ * input block (streamed layout, parva_stream_pack) and the output block
+ * (parva_mapped_layout: plan records[k], config records[m], and for 64-byte
+ * plan records an overflow area of k full 128-byte records -- a scenario
+ * with status PARVA_SPILLED has its full record at index k) live in pinned,
+ * mapped host memory.  Inside the one kernel loader warps copy the input
+ * block over PCIe in 4 KB slices, in order, into a device staging area and
+ * publish each slice with a flag; every warp then takes the next scenario,
+ * waits for its chunk's slices, configures and plans it, and
+ * writes its records straight into the host output block.  So the H2D
+ * stream, the planning and the D2H writes overlap.  Scratch:
+ * parva_plan_host_mapped_scratch bytes of device memory (initialised by the
+ * first call with it; one call at a time per scratch).  Synchronizes
+ * `stream` before returning. */
 int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes,
                         parva_chunk_layout* out);
+size_t parva_plan_host_mapped_scratch(int64_t in_bytes);
 int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
                            int32_t n_scenarios, int32_t n_services, const void* h_in,
-                           void* h_out, int32_t optimize, int32_t threshold,
-                           int32_t cfg_format, int32_t plan_bytes, void* d_work, void* stream);
+                           int64_t in_bytes, void* h_out, int32_t optimize, int32_t threshold,
+                           int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
+                           size_t scratch_bytes, void* stream);
 
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional

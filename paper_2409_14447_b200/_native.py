@@ -64,7 +64,8 @@ EXPORTS = (
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
-    "parva_mapped_layout", "parva_plan_host_mapped",
+    "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
+    "parva_stream_pack",
 )
 
 
@@ -95,6 +96,9 @@ def load_library(build_if_missing: bool = True):
             _LIB.parva_plan_host_scratch.restype = C.c_size_t
             _LIB.parva_plan_general_workspace.restype = C.c_size_t
             _LIB.parva_plan_host_packed_scratch.restype = C.c_size_t
+            _LIB.parva_plan_host_mapped_scratch.restype = C.c_size_t
+            _LIB.parva_stream_bytes.restype = C.c_int64
+            _LIB.parva_stream_pack.restype = C.c_int64
         return _LIB
 
 
@@ -114,6 +118,12 @@ def stream_handle(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def np_ptr(a: np.ndarray):
+    """ctypes pointer to a C-contiguous numpy array (host memory)."""
+    assert a.flags["C_CONTIGUOUS"]
+    return C.c_void_p(a.ctypes.data)
 
 
 def check(rc: int, what: str):

@@ -352,56 +352,68 @@ class PackedHostBatch:
 
 # ------------------------------------------------------------ mapped host
 class MappedHostBatch:
-    """A batch for the zero-copy host entry parva_plan_host_mapped.
+    """A batch for the zero-copy host entry parva_plan_host_mapped (the
+    end-to-end path).
 
-    One pinned input block (the packed chunk layout: offsets, rates, bounds,
-    u16 table ids) and one pinned output block (plan records, config
+    One pinned input block in the streamed layout (a chunk table, then one
+    packed block per `chunk_scen` consecutive scenarios; packed by
+    parva_stream_pack) and one pinned output block (plan records, config
     records, and for 64-byte plan records an overflow area of full records).
-    The planning kernel reads the inputs over PCIe straight from the input
-    block and writes the records straight into the output block; `run` is
+    Inside one kernel, loader warps stream the input block over PCIe in
+    order while the other warps plan each scenario as soon as its chunk has
+    landed and write its records straight into the output block; `run` is
     one launch plus a stream synchronize."""
 
-    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64):
+    def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64,
+                 chunk_scen: int = 64):
         torch = N.require_cuda()
         L = N.lib()
         scen_off = np.asarray(scen_off, dtype=np.int64)
         self.n_scen, self.n_svc = len(scen_off) - 1, int(scen_off[-1] - scen_off[0])
-        self.cfg_format, self.plan_bytes = cfg_format, plan_bytes
+        self.cfg_format, self.plan_bytes, self.chunk_scen = cfg_format, plan_bytes, chunk_scen
         self.layout = ChunkLayout()
         N.check(L.parva_mapped_layout(C.c_int32(self.n_scen), C.c_int32(self.n_svc), C.c_int32(cfg_format),
                                       C.c_int32(plan_bytes), C.byref(self.layout)), "parva_mapped_layout")
-        self.h_in = torch.zeros(self.layout.in_bytes, dtype=torch.uint8).pin_memory()
+        self._off32 = np.ascontiguousarray(scen_off - scen_off[0], dtype=np.int32)
+        self.in_bytes = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(self._off32), C.c_int32(chunk_scen)))
+        if self.in_bytes < 0:
+            raise ValueError("invalid scenario offsets")
+        self.h_in = torch.zeros(self.in_bytes, dtype=torch.uint8).pin_memory()
         self.h_out = torch.zeros(self.layout.out_bytes, dtype=torch.uint8).pin_memory()
-        self.work = torch.zeros(4, dtype=torch.int32, device="cuda")   # zeroed once; kernels leave it zeroed
+        self.scratch_bytes = int(L.parva_plan_host_mapped_scratch(C.c_int64(self.in_bytes)))
+        self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda")
         self.fill(scen_off, svc_table, svc_rate, svc_bound)
 
     def fill(self, scen_off, svc_table, svc_rate, svc_bound):
-        lay, buf = self.layout, self.h_in.numpy()
         scen_off = np.asarray(scen_off, dtype=np.int64)
         sa, sb = int(scen_off[0]), int(scen_off[-1])
-        k, m = self.n_scen, sb - sa
-        buf[lay.in_scen_off:lay.in_scen_off + 4 * (k + 1)].view(np.int32)[:] = scen_off - sa
-        buf[lay.in_rate:lay.in_rate + 8 * m].view(np.float64)[:] = np.asarray(svc_rate)[sa:sb]
-        buf[lay.in_bound:lay.in_bound + 8 * m].view(np.float64)[:] = np.asarray(svc_bound)[sa:sb]
-        buf[lay.in_table:lay.in_table + 2 * m].view(np.uint16)[:] = np.asarray(svc_table)[sa:sb]
+        off32 = np.ascontiguousarray(scen_off - sa, dtype=np.int32)
+        tab = np.ascontiguousarray(np.asarray(svc_table)[sa:sb], dtype=np.uint16)
+        rate = np.ascontiguousarray(np.asarray(svc_rate)[sa:sb], dtype=np.float64)
+        bound = np.ascontiguousarray(np.asarray(svc_bound)[sa:sb], dtype=np.float64)
+        n = N.lib().parva_stream_pack(C.c_int32(self.n_scen), N.np_ptr(off32), N.np_ptr(tab), N.np_ptr(rate),
+                                      N.np_ptr(bound), C.c_int32(self.chunk_scen), C.c_void_p(self.h_in.data_ptr()),
+                                      C.c_int64(self.in_bytes))
+        if n != self.in_bytes:
+            raise ValueError("parva_stream_pack failed (offsets changed shape?)")
 
     def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
         rc = N.lib().parva_plan_host_mapped(
             C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
-            C.c_void_p(self.h_in.data_ptr()), C.c_void_p(self.h_out.data_ptr()), C.c_int32(int(optimize)),
-            C.c_int32(int(threshold)), C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes),
-            N.ptr(self.work), N.stream_handle(stream))
+            C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes), C.c_void_p(self.h_out.data_ptr()),
+            C.c_int32(int(optimize)), C.c_int32(int(threshold)), C.c_int32(self.cfg_format),
+            C.c_int32(self.plan_bytes), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), N.stream_handle(stream))
         N.check(rc, "parva_plan_host_mapped")
 
     @property
     def h2d_bytes(self) -> int:
-        """Bytes the kernel reads from the host block per call (the packed inputs)."""
-        lay = self.layout
-        return int(lay.in_table + 2 * self.n_svc)
+        """Bytes the kernel streams from the host input block per call."""
+        return self.in_bytes
 
     @property
     def d2h_bytes(self) -> int:
-        """Bytes written into the host block per call (records; overflow records only when used)."""
+        """Record bytes the kernel writes into the host output block per call
+        (plan + config records; the overflow area only for spilled scenarios)."""
         lay = self.layout
         return int(lay.out_cfg + _CFG_DT[self.cfg_format].itemsize * self.n_svc)
 

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -416,28 +417,96 @@ int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_b
   return PARVA_OK;
 }
 
-static int tile_scen_for(int n_scen, int grid_cap) {
+static int loaders_for(int64_t in_bytes) {
   static int env = -1;
   if (env < 0) {
-    const char* e = std::getenv("PARVA_TILE_SCEN");
+    const char* e = std::getenv("PARVA_LOADERS");
     env = e ? std::max(0, std::atoi(e)) : 0;
   }
   if (env > 0) return env;
-  // about four tiles per resident CTA, 8..64 scenarios each
-  const int t = n_scen / std::max(1, 4 * grid_cap);
-  return std::min(64, std::max(8, t));
+  // ~400 KB in flight covers the PCIe bandwidth-latency product (~8 us x 50
+  // GB/s) while keeping the slices landing roughly in order
+  return (int)std::min<int64_t>(96, std::max<int64_t>(1, (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice));
 }
 
+int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32_t chunk_scen) {
+  if (n_scenarios < 0 || !h_scen_off || chunk_scen < 1) return -1;
+  const int32_t n_ch = n_scenarios == 0 ? 0 : (n_scenarios + chunk_scen - 1) / chunk_scen;
+  int64_t total = parva_stream_header_bytes(n_ch);
+  for (int32_t c = 0; c < n_ch; c++) {
+    const int32_t a = c * chunk_scen, b = std::min(n_scenarios, a + chunk_scen);
+    parva_chunk_layout L;
+    if (parva_packed_layout(b - a, h_scen_off[b] - h_scen_off[a], PARVA_CFG_TINY, 64, &L) != PARVA_OK) return -1;
+    total += L.in_bytes;
+  }
+  return total;
+}
+
+int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const uint16_t* h_table,
+                          const double* h_rate, const double* h_bound, int32_t chunk_scen, void* h_block,
+                          int64_t capacity) {
+  const int64_t need = parva_stream_bytes(n_scenarios, h_scen_off, chunk_scen);
+  if (need < 0 || need > capacity || !h_block) return -1;
+  if (n_scenarios > 0 && h_scen_off[0] != 0) return -1;
+  for (int32_t k = 0; k < n_scenarios; k++)
+    if (h_scen_off[k + 1] < h_scen_off[k]) return -1;
+  uint8_t* out = (uint8_t*)h_block;
+  const int32_t n_ch = n_scenarios == 0 ? 0 : (n_scenarios + chunk_scen - 1) / chunk_scen;
+  std::memset(out, 0, (size_t)parva_stream_header_bytes(n_ch));
+  reinterpret_cast<int32_t*>(out)[0] = n_ch;
+  reinterpret_cast<int32_t*>(out)[1] = chunk_scen;
+  parva_stream_chunk* tab = reinterpret_cast<parva_stream_chunk*>(out + 16);
+  int64_t off = parva_stream_header_bytes(n_ch);
+  for (int32_t c = 0; c < n_ch; c++) {
+    const int32_t a = c * chunk_scen, b = std::min(n_scenarios, a + chunk_scen);
+    const int32_t sa = h_scen_off[a], sb = h_scen_off[b];
+    parva_chunk_layout L;
+    parva_packed_layout(b - a, sb - sa, PARVA_CFG_TINY, 64, &L);
+    tab[c].scen_lo = a; tab[c].svc_lo = sa; tab[c].k = b - a; tab[c].m = sb - sa; tab[c].offset = off;
+    uint8_t* blk = out + off;
+    std::memset(blk, 0, (size_t)L.in_bytes);
+    int32_t* so = reinterpret_cast<int32_t*>(blk + L.in_scen_off);
+    for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
+    std::memcpy(blk + L.in_rate, h_rate + sa, size_t(sb - sa) * 8);
+    std::memcpy(blk + L.in_bound, h_bound + sa, size_t(sb - sa) * 8);
+    std::memcpy(blk + L.in_table, h_table + sa, size_t(sb - sa) * 2);
+    off += L.in_bytes;
+  }
+  return off;
+}
+
+size_t parva_plan_host_mapped_scratch(int64_t in_bytes) {
+  if (in_bytes < 0) return 0;
+  const int64_t n_slices = (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice;
+  return 256 + up256(16) + up256(size_t(n_slices) * 4) + up256(size_t(in_bytes));
+}
+
+// scratch -> epoch of its slice flags (flags hold the epoch of the call that wrote them)
+struct MappedEpoch {
+  int dev = -1;
+  void* scratch = nullptr;
+  size_t bytes = 0;
+  uint32_t epoch = 0;
+};
+static std::vector<MappedEpoch> g_mapped_epochs;
+
 int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
-                           int32_t n_services, const void* h_in, void* h_out, int32_t optimize, int32_t threshold,
-                           int32_t cfg_format, int32_t plan_bytes, void* d_work, void* stream) {
-  if (!tables || !index || !h_in || !h_out || !d_work || n_scenarios < 0 || n_services < 0) return PARVA_BAD_INPUT;
+                           int32_t n_services, const void* h_in, int64_t in_bytes, void* h_out, int32_t optimize,
+                           int32_t threshold, int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
+                           size_t scratch_bytes, void* stream) {
+  if (!tables || !index || !h_in || !h_out || !d_scratch || n_scenarios < 0 || n_services < 0 || in_bytes < 16 ||
+      in_bytes % 16 != 0)
+    return PARVA_BAD_INPUT;
   parva_chunk_layout L;
   if (parva_mapped_layout(n_scenarios, n_services, cfg_format, plan_bytes, &L) != PARVA_OK) return PARVA_BAD_INPUT;
+  const size_t need = parva_plan_host_mapped_scratch(in_bytes);
+  if (need == 0 || need > scratch_bytes) return PARVA_BAD_INPUT;
   // pinned host blocks are mapped to device addresses; device blocks are used as they are
-  auto dev_ptr = [](const void* p, void** d) {
+  bool in_host = false;
+  auto dev_ptr = [](const void* p, void** d, bool* host) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    *host = at.type == cudaMemoryTypeHost;
     if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) { *d = const_cast<void*>(p); return true; }
     if (at.type != cudaMemoryTypeHost) return false;          // pageable memory cannot be mapped
     if (cudaHostGetDevicePointer(d, const_cast<void*>(p), 0) != cudaSuccess) { cudaGetLastError(); return false; }
@@ -445,19 +514,39 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
   };
   void* d_in = nullptr;
   void* d_out = nullptr;
-  if (!dev_ptr(h_in, &d_in) || !dev_ptr(h_out, &d_out)) return PARVA_BAD_INPUT;
+  bool out_host = false;
+  if (!dev_ptr(h_in, &d_in, &in_host) || !dev_ptr(h_out, &d_out, &out_host)) return PARVA_BAD_INPUT;
+  if (!in_host) return PARVA_BAD_INPUT;   // the streamed input block must be pinned host memory
   cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint8_t* base = (uint8_t*)(((uintptr_t)d_scratch + 255) & ~uintptr_t(255));
+  uint32_t* work = (uint32_t*)base;
+  uint32_t* flags = (uint32_t*)(base + up256(16));
+  const int64_t n_slices = (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice;
+  uint8_t* staging = base + up256(16) + up256(size_t(n_slices) * 4);
+  uint32_t epoch = 0;
+  {
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    MappedEpoch* E = nullptr;
+    for (auto& e : g_mapped_epochs)
+      if (e.dev == dev && e.scratch == d_scratch && e.bytes == scratch_bytes) { E = &e; break; }
+    if (!E || E->epoch == 0xFFFFFFFFu) {
+      // first use of this scratch: zero the counters and flags
+      if (cudaStreamSynchronize(s) != cudaSuccess || cudaMemset(base, 0, up256(16) + up256(size_t(n_slices) * 4)) !=
+          cudaSuccess) return PARVA_LAUNCH_ERROR;
+      if (!E) { g_mapped_epochs.emplace_back(); E = &g_mapped_epochs.back(); }
+      E->dev = dev; E->scratch = d_scratch; E->bytes = scratch_bytes; E->epoch = 0;
+    }
+    epoch = ++E->epoch;
+  }
   if (n_scenarios > 0) {
-    uint8_t* in = (uint8_t*)d_in;
     uint8_t* out = (uint8_t*)d_out;
     parva::PlanArgs A;
     A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
     A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
     A.n_points = tables->n_points; A.n_scen = n_scenarios; A.n_svc = n_services;
-    A.scen_off = (const int32_t*)(in + L.in_scen_off);
-    A.svc_table = nullptr; A.svc_table16 = (const uint16_t*)(in + L.in_table);
-    A.svc_rate = (const double*)(in + L.in_rate);
-    A.svc_bound = (const double*)(in + L.in_bound);
+    A.scen_off = nullptr; A.svc_table = nullptr; A.svc_table16 = nullptr; A.svc_rate = nullptr; A.svc_bound = nullptr;
     A.optimize = optimize; A.threshold = threshold; A.cfg_given = 0;
     A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
     A.cfg = out + L.out_cfg; A.cfg_format = cfg_format;
@@ -466,11 +555,14 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
     A.spill_count = nullptr;
     A.spill = out + L.out_spill;
     A.spill_direct = 1;
-    A.work = (uint32_t*)d_work;
+    A.work = work;
     A.tile_scen = 1;
-    const int cap = parva::plan_batch_grid(A);
-    if (cap < 1) return PARVA_LAUNCH_ERROR;
-    A.tile_scen = tile_scen_for(n_scenarios, cap);
+    A.stream_src = (const uint8_t*)d_in;
+    A.stream_dst = staging;
+    A.stream_bytes = in_bytes;
+    A.slice_flag = flags;
+    A.epoch = epoch;
+    A.n_loaders = loaders_for(in_bytes);
     const int rc = parva::launch_plan_batch(A, s);
     if (rc != PARVA_OK) return rc;
   }

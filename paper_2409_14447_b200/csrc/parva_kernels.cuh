@@ -40,7 +40,20 @@ struct PlanArgs {
   uint32_t* work = nullptr;
   int tile_scen = 0;
   int spill_direct = 0;          // 64-byte records: full record at spill + 128 * scenario
+  // streamed inputs (warp kernel, zero-copy host entry): the packed input
+  // block at stream_src (mapped host memory) is copied in kStreamSlice-byte
+  // slices, in order, by n_loaders loader warps into stream_dst (device; the
+  // scen_off / svc_* pointers point into it); slice s has landed when
+  // slice_flag[s] == epoch
+  const uint8_t* stream_src = nullptr;
+  uint8_t* stream_dst = nullptr;
+  int64_t stream_bytes = 0;
+  uint32_t* slice_flag = nullptr;
+  uint32_t epoch = 0;
+  int n_loaders = 0;
 };
+
+constexpr int kStreamSlice = 4096;
 
 constexpr int kSpillEntry = 144;
 constexpr int kMaxDevices = 64;    // per-device launch-configuration caches   // int32 scenario, 12 B pad, 128-byte record

@@ -17,6 +17,8 @@
 // are re-planned by the general kernel (plan_general.cu).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "parva_async.cuh"
 #include "parva_common.cuh"
 #include "parva_kernels.cuh"
@@ -298,23 +300,28 @@ __device__ __forceinline__ uint64_t pack_meta(int opt, int last, int status, lon
          (uint64_t)(status & 0xFF) << 56;
 }
 
+// configure one service (table t, request rate, internal latency bound) and
+// store its config record at index out_i
+__device__ __forceinline__ uint64_t svc_configure(const PlanArgs& A, const IndexView& V, int t, double rate,
+                                                  double bound, int64_t out_i, double tpc[5]) {
+  parva_config_record r = {};
+  if (t < 0 || t >= A.n_tables) {
+#pragma unroll
+    for (int c = 0; c < 5; c++) { r.best[c] = -1; tpc[c] = 0.0; }
+    r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
+  } else {
+    configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, bound, rate, r, tpc);
+  }
+  store_config(A, out_i, r);
+  return pack_meta(r.opt_sc, r.last_sc, r.status, r.count);
+}
+
 // configure (or load the given config record of) absolute service i; returns
 // the per-size-class tp (0 = absent) and the packed meta word
 __device__ __forceinline__ uint64_t tile_service(const PlanArgs& A, const IndexView& V, int64_t i, double tpc[5]) {
   const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
   const bool bad_t = t < 0 || t >= A.n_tables;
-  if (!A.cfg_given) {
-    parva_config_record r = {};
-    if (bad_t) {
-#pragma unroll
-      for (int c = 0; c < 5; c++) { r.best[c] = -1; tpc[c] = 0.0; }
-      r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
-    } else {
-      configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, A.svc_bound[i], A.svc_rate[i], r, tpc);
-    }
-    store_config(A, i, r);
-    return pack_meta(r.opt_sc, r.last_sc, r.status, r.count);
-  }
+  if (!A.cfg_given) return svc_configure(A, V, t, A.svc_rate[i], A.svc_bound[i], i, tpc);
   // preconfigured (K1 sweep records)
   int16_t best[5];
   int opt, last, st;
@@ -694,6 +701,158 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
 }
 
 
+// K2, warp-autonomous form: every warp takes scenarios one at a time from a
+// device counter (work[0]) and configures its own scenario (lane = service,
+// the same prefix-argmax search) before planning it -- no block barriers,
+// so loads, configuration and planning of different warps overlap freely.
+struct alignas(16) WarpSvc {
+  double tp[32 * 5];                      // best tp per (service, size class); 0 = absent
+  uint64_t meta[32];
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Streamed mode: copy input slices host -> device in ticket order (work[2]).
+// Few loader warps keep ~n_loaders * 4 KB in flight, so slices land roughly
+// in order at PCIe speed instead of every warp's reads interleaving.
+__device__ __forceinline__ void stream_loader(const PlanArgs& A, int lane) {
+  const int n_slices = (int)((A.stream_bytes + kStreamSlice - 1) / kStreamSlice);
+  for (;;) {
+    int s = 0;
+    if (lane == 0) s = (int)atomicAdd(&A.work[2], 1u);
+    s = __shfl_sync(0xffffffffu, s, 0);
+    if (s >= n_slices) break;
+    const int64_t base = (int64_t)s * kStreamSlice;
+    uint4 v[kStreamSlice / 512];
+#pragma unroll
+    for (int i = 0; i < kStreamSlice / 512; i++) {
+      const int64_t o = base + i * 512 + lane * 16;
+      if (o < A.stream_bytes) v[i] = __ldcv(reinterpret_cast<const uint4*>(A.stream_src + o));
+    }
+#pragma unroll
+    for (int i = 0; i < kStreamSlice / 512; i++) {
+      const int64_t o = base + i * 512 + lane * 16;
+      if (o < A.stream_bytes) __stcg(reinterpret_cast<uint4*>(A.stream_dst + o), v[i]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release_u32(&A.slice_flag[s], A.epoch);
+    }
+  }
+}
+
+// Streamed mode: wait until the input bytes [lo, hi) have landed.
+__device__ __forceinline__ void stream_wait(const PlanArgs& A, const void* p_lo, const void* p_hi, int lane) {
+  if (lane == 0) {
+    const int64_t lo = (const uint8_t*)p_lo - A.stream_dst, hi = (const uint8_t*)p_hi - A.stream_dst;
+    if (hi > lo)
+      for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++)
+        while (ld_acquire_u32(&A.slice_flag[s]) != A.epoch) __nanosleep(64);
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(PB_THREADS, 2) plan_warp_kernel(PlanArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool streamed = A.stream_src != nullptr;
+  PHASE(0);
+  // loader warps first (warp 0 of the first n_loaders CTAs), then they plan too
+  if (streamed && warp == 0 && (int)blockIdx.x < A.n_loaders) stream_loader(A, lane);
+  PHASE(1);
+  const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, !A.cfg_given,
+                                 &bar);
+  WarpScratch& W = scratch[warp];
+  WarpSvc& S = wsvc[warp];
+  // streamed mode: the input is a header (chunk table) followed by chunk
+  // blocks; this warp's current chunk (scenarios ascend per warp)
+  int n_ch = 0, ch_scen = 1, c = -1, c_scen_lo = 0, c_svc_lo = 0;
+  const int32_t* c_off = nullptr;
+  const double* c_rate = nullptr;
+  const double* c_bound = nullptr;
+  const uint16_t* c_table = nullptr;
+  if (streamed) {
+    stream_wait(A, A.stream_dst, A.stream_dst + 16, lane);
+    n_ch = __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst));
+    ch_scen = max(1, __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst) + 1));
+    stream_wait(A, A.stream_dst, A.stream_dst + parva_stream_header_bytes(n_ch), lane);
+  }
+  for (;;) {
+    int j = 0;
+    if (lane == 0) j = (int)atomicAdd(&A.work[0], 1u);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    if (j >= A.n_scen) break;
+    int a0, n;
+    if (streamed) {
+      const int cj = min(j / ch_scen, n_ch - 1);     // chunks hold ch_scen scenarios (the last one fewer)
+      if (cj != c) {
+        c = cj;
+        const parva_stream_chunk* tab = reinterpret_cast<const parva_stream_chunk*>(A.stream_dst + 16);
+        c_scen_lo = __ldcg(&tab[c].scen_lo);
+        c_svc_lo = __ldcg(&tab[c].svc_lo);
+        const int kc = __ldcg(&tab[c].k), mc = __ldcg(&tab[c].m);
+        const uint8_t* blk = A.stream_dst + __ldcg(&tab[c].offset);
+        const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
+        c_off = reinterpret_cast<const int32_t*>(blk);
+        c_rate = reinterpret_cast<const double*>(blk + rate_off);
+        c_bound = c_rate + mc;
+        c_table = reinterpret_cast<const uint16_t*>(c_bound + mc);
+        stream_wait(A, blk, c_table + mc, lane);   // the whole chunk block has landed
+      }
+      const int jl = j - c_scen_lo;
+      a0 = __ldcg(c_off + jl);
+      n = __ldcg(c_off + jl + 1) - a0;
+    } else {
+      a0 = A.scen_off[j];
+      n = A.scen_off[j + 1] - a0;
+    }
+    for (int b = 0; b < n; b += 32) {
+      if (b + lane < n) {
+        const int i = a0 + b + lane;
+        double tpc[5];
+        uint64_t m;
+        if (streamed) {
+          m = svc_configure(A, V, (int)__ldcg(c_table + i), __ldcg(c_rate + i), __ldcg(c_bound + i),
+                            (int64_t)c_svc_lo + i, tpc);
+        } else {
+          m = tile_service(A, V, i, tpc);
+        }
+        if (b == 0) {
+#pragma unroll
+          for (int cc = 0; cc < 5; cc++) S.tp[lane * 5 + cc] = tpc[cc];
+          S.meta[lane] = m;
+        }
+      }
+    }
+    __syncwarp();
+    plan_scenario_warp(A, W, j, n, S.tp, S.meta, n >= 0, lane);
+  }
+#ifdef PARVA_PHASE_TIMING
+  if (lane == 0 && blockIdx.x < 1024) g_warp_end[blockIdx.x][warp][0] = gtimer();
+#endif
+  if (lane == 0) {
+    __threadfence();
+    // last warp of the grid resets the counters for the next launch
+    if (atomicAdd(&A.work[1], 1u) == gridDim.x * PB_WARPS - 1) {
+      atomicExch(&A.work[0], 0u);
+      atomicExch(&A.work[2], 0u);
+      atomicExch(&A.work[1], 0u);
+    }
+  }
+}
+
 size_t index_smem_bytes(int n_tables, int64_t n_points, bool smem_index, bool lat_best) {
   size_t b = (size_t(n_tables) * 5 * 8 + 15) & ~size_t(15);
   if (smem_index) {
@@ -708,27 +867,39 @@ struct LaunchCfg {
   size_t smem;
 };
 
+static bool warp_mode(const PlanArgs& A) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("PARVA_K2_MODE");
+    env = e && e[0] == 't' ? 0 : 1;
+  }
+  return A.stream_src || (A.work && env == 1);
+}
+
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
-  const size_t smem = sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem) +
+  const bool wm = warp_mode(A);
+  const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
+  const size_t smem = sizeof(WarpScratch) * PB_WARPS + (wm ? sizeof(WarpSvc) * PB_WARPS : sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
   struct DevCfg { size_t conf, occ; int n_sm, per; };
-  static DevCfg s_cfg[kMaxDevices];
+  static DevCfg s_cfg[kMaxDevices][2];
   int dev = 0;
   cudaGetDevice(&dev);
-  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)];
+  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][wm];
   if (smem > D.conf) {
-    if (cudaFuncSetAttribute(plan_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
     D.conf = smem;
   }
   if (!D.n_sm) cudaDeviceGetAttribute(&D.n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (smem != D.occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per, plan_batch_kernel, PB_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per, fn, PB_THREADS, smem);
     D.occ = smem;
   }
   if (D.per < 1) return false;
-  int g = A.work ? (A.n_scen + A.tile_scen - 1) / A.tile_scen : (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  int g = wm ? (A.n_scen + PB_WARPS - 1) / PB_WARPS
+             : A.work ? (A.n_scen + A.tile_scen - 1) / A.tile_scen : (A.n_scen + PB_WARPS - 1) / PB_WARPS;
   if (g > D.n_sm * D.per) g = D.n_sm * D.per;
   L->grid = g < 1 ? 1 : g;
   L->smem = smem;
@@ -745,7 +916,8 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.work && A.tile_scen < 1) return PARVA_BAD_INPUT;
   LaunchCfg L;
   if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
-  plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+  if (warp_mode(A)) plan_warp_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+  else plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 
@@ -756,7 +928,7 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
   PlanArgs copy = A;
   void* args[] = {&copy};
   cudaKernelNodeParams p = {};
-  p.func = (void*)plan_batch_kernel;
+  p.func = warp_mode(A) ? (void*)plan_warp_kernel : (void*)plan_batch_kernel;
   p.gridDim = dim3(L.grid);
   p.blockDim = dim3(PB_THREADS);
   p.sharedMemBytes = (unsigned)L.smem;

@@ -81,8 +81,47 @@ def run(n=10_000, fmt=0):
     print("  warp cycles per scenario: cfgload %.0f relocate %.0f optimize %.0f emit %.0f" % tuple(tot))
 
 
+def run_mapped(n=10_000):
+    """Streamed zero-copy entry: loader finish times vs warp finish times."""
+    import numpy as np
+    import torch
+    from paper_2409_14447_b200 import _native as N
+    lib = C.CDLL(str(LIB))
+    for name in ("parva_plan_batch_workspace", "parva_plan_host_scratch", "parva_plan_general_workspace",
+                 "parva_plan_host_packed_scratch", "parva_plan_host_mapped_scratch"):
+        getattr(lib, name).restype = C.c_size_t
+    lib.parva_stream_bytes.restype = C.c_int64
+    lib.parva_stream_pack.restype = C.c_int64
+    N._LIB = lib
+    from paper_2409_14447_b200 import batch as B
+    from paper_2409_14447_b200 import workloads as W
+    from bench import c2_inputs
+    fx = W.load_fixtures()
+    dt = N.device_tables_for(fx.tables)
+    off, tab, rate, bound = c2_inputs(fx, n, 0)
+    mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64)
+    for _ in range(10):
+        mb.run(dt)
+    torch.cuda.synchronize()
+    ph = np.zeros((1024, 4), dtype=np.uint64)
+    we = np.zeros((1024, 16, 2), dtype=np.uint64)
+    cyc = np.zeros((1024, 16, 4), dtype=np.uint64)
+    lib.parva_dbg_phase(ph.ctypes.data_as(C.c_void_p), we.ctypes.data_as(C.c_void_p), cyc.ctypes.data_as(C.c_void_p))
+    used = ph[:, 0] > 0
+    ph = ph[used].astype(np.int64)
+    we = we[used].astype(np.int64)
+    t0 = ph[:, 0].min()
+    load_end = (ph[:, 1] - t0) / 1e3
+    wend = (we[:, :, 0] - t0) / 1e3
+    print(f"CTAs {used.sum()}  start spread {(ph[:, 0].max() - t0) / 1e3:.2f} us")
+    print(f"  loader CTAs phase-1 end: min {load_end.min():.2f} p50 {np.median(load_end):.2f} max {load_end.max():.2f} us")
+    print(f"  warp end: min {wend.min():.2f} p50 {np.median(wend):.2f} p90 {np.percentile(wend, 90):.2f} max {wend.max():.2f} us")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2:])
+    elif sys.argv[1] == "mapped":
+        run_mapped(int(sys.argv[2]) if len(sys.argv) > 2 else 10_000)
     else:
         run(int(sys.argv[2]) if len(sys.argv) > 2 else 10_000, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
