@@ -378,8 +378,8 @@ class MappedHostBatch:
         self.in_bytes = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(self._off32), C.c_int32(chunk_scen)))
         if self.in_bytes < 0:
             raise ValueError("invalid scenario offsets")
-        self.h_in = torch.zeros(self.in_bytes, dtype=torch.uint8).pin_memory()
-        self.h_out = torch.zeros(self.layout.out_bytes, dtype=torch.uint8).pin_memory()
+        self.h_in = torch.zeros(max(self.in_bytes, 256), dtype=torch.uint8).pin_memory()
+        self.h_out = torch.zeros(max(self.layout.out_bytes, 256), dtype=torch.uint8).pin_memory()
         self.scratch_bytes = int(L.parva_plan_host_mapped_scratch(C.c_int64(self.in_bytes)))
         self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda")
         self.fill(scen_off, svc_table, svc_rate, svc_bound)

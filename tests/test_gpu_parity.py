@@ -319,6 +319,65 @@ def test_host_entry_packed_vs_oracle(fx):
                     assert sorted(int(x) for x in spills["scenario"]) == exp_sp
 
 
+def _mapped_raw(mb):
+    """(config records, plan records as written) of a MappedHostBatch."""
+    from paper_2409_14447_b200.records import PLAN64_DTYPE, PLAN_DTYPE
+    lay, buf = mb.layout, mb.h_out.numpy()
+    pdt = PLAN64_DTYPE if mb.plan_bytes == 64 else PLAN_DTYPE
+    return buf[lay.out_plan:lay.out_plan + mb.plan_bytes * mb.n_scen].view(pdt)
+
+
+def test_host_entry_mapped_vs_oracle(fx):
+    """parva_plan_host_mapped (in-kernel PCIe streaming, records written to
+    mapped host memory) == oracle, for every record format and chunking;
+    repeated calls reuse the scratch (slice-flag epochs)."""
+    from paper_2409_14447_b200.records import plan64_view, tiny_config
+    sb = W.scenario_batch(fx, 7_003, seed=11)
+    n, M = sb.rate.shape
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
+    dt = N.device_tables_for(fx.tables)
+    ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, rate, bound)
+    conv = {0: lambda c: c, 1: compact_config, 2: tiny_config}
+    for fmt, pbytes, chunk in ((2, 64, 64), (1, 128, 16), (0, 128, 1000), (2, 64, 1), (2, 128, 7003)):
+        mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=fmt, plan_bytes=pbytes, chunk_scen=chunk)
+        for _ in range(3):
+            mb.h_out.zero_()
+            mb.run(dt)
+            cfg, plan = mb.outputs()
+            assert plan.tobytes() == oplan.tobytes(), (fmt, pbytes, chunk)
+            assert cfg.tobytes() == conv[fmt](ocfg).tobytes(), (fmt, pbytes, chunk)
+            if pbytes == 64:
+                exp64, _ = plan64_view(oplan, n)
+                assert _mapped_raw(mb).tobytes() == exp64.tobytes()
+
+
+def test_host_entry_mapped_fuzz(fx):
+    """Mapped entry on ragged batches: empty scenarios, >32 services
+    (CAPACITY), zero rates, infeasible SLOs, options; and 0 / 1 scenarios."""
+    import random
+    from paper_2409_14447_b200.records import tiny_config
+    rng = random.Random(77)
+    dt = N.device_tables_for(fx.tables)
+    pt = pack_tables(fx.tables)
+    nm = len(fx.models)
+    for trial, n_scen in enumerate((0, 1, 2, 500, 2500)):
+        sizes = [rng.choice([0, 1, 3, 11, 11, 20, 33, 40]) for _ in range(n_scen)]
+        total = int(sum(sizes))
+        tab = np.array([rng.randrange(nm) for _ in range(total)], dtype=np.int32)
+        rate = np.array([0.0 if rng.random() < 0.05 else math_exp(rng.uniform(1.0, 9.0)) for _ in range(total)])
+        bound = np.array([math_exp(rng.uniform(2.5, 8.0)) / 2.0 for _ in range(total)])
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        optimize, threshold = rng.random() < 0.8, rng.choice([2, 4, 5])
+        ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound, optimize=optimize, threshold=threshold)
+        mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, chunk_scen=rng.choice([1, 5, 64]))
+        mb.run(dt, optimize=optimize, threshold=threshold)
+        cfg, plan = mb.outputs()
+        assert plan.tobytes() == oplan.tobytes(), trial
+        assert cfg.tobytes() == tiny_config(ocfg).tobytes(), trial
+
+
 def test_reconfigure_service(fx):
     """§III-F re-planning (allocator.py:494-537) + diff_maps (:484-491) vs reference goldens."""
     for i, c in enumerate(golden("reconfigure_cases.json")):
