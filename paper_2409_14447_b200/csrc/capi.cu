@@ -556,7 +556,6 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
     A.spill = out + L.out_spill;
     A.spill_direct = 1;
     A.work = work;
-    A.tile_scen = 1;
     A.stream_src = (const uint8_t*)d_in;
     A.stream_dst = staging;
     A.stream_bytes = in_bytes;

@@ -34,11 +34,10 @@ struct PlanArgs {
   int spill_cap;
   int32_t* spill_count;          // 64-byte records: spill list header
   uint8_t* spill;                // spill_cap entries of kSpillEntry bytes
-  // streamed mode (zero-copy host entry): CTAs take tiles of tile_scen
-  // scenarios from work[0]; work[1] counts finished CTAs (the last one
-  // resets both, so the counters are zero between launches)
+  // warp kernel (zero-copy host entry): warps take scenarios from work[0],
+  // loader warps take input slices from work[2]; work[1] counts finished
+  // warps (the last one resets all three, so they are zero between launches)
   uint32_t* work = nullptr;
-  int tile_scen = 0;
   int spill_direct = 0;          // 64-byte records: full record at spill + 128 * scenario
   // streamed inputs (warp kernel, zero-copy host entry): the packed input
   // block at stream_src (mapped host memory) is copied in kStreamSlice-byte

@@ -291,7 +291,6 @@ struct alignas(16) TileSmem {
   uint64_t meta[kTileSvc];                // count | opt << 48 | last << 52 | status << 56 (15 = none)
   int32_t off[PB_THREADS + 1];            // tile scenario offsets (absolute service index)
   int32_t next;                           // next tile scenario to plan
-  int32_t tile;                           // streamed mode: tile taken from the device counter
 };
 
 __device__ __forceinline__ uint64_t pack_meta(int opt, int last, int status, long long count) {
@@ -620,25 +619,10 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   WarpScratch& W = scratch[warp];
 
-  // this CTA's contiguous block of scenarios, or (streamed mode) tiles of
-  // tile_scen scenarios taken in order from a device counter
-  int k, k1;
-  if (A.work) {
-    k = 0; k1 = 0;
-  } else {
-    const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
-    k = blockIdx.x * per;
-    k1 = min(A.n_scen, k + per);
-  }
-  for (;;) {
-  if (A.work) {
-    if (tid == 0) T.tile = (int)atomicAdd(&A.work[0], 1u);
-    __syncthreads();
-    const int t = T.tile;
-    if ((long long)t * A.tile_scen >= A.n_scen) break;
-    k = t * A.tile_scen;
-    k1 = min(A.n_scen, k + A.tile_scen);
-  }
+  // this CTA's contiguous block of scenarios
+  const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
+  int k = blockIdx.x * per;
+  const int k1 = min(A.n_scen, k + per);
   while (k < k1) {
     // tile = the longest run of scenarios from k with <= kTileSvc services
     // (at least one scenario; offsets are non-decreasing)
@@ -687,15 +671,6 @@ __global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
 #endif
     __syncthreads();
     k += n_tile;
-  }
-  if (!A.work) break;
-  }
-  if (A.work && tid == 0) {
-    __threadfence();
-    if (atomicAdd(&A.work[1], 1u) == gridDim.x - 1) {   // last CTA: reset for the next launch
-      atomicExch(&A.work[0], 0u);
-      atomicExch(&A.work[1], 0u);
-    }
   }
   PHASE(3);
 }
@@ -867,14 +842,9 @@ struct LaunchCfg {
   size_t smem;
 };
 
-static bool warp_mode(const PlanArgs& A) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = std::getenv("PARVA_K2_MODE");
-    env = e && e[0] == 't' ? 0 : 1;
-  }
-  return A.stream_src || (A.work && env == 1);
-}
+// device-resident batches: the tile kernel (configure a tile with every
+// thread, then plan); streamed batches: the warp-autonomous kernel
+static bool warp_mode(const PlanArgs& A) { return A.stream_src != nullptr; }
 
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
@@ -898,8 +868,7 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
     D.occ = smem;
   }
   if (D.per < 1) return false;
-  int g = wm ? (A.n_scen + PB_WARPS - 1) / PB_WARPS
-             : A.work ? (A.n_scen + A.tile_scen - 1) / A.tile_scen : (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  int g = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
   if (g > D.n_sm * D.per) g = D.n_sm * D.per;
   L->grid = g < 1 ? 1 : g;
   L->smem = smem;
@@ -913,7 +882,7 @@ int plan_batch_grid(const PlanArgs& A) {
 
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.n_scen <= 0) return PARVA_OK;
-  if (A.work && A.tile_scen < 1) return PARVA_BAD_INPUT;
+  if (A.stream_src && !A.work) return PARVA_BAD_INPUT;
   LaunchCfg L;
   if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
   if (warp_mode(A)) plan_warp_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
