@@ -25,7 +25,13 @@
 
 namespace parva {
 
-constexpr int PB_WARPS = 16;
+#ifndef PARVA_PB_WARPS
+#define PARVA_PB_WARPS 16
+#endif
+#ifndef PARVA_PB_MINB
+#define PARVA_PB_MINB 2
+#endif
+constexpr int PB_WARPS = PARVA_PB_WARPS;
 constexpr int PB_THREADS = PB_WARPS * 32;
 constexpr int QCAP = 224;                 // > 31 GPUs x 7 slots: longer queues cannot fit
 
@@ -421,10 +427,14 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
     if (A.optimize) {
       // ----------------------------------------- optimize_allocation
       int next = 0;
-      for (int index = ngpus - 1; index >= 0; index--) {
+      // GPUs last -> first (allocator.py:382): the next GPU to drain is the
+      // highest-index one below the last that is non-empty with <= threshold
+      // GPCs (skipped GPUs are not touched, so checking them now is the same)
+      for (int index = ngpus; ;) {
+        const unsigned cand = __ballot_sync(0xffffffffu, lane < index && len > 0 && ngpc <= A.threshold);
+        if (!cand) break;
+        index = 31 - __clz(cand);
         const int nl = __shfl_sync(0xffffffffu, len, index);
-        const int ng = __shfl_sync(0xffffffffu, ngpc, index);
-        if (nl == 0 || ng > A.threshold) continue;
         const double sv_freed = freed;
         const int sv_order = order, sv_next = next;
         int q2n = 0, q1n = 0, fail = -1, fsvc = 0, rot = nl;
@@ -549,7 +559,12 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
     } else {
       spill = A.plan_bytes == 64 && need > 64 - 8;
       uint16_t* pay16 = reinterpret_cast<uint16_t*>(W.rec.payload);
-      for (int j = 0; j < mine; j++) pay16[incl - mine + j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+      {
+        uint16_t* dst16 = pay16 + (incl - mine);
+#pragma unroll
+        for (int j = 0; j < 7; j++)
+          if (j < mine) dst16[j] = (uint16_t)(lane << 11 | W.lst[lane][j]);
+      }
       if (lane < nd) pay16[n_place + lane] = W.diag[lane];
       if (lane < n && order > 0) {
         reinterpret_cast<double*>(W.rec.payload + led_off)[order - 1] = freed;
@@ -603,7 +618,7 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
   WCYC(3);
 }
 
-__global__ void __launch_bounds__(PB_THREADS, 2) plan_batch_kernel(PlanArgs A) {
+__global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
@@ -736,7 +751,7 @@ __device__ __forceinline__ void stream_wait(const PlanArgs& A, const void* p_lo,
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(PB_THREADS, 2) plan_warp_kernel(PlanArgs A) {
+__global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);

@@ -1,0 +1,113 @@
+#!/usr/bin/env python3
+"""A/B harness for K2 source variants: each variant is a set of text patches
+applied to a copy of csrc/; every variant is built into tools/_variants/ and
+timed on the C2 batch (device path + zero-copy e2e), with a parity check.
+
+    python tools/k2_variants.py build
+    python tools/k2_variants.py run
+"""
+import ctypes as C
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+OUT = REPO / "tools" / "_variants"
+PATCH_DIR = REPO / "tools" / "k2_patches"
+
+
+def variants():
+    """name -> (patch list, extra flags).  A patch file holds OLD/NEW blocks
+    separated by lines '<<<<' / '====' / '>>>>'."""
+    vs = {"base": ([], [])}
+    if PATCH_DIR.exists():
+        for f in sorted(PATCH_DIR.glob("*.patch")):
+            vs[f.stem] = ([f], [])
+    return vs
+
+
+def apply(src: str, patch: Path) -> str:
+    text = patch.read_text()
+    for block in text.split("<<<<\n")[1:]:
+        old, rest = block.split("====\n", 1)
+        new = rest.split(">>>>\n", 1)[0]
+        assert old in src, (patch, old[:80])
+        src = src.replace(old, new)
+    return src
+
+
+def build():
+    from paper_2409_14447_b200 import build as b
+    OUT.mkdir(parents=True, exist_ok=True)
+    for name, (patches, flags) in variants().items():
+        d = OUT / f"v_{name}" / "csrc"      # csrc/../../include -> OUT/include
+        if d.exists():
+            shutil.rmtree(d)
+        shutil.copytree(b.CSRC, d)
+        if not (OUT / "include").exists():
+            (OUT / "include").symlink_to(REPO / "include")
+        pb = d / "plan_batch.cu"
+        src = pb.read_text()
+        for p in patches:
+            src = apply(src, p)
+        pb.write_text(src)
+        lib = OUT / f"libk2_{name}.so"
+        inc = str(REPO / "include")
+        cmd = [b.NVCC, *b.FLAGS, *flags, "-o", str(lib), *[str(d / s) for s in b.SOURCES], "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        i = r.stderr.find("_ZN5parva17plan_batch_kernel")
+        print(name, r.returncode, r.stderr[i:i + 300].split("\n")[1:2], r.stderr[:300] if r.returncode else "")
+
+
+def run():
+    import time
+    import numpy as np
+    import torch
+    from paper_2409_14447_b200 import _native as N
+    from bench import c2_inputs
+    from paper_2409_14447_b200 import workloads as W
+    from paper_2409_14447_b200.tables import pack_tables
+    fx = W.load_fixtures()
+    off, tab, rate, bound = c2_inputs(fx, 10_000, 0)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    ref = None
+    for name in variants():
+        lib = C.CDLL(str(OUT / f"libk2_{name}.so"))
+        for fn in ("parva_plan_batch_workspace", "parva_plan_host_scratch", "parva_plan_general_workspace",
+                   "parva_plan_host_packed_scratch", "parva_plan_host_mapped_scratch"):
+            getattr(lib, fn).restype = C.c_size_t
+        lib.parva_stream_bytes.restype = C.c_int64
+        lib.parva_stream_pack.restype = C.c_int64
+        N._LIB = lib
+        from paper_2409_14447_b200 import batch as B
+        dt = N.DeviceTables(pack_tables(fx.tables))
+        d = [N.to_device(a) for a in (off, tab, rate, bound)]
+        res = B.plan_batch(dt, *d)
+        got = res.host()[1].copy()
+        ref = got if ref is None else ref
+        s = torch.cuda.current_stream()
+        ts = []
+        for i in range(80):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            B.plan_batch(dt, *d, out=res)
+            b.record(s)
+            torch.cuda.synchronize()
+            if i >= 10:
+                ts.append(a.elapsed_time(b) * 1e3)
+        mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64)
+        for _ in range(20):
+            mb.run(dt)
+        t0 = time.perf_counter()
+        for _ in range(300):
+            mb.run(dt)
+        e2e = (time.perf_counter() - t0) / 300 * 1e6
+        ok = got.tobytes() == ref.tobytes() and mb.outputs()[1].tobytes() == ref.tobytes()
+        print(f"{name:24s}: device K2 p50 {np.median(ts):6.1f} us  min {min(ts):6.1f}   e2e {e2e:6.1f} us  ok {ok}")
+
+
+if __name__ == "__main__":
+    build() if sys.argv[1] == "build" else run()
