@@ -424,9 +424,8 @@ static int loaders_for(int64_t in_bytes) {
     env = e ? std::max(0, std::atoi(e)) : 0;
   }
   if (env > 0) return env;
-  // ~400 KB in flight covers the PCIe bandwidth-latency product (~8 us x 50
-  // GB/s) while keeping the slices landing roughly in order
-  return (int)std::min<int64_t>(96, std::max<int64_t>(1, (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice));
+  // 16 loaders x 2 x 8 KB in flight saturate PCIe (tools/zc/tma_probe.cu)
+  return (int)std::min<int64_t>(16, std::max<int64_t>(1, (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice));
 }
 
 int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32_t chunk_scen) {

@@ -41,7 +41,7 @@ struct PlanArgs {
   int spill_direct = 0;          // 64-byte records: full record at spill + 128 * scenario
   // streamed inputs (warp kernel, zero-copy host entry): the packed input
   // block at stream_src (mapped host memory) is copied in kStreamSlice-byte
-  // slices, in order, by n_loaders loader warps into stream_dst (device; the
+  // slices, in order, by n_loaders loader threads into stream_dst (device; the
   // scen_off / svc_* pointers point into it); slice s has landed when
   // slice_flag[s] == epoch
   const uint8_t* stream_src = nullptr;
@@ -52,7 +52,8 @@ struct PlanArgs {
   int n_loaders = 0;
 };
 
-constexpr int kStreamSlice = 4096;
+constexpr int kStreamSlice = 8192;   // streamed input slice (one TMA bulk copy)
+constexpr int kLoaderBufs = 3;       // shared-memory slice buffers per loader
 
 constexpr int kSpillEntry = 144;
 constexpr int kMaxDevices = 64;    // per-device launch-configuration caches   // int32 scenario, 12 B pad, 128-byte record

@@ -710,32 +710,57 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Streamed mode: copy input slices host -> device in ticket order (work[2]).
-// Few loader warps keep ~n_loaders * 4 KB in flight, so slices land roughly
-// in order at PCIe speed instead of every warp's reads interleaving.
-__device__ __forceinline__ void stream_loader(const PlanArgs& A, int lane) {
-  const int n_slices = (int)((A.stream_bytes + kStreamSlice - 1) / kStreamSlice);
-  for (;;) {
-    int s = 0;
-    if (lane == 0) s = (int)atomicAdd(&A.work[2], 1u);
-    s = __shfl_sync(0xffffffffu, s, 0);
-    if (s >= n_slices) break;
-    const int64_t base = (int64_t)s * kStreamSlice;
-    uint4 v[kStreamSlice / 512];
-#pragma unroll
-    for (int i = 0; i < kStreamSlice / 512; i++) {
-      const int64_t o = base + i * 512 + lane * 16;
-      if (o < A.stream_bytes) v[i] = __ldcv(reinterpret_cast<const uint4*>(A.stream_src + o));
+// Streamed mode: one thread per loader CTA is a DMA engine.  It takes input
+// slices in ticket order (work[2]) and moves each host -> shared memory with
+// a TMA bulk copy (cp.async.bulk reads the pinned, mapped host block over
+// PCIe), then shared -> device staging with a bulk store, double-buffered;
+// a slice is published (slice_flag[s] = epoch, release) once its store has
+// completed.  A handful of loaders keeps ~n_loaders * 16 KB in flight: full
+// PCIe bandwidth while the slices still land nearly in order.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Two warps of a loader CTA: warp 0 (one lane) issues the host -> shared
+// loads and never fences, so its PCIe reads stay in flight; warp 1 (one lane)
+// stores each landed slice to device memory, waits for the store, publishes
+// the slice flag and hands the buffer back (full / empty mbarrier pairs;
+// separate warps, so the store waits never block the load issue).
+__device__ __noinline__ void stream_loader(const PlanArgs& A, uint8_t* buf, uint64_t* bars, int role) {
+  const int64_t n_slices = (A.stream_bytes + kStreamSlice - 1) / kStreamSlice;
+  const int nl = A.n_loaders;
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kLoaderBufs;
+  // loader L moves slices L, L + nl, L + 2 nl, ... (all loaders advance at
+  // PCIe pace, so the slices land in order)
+  if (role == 0) {
+    int i = 0;
+    for (int64_t s = blockIdx.x; s < n_slices; s += nl, i++) {
+      const int b = i % kLoaderBufs;
+      if (i >= kLoaderBufs) mbar_wait(&empty[b], (uint32_t)((i / kLoaderBufs - 1) & 1));
+      const int64_t o = s * kStreamSlice;
+      const uint32_t sz = (uint32_t)min((int64_t)kStreamSlice, A.stream_bytes - o);
+      mbar_arrive_expect_tx(&full[b], sz);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(buf + b * kStreamSlice)),
+          "l"(A.stream_src + o), "r"(sz), "r"(smem_addr(&full[b]))
+          : "memory");
     }
-#pragma unroll
-    for (int i = 0; i < kStreamSlice / 512; i++) {
-      const int64_t o = base + i * 512 + lane * 16;
-      if (o < A.stream_bytes) __stcg(reinterpret_cast<uint4*>(A.stream_dst + o), v[i]);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
+  } else {
+    int i = 0;
+    for (int64_t s = blockIdx.x; s < n_slices; s += nl, i++) {
+      const int b = i % kLoaderBufs;
+      mbar_wait(&full[b], (uint32_t)((i / kLoaderBufs) & 1));
+      const int64_t o = s * kStreamSlice;
+      bulk_s2g(A.stream_dst + o, buf + b * kStreamSlice, (uint32_t)min((int64_t)kStreamSlice, A.stream_bytes - o));
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");      // slice s is in device memory
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       st_release_u32(&A.slice_flag[s], A.epoch);
+      mbar_arrive(&empty[b]);
     }
   }
 }
@@ -745,8 +770,12 @@ __device__ __forceinline__ void stream_wait(const PlanArgs& A, const void* p_lo,
   if (lane == 0) {
     const int64_t lo = (const uint8_t*)p_lo - A.stream_dst, hi = (const uint8_t*)p_hi - A.stream_dst;
     if (hi > lo)
-      for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++)
-        while (ld_acquire_u32(&A.slice_flag[s]) != A.epoch) __nanosleep(64);
+      for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++) {
+        // exponential back-off keeps thousands of waiting warps from
+        // hammering the flag lines in L2 while the loaders stream
+        for (unsigned ns = 128; ld_acquire_u32(&A.slice_flag[s]) != A.epoch; ns = ns < 2048 ? 2 * ns : ns)
+          __nanosleep(ns);
+      }
   }
   __syncwarp();
 }
@@ -756,14 +785,27 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
   __shared__ uint64_t bar;
+  __shared__ uint64_t loader_bars[2 * kLoaderBufs];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool streamed = A.stream_src != nullptr;
   PHASE(0);
-  // loader warps first (warp 0 of the first n_loaders CTAs), then they plan too
-  if (streamed && warp == 0 && (int)blockIdx.x < A.n_loaders) stream_loader(A, lane);
+  // loader threads first (thread 0 of the first n_loaders CTAs), then they plan too
+  if (streamed && (int)blockIdx.x < A.n_loaders) {
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < 2 * kLoaderBufs; b++) mbar_init(&loader_bars[b], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp < 2) {
+      if (lane == 0)
+        stream_loader(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, loader_bars, warp);
+      __syncwarp();
+    }
+  }
   PHASE(1);
-  const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, !A.cfg_given,
-                                 &bar);
+  const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS +
+                                        (streamed ? kLoaderBufs * kStreamSlice : 0),
+                                 !A.cfg_given, &bar);
   WarpScratch& W = scratch[warp];
   WarpSvc& S = wsvc[warp];
   // streamed mode: the input is a header (chunk table) followed by chunk
@@ -864,7 +906,8 @@ static bool warp_mode(const PlanArgs& A) { return A.stream_src != nullptr; }
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
   const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
-  const size_t smem = sizeof(WarpScratch) * PB_WARPS + (wm ? sizeof(WarpSvc) * PB_WARPS : sizeof(TileSmem)) +
+  const size_t smem = sizeof(WarpScratch) * PB_WARPS +
+                      (wm ? sizeof(WarpSvc) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice : sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
   struct DevCfg { size_t conf, occ; int n_sm, per; };
