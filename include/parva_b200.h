@@ -311,7 +311,9 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
  * stream, the planning and the D2H writes overlap.  Scratch:
  * parva_plan_host_mapped_scratch bytes of device memory (initialised by the
  * first call with it; one call at a time per scratch).  Synchronizes
- * `stream` before returning. */
+ * `stream` before returning.  The device address of the last few blocks is
+ * cached: call parva_forget_block before freeing a block. */
+void parva_forget_block(const void* h_block);
 int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes,
                         parva_chunk_layout* out);
 size_t parva_plan_host_mapped_scratch(int64_t in_bytes);

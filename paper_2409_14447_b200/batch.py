@@ -365,7 +365,7 @@ class MappedHostBatch:
     one launch plus a stream synchronize."""
 
     def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64,
-                 chunk_scen: int = 64):
+                 chunk_scen: int = 32):
         torch = N.require_cuda()
         L = N.lib()
         scen_off = np.asarray(scen_off, dtype=np.int64)
@@ -398,12 +398,27 @@ class MappedHostBatch:
             raise ValueError("parva_stream_pack failed (offsets changed shape?)")
 
     def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
-        rc = N.lib().parva_plan_host_mapped(
-            C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
-            C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes), C.c_void_p(self.h_out.data_ptr()),
-            C.c_int32(int(optimize)), C.c_int32(int(threshold)), C.c_int32(self.cfg_format),
-            C.c_int32(self.plan_bytes), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), N.stream_handle(stream))
-        N.check(rc, "parva_plan_host_mapped")
+        sh = N.stream_handle(stream)
+        key = (id(dt), bool(optimize), int(threshold), sh.value)
+        args = self._args.get(key) if hasattr(self, "_args") else None
+        if args is None:   # the argument tuple is built once per (tables, options, stream)
+            args = (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
+                    C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes), C.c_void_p(self.h_out.data_ptr()),
+                    C.c_int32(int(optimize)), C.c_int32(int(threshold)), C.c_int32(self.cfg_format),
+                    C.c_int32(self.plan_bytes), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), sh)
+            self._args = getattr(self, "_args", {})
+            self._args[key] = (args, dt)
+        else:
+            args = args[0]
+        N.check(N.lib().parva_plan_host_mapped(*args), "parva_plan_host_mapped")
+
+    def __del__(self):
+        try:
+            L = N.lib()
+            L.parva_forget_block(C.c_void_p(self.h_in.data_ptr()))
+            L.parva_forget_block(C.c_void_p(self.h_out.data_ptr()))
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
     @property
     def h2d_bytes(self) -> int:

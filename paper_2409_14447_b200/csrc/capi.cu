@@ -424,8 +424,9 @@ static int loaders_for(int64_t in_bytes) {
     env = e ? std::max(0, std::atoi(e)) : 0;
   }
   if (env > 0) return env;
-  // 16 loaders x 2 x 8 KB in flight saturate PCIe (tools/zc/tma_probe.cu)
-  return (int)std::min<int64_t>(16, std::max<int64_t>(1, (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice));
+  // 32 loader CTAs x 3 x 8 KB in flight: PCIe-rate streaming (~49 GB/s
+  // measured) while the slices still land nearly in order
+  return (int)std::min<int64_t>(32, std::max<int64_t>(1, (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice));
 }
 
 int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32_t chunk_scen) {
@@ -480,6 +481,45 @@ size_t parva_plan_host_mapped_scratch(int64_t in_bytes) {
   return 256 + up256(16) + up256(size_t(n_slices) * 4) + up256(size_t(in_bytes));
 }
 
+// (device, pointer) -> device address of a pinned block, or the pointer
+// itself for device memory; pageable memory is rejected.  A small cache of
+// the blocks used last keeps cudaPointerGetAttributes off the per-call path.
+struct MappedPtr {
+  int dev = -1;
+  const void* p = nullptr;
+  void* d = nullptr;
+  bool host = false;
+};
+static MappedPtr g_mapped_ptrs[8];
+static unsigned g_mapped_ptr_next = 0;
+static std::mutex g_mapped_mu;
+
+static bool mapped_ptr(int dev, const void* p, void** d, bool* host) {
+  {
+    std::lock_guard<std::mutex> lock(g_mapped_mu);
+    for (const auto& e : g_mapped_ptrs)
+      if (e.dev == dev && e.p == p) { *d = e.d; *host = e.host; return true; }
+  }
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  *host = at.type == cudaMemoryTypeHost;
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) *d = const_cast<void*>(p);
+  else if (at.type != cudaMemoryTypeHost) return false;      // pageable memory cannot be mapped
+  else if (cudaHostGetDevicePointer(d, const_cast<void*>(p), 0) != cudaSuccess) { cudaGetLastError(); return false; }
+  std::lock_guard<std::mutex> lock(g_mapped_mu);
+  MappedPtr& e = g_mapped_ptrs[g_mapped_ptr_next++ % 8];
+  e.dev = dev; e.p = p; e.d = *d; e.host = *host;
+  return true;
+}
+
+// Forget a block (call before freeing it, so a later allocation at the same
+// address is looked up again).
+void parva_forget_block(const void* p) {
+  std::lock_guard<std::mutex> lock(g_mapped_mu);
+  for (auto& e : g_mapped_ptrs)
+    if (e.p == p) e = MappedPtr{};
+}
+
 // scratch -> epoch of its slice flags (flags hold the epoch of the call that wrote them)
 struct MappedEpoch {
   int dev = -1;
@@ -500,25 +540,16 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
   if (parva_mapped_layout(n_scenarios, n_services, cfg_format, plan_bytes, &L) != PARVA_OK) return PARVA_BAD_INPUT;
   const size_t need = parva_plan_host_mapped_scratch(in_bytes);
   if (need == 0 || need > scratch_bytes) return PARVA_BAD_INPUT;
-  // pinned host blocks are mapped to device addresses; device blocks are used as they are
-  bool in_host = false;
-  auto dev_ptr = [](const void* p, void** d, bool* host) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
-    *host = at.type == cudaMemoryTypeHost;
-    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) { *d = const_cast<void*>(p); return true; }
-    if (at.type != cudaMemoryTypeHost) return false;          // pageable memory cannot be mapped
-    if (cudaHostGetDevicePointer(d, const_cast<void*>(p), 0) != cudaSuccess) { cudaGetLastError(); return false; }
-    return true;
-  };
-  void* d_in = nullptr;
-  void* d_out = nullptr;
-  bool out_host = false;
-  if (!dev_ptr(h_in, &d_in, &in_host) || !dev_ptr(h_out, &d_out, &out_host)) return PARVA_BAD_INPUT;
-  if (!in_host) return PARVA_BAD_INPUT;   // the streamed input block must be pinned host memory
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0;
   cudaGetDevice(&dev);
+  // pinned host blocks are mapped to device addresses (device blocks are used
+  // as they are); the lookup of the last blocks used is cached per device
+  bool in_host = false, out_host = false;
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  if (!mapped_ptr(dev, h_in, &d_in, &in_host) || !mapped_ptr(dev, h_out, &d_out, &out_host)) return PARVA_BAD_INPUT;
+  if (!in_host) return PARVA_BAD_INPUT;   // the streamed input block must be pinned host memory
   uint8_t* base = (uint8_t*)(((uintptr_t)d_scratch + 255) & ~uintptr_t(255));
   uint32_t* work = (uint32_t*)base;
   uint32_t* flags = (uint32_t*)(base + up256(16));

@@ -282,6 +282,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define PHASE(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_phase[blockIdx.x][i] = gtimer(); } while (0)
 __device__ unsigned long long g_warp_cyc[1024][PB_WARPS][4];
+__device__ unsigned long long g_warp_wait[1024][PB_WARPS][4];
 #define WCYC_START long long wc_t = clock64();
 #define WCYC(i) do { const long long wc_n = clock64(); \
     if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) g_warp_cyc[blockIdx.x][threadIdx.x >> 5][i] += wc_n - wc_t; \
@@ -618,32 +619,47 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
   WCYC(3);
 }
 
-__global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(PlanArgs A) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
-  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
-  __shared__ uint64_t bar;
-  PHASE(0);
-  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem), !A.cfg_given,
-                                 &bar);
-  PHASE(1);
+// Where a tile loop reads its scenarios: offsets indexable at [k, k1], the
+// per-service inputs, and the record index bases.  Streamed inputs were
+// written during this kernel, so they are read through L2 (ld.cg).
+struct TileSrc {
+  const int32_t* off;
+  const uint16_t* t16;            // table ids as u16 (packed formats), else t32
+  const int32_t* t32;
+  const double* rate;
+  const double* bound;
+  int scen_base;                  // plan record index = scen_base + k
+  int64_t svc_base;               // config record index = svc_base + i
+  bool cg;
+};
+
+template <typename T>
+__device__ __forceinline__ T src_ld(const T* p, bool cg) { return cg ? __ldcg(p) : *p; }
+
+// configure service i of a tile source (or load its given config record)
+__device__ __forceinline__ uint64_t src_service(const PlanArgs& A, const IndexView& V, const TileSrc& S, int i,
+                                                double tpc[5]) {
+  if (A.cfg_given) return tile_service(A, V, S.svc_base + i, tpc);
+  const int t = S.t16 ? (int)src_ld(S.t16 + i, S.cg) : src_ld(S.t32 + i, S.cg);
+  return svc_configure(A, V, t, src_ld(S.rate + i, S.cg), src_ld(S.bound + i, S.cg), S.svc_base + i, tpc);
+}
+
+// Configure-then-plan over scenarios [k, k1) of a source, tile by tile: all
+// threads configure a tile's services into shared memory, then the warps
+// plan its scenarios (taken from a shared counter, so uneven scenarios
+// balance inside the CTA).  All threads of the CTA call it.
+__device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, WarpScratch& W,
+                                          const TileSrc& S, int k, const int k1, int tid, int lane) {
 #ifdef PARVA_PHASE_TIMING
   int dbg_n = 0;
   bool dbg_first = true;
 #endif
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  WarpScratch& W = scratch[warp];
-
-  // this CTA's contiguous block of scenarios
-  const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
-  int k = blockIdx.x * per;
-  const int k1 = min(A.n_scen, k + per);
   while (k < k1) {
     // tile = the longest run of scenarios from k with <= kTileSvc services
     // (at least one scenario; offsets are non-decreasing)
-    const int a0 = A.scen_off[k];
+    const int a0 = src_ld(S.off + k, S.cg);
     const int e = k + 1 + tid;
-    const int off_e = e <= k1 ? A.scen_off[e] : 0;
+    const int off_e = e <= k1 ? src_ld(S.off + e, S.cg) : 0;
     const bool fits = e <= k1 && (tid == 0 || off_e - a0 <= kTileSvc);
     if (e <= k1) T.off[tid + 1] = off_e;
     if (tid == 0) { T.off[0] = a0; T.next = 0; }
@@ -653,7 +669,7 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(P
     // configure the tile's services
     for (int i = a0 + tid; i < a_end; i += PB_THREADS) {
       double tpc[5];
-      const uint64_t m = tile_service(A, V, i, tpc);
+      const uint64_t m = src_service(A, V, S, i, tpc);
       const int li = i - a0;
       if (li < kTileSvc) {
 #pragma unroll
@@ -676,20 +692,40 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(P
       const int b = T.off[j] - a0;
       const int n = T.off[j + 1] - T.off[j];
       const bool in_tile = b >= 0 && n >= 0 && b + n <= kTileSvc;
-      plan_scenario_warp(A, W, k + j, n, T.tp + (in_tile ? b * 5 : 0), T.meta + (in_tile ? b : 0), in_tile, lane);
+      plan_scenario_warp(A, W, S.scen_base + k + j, n, T.tp + (in_tile ? b * 5 : 0), T.meta + (in_tile ? b : 0),
+                         in_tile, lane);
 #ifdef PARVA_PHASE_TIMING
       dbg_n++;
 #endif
     }
 #ifdef PARVA_PHASE_TIMING
-    if (lane == 0 && blockIdx.x < 1024) { g_warp_end[blockIdx.x][warp][0] = gtimer(); g_warp_end[blockIdx.x][warp][1] = dbg_n; }
+    if (lane == 0 && blockIdx.x < 1024) {
+      g_warp_end[blockIdx.x][threadIdx.x >> 5][0] = gtimer();
+      g_warp_end[blockIdx.x][threadIdx.x >> 5][1] = dbg_n;
+    }
 #endif
     __syncthreads();
     k += n_tile;
   }
-  PHASE(3);
 }
 
+__global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(PlanArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
+  __shared__ uint64_t bar;
+  PHASE(0);
+  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem), !A.cfg_given,
+                                 &bar);
+  PHASE(1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // this CTA's contiguous block of scenarios
+  const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
+  const int k = blockIdx.x * per;
+  const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
+  run_tiles(A, V, T, scratch[warp], S, k, min(A.n_scen, k + per), tid, lane);
+  PHASE(3);
+}
 
 // K2, warp-autonomous form: every warp takes scenarios one at a time from a
 // device counter (work[0]) and configures its own scenario (lane = service,
@@ -729,7 +765,7 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
 // stores each landed slice to device memory, waits for the store, publishes
 // the slice flag and hands the buffer back (full / empty mbarrier pairs;
 // separate warps, so the store waits never block the load issue).
-__device__ __noinline__ void stream_loader(const PlanArgs& A, uint8_t* buf, uint64_t* bars, int role) {
+__device__ __forceinline__ void stream_loader(const PlanArgs& A, uint8_t* buf, uint64_t* bars, int role) {
   const int64_t n_slices = (A.stream_bytes + kStreamSlice - 1) / kStreamSlice;
   const int nl = A.n_loaders;
   uint64_t* full = bars;
@@ -765,18 +801,21 @@ __device__ __noinline__ void stream_loader(const PlanArgs& A, uint8_t* buf, uint
   }
 }
 
-// Streamed mode: wait until the input bytes [lo, hi) have landed.
+// Streamed mode: wait (this thread) until the input bytes [lo, hi) have landed.
+__device__ __forceinline__ void stream_wait_thread(const PlanArgs& A, const void* p_lo, const void* p_hi) {
+  const int64_t lo = (const uint8_t*)p_lo - A.stream_dst, hi = (const uint8_t*)p_hi - A.stream_dst;
+  if (hi > lo)
+    for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++) {
+      // exponential back-off keeps thousands of waiting warps from
+      // hammering the flag lines in L2 while the loaders stream
+      for (unsigned ns = 128; ld_acquire_u32(&A.slice_flag[s]) != A.epoch; ns = ns < 2048 ? 2 * ns : ns)
+        __nanosleep(ns);
+    }
+}
+
+// the same for a warp (lane 0 waits)
 __device__ __forceinline__ void stream_wait(const PlanArgs& A, const void* p_lo, const void* p_hi, int lane) {
-  if (lane == 0) {
-    const int64_t lo = (const uint8_t*)p_lo - A.stream_dst, hi = (const uint8_t*)p_hi - A.stream_dst;
-    if (hi > lo)
-      for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++) {
-        // exponential back-off keeps thousands of waiting warps from
-        // hammering the flag lines in L2 while the loaders stream
-        for (unsigned ns = 128; ld_acquire_u32(&A.slice_flag[s]) != A.epoch; ns = ns < 2048 ? 2 * ns : ns)
-          __nanosleep(ns);
-      }
-  }
+  if (lane == 0) stream_wait_thread(A, p_lo, p_hi);
   __syncwarp();
 }
 
@@ -827,6 +866,9 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
     j = __shfl_sync(0xffffffffu, j, 0);
     if (j >= A.n_scen) break;
     int a0, n;
+#ifdef PARVA_PHASE_TIMING
+    long long wt0 = clock64(), wt1 = wt0;
+#endif
     if (streamed) {
       const int cj = min(j / ch_scen, n_ch - 1);     // chunks hold ch_scen scenarios (the last one fewer)
       if (cj != c) {
@@ -846,6 +888,9 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
       const int jl = j - c_scen_lo;
       a0 = __ldcg(c_off + jl);
       n = __ldcg(c_off + jl + 1) - a0;
+#ifdef PARVA_PHASE_TIMING
+      wt1 = clock64();
+#endif
     } else {
       a0 = A.scen_off[j];
       n = A.scen_off[j + 1] - a0;
@@ -869,7 +914,18 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
       }
     }
     __syncwarp();
+#ifdef PARVA_PHASE_TIMING
+    long long wt2 = clock64();
+#endif
     plan_scenario_warp(A, W, j, n, S.tp, S.meta, n >= 0, lane);
+#ifdef PARVA_PHASE_TIMING
+    if (lane == 0 && blockIdx.x < 1024) {
+      g_warp_wait[blockIdx.x][warp][0] += wt1 - wt0;
+      g_warp_wait[blockIdx.x][warp][1] += wt2 - wt1;
+      g_warp_wait[blockIdx.x][warp][2] += clock64() - wt2;
+      g_warp_wait[blockIdx.x][warp][3] += 1;
+    }
+#endif
   }
 #ifdef PARVA_PHASE_TIMING
   if (lane == 0 && blockIdx.x < 1024) g_warp_end[blockIdx.x][warp][0] = gtimer();
@@ -906,6 +962,7 @@ static bool warp_mode(const PlanArgs& A) { return A.stream_src != nullptr; }
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
   const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
+  const int kind = wm ? 1 : 0;
   const size_t smem = sizeof(WarpScratch) * PB_WARPS +
                       (wm ? sizeof(WarpSvc) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice : sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
@@ -914,7 +971,7 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   static DevCfg s_cfg[kMaxDevices][2];
   int dev = 0;
   cudaGetDevice(&dev);
-  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][wm];
+  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][kind];
   if (smem > D.conf) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
@@ -968,7 +1025,8 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
 #ifdef PARVA_PHASE_TIMING
 extern "C" int parva_dbg_phase(unsigned long long* phase, unsigned long long* warp_end, unsigned long long* cyc) {
   cudaMemcpyFromSymbol(phase, parva::g_phase, sizeof(parva::g_phase));
-  cudaMemcpyFromSymbol(cyc, parva::g_warp_cyc, sizeof(parva::g_warp_cyc));
+  cudaMemcpyFromSymbol(cyc, std::getenv("PARVA_DBG_WAIT") ? parva::g_warp_wait : parva::g_warp_cyc,
+                       sizeof(parva::g_warp_cyc));
   return cudaMemcpyFromSymbol(warp_end, parva::g_warp_end, sizeof(parva::g_warp_end)) == cudaSuccess ? 0 : 1;
 }
 #endif

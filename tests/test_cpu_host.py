@@ -18,7 +18,7 @@ REPO = Path(__file__).resolve().parent.parent
 
 def _declared():
     text = (REPO / "include" / "parva_b200.h").read_text()
-    return sorted(set(re.findall(r"^(?:int|int64_t|size_t)\s+(parva_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|size_t|void)\s+(parva_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_library_exports_every_declared_symbol():
