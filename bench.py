@@ -40,6 +40,17 @@ METRIC = "scenarios scheduled/sec (configurator+allocator)"
 UNIT = "scenarios/s"
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        t = json.loads((REPO / "profiles" / "ncu_traffic.json").read_text())
+        k = t[kernel]
+        return int(k["dram_read"] + k["dram_write"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def peaks():
     try:
         p = json.loads(PEAKS_PATH.read_text())
@@ -315,8 +326,9 @@ def main():
         "gpu_launches": args.steps,
         "kernel_ms_per_step": kern_ms / args.steps,
         "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel (fused configure + relocate + optimize)", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("plan_batch_kernel"),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write per launch)",
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
         "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": mb.h2d_bytes, "d2h_bytes_per_step": mb.d2h_bytes,
@@ -434,7 +446,8 @@ def sweep_measure(args, torch, N, B, W, hbm, peak_src, local):
             "workloads": nw, "points": points, "ms_per_launch": ms, "value": nw / (ms / 1000.0),
             "unit": "workloads/s", "points_per_s": points / (ms / 1000.0),
             "roofline": {"bound": "hbm", "kernel": "configure_sweep_kernel", "achieved": achieved, "peak": hbm,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("configure_sweep_kernel"),
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": alg},
             "parity_vs_oracle_first_1000": bool(recs[:k].tobytes() == orec.tobytes()),
             "l2": "no flush: the 760 MB of profile points per launch exceed the 126 MB L2",
