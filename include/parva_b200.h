@@ -380,6 +380,36 @@ size_t parva_plan_general_workspace(const parva_general_problem* p, int32_t gpu_
 int parva_plan_general(const parva_general_problem* p, parva_general_result* r,
                        void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------- simulator */
+/* Batched run_simulation event loops (evaluation.py:337-416; SURVEY §8f row
+ * 4): one independent simulation per service, for any number of runs at
+ * once.  Service s owns arrivals [d_arr_off[s], d_arr_off[s+1]) (ms, sorted,
+ * from the reference's numpy RNG) and segments [d_seg_off[s], d_seg_off[s+1])
+ * in dispatch order (deployment-map order).  All arrays are device arrays. */
+typedef struct {
+  int32_t n_services;
+  const int64_t* d_arr_off;      /* [n_services + 1]                       */
+  const double*  d_arrivals;     /* ms                                     */
+  const int32_t* d_seg_off;      /* [n_services + 1]                       */
+  const double*  d_seg_ms;       /* segment service time (profiled latency) */
+  const int32_t* d_seg_batch;
+  const int32_t* d_seg_lanes;    /* process count                          */
+  const double*  d_slo;          /* per service: client-facing SLO (ms)     */
+  const double*  d_horizon_ms;   /* per service: its run's horizon          */
+} parva_sim_problem;
+
+typedef struct {
+  int64_t* d_served;             /* [n_services]                            */
+  int64_t* d_batches;
+  int64_t* d_violations;
+  double*  d_latency;            /* batch b of service s at d_arr_off[s] + b */
+  double*  d_busy_ms;            /* per segment                              */
+  int32_t* d_status;             /* per service: PARVA_OK, or PARVA_CAPACITY
+                                    (> 32 segments or > 64 lanes)           */
+} parva_sim_result;
+
+int parva_simulate(const parva_sim_problem* problem, const parva_sim_result* result, void* stream);
+
 /* ------------------------------------------------ fine-grained API kernels */
 /* Lists k = [d_off[k], d_off[k+1]) of (instance size, throughput) triplets in
  * caller order (one thread per list). */

@@ -220,3 +220,19 @@ def plan_general(n_names, services, gpus, ledger, relocate, optimize, threshold,
     buf = _ResultBuf(n_names, gcap=gcap or max(64, len(gpus) + total_pl + 1))
     lib().oracle_plan_general(C.byref(P), C.byref(buf.s))
     return buf.decode(n_names)
+
+
+def simulate_service(arr_ms, seg_ms, seg_batch, seg_lanes, slo, horizon_ms):
+    """One service of run_simulation's event loop -> (served, batches, violations,
+    latencies[batches], busy_ms per segment)."""
+    arr = np.ascontiguousarray(arr_ms, dtype=np.float64)
+    ms = np.ascontiguousarray(seg_ms, dtype=np.float64)
+    b = np.ascontiguousarray(seg_batch, dtype=np.int32)
+    ln = np.ascontiguousarray(seg_lanes, dtype=np.int32)
+    lat = np.zeros(max(arr.shape[0], 1), dtype=np.float64)
+    busy = np.zeros(max(ms.shape[0], 1), dtype=np.float64)
+    out = np.zeros(3, dtype=np.int64)
+    lib().oracle_simulate_service(C.c_int64(arr.shape[0]), _p(arr), C.c_int32(ms.shape[0]), _p(ms), _p(b), _p(ln),
+                                  C.c_double(slo), C.c_double(horizon_ms), _p(out[0:1]), _p(out[1:2]),
+                                  _p(out[2:3]), _p(lat), _p(busy))
+    return int(out[0]), int(out[1]), int(out[2]), lat[:out[1]].copy(), busy[:ms.shape[0]].copy()

@@ -722,3 +722,118 @@ int oracle_configure_batch(const double* tp, const double* lat, const int32_t* b
   }
   return 0;
 }
+
+/* ------------------------------------------------------------ simulator */
+/* One service of run_simulation's event loop (evaluation.py:337-416),
+ * restated with a binary heap of (time, seq, kind, payload) as in the
+ * reference (heapq, evaluation.py:341-349).  Arrivals in ms, sorted. */
+typedef struct { double t; int64_t seq; int kind; int payload; } sim_ev;
+
+static int ev_less(const sim_ev* a, const sim_ev* b) {
+  if (a->t != b->t) return a->t < b->t;
+  return a->seq < b->seq;
+}
+
+static void heap_push(sim_ev* h, int* n, sim_ev e) {
+  int i = (*n)++;
+  h[i] = e;
+  while (i > 0) {
+    int p = (i - 1) / 2;
+    if (!ev_less(&h[i], &h[p])) break;
+    sim_ev tmp = h[i]; h[i] = h[p]; h[p] = tmp; i = p;
+  }
+}
+
+static sim_ev heap_pop(sim_ev* h, int* n) {
+  sim_ev top = h[0];
+  h[0] = h[--(*n)];
+  int i = 0;
+  for (;;) {
+    int l = 2 * i + 1, r = l + 1, m = i;
+    if (l < *n && ev_less(&h[l], &h[m])) m = l;
+    if (r < *n && ev_less(&h[r], &h[m])) m = r;
+    if (m == i) break;
+    sim_ev tmp = h[i]; h[i] = h[m]; h[m] = tmp; i = m;
+  }
+  return top;
+}
+
+typedef struct {
+  const double* arr; int64_t na; const double* seg_ms; const int32_t* seg_batch; double slo, horizon;
+  sim_ev* heap; int nh; int* free_seg; int free_lanes, wake;
+  int64_t seq, ptr, qh, served, batches, viol;
+  double* lat; double* busy;
+} sim_state;
+
+/* schedule_wakeup (evaluation.py:362-366) */
+static void sim_wakeup(sim_state* S) {
+  if (S->wake || S->ptr >= S->na) return;
+  S->wake = 1;
+  sim_ev e = {S->arr[S->ptr], S->seq++, 1, 0};
+  heap_push(S->heap, &S->nh, e);
+}
+
+/* ingest (evaluation.py:353-360): searchsorted(side="right") on a monotone clock */
+static void sim_ingest(sim_state* S, double now) {
+  while (S->ptr < S->na && S->arr[S->ptr] <= now) S->ptr++;
+}
+
+/* dispatch (evaluation.py:368-388) */
+static void sim_dispatch(sim_state* S, double now) {
+  if (now >= S->horizon) return;
+  while (S->qh < S->ptr && S->free_lanes > 0) {
+    int g = 0;
+    while (S->free_seg[g] == 0) g++;
+    int64_t n = S->ptr - S->qh < S->seg_batch[g] ? S->ptr - S->qh : S->seg_batch[g];
+    double first = S->arr[S->qh];
+    S->qh += n;
+    double wait = now - first;
+    double latency = wait + S->seg_ms[g];
+    S->lat[S->batches++] = latency;
+    S->served += n;
+    if (latency > S->slo) S->viol++;
+    S->free_seg[g]--;
+    S->free_lanes--;
+    double rem = S->horizon - now;
+    double m = S->seg_ms[g] <= rem ? S->seg_ms[g] : rem;
+    S->busy[g] += m > 0.0 ? m : 0.0;
+    sim_ev c = {now + S->seg_ms[g], S->seq++, 0, g};
+    heap_push(S->heap, &S->nh, c);
+  }
+}
+
+int oracle_simulate_service(int64_t na, const double* arr, int32_t ns, const double* seg_ms,
+                            const int32_t* seg_batch, const int32_t* seg_lanes, double slo, double horizon_ms,
+                            int64_t* served_o, int64_t* batches_o, int64_t* viol_o, double* lat, double* busy) {
+  int cap = 1;
+  for (int g = 0; g < ns; g++) cap += seg_lanes[g];
+  sim_state S = {0};
+  S.arr = arr; S.na = na; S.seg_ms = seg_ms; S.seg_batch = seg_batch; S.slo = slo; S.horizon = horizon_ms;
+  S.heap = (sim_ev*)malloc(sizeof(sim_ev) * (size_t)(cap + 1));
+  S.free_seg = (int*)malloc(sizeof(int) * (size_t)(ns + 1));
+  S.lat = lat; S.busy = busy;
+  for (int g = 0; g < ns; g++) { S.free_seg[g] = seg_lanes[g]; S.free_lanes += seg_lanes[g]; busy[g] = 0.0; }
+  if (ns > 0) sim_wakeup(&S);
+  /* main loop (evaluation.py:395-416) */
+  while (S.nh > 0) {
+    sim_ev e = heap_pop(S.heap, &S.nh);
+    if (e.kind == 0) {
+      S.free_seg[e.payload]++;
+      S.free_lanes++;
+      if (e.t < horizon_ms) {
+        sim_ingest(&S, e.t);
+        sim_dispatch(&S, e.t);
+        if (S.qh == S.ptr) sim_wakeup(&S);
+      }
+    } else {
+      S.wake = 0;
+      sim_ingest(&S, e.t);
+      sim_dispatch(&S, e.t);
+      if (S.free_lanes > 0) sim_wakeup(&S);
+    }
+  }
+  free(S.heap);
+  free(S.free_seg);
+  *served_o = S.served; *batches_o = S.batches; *viol_o = S.viol;
+  return 0;
+}

@@ -107,7 +107,13 @@ int oracle_configure_batch(const double* tp, const double* lat, const int32_t* b
                            const double* q_rate, const double* q_bound,
                            parva_config_record* out, int32_t n_threads);
 
+/* run_simulation event loop for one service (evaluation.py:337-416) */
+int oracle_simulate_service(int64_t na, const double* arr, int32_t ns, const double* seg_ms,
+                            const int32_t* seg_batch, const int32_t* seg_lanes, double slo, double horizon_ms,
+                            int64_t* served_o, int64_t* batches_o, int64_t* viol_o, double* lat, double* busy);
+
 #ifdef __cplusplus
 }
 #endif
+
 #endif

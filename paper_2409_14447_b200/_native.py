@@ -58,6 +58,17 @@ class GeneralResult(C.Structure):
                 ("d_fallback", C.c_void_p)]
 
 
+class SimProblem(C.Structure):
+    _fields_ = [("n_services", C.c_int32), ("d_arr_off", C.c_void_p), ("d_arrivals", C.c_void_p),
+                ("d_seg_off", C.c_void_p), ("d_seg_ms", C.c_void_p), ("d_seg_batch", C.c_void_p),
+                ("d_seg_lanes", C.c_void_p), ("d_slo", C.c_void_p), ("d_horizon_ms", C.c_void_p)]
+
+
+class SimResult(C.Structure):
+    _fields_ = [("d_served", C.c_void_p), ("d_batches", C.c_void_p), ("d_violations", C.c_void_p),
+                ("d_latency", C.c_void_p), ("d_busy_ms", C.c_void_p), ("d_status", C.c_void_p)]
+
+
 EXPORTS = (
     "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
     "parva_plan_batch", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
@@ -65,7 +76,7 @@ EXPORTS = (
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
-    "parva_stream_pack", "parva_forget_block",
+    "parva_stream_pack", "parva_forget_block", "parva_simulate",
 )
 
 

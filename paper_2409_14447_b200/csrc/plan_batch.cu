@@ -808,7 +808,7 @@ __device__ __forceinline__ void stream_wait_thread(const PlanArgs& A, const void
     for (int64_t s = lo / kStreamSlice; s <= (hi - 1) / kStreamSlice; s++) {
       // exponential back-off keeps thousands of waiting warps from
       // hammering the flag lines in L2 while the loaders stream
-      for (unsigned ns = 128; ld_acquire_u32(&A.slice_flag[s]) != A.epoch; ns = ns < 2048 ? 2 * ns : ns)
+      for (unsigned ns = 64; ld_acquire_u32(&A.slice_flag[s]) != A.epoch; ns = ns < 512 ? 2 * ns : ns)
         __nanosleep(ns);
     }
 }
@@ -828,23 +828,22 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool streamed = A.stream_src != nullptr;
   PHASE(0);
-  // loader threads first (thread 0 of the first n_loaders CTAs), then they plan too
-  if (streamed && (int)blockIdx.x < A.n_loaders) {
-    if (threadIdx.x == 0) {
-      for (int b = 0; b < 2 * kLoaderBufs; b++) mbar_init(&loader_bars[b], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-    if (warp < 2) {
-      if (lane == 0)
-        stream_loader(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, loader_bars, warp);
-      __syncwarp();
-    }
+  if (streamed && (int)blockIdx.x < A.n_loaders && threadIdx.x == 0) {
+    for (int b = 0; b < 2 * kLoaderBufs; b++) mbar_init(&loader_bars[b], 1);
+    fence_mbar_init();
   }
-  PHASE(1);
+  // (load_index's block barriers also publish the loader mbarrier inits)
   const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS +
                                         (streamed ? kLoaderBufs * kStreamSlice : 0),
                                  !A.cfg_given, &bar);
+  // loader roles (warps 0 and 1 of the first n_loaders CTAs), then they plan
+  // too; the CTAs' other warps start planning right away
+  if (streamed && (int)blockIdx.x < A.n_loaders && warp < 2) {
+    if (lane == 0)
+      stream_loader(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, loader_bars, warp);
+    __syncwarp();
+  }
+  PHASE(1);
   WarpScratch& W = scratch[warp];
   WarpSvc& S = wsvc[warp];
   // streamed mode: the input is a header (chunk table) followed by chunk

@@ -1,8 +1,8 @@
 """Deployment metrics used by PlanResult.summary (reference evaluation.py:56-82).
 
-Post-processing of a DeploymentMap (SURVEY §8f "next" row 3); the
-discrete-event simulator of the reference (evaluation.py:85-464) is out of
-scope for this build.
+Post-processing of a DeploymentMap (SURVEY §8f "next" row 3).  The
+discrete-event simulator of the reference (evaluation.py:85-464) is in
+simulation.py (§8f row 4, event loops on the GPU).
 """
 
 from __future__ import annotations

@@ -1,0 +1,337 @@
+"""Discrete-event request simulator, batched on the GPU.
+
+Mirrors the reference's simulator API (migplan evaluation.py:85-464):
+`Workload`, `ServiceSimStats`, `SimReport`, `SegmentActivity`,
+`ActivityReport`, `run_simulation`, `slo_compliance`, `internal_slack` --
+same names, signatures, report fields and JSON.  `run_simulations` runs any
+number of (deployment, services, workload, horizon, seed) jobs in ONE kernel
+launch.
+
+Split of the work:
+  * arrivals: generated on the host with the reference's own numpy calls
+    (SeedSequence(seed).spawn over the sorted service ids, default_rng,
+    exponential gaps, chunked cumsum; evaluation.py:207-226, 327-335), so
+    they are bit-identical by construction;
+  * the event loop (evaluation.py:337-416) -- heap of completions and
+    arrival wakeups, FIFO batching, lane accounting, busy time -- runs on the
+    GPU, one thread per service (parva_simulate, csrc/simulate.cu): services
+    never interact in that loop, so each is an independent simulation;
+  * statistics (numpy mean / percentile / max, rounding) on the host, with
+    the reference's calls (evaluation.py:436-456).
+There is no CPU event loop here: without the CUDA library this raises
+NativeLibraryError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Mapping, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import SimulationConfigError, UndefinedMetricError, ValidationError
+from .evaluation import DEFAULT_SMS_PER_GPC
+from .mig import SLOT_COUNT
+
+ARRIVAL_KINDS = ("poisson", "deterministic")
+
+
+@dataclass(frozen=True)
+class SegmentActivity:
+    service_id: str
+    gpu: int
+    start_slot: int
+    instance_size: int
+    sm_count: int
+    activity: float
+
+
+@dataclass(frozen=True)
+class ActivityReport:
+    """Per-segment SM activity plus the provisioned totals (evaluation.py:46-52)."""
+
+    segments: tuple
+    gpu_count: int
+    sms_per_gpu: int
+
+
+def internal_slack(report: ActivityReport) -> float:
+    """One minus SM-weighted activity over all allocated SMs (evaluation.py:55-62)."""
+    if not report.segments:
+        raise UndefinedMetricError("internal slack is undefined for an empty report")
+    weighted = sum(s.sm_count * s.activity for s in report.segments)
+    total = sum(s.sm_count for s in report.segments)
+    return 1.0 - weighted / total
+
+
+@dataclass(frozen=True)
+class Workload:
+    """Arrival process: per-service rates in requests/s (evaluation.py:85-109)."""
+
+    rates: tuple
+    kind: str = "poisson"
+
+    def __post_init__(self) -> None:
+        if self.kind not in ARRIVAL_KINDS:
+            raise ValidationError(f"arrival kind {self.kind!r} not in {ARRIVAL_KINDS}")
+        for sid, rate in self.rates:
+            if rate < 0:
+                raise ValidationError(f"negative arrival rate for {sid!r}")
+
+    @classmethod
+    def from_services(cls, services, kind: str = "poisson", scale: float = 1.0) -> "Workload":
+        return cls(rates=tuple((s.id, s.request_rate * scale) for s in services), kind=kind)
+
+    def rate_map(self) -> dict:
+        return dict(self.rates)
+
+
+@dataclass
+class ServiceSimStats:
+    service_id: str
+    arrived: int = 0
+    served: int = 0
+    queued_at_end: int = 0
+    batches: int = 0
+    violations: int = 0
+    achieved_rps: float = 0.0
+    latency_ms: dict = field(default_factory=dict)
+
+    @property
+    def slo_compliance(self) -> float:
+        """Share of batches within the SLO; 1.0 with no batches (evaluation.py:122-127)."""
+        if self.batches == 0:
+            return 1.0
+        return 1.0 - self.violations / self.batches
+
+
+@dataclass
+class SimReport:
+    horizon_s: float
+    seed: int
+    kind: str
+    services: dict
+    activity: ActivityReport
+
+    def to_json_obj(self) -> dict:
+        """The reference's report JSON (evaluation.py:138-169)."""
+        return {
+            "horizon_s": self.horizon_s,
+            "seed": self.seed,
+            "arrivals": self.kind,
+            "services": {
+                sid: {"arrived": st.arrived, "served": st.served, "queued_at_end": st.queued_at_end,
+                      "batches": st.batches, "violations": st.violations, "slo_compliance": st.slo_compliance,
+                      "achieved_rps": round(st.achieved_rps, 6), "latency_ms": st.latency_ms}
+                for sid, st in sorted(self.services.items())
+            },
+            "segments": [
+                {"service": s.service_id, "gpu": s.gpu, "start_slot": s.start_slot,
+                 "instance_size": s.instance_size, "sm_count": s.sm_count, "activity": round(s.activity, 9)}
+                for s in self.activity.segments
+            ],
+        }
+
+    def csv_rows(self, run_label: str = "") -> list:
+        """One flat row per service (evaluation.py:171-192)."""
+        rows = []
+        for sid, st in sorted(self.services.items()):
+            rows.append({
+                "run": run_label, "seed": self.seed, "horizon_s": self.horizon_s, "arrivals": self.kind,
+                "service": sid, "arrived": st.arrived, "served": st.served, "queued_at_end": st.queued_at_end,
+                "batches": st.batches, "violations": st.violations, "slo_compliance": st.slo_compliance,
+                "achieved_rps": round(st.achieved_rps, 6), "latency_mean_ms": st.latency_ms.get("mean", ""),
+                "latency_p95_ms": st.latency_ms.get("p95", ""), "latency_max_ms": st.latency_ms.get("max", ""),
+            })
+        return rows
+
+
+def slo_compliance(report: SimReport) -> dict:
+    """Per-service share of batches meeting the SLO; None without batches (evaluation.py:195-204)."""
+    return {sid: (None if st.batches == 0 else 1.0 - st.violations / st.batches)
+            for sid, st in report.services.items()}
+
+
+def _arrival_times(kind: str, rate: float, horizon: float, rng: np.random.Generator) -> np.ndarray:
+    """All arrival instants in [0, horizon), seconds (evaluation.py:207-226).
+
+    The same numpy calls in the same order as the reference, so the stream
+    of each service's generator is consumed identically."""
+    if rate <= 0:
+        return np.empty(0)
+    if kind == "deterministic":
+        step = 1.0 / rate
+        n = int(math.floor(horizon / step))
+        times = np.arange(1, n + 1, dtype=np.float64) * step
+        return times[times < horizon]
+    chunks = []
+    total = 0.0
+    expected = max(int(rate * horizon * 1.2) + 16, 64)
+    while total < horizon:
+        gaps = rng.exponential(1.0 / rate, size=expected)
+        chunk = np.cumsum(gaps) + total
+        total = float(chunk[-1])
+        chunks.append(chunk)
+    times = np.concatenate(chunks)
+    return times[times < horizon]
+
+
+@dataclass
+class SimJob:
+    """One run_simulation call of a batch."""
+
+    dmap: object
+    tables: Mapping
+    services: Sequence
+    workload: Optional[Workload] = None
+    horizon_s: float = 60.0
+    seed: int = 0
+    sms_per_gpc: int = DEFAULT_SMS_PER_GPC
+
+
+class _Prepared:
+    """Host-side layout of one job: service order, arrivals, segments."""
+
+    def __init__(self, job: SimJob):
+        if job.horizon_s <= 0:
+            raise SimulationConfigError("horizon must be positive")
+        self.job = job
+        services_by_id = {s.id: s for s in job.services}
+        workload = job.workload or Workload.from_services(job.services)
+        self.kind = workload.kind
+        rates = workload.rate_map()
+        dmap = job.dmap
+        ordered = sorted({p.service_id for _, p in dmap.placements()} | set(rates) | set(services_by_id))
+        spawned = np.random.SeedSequence(job.seed).spawn(len(ordered))
+        self.ids = ordered
+        self.svc = []
+        self.arrivals = []
+        for sid, ss in zip(ordered, spawned):
+            svc = services_by_id.get(sid)
+            if svc is None:
+                raise SimulationConfigError(f"no service definition for {sid!r}")
+            rng = np.random.default_rng(ss)
+            self.svc.append(svc)
+            self.arrivals.append(_arrival_times(workload.kind, rates.get(sid, 0.0), job.horizon_s, rng) * 1000.0)
+        # segments in deployment-map order; per service in that order too (dispatch order)
+        index = {sid: i for i, sid in enumerate(ordered)}
+        self.segments = []            # (service position, placement, gpu id, service_ms)
+        for gpu in dmap.gpus:
+            for p in sorted(gpu.placements, key=lambda p: p.start_slot):
+                svc = services_by_id.get(p.service_id)
+                if svc is None:
+                    raise SimulationConfigError(f"no service definition for {p.service_id!r}")
+                table = job.tables.get(svc.model_id)
+                if table is None:
+                    raise SimulationConfigError(f"no profile table for model {svc.model_id!r}")
+                try:
+                    point = table.get(p.instance_size, p.batch_size, p.process_count)
+                except KeyError:
+                    raise SimulationConfigError(
+                        f"segment {p.service_id!r} ({p.instance_size},{p.batch_size},"
+                        f"{p.process_count}) has no matching profile point") from None
+                self.segments.append((index[p.service_id], p, gpu.id, point.latency))
+        self.horizon_ms = job.horizon_s * 1000.0
+        self.gpu_count = len(dmap.gpus)
+
+
+def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
+    """Batched run_simulation: every job's services simulated in one launch."""
+    torch = N.require_cuda()
+    preps = [_Prepared(j) for j in jobs]
+    arr_off, arrivals, seg_off, seg_ms, seg_batch, seg_lanes, slo, horizon = [0], [], [0], [], [], [], [], []
+    seg_rows = []                      # per flat service: list of global segment rows (job, position)
+    for pi, pr in enumerate(preps):
+        per_svc = [[] for _ in pr.ids]
+        for gi, (si, p, gid, ms) in enumerate(pr.segments):
+            per_svc[si].append(gi)
+        for si in range(len(pr.ids)):
+            a = pr.arrivals[si]
+            arrivals.append(a)
+            arr_off.append(arr_off[-1] + a.shape[0])
+            for gi in per_svc[si]:
+                _, p, _, ms = pr.segments[gi]
+                seg_ms.append(ms); seg_batch.append(p.batch_size); seg_lanes.append(p.process_count)
+                seg_rows.append((pi, gi))
+            seg_off.append(len(seg_ms))
+            slo.append(pr.svc[si].slo_latency)
+            horizon.append(pr.horizon_ms)
+    n = len(slo)
+    reports = []
+    if n == 0:
+        return [_report(pr, [], np.zeros(0), np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64), {})
+                for pr in preps]
+    dev = lambda a, dt: N.to_device(np.ascontiguousarray(a if len(a) else [0], dtype=dt))  # noqa: E731
+    d_arr_off = dev(arr_off, np.int64)
+    d_arr = dev(np.concatenate(arrivals) if arr_off[-1] else [], np.float64)
+    d_seg_off = dev(seg_off, np.int32)
+    d_seg_ms, d_seg_batch, d_seg_lanes = dev(seg_ms, np.float64), dev(seg_batch, np.int32), dev(seg_lanes, np.int32)
+    d_slo, d_h = dev(slo, np.float64), dev(horizon, np.float64)
+    o_served = torch.zeros(n, dtype=torch.int64, device="cuda")
+    o_batches = torch.zeros(n, dtype=torch.int64, device="cuda")
+    o_viol = torch.zeros(n, dtype=torch.int64, device="cuda")
+    o_lat = torch.zeros(max(arr_off[-1], 1), dtype=torch.float64, device="cuda")
+    o_busy = torch.zeros(max(len(seg_ms), 1), dtype=torch.float64, device="cuda")
+    o_status = torch.zeros(n, dtype=torch.int32, device="cuda")
+    P = N.SimProblem(n, N.ptr(d_arr_off).value, N.ptr(d_arr).value, N.ptr(d_seg_off).value, N.ptr(d_seg_ms).value,
+                     N.ptr(d_seg_batch).value, N.ptr(d_seg_lanes).value, N.ptr(d_slo).value, N.ptr(d_h).value)
+    R = N.SimResult(N.ptr(o_served).value, N.ptr(o_batches).value, N.ptr(o_viol).value, N.ptr(o_lat).value,
+                    N.ptr(o_busy).value, N.ptr(o_status).value)
+    N.check(N.lib().parva_simulate(C.byref(P), C.byref(R), N.stream_handle(stream)), "parva_simulate")
+    served, batches, viol = o_served.cpu().numpy(), o_batches.cpu().numpy(), o_viol.cpu().numpy()
+    status, lat, busy = o_status.cpu().numpy(), o_lat.cpu().numpy(), o_busy.cpu().numpy()
+    if (status != 0).any():
+        raise SimulationConfigError("a service has more than 32 segments or 64 lanes (simulator capacity)")
+    k = 0
+    for pi, pr in enumerate(preps):
+        m = len(pr.ids)
+        busy_by_seg = {}
+        for si in range(m):
+            for r in range(seg_off[k + si], seg_off[k + si + 1]):
+                busy_by_seg[seg_rows[r][1]] = busy[r]
+        lats = [lat[arr_off[k + si]:arr_off[k + si] + batches[k + si]] for si in range(m)]
+        reports.append(_report(pr, lats, served[k:k + m], batches[k:k + m], viol[k:k + m], arr_off[k:k + m + 1],
+                               busy_by_seg))
+        k += m
+    return reports
+
+
+def _report(pr: _Prepared, lats, served, batches, viol, arr_off, busy_by_seg) -> SimReport:
+    job = pr.job
+    activity = ActivityReport(
+        segments=tuple(
+            SegmentActivity(service_id=p.service_id, gpu=gid, start_slot=p.start_slot, instance_size=p.instance_size,
+                            sm_count=p.instance_size * job.sms_per_gpc,
+                            # Python floats, as in the reference: sum() compensates only exact floats
+                            activity=min(1.0, float(busy_by_seg.get(gi, 0.0)) / (p.process_count * pr.horizon_ms)))
+            for gi, (si, p, gid, ms) in enumerate(pr.segments)),
+        gpu_count=pr.gpu_count,
+        sms_per_gpu=SLOT_COUNT * job.sms_per_gpc,
+    )
+    out = {}
+    for si, sid in enumerate(pr.ids):
+        arrived = int(pr.arrivals[si].shape[0])
+        nb = int(batches[si]) if len(batches) else 0
+        sv = int(served[si]) if len(served) else 0
+        lat = lats[si] if nb else None
+        out[sid] = ServiceSimStats(
+            service_id=sid, arrived=arrived, served=sv, queued_at_end=arrived - sv, batches=nb,
+            violations=int(viol[si]) if len(viol) else 0, achieved_rps=sv / job.horizon_s,
+            latency_ms=({} if lat is None else {
+                "mean": round(float(lat.mean()), 6),
+                "p50": round(float(np.percentile(lat, 50)), 6),
+                "p95": round(float(np.percentile(lat, 95)), 6),
+                "p99": round(float(np.percentile(lat, 99)), 6),
+                "max": round(float(lat.max()), 6),
+            }),
+        )
+    return SimReport(horizon_s=job.horizon_s, seed=job.seed, kind=pr.kind, services=out, activity=activity)
+
+
+def run_simulation(dmap, tables: Mapping, services: Sequence, workload: Workload | None = None,
+                   horizon_s: float = 60.0, seed: int = 0, sms_per_gpc: int = DEFAULT_SMS_PER_GPC) -> SimReport:
+    """Simulate request service against a deployment map (evaluation.py:286-464)."""
+    return run_simulations([SimJob(dmap, tables, services, workload, horizon_s, seed, sms_per_gpc)])[0]

@@ -22,6 +22,8 @@ Files:
   c2_digests.json       digest of every C2 scenario plan (seed 0, 10^4) + 200 full plans
   c3_sample.json        200 C3 dense workloads: table digest + configure result
   c5_summary.json       C5 large-cluster allocation summary (with --c5)
+  sim_cases.json        run_simulation (evaluation.py:286-464) reports on the S1-S6
+                        plans: arrival kinds, rate scales, horizons, seeds (§8f row 4)
 """
 
 from __future__ import annotations
@@ -460,6 +462,40 @@ def gen_c5(tables):
           f"(relocate {t1 - t0:.1f}s optimize {t2 - t1:.1f}s)")
 
 
+# ------------------------------------------------------------ simulator
+SIM_SETS = [
+    # (scenario, plan options, arrivals, rate scale, horizon s, seed)
+    *[(name, "default", "poisson", 1.0, 3.0, 0) for name in ("S1", "S2", "S3", "S4", "S5", "S6")],
+    *[(name, "default", "deterministic", 1.0, 3.0, 1) for name in ("S1", "S3", "S6")],
+    ("S2", "default", "poisson", 1.6, 4.0, 7), ("S6", "default", "poisson", 1.4, 2.0, 3),
+    ("S4", "default", "poisson", 0.3, 5.0, 11), ("S5", "single", "poisson", 1.0, 2.5, 5),
+    ("S6", "default", "deterministic", 1.7, 2.0, 2), ("S1", "default", "poisson", 2.5, 6.0, 13),
+    ("S6", "default", "poisson", 1.0, 10.0, 21),
+]
+
+
+def gen_sim(tables):
+    out = []
+    for name, oname, kind, scale, horizon, seed in SIM_SETS:
+        sc = RF.make_scenario(name)
+        opts = R.PlanOptions(**OPTION_SETS[oname])
+        res = R.plan_scenario(sc, tables, opts)
+        from migplan.pipeline import prepare_tables as _prep
+        prepared = _prep(tables, opts)
+        wl = R.Workload.from_services(R.scenario_services(sc), kind=kind, scale=scale)
+        t0 = time.perf_counter()
+        rep = R.run_simulation(res.deployment, prepared, res.services, workload=wl, horizon_s=horizon, seed=seed)
+        dt = time.perf_counter() - t0
+        obj = rep.to_json_obj()
+        obj["metrics"] = {"internal_slack": R.internal_slack(rep.activity) if rep.activity.segments else None,
+                          "slo_compliance": R.slo_compliance(rep)}
+        out.append({"scenario": name, "options": oname, "arrivals": kind, "rate_scale": scale,
+                    "horizon_s": horizon, "seed": seed, "map": res.deployment.to_json(), "report": obj,
+                    "reference_s": dt})
+        print(f"  sim {name} {oname} {kind} x{scale} {horizon}s seed {seed}: {dt:.2f} s")
+    write("sim_cases.json", out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c5", action="store_true")
@@ -469,7 +505,7 @@ def main():
     steps = {"tables": lambda: gen_fixture_tables(tables), "fixture": lambda: gen_fixture_plans(tables),
              "fuzz": lambda: gen_fuzz_plans(tables), "unit": gen_unit_cases,
              "alloc": lambda: gen_alloc_cases(tables), "reconf": lambda: gen_reconfigure(tables),
-             "c2": lambda: gen_c2(tables), "c3": gen_c3}
+             "c2": lambda: gen_c2(tables), "c3": gen_c3, "sim": lambda: gen_sim(tables)}
     if a.c5:
         steps["c5"] = lambda: gen_c5(tables)
     for name, fn in steps.items():

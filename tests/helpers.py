@@ -74,3 +74,37 @@ def map_canon(res, names, prior_diags=()):
     gpus = [[gid, [[names[n], sz, b, p, tp, slot] for n, sz, b, p, tp, slot in pls]] for gid, pls in res["gpus"]]
     diags = list(prior_diags) + [format_diag(r, g, names[n] if n >= 0 else None) for r, g, n in res["diags"]]
     return {"gpus": gpus, "freed": [[names[k], v] for k, v in res["ledger"]], "diags": diags}
+
+
+def sim_scenario_inputs(case, fixtures):
+    """(DeploymentMap, services, Workload) of a tests/golden/sim_cases.json case."""
+    import paper_2409_14447_b200 as P
+    from paper_2409_14447_b200.scenario import ScenarioService
+    from paper_2409_14447_b200.simulation import Workload
+    sc = P.Scenario(case["scenario"], tuple(ScenarioService(m, r, s) for m, r, s in fixtures.scenarios[case["scenario"]]))
+    services = P.scenario_services(sc)
+    dmap = P.DeploymentMap.from_json(case["map"])
+    wl = Workload.from_services(services, kind=case["arrivals"], scale=case["rate_scale"])
+    return dmap, services, wl
+
+
+def sim_report_with_oracle(oracle, job):
+    """run_simulation with the C oracle as the event loop (CPU; test only):
+    the product's host-side arrivals and statistics around oracle.simulate_service."""
+    import numpy as np
+    from paper_2409_14447_b200 import simulation as S
+    pr = S._Prepared(job)
+    per = [[] for _ in pr.ids]
+    for gi, (si, p, gid, ms) in enumerate(pr.segments):
+        per[si].append(gi)
+    served, batches, viol, lats, busy = [], [], [], [], {}
+    for si in range(len(pr.ids)):
+        segs = [pr.segments[g] for g in per[si]]
+        sv, nb, nv, lat, bz = oracle.simulate_service(pr.arrivals[si], [x[3] for x in segs],
+                                                      [x[1].batch_size for x in segs],
+                                                      [x[1].process_count for x in segs],
+                                                      pr.svc[si].slo_latency, pr.horizon_ms)
+        served.append(sv); batches.append(nb); viol.append(nv); lats.append(lat)
+        for k, g in enumerate(per[si]):
+            busy[g] = bz[k]
+    return S._report(pr, lats, np.array(served), np.array(batches), np.array(viol), None, busy), lats, busy

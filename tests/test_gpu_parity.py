@@ -477,3 +477,51 @@ def test_broad_fuzz_vs_oracle(fx):
 def math_exp(x):
     import math
     return math.exp(x)
+
+
+def test_simulation_reports_vs_reference(fx):
+    """run_simulation / run_simulations (event loops on the GPU) reproduce every
+    reference report of tests/golden/sim_cases.json exactly; the batched call
+    gives the same reports as one call per job."""
+    import json
+    from helpers import sim_scenario_inputs
+    from paper_2409_14447_b200 import simulation as S
+    cases = golden("sim_cases.json")
+    jobs = []
+    for case in cases:
+        dmap, services, wl = sim_scenario_inputs(case, fx)
+        jobs.append(S.SimJob(dmap, fx.tables, services, wl, case["horizon_s"], case["seed"]))
+    batched = S.run_simulations(jobs)
+    for case, job, rep in zip(cases, jobs, batched):
+        for r in (rep, S.run_simulation(job.dmap, job.tables, job.services, job.workload, job.horizon_s, job.seed)):
+            obj = r.to_json_obj()
+            obj["metrics"] = {"internal_slack": S.internal_slack(r.activity) if r.activity.segments else None,
+                              "slo_compliance": S.slo_compliance(r)}
+            assert json.loads(json.dumps(obj)) == case["report"], (case["scenario"], case["arrivals"], case["seed"])
+
+
+def test_simulation_event_loop_vs_oracle(fx):
+    """Raw event-loop outputs (every batch latency, busy time per segment,
+    counters) bit-identical to the C oracle on random maps, overloads,
+    horizons and seeds -- including services without segments or arrivals."""
+    import random
+    from helpers import sim_report_with_oracle
+    from paper_2409_14447_b200 import simulation as S
+    rng = random.Random(99)
+    names = list(fx.scenarios)
+    jobs = []
+    for i in range(40):
+        sc = P.Scenario(f"r{i}", tuple(P.scenario.ScenarioService(m, r, s) for m, r, s in fx.scenarios[rng.choice(names)]))
+        res = P.plan_scenario(sc, fx.tables)
+        services = list(res.services)
+        wl = S.Workload.from_services(services, kind=rng.choice(["poisson", "poisson", "deterministic"]),
+                                      scale=rng.choice([0.0, 0.2, 1.0, 1.5, 3.0]))
+        jobs.append(S.SimJob(res.deployment, fx.tables, services, wl, rng.choice([0.5, 1.0, 2.0]), rng.randrange(1000)))
+    gpu = S.run_simulations(jobs)
+    for job, rep in zip(jobs, gpu):
+        orep, _, _ = sim_report_with_oracle(oracle, job)
+        assert rep.to_json_obj() == orep.to_json_obj()
+        assert [s.activity for s in rep.activity.segments] == [s.activity for s in orep.activity.segments]
+        for sid in rep.services:
+            a, b = rep.services[sid], orep.services[sid]
+            assert (a.served, a.batches, a.violations, a.latency_ms) == (b.served, b.batches, b.violations, b.latency_ms)

@@ -254,3 +254,24 @@ def test_plan_metrics_from_records(fx):
         assert met["total_gpcs"][k] == c["summary"]["total_gpcs"]
         assert met["allocated_fraction"][k] == c["summary"]["allocated_fraction"]
         assert met["external_fragmentation"][k] == c["summary"]["external_fragmentation"]
+
+
+def test_sim_oracle_vs_reference_reports():
+    """run_simulation (evaluation.py:286-464) with the C event loop: every
+    report of tests/golden/sim_cases.json (rendered by the reference) is
+    reproduced exactly -- JSON, internal slack and SLO compliance."""
+    import json
+    from helpers import sim_report_with_oracle, sim_scenario_inputs
+    from paper_2409_14447_b200 import simulation as S
+    from paper_2409_14447_b200 import workloads as W
+    fx = W.load_fixtures()
+    cases = golden("sim_cases.json")
+    assert len(cases) >= 16
+    for case in cases:
+        dmap, services, wl = sim_scenario_inputs(case, fx)
+        job = S.SimJob(dmap, fx.tables, services, wl, case["horizon_s"], case["seed"])
+        rep, _, _ = sim_report_with_oracle(oracle, job)
+        obj = rep.to_json_obj()
+        obj["metrics"] = {"internal_slack": S.internal_slack(rep.activity) if rep.activity.segments else None,
+                          "slo_compliance": S.slo_compliance(rep)}
+        assert json.loads(json.dumps(obj)) == case["report"], (case["scenario"], case["arrivals"], case["seed"])
