@@ -381,34 +381,48 @@ int parva_plan_general(const parva_general_problem* p, parva_general_result* r,
                        void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------- simulator */
-/* Batched run_simulation event loops (evaluation.py:337-416; SURVEY §8f row
- * 4): one independent simulation per service, for any number of runs at
- * once.  Service s owns arrivals [d_arr_off[s], d_arr_off[s+1]) (ms, sorted,
- * from the reference's numpy RNG) and segments [d_seg_off[s], d_seg_off[s+1])
- * in dispatch order (deployment-map order).  All arrays are device arrays. */
+/* Batched run_simulation (evaluation.py:207-226, 327-416):
+ * one independent simulation per service, for any number of runs at once.
+ * Service s: arrival process d_kind[s] (0 none, 1 poisson, 2 deterministic)
+ * from its numpy PCG64 state d_pcg[4s..4s+3] (state hi, lo, increment hi,
+ * lo -- SeedSequence(seed).spawn(n)[i] seeded on the host), d_scale[s]
+ * (poisson: 1/rate; deterministic: step = 1/rate), d_count[s] (poisson: the
+ * chunk size max(int(rate*horizon*1.2)+16, 64); deterministic: floor(
+ * horizon/step)); a buffer [d_buf_off[s], d_buf_off[s+1]) for its arrivals
+ * (ms), which afterwards holds its batch latencies; segments [d_seg_off[s],
+ * d_seg_off[s+1]) in dispatch (deployment-map) order.  Device arrays. */
 typedef struct {
   int32_t n_services;
-  const int64_t* d_arr_off;      /* [n_services + 1]                       */
-  const double*  d_arrivals;     /* ms                                     */
-  const int32_t* d_seg_off;      /* [n_services + 1]                       */
-  const double*  d_seg_ms;       /* segment service time (profiled latency) */
-  const int32_t* d_seg_batch;
-  const int32_t* d_seg_lanes;    /* process count                          */
-  const double*  d_slo;          /* per service: client-facing SLO (ms)     */
-  const double*  d_horizon_ms;   /* per service: its run's horizon          */
+  const int32_t*  d_kind;
+  const uint64_t* d_pcg;         /* [4 n_services]                           */
+  const double*   d_scale;
+  const int64_t*  d_count;
+  const double*   d_horizon_s;
+  const int64_t*  d_buf_off;     /* [n_services + 1]                         */
+  const int32_t*  d_seg_off;     /* [n_services + 1]                         */
+  const double*   d_seg_ms;      /* segment service time (profiled latency)  */
+  const int32_t*  d_seg_batch;
+  const int32_t*  d_seg_lanes;   /* process count                            */
+  const double*   d_slo;         /* client-facing SLO (ms)                   */
+  const double*   d_horizon_ms;
 } parva_sim_problem;
 
 typedef struct {
-  int64_t* d_served;             /* [n_services]                            */
+  int64_t* d_arrived;            /* [n_services]                             */
+  int64_t* d_served;
   int64_t* d_batches;
   int64_t* d_violations;
-  double*  d_latency;            /* batch b of service s at d_arr_off[s] + b */
+  double*  d_buf;                /* batch b of service s at d_buf_off[s] + b  */
   double*  d_busy_ms;            /* per segment                              */
   int32_t* d_status;             /* per service: PARVA_OK, or PARVA_CAPACITY
-                                    (> 32 segments or > 64 lanes)           */
+                                    (buffer, > 32 segments or > 64 lanes)   */
 } parva_sim_result;
 
 int parva_simulate(const parva_sim_problem* problem, const parva_sim_result* result, void* stream);
+/* Test hooks: glibc log1p on (-1, 0] as the simulator computes it, and numpy
+ * Generator.exponential(scale) draws from a PCG64 state. */
+int parva_sim_log1p(const double* d_x, double* d_out, int64_t n, void* stream);
+int parva_sim_exponential(const uint64_t* d_pcg, double scale, int64_t n, double* d_out, void* stream);
 
 /* ------------------------------------------------ fine-grained API kernels */
 /* Lists k = [d_off[k], d_off[k+1]) of (instance size, throughput) triplets in

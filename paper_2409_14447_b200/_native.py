@@ -59,14 +59,16 @@ class GeneralResult(C.Structure):
 
 
 class SimProblem(C.Structure):
-    _fields_ = [("n_services", C.c_int32), ("d_arr_off", C.c_void_p), ("d_arrivals", C.c_void_p),
+    _fields_ = [("n_services", C.c_int32), ("d_kind", C.c_void_p), ("d_pcg", C.c_void_p), ("d_scale", C.c_void_p),
+                ("d_count", C.c_void_p), ("d_horizon_s", C.c_void_p), ("d_buf_off", C.c_void_p),
                 ("d_seg_off", C.c_void_p), ("d_seg_ms", C.c_void_p), ("d_seg_batch", C.c_void_p),
                 ("d_seg_lanes", C.c_void_p), ("d_slo", C.c_void_p), ("d_horizon_ms", C.c_void_p)]
 
 
 class SimResult(C.Structure):
-    _fields_ = [("d_served", C.c_void_p), ("d_batches", C.c_void_p), ("d_violations", C.c_void_p),
-                ("d_latency", C.c_void_p), ("d_busy_ms", C.c_void_p), ("d_status", C.c_void_p)]
+    _fields_ = [("d_arrived", C.c_void_p), ("d_served", C.c_void_p), ("d_batches", C.c_void_p),
+                ("d_violations", C.c_void_p), ("d_buf", C.c_void_p), ("d_busy_ms", C.c_void_p),
+                ("d_status", C.c_void_p)]
 
 
 EXPORTS = (
@@ -76,7 +78,7 @@ EXPORTS = (
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
-    "parva_stream_pack", "parva_forget_block", "parva_simulate",
+    "parva_stream_pack", "parva_forget_block", "parva_simulate", "parva_sim_log1p", "parva_sim_exponential",
 )
 
 

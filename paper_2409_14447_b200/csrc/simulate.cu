@@ -1,26 +1,31 @@
-// simulate.cu — batched run_simulation event loops, sm_100a.
+// simulate.cu — batched run_simulation, sm_100a.
 //
-// Replaces the heap-driven event loop of the reference simulator
-// (evaluation.py:337-416) for many (deployment, workload, seed) runs at once.
-// Services never interact in that loop: a service's events only touch its
-// own queue, lanes and segments, and the global (time, seq) heap order
-// restricted to one service is the order of that service's own pushes.  So
-// every service is an independent sequential simulation: one thread each.
+// Replaces the reference simulator's arrival generation and heap-driven
+// event loop (evaluation.py:207-226, 327-416) for many (deployment,
+// workload, seed) runs at once.  Services never interact in that loop: a
+// service's events only touch its own queue, lanes and segments, and the
+// global (time, seq) heap order restricted to one service is the order of
+// that service's own pushes.  So every service is an independent sequential
+// simulation: one thread each, in two stages.
 //
-// Per service (thread):
-//   * arrivals: the service's arrival times in ms (sorted; generated on the
-//     host with the reference's numpy RNG, evaluation.py:207-226, 327-335);
-//     the FIFO queue is the index range [qh, ptr) of that array, ingest()
-//     advances ptr (searchsorted(side="right") on a monotone clock);
-//   * pending events: one completion per busy lane (time, seq, segment) and
-//     at most one arrival wakeup, popped by (time, seq) with a linear scan;
-//   * dispatch(): first segment (in dmap order) with a free lane takes
-//     min(batch, queue) requests; latency = (now - first) + service_ms;
-//     busy_ms += max(0, min(service_ms, horizon - now)).
-// Floating-point operations are the reference's, one rounding each
-// (--fmad=false), so latencies and busy times are bit-identical.
+// 1. Arrivals, from the service's own numpy generator state (PCG64 XSL-RR
+//    128/64, seeded on the host by SeedSequence(seed).spawn(n)[i] exactly as
+//    the reference does): Generator.exponential(1/rate, size=chunk) gaps by
+//    numpy's ziggurat (tables in numpy_ziggurat.h), per-chunk cumsum plus the
+//    previous chunk's last time, stop at the horizon; or the deterministic
+//    grid i * step.  Times in seconds, then * 1000.0 -> ms.
+// 2. The event loop: the FIFO queue is the index range [qh, ptr) of the
+//    arrival array; ingest() advances ptr (searchsorted(side="right") on a
+//    monotone clock); pending events are one completion per busy lane plus
+//    at most one arrival wakeup, popped by (time, seq); dispatch() gives the
+//    first segment (deployment-map order) with a free lane min(batch, queue)
+//    requests.  Batch latencies overwrite the consumed prefix of the arrival
+//    array (batch b is written after >= b + 1 arrivals left the queue).
+// Every floating-point operation is the reference's, one rounding each
+// (--fmad=false; explicit __fma_rn only where glibc's log1p fuses).
 #include <cuda_runtime.h>
 
+#include "numpy_ziggurat.h"
 #include "parva_common.cuh"
 
 namespace parva {
@@ -28,21 +33,156 @@ namespace parva {
 constexpr int kSimLanes = 64;     // pending completions per service (its total lanes)
 constexpr int kSimSegs = 32;      // segments per service
 
+// ------------------------------------------------------------- numpy PCG64
+struct Pcg64 {
+  uint64_t hi, lo, inc_hi, inc_lo;
+
+  __device__ __forceinline__ uint64_t next64() {
+    // state = state * 0x2360ED051FC65DA44385DF649FCCF645 + inc (mod 2^128), then XSL-RR
+    const uint64_t mlo = 0x4385DF649FCCF645ull, mhi = 0x2360ED051FC65DA4ull;
+    uint64_t nlo = lo * mlo;
+    uint64_t nhi = __umul64hi(lo, mlo) + hi * mlo + lo * mhi;
+    nlo += inc_lo;
+    nhi += inc_hi + (nlo < inc_lo ? 1ull : 0ull);
+    lo = nlo;
+    hi = nhi;
+    const uint64_t x = nhi ^ nlo;
+    const unsigned rot = (unsigned)(nhi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+
+  __device__ __forceinline__ double next_double() {
+    return __dmul_rn((double)(next64() >> 11), 1.0 / 9007199254740992.0);
+  }
+};
+
+// glibc's log1p (sysdeps/ieee754/dbl-64/s_log1p.c, the FMA build its ifunc
+// picks on x86-64 hosts) for x in (-1, 0]: the argument numpy's exponential
+// tail passes (evaluation's ziggurat: r - log1p(-U)).  Same operations and
+// the same fused multiply-adds, so the value is bit-identical (checked on
+// 2.2e8 random inputs against the host libm, tools/sim/log1p_check).
+__device__ __forceinline__ double glibc_log1p_neg(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01, Lp3 = 2.857142874366239149e-01,
+               Lp4 = 2.222219843214978396e-01, Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int32_t hx = (int32_t)(__double_as_longlong(x) >> 32);
+  const int32_t ax = hx & 0x7fffffff;
+  if (ax < 0x3e200000) {                                  // |x| < 2^-29
+    if (ax < 0x3c900000) return x;
+    return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+  }
+  int k = 0;
+  double f, c = 0.0;
+  int32_t hu;
+  if (hx < (int32_t)0xbfd2bec4) {                          // sqrt(2)/2- <= 1+x: k = 0, f = x
+    f = x;
+    hu = 1;
+  } else {
+    const double u0 = __dadd_rn(x, 1.0);
+    hu = (int32_t)(__double_as_longlong(u0) >> 32);
+    k = (hu >> 20) - 1023;
+    c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u0, x)) : __dsub_rn(x, __dsub_rn(u0, 1.0));
+    c = __ddiv_rn(c, u0);
+    hu &= 0x000fffff;
+    const uint64_t lo32 = (uint64_t)__double_as_longlong(u0) & 0xffffffffull;
+    double u;
+    if (hu < 0x6a09e) {
+      u = __longlong_as_double((long long)(((uint64_t)(uint32_t)(hu | 0x3ff00000) << 32) | lo32));
+    } else {
+      k += 1;
+      u = __longlong_as_double((long long)(((uint64_t)(uint32_t)(hu | 0x3fe00000) << 32) | lo32));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+  const double dk = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      return __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+    }
+    const double R = __dmul_rn(__fma_rn(-f, 0.66666666666666666, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double sr = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, sr));
+  return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(__fma_rn(dk, ln2_lo, c), sr)), f));
+}
+
+// numpy random_standard_exponential (distributions.c, ziggurat method)
+__device__ __forceinline__ double standard_exponential(Pcg64& g) {
+  for (;;) {
+    uint64_t ri = g.next64() >> 3;
+    const int idx = (int)(ri & 0xFF);
+    ri >>= 8;
+    const double x = __dmul_rn((double)ri, __ldg(&kZigWe[idx]));
+    if (ri < __ldg(&kZigKe[idx])) return x;
+    if (idx == 0) return __dsub_rn(kZigExpR, glibc_log1p_neg(-g.next_double()));
+    const double fe1 = __ldg(&kZigFe[idx - 1]), fe0 = __ldg(&kZigFe[idx]);
+    if (__dadd_rn(__dmul_rn(__dsub_rn(fe1, fe0), g.next_double()), fe0) < exp(-x)) return x;
+  }
+}
+
 __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < P.n_services; s += gridDim.x * blockDim.x) {
-    const int64_t a0 = P.d_arr_off[s];
-    const int64_t na = P.d_arr_off[s + 1] - a0;
-    const double* arr = P.d_arrivals + a0;
+    const int64_t b0 = P.d_buf_off[s];
+    const int64_t cap = P.d_buf_off[s + 1] - b0;
+    double* buf = R.d_buf + b0;
+    const double horizon_s = P.d_horizon_s[s];
+    // ---------------------------------------------------- 1. arrivals (ms)
+    int64_t na = 0;
+    bool overflow = false;
+    const int kind = P.d_kind[s];
+    if (kind == 1) {                       // poisson (evaluation.py:218-226)
+      Pcg64 g{P.d_pcg[4 * s], P.d_pcg[4 * s + 1], P.d_pcg[4 * s + 2], P.d_pcg[4 * s + 3]};
+      const double scale = P.d_scale[s];
+      const int64_t chunk = P.d_count[s];
+      double total = 0.0;
+      bool done = false;
+      while (!done && total < horizon_s) {
+        double cs = 0.0;
+        for (int64_t i = 0; i < chunk; i++) {
+          const double gap = __dmul_rn(scale, standard_exponential(g));
+          cs = i == 0 ? gap : __dadd_rn(cs, gap);
+          const double t = __dadd_rn(cs, total);
+          if (t >= horizon_s) { done = true; break; }      // times are monotone: the rest is filtered out
+          if (na == cap) { overflow = true; done = true; break; }
+          buf[na++] = __dmul_rn(t, 1000.0);
+          if (i == chunk - 1) total = t;
+        }
+      }
+    } else if (kind == 2) {                // deterministic (evaluation.py:213-217)
+      const double step = P.d_scale[s];
+      const int64_t n = P.d_count[s];
+      for (int64_t i = 1; i <= n; i++) {
+        const double t = __dmul_rn((double)i, step);
+        if (!(t < horizon_s)) continue;
+        if (na == cap) { overflow = true; break; }
+        buf[na++] = __dmul_rn(t, 1000.0);
+      }
+    }
+    R.d_arrived[s] = na;
     const int g0 = P.d_seg_off[s];
     const int ns = P.d_seg_off[s + 1] - g0;
-    const double H = P.d_horizon_ms[s];
-    const double slo = P.d_slo[s];
     int lanes_total = 0;
     for (int g = 0; g < ns; g++) lanes_total += P.d_seg_lanes[g0 + g];
-    if (ns > kSimSegs || lanes_total > kSimLanes) {
+    if (overflow || ns > kSimSegs || lanes_total > kSimLanes) {
       R.d_status[s] = PARVA_CAPACITY;
       continue;
     }
+    // ------------------------------------------------------ 2. event loop
+    const double H = P.d_horizon_ms[s];
+    const double slo = P.d_slo[s];
     int free_seg[kSimSegs];
     double busy[kSimSegs];
     for (int g = 0; g < ns; g++) { free_seg[g] = P.d_seg_lanes[g0 + g]; busy[g] = 0.0; }
@@ -56,7 +196,7 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
     bool wake = false;
     double wake_t = 0.0;
     uint32_t wake_q = 0;
-    double* lat = R.d_latency + a0;
+    const double* arr = buf;
 
     auto schedule_wakeup = [&]() {
       if (wake || ptr >= na) return;
@@ -79,7 +219,7 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
         const double first = arr[qh];
         qh += n;
         const double latency = __dadd_rn(__dsub_rn(now, first), ms);
-        lat[batches++] = latency;
+        buf[batches++] = latency;          // slot < qh: that arrival has left the queue
         served += n;
         if (latency > slo) violations++;
         free_seg[g]--;
@@ -134,6 +274,19 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
   }
 }
 
+// glibc log1p check kernel (tests): out[i] = glibc_log1p_neg(x[i])
+__global__ void log1p_kernel(const double* x, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = glibc_log1p_neg(x[i]);
+}
+
+// numpy exponential check kernel (tests): draws of Generator.exponential(scale)
+__global__ void exponential_kernel(const uint64_t* pcg, double scale, int64_t n, double* out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  Pcg64 g{pcg[0], pcg[1], pcg[2], pcg[3]};
+  for (int64_t i = 0; i < n; i++) out[i] = __dmul_rn(scale, standard_exponential(g));
+}
+
 }  // namespace parva
 
 extern "C" int parva_simulate(const parva_sim_problem* p, const parva_sim_result* r, void* stream) {
@@ -147,5 +300,19 @@ extern "C" int parva_simulate(const parva_sim_problem* p, const parva_sim_result
   int blocks = (p->n_services + threads - 1) / threads;
   if (blocks > n_sm * 32) blocks = n_sm * 32;
   parva::simulate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*p, *r);
+  return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+extern "C" int parva_sim_log1p(const double* d_x, double* d_out, int64_t n, void* stream) {
+  if (n < 0) return PARVA_BAD_INPUT;
+  if (n == 0) return PARVA_OK;
+  parva::log1p_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(d_x, d_out, n);
+  return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+extern "C" int parva_sim_exponential(const uint64_t* d_pcg, double scale, int64_t n, double* d_out, void* stream) {
+  if (n < 0) return PARVA_BAD_INPUT;
+  if (n == 0) return PARVA_OK;
+  parva::exponential_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_pcg, scale, n, d_out);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }

@@ -8,14 +8,16 @@ number of (deployment, services, workload, horizon, seed) jobs in ONE kernel
 launch.
 
 Split of the work:
-  * arrivals: generated on the host with the reference's own numpy calls
-    (SeedSequence(seed).spawn over the sorted service ids, default_rng,
-    exponential gaps, chunked cumsum; evaluation.py:207-226, 327-335), so
-    they are bit-identical by construction;
-  * the event loop (evaluation.py:337-416) -- heap of completions and
-    arrival wakeups, FIFO batching, lane accounting, busy time -- runs on the
-    GPU, one thread per service (parva_simulate, csrc/simulate.cu): services
-    never interact in that loop, so each is an independent simulation;
+  * seeding on the host: SeedSequence(seed).spawn over the sorted service
+    ids and default_rng(child), exactly as the reference (evaluation.py:
+    327-335); only each generator's 256-bit PCG64 state goes to the GPU;
+  * arrivals on the GPU (parva_simulate, csrc/simulate.cu): numpy's
+    Generator.exponential (PCG64 + ziggurat, tables from numpy itself) with
+    the reference's chunked cumsum (evaluation.py:207-226), bit-identical;
+  * the event loop (evaluation.py:337-416) -- completions and arrival
+    wakeups in (time, seq) order, FIFO batching, lane accounting, busy time --
+    on the GPU, one thread per service: services never interact in that
+    loop, so each is an independent simulation;
   * statistics (numpy mean / percentile / max, rounding) on the host, with
     the reference's calls (evaluation.py:436-456).
 There is no CPU event loop here: without the CUDA library this raises
@@ -193,7 +195,8 @@ class SimJob:
 
 
 class _Prepared:
-    """Host-side layout of one job: service order, arrivals, segments."""
+    """Host-side layout of one job: service order, per-service generator
+    state and arrival parameters, segments (evaluation.py:311-345)."""
 
     def __init__(self, job: SimJob):
         if job.horizon_s <= 0:
@@ -207,15 +210,29 @@ class _Prepared:
         ordered = sorted({p.service_id for _, p in dmap.placements()} | set(rates) | set(services_by_id))
         spawned = np.random.SeedSequence(job.seed).spawn(len(ordered))
         self.ids = ordered
-        self.svc = []
-        self.arrivals = []
+        self.svc, self.children, self.rates = [], [], []
+        # per service: arrival kind (0 none, 1 poisson, 2 deterministic), PCG64
+        # state, scale / step, chunk size / count
+        self.akind, self.pcg, self.scale, self.count = [], [], [], []
         for sid, ss in zip(ordered, spawned):
             svc = services_by_id.get(sid)
             if svc is None:
                 raise SimulationConfigError(f"no service definition for {sid!r}")
-            rng = np.random.default_rng(ss)
+            rate = rates.get(sid, 0.0)
             self.svc.append(svc)
-            self.arrivals.append(_arrival_times(workload.kind, rates.get(sid, 0.0), job.horizon_s, rng) * 1000.0)
+            self.children.append(ss)
+            self.rates.append(rate)
+            st = np.random.default_rng(ss).bit_generator.state["state"]
+            m = (1 << 64) - 1
+            self.pcg.append((st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m))
+            if rate <= 0:
+                self.akind.append(0); self.scale.append(0.0); self.count.append(0)
+            elif workload.kind == "deterministic":
+                step = 1.0 / rate
+                self.akind.append(2); self.scale.append(step); self.count.append(int(math.floor(job.horizon_s / step)))
+            else:
+                self.akind.append(1); self.scale.append(1.0 / rate)
+                self.count.append(max(int(rate * job.horizon_s * 1.2) + 16, 64))
         # segments in deployment-map order; per service in that order too (dispatch order)
         index = {sid: i for i, sid in enumerate(ordered)}
         self.segments = []            # (service position, placement, gpu id, service_ms)
@@ -237,21 +254,35 @@ class _Prepared:
         self.horizon_ms = job.horizon_s * 1000.0
         self.gpu_count = len(dmap.gpus)
 
+    def buffer_len(self, si: int) -> int:
+        """Arrival buffer of service si: two chunks (a third is needed with
+        vanishing probability and is reported as capacity) or the grid."""
+        k = self.akind[si]
+        return 0 if k == 0 else 2 * self.count[si] if k == 1 else self.count[si]
+
+    def host_arrivals(self, si: int) -> np.ndarray:
+        """Arrivals (ms) of service si with numpy on the host -- the reference's
+        own generator calls (for the CPU oracle in the tests)."""
+        rng = np.random.default_rng(self.children[si])
+        return _arrival_times(self.kind, self.rates[si], self.job.horizon_s, rng) * 1000.0
+
 
 def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
-    """Batched run_simulation: every job's services simulated in one launch."""
+    """Batched run_simulation: every job's services simulated in one launch
+    (arrivals generated on the GPU from each service's numpy generator state)."""
     torch = N.require_cuda()
     preps = [_Prepared(j) for j in jobs]
-    arr_off, arrivals, seg_off, seg_ms, seg_batch, seg_lanes, slo, horizon = [0], [], [0], [], [], [], [], []
-    seg_rows = []                      # per flat service: list of global segment rows (job, position)
+    kind, pcg, scale, count, hs, buf_off = [], [], [], [], [], [0]
+    seg_off, seg_ms, seg_batch, seg_lanes, slo, horizon = [0], [], [], [], [], []
+    seg_rows = []                      # flat segment row -> (job, segment index)
     for pi, pr in enumerate(preps):
         per_svc = [[] for _ in pr.ids]
         for gi, (si, p, gid, ms) in enumerate(pr.segments):
             per_svc[si].append(gi)
         for si in range(len(pr.ids)):
-            a = pr.arrivals[si]
-            arrivals.append(a)
-            arr_off.append(arr_off[-1] + a.shape[0])
+            kind.append(pr.akind[si]); pcg.extend(pr.pcg[si]); scale.append(pr.scale[si]); count.append(pr.count[si])
+            hs.append(pr.job.horizon_s)
+            buf_off.append(buf_off[-1] + pr.buffer_len(si))
             for gi in per_svc[si]:
                 _, p, _, ms = pr.segments[gi]
                 seg_ms.append(ms); seg_batch.append(p.batch_size); seg_lanes.append(p.process_count)
@@ -260,46 +291,53 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
             slo.append(pr.svc[si].slo_latency)
             horizon.append(pr.horizon_ms)
     n = len(slo)
-    reports = []
     if n == 0:
-        return [_report(pr, [], np.zeros(0), np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64), {})
-                for pr in preps]
+        return [_report(pr, [], [], [], [], [], {}) for pr in preps]
     dev = lambda a, dt: N.to_device(np.ascontiguousarray(a if len(a) else [0], dtype=dt))  # noqa: E731
-    d_arr_off = dev(arr_off, np.int64)
-    d_arr = dev(np.concatenate(arrivals) if arr_off[-1] else [], np.float64)
-    d_seg_off = dev(seg_off, np.int32)
-    d_seg_ms, d_seg_batch, d_seg_lanes = dev(seg_ms, np.float64), dev(seg_batch, np.int32), dev(seg_lanes, np.int32)
-    d_slo, d_h = dev(slo, np.float64), dev(horizon, np.float64)
-    o_served = torch.zeros(n, dtype=torch.int64, device="cuda")
-    o_batches = torch.zeros(n, dtype=torch.int64, device="cuda")
-    o_viol = torch.zeros(n, dtype=torch.int64, device="cuda")
-    o_lat = torch.zeros(max(arr_off[-1], 1), dtype=torch.float64, device="cuda")
+    d = {"kind": dev(kind, np.int32), "pcg": dev(pcg, np.uint64), "scale": dev(scale, np.float64),
+         "count": dev(count, np.int64), "hs": dev(hs, np.float64), "buf_off": dev(buf_off, np.int64),
+         "seg_off": dev(seg_off, np.int32), "seg_ms": dev(seg_ms, np.float64), "seg_batch": dev(seg_batch, np.int32),
+         "seg_lanes": dev(seg_lanes, np.int32), "slo": dev(slo, np.float64), "h": dev(horizon, np.float64)}
+    o = {k: torch.zeros(n, dtype=torch.int64, device="cuda") for k in ("arrived", "served", "batches", "viol")}
+    o_buf = torch.empty(max(buf_off[-1], 1), dtype=torch.float64, device="cuda")
     o_busy = torch.zeros(max(len(seg_ms), 1), dtype=torch.float64, device="cuda")
     o_status = torch.zeros(n, dtype=torch.int32, device="cuda")
-    P = N.SimProblem(n, N.ptr(d_arr_off).value, N.ptr(d_arr).value, N.ptr(d_seg_off).value, N.ptr(d_seg_ms).value,
-                     N.ptr(d_seg_batch).value, N.ptr(d_seg_lanes).value, N.ptr(d_slo).value, N.ptr(d_h).value)
-    R = N.SimResult(N.ptr(o_served).value, N.ptr(o_batches).value, N.ptr(o_viol).value, N.ptr(o_lat).value,
-                    N.ptr(o_busy).value, N.ptr(o_status).value)
+    v = lambda t: N.ptr(t).value  # noqa: E731
+    P = N.SimProblem(n, v(d["kind"]), v(d["pcg"]), v(d["scale"]), v(d["count"]), v(d["hs"]), v(d["buf_off"]),
+                     v(d["seg_off"]), v(d["seg_ms"]), v(d["seg_batch"]), v(d["seg_lanes"]), v(d["slo"]), v(d["h"]))
+    R = N.SimResult(v(o["arrived"]), v(o["served"]), v(o["batches"]), v(o["viol"]), v(o_buf), v(o_busy), v(o_status))
     N.check(N.lib().parva_simulate(C.byref(P), C.byref(R), N.stream_handle(stream)), "parva_simulate")
-    served, batches, viol = o_served.cpu().numpy(), o_batches.cpu().numpy(), o_viol.cpu().numpy()
-    status, lat, busy = o_status.cpu().numpy(), o_lat.cpu().numpy(), o_busy.cpu().numpy()
-    if (status != 0).any():
-        raise SimulationConfigError("a service has more than 32 segments or 64 lanes (simulator capacity)")
-    k = 0
+    if bool((o_status != 0).any()):
+        raise SimulationConfigError("simulator capacity exceeded (> 32 segments or > 64 lanes for a service, "
+                                    "or more than two arrival chunks)")
+    # gather every service's batch latencies into one array (device), one copy back
+    b_dev = o["batches"]
+    starts = torch.as_tensor(np.asarray(buf_off[:-1], dtype=np.int64), device="cuda")
+    tot = int(b_dev.sum().item())
+    if tot:
+        within = torch.arange(tot, device="cuda") - torch.repeat_interleave(torch.cumsum(b_dev, 0) - b_dev, b_dev)
+        idx = torch.repeat_interleave(starts, b_dev) + within
+        lat_all = o_buf[idx].cpu().numpy()
+    else:
+        lat_all = np.zeros(0)
+    arrived, served, batches, viol = (o[k].cpu().numpy() for k in ("arrived", "served", "batches", "viol"))
+    busy = o_busy.cpu().numpy()
+    lat_off = np.concatenate([[0], np.cumsum(batches)])
+    reports, k = [], 0
     for pi, pr in enumerate(preps):
         m = len(pr.ids)
         busy_by_seg = {}
         for si in range(m):
             for r in range(seg_off[k + si], seg_off[k + si + 1]):
                 busy_by_seg[seg_rows[r][1]] = busy[r]
-        lats = [lat[arr_off[k + si]:arr_off[k + si] + batches[k + si]] for si in range(m)]
-        reports.append(_report(pr, lats, served[k:k + m], batches[k:k + m], viol[k:k + m], arr_off[k:k + m + 1],
+        lats = [lat_all[lat_off[k + si]:lat_off[k + si + 1]] for si in range(m)]
+        reports.append(_report(pr, lats, arrived[k:k + m], served[k:k + m], batches[k:k + m], viol[k:k + m],
                                busy_by_seg))
         k += m
     return reports
 
 
-def _report(pr: _Prepared, lats, served, batches, viol, arr_off, busy_by_seg) -> SimReport:
+def _report(pr: _Prepared, lats, arrived, served, batches, viol, busy_by_seg) -> SimReport:
     job = pr.job
     activity = ActivityReport(
         segments=tuple(
@@ -313,12 +351,12 @@ def _report(pr: _Prepared, lats, served, batches, viol, arr_off, busy_by_seg) ->
     )
     out = {}
     for si, sid in enumerate(pr.ids):
-        arrived = int(pr.arrivals[si].shape[0])
+        na = int(arrived[si]) if len(arrived) else 0
         nb = int(batches[si]) if len(batches) else 0
         sv = int(served[si]) if len(served) else 0
         lat = lats[si] if nb else None
         out[sid] = ServiceSimStats(
-            service_id=sid, arrived=arrived, served=sv, queued_at_end=arrived - sv, batches=nb,
+            service_id=sid, arrived=na, served=sv, queued_at_end=na - sv, batches=nb,
             violations=int(viol[si]) if len(viol) else 0, achieved_rps=sv / job.horizon_s,
             latency_ms=({} if lat is None else {
                 "mean": round(float(lat.mean()), 6),

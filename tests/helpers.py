@@ -89,22 +89,22 @@ def sim_scenario_inputs(case, fixtures):
 
 
 def sim_report_with_oracle(oracle, job):
-    """run_simulation with the C oracle as the event loop (CPU; test only):
-    the product's host-side arrivals and statistics around oracle.simulate_service."""
+    """run_simulation with numpy arrivals on the host and the C oracle as the
+    event loop (CPU; test only) -- an independent path from the GPU's."""
     import numpy as np
     from paper_2409_14447_b200 import simulation as S
     pr = S._Prepared(job)
     per = [[] for _ in pr.ids]
     for gi, (si, p, gid, ms) in enumerate(pr.segments):
         per[si].append(gi)
-    served, batches, viol, lats, busy = [], [], [], [], {}
+    arrived, served, batches, viol, lats, busy = [], [], [], [], [], {}
     for si in range(len(pr.ids)):
         segs = [pr.segments[g] for g in per[si]]
-        sv, nb, nv, lat, bz = oracle.simulate_service(pr.arrivals[si], [x[3] for x in segs],
-                                                      [x[1].batch_size for x in segs],
+        arr = pr.host_arrivals(si)
+        sv, nb, nv, lat, bz = oracle.simulate_service(arr, [x[3] for x in segs], [x[1].batch_size for x in segs],
                                                       [x[1].process_count for x in segs],
                                                       pr.svc[si].slo_latency, pr.horizon_ms)
-        served.append(sv); batches.append(nb); viol.append(nv); lats.append(lat)
+        arrived.append(arr.shape[0]); served.append(sv); batches.append(nb); viol.append(nv); lats.append(lat)
         for k, g in enumerate(per[si]):
             busy[g] = bz[k]
-    return S._report(pr, lats, np.array(served), np.array(batches), np.array(viol), None, busy), lats, busy
+    return S._report(pr, lats, np.array(arrived), np.array(served), np.array(batches), np.array(viol), busy), lats, busy

@@ -525,3 +525,39 @@ def test_simulation_event_loop_vs_oracle(fx):
         for sid in rep.services:
             a, b = rep.services[sid], orep.services[sid]
             assert (a.served, a.batches, a.violations, a.latency_ms) == (b.served, b.batches, b.violations, b.latency_ms)
+
+
+def test_simulator_log1p_matches_host_libm():
+    """The exponential tail's log1p on the GPU equals the host libm's (glibc)
+    on random arguments in (-1, 0], incl. the branch boundaries."""
+    import ctypes as C
+    import math
+    rng = np.random.default_rng(4)
+    u = rng.random(2_000_000)
+    u[:4] = [0.0, 2.0 ** -60, 2.0 ** -30, 1.0 - 2.0 ** -53]
+    x = np.concatenate([-u, -np.array([0.29289321881345254, 0.2928932188134524, 0.29289321881345265])])
+    d_x = N.to_device(x)
+    d_o = torch.empty_like(d_x)
+    N.check(N.lib().parva_sim_log1p(N.ptr(d_x), N.ptr(d_o), C.c_int64(x.shape[0]), N.stream_handle()),
+            "parva_sim_log1p")
+    got = d_o.cpu().numpy()
+    exp = np.array([math.log1p(v) for v in x])
+    assert got.tobytes() == exp.tobytes()
+
+
+def test_simulator_exponential_matches_numpy():
+    """numpy Generator.exponential reproduced draw for draw on the GPU
+    (PCG64 + ziggurat incl. the wedge and tail paths)."""
+    import ctypes as C
+    for seed, scale in ((0, 1.0), (7, 1.0 / 1234.5), (12345, 3.0)):
+        rng = np.random.default_rng(np.random.SeedSequence(seed).spawn(2)[1])
+        st = rng.bit_generator.state["state"]
+        m = (1 << 64) - 1
+        pcg = np.array([st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m], dtype=np.uint64)
+        n = 200_000
+        ref = rng.exponential(scale, size=n)
+        d_p = N.to_device(pcg)
+        d_o = torch.empty(n, dtype=torch.float64, device="cuda")
+        N.check(N.lib().parva_sim_exponential(N.ptr(d_p), C.c_double(scale), C.c_int64(n), N.ptr(d_o),
+                                              N.stream_handle()), "parva_sim_exponential")
+        assert d_o.cpu().numpy().tobytes() == ref.tobytes(), seed
