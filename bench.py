@@ -350,6 +350,7 @@ def main():
         line["configurator_sweep"] = sweep_measure(args, torch, N, B, W, hbm, peak_src, local)
     if not args.no_extra and rank == 0:
         line["large_cluster"] = c5_measure(torch, fx)
+        line["simulation"] = sim_measure(torch, fx)
         line["c4_single_gpu"] = c4_measure(torch, N, B, W, fx, dt, local)
     if not args.no_cpu and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline_c2(fx, n)
@@ -357,6 +358,48 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def sim_measure(torch, fx, runs=256, horizon=10.0):
+    """Batched run_simulation: the S6 plan under `runs`
+    seeds, 10 s of Poisson arrivals each, in one call (host seeding + GPU
+    arrivals and event loops + host statistics, all inside the wall time).
+    CPU comparison on the box: numpy arrivals + the C oracle event loop on
+    one core for a sample; the Python reference's time per run was measured
+    in the build container (tests/golden/sim_cases.json)."""
+    import paper_2409_14447_b200 as P
+    from paper_2409_14447_b200 import simulation as S
+    sc = P.Scenario("S6", tuple(P.scenario.ScenarioService(m, r, l) for m, r, l in fx.scenarios["S6"]))
+    res = P.plan_scenario(sc, fx.tables)
+    services = list(res.services)
+    wl = S.Workload.from_services(services)
+    jobs = [S.SimJob(res.deployment, fx.tables, services, wl, horizon, seed) for seed in range(runs)]
+    S.run_simulations(jobs[:8])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps = S.run_simulations(jobs)
+    wall = time.perf_counter() - t0
+    arrivals = sum(st.arrived for r in reps for st in r.services.values())
+    # CPU path on the box (test infrastructure as the checker/baseline): a sample of runs
+    import oracle
+    sys.path.insert(0, str(REPO / "tests"))
+    from helpers import sim_report_with_oracle
+    k = 8
+    t0 = time.perf_counter()
+    for j in jobs[:k]:
+        orep, _, _ = sim_report_with_oracle(oracle, j)
+    cpu = (time.perf_counter() - t0) / k
+    ok = all(sim_report_with_oracle(oracle, j)[0].to_json_obj() == r.to_json_obj() for j, r in zip(jobs[:4], reps[:4]))
+    ref = None
+    try:
+        cases = json.loads((REPO / "tests" / "golden" / "sim_cases.json").read_text())
+        ref = [c["reference_s"] for c in cases if c["scenario"] == "S6" and c["horizon_s"] == 10.0][0]
+    except Exception:  # noqa: BLE001
+        pass
+    return {"workload": f"S6 plan x {runs} seeds x {horizon:g} s Poisson arrivals, one batched run_simulations call",
+            "runs": runs, "arrivals": int(arrivals), "wall_s": wall, "runs_per_s": runs / wall,
+            "arrivals_per_s": arrivals / wall, "cpu_c_oracle_s_per_run": cpu,
+            "reference_python_s_per_run": ref, "reports_equal_cpu_path_first_4": ok}
 
 
 def c5_measure(torch, fx):
