@@ -8,19 +8,20 @@
 // that service's own pushes.  So every service is an independent sequential
 // simulation: one thread each, in two stages.
 //
-// 1. Arrivals, from the service's own numpy generator state (PCG64 XSL-RR
-//    128/64, seeded on the host by SeedSequence(seed).spawn(n)[i] exactly as
-//    the reference does): Generator.exponential(1/rate, size=chunk) gaps by
-//    numpy's ziggurat (tables in numpy_ziggurat.h), per-chunk cumsum plus the
-//    previous chunk's last time, stop at the horizon; or the deterministic
-//    grid i * step.  Times in seconds, then * 1000.0 -> ms.
-// 2. The event loop: the FIFO queue is the index range [qh, ptr) of the
-//    arrival array; ingest() advances ptr (searchsorted(side="right") on a
-//    monotone clock); pending events are one completion per busy lane plus
-//    at most one arrival wakeup, popped by (time, seq); dispatch() gives the
-//    first segment (deployment-map order) with a free lane min(batch, queue)
-//    requests.  Batch latencies overwrite the consumed prefix of the arrival
-//    array (batch b is written after >= b + 1 arrivals left the queue).
+// * Arrivals, from the service's own numpy generator state (PCG64 XSL-RR
+//   128/64, seeded on the host by SeedSequence(seed).spawn(n)[i] exactly as
+//   the reference does): Generator.exponential(1/rate, size=chunk) gaps by
+//   numpy's ziggurat (tables in numpy_ziggurat.h), per-chunk cumsum plus the
+//   previous chunk's last time, stop at the horizon; or the deterministic
+//   grid i * step.  Generated lazily, in the order the loop ingests them.
+// * The event loop: the FIFO queue is the index range [qh, ptr) of the
+//   ingested arrivals; ingest() moves arrivals <= now into the buffer
+//   (searchsorted(side="right") on a monotone clock); pending events are one
+//   completion per busy lane plus at most one arrival wakeup, popped by
+//   (time, seq); dispatch() gives the first segment (deployment-map order)
+//   with a free lane min(batch, queue) requests.  Batch latencies overwrite
+//   the consumed prefix of the buffer (batch b is written after >= b + 1
+//   arrivals left the queue).
 // Every floating-point operation is the reference's, one rounding each
 // (--fmad=false; explicit __fma_rn only where glibc's log1p fuses).
 #include <cuda_runtime.h>
@@ -133,54 +134,71 @@ __device__ __forceinline__ double standard_exponential(Pcg64& g) {
   }
 }
 
+// A service's arrival stream, generated lazily in order (the event loop
+// consumes arrivals strictly in order, so the next one is always a register,
+// never a dependent load).  Poisson: numpy exponential gaps, per-chunk cumsum
+// plus the previous chunk's last time (evaluation.py:218-226); deterministic:
+// i * step (:213-217).  Times in seconds; next() returns ms, false at the
+// horizon (times are monotone, so the rest would be filtered out).
+struct ArrivalGen {
+  Pcg64 g;
+  double scale, horizon_s, cs, total;
+  int64_t chunk, i;
+  int kind;
+  bool done;
+
+  __device__ __forceinline__ bool next(double& t_ms) {
+    if (done) return false;
+    if (kind == 1) {
+      if (i == chunk) {                  // the reference draws another chunk while total < horizon
+        if (!(total < horizon_s)) { done = true; return false; }
+        i = 0;
+      }
+      const double gap = __dmul_rn(scale, standard_exponential(g));
+      cs = i == 0 ? gap : __dadd_rn(cs, gap);
+      const double t = __dadd_rn(cs, total);
+      if (i == chunk - 1) total = t;
+      i++;
+      if (t >= horizon_s) { done = true; return false; }
+      t_ms = __dmul_rn(t, 1000.0);
+      return true;
+    }
+    if (kind == 2) {
+      if (i < chunk) {
+        i++;
+        const double t = __dmul_rn((double)i, scale);
+        if (t < horizon_s) { t_ms = __dmul_rn(t, 1000.0); return true; }
+      }
+    }
+    done = true;
+    return false;
+  }
+};
+
 __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < P.n_services; s += gridDim.x * blockDim.x) {
     const int64_t b0 = P.d_buf_off[s];
     const int64_t cap = P.d_buf_off[s + 1] - b0;
-    double* buf = R.d_buf + b0;
-    const double horizon_s = P.d_horizon_s[s];
-    // ---------------------------------------------------- 1. arrivals (ms)
-    int64_t na = 0;
-    bool overflow = false;
+    double* buf = R.d_buf + b0;            // ingested arrivals (ms), later the batch latencies
     const int kind = P.d_kind[s];
-    if (kind == 1) {                       // poisson (evaluation.py:218-226)
-      Pcg64 g{P.d_pcg[4 * s], P.d_pcg[4 * s + 1], P.d_pcg[4 * s + 2], P.d_pcg[4 * s + 3]};
-      const double scale = P.d_scale[s];
-      const int64_t chunk = P.d_count[s];
-      double total = 0.0;
-      bool done = false;
-      while (!done && total < horizon_s) {
-        double cs = 0.0;
-        for (int64_t i = 0; i < chunk; i++) {
-          const double gap = __dmul_rn(scale, standard_exponential(g));
-          cs = i == 0 ? gap : __dadd_rn(cs, gap);
-          const double t = __dadd_rn(cs, total);
-          if (t >= horizon_s) { done = true; break; }      // times are monotone: the rest is filtered out
-          if (na == cap) { overflow = true; done = true; break; }
-          buf[na++] = __dmul_rn(t, 1000.0);
-          if (i == chunk - 1) total = t;
-        }
-      }
-    } else if (kind == 2) {                // deterministic (evaluation.py:213-217)
-      const double step = P.d_scale[s];
-      const int64_t n = P.d_count[s];
-      for (int64_t i = 1; i <= n; i++) {
-        const double t = __dmul_rn((double)i, step);
-        if (!(t < horizon_s)) continue;
-        if (na == cap) { overflow = true; break; }
-        buf[na++] = __dmul_rn(t, 1000.0);
-      }
-    }
-    R.d_arrived[s] = na;
+    ArrivalGen gen;
+    gen.g = Pcg64{P.d_pcg[4 * s], P.d_pcg[4 * s + 1], P.d_pcg[4 * s + 2], P.d_pcg[4 * s + 3]};
+    gen.scale = P.d_scale[s];
+    gen.horizon_s = P.d_horizon_s[s];
+    gen.cs = 0.0;
+    gen.total = 0.0;
+    gen.chunk = P.d_count[s];
+    gen.i = kind == 1 ? gen.chunk : 0;
+    gen.kind = kind;
+    gen.done = kind != 1 && kind != 2;
     const int g0 = P.d_seg_off[s];
     const int ns = P.d_seg_off[s + 1] - g0;
     int lanes_total = 0;
     for (int g = 0; g < ns; g++) lanes_total += P.d_seg_lanes[g0 + g];
-    if (overflow || ns > kSimSegs || lanes_total > kSimLanes) {
+    if (ns > kSimSegs || lanes_total > kSimLanes) {
       R.d_status[s] = PARVA_CAPACITY;
       continue;
     }
-    // ------------------------------------------------------ 2. event loop
     const double H = P.d_horizon_ms[s];
     const double slo = P.d_slo[s];
     int free_seg[kSimSegs];
@@ -193,21 +211,26 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
     int free_lanes = lanes_total;
     int64_t ptr = 0, qh = 0, batches = 0, served = 0, violations = 0;
     uint32_t seq = 0;
-    bool wake = false;
+    bool wake = false, overflow = false;
     double wake_t = 0.0;
     uint32_t wake_q = 0;
-    const double* arr = buf;
+    double nt = 0.0;                       // next arrival not yet ingested (arr[ptr])
+    bool have = gen.next(nt);
 
-    auto schedule_wakeup = [&]() {
-      if (wake || ptr >= na) return;
+    auto schedule_wakeup = [&]() {        // evaluation.py:362-366
+      if (wake || !have) return;
       wake = true;
-      wake_t = arr[ptr];
+      wake_t = nt;
       wake_q = seq++;
     };
-    auto ingest = [&](double now) {
-      while (ptr < na && arr[ptr] <= now) ptr++;
+    auto ingest = [&](double now) {       // evaluation.py:353-360
+      while (have && nt <= now) {
+        if (ptr == cap) { overflow = true; have = false; break; }
+        buf[ptr++] = nt;
+        have = gen.next(nt);
+      }
     };
-    auto dispatch = [&](double now) {
+    auto dispatch = [&](double now) {     // evaluation.py:368-388
       if (now >= H) return;
       while (qh < ptr && free_lanes > 0) {
         int g = 0;
@@ -216,7 +239,7 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
         const int64_t qn = ptr - qh;
         const int64_t b = P.d_seg_batch[g0 + g];
         const int64_t n = b < qn ? b : qn;
-        const double first = arr[qh];
+        const double first = buf[qh];
         qh += n;
         const double latency = __dadd_rn(__dsub_rn(now, first), ms);
         buf[batches++] = latency;          // slot < qh: that arrival has left the queue
@@ -235,7 +258,7 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
     };
 
     if (ns > 0) schedule_wakeup();
-    for (;;) {
+    for (;;) {                             // evaluation.py:395-416
       // pop the (time, seq)-smallest pending event
       int best = -1;
       double bt = 0.0;
@@ -266,11 +289,18 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
         }
       }
     }
+    // arrivals never ingested still count (ServiceSimStats.arrived)
+    int64_t arrived = ptr + (have ? 1 : 0);
+    if (have) {
+      double t;
+      while (gen.next(t)) arrived++;
+    }
+    R.d_arrived[s] = arrived;
     R.d_served[s] = served;
     R.d_batches[s] = batches;
     R.d_violations[s] = violations;
     for (int g = 0; g < ns; g++) R.d_busy_ms[g0 + g] = busy[g];
-    R.d_status[s] = PARVA_OK;
+    R.d_status[s] = overflow ? PARVA_CAPACITY : PARVA_OK;
   }
 }
 

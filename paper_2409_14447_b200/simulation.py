@@ -337,6 +337,37 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
     return reports
 
 
+_Q = (np.true_divide(50, 100), np.true_divide(95, 100), np.true_divide(99, 100))
+
+
+def _percentile_sorted(srt: np.ndarray, q) -> float:
+    """np.percentile(a, 100*q) (method "linear") from the sorted sample, with
+    numpy's own operations (_quantile: virtual index (n-1)*q, floor, clip to
+    the last element, _lerp), so the value is bit-identical."""
+    n = srt.shape[0]
+    v = (n - 1) * q
+    prev = math.floor(v)
+    if v >= n - 1:
+        return float(srt[-1])
+    a, b = srt[prev], srt[prev + 1]
+    gamma = np.float64(v - prev)
+    diff = b - a
+    if gamma >= 0.5:
+        return float(b - diff * (1 - gamma))
+    return float(a + diff * gamma)
+
+
+def _latency_stats(lat: np.ndarray) -> dict:
+    """The reference's latency summary (evaluation.py:436-456): numpy mean
+    (pairwise sum), linear-interpolated percentiles, max; rounded to 6 dp."""
+    srt = np.sort(lat)
+    return {"mean": round(float(lat.mean()), 6),
+            "p50": round(_percentile_sorted(srt, _Q[0]), 6),
+            "p95": round(_percentile_sorted(srt, _Q[1]), 6),
+            "p99": round(_percentile_sorted(srt, _Q[2]), 6),
+            "max": round(float(srt[-1]), 6)}
+
+
 def _report(pr: _Prepared, lats, arrived, served, batches, viol, busy_by_seg) -> SimReport:
     job = pr.job
     activity = ActivityReport(
@@ -358,13 +389,7 @@ def _report(pr: _Prepared, lats, arrived, served, batches, viol, busy_by_seg) ->
         out[sid] = ServiceSimStats(
             service_id=sid, arrived=na, served=sv, queued_at_end=na - sv, batches=nb,
             violations=int(viol[si]) if len(viol) else 0, achieved_rps=sv / job.horizon_s,
-            latency_ms=({} if lat is None else {
-                "mean": round(float(lat.mean()), 6),
-                "p50": round(float(np.percentile(lat, 50)), 6),
-                "p95": round(float(np.percentile(lat, 95)), 6),
-                "p99": round(float(np.percentile(lat, 99)), 6),
-                "max": round(float(lat.max()), 6),
-            }),
+            latency_ms=({} if lat is None else _latency_stats(lat)),
         )
     return SimReport(horizon_s=job.horizon_s, seed=job.seed, kind=pr.kind, services=out, activity=activity)
 
