@@ -27,26 +27,60 @@ FLAGS = [
 ]
 
 
+def _deps():
+    return sorted(CSRC.glob("*")) + [PKG.parent / "include" / "parva_b200.h"]
+
+
+def source_hash() -> str:
+    """Content hash of every source, the header and the compiler flags: a
+    library is current iff it was built from exactly these (mtimes are not
+    trusted -- copies of the tree, e.g. onto a GPU box, do not keep them)."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in _deps():
+        if p.is_file():
+            h.update(p.name.encode())
+            h.update(p.read_bytes())
+    h.update(" ".join(FLAGS + SOURCES).encode())
+    return h.hexdigest()
+
+
+HASH_FILE = OUT_DIR / "libparva_b200.sha256"
+
+
 def stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not HASH_FILE.exists():
         return True
-    t = LIB.stat().st_mtime
-    deps = list(CSRC.glob("*")) + [PKG.parent / "include" / "parva_b200.h", Path(__file__)]
-    return any(p.stat().st_mtime > t for p in deps)
+    return HASH_FILE.read_text().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """nvcc into a temporary file, then an atomic rename, under a file lock:
+    several processes (e.g. one per rank) may call this at once."""
+    import fcntl
     if not force and not stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", str(LIB), *[str(CSRC / s) for s in SOURCES], "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    (OUT_DIR / "ptxas.log").write_text(res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libparva_b200.so")
-    if verbose:
-        print(res.stderr)
+    with open(OUT_DIR / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if not force and not stale():        # another process built it meanwhile
+                return LIB
+            digest = source_hash()
+            tmp = OUT_DIR / f".libparva_b200.{os.getpid()}.so"
+            cmd = [NVCC, *FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES], "-lcudart"]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            (OUT_DIR / "ptxas.log").write_text(res.stdout + res.stderr)
+            if res.returncode != 0:
+                tmp.unlink(missing_ok=True)
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError("nvcc failed building libparva_b200.so")
+            os.replace(tmp, LIB)
+            HASH_FILE.write_text(digest + "\n")
+            if verbose:
+                print(res.stderr)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
     return LIB
 
 

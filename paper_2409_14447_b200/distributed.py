@@ -6,6 +6,8 @@ collective is the gather of the fixed-size results at the end:
 one all-gather of the 128-byte plan records and one of the 32-byte config
 records, each padded to the largest shard so every rank contributes the
 same byte count (NCCL over NVLink on the GPU box; gloo in the CPU tests).
+`gather_packed` is the one-collective form the benchmark step uses: every
+rank's plan records and 8-byte tiny config records in one block.
 
 `plan_fn(off, tab, rate, bound) -> (cfg_u8[n_svc,32], plan_u8[n_scen,128])`
 is the per-rank planner: batch.plan_batch on the GPU; the tests inject the
@@ -72,6 +74,41 @@ def gather_records(local_cfg, local_plan, shard: Shard, scen_off, group=None, de
     plan = torch.cat([all_pl[r * max(max_s, 1): r * max(max_s, 1) + (b - a)] for r, (a, b) in enumerate(sizes_s)])
     cfg = torch.cat([all_cf[r * max(max_v, 1): r * max(max_v, 1) + (b - a)] for r, (a, b) in enumerate(sizes_v)])
     return cfg, plan
+
+
+def packed_block(scen_off, world: int, plan_bytes: int = 128, cfg_bytes: int = 8) -> tuple[int, int, int]:
+    """Per-rank block of the packed gather: [plan records | config records],
+    each section padded to the largest shard.  Returns (plan section bytes,
+    config section bytes, block bytes)."""
+    n_scen = len(scen_off) - 1
+    spans = [shard_bounds(n_scen, r, world) for r in range(world)]
+    max_s = max(max(b - a for a, b in spans), 1)
+    max_v = max(max(int(scen_off[b]) - int(scen_off[a]) for a, b in spans), 1)
+    ps = max_s * plan_bytes
+    cs = (max_v * cfg_bytes + 15) & ~15
+    return ps, cs, ps + cs
+
+
+def gather_packed(block, scen_off, plan_bytes: int = 128, cfg_bytes: int = 8, group=None):
+    """ONE all-gather of every rank's packed [plan | config] block (the only
+    collective of a sharded step; 8-byte tiny config records keep it at
+    ~216 B per scenario).  `block` is this rank's uint8 tensor of
+    packed_block(...)[2] bytes, plan records first.  Returns (cfg, plan) in
+    global scenario / service order as uint8 tensors [N_svc, cfg_bytes],
+    [N_scen, plan_bytes]."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n_scen = len(scen_off) - 1
+    ps, cs, blk = packed_block(scen_off, world, plan_bytes, cfg_bytes)
+    everything = torch.empty(world * blk, dtype=torch.uint8, device=block.device)
+    dist.all_gather_into_tensor(everything, block, group=group)
+    rows = everything.view(world, blk)
+    spans = [shard_bounds(n_scen, r, world) for r in range(world)]
+    plans = [rows[r, :(b - a) * plan_bytes].view(-1, plan_bytes) for r, (a, b) in enumerate(spans)]
+    cfgs = [rows[r, ps:ps + (int(scen_off[b]) - int(scen_off[a])) * cfg_bytes].view(-1, cfg_bytes)
+            for r, (a, b) in enumerate(spans)]
+    return torch.cat(cfgs), torch.cat(plans)
 
 
 def plan_sharded(scen_off, svc_table, svc_rate, svc_bound, plan_fn, group=None, device=None):

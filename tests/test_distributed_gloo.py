@@ -13,7 +13,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2409_14447_b200.distributed import make_shard, plan_sharded, shard_bounds
+from paper_2409_14447_b200.distributed import gather_packed, make_shard, packed_block, plan_sharded, shard_bounds
 
 
 def _free_port():
@@ -59,7 +59,18 @@ def _worker(rank, world, port, n, q):
     try:
         fx, off, tab, rate, bound = _inputs(n)
         cfg, plan = plan_sharded(off, tab, rate, bound, _oracle_fn(fx))
-        q.put((rank, cfg.numpy().tobytes(), plan.numpy().tobytes()))
+        # the packed one-collective form: [plan records | tiny config records] per rank
+        from paper_2409_14447_b200.records import tiny_config
+        from paper_2409_14447_b200.records import CONFIG_DTYPE
+        sh = make_shard(off, rank, world)
+        lcfg, lplan = _oracle_fn(fx)(sh.off, tab[sh.svc_a:sh.svc_b], rate[sh.svc_a:sh.svc_b], bound[sh.svc_a:sh.svc_b])
+        ps, cs, blk = packed_block(off, world)
+        block = torch.zeros(blk, dtype=torch.uint8)
+        block[:lplan.numel()] = lplan.reshape(-1)
+        tiny = tiny_config(lcfg.numpy().reshape(-1).view(CONFIG_DTYPE)).view(np.uint8)
+        block[ps:ps + tiny.shape[0]] = torch.from_numpy(tiny.copy())
+        pcfg, pplan = gather_packed(block, off)
+        q.put((rank, cfg.numpy().tobytes(), plan.numpy().tobytes(), pcfg.numpy().tobytes(), pplan.numpy().tobytes()))
     finally:
         dist.destroy_process_group()
 
@@ -88,9 +99,13 @@ def test_two_rank_gather_matches_single_process(n):
         assert p.exitcode == 0
     fx, off, tab, rate, bound = _inputs(n)
     cfg, plan = _oracle_fn(fx)(off, tab, rate, bound)
-    for rank, c, pl in out:
+    from paper_2409_14447_b200.records import CONFIG_DTYPE, tiny_config
+    tiny = tiny_config(cfg.numpy().reshape(-1).view(CONFIG_DTYPE)).view(np.uint8)
+    for rank, c, pl, pc, ppl in out:
         assert c == cfg.numpy().tobytes(), rank
         assert pl == plan.numpy().tobytes(), rank
+        assert pc == tiny.tobytes(), rank
+        assert ppl == plan.numpy().tobytes(), rank
 
 
 def test_make_shard_offsets():

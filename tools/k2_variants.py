@@ -20,8 +20,11 @@ PATCH_DIR = REPO / "tools" / "k2_patches"
 
 def variants():
     """name -> (patch list, extra flags).  A patch file holds OLD/NEW blocks
-    separated by lines '<<<<' / '====' / '>>>>'."""
-    vs = {"base": ([], [])}
+    separated by lines '<<<<' / '====' / '>>>>'.  "head" is the committed
+    csrc/ (git HEAD), "base" the working tree."""
+    vs = {"head": (["HEAD"], []), "base": ([], [])}
+    for w, mb in ((17, 2), (18, 2), (12, 3), (11, 3), (20, 2), (24, 1)):
+        vs[f"w{w}_b{mb}"] = ([], [f"-DPARVA_PB_WARPS={w}", f"-DPARVA_PB_MINB={mb}"])
     if PATCH_DIR.exists():
         for f in sorted(PATCH_DIR.glob("*.patch")):
             vs[f.stem] = ([f], [])
@@ -48,6 +51,13 @@ def build():
         shutil.copytree(b.CSRC, d)
         if not (OUT / "include").exists():
             (OUT / "include").symlink_to(REPO / "include")
+        if patches == ["HEAD"]:
+            for f in d.iterdir():
+                r = subprocess.run(["git", "show", f"HEAD:paper_2409_14447_b200/csrc/{f.name}"], cwd=REPO,
+                                   capture_output=True)
+                if r.returncode == 0:
+                    f.write_bytes(r.stdout)
+            patches = []
         pb = d / "plan_batch.cu"
         src = pb.read_text()
         for p in patches:
