@@ -826,19 +826,18 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   __shared__ uint64_t bar;
   __shared__ uint64_t loader_bars[2 * kLoaderBufs];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool streamed = A.stream_src != nullptr;
   PHASE(0);
-  if (streamed && (int)blockIdx.x < A.n_loaders && threadIdx.x == 0) {
+  if ((int)blockIdx.x < A.n_loaders && threadIdx.x == 0) {
     for (int b = 0; b < 2 * kLoaderBufs; b++) mbar_init(&loader_bars[b], 1);
     fence_mbar_init();
   }
   // (load_index's block barriers also publish the loader mbarrier inits)
   const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS +
-                                        (streamed ? kLoaderBufs * kStreamSlice : 0),
-                                 !A.cfg_given, &bar);
+                                        kLoaderBufs * kStreamSlice,
+                                 true, &bar);
   // loader roles (warps 0 and 1 of the first n_loaders CTAs), then they plan
   // too; the CTAs' other warps start planning right away
-  if (streamed && (int)blockIdx.x < A.n_loaders && warp < 2) {
+  if ((int)blockIdx.x < A.n_loaders && warp < 2) {
     if (lane == 0)
       stream_loader(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, loader_bars, warp);
     __syncwarp();
@@ -846,65 +845,52 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   PHASE(1);
   WarpScratch& W = scratch[warp];
   WarpSvc& S = wsvc[warp];
-  // streamed mode: the input is a header (chunk table) followed by chunk
-  // blocks; this warp's current chunk (scenarios ascend per warp)
-  int n_ch = 0, ch_scen = 1, c = -1, c_scen_lo = 0, c_svc_lo = 0;
+  // the input is a header (chunk table) followed by chunk blocks; this
+  // warp's current chunk (scenarios ascend per warp)
+  int c = -1, c_scen_lo = 0, c_svc_lo = 0;
   const int32_t* c_off = nullptr;
   const double* c_rate = nullptr;
   const double* c_bound = nullptr;
   const uint16_t* c_table = nullptr;
-  if (streamed) {
-    stream_wait(A, A.stream_dst, A.stream_dst + 16, lane);
-    n_ch = __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst));
-    ch_scen = max(1, __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst) + 1));
-    stream_wait(A, A.stream_dst, A.stream_dst + parva_stream_header_bytes(n_ch), lane);
-  }
+  stream_wait(A, A.stream_dst, A.stream_dst + 16, lane);
+  const int n_ch = __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst));
+  const int ch_scen = max(1, __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst) + 1));
+  stream_wait(A, A.stream_dst, A.stream_dst + parva_stream_header_bytes(n_ch), lane);
   for (;;) {
     int j = 0;
     if (lane == 0) j = (int)atomicAdd(&A.work[0], 1u);
     j = __shfl_sync(0xffffffffu, j, 0);
     if (j >= A.n_scen) break;
-    int a0, n;
 #ifdef PARVA_PHASE_TIMING
     long long wt0 = clock64(), wt1 = wt0;
 #endif
-    if (streamed) {
-      const int cj = min(j / ch_scen, n_ch - 1);     // chunks hold ch_scen scenarios (the last one fewer)
-      if (cj != c) {
-        c = cj;
-        const parva_stream_chunk* tab = reinterpret_cast<const parva_stream_chunk*>(A.stream_dst + 16);
-        c_scen_lo = __ldcg(&tab[c].scen_lo);
-        c_svc_lo = __ldcg(&tab[c].svc_lo);
-        const int kc = __ldcg(&tab[c].k), mc = __ldcg(&tab[c].m);
-        const uint8_t* blk = A.stream_dst + __ldcg(&tab[c].offset);
-        const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
-        c_off = reinterpret_cast<const int32_t*>(blk);
-        c_rate = reinterpret_cast<const double*>(blk + rate_off);
-        c_bound = c_rate + mc;
-        c_table = reinterpret_cast<const uint16_t*>(c_bound + mc);
-        stream_wait(A, blk, c_table + mc, lane);   // the whole chunk block has landed
-      }
-      const int jl = j - c_scen_lo;
-      a0 = __ldcg(c_off + jl);
-      n = __ldcg(c_off + jl + 1) - a0;
-#ifdef PARVA_PHASE_TIMING
-      wt1 = clock64();
-#endif
-    } else {
-      a0 = A.scen_off[j];
-      n = A.scen_off[j + 1] - a0;
+    const int cj = min(j / ch_scen, n_ch - 1);     // chunks hold ch_scen scenarios (the last one fewer)
+    if (cj != c) {
+      c = cj;
+      const parva_stream_chunk* tab = reinterpret_cast<const parva_stream_chunk*>(A.stream_dst + 16);
+      c_scen_lo = __ldcg(&tab[c].scen_lo);
+      c_svc_lo = __ldcg(&tab[c].svc_lo);
+      const int kc = __ldcg(&tab[c].k), mc = __ldcg(&tab[c].m);
+      const uint8_t* blk = A.stream_dst + __ldcg(&tab[c].offset);
+      const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
+      c_off = reinterpret_cast<const int32_t*>(blk);
+      c_rate = reinterpret_cast<const double*>(blk + rate_off);
+      c_bound = c_rate + mc;
+      c_table = reinterpret_cast<const uint16_t*>(c_bound + mc);
+      stream_wait(A, blk, c_table + mc, lane);   // the whole chunk block has landed
     }
+    const int jl = j - c_scen_lo;
+    const int a0 = __ldcg(c_off + jl);
+    const int n = __ldcg(c_off + jl + 1) - a0;
+#ifdef PARVA_PHASE_TIMING
+    wt1 = clock64();
+#endif
     for (int b = 0; b < n; b += 32) {
       if (b + lane < n) {
         const int i = a0 + b + lane;
         double tpc[5];
-        uint64_t m;
-        if (streamed) {
-          m = svc_configure(A, V, (int)__ldcg(c_table + i), __ldcg(c_rate + i), __ldcg(c_bound + i),
-                            (int64_t)c_svc_lo + i, tpc);
-        } else {
-          m = tile_service(A, V, i, tpc);
-        }
+        const uint64_t m = svc_configure(A, V, (int)__ldcg(c_table + i), __ldcg(c_rate + i),
+                                         __ldcg(c_bound + i), (int64_t)c_svc_lo + i, tpc);
         if (b == 0) {
 #pragma unroll
           for (int cc = 0; cc < 5; cc++) S.tp[lane * 5 + cc] = tpc[cc];
