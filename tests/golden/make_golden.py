@@ -493,6 +493,22 @@ def gen_sim(tables):
                     "horizon_s": horizon, "seed": seed, "map": res.deployment.to_json(), "report": obj,
                     "reference_s": dt})
         print(f"  sim {name} {oname} {kind} x{scale} {horizon}s seed {seed}: {dt:.2f} s")
+    # explicit-input cases: an extra service that is defined but never placed,
+    # zero rates, both arrival kinds
+    sc = RF.make_scenario("S3")
+    res = R.plan_scenario(sc, tables, R.PlanOptions())
+    services = list(res.services) + [R.make_service("idle", res.services[0].model_id, 50.0, 500.0)]
+    rates = [(s.id, 0.0 if i % 3 == 0 else s.request_rate) for i, s in enumerate(res.services)] + [("idle", 50.0)]
+    for kind in ("poisson", "deterministic"):
+        rep = R.run_simulation(res.deployment, tables, services, workload=R.Workload(tuple(rates), kind),
+                               horizon_s=1.5, seed=3)
+        obj = rep.to_json_obj()
+        obj["metrics"] = {"internal_slack": R.internal_slack(rep.activity) if rep.activity.segments else None,
+                          "slo_compliance": R.slo_compliance(rep)}
+        out.append({"scenario": "S3", "options": "default", "arrivals": kind, "rate_scale": 1.0, "horizon_s": 1.5,
+                    "seed": 3, "map": res.deployment.to_json(), "report": obj, "reference_s": None,
+                    "services": [[s.id, s.model_id, s.request_rate, s.slo_latency] for s in services],
+                    "rates": [[sid, r] for sid, r in rates]})
     write("sim_cases.json", out)
 
 

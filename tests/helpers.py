@@ -81,9 +81,13 @@ def sim_scenario_inputs(case, fixtures):
     import paper_2409_14447_b200 as P
     from paper_2409_14447_b200.scenario import ScenarioService
     from paper_2409_14447_b200.simulation import Workload
+    dmap = P.DeploymentMap.from_json(case["map"])
+    if "services" in case:        # explicit inputs
+        services = [P.make_service(sid, model, rate, slo) for sid, model, rate, slo in case["services"]]
+        wl = Workload(tuple((sid, r) for sid, r in case["rates"]), case["arrivals"])
+        return dmap, services, wl
     sc = P.Scenario(case["scenario"], tuple(ScenarioService(m, r, s) for m, r, s in fixtures.scenarios[case["scenario"]]))
     services = P.scenario_services(sc)
-    dmap = P.DeploymentMap.from_json(case["map"])
     wl = Workload.from_services(services, kind=case["arrivals"], scale=case["rate_scale"])
     return dmap, services, wl
 

@@ -561,3 +561,51 @@ def test_simulator_exponential_matches_numpy():
         N.check(N.lib().parva_sim_exponential(N.ptr(d_p), C.c_double(scale), C.c_int64(n), N.ptr(d_o),
                                               N.stream_handle()), "parva_sim_exponential")
         assert d_o.cpu().numpy().tobytes() == ref.tobytes(), seed
+
+
+def test_simulation_edge_cases(fx):
+    """Unplaced services (no segments), services with zero rate, a service
+    missing from the definitions, a non-positive horizon: the reference's
+    reports / errors (checked against the C-oracle path, which is pinned on
+    the reference's reports)."""
+    import json
+    from helpers import sim_report_with_oracle
+    from paper_2409_14447_b200 import simulation as S
+    sc = P.Scenario("S3", tuple(P.scenario.ScenarioService(m, r, s) for m, r, s in fx.scenarios["S3"]))
+    res = P.plan_scenario(sc, fx.tables)
+    services = list(res.services)
+    extra = P.make_service("idle", services[0].model_id, 50.0, 500.0)      # defined, never placed
+    rates = tuple((s.id, 0.0 if i % 3 == 0 else s.request_rate) for i, s in enumerate(services)) + (("idle", 50.0),)
+    for kind in ("poisson", "deterministic"):
+        wl = S.Workload(rates, kind)
+        job = S.SimJob(res.deployment, fx.tables, services + [extra], wl, 1.5, 3)
+        rep = S.run_simulation(job.dmap, job.tables, job.services, job.workload, job.horizon_s, job.seed)
+        orep, _, _ = sim_report_with_oracle(oracle, job)
+        assert json.dumps(rep.to_json_obj()) == json.dumps(orep.to_json_obj())
+        assert rep.services["idle"].batches == 0 and rep.services["idle"].arrived > 0
+    with pytest.raises(P.SimulationConfigError):
+        S.run_simulation(res.deployment, fx.tables, services[1:], S.Workload.from_services(services), 1.0, 0)
+    with pytest.raises(P.SimulationConfigError):
+        S.run_simulation(res.deployment, fx.tables, services, None, 0.0, 0)
+
+
+def test_mapped_entry_rejects_pageable_memory(fx):
+    """The zero-copy entry refuses pageable host blocks (status BAD_INPUT)
+    instead of letting the kernel fault on an unmapped address."""
+    import ctypes as C
+    sb = W.scenario_batch(fx, 16, seed=1)
+    n, M = sb.rate.shape
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    mb = B.MappedHostBatch(off, tab, sb.rate.ravel(), sb.bound.ravel())
+    dt = N.device_tables_for(fx.tables)
+    pageable_in = np.frombuffer(mb.h_in.numpy().tobytes(), dtype=np.uint8).copy()
+    rc = N.lib().parva_plan_host_mapped(
+        C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(mb.n_scen), C.c_int32(mb.n_svc),
+        C.c_void_p(pageable_in.ctypes.data), C.c_int64(mb.in_bytes), C.c_void_p(mb.h_out.data_ptr()),
+        C.c_int32(1), C.c_int32(4), C.c_int32(2), C.c_int32(64), N.ptr(mb.scratch), C.c_size_t(mb.scratch_bytes),
+        N.stream_handle())
+    assert rc == 5          # PARVA_BAD_INPUT
+    mb.run(dt)              # and the pinned path still works afterwards
+    ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, sb.rate.ravel(), sb.bound.ravel())
+    assert mb.outputs()[1].tobytes() == oplan.tobytes()
