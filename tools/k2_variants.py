@@ -23,7 +23,7 @@ def variants():
     separated by lines '<<<<' / '====' / '>>>>'.  "head" is the committed
     csrc/ (git HEAD), "base" the working tree."""
     vs = {"head": (["HEAD"], []), "base": ([], [])}
-    for w, mb in ((17, 2), (18, 2), (12, 3), (11, 3), (20, 2), (24, 1)):
+    for w, mb in ():   # launch-shape variants, e.g. ((17, 2), (12, 3), (24, 1))
         vs[f"w{w}_b{mb}"] = ([], [f"-DPARVA_PB_WARPS={w}", f"-DPARVA_PB_MINB={mb}"])
     if PATCH_DIR.exists():
         for f in sorted(PATCH_DIR.glob("*.patch")):
