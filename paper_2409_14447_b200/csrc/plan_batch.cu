@@ -33,27 +33,54 @@ namespace parva {
 #endif
 constexpr int PB_WARPS = PARVA_PB_WARPS;
 constexpr int PB_THREADS = PB_WARPS * 32;
-constexpr int QCAP = 224;                 // > 31 GPUs x 7 slots: longer queues cannot fit
-
-struct alignas(16) WarpScratch {
-  uint16_t lst[32][8];                    // per GPU placement list: cat << 3 | slot
-  uint16_t bak[32][8];                    // relocation result (regression fallback)
-  uint8_t q2[QCAP];
-  uint8_t q1[QCAP];
-  uint8_t undo[2 * QCAP];
-  uint16_t diag[32];                      // optimize diagnostics, in order
+// Per-group scratch of the warp planner; G lanes = G GPUs at most.  The
+// refill queues hold G*7 segments: more than the other G-1 GPUs' 7(G-1)
+// slots cannot fit anyway (the drain then needs a new GPU).
+template <int G>
+struct alignas(16) GScratch {
+  uint16_t lst[G][8];                     // per GPU placement list: cat << 3 | slot
+  uint16_t bak[G][8];                     // relocation result (regression fallback)
+  uint8_t q2[G * 7];
+  uint8_t q1[G * 7];
+  uint8_t undo[2 * G * 7];
+  uint16_t diag[G];                       // optimize diagnostics, in order
   parva_plan_record rec;
 };
+using WarpScratch = GScratch<32>;
+// a warp's scratch in the tile kernel: two half-warp groups, or (overflow
+// pass) one full-warp group over the same bytes
+constexpr size_t kWarpArea = 2 * sizeof(GScratch<16>) > sizeof(GScratch<32>) ? 2 * sizeof(GScratch<16>)
+                                                                             : sizeof(GScratch<32>);
 
 
-__device__ __forceinline__ int warp_sum_i(int v) {
+// A lane group that plans one scenario: the whole warp (G = 32) or one half
+// (G = 16; two scenarios per warp).  All collectives are restricted to the
+// group's member mask; ballots come back shifted to the group's lanes.
+template <int G>
+struct Grp {
+  unsigned m;
+  int sh;
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return G == 32 ? __ballot_sync(m, p) : (__ballot_sync(m, p) >> sh) & 0xFFFFu;
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(m, p); }
+  __device__ __forceinline__ bool all(bool p) const { return __all_sync(m, p); }
+  template <typename T> __device__ __forceinline__ T shfl(T v, int s) const { return __shfl_sync(m, v, s, G); }
+  template <typename T> __device__ __forceinline__ T shfl_up(T v, int o) const { return __shfl_up_sync(m, v, o, G); }
+  template <typename T> __device__ __forceinline__ T shfl_xor(T v, int o) const { return __shfl_xor_sync(m, v, o, G); }
+  __device__ __forceinline__ void sync() const { __syncwarp(m); }
+};
+
+template <int G>
+__device__ __forceinline__ int warp_sum_i(int v, const Grp<G>& gp) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = G / 2; o > 0; o >>= 1) v += gp.shfl_xor(v, o);
   return v;
 }
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
+template <int G>
+__device__ __forceinline__ long long warp_sum_ll(long long v, const Grp<G>& gp) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = G / 2; o > 0; o >>= 1) v += gp.shfl_xor(v, o);
   return v;
 }
 
@@ -110,10 +137,11 @@ __device__ __forceinline__ int class_capacity(uint32_t m, int c) {
   }
 }
 
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+template <int G>
+__device__ __forceinline__ int warp_incl_scan(int v, int lane, const Grp<G>& gp) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, v, o);
+  for (int o = 1; o < G; o <<= 1) {
+    const int t = gp.shfl_up(v, o);
     if (lane >= o) v += t;
   }
   return v;
@@ -133,13 +161,13 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // capacity prefix has a closed form: relocation starts from an empty map,
 // so when size 4 is queued every existing GPU holds one size-7 segment, and
 // when size 3 is queued the n7 first GPUs are full and the rest hold 4@0.
-template <int c>
-__device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, int my_opt, long long my_count,
+template <int c, int G>
+__device__ __forceinline__ void relocate_class(GScratch<G>& W, int lane, int n, int my_opt, long long my_count,
                                                int my_last, uint32_t& mask, int& ngpc, int& len, int& ngpus,
-                                               int& n7, int& status) {
+                                               int& n7, int& status, const Grp<G>& gp) {
   // total segments <= 224 was checked, so per-service counts fit an int
   const int my_reps = lane < n ? (my_opt == c ? (int)my_count : 0) + (my_last == c ? 1 : 0) : 0;
-  unsigned pending = __ballot_sync(0xffffffffu, my_reps > 0);
+  unsigned pending = gp.ballot(my_reps > 0);
   if (!pending) return;
   int cap, incl;
   if (c == 4) {                      // empty map
@@ -151,14 +179,14 @@ __device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, 
     incl = lane < n7 ? 0 : lane < ngpus ? lane + 1 - n7 : ngpus - n7 + 2 * (lane + 1 - ngpus);
   } else {
     cap = class_capacity(mask, c);
-    incl = warp_incl_scan(cap, lane);
+    incl = warp_incl_scan(cap, lane, gp);
   }
   const int excl = incl - cap;
   int e = 0;                         // queue position of the current service's first item
   do {
     const int s = __ffs(pending) - 1;
     pending &= pending - 1;
-    const int reps = __shfl_sync(0xffffffffu, my_reps, s);
+    const int reps = gp.shfl(my_reps, s);
     const int hi = min(incl, e + reps);
     const uint16_t cat3 = (uint16_t)((s * 5 + c) << 3);
     int j = max(excl, e);
@@ -179,9 +207,78 @@ __device__ __forceinline__ void relocate_class(WarpScratch& W, int lane, int n, 
     }
     e += reps;
   } while (pending);
-  if (e > __shfl_sync(0xffffffffu, incl, 31)) { status = PARVA_CAPACITY; return; }  // needs GPU index >= 32
-  ngpus = max(ngpus, 32 - __clz(__ballot_sync(0xffffffffu, excl < e && cap > 0)));
+  if (e > gp.shfl(incl, G - 1)) { status = PARVA_CAPACITY; return; }  // needs GPU index >= G
+  ngpus = max(ngpus, 32 - __clz(gp.ballot(excl < e && cap > 0)));
   if (c == 4) n7 = ngpus;
+}
+
+// propose_small_segments over a lane group (see propose_small_warp in
+// parva_common.cuh: k2 candidates spread over the lanes, exact lexicographic
+// min reduction)
+template <int G>
+__device__ __forceinline__ bool propose_small_grp(double tp1, double tp2, double freed, long long& k2o,
+                                                 long long& k1o, int lane, const Grp<G>& gp) {
+  k2o = 0; k1o = 0;
+  if (freed <= 0.0) return true;
+  if (tp1 == 0.0 && tp2 == 0.0) return false;
+  long long max_k2 = 0;
+  if (tp2 != 0.0) max_k2 = (long long)ceil(__dsub_rn(__ddiv_rn(freed, tp2), 1e-12));
+  const double m = (1.0 > freed) ? 1.0 : freed;
+  const double thr = __dmul_rn(1e-12, m);
+  bool have = false;
+  long long bg = 0, bc = 0, bn = 0;
+  // (gpcs, count, -k2) packs order-preserving into one u64 when every field
+  // fits 21 bits: key = gpcs << 42 | count << 21 | (2^21 - 1 - k2)
+  const bool packed = max_k2 < (1ll << 19);
+  for (long long base = 0; base <= max_k2; base += G) {
+    const long long k2 = base + lane;
+    bool ok = k2 <= max_k2;
+    long long k1 = 0;
+    if (ok) {
+      const double covered = tp2 != 0.0 ? __dmul_rn((double)k2, tp2) : 0.0;
+      const double sh = __dsub_rn(freed, covered);
+      if (sh <= thr) k1 = 0;
+      else if (tp1 != 0.0) {
+        k1 = (long long)ceil(__dsub_rn(__ddiv_rn(sh, tp1), 1e-12));
+        if (k1 < 1) k1 = 1;
+      } else ok = false;
+    }
+    long long g, cn, nk;
+    // warp-uniform choice (the reductions are collective)
+    if (packed && gp.all(!ok || 2 * k2 + k1 < (1ll << 21))) {
+      unsigned long long key = ok ? ((unsigned long long)(2 * k2 + k1) << 42) |
+                                        ((unsigned long long)(k2 + k1) << 21) |
+                                        (unsigned long long)((1ll << 21) - 1 - k2)
+                                  : ~0ull;
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const unsigned long long k = gp.shfl_xor(key, o);
+        key = k < key ? k : key;
+      }
+      if (key == ~0ull) { g = cn = nk = LLONG_MAX; }
+      else {
+        g = (long long)(key >> 42);
+        cn = (long long)((key >> 21) & ((1ull << 21) - 1));
+        nk = (long long)(key & ((1ull << 21) - 1)) - ((1ll << 21) - 1);
+      }
+    } else {
+      g = ok ? 2 * k2 + k1 : LLONG_MAX; cn = ok ? k2 + k1 : LLONG_MAX; nk = ok ? -k2 : LLONG_MAX;
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const long long g2 = gp.shfl_xor(g, o);
+        const long long c2 = gp.shfl_xor(cn, o);
+        const long long n2 = gp.shfl_xor(nk, o);
+        if (g2 < g || (g2 == g && (c2 < cn || (c2 == cn && n2 < nk)))) { g = g2; cn = c2; nk = n2; }
+      }
+    }
+    if (g != LLONG_MAX && (!have || g < bg || (g == bg && (cn < bc || (cn == bc && nk < bn))))) {
+      have = true; bg = g; bc = cn; bn = nk;
+    }
+  }
+  if (!have) return false;
+  k2o = -bn;
+  k1o = bc + bn;
+  return true;
 }
 
 // Index view: segment tables always in shared memory; latency-sorted
@@ -297,7 +394,10 @@ struct alignas(16) TileSmem {
   double tp[kTileSvc * 5];                // best tp per (tile service, size class); 0 = absent
   uint64_t meta[kTileSvc];                // count | opt << 48 | last << 52 | status << 56 (15 = none)
   int32_t off[PB_THREADS + 1];            // tile scenario offsets (absolute service index)
-  int32_t next;                           // next tile scenario to plan
+  int32_t next;                           // next tile scenario to plan (half-warp pass)
+  int32_t next_over;                      // next overflow entry (full-warp pass)
+  int32_t n_over;
+  int16_t over[PB_THREADS];               // tile scenarios beyond a half-warp's width
 };
 
 __device__ __forceinline__ uint64_t pack_meta(int opt, int last, int status, long long count) {
@@ -360,11 +460,15 @@ __device__ __forceinline__ uint64_t tile_service(const PlanArgs& A, const IndexV
 
 // relocate + optimize + emit for scenario k (scenario-local services [0, n),
 // their tile results at cat_tp / meta); one warp.
-__device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratch& W, int k, int n,
+// Returns false (writing nothing) when a half-warp group (G = 16) meets a
+// limit of its width -- more than 16 services or GPUs -- so that a full warp
+// re-plans the scenario; for G = 32 those limits are the record's (CAPACITY).
+template <int G>
+__device__ __forceinline__ bool plan_scenario_warp(const PlanArgs& A, GScratch<G>& W, int k, int n,
                                                    const double* cat_tp, const uint64_t* meta, bool in_tile,
-                                                   int lane) {
+                                                   int lane, const Grp<G>& gp) {
   WCYC_START
-  reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
+  for (int w = lane; w < 32; w += G) reinterpret_cast<uint32_t*>(&W.rec)[w] = 0u;
 
   // ------------------------------------------------ configured services
   int err_status = 0, err_svc = 0;
@@ -379,21 +483,25 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
       my_last = (int)(m >> 52 & 15); if (my_last == 15) my_last = -1;
       st = (int)(m >> 56);
     }
-    const unsigned bad = __ballot_sync(0xffffffffu, lane < n && st != PARVA_OK);
+    const unsigned bad = gp.ballot(lane < n && st != PARVA_OK);
     if (bad) {
       err_svc = __ffs(bad) - 1;
-      err_status = __shfl_sync(0xffffffffu, st, err_svc);
+      err_status = gp.shfl(st, err_svc);
     }
   }
 
   int status = PARVA_OK;
   bool spill = false;
+  if (G < 32 && (n > G || !in_tile)) return false;
   if (n > PARVA_PLAN_MAX_SERVICES) status = PARVA_CAPACITY;
   else if (!in_tile) status = PARVA_BAD_INPUT;
   else if (err_status) status = err_status;
   else {
-    const long long segs = warp_sum_ll(lane < n ? my_count + (my_last >= 0) : 0);
-    if (segs > 32 * 7) status = PARVA_CAPACITY;
+    const long long segs = warp_sum_ll(lane < n ? my_count + (my_last >= 0) : 0, gp);
+    if (segs > G * 7) {
+      if (G < 32) return false;
+      status = PARVA_CAPACITY;
+    }
   }
 
   // per-lane GPU state (lane = GPU index) and ledger state (lane = service)
@@ -409,18 +517,19 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
   if (status == PARVA_OK) {
     // --------------------------------------------- relocate_segments
     // queue order (allocator.py:46-51): size classes 7,4,3,2,1
-    relocate_class<4>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
-    if (status == PARVA_OK) relocate_class<3>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
-    if (status == PARVA_OK) relocate_class<2>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
-    if (status == PARVA_OK) relocate_class<1>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
-    if (status == PARVA_OK) relocate_class<0>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status);
+    relocate_class<4>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status, gp);
+    if (status == PARVA_OK) relocate_class<3>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status, gp);
+    if (status == PARVA_OK) relocate_class<2>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status, gp);
+    if (status == PARVA_OK) relocate_class<1>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status, gp);
+    if (status == PARVA_OK) relocate_class<0>(W, lane, n, my_opt, my_count, my_last, mask, ngpc, len, ngpus, n7, status, gp);
   }
-  __syncwarp();
+  gp.sync();
   WCYC(1);
+  if (G < 32 && status == PARVA_CAPACITY) return false;   // would need more than G GPUs
 
   if (status == PARVA_OK) {
     n_before = ngpus;
-    const int total_before = warp_sum_i(lane < ngpus ? ngpc : 0);
+    const int total_before = warp_sum_i(lane < ngpus ? ngpc : 0, gp);
     *reinterpret_cast<uint4*>(W.bak[lane]) = *reinterpret_cast<const uint4*>(W.lst[lane]);
     const int bak_len = len, bak_ngpc = ngpc;
     const uint32_t bak_mask = mask;
@@ -432,10 +541,10 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
       // highest-index one below the last that is non-empty with <= threshold
       // GPCs (skipped GPUs are not touched, so checking them now is the same)
       for (int index = ngpus; ;) {
-        const unsigned cand = __ballot_sync(0xffffffffu, lane < index && len > 0 && ngpc <= A.threshold);
+        const unsigned cand = gp.ballot(lane < index && len > 0 && ngpc <= A.threshold);
         if (!cand) break;
         index = 31 - __clz(cand);
-        const int nl = __shfl_sync(0xffffffffu, len, index);
+        const int nl = gp.shfl(len, index);
         const double sv_freed = freed;
         const int sv_order = order, sv_next = next;
         int q2n = 0, q1n = 0, fail = -1, fsvc = 0, rot = nl;
@@ -444,28 +553,28 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
           const int cat = W.lst[index][kk] >> 3;
           const int s = cat / 5;
           const double tpp = cat_tp[cat];
-          const bool newkey = __shfl_sync(0xffffffffu, order, s) == 0;
+          const bool newkey = gp.shfl(order, s) == 0;
           if (newkey) next++;
           if (lane == s) {
             if (newkey) { order = next; freed = __dadd_rn(0.0, tpp); }
             else freed = __dadd_rn(freed, tpp);
           }
-          const double f = __shfl_sync(0xffffffffu, freed, s);
+          const double f = gp.shfl(freed, s);
           const double t1 = cat_tp[s * 5 + 0], t2 = cat_tp[s * 5 + 1];
           long long k2, k1;
-          if (!propose_small_warp(t1, t2, f, k2, k1, lane)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fsvc = s; rot = kk + 1; break; }
+          if (!propose_small_grp(t1, t2, f, k2, k1, lane, gp)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fsvc = s; rot = kk + 1; break; }
           if (lane == s) {
             for (long long j = 0; j < k2; j++) freed = __dsub_rn(freed, t2);
             for (long long j = 0; j < k1; j++) freed = __dsub_rn(freed, t1);
           }
-          if (qover || q2n + k2 > QCAP || q1n + k1 > QCAP) qover = true;
+          if (qover || q2n + k2 > G * 7 || q1n + k1 > G * 7) qover = true;
           else {
             for (int j = lane; j < k2; j += 32) W.q2[q2n + j] = (uint8_t)(s * 5 + 1);
             for (int j = lane; j < k1; j += 32) W.q1[q1n + j] = (uint8_t)(s * 5 + 0);
             q2n += (int)k2; q1n += (int)k1;
           }
         }
-        __syncwarp();
+        gp.sync();
         if (fail < 0) {
           if (qover) fail = PARVA_DIAG_NEED_NEW_GPU;
           else {
@@ -474,7 +583,7 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
               const int cat = j < q2n ? W.q2[j] : W.q1[j - q2n];
               const int c = cat % 5;
               const int st = (lane < ngpus && lane != index) ? find_start(mask, c) : -1;
-              const unsigned b = __ballot_sync(0xffffffffu, st >= 0);
+              const unsigned b = gp.ballot(st >= 0);
               if (!b) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
               const int g = __ffs(b) - 1;
               if (lane == g) {
@@ -485,7 +594,7 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
               if (lane == 0) W.undo[nu] = (uint8_t)g;
               nu++;
             }
-            __syncwarp();
+            gp.sync();
             if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
               for (int j = nu - 1; j >= 0; j--) {
                 const int g = W.undo[j];
@@ -524,11 +633,11 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
         } else if (lane == index) {
           len = 0; mask = 0; ngpc = 0;
         }
-        __syncwarp();
+        gp.sync();
       }
       // compaction + regression check (allocator.py:423-435)
-      const int n_after = __popc(__ballot_sync(0xffffffffu, lane < ngpus && len > 0));
-      const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0);
+      const int n_after = __popc(gp.ballot(lane < ngpus && len > 0));
+      const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0, gp);
       const double ua_before = unallocated(total_before, n_before);
       const double ua_after = unallocated(total_after, n_after);
       if (n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12)) {
@@ -538,7 +647,7 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
         freed = 0.0; order = 0; nd = 0;
       }
     }
-    __syncwarp();
+    gp.sync();
     WCYC(2);
 
     // ------------------------------------------------------- emit record
@@ -546,13 +655,13 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
     const int mine = good ? len : 0;
     int incl = mine;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    for (int o = 1; o < G; o <<= 1) {
+      const int v = gp.shfl_up(incl, o);
       if (lane >= o) incl += v;
     }
-    const int n_place = __shfl_sync(0xffffffffu, incl, 31);
-    const int n_final = __popc(__ballot_sync(0xffffffffu, good));
-    const int n_led = __popc(__ballot_sync(0xffffffffu, lane < n && order > 0));
+    const int n_place = gp.shfl(incl, G - 1);
+    const int n_final = __popc(gp.ballot(good));
+    const int n_led = __popc(gp.ballot(lane < n && order > 0));
     const int led_off = (2 * (n_place + nd) + 7) & ~7;
     const int need = led_off + 10 * n_led;
     if (need > PARVA_PLAN_PAYLOAD) {
@@ -583,16 +692,16 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
     // reset this lane's GPU list slots for the next scenario
     *reinterpret_cast<uint4*>(W.lst[lane]) = make_uint4(0, 0, 0, 0);
   }
-  __syncwarp();
+  gp.sync();
   if (status != PARVA_OK) {
-    reinterpret_cast<uint32_t*>(&W.rec)[lane] = 0u;
-    __syncwarp();
+    for (int w = lane; w < 32; w += G) reinterpret_cast<uint32_t*>(&W.rec)[w] = 0u;
+    gp.sync();
     if (lane == 0) {
       W.rec.status = (uint8_t)status;
       W.rec.err_service = (uint8_t)((status == PARVA_CAPACITY || (status == PARVA_BAD_INPUT && !in_tile)) ? 0 : err_svc);
     }
   }
-  __syncwarp();
+  gp.sync();
   uint8_t* dst = reinterpret_cast<uint8_t*>(A.plan) + (size_t)k * A.plan_bytes;
   if (status == PARVA_OK && spill && A.spill_direct) {
     // 64-byte records, streamed mode: the full record goes to its scenario's
@@ -603,7 +712,7 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
     // 64-byte records: the full record goes to the spill list
     int slot = 0;
     if (lane == 0) slot = atomicAdd(A.spill_count, 1);
-    slot = __shfl_sync(0xffffffffu, slot, 0);
+    slot = gp.shfl(slot, 0);
     if (slot < A.spill_cap) {
       uint8_t* e = A.spill + (size_t)slot * kSpillEntry;
       if (lane == 0) *reinterpret_cast<int4*>(e) = make_int4(k, 0, 0, 0);
@@ -615,8 +724,9 @@ __device__ __forceinline__ void plan_scenario_warp(const PlanArgs& A, WarpScratc
   } else if (lane < A.plan_bytes / 16) {
     reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
   }
-  __syncwarp();
+  gp.sync();
   WCYC(3);
+  return true;
 }
 
 // Where a tile loop reads its scenarios: offsets indexable at [k, k1], the
@@ -648,7 +758,7 @@ __device__ __forceinline__ uint64_t src_service(const PlanArgs& A, const IndexVi
 // threads configure a tile's services into shared memory, then the warps
 // plan its scenarios (taken from a shared counter, so uneven scenarios
 // balance inside the CTA).  All threads of the CTA call it.
-__device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, WarpScratch& W,
+__device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, uint8_t* area,
                                           const TileSrc& S, int k, const int k1, int tid, int lane) {
 #ifdef PARVA_PHASE_TIMING
   int dbg_n = 0;
@@ -662,7 +772,7 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
     const int off_e = e <= k1 ? src_ld(S.off + e, S.cg) : 0;
     const bool fits = e <= k1 && (tid == 0 || off_e - a0 <= kTileSvc);
     if (e <= k1) T.off[tid + 1] = off_e;
-    if (tid == 0) { T.off[0] = a0; T.next = 0; }
+    if (tid == 0) { T.off[0] = a0; T.next = 0; T.next_over = 0; T.n_over = 0; }
     const int n_tile = __syncthreads_count(fits);
     const int a_end = T.off[n_tile];
 
@@ -683,20 +793,43 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
     dbg_first = false;
 #endif
 
-    // plan the tile's scenarios, warp per scenario
+    // plan the tile's scenarios, two per warp: each half-warp takes
+    // scenarios from the shared counter; one that needs more than 16
+    // services or GPUs goes to the overflow list, re-planned by full warps
+    {
+      const int h = lane >> 4, hl = lane & 15;
+      const Grp<16> gh{0xFFFFu << (16 * h), 16 * h};
+      GScratch<16>& Wh = reinterpret_cast<GScratch<16>*>(area)[h];
+      for (;;) {
+        int j = 0;
+        if (hl == 0) j = atomicAdd(&T.next, 1);
+        j = gh.shfl(j, 0);
+        if (j >= n_tile) break;
+        const int b = T.off[j] - a0;
+        const int n = T.off[j + 1] - T.off[j];
+        const bool in_tile = b >= 0 && n >= 0 && b + n <= kTileSvc;
+        if (!plan_scenario_warp<16>(A, Wh, S.scen_base + k + j, n, T.tp + (in_tile ? b * 5 : 0),
+                                    T.meta + (in_tile ? b : 0), in_tile, hl, gh)) {
+          if (hl == 0) T.over[atomicAdd(&T.n_over, 1)] = (int16_t)j;
+        }
+#ifdef PARVA_PHASE_TIMING
+        dbg_n++;
+#endif
+      }
+    }
+    __syncthreads();
     for (;;) {
-      int j = 0;
-      if (lane == 0) j = atomicAdd(&T.next, 1);
-      j = __shfl_sync(0xffffffffu, j, 0);
-      if (j >= n_tile) break;
+      int x = 0;
+      if (lane == 0) x = atomicAdd(&T.next_over, 1);
+      x = __shfl_sync(0xffffffffu, x, 0);
+      if (x >= T.n_over) break;
+      const int j = T.over[x];
       const int b = T.off[j] - a0;
       const int n = T.off[j + 1] - T.off[j];
       const bool in_tile = b >= 0 && n >= 0 && b + n <= kTileSvc;
-      plan_scenario_warp(A, W, S.scen_base + k + j, n, T.tp + (in_tile ? b * 5 : 0), T.meta + (in_tile ? b : 0),
-                         in_tile, lane);
-#ifdef PARVA_PHASE_TIMING
-      dbg_n++;
-#endif
+      plan_scenario_warp<32>(A, *reinterpret_cast<GScratch<32>*>(area), S.scen_base + k + j, n,
+                             T.tp + (in_tile ? b * 5 : 0), T.meta + (in_tile ? b : 0),
+                             in_tile, lane, Grp<32>{0xffffffffu, 0});
     }
 #ifdef PARVA_PHASE_TIMING
     if (lane == 0 && blockIdx.x < 1024) {
@@ -709,21 +842,22 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
   }
 }
 
-__global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_batch_kernel(PlanArgs A) {
+#ifndef PARVA_TILE_MINB
+#define PARVA_TILE_MINB 2
+#endif
+__global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
-  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
+    TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
   __shared__ uint64_t bar;
   PHASE(0);
-  const IndexView V = load_index(A, smem_raw + sizeof(WarpScratch) * PB_WARPS + sizeof(TileSmem), !A.cfg_given,
-                                 &bar);
+  const IndexView V = load_index(A, smem_raw + kWarpArea * PB_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
   PHASE(1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // this CTA's contiguous block of scenarios
   const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
   const int k = blockIdx.x * per;
   const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
-  run_tiles(A, V, T, scratch[warp], S, k, min(A.n_scen, k + per), tid, lane);
+  run_tiles(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
   PHASE(3);
 }
 
@@ -902,7 +1036,7 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
 #ifdef PARVA_PHASE_TIMING
     long long wt2 = clock64();
 #endif
-    plan_scenario_warp(A, W, j, n, S.tp, S.meta, n >= 0, lane);
+    plan_scenario_warp<32>(A, W, j, n, S.tp, S.meta, n >= 0, lane, Grp<32>{0xffffffffu, 0});
 #ifdef PARVA_PHASE_TIMING
     if (lane == 0 && blockIdx.x < 1024) {
       g_warp_wait[blockIdx.x][warp][0] += wt1 - wt0;
@@ -948,8 +1082,8 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
   const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
   const int kind = wm ? 1 : 0;
-  const size_t smem = sizeof(WarpScratch) * PB_WARPS +
-                      (wm ? sizeof(WarpSvc) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice : sizeof(TileSmem)) +
+  const size_t smem = (wm ? (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
+                          : kWarpArea * PB_WARPS + sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
   struct DevCfg { size_t conf, occ; int n_sm, per; };
