@@ -304,9 +304,10 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
  * plan records an overflow area of k full 128-byte records -- a scenario
  * with status PARVA_SPILLED has its full record at index k) live in pinned,
  * mapped host memory.  Inside the one kernel loader warps copy the input
- * block over PCIe in 4 KB slices, in order, into a device staging area and
- * publish each slice with a flag; every warp then takes the next scenario,
- * waits for its chunk's slices, configures and plans it, and
+ * block over PCIe in 8 KB slices, in order, into a device staging area and
+ * publish each slice with a flag; every half warp then takes the next
+ * scenario, waits for its chunk's slices, configures and plans it (full
+ * warps re-plan the few that need more than 16 services or GPUs), and
  * writes its records straight into the host output block.  So the H2D
  * stream, the planning and the D2H writes overlap.  Scratch:
  * parva_plan_host_mapped_scratch bytes of device memory (initialised by the

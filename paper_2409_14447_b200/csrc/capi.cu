@@ -475,10 +475,15 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
   return off;
 }
 
+// scratch head: work counters, slice flags
+static size_t mapped_head_bytes(int64_t n_slices) {
+  return up256(size_t(parva::kWorkWords) * 4) + up256(size_t(n_slices) * 4);
+}
+
 size_t parva_plan_host_mapped_scratch(int64_t in_bytes) {
   if (in_bytes < 0) return 0;
   const int64_t n_slices = (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice;
-  return 256 + up256(16) + up256(size_t(n_slices) * 4) + up256(size_t(in_bytes));
+  return 256 + mapped_head_bytes(n_slices) + up256(size_t(in_bytes));
 }
 
 // (device, pointer) -> device address of a pinned block, or the pointer
@@ -534,7 +539,7 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
                            int32_t threshold, int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
                            size_t scratch_bytes, void* stream) {
   if (!tables || !index || !h_in || !h_out || !d_scratch || n_scenarios < 0 || n_services < 0 || in_bytes < 16 ||
-      in_bytes % 16 != 0)
+      in_bytes % 16 != 0 || int64_t(n_scenarios) > in_bytes / 4)
     return PARVA_BAD_INPUT;
   parva_chunk_layout L;
   if (parva_mapped_layout(n_scenarios, n_services, cfg_format, plan_bytes, &L) != PARVA_OK) return PARVA_BAD_INPUT;
@@ -551,10 +556,11 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
   if (!mapped_ptr(dev, h_in, &d_in, &in_host) || !mapped_ptr(dev, h_out, &d_out, &out_host)) return PARVA_BAD_INPUT;
   if (!in_host) return PARVA_BAD_INPUT;   // the streamed input block must be pinned host memory
   uint8_t* base = (uint8_t*)(((uintptr_t)d_scratch + 255) & ~uintptr_t(255));
-  uint32_t* work = (uint32_t*)base;
-  uint32_t* flags = (uint32_t*)(base + up256(16));
   const int64_t n_slices = (in_bytes + parva::kStreamSlice - 1) / parva::kStreamSlice;
-  uint8_t* staging = base + up256(16) + up256(size_t(n_slices) * 4);
+  uint32_t* work = (uint32_t*)base;
+  uint32_t* flags = (uint32_t*)(base + up256(size_t(parva::kWorkWords) * 4));
+  const size_t head = mapped_head_bytes(n_slices);
+  uint8_t* staging = base + head;
   uint32_t epoch = 0;
   {
     std::lock_guard<std::mutex> lock(g_graph_mu);
@@ -563,8 +569,8 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
       if (e.dev == dev && e.scratch == d_scratch && e.bytes == scratch_bytes) { E = &e; break; }
     if (!E || E->epoch == 0xFFFFFFFFu) {
       // first use of this scratch: zero the counters and flags
-      if (cudaStreamSynchronize(s) != cudaSuccess || cudaMemset(base, 0, up256(16) + up256(size_t(n_slices) * 4)) !=
-          cudaSuccess) return PARVA_LAUNCH_ERROR;
+      if (cudaStreamSynchronize(s) != cudaSuccess || cudaMemset(base, 0, head) != cudaSuccess)
+        return PARVA_LAUNCH_ERROR;
       if (!E) { g_mapped_epochs.emplace_back(); E = &g_mapped_epochs.back(); }
       E->dev = dev; E->scratch = d_scratch; E->bytes = scratch_bytes; E->epoch = 0;
     }

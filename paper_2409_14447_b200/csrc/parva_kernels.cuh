@@ -34,9 +34,9 @@ struct PlanArgs {
   int spill_cap;
   int32_t* spill_count;          // 64-byte records: spill list header
   uint8_t* spill;                // spill_cap entries of kSpillEntry bytes
-  // warp kernel (zero-copy host entry): warps take scenarios from work[0],
-  // loader warps take input slices from work[2]; work[1] counts finished
-  // warps (the last one resets all three, so they are zero between launches)
+  // warp kernel (zero-copy host entry): half warps take scenarios from
+  // work[0]; work[1] counts finished warps (the last one resets the counters,
+  // so they are zero between launches)
   uint32_t* work = nullptr;
   int spill_direct = 0;          // 64-byte records: full record at spill + 128 * scenario
   // streamed inputs (warp kernel, zero-copy host entry): the packed input
@@ -55,8 +55,9 @@ struct PlanArgs {
 constexpr int kStreamSlice = 8192;   // streamed input slice (one TMA bulk copy)
 constexpr int kLoaderBufs = 3;       // shared-memory slice buffers per loader
 
-constexpr int kSpillEntry = 144;
-constexpr int kMaxDevices = 64;    // per-device launch-configuration caches   // int32 scenario, 12 B pad, 128-byte record
+constexpr int kSpillEntry = 144;   // int32 scenario, 12 B pad, 128-byte record
+constexpr int kMaxDevices = 64;    // per-device launch-configuration caches
+constexpr int kWorkWords = 8;      // work counters of the warp kernel
 
 int launch_configure_sweep(const parva_tables* t, int nq, const int32_t* q_table, const double* q_rate,
                            const double* q_bound, parva_config_record* out, cudaStream_t stream);

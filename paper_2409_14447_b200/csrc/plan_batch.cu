@@ -861,14 +861,18 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   PHASE(3);
 }
 
-// K2, warp-autonomous form: every warp takes scenarios one at a time from a
-// device counter (work[0]) and configures its own scenario (lane = service,
-// the same prefix-argmax search) before planning it -- no block barriers,
-// so loads, configuration and planning of different warps overlap freely.
-struct alignas(16) WarpSvc {
-  double tp[32 * 5];                      // best tp per (service, size class); 0 = absent
-  uint64_t meta[32];
+// K2, warp-autonomous form: every half warp takes scenarios one at a time
+// from a device counter (work[0]) and configures its own scenario (lane =
+// service, the same prefix-argmax search) before planning it -- no block
+// barriers, so loads, configuration and planning of different warps overlap
+// freely.  Per-group service staging:
+template <int G>
+struct alignas(16) GSvc {
+  double tp[G * 5];                       // best tp per (service, size class); 0 = absent
+  uint64_t meta[G];
 };
+using WarpSvc = GSvc<32>;
+static_assert(2 * sizeof(GSvc<16>) == sizeof(WarpSvc), "two half-warp staging areas fill one warp's");
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -932,6 +936,9 @@ __device__ __forceinline__ void stream_loader(const PlanArgs& A, uint8_t* buf, u
       st_release_u32(&A.slice_flag[s], A.epoch);
       mbar_arrive(&empty[b]);
     }
+#ifdef PARVA_PHASE_TIMING
+    if (blockIdx.x < 1024) g_phase[blockIdx.x][2] = gtimer();   // this loader's last slice published
+#endif
   }
 }
 
@@ -947,104 +954,151 @@ __device__ __forceinline__ void stream_wait_thread(const PlanArgs& A, const void
     }
 }
 
-// the same for a warp (lane 0 waits)
-__device__ __forceinline__ void stream_wait(const PlanArgs& A, const void* p_lo, const void* p_hi, int lane) {
-  if (lane == 0) stream_wait_thread(A, p_lo, p_hi);
-  __syncwarp();
+// the same for a lane group (its lane 0 waits)
+template <int G>
+__device__ __forceinline__ void group_wait(const PlanArgs& A, const void* p_lo, const void* p_hi, int gl,
+                                           const Grp<G>& gp) {
+  if (gl == 0) stream_wait_thread(A, p_lo, p_hi);
+  gp.sync();
+}
+
+// A group's current chunk of the streamed input (a header, i.e. the chunk
+// table, followed by chunk blocks; scenarios ascend per group).
+struct ChunkCursor {
+  int c = -1, scen_lo = 0, svc_lo = 0;
+  const int32_t* off = nullptr;
+  const double* rate = nullptr;
+  const double* bound = nullptr;
+  const uint16_t* table = nullptr;
+};
+
+// Configure and plan streamed scenario j with one lane group.  A half warp
+// returns false (no plan written) for a scenario with more than 16 services
+// and plan_scenario_warp<16>'s false (more than 16 GPUs / 112 segments): the
+// whole warp re-plans it.
+template <int G>
+__device__ __forceinline__ bool stream_plan_one(const PlanArgs& A, const IndexView& V, GScratch<G>& W,
+                                                GSvc<G>& S, ChunkCursor& C, int j, int n_ch, int ch_scen,
+                                                int gl, const Grp<G>& gp) {
+#ifdef PARVA_PHASE_TIMING
+  const long long wt0 = clock64();
+#endif
+  const int cj = min(j / ch_scen, n_ch - 1);      // chunks hold ch_scen scenarios (the last one fewer)
+  if (cj != C.c) {
+    C.c = cj;
+    const parva_stream_chunk* tab = reinterpret_cast<const parva_stream_chunk*>(A.stream_dst + 16);
+    C.scen_lo = __ldcg(&tab[cj].scen_lo);
+    C.svc_lo = __ldcg(&tab[cj].svc_lo);
+    const int kc = __ldcg(&tab[cj].k), mc = __ldcg(&tab[cj].m);
+    const uint8_t* blk = A.stream_dst + __ldcg(&tab[cj].offset);
+    const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
+    C.off = reinterpret_cast<const int32_t*>(blk);
+    C.rate = reinterpret_cast<const double*>(blk + rate_off);
+    C.bound = C.rate + mc;
+    C.table = reinterpret_cast<const uint16_t*>(C.bound + mc);
+    group_wait<G>(A, blk, C.table + mc, gl, gp);  // the whole chunk block has landed
+  }
+  const int jl = j - C.scen_lo;
+  const int a0 = __ldcg(C.off + jl);
+  const int n = __ldcg(C.off + jl + 1) - a0;
+  if (G < 32 && n > G) return false;
+#ifdef PARVA_PHASE_TIMING
+  const long long wt1 = clock64();
+#endif
+  for (int b = 0; b < n; b += G) {
+    if (b + gl < n) {
+      const int i = a0 + b + gl;
+      double tpc[5];
+      const uint64_t m = svc_configure(A, V, (int)__ldcg(C.table + i), __ldcg(C.rate + i), __ldcg(C.bound + i),
+                                       (int64_t)C.svc_lo + i, tpc);
+      if (b == 0) {
+#pragma unroll
+        for (int cc = 0; cc < 5; cc++) S.tp[gl * 5 + cc] = tpc[cc];
+        S.meta[gl] = m;
+      }
+    }
+  }
+  gp.sync();
+#ifdef PARVA_PHASE_TIMING
+  const long long wt2 = clock64();
+  const bool ok = plan_scenario_warp<G>(A, W, j, n, S.tp, S.meta, n >= 0, gl, gp);
+  if (gl == 0 && blockIdx.x < 1024) {
+    unsigned long long* w = g_warp_wait[blockIdx.x][threadIdx.x >> 5];
+    atomicAdd(&w[0], (unsigned long long)(wt1 - wt0));
+    atomicAdd(&w[1], (unsigned long long)(wt2 - wt1));
+    atomicAdd(&w[2], (unsigned long long)(clock64() - wt2));
+    atomicAdd(&w[3], 1ull);
+  }
+  return ok;
+#else
+  return plan_scenario_warp<G>(A, W, j, n, S.tp, S.meta, n >= 0, gl, gp);
+#endif
 }
 
 __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
-  WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + sizeof(WarpScratch) * PB_WARPS);
   __shared__ uint64_t bar;
   __shared__ uint64_t loader_bars[2 * kLoaderBufs];
+  __shared__ int stop_flag[PB_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) stop_flag[warp] = 0;
+  uint8_t* area = smem_raw + kWarpArea * warp;
+  WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + kWarpArea * PB_WARPS);
+  uint8_t* loader_buf = smem_raw + (kWarpArea + sizeof(WarpSvc)) * PB_WARPS;
   PHASE(0);
   if ((int)blockIdx.x < A.n_loaders && threadIdx.x == 0) {
     for (int b = 0; b < 2 * kLoaderBufs; b++) mbar_init(&loader_bars[b], 1);
     fence_mbar_init();
   }
   // (load_index's block barriers also publish the loader mbarrier inits)
-  const IndexView V = load_index(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS +
-                                        kLoaderBufs * kStreamSlice,
-                                 true, &bar);
+  const IndexView V = load_index(A, loader_buf + kLoaderBufs * kStreamSlice, true, &bar);
   // loader roles (warps 0 and 1 of the first n_loaders CTAs), then they plan
   // too; the CTAs' other warps start planning right away
   if ((int)blockIdx.x < A.n_loaders && warp < 2) {
-    if (lane == 0)
-      stream_loader(A, smem_raw + (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS, loader_bars, warp);
+    if (lane == 0) stream_loader(A, loader_buf, loader_bars, warp);
     __syncwarp();
   }
   PHASE(1);
-  WarpScratch& W = scratch[warp];
-  WarpSvc& S = wsvc[warp];
-  // the input is a header (chunk table) followed by chunk blocks; this
-  // warp's current chunk (scenarios ascend per warp)
-  int c = -1, c_scen_lo = 0, c_svc_lo = 0;
-  const int32_t* c_off = nullptr;
-  const double* c_rate = nullptr;
-  const double* c_bound = nullptr;
-  const uint16_t* c_table = nullptr;
-  stream_wait(A, A.stream_dst, A.stream_dst + 16, lane);
+  const Grp<32> gw{0xffffffffu, 0};
+  group_wait<32>(A, A.stream_dst, A.stream_dst + 16, lane, gw);
   const int n_ch = __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst));
   const int ch_scen = max(1, __ldcg(reinterpret_cast<const int32_t*>(A.stream_dst) + 1));
-  stream_wait(A, A.stream_dst, A.stream_dst + parva_stream_header_bytes(n_ch), lane);
-  for (;;) {
-    int j = 0;
-    if (lane == 0) j = (int)atomicAdd(&A.work[0], 1u);
-    j = __shfl_sync(0xffffffffu, j, 0);
-    if (j >= A.n_scen) break;
-#ifdef PARVA_PHASE_TIMING
-    long long wt0 = clock64(), wt1 = wt0;
-#endif
-    const int cj = min(j / ch_scen, n_ch - 1);     // chunks hold ch_scen scenarios (the last one fewer)
-    if (cj != c) {
-      c = cj;
-      const parva_stream_chunk* tab = reinterpret_cast<const parva_stream_chunk*>(A.stream_dst + 16);
-      c_scen_lo = __ldcg(&tab[c].scen_lo);
-      c_svc_lo = __ldcg(&tab[c].svc_lo);
-      const int kc = __ldcg(&tab[c].k), mc = __ldcg(&tab[c].m);
-      const uint8_t* blk = A.stream_dst + __ldcg(&tab[c].offset);
-      const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
-      c_off = reinterpret_cast<const int32_t*>(blk);
-      c_rate = reinterpret_cast<const double*>(blk + rate_off);
-      c_bound = c_rate + mc;
-      c_table = reinterpret_cast<const uint16_t*>(c_bound + mc);
-      stream_wait(A, blk, c_table + mc, lane);   // the whole chunk block has landed
-    }
-    const int jl = j - c_scen_lo;
-    const int a0 = __ldcg(c_off + jl);
-    const int n = __ldcg(c_off + jl + 1) - a0;
-#ifdef PARVA_PHASE_TIMING
-    wt1 = clock64();
-#endif
-    for (int b = 0; b < n; b += 32) {
-      if (b + lane < n) {
-        const int i = a0 + b + lane;
-        double tpc[5];
-        const uint64_t m = svc_configure(A, V, (int)__ldcg(c_table + i), __ldcg(c_rate + i),
-                                         __ldcg(c_bound + i), (int64_t)c_svc_lo + i, tpc);
-        if (b == 0) {
-#pragma unroll
-          for (int cc = 0; cc < 5; cc++) S.tp[lane * 5 + cc] = tpc[cc];
-          S.meta[lane] = m;
+  group_wait<32>(A, A.stream_dst, A.stream_dst + parva_stream_header_bytes(n_ch), lane, gw);
+
+  // Each half warp takes scenarios from the ticket counter.  A half that
+  // meets a scenario it cannot plan (more than 16 services / GPUs) raises
+  // the warp's stop flag; once its sibling has finished its current
+  // scenario the whole warp plans the pending one(s), then both halves go on.
+  {
+    const int h = lane >> 4, hl = lane & 15;
+    const Grp<16> gh{0xFFFFu << (16 * h), 16 * h};
+    GScratch<16>& Wh = reinterpret_cast<GScratch<16>*>(area)[h];
+    GSvc<16>& Sh = reinterpret_cast<GSvc<16>*>(&wsvc[warp])[h];
+    volatile int* stop = &stop_flag[warp];
+    ChunkCursor C, Cw;
+    bool out = false;                                  // this half saw the tickets run out
+    for (;;) {
+      int pend = -1;
+      while (!out && !*stop) {
+        int j = 0;
+        if (hl == 0) j = (int)atomicAdd(&A.work[0], 1u);
+        j = gh.shfl(j, 0);
+        if (j >= A.n_scen) { out = true; break; }
+        if (!stream_plan_one<16>(A, V, Wh, Sh, C, j, n_ch, ch_scen, hl, gh)) {
+          pend = j;
+          if (hl == 0) *stop = 1;
         }
       }
+      __syncwarp();
+      const int p0 = __shfl_sync(0xffffffffu, pend, 0), p1 = __shfl_sync(0xffffffffu, pend, 16);
+      if (p0 >= 0)
+        stream_plan_one<32>(A, V, *reinterpret_cast<GScratch<32>*>(area), wsvc[warp], Cw, p0, n_ch, ch_scen, lane, gw);
+      if (p1 >= 0)
+        stream_plan_one<32>(A, V, *reinterpret_cast<GScratch<32>*>(area), wsvc[warp], Cw, p1, n_ch, ch_scen, lane, gw);
+      if (__all_sync(0xffffffffu, out)) break;
+      if (lane == 0) *stop = 0;
+      __syncwarp();
     }
-    __syncwarp();
-#ifdef PARVA_PHASE_TIMING
-    long long wt2 = clock64();
-#endif
-    plan_scenario_warp<32>(A, W, j, n, S.tp, S.meta, n >= 0, lane, Grp<32>{0xffffffffu, 0});
-#ifdef PARVA_PHASE_TIMING
-    if (lane == 0 && blockIdx.x < 1024) {
-      g_warp_wait[blockIdx.x][warp][0] += wt1 - wt0;
-      g_warp_wait[blockIdx.x][warp][1] += wt2 - wt1;
-      g_warp_wait[blockIdx.x][warp][2] += clock64() - wt2;
-      g_warp_wait[blockIdx.x][warp][3] += 1;
-    }
-#endif
   }
 #ifdef PARVA_PHASE_TIMING
   if (lane == 0 && blockIdx.x < 1024) g_warp_end[blockIdx.x][warp][0] = gtimer();
@@ -1082,7 +1136,7 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
   const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
   const int kind = wm ? 1 : 0;
-  const size_t smem = (wm ? (sizeof(WarpScratch) + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
+  const size_t smem = (wm ? (kWarpArea + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
                           : kWarpArea * PB_WARPS + sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used

@@ -115,10 +115,14 @@ def run_mapped(n=10_000):
     wend = (we[:, :, 0] - t0) / 1e3
     print(f"CTAs {used.sum()}  start spread {(ph[:, 0].max() - t0) / 1e3:.2f} us")
     print(f"  loader CTAs phase-1 end: min {load_end.min():.2f} p50 {np.median(load_end):.2f} max {load_end.max():.2f} us")
+    pub = ph[:, 2][ph[:, 2] > 0]
+    if pub.size:
+        pub = (pub - t0) / 1e3
+        print(f"  last slice published: min {pub.min():.2f} p50 {np.median(pub):.2f} max {pub.max():.2f} us")
     print(f"  warp end: min {wend.min():.2f} p50 {np.median(wend):.2f} p90 {np.percentile(wend, 90):.2f} max {wend.max():.2f} us")
     cy = cyc[used].astype(np.float64)
     nsc = cy[:, :, 3].sum()
-    print(f"  per scenario (warp cycles, 10 runs): wait {cy[:, :, 0].sum() / nsc:.0f}  configure {cy[:, :, 1].sum() / nsc:.0f}"
+    print(f"  per scenario (group cycles, 10 runs): locate+wait {cy[:, :, 0].sum() / nsc:.0f}  configure {cy[:, :, 1].sum() / nsc:.0f}"
           f"  plan {cy[:, :, 2].sum() / nsc:.0f}   scenarios counted {nsc:.0f}")
 
 

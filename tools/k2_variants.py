@@ -25,7 +25,7 @@ def variants():
     vs = {"head": (["HEAD"], []), "base": ([], [])}
     for w, mb in ():   # launch-shape variants, e.g. ((17, 2), (12, 3), (24, 1))
         vs[f"w{w}_b{mb}"] = ([], [f"-DPARVA_PB_WARPS={w}", f"-DPARVA_PB_MINB={mb}"])
-    for flags in (("-DPARVA_TILE_MINB=1",), ("-DPARVA_PB_WARPS=12", "-DPARVA_TILE_MINB=2")):
+    for flags in ():   # flag variants, e.g. (("-DPARVA_TILE_MINB=1",),)
         vs["_".join(f.split("=")[0][8:] + f.split("=")[1] for f in flags)] = ([], list(flags))
     if PATCH_DIR.exists():
         for f in sorted(PATCH_DIR.glob("*.patch")):
