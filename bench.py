@@ -315,22 +315,40 @@ def main():
     # Every timed call streams the 2 MB input block over PCIe into the GPU
     # (loader warps, in order), plans, writes config + plan records (freed_rate
     # ledger included) straight into the pinned output block, and synchronizes.
-    mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64)
-    for _ in range(args.warmup):
-        mb.run(dt)
+    # Steps are pipelined E2E_DEPTH deep (submit / wait, one scratch and
+    # output block per slot): step i+1's input streams while step i finishes
+    # planning; the host waits for every step's completion word.
+    E2E_DEPTH = 4
+    mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, depth=E2E_DEPTH)
+
+    def e2e_steps(k):
+        for i in range(k):
+            mb.submit(dt, i % E2E_DEPTH)
+            if i >= E2E_DEPTH - 1:
+                mb.wait((i - E2E_DEPTH + 1) % E2E_DEPTH)
+        for i in range(max(0, k - E2E_DEPTH + 1), k):
+            mb.wait(i % E2E_DEPTH)
+
+    e2e_steps(max(args.warmup, E2E_DEPTH))
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
+    e2e_steps(args.steps)
+    e2e_s = time.perf_counter() - t0
+    dev_plan = N.records_to_numpy(res.plan, n, PLAN_DTYPE)
+    e2e_parity = all(mb.outputs(s)[1].tobytes() == dev_plan.tobytes() for s in range(E2E_DEPTH))
+    # one synchronous call per step (launch + stream synchronize), reported beside it
+    for _ in range(args.warmup):
+        mb.run(dt)
+    t0 = time.perf_counter()
     for _ in range(args.steps):
         mb.run(dt)
-    e2e_s = time.perf_counter() - t0
-    e_cfg, e_plan = mb.outputs()
-    dev_plan = N.records_to_numpy(res.plan, n, PLAN_DTYPE)
-    e2e_parity = bool(e_plan.tobytes() == dev_plan.tobytes())
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    sync_s = time.perf_counter() - t0
+    e2e_parity = e2e_parity and mb.outputs(0)[1].tobytes() == dev_plan.tobytes()
+    te = torch.tensor([e2e_s, sync_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te[0])
+    e2e_s, sync_s = float(te[0]), float(te[1])
     # the staged-copy alternative (3-chunk H2D / plan / D2H CUDA-graph pipeline), reported beside it
     pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=3, cfg_format=2, plan_bytes=64)
     for _ in range(args.warmup):
@@ -374,11 +392,17 @@ def main():
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
         "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": mb.h2d_bytes, "d2h_bytes_per_step": mb.d2h_bytes,
-                "api": "parva_plan_host_mapped (C ABI): one launch per step; loader warps stream the pinned "
-                       "input block over PCIe in order while the other warps plan each scenario as its chunk "
-                       "lands and write 8-B config + 64-B plan records (freed_rate ledger included; full records "
-                       "of overflowing scenarios in an overflow area) straight into the pinned output block",
+                "api": "parva_plan_host_mapped_submit / _wait (C ABI): one launch per step, pipelined "
+                       f"{E2E_DEPTH} deep (programmatic dependent launches: the next step's input streams while "
+                       "this one finishes planning; the host waits for every step's completion word); loader "
+                       "warps stream the pinned input block over PCIe in order while the other warps plan each "
+                       "scenario as its chunk lands and write 8-B config + 64-B plan records (freed_rate ledger "
+                       "included; full records of overflowing scenarios in an overflow area) straight into the "
+                       "step's pinned output block",
+                "pipeline_depth": E2E_DEPTH,
                 "plan_records_equal_device_path": e2e_parity,
+                "synchronous": {"value": n_global * args.steps / sync_s, "unit": UNIT,
+                                "api": "parva_plan_host_mapped: one launch + stream synchronize per step"},
                 "copy_pipeline": {"value": n_global * args.steps / copy_s, "unit": UNIT,
                                   "api": "parva_plan_host_packed: 3-chunk H2D / plan / D2H CUDA-graph pipeline",
                                   "plan_records_equal_device_path": copy_parity}},

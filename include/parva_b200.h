@@ -313,7 +313,8 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
  * parva_plan_host_mapped_scratch bytes of device memory (initialised by the
  * first call with it; one call at a time per scratch).  Synchronizes
  * `stream` before returning.  The device address of the last few blocks is
- * cached: call parva_forget_block before freeing a block. */
+ * cached and a scratch keeps its flag epoch: call parva_forget_block before
+ * freeing a block or a scratch. */
 void parva_forget_block(const void* h_block);
 int parva_mapped_layout(int32_t k, int32_t m, int32_t cfg_format, int32_t plan_bytes,
                         parva_chunk_layout* out);
@@ -323,6 +324,23 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
                            int64_t in_bytes, void* h_out, int32_t optimize, int32_t threshold,
                            int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
                            size_t scratch_bytes, void* stream);
+
+/* Asynchronous form: enqueue the same call and return at once with a ticket
+ * for parva_plan_host_mapped_wait, which spins on a completion word the
+ * kernel writes into pinned host memory after a system-scope fence (no
+ * stream synchronize).  Consecutive calls on one stream overlap: each is a
+ * programmatic dependent launch, so the next call's loaders start streaming
+ * its input while the previous call plans its last scenarios.  Each call in
+ * flight needs its own scratch and output block (a second call on a scratch
+ * first waits for the first).  Replaces a sequence of plan_services calls
+ * (pipeline.py:83-111) over successive scenario batches. */
+int parva_plan_host_mapped_submit(const parva_tables* tables, const parva_index* index,
+                                  int32_t n_scenarios, int32_t n_services, const void* h_in,
+                                  int64_t in_bytes, void* h_out, int32_t optimize,
+                                  int32_t threshold, int32_t cfg_format, int32_t plan_bytes,
+                                  void* d_scratch, size_t scratch_bytes, void* stream,
+                                  uint64_t* ticket);
+int parva_plan_host_mapped_wait(uint64_t ticket);
 
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional

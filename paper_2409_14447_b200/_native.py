@@ -78,7 +78,8 @@ EXPORTS = (
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
-    "parva_stream_pack", "parva_forget_block", "parva_simulate", "parva_sim_log1p", "parva_sim_exponential",
+    "parva_stream_pack", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
+    "parva_simulate", "parva_sim_log1p", "parva_sim_exponential",
 )
 
 

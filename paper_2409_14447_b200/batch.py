@@ -362,10 +362,16 @@ class MappedHostBatch:
     Inside one kernel, loader warps stream the input block over PCIe in
     order while the other warps plan each scenario as soon as its chunk has
     landed and write its records straight into the output block; `run` is
-    one launch plus a stream synchronize."""
+    one launch plus a stream synchronize.
+
+    depth > 1 keeps that many calls in flight (one scratch and one output
+    block per slot): `submit(dt, slot)` enqueues a call without waiting,
+    `wait(slot)` spins on its completion word; consecutive submits on a
+    stream overlap (the next call's input stream starts while the previous
+    call finishes planning)."""
 
     def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64,
-                 chunk_scen: int = 32):
+                 chunk_scen: int = 32, depth: int = 1):
         torch = N.require_cuda()
         L = N.lib()
         scen_off = np.asarray(scen_off, dtype=np.int64)
@@ -378,11 +384,25 @@ class MappedHostBatch:
         self.in_bytes = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(self._off32), C.c_int32(chunk_scen)))
         if self.in_bytes < 0:
             raise ValueError("invalid scenario offsets")
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.depth = depth
         self.h_in = torch.zeros(max(self.in_bytes, 256), dtype=torch.uint8).pin_memory()
-        self.h_out = torch.zeros(max(self.layout.out_bytes, 256), dtype=torch.uint8).pin_memory()
+        self.h_outs = [torch.zeros(max(self.layout.out_bytes, 256), dtype=torch.uint8).pin_memory()
+                       for _ in range(depth)]
         self.scratch_bytes = int(L.parva_plan_host_mapped_scratch(C.c_int64(self.in_bytes)))
-        self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda")
+        self.scratches = [torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda") for _ in range(depth)]
+        self._tickets = [0] * depth
+        self._ticket = C.c_uint64(0)
         self.fill(scen_off, svc_table, svc_rate, svc_bound)
+
+    @property
+    def h_out(self):
+        return self.h_outs[0]
+
+    @property
+    def scratch(self):
+        return self.scratches[0]
 
     def fill(self, scen_off, svc_table, svc_rate, svc_bound):
         scen_off = np.asarray(scen_off, dtype=np.int64)
@@ -397,26 +417,50 @@ class MappedHostBatch:
         if n != self.in_bytes:
             raise ValueError("parva_stream_pack failed (offsets changed shape?)")
 
-    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
+    def _call_args(self, dt, optimize, threshold, stream, slot):
         sh = N.stream_handle(stream)
-        key = (id(dt), bool(optimize), int(threshold), sh.value)
-        args = self._args.get(key) if hasattr(self, "_args") else None
-        if args is None:   # the argument tuple is built once per (tables, options, stream)
+        key = (id(dt), bool(optimize), int(threshold), sh.value, slot)
+        hit = self._args.get(key) if hasattr(self, "_args") else None
+        if hit is None:   # the argument tuple is built once per (tables, options, stream, slot)
             args = (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
-                    C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes), C.c_void_p(self.h_out.data_ptr()),
-                    C.c_int32(int(optimize)), C.c_int32(int(threshold)), C.c_int32(self.cfg_format),
-                    C.c_int32(self.plan_bytes), N.ptr(self.scratch), C.c_size_t(self.scratch_bytes), sh)
+                    C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes),
+                    C.c_void_p(self.h_outs[slot].data_ptr()), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
+                    C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes), N.ptr(self.scratches[slot]),
+                    C.c_size_t(self.scratch_bytes), sh)
             self._args = getattr(self, "_args", {})
             self._args[key] = (args, dt)
-        else:
-            args = args[0]
-        N.check(N.lib().parva_plan_host_mapped(*args), "parva_plan_host_mapped")
+            return args
+        return hit[0]
+
+    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
+        """One synchronous call on slot 0."""
+        self.wait(0)
+        N.check(N.lib().parva_plan_host_mapped(*self._call_args(dt, optimize, threshold, stream, 0)),
+                "parva_plan_host_mapped")
+
+    def submit(self, dt: N.DeviceTables, slot: int = 0, optimize: bool = True, threshold: int = 4, stream=None):
+        """Enqueue a call writing into slot `slot`'s output block; returns at once."""
+        N.check(N.lib().parva_plan_host_mapped_submit(*self._call_args(dt, optimize, threshold, stream, slot),
+                                                      C.byref(self._ticket)), "parva_plan_host_mapped_submit")
+        self._tickets[slot] = self._ticket.value
+
+    def wait(self, slot: int = 0):
+        """Wait until slot `slot`'s last submitted call has written its records."""
+        t = self._tickets[slot]
+        if t:
+            self._tickets[slot] = 0
+            N.check(N.lib().parva_plan_host_mapped_wait(C.c_uint64(t)), "parva_plan_host_mapped_wait")
 
     def __del__(self):
         try:
+            for s in range(self.depth):
+                self.wait(s)
             L = N.lib()
             L.parva_forget_block(C.c_void_p(self.h_in.data_ptr()))
-            L.parva_forget_block(C.c_void_p(self.h_out.data_ptr()))
+            for h in self.h_outs:
+                L.parva_forget_block(C.c_void_p(h.data_ptr()))
+            for d in self.scratches:
+                L.parva_forget_block(C.c_void_p(d.data_ptr()))
         except Exception:  # noqa: BLE001 -- interpreter shutdown
             pass
 
@@ -432,10 +476,10 @@ class MappedHostBatch:
         lay = self.layout
         return int(lay.out_cfg + _CFG_DT[self.cfg_format].itemsize * self.n_svc)
 
-    def outputs(self):
-        """(config records, 128-byte plan records); spilled scenarios are
-        restored from the overflow area."""
-        lay, buf = self.layout, self.h_out.numpy()
+    def outputs(self, slot: int = 0):
+        """(config records, 128-byte plan records) of slot `slot`; spilled
+        scenarios are restored from the overflow area."""
+        lay, buf = self.layout, self.h_outs[slot].numpy()
         cdt = _CFG_DT[self.cfg_format]
         pdt = PLAN64_DTYPE if self.plan_bytes == 64 else PLAN_DTYPE
         k, m = self.n_scen, self.n_svc

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -517,27 +518,62 @@ static bool mapped_ptr(int dev, const void* p, void** d, bool* host) {
   return true;
 }
 
-// Forget a block (call before freeing it, so a later allocation at the same
-// address is looked up again).
-void parva_forget_block(const void* p) {
-  std::lock_guard<std::mutex> lock(g_mapped_mu);
-  for (auto& e : g_mapped_ptrs)
-    if (e.p == p) e = MappedPtr{};
-}
-
-// scratch -> epoch of its slice flags (flags hold the epoch of the call that wrote them)
-struct MappedEpoch {
+// scratch -> its call slot: the epoch of its slice flags (flags hold the
+// epoch of the call that wrote them), and for asynchronous calls a completion
+// word in pinned host memory (the kernel stores the epoch of each finished
+// call) plus the epoch last submitted, so a new call on the same scratch
+// first waits for the previous one
+struct MappedSlot {
   int dev = -1;
   void* scratch = nullptr;
   size_t bytes = 0;
   uint32_t epoch = 0;
+  uint32_t submitted = 0;       // epoch of the last asynchronous call (0 = none)
+  cudaStream_t stream = nullptr;
 };
-static std::vector<MappedEpoch> g_mapped_epochs;
+constexpr int kMappedSlots = 1024;
+static std::vector<MappedSlot> g_mapped_slots;
+static uint32_t* g_done_host = nullptr;   // kMappedSlots completion words (pinned, mapped, portable)
 
-int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
-                           int32_t n_services, const void* h_in, int64_t in_bytes, void* h_out, int32_t optimize,
-                           int32_t threshold, int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
-                           size_t scratch_bytes, void* stream) {
+// Forget a block or scratch (call before freeing it, so a later allocation at
+// the same address is looked up again and a scratch's flags are re-zeroed).
+void parva_forget_block(const void* p) {
+  {
+    std::lock_guard<std::mutex> lock(g_mapped_mu);
+    for (auto& e : g_mapped_ptrs)
+      if (e.p == p) e = MappedPtr{};
+  }
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  for (auto& e : g_mapped_slots)
+    if (e.scratch == p) e = MappedSlot{};
+}
+
+static bool done_reached(uint32_t slot, uint32_t epoch) {
+  const uint32_t v = *reinterpret_cast<volatile uint32_t*>(g_done_host + slot);
+  return (int32_t)(v - epoch) >= 0;
+}
+
+// Spin until the call (slot, epoch) has published completion; the stream is
+// queried now and then so a failed launch cannot hang the host.
+static int wait_done(uint32_t slot, uint32_t epoch, cudaStream_t s) {
+  for (uint64_t i = 0;; i++) {
+    if (done_reached(slot, epoch)) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return PARVA_OK;
+    }
+    if ((i & 4095) == 4095) {
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) return done_reached(slot, epoch) ? PARVA_OK : PARVA_LAUNCH_ERROR;
+      if (e != cudaErrorNotReady) return PARVA_LAUNCH_ERROR;
+    }
+  }
+}
+
+static int plan_host_mapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                            int32_t n_services, const void* h_in, int64_t in_bytes, void* h_out, int32_t optimize,
+                            int32_t threshold, int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
+                            size_t scratch_bytes, void* stream, uint64_t* ticket) {
+  if (ticket) *ticket = 0;
   if (!tables || !index || !h_in || !h_out || !d_scratch || n_scenarios < 0 || n_services < 0 || in_bytes < 16 ||
       in_bytes % 16 != 0 || int64_t(n_scenarios) > in_bytes / 4)
     return PARVA_BAD_INPUT;
@@ -561,20 +597,56 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
   uint32_t* flags = (uint32_t*)(base + up256(size_t(parva::kWorkWords) * 4));
   const size_t head = mapped_head_bytes(n_slices);
   uint8_t* staging = base + head;
-  uint32_t epoch = 0;
+  uint32_t epoch = 0, slot = 0, pending = 0;
+  uint32_t* d_done = nullptr;
+  cudaStream_t pending_stream = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_graph_mu);
-    MappedEpoch* E = nullptr;
-    for (auto& e : g_mapped_epochs)
-      if (e.dev == dev && e.scratch == d_scratch && e.bytes == scratch_bytes) { E = &e; break; }
-    if (!E || E->epoch == 0xFFFFFFFFu) {
+    if (ticket && !g_done_host) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, kMappedSlots * 4, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+        return PARVA_LAUNCH_ERROR;
+      std::memset(p, 0, kMappedSlots * 4);
+      g_done_host = (uint32_t*)p;
+    }
+    int E = -1, free_slot = -1;
+    for (int i = 0; i < (int)g_mapped_slots.size(); i++) {
+      const auto& e = g_mapped_slots[i];
+      if (e.dev == dev && e.scratch == d_scratch && e.bytes == scratch_bytes) { E = i; break; }
+      if (!e.scratch && free_slot < 0) free_slot = i;
+    }
+    if (E < 0 || g_mapped_slots[E].epoch == 0xFFFFFFFFu) {
       // first use of this scratch: zero the counters and flags
+      if (E >= 0 && g_mapped_slots[E].submitted &&
+          wait_done((uint32_t)E, g_mapped_slots[E].submitted, g_mapped_slots[E].stream) != PARVA_OK)
+        return PARVA_LAUNCH_ERROR;
       if (cudaStreamSynchronize(s) != cudaSuccess || cudaMemset(base, 0, head) != cudaSuccess)
         return PARVA_LAUNCH_ERROR;
-      if (!E) { g_mapped_epochs.emplace_back(); E = &g_mapped_epochs.back(); }
-      E->dev = dev; E->scratch = d_scratch; E->bytes = scratch_bytes; E->epoch = 0;
+      if (E < 0) E = free_slot;
+      if (E < 0) {
+        if ((int)g_mapped_slots.size() >= kMappedSlots) return PARVA_CAPACITY;
+        g_mapped_slots.emplace_back();
+        E = (int)g_mapped_slots.size() - 1;
+      }
+      MappedSlot& M = g_mapped_slots[E];
+      M = MappedSlot{};
+      M.dev = dev; M.scratch = d_scratch; M.bytes = scratch_bytes;
+      if (g_done_host) g_done_host[E] = 0;
     }
-    epoch = ++E->epoch;
+    MappedSlot& M = g_mapped_slots[E];
+    slot = (uint32_t)E;
+    pending = M.submitted;
+    pending_stream = M.stream;
+    epoch = ++M.epoch;
+    if (ticket) { M.submitted = epoch; M.stream = s; }
+    else M.submitted = 0;
+  }
+  // one call in flight per scratch: an unfinished asynchronous call on it
+  // must complete first
+  if (pending && wait_done(slot, pending, pending_stream) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+  if (ticket && cudaHostGetDevicePointer((void**)&d_done, g_done_host + slot, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return PARVA_LAUNCH_ERROR;
   }
   if (n_scenarios > 0) {
     uint8_t* out = (uint8_t*)d_out;
@@ -598,10 +670,53 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
     A.slice_flag = flags;
     A.epoch = epoch;
     A.n_loaders = loaders_for(in_bytes);
+    A.done_word = d_done;
+    A.pdl = ticket ? 1 : 0;
     const int rc = parva::launch_plan_batch(A, s);
-    if (rc != PARVA_OK) return rc;
+    if (rc != PARVA_OK) {
+      if (ticket) {   // nothing will complete this epoch
+        std::lock_guard<std::mutex> lock(g_graph_mu);
+        g_mapped_slots[slot].submitted = 0;
+      }
+      return rc;
+    }
+  } else if (ticket) {
+    g_done_host[slot] = epoch;     // nothing to launch: complete at once (host store, in submission order)
+  }
+  if (ticket) {
+    *ticket = (uint64_t)slot << 32 | epoch;
+    return PARVA_OK;
   }
   return cudaStreamSynchronize(s) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
+
+int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                           int32_t n_services, const void* h_in, int64_t in_bytes, void* h_out, int32_t optimize,
+                           int32_t threshold, int32_t cfg_format, int32_t plan_bytes, void* d_scratch,
+                           size_t scratch_bytes, void* stream) {
+  return plan_host_mapped(tables, index, n_scenarios, n_services, h_in, in_bytes, h_out, optimize, threshold,
+                          cfg_format, plan_bytes, d_scratch, scratch_bytes, stream, nullptr);
+}
+
+int parva_plan_host_mapped_submit(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                                  int32_t n_services, const void* h_in, int64_t in_bytes, void* h_out,
+                                  int32_t optimize, int32_t threshold, int32_t cfg_format, int32_t plan_bytes,
+                                  void* d_scratch, size_t scratch_bytes, void* stream, uint64_t* ticket) {
+  if (!ticket) return PARVA_BAD_INPUT;
+  return plan_host_mapped(tables, index, n_scenarios, n_services, h_in, in_bytes, h_out, optimize, threshold,
+                          cfg_format, plan_bytes, d_scratch, scratch_bytes, stream, ticket);
+}
+
+int parva_plan_host_mapped_wait(uint64_t ticket) {
+  const uint32_t slot = (uint32_t)(ticket >> 32), epoch = (uint32_t)ticket;
+  if (epoch == 0) return PARVA_OK;                  // an empty call's ticket
+  cudaStream_t s = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    if (!g_done_host || slot >= g_mapped_slots.size()) return PARVA_BAD_INPUT;
+    s = g_mapped_slots[slot].stream;
+  }
+  return wait_done(slot, epoch, s);
 }
 
 size_t parva_plan_general_workspace(const parva_general_problem* p, int32_t gpu_cap) {

@@ -50,6 +50,12 @@ struct PlanArgs {
   uint32_t* slice_flag = nullptr;
   uint32_t epoch = 0;
   int n_loaders = 0;
+  // asynchronous calls: the last warp stores epoch to done_word (mapped host
+  // memory) after a system-scope fence; pdl launches the kernel with
+  // programmatic stream serialization, so it may start while the previous
+  // streamed call on the stream is still finishing its last scenarios
+  uint32_t* done_word = nullptr;
+  int pdl = 0;
 };
 
 constexpr int kStreamSlice = 8192;   // streamed input slice (one TMA bulk copy)

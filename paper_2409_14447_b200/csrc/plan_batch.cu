@@ -17,6 +17,7 @@
 // are re-planned by the general kernel (plan_general.cu).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "parva_async.cuh"
@@ -1042,6 +1043,9 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   __shared__ int stop_flag[PB_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) stop_flag[warp] = 0;
+  // a dependent streamed call (its own scratch and blocks) may start as soon
+  // as SM space frees up; nothing here waits for a predecessor
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint8_t* area = smem_raw + kWarpArea * warp;
   WarpSvc* wsvc = reinterpret_cast<WarpSvc*>(smem_raw + kWarpArea * PB_WARPS);
   uint8_t* loader_buf = smem_raw + (kWarpArea + sizeof(WarpSvc)) * PB_WARPS;
@@ -1103,13 +1107,22 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
 #ifdef PARVA_PHASE_TIMING
   if (lane == 0 && blockIdx.x < 1024) g_warp_end[blockIdx.x][warp][0] = gtimer();
 #endif
+  // every lane's record stores are ordered before the warp counts itself
+  // done (system scope when the host polls done_word instead of the stream)
+  if (A.done_word) __threadfence_system();
+  else __threadfence();
+  __syncwarp();
   if (lane == 0) {
-    __threadfence();
-    // last warp of the grid resets the counters for the next launch
+    // last warp of the grid resets the counters for the next launch and
+    // publishes completion
     if (atomicAdd(&A.work[1], 1u) == gridDim.x * PB_WARPS - 1) {
       atomicExch(&A.work[0], 0u);
       atomicExch(&A.work[2], 0u);
       atomicExch(&A.work[1], 0u);
+      if (A.done_word) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.done_word), "r"(A.epoch) : "memory");
+      }
     }
   }
 }
@@ -1156,8 +1169,22 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
     D.occ = smem;
   }
   if (D.per < 1) return false;
+  int per = D.per;
+  if (wm) {
+    // streamed calls: one CTA per SM (PARVA_STREAM_PER_SM; 0 = all that
+    // fit), so a dependent call's CTAs find SM space while this one is still
+    // planning (PCIe, not the planners, bounds a streamed call); every loader
+    // CTA must exist
+    static int s_env = -1;
+    if (s_env < 0) {
+      const char* e = std::getenv("PARVA_STREAM_PER_SM");
+      s_env = e ? std::max(0, std::atoi(e)) : 1;
+    }
+    if (s_env > 0) per = std::min(per, s_env);
+  }
   int g = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
-  if (g > D.n_sm * D.per) g = D.n_sm * D.per;
+  if (wm) g = std::max(g, A.n_loaders);
+  if (g > D.n_sm * per) g = D.n_sm * per;
   L->grid = g < 1 ? 1 : g;
   L->smem = smem;
   return true;
@@ -1173,8 +1200,23 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
   if (A.stream_src && !A.work) return PARVA_BAD_INPUT;
   LaunchCfg L;
   if (!plan_launch_config(A, &L)) return PARVA_LAUNCH_ERROR;
-  if (warp_mode(A)) plan_warp_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
-  else plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+  if (warp_mode(A)) {
+    PlanArgs B = A;
+    B.n_loaders = std::min(A.n_loaders, L.grid);   // loaders are the first CTAs
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(PB_THREADS);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = A.pdl ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, plan_warp_kernel, B) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+  } else {
+    plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+  }
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 

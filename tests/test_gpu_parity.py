@@ -378,6 +378,74 @@ def test_host_entry_mapped_fuzz(fx):
         assert cfg.tobytes() == tiny_config(ocfg).tobytes(), trial
 
 
+def test_host_entry_mapped_few_scenarios_many_services(fx):
+    """More input slices than scenarios-per-16: every loader CTA must be
+    launched (the grid covers the loaders), else the slices never land."""
+    from paper_2409_14447_b200.records import tiny_config
+    rng = np.random.default_rng(5)
+    nm = len(fx.models)
+    dt = N.device_tables_for(fx.tables)
+    for sizes in ((700, 650, 720), (1, 2000), (3000,)):
+        total = int(sum(sizes))
+        tab = rng.integers(0, nm, total).astype(np.int32)
+        rate = np.exp(rng.uniform(1.0, 9.0, total))
+        bound = np.exp(rng.uniform(2.5, 8.0, total)) / 2.0
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, rate, bound)
+        mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, chunk_scen=1)
+        assert mb.in_bytes > 8192 * len(sizes)
+        mb.run(dt)
+        cfg, plan = mb.outputs()
+        assert plan.tobytes() == oplan.tobytes(), sizes
+        assert cfg.tobytes() == tiny_config(ocfg).tobytes(), sizes
+
+
+def test_host_entry_mapped_async_overlap(fx):
+    """parva_plan_host_mapped_submit / _wait: calls of two batches
+    interleaved on one stream, two slots each (overlapping programmatic
+    dependent launches), a synchronous call and an empty batch in between;
+    every slot's records == oracle."""
+    from paper_2409_14447_b200.records import tiny_config
+    dt = N.device_tables_for(fx.tables)
+    pt = pack_tables(fx.tables)
+    batches = []
+    for n, seed in ((6_001, 21), (2_500, 22)):
+        sb = W.scenario_batch(fx, n, seed=seed)
+        k, M = sb.rate.shape
+        off = np.arange(k + 1, dtype=np.int32) * M
+        tab = np.tile(np.arange(M, dtype=np.int32), k)
+        rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
+        ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
+        mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, depth=2)
+        batches.append((mb, tiny_config(ocfg).tobytes(), oplan.tobytes()))
+    empty = B.MappedHostBatch(np.zeros(1, dtype=np.int32), np.zeros(0, np.int32), np.zeros(0), np.zeros(0),
+                              depth=2)
+    for rnd in range(3):
+        for slot in (0, 1):
+            for mb, _, _ in batches:
+                mb.h_outs[slot].zero_()
+        for slot in (0, 1):
+            for mb, _, _ in batches:
+                mb.submit(dt, slot)
+            empty.submit(dt, slot)
+        if rnd == 1:
+            batches[1][0].wait(0)
+            batches[1][0].run(dt)      # synchronous call on a slot with a finished async call
+        for slot in (0, 1):
+            empty.wait(slot)
+            for i, (mb, ecfg, eplan) in enumerate(batches):
+                mb.wait(slot)
+                cfg, plan = mb.outputs(slot)
+                assert plan.tobytes() == eplan, (rnd, slot, i)
+                assert cfg.tobytes() == ecfg, (rnd, slot, i)
+    # a second submit on a busy slot waits for the first (one call per scratch)
+    mb, ecfg, eplan = batches[0]
+    for _ in range(4):
+        mb.submit(dt, 0)
+    mb.wait(0)
+    assert mb.outputs(0)[1].tobytes() == eplan
+
+
 def test_reconfigure_service(fx):
     """§III-F re-planning (allocator.py:494-537) + diff_maps (:484-491) vs reference goldens."""
     for i, c in enumerate(golden("reconfigure_cases.json")):
