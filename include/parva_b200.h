@@ -215,6 +215,18 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index,
                      void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
                      void* stream);
 
+/* parva_plan_batch as a programmatic dependent launch: it may start while
+ * the previous call on `stream` is still planning its last scenarios (its
+ * CTAs take SM slots as the predecessor's retire), so back-to-back batches
+ * leave no idle tail.  The caller guarantees that no call still in flight
+ * writes anything this call reads or writes (rotate output buffers). */
+int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* index,
+                                int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,
+                                const int32_t* d_svc_table, const double* d_svc_rate,
+                                const double* d_svc_bound, int32_t optimize, int32_t threshold,
+                                void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
+                                void* stream);
+
 /* parva_plan_batch for tables too large for the shared-memory index: the
  * config records in d_cfg were produced by parva_configure_sweep. */
 int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios,

@@ -73,7 +73,7 @@ class SimResult(C.Structure):
 
 EXPORTS = (
     "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
-    "parva_plan_batch", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
+    "parva_plan_batch", "parva_plan_batch_overlapped", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",

@@ -45,8 +45,10 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries, const i
 static int plan_batch_impl(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                            int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
                            const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
-                           int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream) {
+                           int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream,
+                           int pdl = 0) {
   parva::PlanArgs A;
+  A.pdl = pdl;
   A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
   A.idx_best = index ? index->d_best : nullptr;
@@ -84,6 +86,21 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32
   if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
                          optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream);
+}
+
+// parva_plan_batch as a programmatic dependent launch: it may start while the
+// previous overlapped call on the stream is still finishing (its CTAs take
+// SM slots as the predecessor's retire).  The caller guarantees that no call
+// still in flight writes what this one reads or writes.
+int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                                int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table,
+                                const double* d_svc_rate, const double* d_svc_bound, int32_t optimize,
+                                int32_t threshold, void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
+                                void* stream) {
+  if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
+  if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
+  return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
+                         optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream, 1);
 }
 
 // Same as parva_plan_batch but the config records in d_cfg were produced by

@@ -848,8 +848,11 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
 #endif
 __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-    TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
+  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
   __shared__ uint64_t bar;
+  // an overlapped successor (parva_plan_batch_overlapped: disjoint buffers by
+  // contract) may take SM slots as this grid's CTAs retire
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   PHASE(0);
   const IndexView V = load_index(A, smem_raw + kWarpArea * PB_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
   PHASE(1);
@@ -1214,6 +1217,18 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
     cfg.attrs = at;
     cfg.numAttrs = A.pdl ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, plan_warp_kernel, B) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+  } else if (A.pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(PB_THREADS);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, plan_batch_kernel, A) != cudaSuccess) return PARVA_LAUNCH_ERROR;
   } else {
     plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
   }

@@ -24,7 +24,8 @@ from paper_2409_14447_b200 import _native as N  # noqa: E402
 from paper_2409_14447_b200 import batch as B  # noqa: E402
 from paper_2409_14447_b200 import workloads as W  # noqa: E402
 from paper_2409_14447_b200.configurator import Service, Triplet  # noqa: E402
-from paper_2409_14447_b200.records import CFG_COMPACT, CONFIG_DTYPE, compact_config  # noqa: E402
+from paper_2409_14447_b200.records import (CFG_COMPACT, CFG_TINY, CONFIG_DTYPE, PLAN_DTYPE, TINY_DTYPE,  # noqa: E402
+                                           compact_config)
 from paper_2409_14447_b200.tables import pack_dense, pack_tables  # noqa: E402
 
 
@@ -212,6 +213,42 @@ def test_c2_records_vs_oracle_and_goldens(fx):
     results = P.plan_many(sets, fx.tables)
     bad = [k for k, r in enumerate(results) if canon.digest(_canon_result(r)) != g["digests"][k]]
     assert not bad, bad[:10]
+
+
+def test_plan_batch_overlapped_back_to_back(fx):
+    """parva_plan_batch_overlapped: 24 back-to-back programmatic dependent
+    launches over 6 different batches into 3 rotating output blocks (and a
+    plain launch in between); every block holds exactly the oracle's records
+    of the batch planned into it last."""
+    from paper_2409_14447_b200.records import tiny_config
+    pt = pack_tables(fx.tables)
+    dt = N.device_tables_for(fx.tables)
+    ins, exp = [], []
+    for b in range(6):
+        sb = W.scenario_batch(fx, 3_001 + 500 * b, seed=40 + b)
+        n, M = sb.rate.shape
+        off = np.arange(n + 1, dtype=np.int32) * M
+        tab = np.tile(np.arange(M, dtype=np.int32), n)
+        rate, bound = sb.rate.ravel().copy(), sb.bound.ravel().copy()
+        ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
+        ins.append(tuple(N.to_device(a) for a in (off, tab, rate, bound)))
+        exp.append((tiny_config(ocfg).tobytes(), oplan.tobytes()))
+    big = max(int(x[0].shape[0]) - 1 for x in ins), max(int(x[1].shape[0]) for x in ins)
+    outs = [B.BatchResult(N.empty_records(big[1], TINY_DTYPE), N.empty_records(big[0], PLAN_DTYPE), big[0], big[1],
+                          CFG_TINY) for _ in range(3)]
+    last = {}
+    for i in range(24):
+        b, r = (5 * i + 1) % 6, i % 3
+        o = outs[r]
+        k, m = int(ins[b][0].shape[0]) - 1, int(ins[b][1].shape[0])
+        view = B.BatchResult(o.cfg[:m], o.plan[:k], k, m, CFG_TINY)
+        B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view, overlap=(i != 11))
+        last[r] = (b, view)
+    torch.cuda.synchronize()
+    for r, (b, view) in last.items():
+        cfg, plan = view.host()
+        assert plan.tobytes() == exp[b][1], (r, b)
+        assert cfg.tobytes() == exp[b][0], (r, b)
 
 
 def test_c4_sample_vs_oracle(fx):
