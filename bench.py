@@ -51,6 +51,28 @@ def ncu_traffic(kernel):
         return None
 
 
+def ncu_inst(kernel):
+    """Warp instructions per launch of `kernel` (smsp__inst_executed.sum of the
+    committed ncu capture), or None."""
+    try:
+        return int(json.loads((REPO / "profiles" / "ncu_traffic.json").read_text())[kernel]["warp_inst"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def issue_roofline(kernel, kern_s, sm_mhz):
+    """Instruction-issue roofline of a latency/issue-bound kernel: warp
+    instructions per launch (ncu) / launch time, against one instruction per
+    SM sub-partition per clock (148 SMs x 4 SMSPs x the sampled SM clock)."""
+    inst = ncu_inst(kernel)
+    if inst is None or not sm_mhz:
+        return None
+    peak = 148 * 4 * sm_mhz * 1e6
+    ach = inst / kern_s
+    return {"achieved": ach, "peak": peak, "unit": "warp-instructions/s", "frac": ach / peak,
+            "warp_inst_per_launch": inst, "source": "profiles/ncu_traffic.json warp_inst; peak at the sampled SM clock"}
+
+
 def peaks():
     try:
         p = json.loads(PEAKS_PATH.read_text())
@@ -431,6 +453,9 @@ def main():
     }
     clk_summary = clk.summary()
     line["clocks"] = clk_summary
+    line["roofline"]["issue"] = issue_roofline("plan_batch_kernel", kern_s, clk_summary.get("sm_mhz"))
+    line["roofline"]["issue_overlapped"] = issue_roofline("plan_batch_kernel", step_ms / 1000.0 / args.steps,
+                                                          clk_summary.get("sm_mhz"))
 
     # ---- C3 configurator sweep (HBM-roofline kernel), rank 0
     if not args.no_sweep and rank == 0:
