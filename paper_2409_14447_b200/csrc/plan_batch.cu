@@ -26,8 +26,10 @@
 
 namespace parva {
 
+// 12 warps x 3 CTAs per SM (56 registers, 36 warps resident) measured best
+// for K2 among 8-16 warps x 2-4 CTAs (tools/k2_variants.py)
 #ifndef PARVA_PB_WARPS
-#define PARVA_PB_WARPS 16
+#define PARVA_PB_WARPS 12
 #endif
 #ifndef PARVA_PB_MINB
 #define PARVA_PB_MINB 2
@@ -363,10 +365,13 @@ __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const
 // walks it in tiles of at most kTileSvc services: all threads configure the
 // tile's services (thread per service, configurator.py:189-191 through the
 // prefix-argmax index in shared memory), the per-service results stay in
-// shared memory, then the CTA's warps plan the tile's scenarios (warp per
-// scenario, taken from a shared counter so that uneven scenarios balance
-// inside the CTA).
-constexpr int kTileSvc = 1024;
+// shared memory, then the CTA's half warps plan the tile's scenarios (taken
+// from a shared counter so that uneven scenarios balance inside the CTA).
+// 256-service tiles keep three CTAs per SM within shared memory.
+#ifndef PARVA_TILE_SVC
+#define PARVA_TILE_SVC 256
+#endif
+constexpr int kTileSvc = PARVA_TILE_SVC;
 
 #ifdef PARVA_PHASE_TIMING
 // development probe (tools/k2_probe.py): per-CTA phase timestamps and per-warp
@@ -844,7 +849,7 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
 }
 
 #ifndef PARVA_TILE_MINB
-#define PARVA_TILE_MINB 2
+#define PARVA_TILE_MINB 3
 #endif
 __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
