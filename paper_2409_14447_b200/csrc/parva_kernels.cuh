@@ -58,8 +58,14 @@ struct PlanArgs {
   int pdl = 0;
 };
 
-constexpr int kStreamSlice = 8192;   // streamed input slice (one TMA bulk copy)
-constexpr int kLoaderBufs = 3;       // shared-memory slice buffers per loader
+#ifndef PARVA_STREAM_SLICE
+#define PARVA_STREAM_SLICE 8192
+#endif
+#ifndef PARVA_LOADER_BUFS
+#define PARVA_LOADER_BUFS 3
+#endif
+constexpr int kStreamSlice = PARVA_STREAM_SLICE;   // streamed input slice (one TMA bulk copy)
+constexpr int kLoaderBufs = PARVA_LOADER_BUFS;     // shared-memory slice buffers per loader
 
 constexpr int kSpillEntry = 144;   // int32 scenario, 12 B pad, 128-byte record
 constexpr int kMaxDevices = 64;    // per-device launch-configuration caches

@@ -25,11 +25,10 @@ def variants():
     vs = {"head": (["HEAD"], []), "base": ([], [])}
     for w, mb in ():   # launch-shape variants, e.g. ((17, 2), (12, 3), (24, 1))
         vs[f"w{w}_b{mb}"] = ([], [f"-DPARVA_PB_WARPS={w}", f"-DPARVA_PB_MINB={mb}"])
-    for flags in (("-DPARVA_PB_WARPS=12", "-DPARVA_TILE_MINB=3", "-DPARVA_TILE_SVC=256"),
-                  ("-DPARVA_PB_WARPS=12", "-DPARVA_TILE_MINB=3", "-DPARVA_TILE_SVC=384"),
-                  ("-DPARVA_PB_WARPS=10", "-DPARVA_TILE_MINB=4", "-DPARVA_TILE_SVC=128"),
-                  ("-DPARVA_PB_WARPS=14", "-DPARVA_TILE_MINB=3", "-DPARVA_TILE_SVC=256")):
-        vs["_".join(f.split("=")[0][8:] + f.split("=")[1] for f in flags)] = ([], list(flags))
+    # flag variants, e.g. ("-DPARVA_PB_WARPS=12", "-DPARVA_TILE_MINB=3", "-DPARVA_TILE_SVC=256"),
+    # ("-DPARVA_STREAM_SLICE=16384",), ("-DPARVA_NO_OUT",) (K2s without its record writes)
+    for flags in ():
+        vs["_".join(f[8:].replace("=", "") for f in flags)] = ([], list(flags))
     if PATCH_DIR.exists():
         for f in sorted(PATCH_DIR.glob("*.patch")):
             vs[f.stem] = ([f], [])
