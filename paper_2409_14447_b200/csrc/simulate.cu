@@ -33,6 +33,12 @@ namespace parva {
 
 constexpr int kSimLanes = 64;     // pending completions per service (its total lanes)
 constexpr int kSimSegs = 32;      // segments per service
+// One service per WARP (lane 0): every service's event loop takes its own
+// data-dependent path, so services sharing a warp would serialise (a warp
+// of 32 services ran ~20x slower than its arithmetic); a warp each also
+// spreads the few thousand services over every SM.
+constexpr int kSimWarps = 4;      // services (warps) per CTA
+constexpr int kRing = 32;         // last ingested arrivals per service, in shared memory
 
 // ------------------------------------------------------------- numpy PCG64
 struct Pcg64 {
@@ -175,8 +181,13 @@ struct ArrivalGen {
   }
 };
 
-__global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < P.n_services; s += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_problem P, parva_sim_result R) {
+  // the queue head (the oldest waiting arrival) is nearly always one of the
+  // last kRing ingested: read it from shared memory, not back from L2
+  __shared__ double ring[kRing][kSimWarps];
+  const int tx = threadIdx.x >> 5;
+  if (threadIdx.x & 31) return;
+  for (int s = blockIdx.x * kSimWarps + tx; s < P.n_services; s += gridDim.x * kSimWarps) {
     const int64_t b0 = P.d_buf_off[s];
     const int64_t cap = P.d_buf_off[s + 1] - b0;
     double* buf = R.d_buf + b0;            // ingested arrivals (ms), later the batch latencies
@@ -226,7 +237,9 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
     auto ingest = [&](double now) {       // evaluation.py:353-360
       while (have && nt <= now) {
         if (ptr == cap) { overflow = true; have = false; break; }
-        buf[ptr++] = nt;
+        buf[ptr] = nt;
+        ring[ptr & (kRing - 1)][tx] = nt;
+        ptr++;
         have = gen.next(nt);
       }
     };
@@ -239,7 +252,7 @@ __global__ void simulate_kernel(parva_sim_problem P, parva_sim_result R) {
         const int64_t qn = ptr - qh;
         const int64_t b = P.d_seg_batch[g0 + g];
         const int64_t n = b < qn ? b : qn;
-        const double first = buf[qh];
+        const double first = ptr - qh <= kRing ? ring[qh & (kRing - 1)][tx] : buf[qh];
         qh += n;
         const double latency = __dadd_rn(__dsub_rn(now, first), ms);
         buf[batches++] = latency;          // slot < qh: that arrival has left the queue
@@ -325,11 +338,10 @@ extern "C" int parva_simulate(const parva_sim_problem* p, const parva_sim_result
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  // one thread per service; small blocks spread the (few, long) threads over every SM
-  const int threads = 32;
-  int blocks = (p->n_services + threads - 1) / threads;
-  if (blocks > n_sm * 32) blocks = n_sm * 32;
-  parva::simulate_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*p, *r);
+  // one warp per service (lane 0), kSimWarps services per CTA
+  int blocks = (p->n_services + parva::kSimWarps - 1) / parva::kSimWarps;
+  if (blocks > n_sm * 16) blocks = n_sm * 16;
+  parva::simulate_kernel<<<blocks, parva::kSimWarps * 32, 0, (cudaStream_t)stream>>>(*p, *r);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
 

@@ -37,8 +37,26 @@ def timed_report(*a, **k):
 
 
 S._report = timed_report
+ev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+_lib = S.N.lib
+
+
+class _Timed:
+    def __getattr__(self, k):
+        return getattr(_lib(), k)
+
+    def parva_simulate(self, *a):
+        ev[0].record()
+        r = _lib().parva_simulate(*a)
+        ev[1].record()
+        return r
+
+
+S.N.lib = lambda: _Timed()
 s = torch.cuda.current_stream()
 t0 = time.perf_counter()
 S.run_simulations(jobs)
 t1 = time.perf_counter()
-print(f"run_simulations total {(t1 - t0) * 1e3:.1f} ms, of which host stats {tr[0] * 1e3:.1f} ms")
+torch.cuda.synchronize()
+print(f"run_simulations total {(t1 - t0) * 1e3:.1f} ms, of which host stats {tr[0] * 1e3:.1f} ms, "
+      f"simulate kernel {ev[0].elapsed_time(ev[1]):.1f} ms")
