@@ -450,6 +450,12 @@ typedef struct {
 } parva_sim_result;
 
 int parva_simulate(const parva_sim_problem* problem, const parva_sim_result* result, void* stream);
+/* Host-side seeding: the PCG64 states (state hi, lo, inc hi, lo per child)
+ * of np.random.default_rng(SeedSequence(seed).spawn(...)[first_child + c])
+ * for c < n_children, the seed given as little-endian uint32 words
+ * (evaluation.py:308-315 seeding; numpy SeedSequence + PCG64 seeding restated). */
+int parva_sim_seed_states(const uint32_t* seed_words, int32_t n_seed_words, int64_t first_child,
+                          int64_t n_children, uint64_t* out);
 /* Test hooks: glibc log1p on (-1, 0] as the simulator computes it, and numpy
  * Generator.exponential(scale) draws from a PCG64 state. */
 int parva_sim_log1p(const double* d_x, double* d_out, int64_t n, void* stream);

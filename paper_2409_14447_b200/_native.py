@@ -79,7 +79,7 @@ EXPORTS = (
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
     "parva_stream_pack", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
-    "parva_simulate", "parva_sim_log1p", "parva_sim_exponential",
+    "parva_simulate", "parva_sim_seed_states", "parva_sim_log1p", "parva_sim_exponential",
 )
 
 

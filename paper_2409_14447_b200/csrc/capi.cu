@@ -748,3 +748,81 @@ int parva_plan_general(const parva_general_problem* p, parva_general_result* r, 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- simulator seeding
+// numpy's SeedSequence(seed).spawn(n)[i] -> default_rng(child) PCG64 state,
+// restated (numpy/random/bit_generator.pyx: SeedSequence.mix_entropy,
+// generate_state; _pcg64.pyx / pcg64.h: pcg64_set_seed -> pcg64_srandom_r).
+// Host code: replaces ~11 us of Python object construction per service.
+namespace {
+constexpr uint32_t kInitA = 0x43b0d7e5u, kMultA = 0x931e8875u, kInitB = 0x8b51f9ddu, kMultB = 0x58f38dedu;
+constexpr uint32_t kMixL = 0xca01f9ddu, kMixR = 0x4973f715u;
+constexpr int kXShift = 16, kPool = 4;
+
+inline uint32_t hashmix(uint32_t v, uint32_t& h) {
+  v ^= h;
+  h *= kMultA;
+  v *= h;
+  v ^= v >> kXShift;
+  return v;
+}
+inline uint32_t mixw(uint32_t x, uint32_t y) {
+  uint32_t r = kMixL * x - kMixR * y;
+  r ^= r >> kXShift;
+  return r;
+}
+}  // namespace
+
+int parva_sim_seed_states(const uint32_t* seed_words, int32_t n_seed_words, int64_t first_child, int64_t n_children,
+                          uint64_t* out) {
+  if (!seed_words || n_seed_words < 1 || n_seed_words > 64 || first_child < 0 || n_children < 0 || !out)
+    return PARVA_BAD_INPUT;
+  typedef unsigned __int128 u128;
+  const u128 kMult = ((u128)0x2360ed051fc65da4ull << 64) | 0x4385df649fccf645ull;
+  uint32_t ent[80];
+  for (int64_t c = 0; c < n_children; c++) {
+    // assembled entropy: run entropy (zero-padded to the pool size, since a
+    // spawn key follows), then the spawn key (child index as uint32 words)
+    int ne = 0;
+    for (int i = 0; i < n_seed_words; i++) ent[ne++] = seed_words[i];
+    while (ne < kPool) ent[ne++] = 0u;
+    uint64_t key = (uint64_t)(first_child + c);
+    if (key == 0) ent[ne++] = 0u;
+    while (key) { ent[ne++] = (uint32_t)key; key >>= 32; }
+    // mix_entropy
+    uint32_t pool[kPool];
+    uint32_t h = kInitA;
+    for (int i = 0; i < kPool; i++) pool[i] = hashmix(i < ne ? ent[i] : 0u, h);
+    for (int s = 0; s < kPool; s++)
+      for (int d = 0; d < kPool; d++)
+        if (s != d) pool[d] = mixw(pool[d], hashmix(pool[s], h));
+    for (int s = kPool; s < ne; s++)
+      for (int d = 0; d < kPool; d++) pool[d] = mixw(pool[d], hashmix(ent[s], h));
+    // generate_state(4, uint64): 8 uint32 words from the cycled pool
+    uint32_t w[8];
+    uint32_t hb = kInitB;
+    for (int i = 0; i < 8; i++) {
+      uint32_t v = pool[i % kPool];
+      v ^= hb;
+      hb *= kMultB;
+      v *= hb;
+      v ^= v >> kXShift;
+      w[i] = v;
+    }
+    uint64_t val[4];
+    for (int k = 0; k < 4; k++) val[k] = (uint64_t)w[2 * k] | (uint64_t)w[2 * k + 1] << 32;
+    // pcg64_srandom_r(initstate = val[0]:val[1], initseq = val[2]:val[3])
+    const u128 initstate = ((u128)val[0] << 64) | val[1];
+    const u128 initseq = ((u128)val[2] << 64) | val[3];
+    const u128 inc = (initseq << 1) | 1u;
+    u128 st = 0;
+    st = st * kMult + inc;
+    st += initstate;
+    st = st * kMult + inc;
+    out[4 * c + 0] = (uint64_t)(st >> 64);
+    out[4 * c + 1] = (uint64_t)st;
+    out[4 * c + 2] = (uint64_t)(inc >> 64);
+    out[4 * c + 3] = (uint64_t)inc;
+  }
+  return PARVA_OK;
+}

@@ -194,6 +194,31 @@ class SimJob:
     sms_per_gpc: int = DEFAULT_SMS_PER_GPC
 
 
+def _spawn_states(seed, n: int) -> list:
+    """PCG64 states (state hi, lo, inc hi, lo) of default_rng(child) for the
+    children of SeedSequence(seed).spawn(n): the library's restatement for
+    non-negative integer seeds, numpy itself otherwise."""
+    if isinstance(seed, (int, np.integer)) and not isinstance(seed, bool) and int(seed) >= 0 and n > 0:
+        v, words = int(seed), []
+        while True:
+            words.append(v & 0xFFFFFFFF)
+            v >>= 32
+            if not v:
+                break
+        if len(words) <= 64:
+            w = np.asarray(words, dtype=np.uint32)
+            out = np.zeros(4 * n, dtype=np.uint64)
+            N.check(N.lib().parva_sim_seed_states(N.np_ptr(w), C.c_int32(len(words)), C.c_int64(0), C.c_int64(n),
+                                                  N.np_ptr(out)), "parva_sim_seed_states")
+            return [tuple(int(x) for x in out[4 * i:4 * i + 4]) for i in range(n)]
+    m = (1 << 64) - 1
+    states = []
+    for ss in np.random.SeedSequence(seed).spawn(n):
+        st = np.random.default_rng(ss).bit_generator.state["state"]
+        states.append((st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m))
+    return states
+
+
 class _Prepared:
     """Host-side layout of one job: service order, per-service generator
     state and arrival parameters, segments (evaluation.py:311-345)."""
@@ -208,23 +233,19 @@ class _Prepared:
         rates = workload.rate_map()
         dmap = job.dmap
         ordered = sorted({p.service_id for _, p in dmap.placements()} | set(rates) | set(services_by_id))
-        spawned = np.random.SeedSequence(job.seed).spawn(len(ordered))
         self.ids = ordered
-        self.svc, self.children, self.rates = [], [], []
+        self.svc, self.rates = [], []
         # per service: arrival kind (0 none, 1 poisson, 2 deterministic), PCG64
         # state, scale / step, chunk size / count
         self.akind, self.pcg, self.scale, self.count = [], [], [], []
-        for sid, ss in zip(ordered, spawned):
+        self.pcg = _spawn_states(job.seed, len(ordered))      # evaluation.py:308-315
+        for sid in ordered:
             svc = services_by_id.get(sid)
             if svc is None:
                 raise SimulationConfigError(f"no service definition for {sid!r}")
             rate = rates.get(sid, 0.0)
             self.svc.append(svc)
-            self.children.append(ss)
             self.rates.append(rate)
-            st = np.random.default_rng(ss).bit_generator.state["state"]
-            m = (1 << 64) - 1
-            self.pcg.append((st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m))
             if rate <= 0:
                 self.akind.append(0); self.scale.append(0.0); self.count.append(0)
             elif workload.kind == "deterministic":
@@ -263,7 +284,7 @@ class _Prepared:
     def host_arrivals(self, si: int) -> np.ndarray:
         """Arrivals (ms) of service si with numpy on the host -- the reference's
         own generator calls (for the CPU oracle in the tests)."""
-        rng = np.random.default_rng(self.children[si])
+        rng = np.random.default_rng(np.random.SeedSequence(self.job.seed).spawn(len(self.ids))[si])
         return _arrival_times(self.kind, self.rates[si], self.job.horizon_s, rng) * 1000.0
 
 

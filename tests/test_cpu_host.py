@@ -38,6 +38,20 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_sim_seed_states_match_numpy():
+    """parva_sim_seed_states (host C) == default_rng(SeedSequence(seed).spawn(n)[i])
+    PCG64 states, for small, 32-bit-boundary and multi-word seeds."""
+    from paper_2409_14447_b200.simulation import _spawn_states
+    m = (1 << 64) - 1
+    for seed in (0, 1, 7, 2**32 - 1, 2**32, 2**40 + 7, 2**70 + 3, 2**200 + 5):
+        got = _spawn_states(seed, 40)
+        exp = []
+        for ss in np.random.SeedSequence(seed).spawn(40):
+            st = np.random.default_rng(ss).bit_generator.state["state"]
+            exp.append((st["state"] >> 64, st["state"] & m, st["inc"] >> 64, st["inc"] & m))
+        assert got == exp, seed
+
+
 def test_record_layouts():
     assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128
 
