@@ -26,6 +26,7 @@ NativeLibraryError.
 
 from __future__ import annotations
 
+import copy
 import ctypes as C
 import math
 from dataclasses import dataclass, field
@@ -288,11 +289,30 @@ class _Prepared:
         return _arrival_times(self.kind, self.rates[si], self.job.horizon_s, rng) * 1000.0
 
 
+def _prepare_all(jobs: Sequence[SimJob]) -> list:
+    """_Prepared per job; jobs that share the deployment, tables, services,
+    workload and horizon (e.g. many seeds of one plan) share everything but
+    the generator states."""
+    memo, out = {}, []
+    for j in jobs:
+        key = (id(j.dmap), id(j.tables), id(j.services), id(j.workload), j.horizon_s)
+        t = memo.get(key)
+        if t is None:
+            t = memo[key] = _Prepared(j)
+            out.append(t)
+        else:
+            p = copy.copy(t)
+            p.job = j
+            p.pcg = _spawn_states(j.seed, len(t.ids))
+            out.append(p)
+    return out
+
+
 def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
     """Batched run_simulation: every job's services simulated in one launch
     (arrivals generated on the GPU from each service's numpy generator state)."""
     torch = N.require_cuda()
-    preps = [_Prepared(j) for j in jobs]
+    preps = _prepare_all(jobs)
     kind, pcg, scale, count, hs, buf_off = [], [], [], [], [], [0]
     seg_off, seg_ms, seg_batch, seg_lanes, slo, horizon = [0], [], [], [], [], []
     seg_rows = []                      # flat segment row -> (job, segment index)
@@ -338,9 +358,16 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
     if tot:
         within = torch.arange(tot, device="cuda") - torch.repeat_interleave(torch.cumsum(b_dev, 0) - b_dev, b_dev)
         idx = torch.repeat_interleave(starts, b_dev) + within
-        lat_all = o_buf[idx].cpu().numpy()
+        lat_dev = o_buf[idx]
+        # per-service sorted samples for the percentiles: one segmented sort
+        # on the device (values, then service id, both stable)
+        seg = torch.repeat_interleave(torch.arange(n, device="cuda"), b_dev)
+        v_sorted, perm = torch.sort(lat_dev, stable=True)
+        _, perm2 = torch.sort(seg[perm], stable=True)
+        srt_all = v_sorted[perm2].cpu().numpy()
+        lat_all = lat_dev.cpu().numpy()
     else:
-        lat_all = np.zeros(0)
+        lat_all = srt_all = np.zeros(0)
     arrived, served, batches, viol = (o[k].cpu().numpy() for k in ("arrived", "served", "batches", "viol"))
     busy = o_busy.cpu().numpy()
     lat_off = np.concatenate([[0], np.cumsum(batches)])
@@ -351,7 +378,8 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
         for si in range(m):
             for r in range(seg_off[k + si], seg_off[k + si + 1]):
                 busy_by_seg[seg_rows[r][1]] = busy[r]
-        lats = [lat_all[lat_off[k + si]:lat_off[k + si + 1]] for si in range(m)]
+        lats = [(lat_all[lat_off[k + si]:lat_off[k + si + 1]], srt_all[lat_off[k + si]:lat_off[k + si + 1]])
+                for si in range(m)]
         reports.append(_report(pr, lats, arrived[k:k + m], served[k:k + m], batches[k:k + m], viol[k:k + m],
                                busy_by_seg))
         k += m
@@ -378,10 +406,12 @@ def _percentile_sorted(srt: np.ndarray, q) -> float:
     return float(a + diff * gamma)
 
 
-def _latency_stats(lat: np.ndarray) -> dict:
+def _latency_stats(lat: np.ndarray, srt: np.ndarray | None = None) -> dict:
     """The reference's latency summary (evaluation.py:436-456): numpy mean
-    (pairwise sum), linear-interpolated percentiles, max; rounded to 6 dp."""
-    srt = np.sort(lat)
+    (pairwise sum, in batch order), linear-interpolated percentiles, max;
+    rounded to 6 dp.  `srt` = the sample sorted (else sorted here)."""
+    if srt is None:
+        srt = np.sort(lat)
     return {"mean": round(float(lat.mean()), 6),
             "p50": round(_percentile_sorted(srt, _Q[0]), 6),
             "p95": round(_percentile_sorted(srt, _Q[1]), 6),
@@ -406,11 +436,11 @@ def _report(pr: _Prepared, lats, arrived, served, batches, viol, busy_by_seg) ->
         na = int(arrived[si]) if len(arrived) else 0
         nb = int(batches[si]) if len(batches) else 0
         sv = int(served[si]) if len(served) else 0
-        lat = lats[si] if nb else None
+        lat, srt = lats[si] if nb else (None, None)
         out[sid] = ServiceSimStats(
             service_id=sid, arrived=na, served=sv, queued_at_end=na - sv, batches=nb,
             violations=int(viol[si]) if len(viol) else 0, achieved_rps=sv / job.horizon_s,
-            latency_ms=({} if lat is None else _latency_stats(lat)),
+            latency_ms=({} if lat is None else _latency_stats(lat, srt)),
         )
     return SimReport(horizon_s=job.horizon_s, seed=job.seed, kind=pr.kind, services=out, activity=activity)
 

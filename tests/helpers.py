@@ -111,4 +111,6 @@ def sim_report_with_oracle(oracle, job):
         arrived.append(arr.shape[0]); served.append(sv); batches.append(nb); viol.append(nv); lats.append(lat)
         for k, g in enumerate(per[si]):
             busy[g] = bz[k]
-    return S._report(pr, lats, np.array(arrived), np.array(served), np.array(batches), np.array(viol), busy), lats, busy
+    rep = S._report(pr, [(x, None) for x in lats], np.array(arrived), np.array(served), np.array(batches),
+                    np.array(viol), busy)
+    return rep, lats, busy

@@ -22,7 +22,7 @@ runs = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 jobs = [S.SimJob(res.deployment, fx.tables, services, wl, 10.0, seed) for seed in range(runs)]
 S.run_simulations(jobs[:4])
 t0 = time.perf_counter()
-preps = [S._Prepared(j) for j in jobs]
+preps = S._prepare_all(jobs)
 t1 = time.perf_counter()
 print(f"host prep (seeding, {sum(len(p.ids) for p in preps)} services): {(t1 - t0) * 1e3:.1f} ms")
 orig = S._report
