@@ -371,6 +371,7 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
     arrived, served, batches, viol = (o[k].cpu().numpy() for k in ("arrived", "served", "batches", "viol"))
     busy = o_busy.cpu().numpy()
     lat_off = np.concatenate([[0], np.cumsum(batches)])
+    pct = _percentiles_batch(srt_all, lat_off[:-1], batches)
     reports, k = [], 0
     for pi, pr in enumerate(preps):
         m = len(pr.ids)
@@ -378,8 +379,7 @@ def run_simulations(jobs: Sequence[SimJob], stream=None) -> list:
         for si in range(m):
             for r in range(seg_off[k + si], seg_off[k + si + 1]):
                 busy_by_seg[seg_rows[r][1]] = busy[r]
-        lats = [(lat_all[lat_off[k + si]:lat_off[k + si + 1]], srt_all[lat_off[k + si]:lat_off[k + si + 1]])
-                for si in range(m)]
+        lats = [(lat_all[lat_off[k + si]:lat_off[k + si + 1]], pct[k + si]) for si in range(m)]
         reports.append(_report(pr, lats, arrived[k:k + m], served[k:k + m], batches[k:k + m], viol[k:k + m],
                                busy_by_seg))
         k += m
@@ -406,17 +406,49 @@ def _percentile_sorted(srt: np.ndarray, q) -> float:
     return float(a + diff * gamma)
 
 
-def _latency_stats(lat: np.ndarray, srt: np.ndarray | None = None) -> dict:
+def _percentiles_batch(srt_all: np.ndarray, off: np.ndarray, cnt: np.ndarray) -> list:
+    """_percentile_sorted for many sorted samples at once (sample i =
+    srt_all[off[i]:off[i] + cnt[i]]), elementwise with the same float64
+    operations, so every value is bit-identical: per sample (p50, p95, p99, max),
+    or None for an empty sample."""
+    cnt = np.asarray(cnt, dtype=np.int64)
+    off = np.asarray(off, dtype=np.int64)
+    ok = cnt > 0
+    res = np.zeros((cnt.shape[0], 4))
+    if ok.any():
+        o, n = off[ok], cnt[ok]
+        last = o + n - 1
+        cols = []
+        for q in _Q:
+            v = (n - 1).astype(np.float64) * q
+            prev = np.floor(v)
+            at_end = v >= (n - 1)
+            pi = np.minimum(prev.astype(np.int64), n - 2).clip(min=0)
+            a = srt_all[o + pi]
+            b = srt_all[np.minimum(o + pi + 1, last)]
+            gamma = v - prev
+            diff = b - a
+            val = np.where(gamma >= 0.5, b - diff * (1 - gamma), a + diff * gamma)
+            cols.append(np.where(at_end, srt_all[last], val))
+        cols.append(srt_all[last])
+        res[ok] = np.stack(cols, axis=1)
+    return [tuple(float(x) for x in r) if k else None for r, k in zip(res, ok)]
+
+
+def _latency_stats(lat: np.ndarray, srt=None) -> dict:
     """The reference's latency summary (evaluation.py:436-456): numpy mean
     (pairwise sum, in batch order), linear-interpolated percentiles, max;
-    rounded to 6 dp.  `srt` = the sample sorted (else sorted here)."""
-    if srt is None:
-        srt = np.sort(lat)
-    return {"mean": round(float(lat.mean()), 6),
-            "p50": round(_percentile_sorted(srt, _Q[0]), 6),
-            "p95": round(_percentile_sorted(srt, _Q[1]), 6),
-            "p99": round(_percentile_sorted(srt, _Q[2]), 6),
-            "max": round(float(srt[-1]), 6)}
+    rounded to 6 dp.  `srt` = the sample sorted (else sorted here), or the
+    precomputed (p50, p95, p99, max)."""
+    if isinstance(srt, tuple):
+        p50, p95, p99, mx = srt
+    else:
+        if srt is None:
+            srt = np.sort(lat)
+        p50, p95, p99 = (_percentile_sorted(srt, q) for q in _Q)
+        mx = float(srt[-1])
+    return {"mean": round(float(lat.mean()), 6), "p50": round(p50, 6), "p95": round(p95, 6),
+            "p99": round(p99, 6), "max": round(mx, 6)}
 
 
 def _report(pr: _Prepared, lats, arrived, served, batches, viol, busy_by_seg) -> SimReport:

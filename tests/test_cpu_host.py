@@ -52,6 +52,23 @@ def test_sim_seed_states_match_numpy():
         assert got == exp, seed
 
 
+def test_batched_percentiles_match_numpy():
+    """Simulator statistics: the batched linear percentiles equal
+    np.percentile bit for bit (sizes 0-1000, ties, exact index hits)."""
+    from paper_2409_14447_b200 import simulation as S
+    rng = np.random.default_rng(3)
+    sizes = [1, 2, 3, 4, 5, 7, 10, 19, 20, 21, 100, 101, 1000, 0, 13] + list(rng.integers(1, 300, 40))
+    samples = [np.sort(rng.exponential(5, size=int(n))) for n in sizes] + [np.ones(3), np.array([2.0, 2.0])]
+    cnt = np.array([len(x) for x in samples])
+    off = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    got = S._percentiles_batch(np.concatenate(samples), off, cnt)
+    for x, g in zip(samples, got):
+        if len(x) == 0:
+            assert g is None
+            continue
+        assert g == tuple(float(np.percentile(x, 100 * q)) for q in S._Q) + (float(x.max()),)
+
+
 def test_record_layouts():
     assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128
 
