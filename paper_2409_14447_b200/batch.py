@@ -78,7 +78,7 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     if dt.index_struct is None:
         cfg_format = CFG_FULL
     if out is None:
-        out = BatchResult(N.empty_records(n_svc, COMPACT_DTYPE if cfg_format == CFG_COMPACT else CONFIG_DTYPE),
+        out = BatchResult(N.empty_records(n_svc, _CFG_DT[cfg_format]),
                           N.empty_records(n_scen, PLAN_DTYPE), n_scen, n_svc, cfg_format)
     s = N.stream_handle(stream)
     L = N.lib()

@@ -267,6 +267,24 @@ def test_c4_sample_vs_oracle(fx):
         assert plan.tobytes() == oplan.tobytes()
 
 
+def test_c4_full_vs_oracle(fx):
+    """All 10^6 C4 scenarios (seed 1) in one K2 launch, byte for
+    byte against the oracle (every host thread)."""
+    sb = W.scenario_batch(fx, 1_000_000, seed=1)
+    pt = pack_tables(fx.tables)
+    dt = N.device_tables_for(fx.tables)
+    n, M = sb.rate.shape
+    off = np.arange(n + 1, dtype=np.int32) * M
+    tab = np.tile(np.arange(M, dtype=np.int32), n)
+    rate, bound = sb.rate.ravel(), sb.bound.ravel()
+    res = B.plan_batch(dt, off, tab, rate, bound, cfg_format=CFG_TINY)
+    cfg, plan = res.host()
+    ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
+    from paper_2409_14447_b200.records import tiny_config
+    assert plan.tobytes() == oplan.tobytes()
+    assert cfg.tobytes() == tiny_config(ocfg).tobytes()
+
+
 def test_c3_sweep_vs_goldens_and_oracle():
     g = golden("c3_sample.json")
     dt_h = W.dense_tables(2000, seed=3)
