@@ -6,14 +6,15 @@
 // service's events only touch its own queue, lanes and segments, and the
 // global (time, seq) heap order restricted to one service is the order of
 // that service's own pushes.  So every service is an independent sequential
-// simulation: one thread each, in two stages.
+// simulation: one warp each, in two stages.
 //
 // * Arrivals, from the service's own numpy generator state (PCG64 XSL-RR
 //   128/64, seeded on the host by SeedSequence(seed).spawn(n)[i] exactly as
 //   the reference does): Generator.exponential(1/rate, size=chunk) gaps by
 //   numpy's ziggurat (tables in numpy_ziggurat.h), per-chunk cumsum plus the
 //   previous chunk's last time, stop at the horizon; or the deterministic
-//   grid i * step.  Generated lazily, in the order the loop ingests them.
+//   grid i * step.  Draws are generated 32 at a time by the warp's lanes
+//   (PCG64 jump-ahead), gaps consumed lazily in the order the loop ingests.
 // * The event loop: the FIFO queue is the index range [qh, ptr) of the
 //   ingested arrivals; ingest() moves arrivals <= now into the buffer
 //   (searchsorted(side="right") on a monotone clock); pending events are one
@@ -33,10 +34,11 @@ namespace parva {
 
 constexpr int kSimLanes = 64;     // pending completions per service (its total lanes)
 constexpr int kSimSegs = 32;      // segments per service
-// One service per WARP (lane 0): every service's event loop takes its own
+// One service per WARP: every service's event loop takes its own
 // data-dependent path, so services sharing a warp would serialise (a warp
 // of 32 services ran ~20x slower than its arithmetic); a warp each also
-// spreads the few thousand services over every SM.
+// spreads the few thousand services over every SM, and its lanes generate
+// the service's random draws 32 at a time.
 constexpr int kSimWarps = 4;      // services (warps) per CTA
 constexpr int kRing = 32;         // last ingested arrivals per service, in shared memory
 
@@ -140,85 +142,236 @@ __device__ __forceinline__ double standard_exponential(Pcg64& g) {
   }
 }
 
-// A service's arrival stream, generated lazily in order (the event loop
-// consumes arrivals strictly in order, so the next one is always a register,
-// never a dependent load).  Poisson: numpy exponential gaps, per-chunk cumsum
-// plus the previous chunk's last time (evaluation.py:218-226); deterministic:
-// i * step (:213-217).  Times in seconds; next() returns ms, false at the
-// horizon (times are monotone, so the rest would be filtered out).
-struct ArrivalGen {
-  Pcg64 g;
-  double scale, horizon_s, cs, total;
-  int64_t chunk, i;
-  int kind;
-  bool done;
+// ------------------------------------------------ warp-cooperative arrivals
+// A service's arrivals are a strictly sequential stream (PCG64 draws -> the
+// ziggurat -> per-chunk cumsum), but the draws themselves are an affine
+// recurrence mod 2^128, so a warp takes 32 at once: lane L jumps the base
+// state by L + 1 steps (s' = A_L s + C_L, (A_L, C_L) = the (L+1)-fold step,
+// from a warp scan at service start), maps its draw through the ziggurat's
+// fast path, and the rare slow draws (about 1 in 80: the tail or a wedge
+// test, each consuming the next draw as its uniform) are resolved in stream
+// order by walking the ballot of slow lanes.  The gaps land in shared memory
+// in draw order; the event loop -- run by all 32 lanes in lockstep on
+// identical values -- consumes them one by one.
+struct U128 {
+  uint64_t hi, lo;
+};
+__device__ __forceinline__ U128 mul128(U128 a, U128 b) {
+  return U128{__umul64hi(a.lo, b.lo) + a.hi * b.lo + a.lo * b.hi, a.lo * b.lo};
+}
+__device__ __forceinline__ U128 add128(U128 a, U128 b) {
+  const uint64_t lo = a.lo + b.lo;
+  return U128{a.hi + b.hi + (lo < a.lo ? 1ull : 0ull), lo};
+}
+__device__ __forceinline__ U128 shfl128(U128 v, int src) {
+  return U128{__shfl_sync(0xffffffffu, v.hi, src), __shfl_sync(0xffffffffu, v.lo, src)};
+}
+__device__ __forceinline__ U128 shfl_up128(U128 v, int o) {
+  return U128{__shfl_up_sync(0xffffffffu, v.hi, o), __shfl_up_sync(0xffffffffu, v.lo, o)};
+}
+__device__ __forceinline__ uint64_t xsl_rr(U128 st) {
+  const uint64_t x = st.hi ^ st.lo;
+  const unsigned rot = (unsigned)(st.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+__device__ __forceinline__ double draw_double(uint64_t o) {
+  return __dmul_rn((double)(o >> 11), 1.0 / 9007199254740992.0);
+}
+// the slow branch of random_standard_exponential for draw (idx, x) and the
+// next draw's uniform u: the tail value, or x if the wedge test accepts
+__device__ __forceinline__ bool zig_slow(int idx, double x, double u, double& e) {
+  if (idx == 0) { e = __dsub_rn(kZigExpR, glibc_log1p_neg(-u)); return true; }
+  const double fe1 = __ldg(&kZigFe[idx - 1]), fe0 = __ldg(&kZigFe[idx]);
+  if (__dadd_rn(__dmul_rn(__dsub_rn(fe1, fe0), u), fe0) < exp(-x)) { e = x; return true; }
+  return false;
+}
 
-  __device__ __forceinline__ bool next(double& t_ms) {
-    if (done) return false;
-    if (kind == 1) {
-      if (i == chunk) {                  // the reference draws another chunk while total < horizon
-        if (!(total < horizon_s)) { done = true; return false; }
-        i = 0;
+// per-warp (per-service) shared state: generated gaps, the queue-head ring,
+// pending completions and the segments (one copy; every lane reads and
+// writes the same values)
+struct alignas(16) SimWarp {
+  double smp[64];                 // scale * exponential draws, in stream order
+  double tm[32];                  // next arrival times (ms), in order
+  double ring[kRing];             // last kRing ingested arrivals (ms)
+  double ev_t[kSimLanes];         // pending completions, one FIFO per segment:
+  double busy[kSimSegs];
+  uint32_t ev_q[kSimLanes];       // segment g owns slots [seg_lo[g], seg_lo[g] + lanes_g)
+  int free_seg[kSimSegs];
+  int seg_lo[kSimSegs];
+  int seg_head[kSimSegs];
+  int seg_n[kSimSegs];
+};
+
+// Arrival stream of one service (evaluation.py:207-226): Poisson = numpy
+// exponential gaps, per-chunk cumsum plus the previous chunk's last time;
+// deterministic = i * step.  Times in seconds; next() returns ms, false at the
+// horizon (times are monotone, so the rest would be filtered out).
+struct WarpArrivals {
+  U128 st;                        // base PCG64 state (uniform)
+  U128 ja, jc;                    // this lane's jump: L + 1 steps
+  double scale, horizon_s, cs, total, pend_x;
+  int64_t chunk, i;
+  int kind, head, cnt, pend_idx, lane;
+  int th, tn;                     // W.tm[th, tn): arrival times not yet ingested
+  bool done, pend;
+
+  __device__ __forceinline__ void init(const uint64_t* pcg, int kind_, double scale_, double hs, int64_t count,
+                                       int lane_) {
+    st = U128{pcg[0], pcg[1]};
+    const U128 inc{pcg[2], pcg[3]};
+    lane = lane_;
+    // (A, C) of one step is (M, inc); inclusive warp scan of the composition
+    // (A, C) o (A', C') = (A A', A C' + C): lane L ends with L + 1 steps
+    ja = U128{0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull};
+    jc = inc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const U128 pa = shfl_up128(ja, o), pc = shfl_up128(jc, o);
+      if (lane >= o) {
+        jc = add128(mul128(ja, pc), jc);
+        ja = mul128(ja, pa);
       }
-      const double gap = __dmul_rn(scale, standard_exponential(g));
-      cs = i == 0 ? gap : __dadd_rn(cs, gap);
-      const double t = __dadd_rn(cs, total);
-      if (i == chunk - 1) total = t;
-      i++;
-      if (t >= horizon_s) { done = true; return false; }
-      t_ms = __dmul_rn(t, 1000.0);
-      return true;
     }
-    if (kind == 2) {
-      if (i < chunk) {
-        i++;
-        const double t = __dmul_rn((double)i, scale);
-        if (t < horizon_s) { t_ms = __dmul_rn(t, 1000.0); return true; }
+    kind = kind_;
+    scale = scale_;
+    horizon_s = hs;
+    cs = 0.0;
+    total = 0.0;
+    chunk = count;
+    i = kind == 1 ? chunk : 0;
+    done = kind != 1 && kind != 2;
+    head = cnt = 0;
+    th = tn = 0;
+    pend = false;
+    pend_idx = 0;
+    pend_x = 0.0;
+  }
+
+  // 32 more draws -> the gaps they complete, in order (warp-collective)
+  __device__ __noinline__ void refill(SimWarp& W) {
+    cnt = 0;
+    head = 0;
+    do {
+      const U128 s = add128(mul128(ja, st), jc);
+      const uint64_t out = xsl_rr(s);
+      st = shfl128(s, 31);
+      uint64_t ri = out >> 3;
+      const int idx = (int)(ri & 0xFF);
+      ri >>= 8;
+      const double x = __dmul_rn((double)ri, __ldg(&kZigWe[idx]));
+      const unsigned slow = __ballot_sync(0xffffffffu, !(ri < __ldg(&kZigKe[idx])));
+      int pos = 0;
+      if (pend) {                 // the last batch ended on a slow draw: its uniform is draw 0
+        const double u = draw_double(__shfl_sync(0xffffffffu, out, 0));
+        double e;
+        if (zig_slow(pend_idx, pend_x, u, e)) W.smp[cnt++] = __dmul_rn(scale, e);
+        pend = false;
+        pos = 1;
+      }
+      while (pos < 32) {
+        const unsigned m = slow & (0xffffffffu << pos);
+        const int sl = m ? __ffs(m) - 1 : 32;
+        if (lane >= pos && lane < sl) W.smp[cnt + lane - pos] = __dmul_rn(scale, x);
+        cnt += sl - pos;
+        if (sl >= 31) {
+          if (sl == 31) {
+            pend = true;
+            pend_idx = __shfl_sync(0xffffffffu, idx, 31);
+            pend_x = __shfl_sync(0xffffffffu, x, 31);
+          }
+          break;
+        }
+        const double u = draw_double(__shfl_sync(0xffffffffu, out, sl + 1));
+        const int si = __shfl_sync(0xffffffffu, idx, sl);
+        const double sx = __shfl_sync(0xffffffffu, x, sl);
+        double e;
+        if (zig_slow(si, sx, u, e)) W.smp[cnt++] = __dmul_rn(scale, e);
+        pos = sl + 2;
+      }
+    } while (cnt == 0);
+    __syncwarp();
+  }
+
+  // the next up to 32 arrival times (ms) into W.tm[0, tn): the reference's
+  // per-chunk cumsum plus the previous chunk's last time (a sequential
+  // chain), or the grid i * step; false once the horizon is reached
+  __device__ __noinline__ bool fill(SimWarp& W) {
+    th = tn = 0;
+    while (!done && tn == 0) {
+      if (kind == 1) {
+        while (tn < 32) {
+          if (i == chunk) {              // the reference draws another chunk while total < horizon
+            if (!(total < horizon_s)) { done = true; break; }
+            i = 0;
+          }
+          if (head == cnt) refill(W);
+          const double gap = W.smp[head++];
+          cs = i == 0 ? gap : __dadd_rn(cs, gap);
+          const double t = __dadd_rn(cs, total);
+          if (i == chunk - 1) total = t;
+          i++;
+          if (t >= horizon_s) { done = true; break; }
+          W.tm[tn++] = __dmul_rn(t, 1000.0);
+        }
+      } else if (kind == 2) {
+        while (tn < 32) {
+          if (i >= chunk) { done = true; break; }
+          i++;
+          const double t = __dmul_rn((double)i, scale);
+          if (!(t < horizon_s)) { done = true; break; }
+          W.tm[tn++] = __dmul_rn(t, 1000.0);
+        }
+      } else {
+        done = true;
       }
     }
-    done = true;
-    return false;
+    __syncwarp();
+    return tn > 0;
+  }
+
+  // next arrival not yet ingested: its time, or false if there is none
+  __device__ __forceinline__ bool peek(SimWarp& W, double& t_ms) {
+    if (th == tn && !fill(W)) return false;
+    t_ms = W.tm[th];
+    return true;
   }
 };
 
+// One service per warp.  Every lane runs the event loop on identical values
+// (so the generator's collectives are always converged); lane 0 alone
+// writes global memory.
 __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_problem P, parva_sim_result R) {
-  // the queue head (the oldest waiting arrival) is nearly always one of the
-  // last kRing ingested: read it from shared memory, not back from L2
-  __shared__ double ring[kRing][kSimWarps];
-  const int tx = threadIdx.x >> 5;
-  if (threadIdx.x & 31) return;
-  for (int s = blockIdx.x * kSimWarps + tx; s < P.n_services; s += gridDim.x * kSimWarps) {
+  __shared__ SimWarp sw[kSimWarps];
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  SimWarp& W = sw[wi];
+  for (int s = blockIdx.x * kSimWarps + wi; s < P.n_services; s += gridDim.x * kSimWarps) {
     const int64_t b0 = P.d_buf_off[s];
     const int64_t cap = P.d_buf_off[s + 1] - b0;
     double* buf = R.d_buf + b0;            // ingested arrivals (ms), later the batch latencies
     const int kind = P.d_kind[s];
-    ArrivalGen gen;
-    gen.g = Pcg64{P.d_pcg[4 * s], P.d_pcg[4 * s + 1], P.d_pcg[4 * s + 2], P.d_pcg[4 * s + 3]};
-    gen.scale = P.d_scale[s];
-    gen.horizon_s = P.d_horizon_s[s];
-    gen.cs = 0.0;
-    gen.total = 0.0;
-    gen.chunk = P.d_count[s];
-    gen.i = kind == 1 ? gen.chunk : 0;
-    gen.kind = kind;
-    gen.done = kind != 1 && kind != 2;
+    WarpArrivals gen;
+    gen.init(P.d_pcg + 4 * s, kind, P.d_scale[s], P.d_horizon_s[s], P.d_count[s], lane);
     const int g0 = P.d_seg_off[s];
     const int ns = P.d_seg_off[s + 1] - g0;
     int lanes_total = 0;
     for (int g = 0; g < ns; g++) lanes_total += P.d_seg_lanes[g0 + g];
     if (ns > kSimSegs || lanes_total > kSimLanes) {
-      R.d_status[s] = PARVA_CAPACITY;
+      if (lane == 0) R.d_status[s] = PARVA_CAPACITY;
       continue;
     }
     const double H = P.d_horizon_ms[s];
     const double slo = P.d_slo[s];
-    int free_seg[kSimSegs];
-    double busy[kSimSegs];
-    for (int g = 0; g < ns; g++) { free_seg[g] = P.d_seg_lanes[g0 + g]; busy[g] = 0.0; }
-    double ev_t[kSimLanes];
-    uint32_t ev_q[kSimLanes];
-    uint8_t ev_g[kSimLanes];
-    int n_ev = 0;
+    for (int g = 0, lo = 0; g < ns; g++) {
+      W.free_seg[g] = P.d_seg_lanes[g0 + g];
+      W.busy[g] = 0.0;
+      W.seg_lo[g] = lo;
+      W.seg_head[g] = 0;
+      W.seg_n[g] = 0;
+      lo += P.d_seg_lanes[g0 + g];
+    }
+    __syncwarp();
+    // reduction rounds that cover the segments (lane g = segment g)
+    const int seg_rounds = ns <= 1 ? 0 : 32 - __clz(ns - 1);
     int free_lanes = lanes_total;
     int64_t ptr = 0, qh = 0, batches = 0, served = 0, violations = 0;
     uint32_t seq = 0;
@@ -226,7 +379,7 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
     double wake_t = 0.0;
     uint32_t wake_q = 0;
     double nt = 0.0;                       // next arrival not yet ingested (arr[ptr])
-    bool have = gen.next(nt);
+    bool have = gen.peek(W, nt);
 
     auto schedule_wakeup = [&]() {        // evaluation.py:362-366
       if (wake || !have) return;
@@ -235,49 +388,86 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
       wake_q = seq++;
     };
     auto ingest = [&](double now) {       // evaluation.py:353-360
+      // arrivals <= now, a batch of up to 32 per step: times are monotone, so
+      // the lanes whose time is <= now are a prefix
       while (have && nt <= now) {
-        if (ptr == cap) { overflow = true; have = false; break; }
-        buf[ptr] = nt;
-        ring[ptr & (kRing - 1)][tx] = nt;
-        ptr++;
-        have = gen.next(nt);
+        const int rem = gen.tn - gen.th;
+        const unsigned le = __ballot_sync(0xffffffffu, lane < rem && W.tm[gen.th + lane] <= now);
+        int take = __popc(le);
+        if (take > cap - ptr) { take = (int)(cap - ptr); overflow = true; }
+        if (lane < take) {
+          const double v = W.tm[gen.th + lane];
+          buf[ptr + lane] = v;
+          W.ring[(ptr + lane) & (kRing - 1)] = v;
+        }
+        __syncwarp();
+        ptr += take;
+        gen.th += take;
+        if (overflow) { have = false; break; }
+        have = gen.peek(W, nt);
       }
     };
     auto dispatch = [&](double now) {     // evaluation.py:368-388
       if (now >= H) return;
       while (qh < ptr && free_lanes > 0) {
-        int g = 0;
-        while (free_seg[g] == 0) g++;
+        const int g = __ffs(__ballot_sync(0xffffffffu, lane < ns && W.free_seg[lane] > 0)) - 1;
         const double ms = P.d_seg_ms[g0 + g];
         const int64_t qn = ptr - qh;
         const int64_t b = P.d_seg_batch[g0 + g];
         const int64_t n = b < qn ? b : qn;
-        const double first = ptr - qh <= kRing ? ring[qh & (kRing - 1)][tx] : buf[qh];
+        const double first = ptr - qh <= kRing ? W.ring[qh & (kRing - 1)] : buf[qh];
         qh += n;
         const double latency = __dadd_rn(__dsub_rn(now, first), ms);
-        buf[batches++] = latency;          // slot < qh: that arrival has left the queue
+        __syncwarp();                      // every lane has read buf[qh] before lane 0 overwrites a slot
+        if (lane == 0) buf[batches] = latency;   // slot < qh: that arrival has left the queue
+        batches++;
         served += n;
         if (latency > slo) violations++;
-        free_seg[g]--;
+        W.free_seg[g]--;
         free_lanes--;
         const double rem = __dsub_rn(H, now);
         const double m = ms < rem ? ms : rem;
-        busy[g] = __dadd_rn(busy[g], m > 0.0 ? m : 0.0);
-        ev_t[n_ev] = __dadd_rn(now, ms);
-        ev_q[n_ev] = seq++;
-        ev_g[n_ev] = (uint8_t)g;
-        n_ev++;
+        W.busy[g] = __dadd_rn(W.busy[g], m > 0.0 ? m : 0.0);
+        // a segment's completions are pushed in (time, seq) order (now is
+        // monotone, ms fixed), so each segment's pending events are a FIFO
+        const int lanes_g = P.d_seg_lanes[g0 + g];
+        int slot = W.seg_head[g] + W.seg_n[g];
+        if (slot >= lanes_g) slot -= lanes_g;
+        W.ev_t[W.seg_lo[g] + slot] = __dadd_rn(now, ms);
+        W.ev_q[W.seg_lo[g] + slot] = seq++;
+        W.seg_n[g]++;
       }
     };
 
     if (ns > 0) schedule_wakeup();
     for (;;) {                             // evaluation.py:395-416
-      // pop the (time, seq)-smallest pending event
+      // pop the (time, seq)-smallest pending event: the smallest FIFO head
+      // over the segments (lane g = segment g, argmin over the lanes that
+      // cover the segments; seqs are unique, so it is exact)
       int best = -1;
       double bt = 0.0;
       uint32_t bq = 0;
-      for (int e = 0; e < n_ev; e++)
-        if (best < 0 || ev_t[e] < bt || (ev_t[e] == bt && ev_q[e] < bq)) { best = e; bt = ev_t[e]; bq = ev_q[e]; }
+      if (free_lanes < lanes_total) {
+        int ei = -1;
+        double et = 0.0;
+        uint32_t eq = 0xFFFFFFFFu;
+        if (lane < ns && W.seg_n[lane] > 0) {
+          const int k = W.seg_lo[lane] + W.seg_head[lane];
+          et = W.ev_t[k];
+          eq = W.ev_q[k];
+          ei = lane;
+        }
+        for (int r = 0; r < seg_rounds; r++) {
+          const int o = 1 << r;
+          const double t2 = __shfl_xor_sync(0xffffffffu, et, o);
+          const uint32_t q2 = __shfl_xor_sync(0xffffffffu, eq, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, ei, o);
+          if (i2 >= 0 && (ei < 0 || t2 < et || (t2 == et && q2 < eq))) { et = t2; eq = q2; ei = i2; }
+        }
+        best = __shfl_sync(0xffffffffu, ei, 0);
+        bt = __shfl_sync(0xffffffffu, et, 0);
+        bq = __shfl_sync(0xffffffffu, eq, 0);
+      }
       const bool take_wake = wake && (best < 0 || wake_t < bt || (wake_t == bt && wake_q < bq));
       if (best < 0 && !take_wake) break;
       if (take_wake) {
@@ -288,12 +478,11 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
         if (free_lanes > 0) schedule_wakeup();
       } else {
         const double now = bt;
-        const int g = ev_g[best];
-        ev_t[best] = ev_t[n_ev - 1];
-        ev_q[best] = ev_q[n_ev - 1];
-        ev_g[best] = ev_g[n_ev - 1];
-        n_ev--;
-        free_seg[g]++;
+        const int g = best;
+        const int lanes_g = P.d_seg_lanes[g0 + g];
+        W.seg_head[g] = W.seg_head[g] + 1 == lanes_g ? 0 : W.seg_head[g] + 1;
+        W.seg_n[g]--;
+        W.free_seg[g]++;
         free_lanes++;
         if (now < H) {
           ingest(now);
@@ -303,17 +492,20 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
       }
     }
     // arrivals never ingested still count (ServiceSimStats.arrived)
-    int64_t arrived = ptr + (have ? 1 : 0);
+    int64_t arrived = ptr;
     if (have) {
-      double t;
-      while (gen.next(t)) arrived++;
+      arrived += gen.tn - gen.th;
+      while (gen.fill(W)) arrived += gen.tn;
     }
-    R.d_arrived[s] = arrived;
-    R.d_served[s] = served;
-    R.d_batches[s] = batches;
-    R.d_violations[s] = violations;
-    for (int g = 0; g < ns; g++) R.d_busy_ms[g0 + g] = busy[g];
-    R.d_status[s] = overflow ? PARVA_CAPACITY : PARVA_OK;
+    if (lane == 0) {
+      R.d_arrived[s] = arrived;
+      R.d_served[s] = served;
+      R.d_batches[s] = batches;
+      R.d_violations[s] = violations;
+      for (int g = 0; g < ns; g++) R.d_busy_ms[g0 + g] = W.busy[g];
+      R.d_status[s] = overflow ? PARVA_CAPACITY : PARVA_OK;
+    }
+    __syncwarp();
   }
 }
 
