@@ -84,23 +84,55 @@ def make_service(service_id: str, model_id: str, request_rate: float, slo_latenc
 
 
 # ------------------------------------------------------------ decoding
+def _triplet_cache(pt):
+    """(point index -> Triplet cache, segment starts as Python ints) of a
+    PackedTables, created on first use."""
+    d = pt.__dict__
+    cache = d.get("_triplet_cache")
+    if cache is None:
+        cache = d["_triplet_cache"] = {}
+        d["_seg_start_py"] = [int(x) for x in pt.seg_start]
+    return cache, d["_seg_start_py"]
+
+
 def triplet_at(pt, t: int, c: int, j: int) -> Triplet:
-    i = pt.point(t, c, j)
-    return Triplet(INSTANCE_SIZES[c], int(pt.batch[i]), int(pt.procs[i]), float(pt.tp[i]), float(pt.lat[i]))
+    """The Triplet of point j of table t, size class c (one shared, immutable
+    instance per point, built on first use)."""
+    cache, seg = _triplet_cache(pt)
+    i = seg[t * 5 + c] + j
+    tr = cache.get(i)
+    if tr is None:
+        tr = cache[i] = Triplet(INSTANCE_SIZES[c], int(pt.batch[i]), int(pt.procs[i]), float(pt.tp[i]),
+                                float(pt.lat[i]))
+    return tr
+
+
+_SERVICE_INIT = Service.__init__
 
 
 def service_from_record(svc: Service, pt, t: int, rec) -> Service:
-    """Configured Service from a 32-byte config record (status must be OK)."""
-    best = {c: triplet_at(pt, t, c, int(rec["best"][c])) for c in range(5) if rec["best"][c] >= 0}
-    o, l = int(rec["opt_sc"]), int(rec["last_sc"])
-    return replace(svc, best_triplets=tuple(best[c] for c in sorted(best)),
-                   optimal_segment=best[o] if o >= 0 else None,
-                   optimal_segment_count=int(rec["count"]),
-                   last_segment=best[l] if l >= 0 else None)
+    """Configured Service from a config record (status must be OK): a numpy
+    record, or the same record as a tuple (records.tolist())."""
+    if isinstance(rec, tuple):
+        bests, o, l, count = rec[0], rec[1], rec[2], rec[6]
+    else:
+        bests, o, l, count = rec["best"].tolist(), int(rec["opt_sc"]), int(rec["last_sc"]), int(rec["count"])
+    best = [None] * 5
+    cache, seg = _triplet_cache(pt)
+    for c in range(5):
+        j = bests[c]
+        if j >= 0:
+            tr = cache.get(seg[t * 5 + c] + j)
+            best[c] = tr if tr is not None else triplet_at(pt, t, c, j)
+    out = object.__new__(Service)
+    _SERVICE_INIT(out, svc.id, svc.model_id, svc.request_rate, svc.slo_latency, svc.internal_latency,
+                  tuple(b for b in best if b is not None), best[o] if o >= 0 else None, int(count),
+                  best[l] if l >= 0 else None)
+    return out
 
 
 def raise_for_record(svc: Service, rec) -> None:
-    st = int(rec["status"])
+    st = rec[3] if isinstance(rec, tuple) else int(rec["status"])
     if st == OK:
         return
     if st == INFEASIBLE_SLO:

@@ -80,13 +80,13 @@ def _decode_record(services: list[Service], rec) -> DeploymentMap:
     """DeploymentMap from a 128-byte plan record (include/parva_b200.h)."""
     places, diag_codes, ledger = plan_payload(rec)
     gpus: list[GpuState] = []
-    by_class = [{INSTANCE_SIZES.index(t.instance_size): t for t in s.best_triplets} for s in services]
+    by_size = [{t.instance_size: t for t in s.best_triplets} for s in services]
     for v in places:
         g, cat, slot = unpack_place(v)
         s, c = divmod(cat, 5)
         if not gpus or gpus[-1].id != g:
             gpus.append(GpuState(id=g))
-        t = by_class[s][c]
+        t = by_size[s][INSTANCE_SIZES[c]]
         gpus[-1].placements.append(Placement(services[s].id, t.instance_size, t.batch_size,
                                              t.process_count, t.throughput, slot))
     freed = {services[s].id: v for s, v in ledger}
@@ -142,13 +142,14 @@ def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, Pr
     torch.cuda.synchronize()
     elapsed_ms = (time.perf_counter() - t0) * 1000.0
     out = []
+    cfg_t = cfg.tolist()                   # records as tuples: plain attribute-free access below
     for k, ss in enumerate(service_sets):
         a = int(off[k])
         try:
             configured = []
             for i, s in enumerate(ss):
-                rec = cfg[a + i]
-                if int(rec["status"]) == BAD_INPUT:
+                rec = cfg_t[a + i]
+                if rec[3] == BAD_INPUT:
                     raise KeyError(s.model_id)
                 raise_for_record(s, rec)
                 configured.append(service_from_record(s, pt, tab[a + i], rec))

@@ -69,6 +69,24 @@ def test_batched_percentiles_match_numpy():
         assert g == tuple(float(np.percentile(x, 100 * q)) for q in S._Q) + (float(x.max()),)
 
 
+def test_service_from_record_with_empty_size_classes():
+    """Record decoding (host): a table with only size-7 points (size classes
+    0-3 empty, so their segments start where size 7's does) decodes to
+    size-7 triplets, from a numpy record and from its tuple form."""
+    from paper_2409_14447_b200.configurator import service_from_record
+    pts = tuple(P.ProfilePoint("m", 7, b, p, 100.0 * b + p, 10.0 + b) for b in (1, 2, 4) for p in (1, 2))
+    pt = pack_tables([P.ProfileTable("m", pts)], prepared=True)
+    rec = np.zeros(1, dtype=CONFIG_DTYPE)[0]
+    rec["best"] = [-1, -1, -1, -1, 0]
+    rec["opt_sc"], rec["last_sc"], rec["count"] = 4, -1, 2
+    svc = P.make_service("s", "m", 500.0, 100.0)
+    for r in (rec, rec.tolist()):
+        got = service_from_record(svc, pt, 0, r)
+        assert [t.instance_size for t in got.best_triplets] == [7]
+        assert got.optimal_segment.instance_size == 7 and got.optimal_segment_count == 2
+        assert got.last_segment is None
+
+
 def test_record_layouts():
     assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128
 
