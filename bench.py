@@ -194,6 +194,9 @@ def main():
     ap.add_argument("--scenarios", type=int, default=10_000,
                     help="scenarios per GPU per step (weak) or in total (strong)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: K2 stores its records into every rank's gathered block over peer memory "
+                         "(fused), or one NCCL all-gather per step")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C3 configurator-sweep measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 side measurements")
@@ -227,6 +230,7 @@ def main():
     from paper_2409_14447_b200 import workloads as W
     from paper_2409_14447_b200.records import PLAN_DTYPE
 
+    from paper_2409_14447_b200 import distributed as D
     from paper_2409_14447_b200.distributed import gather_packed, make_shard, packed_block
     from paper_2409_14447_b200.records import CFG_TINY, TINY_DTYPE
 
@@ -283,8 +287,29 @@ def main():
     n_calls = max(args.steps, args.warmup)
     step_args = [call_args(i % P, i % R) for i in range(n_calls)]
 
+    # N > 1, fused: the records go straight into every rank's gathered block
+    # from inside K2 (peer memory mapped by CUDA IPC); the all-gather of a
+    # step is complete when every rank's flag reached its epoch
+    peer = None
+    gather_mode = "none" if world == 1 else args.gather
+    if world > 1 and args.gather == "fused":
+        try:
+            peer = D.PeerGather(blk, n_slots=R)
+        except Exception as exc:  # noqa: BLE001 -- no peer access: the NCCL collective instead
+            print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
+            gather_mode = "nccl"
+    mirrors = {}
+
+    def mirror_for(i):
+        m = mirrors.pop(i, None)
+        return m if m is not None else peer.mirror(i % R, ps, overlap=True)
+
     def step(i):
         b = i % R
+        if peer is not None:
+            N.check(L.parva_plan_batch_fused(*step_args[i][:-1], C.byref(mirror_for(i)), sh),
+                    "parva_plan_batch_fused")
+            return
         if works[b] is not None:
             works[b].wait()              # step i-R's all-gather has read blocks[b] (a stream wait under NCCL)
             works[b] = None
@@ -293,6 +318,9 @@ def main():
             works[b] = dist.all_gather_into_tensor(gathered[b], blocks[b], async_op=True)
 
     def drain():
+        if peer is not None:
+            peer.wait()                  # every rank's records of the last step have landed here
+            return
         for b in range(R):
             if works[b] is not None:
                 works[b].wait()
@@ -305,6 +333,11 @@ def main():
     if world > 1:
         dist.barrier()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if peer is not None:
+        torch.cuda.synchronize()
+        peer.check()
+        dist.barrier()
+        mirrors = {i: peer.mirror(i % R, ps, overlap=True) for i in range(args.steps)}   # built outside the timing
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t_start.record(stream)
@@ -333,6 +366,9 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms, kern_ms = float(t[0]), float(t[1])
+    if peer is not None:
+        peer.check()
+        peer.close()
     # batch 0 once more into block 0, for the parity check and the e2e comparison
     res = results[0]
     B.plan_batch(dt, *batches[0], cfg_format=CFG_TINY, out=res)
@@ -422,9 +458,13 @@ def main():
                    "input_batches": P,
                    "launch": "parva_plan_batch_overlapped per step (programmatic dependent launches, 3 rotating "
                              "output blocks); kernel_ms_per_step from separate one-at-a-time launches",
-                   "parallelism": f"scenario-sharded x{world}" + (" + one all-gather per step of the packed plan + tiny config "
-                                                                  "records, overlapped with the next step's planning"
-                                                                  if world > 1 else ""),
+                   "parallelism": f"scenario-sharded x{world}" + (
+                       " + all-gather of the packed plan + tiny config records every step: "
+                       + ("fused into K2 (records stored into every rank's gathered block over peer memory, "
+                          "completion flags per rank)" if gather_mode == "fused" else
+                          "one NCCL all-gather, overlapped with the next steps' planning")
+                       if world > 1 else ""),
+                   "gather": gather_mode,
                    "optimize": True, "threshold": 4},
         "gpu_launches": args.steps,
         "kernel_ms_per_step": kern_ms / args.steps,

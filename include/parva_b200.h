@@ -227,6 +227,48 @@ int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* i
                                 void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
                                 void* stream);
 
+/* Fused all-gather for the sharded device path (one process per GPU):
+ * parva_plan_batch that also stores every plan / config record into this
+ * rank's slot of every rank's gathered block over peer memory (NVLink P2P
+ * stores from inside K2, so the transfer overlaps the planning), then, after
+ * a system-scope fence, stores `epoch` into this rank's flag word on every
+ * rank.  plan[m] / cfg[m]: where this rank's records go on rank m (device
+ * pointers valid in this process: parva_ipc_open of rank m's block plus the
+ * slot offset; m = this rank is the local block).  d_done: a zeroed u32 the
+ * launch uses as its CTA counter (one per launch in flight).  overlap: launch
+ * as a programmatic dependent launch (parva_plan_batch_overlapped).
+ * parva_gather_wait makes `stream` wait until every rank's flag word in
+ * d_flags (this rank's flag array) has reached `epoch` (status set to
+ * PARVA_LAUNCH_ERROR after timeout_ns instead of waiting forever).
+ * Replaces plan_services per scenario plus the NCCL all-gather of the
+ * per-scenario plans. */
+typedef struct {
+  int32_t n;
+  int32_t overlap;
+  void* plan[8];
+  void* cfg[8];
+  uint32_t* flag[8];
+  uint32_t* d_done;
+  uint32_t epoch;
+} parva_mirror;
+int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
+                           int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,
+                           const int32_t* d_svc_table, const double* d_svc_rate,
+                           const double* d_svc_bound, int32_t optimize, int32_t threshold,
+                           void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
+                           const parva_mirror* mirror, void* stream);
+int parva_gather_wait(const uint32_t* d_flags, int32_t n, uint32_t epoch, int64_t timeout_ns,
+                      int32_t* d_status, void* stream);
+/* CUDA IPC plumbing for the gathered blocks: an exportable zeroed device
+ * allocation, its handle (parva_ipc_handle_bytes() bytes), and the mapping
+ * of a peer's handle into this process (peer access enabled lazily). */
+int parva_ipc_alloc(size_t bytes, void** d_ptr);
+int parva_ipc_free(void* d_ptr);
+int parva_ipc_handle_bytes(void);
+int parva_ipc_handle(void* d_ptr, void* handle);
+int parva_ipc_open(const void* handle, void** d_ptr);
+int parva_ipc_close(void* d_ptr);
+
 /* parva_plan_batch for tables too large for the shared-memory index: the
  * config records in d_cfg were produced by parva_configure_sweep. */
 int parva_plan_batch_preconfigured(const parva_tables* tables, int32_t n_scenarios,

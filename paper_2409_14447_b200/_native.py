@@ -73,7 +73,9 @@ class SimResult(C.Structure):
 
 EXPORTS = (
     "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
-    "parva_plan_batch", "parva_plan_batch_overlapped", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
+    "parva_plan_batch", "parva_plan_batch_overlapped", "parva_plan_batch_fused", "parva_gather_wait",
+    "parva_ipc_alloc", "parva_ipc_free", "parva_ipc_handle_bytes", "parva_ipc_handle", "parva_ipc_open",
+    "parva_ipc_close", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
@@ -81,6 +83,12 @@ EXPORTS = (
     "parva_stream_pack", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
     "parva_simulate", "parva_sim_seed_states", "parva_sim_log1p", "parva_sim_exponential",
 )
+
+
+class Mirror(C.Structure):
+    """parva_mirror (include/parva_b200.h): the fused all-gather's destinations."""
+    _fields_ = [("n", C.c_int32), ("overlap", C.c_int32), ("plan", C.c_void_p * 8), ("cfg", C.c_void_p * 8),
+                ("flag", C.c_void_p * 8), ("d_done", C.c_void_p), ("epoch", C.c_uint32)]
 
 
 def lib_path():

@@ -60,13 +60,15 @@ class BatchResult:
 
 def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, optimize: bool = True,
                threshold: int = 4, cfg_format: int = CFG_FULL, stream=None,
-               out: BatchResult | None = None, overlap: bool = False) -> BatchResult:
+               out: BatchResult | None = None, overlap: bool = False, mirror=None) -> BatchResult:
     """Plan independent scenarios; scenario k owns services [scen_off[k], scen_off[k+1]).
 
     overlap=True launches the kernel as a programmatic dependent launch
     (parva_plan_batch_overlapped): it may start while the previous planning
     call on the stream is still running, so `out` must not be written or
-    read by a call still in flight."""
+    read by a call still in flight.  mirror (an N.Mirror, e.g. from
+    distributed.PeerGather.mirror) adds the fused all-gather
+    (parva_plan_batch_fused)."""
     torch = N.require_cuda()
     dev = lambda a, f: a if isinstance(a, torch.Tensor) else N.to_device(f(a))  # noqa: E731
     scen_off = dev(scen_off, _i32)
@@ -83,10 +85,13 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     s = N.stream_handle(stream)
     L = N.lib()
     if dt.index_struct is not None:
-        fn = L.parva_plan_batch_overlapped if overlap else L.parva_plan_batch
-        rc = fn(C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), C.c_int32(n_svc), N.ptr(scen_off),
+        args = (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n_scen), C.c_int32(n_svc), N.ptr(scen_off),
                 N.ptr(svc_table), N.ptr(svc_rate), N.ptr(svc_bound), C.c_int32(int(optimize)),
-                C.c_int32(int(threshold)), N.ptr(out.cfg), C.c_int32(out.cfg_format), N.ptr(out.plan), s)
+                C.c_int32(int(threshold)), N.ptr(out.cfg), C.c_int32(out.cfg_format), N.ptr(out.plan))
+        if mirror is not None:
+            rc = L.parva_plan_batch_fused(*args, C.byref(mirror), s)
+        else:
+            rc = (L.parva_plan_batch_overlapped if overlap else L.parva_plan_batch)(*args, s)
         N.check(rc, "parva_plan_batch")
     else:
         configure_sweep(dt, svc_table, svc_rate, svc_bound, out=out.cfg, stream=stream)

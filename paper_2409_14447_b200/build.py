@@ -15,7 +15,7 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_build"
 LIB = OUT_DIR / "libparva_b200.so"
 SOURCES = ["configure.cu", "plan_batch.cu", "plan_general.cu", "unit_ops.cu", "prepare.cu", "capi.cu",
-           "simulate.cu"]
+           "simulate.cu", "gather.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

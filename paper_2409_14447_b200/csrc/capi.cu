@@ -46,9 +46,19 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
                            int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
                            const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
                            int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream,
-                           int pdl = 0) {
+                           int pdl = 0, const parva_mirror* mirror = nullptr) {
   parva::PlanArgs A;
   A.pdl = pdl;
+  if (mirror) {
+    A.n_mirror = mirror->n;
+    for (int m = 0; m < mirror->n; m++) {
+      A.mirror_plan[m] = (uint8_t*)mirror->plan[m];
+      A.mirror_cfg[m] = (uint8_t*)mirror->cfg[m];
+      A.peer_flag[m] = mirror->flag[m];
+    }
+    A.done_ctas = mirror->d_done;
+    A.flag_epoch = mirror->epoch;
+  }
   A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
   A.idx_best = index ? index->d_best : nullptr;
@@ -101,6 +111,25 @@ int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* i
   if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
                          optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream, 1);
+}
+
+// parva_plan_batch with a fused all-gather: every record is also stored into
+// this rank's slot of each rank's gathered block (peer memory), and the last
+// CTA stores `epoch` into this rank's flag word on every rank.
+int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                           int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table,
+                           const double* d_svc_rate, const double* d_svc_bound, int32_t optimize, int32_t threshold,
+                           void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan, const parva_mirror* mirror,
+                           void* stream) {
+  if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan || !mirror) return PARVA_BAD_INPUT;
+  if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
+  if (mirror->n < 1 || mirror->n > parva::kMaxMirror || !mirror->d_done) return PARVA_BAD_INPUT;
+  for (int m = 0; m < mirror->n; m++)
+    if (!mirror->plan[m] || !mirror->cfg[m] || !mirror->flag[m]) return PARVA_BAD_INPUT;
+  if (n_scenarios == 0) return PARVA_BAD_INPUT;   // nothing would publish the epoch
+  return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
+                         optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream,
+                         mirror->overlap ? 1 : 0, mirror);
 }
 
 // Same as parva_plan_batch but the config records in d_cfg were produced by

@@ -8,6 +8,8 @@
 
 namespace parva {
 
+constexpr int kMaxMirror = 8;        // ranks of a fused all-gather (one NVLink domain)
+
 struct PlanArgs {
   const double* pts;             // prepared (tp, lat) pairs (global)
   const double* idx_lat;         // prefix-argmax index (global; copied to smem)
@@ -56,6 +58,17 @@ struct PlanArgs {
   // streamed call on the stream is still finishing its last scenarios
   uint32_t* done_word = nullptr;
   int pdl = 0;
+  // fused all-gather (device path): every plan / config record is also
+  // stored at mirror_plan[m] / mirror_cfg[m] (the same record index), i.e.
+  // into this rank's slot of every rank's gathered block over peer memory;
+  // the last CTA (done_ctas, self-resetting) then stores flag_epoch into
+  // peer_flag[m] (this rank's flag word on rank m) after a system fence
+  int n_mirror = 0;
+  uint8_t* mirror_plan[kMaxMirror] = {};
+  uint8_t* mirror_cfg[kMaxMirror] = {};
+  uint32_t* peer_flag[kMaxMirror] = {};
+  uint32_t* done_ctas = nullptr;
+  uint32_t flag_epoch = 0;
 };
 
 #ifndef PARVA_STREAM_SLICE

@@ -334,7 +334,14 @@ __device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base
 }
 
 // config record store, words assembled in registers (no local copy)
+__device__ __forceinline__ void store_config_to(const PlanArgs& A, void* cfg, int64_t i, const parva_config_record& r);
+
 __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
+  store_config_to(A, A.cfg, i, r);
+  for (int m = 0; m < A.n_mirror; m++) store_config_to(A, A.mirror_cfg[m], i, r);   // fused all-gather
+}
+
+__device__ __forceinline__ void store_config_to(const PlanArgs& A, void* cfg, int64_t i, const parva_config_record& r) {
 #ifdef PARVA_NO_OUT
   if (A.stream_src) return;   // development probe: PCIe reads without the record writes
 #endif
@@ -349,13 +356,13 @@ __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const
     const uint32_t sf = (uint32_t)(r.status | (r.count > 255 ? 0x80 : 0));
     const uint32_t cn = (uint32_t)(r.count > 255 ? 255 : r.count);
     hi = (uint32_t)(r.best[4] < 0 ? 255 : (uint8_t)r.best[4]) | ol << 8 | sf << 16 | cn << 24;
-    reinterpret_cast<uint2*>(A.cfg)[i] = make_uint2(lo, hi);
+    reinterpret_cast<uint2*>(cfg)[i] = make_uint2(lo, hi);
   } else if (A.cfg_format == PARVA_CFG_COMPACT) {
     const uint32_t w3 = (uint32_t)r.status | (uint32_t)(r.count > 65535 ? 1 : 0) << 8 |
                         (uint32_t)(r.count > 65535 ? 65535 : r.count) << 16;
-    reinterpret_cast<uint4*>(A.cfg)[i] = make_uint4(b01, b23, b4ol, w3);
+    reinterpret_cast<uint4*>(cfg)[i] = make_uint4(b01, b23, b4ol, w3);
   } else {
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(A.cfg) + i);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<parva_config_record*>(cfg) + i);
     const unsigned long long cbits = (unsigned long long)r.count;
     const unsigned long long vbits = (unsigned long long)__double_as_longlong(r.coverage);
     dst[0] = make_uint4(b01, b23, b4ol, (uint32_t)r.status | (uint32_t)r.flags << 8);
@@ -734,7 +741,10 @@ __device__ __forceinline__ bool plan_scenario_warp(const PlanArgs& A, GScratch<G
       reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_CAPACITY, 0, 0, 0) : make_uint4(0, 0, 0, 0);
     }
   } else if (lane < A.plan_bytes / 16) {
-    reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    const uint4 v = reinterpret_cast<const uint4*>(&W.rec)[lane];
+    reinterpret_cast<uint4*>(dst)[lane] = v;
+    for (int m = 0; m < A.n_mirror; m++)      // fused all-gather: peer copies
+      reinterpret_cast<uint4*>(A.mirror_plan[m] + (size_t)k * A.plan_bytes)[lane] = v;
   }
   gp.sync();
   WCYC(3);
@@ -874,6 +884,19 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
   run_tiles(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
   PHASE(3);
+  if (A.n_mirror) {
+    // fused all-gather completion: every thread's peer stores are fenced
+    // before its CTA counts itself done; the last CTA publishes the epoch
+    // into this rank's flag word on every rank
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0 && atomicAdd(A.done_ctas, 1u) == gridDim.x - 1) {
+      atomicExch(A.done_ctas, 0u);
+      __threadfence_system();
+      for (int m = 0; m < A.n_mirror; m++)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.peer_flag[m]), "r"(A.flag_epoch) : "memory");
+    }
+  }
 }
 
 // K2, warp-autonomous form: every half warp takes scenarios one at a time

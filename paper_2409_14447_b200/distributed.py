@@ -20,6 +20,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native as N
+
 
 def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous block [a, b) of n items for `rank` (sizes differ by at most 1)."""
@@ -121,3 +123,112 @@ def plan_sharded(scen_off, svc_table, svc_rate, svc_bound, plan_fn, group=None, 
     cfg, plan = plan_fn(sh.off, np.asarray(svc_table)[sh.svc_a:sh.svc_b],
                         np.asarray(svc_rate)[sh.svc_a:sh.svc_b], np.asarray(svc_bound)[sh.svc_a:sh.svc_b])
     return gather_records(cfg, plan, sh, scen_off, group=group, device=device)
+
+
+# --------------------------------------------------- fused all-gather (peer memory)
+class PeerGather:
+    """Gathered blocks in peer memory for the fused all-gather.
+
+    Every rank allocates one exportable device buffer: a flag array (one u32
+    per source rank) followed by `n_slots` gathered blocks of world x blk
+    bytes (the packed_block layout, rank r's block at r * blk).  The CUDA IPC
+    handles are exchanged with one all_gather_object, every process maps its
+    peers' buffers, and K2 (parva_plan_batch_fused) stores each record into
+    this rank's block of slot s on every rank while it plans, then raises its
+    flag word on every rank to the launch's epoch.  wait(epoch) makes the
+    stream wait until every rank's records of that epoch have landed here.
+    One process per GPU (peers on other GPUs of the NVLink domain; the tests
+    also run two processes on one GPU)."""
+
+    FLAG_BYTES = 256
+
+    def __init__(self, blk_bytes: int, n_slots: int = 3, group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        L = N.lib()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("the fused all-gather spans at most 8 ranks (one NVLink domain)")
+        self.blk, self.n_slots = int(blk_bytes), int(n_slots)
+        self.slot_bytes = self.world * self.blk
+        size = self.FLAG_BYTES + self.n_slots * self.slot_bytes
+        p = C.c_void_p()
+        N.check(L.parva_ipc_alloc(C.c_size_t(size), C.byref(p)), "parva_ipc_alloc")
+        self.base = p.value
+        hb = int(L.parva_ipc_handle_bytes())
+        h = (C.c_uint8 * hb)()
+        N.check(L.parva_ipc_handle(C.c_void_p(self.base), h), "parva_ipc_handle")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.peers, self.opened = [], []
+        for m, hm in enumerate(handles):
+            if m == self.rank:
+                self.peers.append(self.base)
+                continue
+            q = C.c_void_p()
+            N.check(L.parva_ipc_open((C.c_uint8 * hb).from_buffer_copy(hm), C.byref(q)), "parva_ipc_open")
+            self.peers.append(q.value)
+            self.opened.append(q.value)
+        self.done = torch.zeros(self.n_slots, dtype=torch.int32, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def slot_view(self, slot: int):
+        """This process's gathered block of `slot` as a uint8 tensor view
+        (world x blk), for reading the results."""
+        n = self.slot_bytes
+        return _device_view(self.base + self.FLAG_BYTES + slot * n, n)
+
+    def mirror(self, slot: int, ps: int, overlap: bool = False):
+        """parva_mirror for a launch into `slot` (next epoch): this rank's
+        plan / config sections on every rank."""
+        import ctypes as C
+        self.epoch += 1
+        m = N.Mirror()
+        m.n = self.world
+        m.overlap = 1 if overlap else 0
+        off = self.FLAG_BYTES + slot * self.slot_bytes + self.rank * self.blk
+        for r, b in enumerate(self.peers):
+            m.plan[r] = b + off
+            m.cfg[r] = b + off + ps
+            m.flag[r] = b + 4 * self.rank
+        m.d_done = self.done.data_ptr() + 4 * slot
+        m.epoch = self.epoch
+        return m
+
+    def wait(self, epoch: int | None = None, timeout_s: float = 10.0, stream=None):
+        """Stream-ordered wait until every rank's flag reached `epoch` (default:
+        the last launch's); raises later via check() if a peer timed out."""
+        import ctypes as C
+        e = self.epoch if epoch is None else int(epoch)
+        N.check(N.lib().parva_gather_wait(C.c_void_p(self.base), C.c_int32(self.world), C.c_uint32(e),
+                                          C.c_int64(int(timeout_s * 1e9)), N.ptr(self.status),
+                                          N.stream_handle(stream)), "parva_gather_wait")
+
+    def check(self):
+        if int(self.status.item()) != 0:
+            raise RuntimeError("fused all-gather: a peer's records did not arrive (timeout)")
+
+    def close(self):
+        import ctypes as C
+        L = N.lib()
+        self.torch.cuda.synchronize()
+        for q in self.opened:
+            L.parva_ipc_close(C.c_void_p(q))
+        self.opened = []
+        if self.base:
+            L.parva_ipc_free(C.c_void_p(self.base))
+            self.base = 0
+
+
+def _device_view(addr: int, nbytes: int):
+    """uint8 CUDA tensor over raw device memory owned elsewhere (no copy)."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (addr, False), "version": 3}
+
+    return torch.as_tensor(_Holder(), device="cuda")
