@@ -230,7 +230,8 @@ int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* i
 /* Fused all-gather for the sharded device path (one process per GPU):
  * parva_plan_batch that also stores every plan / config record into this
  * rank's slot of every rank's gathered block over peer memory (NVLink P2P
- * stores from inside K2, so the transfer overlaps the planning), then, after
+ * stores from inside K2, tile by tile, so the transfer overlaps the
+ * planning), then, after
  * a system-scope fence, stores `epoch` into this rank's flag word on every
  * rank.  plan[m] / cfg[m]: where this rank's records go on rank m (device
  * pointers valid in this process: parva_ipc_open of rank m's block plus the

@@ -334,14 +334,8 @@ __device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base
 }
 
 // config record store, words assembled in registers (no local copy)
-__device__ __forceinline__ void store_config_to(const PlanArgs& A, void* cfg, int64_t i, const parva_config_record& r);
-
 __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
-  store_config_to(A, A.cfg, i, r);
-  for (int m = 0; m < A.n_mirror; m++) store_config_to(A, A.mirror_cfg[m], i, r);   // fused all-gather
-}
-
-__device__ __forceinline__ void store_config_to(const PlanArgs& A, void* cfg, int64_t i, const parva_config_record& r) {
+  void* cfg = A.cfg;
 #ifdef PARVA_NO_OUT
   if (A.stream_src) return;   // development probe: PCIe reads without the record writes
 #endif
@@ -741,10 +735,7 @@ __device__ __forceinline__ bool plan_scenario_warp(const PlanArgs& A, GScratch<G
       reinterpret_cast<uint4*>(dst)[lane] = lane == 0 ? make_uint4(PARVA_CAPACITY, 0, 0, 0) : make_uint4(0, 0, 0, 0);
     }
   } else if (lane < A.plan_bytes / 16) {
-    const uint4 v = reinterpret_cast<const uint4*>(&W.rec)[lane];
-    reinterpret_cast<uint4*>(dst)[lane] = v;
-    for (int m = 0; m < A.n_mirror; m++)      // fused all-gather: peer copies
-      reinterpret_cast<uint4*>(A.mirror_plan[m] + (size_t)k * A.plan_bytes)[lane] = v;
+    reinterpret_cast<uint4*>(dst)[lane] = reinterpret_cast<const uint4*>(&W.rec)[lane];
   }
   gp.sync();
   WCYC(3);
@@ -780,6 +771,7 @@ __device__ __forceinline__ uint64_t src_service(const PlanArgs& A, const IndexVi
 // threads configure a tile's services into shared memory, then the warps
 // plan its scenarios (taken from a shared counter, so uneven scenarios
 // balance inside the CTA).  All threads of the CTA call it.
+template <bool kMirror>
 __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, uint8_t* area,
                                           const TileSrc& S, int k, const int k1, int tid, int lane) {
 #ifdef PARVA_PHASE_TIMING
@@ -860,6 +852,22 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
     }
 #endif
     __syncthreads();
+    if (kMirror) {
+      // fused all-gather: the tile's records (contiguous plan and config
+      // ranges, written by this CTA, visible after the barrier) go to this
+      // rank's slot on every rank as coalesced 16-B / 8-B peer stores
+      const int cfg_b = A.cfg_format == PARVA_CFG_TINY ? 8 : A.cfg_format == PARVA_CFG_COMPACT ? 16 : 32;
+      const size_t p0 = (size_t)(S.scen_base + k) * A.plan_bytes, pn = (size_t)n_tile * A.plan_bytes / 16;
+      const size_t c0 = (size_t)(S.svc_base + a0) * cfg_b, cn = (size_t)(a_end - a0) * cfg_b / 8;
+      const uint4* ps = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(A.plan) + p0);
+      const uint2* cs = reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(A.cfg) + c0);
+      for (int m = 0; m < A.n_mirror; m++) {
+        uint4* pd = reinterpret_cast<uint4*>(A.mirror_plan[m] + p0);
+        uint2* cd = reinterpret_cast<uint2*>(A.mirror_cfg[m] + c0);
+        for (size_t x = tid; x < pn; x += PB_THREADS) pd[x] = ps[x];
+        for (size_t x = tid; x < cn; x += PB_THREADS) cd[x] = cs[x];
+      }
+    }
     k += n_tile;
   }
 }
@@ -867,6 +875,8 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
 #ifndef PARVA_TILE_MINB
 #define PARVA_TILE_MINB 3
 #endif
+// kMirror: the fused all-gather instantiation (parva_plan_batch_fused)
+template <bool kMirror>
 __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
@@ -882,9 +892,9 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
   const int k = blockIdx.x * per;
   const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
-  run_tiles(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
+  run_tiles<kMirror>(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
   PHASE(3);
-  if (A.n_mirror) {
+  if (kMirror) {
     // fused all-gather completion: every thread's peer stores are fenced
     // before its CTA counts itself done; the last CTA publishes the epoch
     // into this rank's flag word on every rank
@@ -1184,14 +1194,16 @@ static bool warp_mode(const PlanArgs& A) { return A.stream_src != nullptr; }
 
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
-  const void* fn = wm ? (const void*)plan_warp_kernel : (const void*)plan_batch_kernel;
-  const int kind = wm ? 1 : 0;
+  const bool mir = !wm && A.n_mirror > 0;
+  const void* fn = wm ? (const void*)plan_warp_kernel
+                      : mir ? (const void*)plan_batch_kernel<true> : (const void*)plan_batch_kernel<false>;
+  const int kind = wm ? 1 : mir ? 2 : 0;
   const size_t smem = (wm ? (kWarpArea + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
                           : kWarpArea * PB_WARPS + sizeof(TileSmem)) +
                       index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
   struct DevCfg { size_t conf, occ; int n_sm, per; };
-  static DevCfg s_cfg[kMaxDevices][2];
+  static DevCfg s_cfg[kMaxDevices][3];
   int dev = 0;
   cudaGetDevice(&dev);
   DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][kind];
@@ -1262,9 +1274,12 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, plan_batch_kernel, A) != cudaSuccess) return PARVA_LAUNCH_ERROR;
+    const cudaError_t e = A.n_mirror ? cudaLaunchKernelEx(&cfg, plan_batch_kernel<true>, A)
+                                     : cudaLaunchKernelEx(&cfg, plan_batch_kernel<false>, A);
+    if (e != cudaSuccess) return PARVA_LAUNCH_ERROR;
   } else {
-    plan_batch_kernel<<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+    if (A.n_mirror) plan_batch_kernel<true><<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+    else plan_batch_kernel<false><<<L.grid, PB_THREADS, L.smem, stream>>>(A);
   }
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
@@ -1276,7 +1291,8 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
   PlanArgs copy = A;
   void* args[] = {&copy};
   cudaKernelNodeParams p = {};
-  p.func = warp_mode(A) ? (void*)plan_warp_kernel : (void*)plan_batch_kernel;
+  p.func = warp_mode(A) ? (void*)plan_warp_kernel
+                         : A.n_mirror ? (void*)plan_batch_kernel<true> : (void*)plan_batch_kernel<false>;
   p.gridDim = dim3(L.grid);
   p.blockDim = dim3(PB_THREADS);
   p.sharedMemBytes = (unsigned)L.smem;

@@ -7,6 +7,7 @@ timed on the C2 batch (device path + zero-copy e2e), with a parity check.
     python tools/k2_variants.py run
 """
 import ctypes as C
+import os
 import shutil
 import subprocess
 import sys
@@ -55,12 +56,16 @@ def build():
         shutil.copytree(b.CSRC, d)
         if not (OUT / "include").exists():
             (OUT / "include").symlink_to(REPO / "include")
-        if patches == ["HEAD"]:
+        sources = list(b.SOURCES)
+        if patches == ["HEAD"]:            # the committed csrc/ at K2_REF (default HEAD)
+            ref = os.environ.get("K2_REF", "HEAD")
             for f in d.iterdir():
-                r = subprocess.run(["git", "show", f"HEAD:paper_2409_14447_b200/csrc/{f.name}"], cwd=REPO,
+                r = subprocess.run(["git", "show", f"{ref}:paper_2409_14447_b200/csrc/{f.name}"], cwd=REPO,
                                    capture_output=True)
                 if r.returncode == 0:
                     f.write_bytes(r.stdout)
+                elif f.name in sources:
+                    sources.remove(f.name)
             patches = []
         pb = d / "plan_batch.cu"
         src = pb.read_text()
@@ -69,7 +74,7 @@ def build():
         pb.write_text(src)
         lib = OUT / f"libk2_{name}.so"
         inc = str(REPO / "include")
-        cmd = [b.NVCC, *b.FLAGS, *flags, "-o", str(lib), *[str(d / s) for s in b.SOURCES], "-lcudart"]
+        cmd = [b.NVCC, *b.FLAGS, *flags, "-o", str(lib), *[str(d / s) for s in sources], "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         i = r.stderr.find("_ZN5parva17plan_batch_kernel")
         print(name, r.returncode, r.stderr[i:i + 300].split("\n")[1:2], r.stderr[:300] if r.returncode else "")
