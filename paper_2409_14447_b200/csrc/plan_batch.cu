@@ -49,8 +49,7 @@ struct alignas(16) GScratch {
   uint16_t diag[G];                       // optimize diagnostics, in order
   parva_plan_record rec;
 };
-using WarpScratch = GScratch<32>;
-// a warp's scratch in the tile kernel: two half-warp groups, or (overflow
+// a warp's scratch (tile and streamed kernels): two half-warp groups, or (overflow
 // pass) one full-warp group over the same bytes
 constexpr size_t kWarpArea = 2 * sizeof(GScratch<16>) > sizeof(GScratch<32>) ? 2 * sizeof(GScratch<16>)
                                                                              : sizeof(GScratch<32>);
