@@ -193,13 +193,8 @@ struct alignas(16) SimWarp {
   double smp[64];                 // scale * exponential draws, in stream order
   double tm[32];                  // next arrival times (ms), in order
   double ring[kRing];             // last kRing ingested arrivals (ms)
-  double ev_t[kSimLanes];         // pending completions, one FIFO per segment:
-  double busy[kSimSegs];
-  uint32_t ev_q[kSimLanes];       // segment g owns slots [seg_lo[g], seg_lo[g] + lanes_g)
-  int free_seg[kSimSegs];
-  int seg_lo[kSimSegs];
-  int seg_head[kSimSegs];
-  int seg_n[kSimSegs];
+  double ev_t[kSimLanes];         // pending completions, one FIFO per segment
+  uint32_t ev_q[kSimLanes];       // (segment g's slots: [sg_lo, sg_lo + lanes_g), lane g's registers)
 };
 
 // Arrival stream of one service (evaluation.py:207-226): Poisson = numpy
@@ -353,23 +348,34 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
     gen.init(P.d_pcg + 4 * s, kind, P.d_scale[s], P.d_horizon_s[s], P.d_count[s], lane);
     const int g0 = P.d_seg_off[s];
     const int ns = P.d_seg_off[s + 1] - g0;
-    int lanes_total = 0;
-    for (int g = 0; g < ns; g++) lanes_total += P.d_seg_lanes[g0 + g];
-    if (ns > kSimSegs || lanes_total > kSimLanes) {
+    if (ns > kSimSegs) {
       if (lane == 0) R.d_status[s] = PARVA_CAPACITY;
       continue;
     }
+    // segment g's state lives in lane g's registers: free lanes, busy time,
+    // service time, batch size, and its completion FIFO (slots [sg_lo,
+    // sg_lo + sg_lanes) of W.ev_*, head cached in head_t / head_q)
+    const bool own = lane < ns;
+    const int sg_lanes = own ? P.d_seg_lanes[g0 + lane] : 0;
+    const double sg_ms = own ? P.d_seg_ms[g0 + lane] : 0.0;
+    const int64_t sg_batch = own ? (int64_t)P.d_seg_batch[g0 + lane] : 0;
+    int sg_lo = sg_lanes;                  // exclusive prefix of the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, sg_lo, o);
+      if (lane >= o) sg_lo += v;
+    }
+    const int lanes_total = __shfl_sync(0xffffffffu, sg_lo, 31);
+    sg_lo -= sg_lanes;
+    if (lanes_total > kSimLanes) {
+      if (lane == 0) R.d_status[s] = PARVA_CAPACITY;
+      continue;
+    }
+    int sg_free = sg_lanes, sg_head = 0, sg_n = 0;
+    double sg_busy = 0.0, head_t = 0.0;
+    uint32_t head_q = 0;
     const double H = P.d_horizon_ms[s];
     const double slo = P.d_slo[s];
-    for (int g = 0, lo = 0; g < ns; g++) {
-      W.free_seg[g] = P.d_seg_lanes[g0 + g];
-      W.busy[g] = 0.0;
-      W.seg_lo[g] = lo;
-      W.seg_head[g] = 0;
-      W.seg_n[g] = 0;
-      lo += P.d_seg_lanes[g0 + g];
-    }
-    __syncwarp();
     // reduction rounds that cover the segments (lane g = segment g)
     const int seg_rounds = ns <= 1 ? 0 : 32 - __clz(ns - 1);
     int free_lanes = lanes_total;
@@ -410,10 +416,10 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
     auto dispatch = [&](double now) {     // evaluation.py:368-388
       if (now >= H) return;
       while (qh < ptr && free_lanes > 0) {
-        const int g = __ffs(__ballot_sync(0xffffffffu, lane < ns && W.free_seg[lane] > 0)) - 1;
-        const double ms = P.d_seg_ms[g0 + g];
+        const int g = __ffs(__ballot_sync(0xffffffffu, own && sg_free > 0)) - 1;
+        const double ms = __shfl_sync(0xffffffffu, sg_ms, g);
         const int64_t qn = ptr - qh;
-        const int64_t b = P.d_seg_batch[g0 + g];
+        const int64_t b = __shfl_sync(0xffffffffu, sg_batch, g);
         const int64_t n = b < qn ? b : qn;
         const double first = ptr - qh <= kRing ? W.ring[qh & (kRing - 1)] : buf[qh];
         qh += n;
@@ -423,19 +429,23 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
         batches++;
         served += n;
         if (latency > slo) violations++;
-        W.free_seg[g]--;
         free_lanes--;
         const double rem = __dsub_rn(H, now);
         const double m = ms < rem ? ms : rem;
-        W.busy[g] = __dadd_rn(W.busy[g], m > 0.0 ? m : 0.0);
-        // a segment's completions are pushed in (time, seq) order (now is
-        // monotone, ms fixed), so each segment's pending events are a FIFO
-        const int lanes_g = P.d_seg_lanes[g0 + g];
-        int slot = W.seg_head[g] + W.seg_n[g];
-        if (slot >= lanes_g) slot -= lanes_g;
-        W.ev_t[W.seg_lo[g] + slot] = __dadd_rn(now, ms);
-        W.ev_q[W.seg_lo[g] + slot] = seq++;
-        W.seg_n[g]++;
+        const double t_done = __dadd_rn(now, ms);
+        const uint32_t q = seq++;
+        if (lane == g) {
+          sg_free--;
+          sg_busy = __dadd_rn(sg_busy, m > 0.0 ? m : 0.0);
+          // a segment's completions are pushed in (time, seq) order (now is
+          // monotone, ms fixed), so each segment's pending events are a FIFO
+          int slot = sg_head + sg_n;
+          if (slot >= sg_lanes) slot -= sg_lanes;
+          W.ev_t[sg_lo + slot] = t_done;
+          W.ev_q[sg_lo + slot] = q;
+          if (sg_n == 0) { head_t = t_done; head_q = q; }
+          sg_n++;
+        }
       }
     };
 
@@ -451,12 +461,7 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
         int ei = -1;
         double et = 0.0;
         uint32_t eq = 0xFFFFFFFFu;
-        if (lane < ns && W.seg_n[lane] > 0) {
-          const int k = W.seg_lo[lane] + W.seg_head[lane];
-          et = W.ev_t[k];
-          eq = W.ev_q[k];
-          ei = lane;
-        }
+        if (own && sg_n > 0) { et = head_t; eq = head_q; ei = lane; }
         for (int r = 0; r < seg_rounds; r++) {
           const int o = 1 << r;
           const double t2 = __shfl_xor_sync(0xffffffffu, et, o);
@@ -478,11 +483,12 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
         if (free_lanes > 0) schedule_wakeup();
       } else {
         const double now = bt;
-        const int g = best;
-        const int lanes_g = P.d_seg_lanes[g0 + g];
-        W.seg_head[g] = W.seg_head[g] + 1 == lanes_g ? 0 : W.seg_head[g] + 1;
-        W.seg_n[g]--;
-        W.free_seg[g]++;
+        if (lane == best) {
+          sg_head = sg_head + 1 == sg_lanes ? 0 : sg_head + 1;
+          sg_n--;
+          sg_free++;
+          if (sg_n > 0) { head_t = W.ev_t[sg_lo + sg_head]; head_q = W.ev_q[sg_lo + sg_head]; }
+        }
         free_lanes++;
         if (now < H) {
           ingest(now);
@@ -502,9 +508,10 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(parva_sim_prob
       R.d_served[s] = served;
       R.d_batches[s] = batches;
       R.d_violations[s] = violations;
-      for (int g = 0; g < ns; g++) R.d_busy_ms[g0 + g] = W.busy[g];
+
       R.d_status[s] = overflow ? PARVA_CAPACITY : PARVA_OK;
     }
+    if (own) R.d_busy_ms[g0 + lane] = sg_busy;
     __syncwarp();
   }
 }
