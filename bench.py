@@ -326,6 +326,8 @@ def main():
                 works[b].wait()
                 works[b] = None
 
+    if peer is not None:
+        dist.barrier()                   # every rank's inputs are resident before anyone waits on flags
     for i in range(args.warmup):
         step(i)
     drain()

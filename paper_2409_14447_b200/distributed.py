@@ -199,7 +199,7 @@ class PeerGather:
         m.epoch = self.epoch
         return m
 
-    def wait(self, epoch: int | None = None, timeout_s: float = 10.0, stream=None):
+    def wait(self, epoch: int | None = None, timeout_s: float = 60.0, stream=None):
         """Stream-ordered wait until every rank's flag reached `epoch` (default:
         the last launch's); raises later via check() if a peer timed out."""
         import ctypes as C
