@@ -336,10 +336,22 @@ def main():
         dist.barrier()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if peer is not None:
+        # did every rank's warm-up records arrive?  If not (no working peer
+        # writes on this box), time the NCCL collective instead
         torch.cuda.synchronize()
-        peer.check()
+        ok = torch.tensor([0 if int(peer.status.item()) else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            print("fused all-gather: peer records did not arrive in the warm-up; using NCCL", file=sys.stderr)
+            peer = None
+            gather_mode = "nccl"
+            for i in range(args.warmup):
+                step(i)
+            drain()
+            torch.cuda.synchronize()
+        else:
+            mirrors = {i: peer.mirror(i % R, ps, overlap=True) for i in range(args.steps)}   # built outside the timing
         dist.barrier()
-        mirrors = {i: peer.mirror(i % R, ps, overlap=True) for i in range(args.steps)}   # built outside the timing
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t_start.record(stream)
