@@ -134,7 +134,7 @@ def c2_inputs(fx, n, seed):
     return off, tab, np.ascontiguousarray(sb.rate.ravel()), np.ascontiguousarray(sb.bound.ravel())
 
 
-def cpu_baseline_c2(fx, n, min_seconds=3.0):
+def cpu_baseline_c2(fx, n, min_seconds=10.0):
     """The oracle (C port of the reference) on all host threads, bounded sample."""
     import oracle
     from paper_2409_14447_b200.tables import pack_tables
