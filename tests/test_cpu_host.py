@@ -87,6 +87,32 @@ def test_service_from_record_with_empty_size_classes():
         assert got.last_segment is None
 
 
+def test_c_abi_rejects_bad_arguments_before_touching_the_device():
+    """Argument checks of the C entries run before any CUDA call, so they
+    return PARVA_BAD_INPUT (5) here, on a host without a GPU."""
+    import ctypes as C
+    L = N.load_library()
+    BAD = 5
+    m = N.Mirror()
+    m.n = 0
+    dummy = C.c_void_p(16)
+    assert L.parva_plan_batch_fused(None, None, 0, 0, None, None, None, None, 1, 4, None, 2, None,
+                                    C.byref(m), None) == BAD
+    assert L.parva_gather_wait(None, 1, 1, 0, None, None) == BAD
+    assert L.parva_gather_wait(dummy, 0, 1, 0, dummy, None) == BAD
+    assert L.parva_gather_wait(dummy, 9, 1, 0, dummy, None) == BAD
+    assert L.parva_ipc_handle(None, None) == BAD
+    assert L.parva_ipc_open(None, None) == BAD
+    assert L.parva_ipc_alloc(C.c_size_t(0), C.byref(C.c_void_p())) == BAD
+    assert L.parva_plan_host_mapped_submit(None, None, 0, 0, None, C.c_int64(0), None, 1, 4, 2, 64, None,
+                                           C.c_size_t(0), None, None) == BAD
+    assert L.parva_plan_host_mapped(None, None, 0, 0, None, C.c_int64(0), None, 1, 4, 2, 64, None,
+                                    C.c_size_t(0), None) == BAD
+    assert L.parva_plan_host_mapped_wait(C.c_uint64(0)) == 0          # the empty call's ticket
+    assert L.parva_sim_seed_states(None, 1, C.c_int64(0), C.c_int64(1), None) == BAD
+    assert L.parva_ipc_handle_bytes() == 64
+
+
 def test_record_layouts():
     assert CONFIG_DTYPE.itemsize == 32 and PLAN_DTYPE.itemsize == 128
 
