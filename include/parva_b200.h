@@ -334,21 +334,26 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
  * chunk of consecutive scenarios, so the data of the first scenarios arrives
  * first.  Header: int32 n_chunks, int32 chunk_scen (scenarios per chunk, the
  * last chunk may hold fewer), int32 pad[2], parva_stream_chunk[n_chunks];
- * padded to 256 bytes. */
+ * padded to 256 bytes.  A chunk whose scenarios all list the same table ids
+ * (same count, same order -- e.g. every scenario over one model set) stores
+ * that sequence once (tmpl = its length) instead of one id per service. */
 typedef struct {
   int32_t scen_lo;      /* first scenario of the chunk          */
   int32_t svc_lo;       /* first service of the chunk           */
   int32_t k, m;         /* scenarios, services                  */
   int64_t offset;       /* byte offset of the chunk block       */
+  int32_t tmpl;         /* > 0: table ids stored once per chunk  */
+  int32_t reserved;
 } parva_stream_chunk;
 
-#define parva_stream_header_bytes(n_chunks) ((((int64_t)(n_chunks) * 24 + 16) + 255) & ~(int64_t)255)
+#define parva_stream_header_bytes(n_chunks) ((((int64_t)(n_chunks) * 32 + 16) + 255) & ~(int64_t)255)
 
-/* Bytes of the streamed input block for a batch (exact, for these offsets). */
+/* Bytes of the streamed input block for a batch: an upper bound for these
+ * offsets (exact when no chunk repeats one table-id sequence). */
 int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32_t chunk_scen);
 /* Pack a batch (services of scenario k: [h_scen_off[k], h_scen_off[k+1]),
  * h_scen_off[0] = 0) into a streamed input block of `capacity` bytes;
- * returns the bytes written, or -1. */
+ * returns the bytes written (pass that as in_bytes), or -1. */
 int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const uint16_t* h_table,
                           const double* h_rate, const double* h_bound, int32_t chunk_scen,
                           void* h_block, int64_t capacity);

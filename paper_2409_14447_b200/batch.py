@@ -390,6 +390,7 @@ class MappedHostBatch:
                                       C.c_int32(plan_bytes), C.byref(self.layout)), "parva_mapped_layout")
         self._off32 = np.ascontiguousarray(scen_off - scen_off[0], dtype=np.int32)
         self.in_bytes = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(self._off32), C.c_int32(chunk_scen)))
+        self.in_capacity = self.in_bytes   # upper bound; fill() sets in_bytes to the packed size
         if self.in_bytes < 0:
             raise ValueError("invalid scenario offsets")
         if depth < 1:
@@ -421,9 +422,11 @@ class MappedHostBatch:
         bound = np.ascontiguousarray(np.asarray(svc_bound)[sa:sb], dtype=np.float64)
         n = N.lib().parva_stream_pack(C.c_int32(self.n_scen), N.np_ptr(off32), N.np_ptr(tab), N.np_ptr(rate),
                                       N.np_ptr(bound), C.c_int32(self.chunk_scen), C.c_void_p(self.h_in.data_ptr()),
-                                      C.c_int64(self.in_bytes))
-        if n != self.in_bytes:
+                                      C.c_int64(self.in_capacity))
+        if n < 0:
             raise ValueError("parva_stream_pack failed (offsets changed shape?)")
+        self.in_bytes = int(n)          # chunks that repeat one table-id sequence store it once
+        self._args = {}
 
     def _call_args(self, dt, optimize, threshold, stream, slot):
         sh = N.stream_handle(stream)

@@ -518,15 +518,25 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
     const int32_t sa = h_scen_off[a], sb = h_scen_off[b];
     parva_chunk_layout L;
     parva_packed_layout(b - a, sb - sa, PARVA_CFG_TINY, 64, &L);
+    // one table-id sequence repeated by every scenario of the chunk?
+    const int32_t t0 = h_scen_off[a + 1] - sa;
+    bool tmpl = t0 > 0 && b - a > 1;
+    for (int32_t k = a + 1; tmpl && k < b; k++) {
+      const int32_t ka = h_scen_off[k];
+      tmpl = h_scen_off[k + 1] - ka == t0 && std::memcmp(h_table + ka, h_table + sa, size_t(t0) * 2) == 0;
+    }
+    const int32_t n_tab = tmpl ? t0 : sb - sa;
+    const int64_t blk_bytes = ((int64_t)L.in_table + int64_t(n_tab) * 2 + 15) & ~int64_t(15);   // 16-B aligned blocks
     tab[c].scen_lo = a; tab[c].svc_lo = sa; tab[c].k = b - a; tab[c].m = sb - sa; tab[c].offset = off;
+    tab[c].tmpl = tmpl ? t0 : 0; tab[c].reserved = 0;
     uint8_t* blk = out + off;
-    std::memset(blk, 0, (size_t)L.in_bytes);
+    std::memset(blk, 0, (size_t)blk_bytes);
     int32_t* so = reinterpret_cast<int32_t*>(blk + L.in_scen_off);
     for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
     std::memcpy(blk + L.in_rate, h_rate + sa, size_t(sb - sa) * 8);
     std::memcpy(blk + L.in_bound, h_bound + sa, size_t(sb - sa) * 8);
-    std::memcpy(blk + L.in_table, h_table + sa, size_t(sb - sa) * 2);
-    off += L.in_bytes;
+    std::memcpy(blk + L.in_table, h_table + sa, size_t(n_tab) * 2);
+    off += blk_bytes;
   }
   return off;
 }

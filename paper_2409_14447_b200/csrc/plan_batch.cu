@@ -1012,7 +1012,7 @@ __device__ __forceinline__ void group_wait(const PlanArgs& A, const void* p_lo, 
 // A group's current chunk of the streamed input (a header, i.e. the chunk
 // table, followed by chunk blocks; scenarios ascend per group).
 struct ChunkCursor {
-  int c = -1, scen_lo = 0, svc_lo = 0;
+  int c = -1, scen_lo = 0, svc_lo = 0, tmpl = 0;   // tmpl > 0: one table-id sequence for the chunk
   const int32_t* off = nullptr;
   const double* rate = nullptr;
   const double* bound = nullptr;
@@ -1043,7 +1043,8 @@ __device__ __forceinline__ bool stream_plan_one(const PlanArgs& A, const IndexVi
     C.rate = reinterpret_cast<const double*>(blk + rate_off);
     C.bound = C.rate + mc;
     C.table = reinterpret_cast<const uint16_t*>(C.bound + mc);
-    group_wait<G>(A, blk, C.table + mc, gl, gp);  // the whole chunk block has landed
+    C.tmpl = __ldcg(&tab[cj].tmpl);
+    group_wait<G>(A, blk, C.table + (C.tmpl > 0 ? C.tmpl : mc), gl, gp);  // the whole chunk block has landed
   }
   const int jl = j - C.scen_lo;
   const int a0 = __ldcg(C.off + jl);
@@ -1056,8 +1057,8 @@ __device__ __forceinline__ bool stream_plan_one(const PlanArgs& A, const IndexVi
     if (b + gl < n) {
       const int i = a0 + b + gl;
       double tpc[5];
-      const uint64_t m = svc_configure(A, V, (int)__ldcg(C.table + i), __ldcg(C.rate + i), __ldcg(C.bound + i),
-                                       (int64_t)C.svc_lo + i, tpc);
+      const int t = (int)__ldcg(C.table + (C.tmpl > 0 ? b + gl : i));
+      const uint64_t m = svc_configure(A, V, t, __ldcg(C.rate + i), __ldcg(C.bound + i), (int64_t)C.svc_lo + i, tpc);
       if (b == 0) {
 #pragma unroll
         for (int cc = 0; cc < 5; cc++) S.tp[gl * 5 + cc] = tpc[cc];
