@@ -336,7 +336,9 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
  * last chunk may hold fewer), int32 pad[2], parva_stream_chunk[n_chunks];
  * padded to 256 bytes.  A chunk whose scenarios all list the same table ids
  * (same count, same order -- e.g. every scenario over one model set) stores
- * that sequence once (tmpl = its length) instead of one id per service. */
+ * that sequence once (tmpl = its length) instead of one id per service, and
+ * no offsets (rates at the block start; scenario k owns services
+ * [k tmpl, (k+1) tmpl)).  Chunk blocks are 16-byte aligned. */
 typedef struct {
   int32_t scen_lo;      /* first scenario of the chunk          */
   int32_t svc_lo;       /* first service of the chunk           */

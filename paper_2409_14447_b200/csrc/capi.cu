@@ -525,17 +525,23 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
       const int32_t ka = h_scen_off[k];
       tmpl = h_scen_off[k + 1] - ka == t0 && std::memcmp(h_table + ka, h_table + sa, size_t(t0) * 2) == 0;
     }
+    // template chunks: no offsets (scenario k owns [k t0, (k+1) t0)) and the
+    // table ids once; otherwise offsets | rates | bounds | table ids
     const int32_t n_tab = tmpl ? t0 : sb - sa;
-    const int64_t blk_bytes = ((int64_t)L.in_table + int64_t(n_tab) * 2 + 15) & ~int64_t(15);   // 16-B aligned blocks
+    const int64_t rate_at = tmpl ? 0 : L.in_rate;
+    const int64_t table_at = rate_at + int64_t(sb - sa) * 16;
+    const int64_t blk_bytes = (table_at + int64_t(n_tab) * 2 + 15) & ~int64_t(15);   // 16-B aligned blocks
     tab[c].scen_lo = a; tab[c].svc_lo = sa; tab[c].k = b - a; tab[c].m = sb - sa; tab[c].offset = off;
     tab[c].tmpl = tmpl ? t0 : 0; tab[c].reserved = 0;
     uint8_t* blk = out + off;
     std::memset(blk, 0, (size_t)blk_bytes);
-    int32_t* so = reinterpret_cast<int32_t*>(blk + L.in_scen_off);
-    for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
-    std::memcpy(blk + L.in_rate, h_rate + sa, size_t(sb - sa) * 8);
-    std::memcpy(blk + L.in_bound, h_bound + sa, size_t(sb - sa) * 8);
-    std::memcpy(blk + L.in_table, h_table + sa, size_t(n_tab) * 2);
+    if (!tmpl) {
+      int32_t* so = reinterpret_cast<int32_t*>(blk + L.in_scen_off);
+      for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
+    }
+    std::memcpy(blk + rate_at, h_rate + sa, size_t(sb - sa) * 8);
+    std::memcpy(blk + rate_at + int64_t(sb - sa) * 8, h_bound + sa, size_t(sb - sa) * 8);
+    std::memcpy(blk + table_at, h_table + sa, size_t(n_tab) * 2);
     off += blk_bytes;
   }
   return off;

@@ -1038,17 +1038,18 @@ __device__ __forceinline__ bool stream_plan_one(const PlanArgs& A, const IndexVi
     C.svc_lo = __ldcg(&tab[cj].svc_lo);
     const int kc = __ldcg(&tab[cj].k), mc = __ldcg(&tab[cj].m);
     const uint8_t* blk = A.stream_dst + __ldcg(&tab[cj].offset);
-    const int64_t rate_off = ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
+    C.tmpl = __ldcg(&tab[cj].tmpl);
+    // template chunks carry no offsets: scenario k owns [k tmpl, (k+1) tmpl)
+    const int64_t rate_off = C.tmpl > 0 ? 0 : ((int64_t)(kc + 1) * 4 + 15) & ~int64_t(15);
     C.off = reinterpret_cast<const int32_t*>(blk);
     C.rate = reinterpret_cast<const double*>(blk + rate_off);
     C.bound = C.rate + mc;
     C.table = reinterpret_cast<const uint16_t*>(C.bound + mc);
-    C.tmpl = __ldcg(&tab[cj].tmpl);
     group_wait<G>(A, blk, C.table + (C.tmpl > 0 ? C.tmpl : mc), gl, gp);  // the whole chunk block has landed
   }
   const int jl = j - C.scen_lo;
-  const int a0 = __ldcg(C.off + jl);
-  const int n = __ldcg(C.off + jl + 1) - a0;
+  const int a0 = C.tmpl > 0 ? jl * C.tmpl : __ldcg(C.off + jl);
+  const int n = C.tmpl > 0 ? C.tmpl : __ldcg(C.off + jl + 1) - a0;
   if (G < 32 && n > G) return false;
 #ifdef PARVA_PHASE_TIMING
   const long long wt1 = clock64();
