@@ -32,7 +32,7 @@ for _ in range(steps):
     ref.run(dt)
 sync_us = (time.perf_counter() - t0) / steps * 1e6
 print(f"sync        : {sync_us:7.1f} us/call  {n / sync_us * 1e6:.3e} scen/s")
-for D in (2, 3, 4):
+for D in (int(x) for x in (sys.argv[3].split(",") if len(sys.argv) > 3 else ["2", "3", "4"])):
     mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, depth=D)
 
     def go(k):
