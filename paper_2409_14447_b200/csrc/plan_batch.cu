@@ -3,18 +3,26 @@
 // Replaces plan_services' timed region (pipeline.py:95-103) for a batch of
 // independent scenarios: configure_service x N (configurator.py:189-191),
 // relocate_segments (allocator.py:292-316), optimize_allocation
-// (allocator.py:362-443).  One warp plans one scenario:
-//   * configure: lane = service; per size class a binary search over the
-//     latency-sorted prefix-argmax index held in shared memory (exact:
-//     the points with lat < bound are a prefix of the sorted order and the
-//     argmax under a total order is prefix-decomposable);
+// (allocator.py:362-443).  A lane group (half warp; a full warp for the
+// rare scenario wider than 16 services / GPUs) plans one scenario:
+//   * configure: thread = service (tile kernel) or lane = service (streamed
+//     kernel); per size class a binary search over the latency-sorted
+//     prefix-argmax index, staged in shared memory, or read through L1 by
+//     back-to-back overlapped launches (exact: the points with lat < bound
+//     are a prefix of the sorted order and the argmax under a total order is
+//     prefix-decomposable);
 //   * relocate / optimize: lane = GPU; a GPU is a 7-bit slot mask; first-fit
 //     is one ballot over find_start(mask) (cursorless first-fit is
 //     equivalent to the reference's cursors); the
 //     freed_rate ledger lives in lane = service registers, snapshot/restore
 //     is a register copy.
-// Scenarios beyond the 128-byte record's limits report PARVA_CAPACITY and
-// are re-planned by the general kernel (plan_general.cu).
+// Two kernels: plan_batch_kernel (device-resident batches, tile by tile;
+// the <true> instantiation also copies each tile's records into every
+// rank's gathered block over peer memory) and plan_warp_kernel (the
+// zero-copy entry: loader CTAs stream the input over PCIe with TMA while
+// the other warps plan).  Scenarios beyond the 128-byte record's limits
+// report PARVA_CAPACITY and are re-planned by the general kernel
+// (plan_general.cu).
 #include <cuda_runtime.h>
 
 #include <algorithm>
