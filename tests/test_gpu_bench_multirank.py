@@ -1,0 +1,39 @@
+"""The bench's sharded (N > 1) flow end to end: two ranks on the one GPU over
+gloo (PARVA_DIST_BACKEND=gloo), fused all-gather and the NCCL-style
+collective path, one JSON line each with the driver-contract fields."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+REPO = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("gather", ["fused", "nccl"])
+def test_bench_two_ranks(gather):
+    env = dict(os.environ, PARVA_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "bench.py"),
+           "--gpus", "2", "--steps", "5", "--warmup", "3", "--no-cpu", "--no-extra", "--no-sweep",
+           "--gather", gather]
+    r = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["gather"] == gather
+    assert line["parity_vs_oracle_first_2000"] is True
+    assert line["e2e"]["plan_records_equal_device_path"] is True
+    assert line["value"] > 0 and line["gpu_launches"] == 5
