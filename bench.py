@@ -4,22 +4,35 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 Workload (BASELINE.json configs[1], "C2"): the 11 fixture models x 10^4
-synthetic (SLO, request-rate) scenarios per GPU (SURVEY §8d C2 generator,
-seed = rank).  One step = one pass of the hot path over that batch: the
-fused K2 launch that configures every service, relocates and optimizes
-every scenario (pipeline.py:95-103 semantics), inputs resident in HBM, L2
-flushed between steps.  N>1 (torchrun): every rank plans its own 10^4
-scenarios (weak scaling) and the step ends with one NCCL all-gather of the
-128-byte plan records.  Also reported: e2e through the host-buffer C-ABI
-entry (parva_plan_host: H2D inputs, plan, D2H records), the C3 configurator
-sweep (10^4 dense tables, the HBM-roofline kernel), and the CPU oracle
-(C restatement of the reference, all host threads) as cpu_baseline.
+synthetic (SLO, request-rate) scenarios per GPU (SURVEY §8d C2 generator).
+One step = one pass of the hot path over one batch: one K2 launch that
+configures every service, relocates and optimizes every scenario
+(pipeline.py:95-103 semantics) with its inputs resident in HBM.  Steps cycle
+through ~70 resident input batches (more than the 126 MB L2 in total, so no
+flush is needed) and write into one output slot per step; consecutive steps
+are programmatic dependent launches whose slot tickets serialize launches
+that share a slot.  N > 1 (torchrun, one process per GPU): every rank plans
+its contiguous shard of each global batch (weak scaling: 10^4 scenarios per
+GPU) and the step ends when every rank holds every rank's records: by
+default K2 itself stores them into every rank's slot over NVLink peer
+memory (fused all-gather, 64-byte plan records + 8-byte config records),
+with one exact-epoch wait + release per step; --gather nccl uses one NCCL
+all-gather of the packed 128-byte records instead.  After the timed region
+every rank checks its gathered copy of every timed step against the CPU
+oracle (digests of each rank's own shard, exchanged once).
+
+Also reported: e2e through the C-ABI host entry, the C3 configurator sweep
+(the HBM-roofline kernel; sharded across ranks at N > 1 with one all-gather
+of config records), C4 (10^6 scenarios; sharded at N > 1), C5, the batched
+simulator, and the CPU baselines (the C oracle = a port of the reference,
+and the reference's own Python planner when baseline/_ref is installed).
 """
 
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import math
 import os
@@ -82,47 +95,59 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """nvidia-smi clocks + throttle reasons.  nvidia-smi runs in its own loop
+    mode (-lms) as ONE child process started before the warm-up, so nothing
+    forks while the timed region runs (a fork per sample had stalled the
+    launching thread); mark() brackets the spans whose samples count."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+    def __init__(self, index: int, period_ms: int = 20):
+        self.samples = []          # (monotonic time, fields)
+        self.spans = []
+        self._p = None
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", str(period_ms)],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self._p = None
 
-    def _run(self):
-        while not self._stop.is_set():
+    def _read(self):
+        for line in self._p.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 6:
+                self.samples.append((time.monotonic(), f))
+
+    def begin(self):
+        self._t0 = time.monotonic()
+
+    def end(self):
+        self.spans.append((self._t0, time.monotonic()))
+
+    def close(self):
+        if self._p is not None:
+            self._p.terminate()
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._p.wait(timeout=5)
             except Exception:  # noqa: BLE001
-                pass
-            self._stop.wait(0.05)
-
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+                self._p.kill()
 
     def summary(self):
-        if not self.samples:
+        pad = 0.025
+        sel = [f for t, f in self.samples if any(a - pad <= t <= b + pad for a, b in self.spans)]
+        if not sel:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "").isdigit()  # noqa: E731
+        sm = [float(s[0]) for s in sel if num(s[0])]
+        mx = [float(s[1]) for s in sel if num(s[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].strip() == "Active"})
+        reasons = sorted({names[i] for s in sel for i in range(4) if s[2 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(sel)}
 
 
 def c2_inputs(fx, n, seed):
@@ -134,27 +159,111 @@ def c2_inputs(fx, n, seed):
     return off, tab, np.ascontiguousarray(sb.rate.ravel()), np.ascontiguousarray(sb.bound.ravel())
 
 
-def cpu_baseline_c2(fx, n, min_seconds=10.0):
-    """The oracle (C port of the reference) on all host threads, bounded sample."""
+def batch_seed(p):
+    """Seed of resident input batch p: batch 0 is C2 itself (seed 0)."""
+    return 0 if p == 0 else 1000 + p
+
+
+def n_resident_batches(n_svc_local, n_local):
+    """P resident input batches of one shard's shape, cycled so that every
+    step reads inputs that are not in L2 (P x ~2.2 MB > 126 MB)."""
+    per_batch = n_svc_local * 20 + (n_local + 1) * 4
+    return int(min(256, max(2, -(-160_000_000 // max(per_batch, 1)))))
+
+
+def lscpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
+def digest(cfg_bytes: bytes, plan_bytes: bytes) -> str:
+    return hashlib.sha256(cfg_bytes + plan_bytes).hexdigest()[:32]
+
+
+def ref_python(*argv, timeout=900):
+    """tools/ref_python_bench.py: the reference itself (migplan from
+    baseline/_ref, unmodified) on this host; None if it is not installed."""
+    if not (REPO / "baseline" / "_ref" / "migplan").is_dir():
+        return None
+    try:
+        r = subprocess.run([sys.executable, str(REPO / "tools" / "ref_python_bench.py"), *map(str, argv)],
+                           capture_output=True, text=True, timeout=timeout,
+                           env=dict(os.environ, PYTHONDONTWRITEBYTECODE="1"))
+        return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {"error": r.stderr[-300:]}
+    except Exception as exc:  # noqa: BLE001
+        return {"error": str(exc)}
+
+
+def cpu_baselines(fx, n, min_seconds=10.0):
+    """BASELINE.md §3 on this host: the oracle (C port of the reference) on
+    all host threads (the headline CPU number, the reference arm's) and on
+    one; the reference itself (pure Python migplan) on one core over a
+    bounded C2 sample and on every core (fork Pool) over the full C2 batch."""
     import oracle
     from paper_2409_14447_b200.tables import pack_tables
     pt = pack_tables(fx.tables)
     off, tab, rate, bound = c2_inputs(fx, n, 0)
     threads = os.cpu_count() or 1
-    oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)  # warm
-    done, t0 = 0, time.perf_counter()
-    while True:
-        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
-        done += n
-        el = time.perf_counter() - t0
-        if el >= min_seconds:
-            break
-    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"C2 batch of {n} scenarios x 11 services, repeated {done // n}x ({el:.1f} s), "
-                      f"oracle/migplan_oracle.c via OpenMP"}
+
+    def port(th, budget):
+        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=th)  # warm
+        done, t0 = 0, time.perf_counter()
+        while True:
+            oracle.plan_batch_records(pt, off, tab, rate, bound, threads=th)
+            done += n
+            el = time.perf_counter() - t0
+            if el >= budget:
+                return done / el, done // n, el
+
+    v, reps, el = port(threads, min_seconds)
+    v1, reps1, el1 = port(1, min_seconds / 2)
+    out = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": lscpu_model(),
+           "sample": f"C2 batch of {n} scenarios x 11 services, repeated {reps}x ({el:.1f} s), "
+                     f"oracle/migplan_oracle.c via OpenMP on {threads} threads",
+           "port_1core": {"value": v1, "unit": UNIT, "cores": 1,
+                          "sample": f"C2 batch repeated {reps1}x ({el1:.1f} s) on one thread"}}
+    r1 = ref_python("c2", "--n", 1500, "--procs", 1)
+    ra = ref_python("c2", "--n", n, "--procs", threads)
+    if r1 is not None:
+        out["reference_python_1core"] = {"value": r1.get("scenarios_per_s"), "unit": UNIT, "cores": 1,
+                                         "sample": "first 1500 C2 scenarios (seed 0), configure + relocate + "
+                                                   "optimize per scenario (pipeline.py:95-103)", "raw": r1}
+        out["reference_python_all_cores"] = {"value": ra.get("scenarios_per_s"), "unit": UNIT, "cores": threads,
+                                             "sample": f"full C2 batch ({n} scenarios), fork Pool of {threads} "
+                                                       "over strided chunks", "raw": ra}
+    return out
+
+
+def c5_cpu(fx):
+    """C5 on this host's CPU: the oracle (C port with the reference's
+    cursors, one thread) and the reference itself (migplan, one core)."""
+    import oracle
+    from paper_2409_14447_b200 import workloads as Wm
+    from paper_2409_14447_b200.tables import pack_tables
+    pt = pack_tables(fx.tables)
+    t = pt.index_of()[Wm.C5_MODEL]
+    rates = Wm.c5_rates()
+    k = rates.shape[0]
+    t0 = time.perf_counter()
+    _, res = oracle.plan_scenario(pt, np.full(k, t), rates, np.full(k, Wm.C5_SLO / 2.0), True, 4, gcap=200_000)
+    port_s = time.perf_counter() - t0
+    out = {"port_1core_s": port_s, "port_gpus": len(res["gpus"])}
+    r = ref_python("c5", timeout=900)
+    if r is not None:
+        out["reference_python"] = r
+    return out
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle (C restatement of the reference's
+    planner; the reference itself is pure Python) on all host threads, over
+    the same resident batches in the same order as the repo arm."""
     if rank != 0:
         return
     from paper_2409_14447_b200 import workloads as W
@@ -162,27 +271,47 @@ def run_reference(args, rank, world):
     import oracle
     from paper_2409_14447_b200.tables import pack_tables
     pt = pack_tables(fx.tables)
-    n = 10_000
-    off, tab, rate, bound = c2_inputs(fx, n, 0)
+    n = args.scenarios
+    P = n_resident_batches(n * 11, n)
+    calls = args.warmup + args.steps
+    need = sorted({c % P for c in range(calls)})
+    ins = {p: c2_inputs(fx, n, batch_seed(p)) for p in need}
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
+    for c in range(args.warmup):
+        oracle.plan_batch_records(pt, *ins[c % P], threads=threads)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.plan_batch_records(pt, off, tab, rate, bound, threads=threads)
+    for c in range(args.warmup, calls):
+        oracle.plan_batch_records(pt, *ins[c % P], threads=threads)
     el = time.perf_counter() - t0
     v = n * args.steps / el
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (C2 generator seed 0)",
-            "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios",
-                       "scenarios_per_step": n},
+            "data": "synthetic (C2 generator; the repo arm's resident batches in the same order: batch 0 = seed 0, "
+                    "batch p = seed 1000 + p)",
+            "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU",
+                       "scenarios_per_gpu": n, "input_batches": P},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"full C2 batch ({n} scenarios) per step on {threads} host threads; "
-                                       "the reference itself is pure Python (see DESIGN.md)"},
+                             "cpu_model": lscpu_model(),
+                             "sample": f"one full C2 batch ({n} scenarios) per step on {threads} host threads; "
+                                       "the reference itself is pure Python (its own timing: cpu_baseline."
+                                       "reference_python in the repo arm's line)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def dist_max(dist, torch, world, vals):
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def dist_all(dist, torch, world, ok: bool) -> bool:
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(int(t.item()))
 
 
 def main():
@@ -195,11 +324,16 @@ def main():
                     help="scenarios per GPU per step (weak) or in total (strong)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
-                    help="N > 1: K2 stores its records into every rank's gathered block over peer memory "
-                         "(fused), or one NCCL all-gather per step")
+                    help="N > 1: K2 stores its records into every rank's slot over peer memory (fused), "
+                         "or one NCCL all-gather per step")
+    ap.add_argument("--slots", type=int, default=0,
+                    help="output slots (0: one per timed step up to 64, at least 3)")
+    ap.add_argument("--lag", type=int, default=2,
+                    help="fused gather: step i waits for (and releases) step i - lag's slot")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C3 configurator-sweep measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 / simulator side measurements")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end host-entry measurement")
     ap.add_argument("--sweep-workloads", type=int, default=10_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -224,231 +358,207 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    clk = ClockSampler(local)
 
     from paper_2409_14447_b200 import _native as N
     from paper_2409_14447_b200 import batch as B
-    from paper_2409_14447_b200 import workloads as W
-    from paper_2409_14447_b200.records import PLAN_DTYPE
-
     from paper_2409_14447_b200 import distributed as D
-    from paper_2409_14447_b200.distributed import gather_packed, make_shard, packed_block
-    from paper_2409_14447_b200.records import CFG_TINY, TINY_DTYPE
+    from paper_2409_14447_b200 import workloads as W
+    from paper_2409_14447_b200.records import CFG_TINY, PLAN_DTYPE
 
     fx = W.load_fixtures()
     dt = N.device_tables_for(fx.tables)
     n_global = args.scenarios * (world if args.scaling == "weak" else 1)
-    g_off, g_tab, g_rate, g_bound = c2_inputs(fx, n_global, 0)   # N=1 weak: batch 0 is exactly C2
-    shard = make_shard(g_off, rank, world)
+    g_off, g_tab, _, _ = c2_inputs(fx, n_global, 0)          # every batch has this shape
+    shard = D.make_shard(g_off, rank, world)
     off = shard.off
-    tab = g_tab[shard.svc_a:shard.svc_b]
-    rate = np.ascontiguousarray(g_rate[shard.svc_a:shard.svc_b])
-    bound = np.ascontiguousarray(g_bound[shard.svc_a:shard.svc_b])
+    tab = np.ascontiguousarray(g_tab[shard.svc_a:shard.svc_b])
     n = shard.scen_b - shard.scen_a
     n_svc_local = int(off[-1])
-    # P resident input batches of this shard's shape (batch 0 = the C2 shard
-    # above, the others from the same generator with other seeds), cycled so
-    # that every step reads inputs that are not in L2 (P x ~2.2 MB > 126 MB)
-    per_batch = n_svc_local * 20 + (n + 1) * 4
-    P = int(min(256, max(2, -(-160_000_000 // max(per_batch, 1)))))
+    P = n_resident_batches(n_svc_local, n)
+
+    def shard_inputs(p):
+        _, _, r, b = c2_inputs(fx, n_global, batch_seed(p))
+        return (off, tab, np.ascontiguousarray(r[shard.svc_a:shard.svc_b]),
+                np.ascontiguousarray(b[shard.svc_a:shard.svc_b]))
+
     batches = []
     for p in range(P):
-        if p == 0:
-            b_rate, b_bound = rate, bound
-        else:
-            _, _, r2, b2 = c2_inputs(fx, n_global, 1000 + p)
-            b_rate = np.ascontiguousarray(r2[shard.svc_a:shard.svc_b])
-            b_bound = np.ascontiguousarray(b2[shard.svc_a:shard.svc_b])
-        batches.append((N.to_device(off), N.to_device(tab), N.to_device(b_rate), N.to_device(b_bound)))
+        _, _, r, b = shard_inputs(p)
+        batches.append((N.to_device(off), N.to_device(tab), N.to_device(r), N.to_device(b)))
     stream = torch.cuda.current_stream()
-    # the step's output, at every N: one packed block per rank -- 128-byte plan
-    # records, then 8-byte tiny config records -- which is also the payload of
-    # the step's single all-gather when N > 1.  R blocks rotate: consecutive
-    # steps are overlapped launches (parva_plan_batch_overlapped -- step i+1's
-    # CTAs take SM slots as step i's retire), so no two steps in flight share
-    # a block, and step i+R reuses a block only after its all-gather was read.
-    R = 3
-    ps, cs, blk = packed_block(g_off, world)
-    blocks = [torch.zeros(blk, dtype=torch.uint8, device="cuda") for _ in range(R)]
-    results = [B.BatchResult(bk[ps:ps + 8 * n_svc_local].view(-1, 8), bk[:128 * n].view(-1, 128), n, n_svc_local,
-                             CFG_TINY) for bk in blocks]
-    gathered = [torch.empty(world * blk, dtype=torch.uint8, device="cuda") for _ in range(R)] if world > 1 else None
-    works = [None] * R
-    L = N.lib()
     sh = N.stream_handle(stream)
+    L = N.lib()
 
-    def call_args(p, r):
-        """C-ABI arguments of one step (batch p into block r), built once."""
-        d_off, d_tab, d_rate, d_bound = batches[p]
-        res_r = results[r]
-        return (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n), C.c_int32(n_svc_local), N.ptr(d_off),
-                N.ptr(d_tab), N.ptr(d_rate), N.ptr(d_bound), C.c_int32(1), C.c_int32(4), N.ptr(res_r.cfg),
-                C.c_int32(CFG_TINY), N.ptr(res_r.plan), sh)
-
-    n_calls = max(args.steps, args.warmup)
-    step_args = [call_args(i % P, i % R) for i in range(n_calls)]
-
-    # N > 1, fused: the records go straight into every rank's gathered block
-    # from inside K2 (peer memory mapped by CUDA IPC); the all-gather of a
-    # step is complete when every rank's flag reached its epoch
-    peer = None
+    # output slots: one per timed step (up to 64), so every timed step's
+    # records survive for the parity check; a slot's ticket serializes the
+    # launches that share it
+    S = args.slots if args.slots > 0 else max(3, min(args.steps, 64))
     gather_mode = "none" if world == 1 else args.gather
-    if world > 1 and args.gather == "fused":
+    peer = None
+    if gather_mode == "fused":
         try:
-            peer = D.PeerGather(blk, n_slots=R)
+            lay = D.gather_layout(g_off, world, plan_bytes=64, cfg_bytes=8)
+            peer = D.PeerGather(lay, n_slots=S)
         except Exception as exc:  # noqa: BLE001 -- no peer access: the NCCL collective instead
             print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
             gather_mode = "nccl"
-    mirrors = {}
+    if peer is None:
+        lay = D.gather_layout(g_off, world, plan_bytes=128, cfg_bytes=8)   # = packed_block's layout
+        blocks = [torch.zeros(lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
+        results = [B.BatchResult(bk[lay.ps:lay.ps + 8 * n_svc_local].view(-1, 8),
+                                 bk[:lay.ps].view(-1, 128), n, n_svc_local, CFG_TINY) for bk in blocks]
+        ring = B.SlotRing(S)
+        gathered = ([torch.empty(world * lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
+                    if world > 1 else None)
+        works = [None] * S
+    else:
+        results = [peer.local(s, CFG_TINY) for s in range(S)]
+        gslots = [peer.gather_slot(s, pdl=True) for s in range(S)]
 
-    def mirror_for(i):
-        m = mirrors.pop(i, None)
-        return m if m is not None else peer.mirror(i % R, ps, overlap=True)
+    def base_args(p, res):
+        d_off, d_tab, d_rate, d_bound = batches[p]
+        return (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(n), C.c_int32(n_svc_local),
+                N.ptr(d_off), N.ptr(d_tab), N.ptr(d_rate), N.ptr(d_bound), C.c_int32(1), C.c_int32(4),
+                N.ptr(res.cfg), C.c_int32(CFG_TINY), N.ptr(res.plan))
 
-    def step(i):
-        b = i % R
+    def prepare(c0, c1):
+        """C-ABI arguments of calls [c0, c1) (slot c % S, batch c % P), built
+        before the timed region (tickets and mirrors carry sequential epochs)."""
+        out = []
+        for c in range(c0, c1):
+            s = c % S
+            a = base_args(c % P, results[s])
+            if peer is not None:
+                m = peer.mirror(s, overlap=True)
+                out.append((s, a + (C.byref(m), sh), m))
+            else:
+                t = ring.ticket(s)
+                out.append((s, a + (C.byref(t), sh), t))
+        return out
+
+    unwaited = []
+
+    def launch(item):
+        s, a, _keep = item
         if peer is not None:
-            N.check(L.parva_plan_batch_fused(*step_args[i][:-1], C.byref(mirror_for(i)), sh),
-                    "parva_plan_batch_fused")
+            N.check(L.parva_plan_batch_fused(*a), "parva_plan_batch_fused")
+            unwaited.append(s)
+            while len(unwaited) > args.lag:
+                w = unwaited.pop(0)
+                peer.wait(w, release=True, pdl=True, gslot=gslots[w])
             return
-        if works[b] is not None:
-            works[b].wait()              # step i-R's all-gather has read blocks[b] (a stream wait under NCCL)
-            works[b] = None
-        N.check(L.parva_plan_batch_overlapped(*step_args[i]), "parva_plan_batch_overlapped")
+        if works[s] is not None:
+            works[s].wait()              # the slot's previous all-gather has read it (a stream wait under NCCL)
+            works[s] = None
+        N.check(L.parva_plan_batch_overlapped(*a), "parva_plan_batch_overlapped")
         if world > 1:
-            works[b] = dist.all_gather_into_tensor(gathered[b], blocks[b], async_op=True)
+            works[s] = dist.all_gather_into_tensor(gathered[s], blocks[s], async_op=True)
 
     def drain():
         if peer is not None:
-            peer.wait()                  # every rank's records of the last step have landed here
+            while unwaited:
+                s = unwaited.pop(0)
+                peer.wait(s, release=True, pdl=True, gslot=gslots[s])
             return
-        for b in range(R):
-            if works[b] is not None:
-                works[b].wait()
-                works[b] = None
+        for s in range(S):
+            if works[s] is not None:
+                works[s].wait()
+                works[s] = None
 
-    if peer is not None:
+    # ---- warm-up, then the timed steps
+    if world > 1:
         dist.barrier()                   # every rank's inputs are resident before anyone waits on flags
-    for i in range(args.warmup):
-        step(i)
+    for item in prepare(0, args.warmup):
+        launch(item)
     drain()
     torch.cuda.synchronize()
+    if peer is not None:
+        # did every rank's warm-up records arrive?  If not (no working peer
+        # writes on this box), fail loudly rather than time a broken path
+        ok = dist_all(dist, torch, world, int(peer.status.abs().sum().item()) == 0)
+        if not ok:
+            raise RuntimeError("fused all-gather: peer records did not arrive in the warm-up "
+                               "(run with --gather nccl on a box without peer access)")
+    timed = prepare(args.warmup, args.warmup + args.steps)
     if world > 1:
         dist.barrier()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if peer is not None:
-        # did every rank's warm-up records arrive?  If not (no working peer
-        # writes on this box), time the NCCL collective instead
-        torch.cuda.synchronize()
-        ok = torch.tensor([0 if int(peer.status.item()) else 1], dtype=torch.int32, device="cuda")
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0:
-            print("fused all-gather: peer records did not arrive in the warm-up; using NCCL", file=sys.stderr)
-            peer = None
-            gather_mode = "nccl"
-            for i in range(args.warmup):
-                step(i)
-            drain()
-            torch.cuda.synchronize()
-        else:
-            mirrors = {i: peer.mirror(i % R, ps, overlap=True) for i in range(args.steps)}   # built outside the timing
-        dist.barrier()
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        t_start.record(stream)
-        for i in range(args.steps):
-            step(i)
-        drain()
-        t_stop.record(stream)
-        torch.cuda.synchronize()
-        # keep the GPU busy a little longer so the sampler sees the loaded clocks
-        t_end = time.perf_counter() + 1.0
-        while time.perf_counter() < t_end:
-            for j in range(50):
-                L.parva_plan_batch_overlapped(*step_args[j % len(step_args)])
-            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk.begin()
+    t_start.record(stream)
+    for item in timed:
+        launch(item)
+    drain()
+    t_stop.record(stream)
+    torch.cuda.synchronize()
     step_ms = t_start.elapsed_time(t_stop)
-    # K2's own launch duration (roofline): the same launches one at a time,
-    # each bracketed by events on the launching stream (not overlapped)
+    if peer is not None:
+        peer.check()
+    else:
+        ring.check()
+
+    # ---- parity of every timed step that survives in its slot: every rank
+    # checks its copy of every rank's records against the oracle (digests of
+    # each rank's own shard, computed here and exchanged once)
+    import oracle
+    from paper_2409_14447_b200.records import tiny_config
+    from paper_2409_14447_b200.tables import pack_tables
+    pt = pack_tables(fx.tables)
+    first = max(args.warmup, args.warmup + args.steps - S)
+    checked = list(range(first, args.warmup + args.steps))
+    threads = max(1, (os.cpu_count() or 1) // world)
+    own = {}
+    for c in checked:
+        p = c % P
+        if p not in own:
+            ocfg, oplan = oracle.plan_batch_records(pt, *shard_inputs(p), threads=threads)
+            own[p] = digest(tiny_config(ocfg).tobytes(), oplan.tobytes())
+    if world > 1:
+        every = [None] * world
+        dist.all_gather_object(every, own)
+    else:
+        every = [own]
+    ok = True
+    for c in checked:
+        s, p = c % S, c % P
+        if world == 1:
+            cfg, plan = results[s].host()
+            ok = ok and digest(cfg.tobytes(), plan.tobytes()) == every[0][p]
+            continue
+        if peer is not None:
+            rows = peer.slot_view(s).view(world, lay.blk).cpu().numpy()
+        else:
+            rows = gathered[s].view(world, lay.blk).cpu().numpy()
+        cfg, plan = D.decode_gathered(rows, lay)
+        for r, ((a, b), (sa, sb)) in enumerate(zip(lay.spans, lay.svc_spans)):
+            ok = ok and digest(cfg[sa:sb].tobytes(), plan[a:b].tobytes()) == every[r][p]
+    parity = dist_all(dist, torch, world, ok)
+    parity_info = {"equal": parity, "steps_checked": len(checked), "ranks": world,
+                   "scope": ("every rank's gathered copy of every rank's config + plan records of each timed step"
+                             if world > 1 else "the config + plan records of each timed step"),
+                   "checker": "oracle/migplan_oracle.c (C restatement of the reference), sha256 digests"}
+
+    # ---- K2's own launch duration (roofline): the timed batches one launch
+    # at a time into a scratch output, each bracketed by events on the
+    # launching stream (not overlapped)
+    scratch = B.BatchResult(torch.empty((n_svc_local, 8), dtype=torch.uint8, device="cuda"),
+                            torch.empty((n, 128), dtype=torch.uint8, device="cuda"), n, n_svc_local, CFG_TINY)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         kev[i][0].record(stream)
-        N.check(L.parva_plan_batch(*step_args[i]), "parva_plan_batch")
+        N.check(L.parva_plan_batch(*base_args((args.warmup + i) % P, scratch), sh), "parva_plan_batch")
         kev[i][1].record(stream)
     torch.cuda.synchronize()
     kern_ms = sum(a.elapsed_time(b) for a, b in kev)
-    t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms, kern_ms = float(t[0]), float(t[1])
-    if peer is not None:
-        peer.check()
-        peer.close()
-    # batch 0 once more into block 0, for the parity check and the e2e comparison
-    res = results[0]
-    B.plan_batch(dt, *batches[0], cfg_format=CFG_TINY, out=res)
-    torch.cuda.synchronize()
-
-    # parity spot check of what was timed (oracle = test infrastructure, checker only)
-    parity = None
-    if rank == 0:
-        import oracle
-        from paper_2409_14447_b200.tables import pack_tables
-        plan = N.records_to_numpy(res.plan, n, PLAN_DTYPE)
-        cfg = res.cfg.cpu().numpy().reshape(-1).view(TINY_DTYPE)
-        k = min(n, 2000)
-        ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off[:k + 1], tab[:off[k]],
-                                                      rate[:off[k]], bound[:off[k]])
-        from paper_2409_14447_b200.records import tiny_config
-        parity = bool(cfg[:off[k]].tobytes() == tiny_config(ocfg).tobytes() and plan[:k].tobytes() == oplan.tobytes())
-
-    # ---- e2e through the host-buffer C ABI: parva_plan_host_mapped with pinned
-    # host blocks (inputs packed once by the producer, outside the timed loop).
-    # Every timed call streams the 2 MB input block over PCIe into the GPU
-    # (loader warps, in order), plans, writes config + plan records (freed_rate
-    # ledger included) straight into the pinned output block, and synchronizes.
-    # Steps are pipelined E2E_DEPTH deep (submit / wait, one scratch and
-    # output block per slot): step i+1's input streams while step i finishes
-    # planning; the host waits for every step's completion word.
-    E2E_DEPTH = 4
-    mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, depth=E2E_DEPTH)
-
-    def e2e_steps(k):
-        for i in range(k):
-            mb.submit(dt, i % E2E_DEPTH)
-            if i >= E2E_DEPTH - 1:
-                mb.wait((i - E2E_DEPTH + 1) % E2E_DEPTH)
-        for i in range(max(0, k - E2E_DEPTH + 1), k):
-            mb.wait(i % E2E_DEPTH)
-
-    e2e_steps(max(args.warmup, E2E_DEPTH))
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    e2e_steps(args.steps)
-    e2e_s = time.perf_counter() - t0
-    dev_plan = N.records_to_numpy(res.plan, n, PLAN_DTYPE)
-    e2e_parity = all(mb.outputs(s)[1].tobytes() == dev_plan.tobytes() for s in range(E2E_DEPTH))
-    # one synchronous call per step (launch + stream synchronize), reported beside it
-    for _ in range(args.warmup):
-        mb.run(dt)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        mb.run(dt)
-    sync_s = time.perf_counter() - t0
-    e2e_parity = e2e_parity and mb.outputs(0)[1].tobytes() == dev_plan.tobytes()
-    te = torch.tensor([e2e_s, sync_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s, sync_s = float(te[0]), float(te[1])
-    # the staged-copy alternative (3-chunk H2D / plan / D2H CUDA-graph pipeline), reported beside it
-    pb = B.PackedHostBatch(off, tab, rate, bound, n_chunks=3, cfg_format=2, plan_bytes=64)
-    for _ in range(args.warmup):
-        pb.run(dt)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pb.run(dt)
-    copy_s = time.perf_counter() - t0
-    copy_parity = bool(pb.outputs()[1].tobytes() == dev_plan.tobytes())
+    # keep the GPU busy a little longer so the sampler sees the loaded clocks
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        for j in range(50):
+            L.parva_plan_batch(*base_args(j % P, scratch), sh)
+        torch.cuda.synchronize()
+    clk.end()
+    step_ms, kern_ms = dist_max(dist, torch, world, [step_ms, kern_ms])
 
     n_svc = int(off[-1])
     hbm, peak_src = peaks()
@@ -459,71 +569,154 @@ def main():
     kern_s = kern_ms / 1000.0 / args.steps
     achieved = bytes_per_launch / kern_s / 1e9
     value = n_global * args.steps / (step_ms / 1000.0)
+    if gather_mode == "fused":
+        par = (" + fused all-gather: K2 stores each tile's 64-B plan + 8-B config records (full records of "
+               "spilled scenarios in an overflow section) into every rank's slot over peer memory; per step one "
+               f"exact-epoch wait + release of step i-{args.lag}'s slot")
+    elif gather_mode == "nccl":
+        par = " + one NCCL all-gather of the packed 128-B plan + 8-B config records per step"
+    else:
+        par = ""
+    launches_per_step = 2 if gather_mode == "fused" else 1
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY C2 generator: batch 0 is C2 seed 0, the other resident batches seeds 1001.., sharded contiguously; fixture tables rendered from the reference)",
+        "data": "synthetic (SURVEY C2 generator: batch 0 is C2 seed 0, the other resident batches seeds 1001.., "
+                "sharded contiguously; fixture tables rendered from the reference)",
         "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU"
                                if args.scaling == "weak" else f"C2/C4 generator, {n_global} scenarios total",
                    "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n_global,
                    "l2": "not reused: steps cycle through resident input batches larger than L2 in total",
-                   "input_batches": P,
-                   "launch": "parva_plan_batch_overlapped per step (programmatic dependent launches, 3 rotating "
-                             "output blocks); kernel_ms_per_step from separate one-at-a-time launches",
-                   "parallelism": f"scenario-sharded x{world}" + (
-                       " + all-gather of the packed plan + tiny config records every step: "
-                       + ("fused into K2 (records stored into every rank's gathered block over peer memory, "
-                          "completion flags per rank)" if gather_mode == "fused" else
-                          "one NCCL all-gather, overlapped with the next steps' planning")
-                       if world > 1 else ""),
-                   "gather": gather_mode,
-                   "optimize": True, "threshold": 4},
-        "gpu_launches": args.steps,
+                   "input_batches": P, "output_slots": S,
+                   "launch": "parva_plan_batch_overlapped / _fused per step (programmatic dependent launches; "
+                             "slot tickets serialize launches sharing an output slot); kernel_ms_per_step from "
+                             "separate one-at-a-time launches",
+                   "parallelism": f"scenario-sharded x{world}" + par,
+                   "gather": gather_mode, "optimize": True, "threshold": 4},
+        "gpu_launches": args.steps * launches_per_step,
         "kernel_ms_per_step": kern_ms / args.steps,
-        "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel (fused configure + relocate + optimize)", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("plan_batch_kernel"),
+        "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel (fused configure + relocate + optimize)",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": ncu_traffic("plan_batch_kernel"),
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write per launch)",
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_launch,
                      "note": "issue/latency-bound sequential allocator; HBM fraction reported, not targeted"},
-        "e2e": {"value": n_global * args.steps / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": mb.h2d_bytes, "d2h_bytes_per_step": mb.d2h_bytes,
-                "api": "parva_plan_host_mapped_submit / _wait (C ABI): one launch per step, pipelined "
-                       f"{E2E_DEPTH} deep (programmatic dependent launches: the next step's input streams while "
-                       "this one finishes planning; the host waits for every step's completion word); loader "
-                       "warps stream the pinned input block over PCIe in order while the other warps plan each "
-                       "scenario as its chunk lands and write 8-B config + 64-B plan records (freed_rate ledger "
-                       "included; full records of overflowing scenarios in an overflow area) straight into the "
-                       "step's pinned output block",
-                "pipeline_depth": E2E_DEPTH,
-                "plan_records_equal_device_path": e2e_parity,
-                "synchronous": {"value": n_global * args.steps / sync_s, "unit": UNIT,
-                                "api": "parva_plan_host_mapped: one launch + stream synchronize per step"},
-                "copy_pipeline": {"value": n_global * args.steps / copy_s, "unit": UNIT,
-                                  "api": "parva_plan_host_packed: 3-chunk H2D / plan / D2H CUDA-graph pipeline",
-                                  "plan_records_equal_device_path": copy_parity}},
-        "parity_vs_oracle_first_2000": parity,
+        "parity_timed_steps": parity_info,
     }
     clk_summary = clk.summary()
     line["clocks"] = clk_summary
     line["roofline"]["issue"] = issue_roofline("plan_batch_kernel", kern_s, clk_summary.get("sm_mhz"))
     line["roofline"]["issue_overlapped"] = issue_roofline("plan_batch_kernel", step_ms / 1000.0 / args.steps,
                                                           clk_summary.get("sm_mhz"))
+    if peer is not None:
+        peer.close()
 
-    # ---- C3 configurator sweep (HBM-roofline kernel), rank 0
-    if not args.no_sweep and rank == 0:
-        line["configurator_sweep"] = sweep_measure(args, torch, N, B, W, hbm, peak_src, local)
-    if not args.no_extra and rank == 0:
-        line["large_cluster"] = c5_measure(torch, fx)
-        line["simulation"] = sim_measure(torch, fx)
-        line["c4_single_gpu"] = c4_measure(torch, N, B, W, fx, dt, local)
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_global, pt)
+    if not args.no_sweep:
+        line["configurator_sweep"] = sweep_measure(args, torch, dist, world, rank, N, B, W, hbm, peak_src)
+    if not args.no_extra:
+        if world > 1:
+            line["c4_sharded"] = c4_sharded_measure(torch, dist, world, rank, N, B, D, fx, dt)
+        elif rank == 0:
+            line["c4_single_gpu"] = c4_measure(torch, N, B, W, fx, dt, local)
+        if rank == 0:
+            line["large_cluster"] = c5_measure(torch, fx)
+            line["simulation"] = sim_measure(torch, fx)
     if not args.no_cpu and rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_baseline_c2(fx, n)
+        line["cpu_baseline"] = cpu_baselines(fx, n)
+        if "large_cluster" in line:
+            line["large_cluster"]["cpu"] = c5_cpu(fx)
+    clk.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_global, pt):
+    """End to end through the C ABI, starting every step from a caller's
+    plain host arrays (scenario offsets, int32 table ids, f64 rates and
+    bounds in pageable numpy memory; 8 different C2 batches in rotation).
+    Per step: pack the batch into a pinned input block on the library's host
+    threads (parva_stream_pack_arrays), submit one K2s launch
+    (parva_plan_host_mapped_submit) that streams the block over PCIe and
+    writes its config + plan records (ledger included) into pinned host
+    memory; E2E_DEPTH steps in flight, the host waits for every step's
+    completion word (parva_plan_host_mapped_wait) before reusing its slot.
+    The packing of step i overlaps the GPU work of steps i-3..i-1.  Reported
+    beside it: the same pipeline with inputs packed once outside the loop
+    (prepacked), and one synchronous call per step."""
+    import oracle
+    from paper_2409_14447_b200.records import tiny_config
+    E2E_DEPTH, E2E_BATCHES = 4, 8
+    host = [shard_inputs(p) for p in range(E2E_BATCHES)]      # the caller's arrays (pageable)
+    off = host[0][0]
+    n = len(off) - 1
+    mb = B.MappedHostBatch(*host[0], cfg_format=2, plan_bytes=64, depth=E2E_DEPTH)
+    pack_s = []
+
+    def steps(c0, k, pack=True):
+        for i in range(c0, c0 + k):
+            slot = i % E2E_DEPTH
+            mb.wait(slot)                    # step i - depth has finished with this slot's blocks
+            if pack:
+                t = time.perf_counter()
+                mb.fill(*host[i % E2E_BATCHES], slot=slot)
+                pack_s.append(time.perf_counter() - t)
+            mb.submit(dt, slot)
+        for slot in range(E2E_DEPTH):
+            mb.wait(slot)
+
+    steps(0, max(args.warmup, E2E_DEPTH))
+    pack_s.clear()
+    if world > 1:
+        dist.barrier()
+    c0 = max(args.warmup, E2E_DEPTH)
+    t0 = time.perf_counter()
+    steps(c0, args.steps)
+    e2e_s = time.perf_counter() - t0
+    h2d = mb.h2d_bytes
+    # the last E2E_DEPTH steps' records against the oracle
+    ok = True
+    for i in range(c0 + args.steps - E2E_DEPTH, c0 + args.steps):
+        ocfg, oplan = oracle.plan_batch_records(pt, *host[i % E2E_BATCHES])
+        cfg, plan = mb.outputs(i % E2E_DEPTH)
+        ok = ok and plan.tobytes() == oplan.tobytes() and cfg.tobytes() == tiny_config(ocfg).tobytes()
+    # the same pipeline with the inputs packed outside the loop (one batch per slot)
+    for slot in range(E2E_DEPTH):
+        mb.fill(*host[slot], slot=slot)
+    steps(0, args.warmup, pack=False)
+    t0 = time.perf_counter()
+    steps(0, args.steps, pack=False)
+    pre_s = time.perf_counter() - t0
+    # one synchronous call per step (pack + launch + stream synchronize)
+    for i in range(args.warmup):
+        mb.fill(*host[i % E2E_BATCHES], slot=0)
+        mb.run(dt)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        mb.fill(*host[i % E2E_BATCHES], slot=0)
+        mb.run(dt)
+    sync_s = time.perf_counter() - t0
+    ok = dist_all(dist, torch, world, ok)
+    e2e_s, pre_s, sync_s = dist_max(dist, torch, world, [e2e_s, pre_s, sync_s])
+    K = n_global * args.steps
+    return {"value": K / e2e_s, "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": mb.d2h_bytes,
+            "api": "per step: parva_stream_pack_arrays (plain host arrays -> pinned streamed block, host threads) + "
+                   "parva_plan_host_mapped_submit; parva_plan_host_mapped_wait before a slot is reused",
+            "inputs": f"{E2E_BATCHES} different C2 batches in rotation, plain pageable numpy arrays "
+                      "(int32 offsets and table ids, f64 rates and bounds)",
+            "pipeline_depth": E2E_DEPTH,
+            "host_pack_us_per_step_median": statistics.median(pack_s) * 1e6 if pack_s else None,
+            "records_equal_oracle_last_steps": ok,
+            "prepacked": {"value": K / pre_s, "unit": UNIT,
+                          "api": "the same pipeline with every slot's input block packed once outside the loop"},
+            "synchronous": {"value": K / sync_s, "unit": UNIT,
+                            "api": "pack + parva_plan_host_mapped (one launch + stream synchronize) per step"}}
 
 
 def sim_measure(torch, fx, runs=256, horizon=10.0):
@@ -598,12 +791,11 @@ def c5_measure(torch, fx):
     return {"workload": "C5: 49,612 densenet121 services, 100,002 segments, one allocation",
             "gpus_before_optimize": out.n_gpus_unopt, "gpus": int(len(out.gpu_id)),
             "ms_wall_incl_transfers": min(m[0] for m in ms), "ms_stream": min(m[1] for m in ms),
-            "reference_python_s": 75.1, "note": "reference relocate 73.8 s + optimize 1.3 s measured in the "
-                                                "build container (tests/golden/c5_summary.json)"}
+            "note": "CPU times on this host in large_cluster.cpu (cpu leg)"}
 
 
 def c4_measure(torch, N, B, W, fx, dt, local):
-    """C4 on one GPU: 10^6 scenarios in one fused launch pair (strong-scaling unit)."""
+    """C4 on one GPU: 10^6 scenarios in one K2 launch (the strong-scaling unit)."""
     n = 1_000_000
     off, tab, rate, bound = c2_inputs(fx, n, 1)
     d = [N.to_device(a) for a in (off, tab, rate, bound)]
@@ -623,48 +815,160 @@ def c4_measure(torch, N, B, W, fx, dt, local):
             "value": n / (ms / 1000.0), "unit": UNIT, "l2": "inputs 17.6 MB + outputs 480 MB exceed L2 reuse"}
 
 
-def sweep_measure(args, torch, N, B, W, hbm, peak_src, local):
+def c4_sharded_measure(torch, dist, world, rank, N, B, D, fx, dt, reps=5):
+    """C4 strong-scaled (BASELINE configs[3]): 10^6 scenarios sharded
+    contiguously across the ranks; the step is done when every rank holds
+    every rank's records.  Reported: this shard's K2 alone (compute), one
+    NCCL all-gather of the packed 128-B records (collective only), and the
+    fused K2 + peer-store all-gather with 64-B records + one exact-epoch wait
+    (the product path); each the median of `reps`, max over ranks.  Every
+    rank checks its gathered copy against the oracle (digests per shard)."""
+    import oracle
+    from paper_2409_14447_b200.records import CFG_TINY, tiny_config
+    from paper_2409_14447_b200.tables import pack_tables
+    n = 1_000_000
+    off, tab, rate, bound = c2_inputs(fx, n, 1)
+    sh = D.make_shard(off, rank, world)
+    ins = (sh.off, tab[sh.svc_a:sh.svc_b], rate[sh.svc_a:sh.svc_b], bound[sh.svc_a:sh.svc_b])
+    d = [N.to_device(np.ascontiguousarray(a)) for a in ins]
+    k, m = sh.scen_b - sh.scen_a, sh.svc_b - sh.svc_a
+    s = torch.cuda.current_stream()
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[len(ts) // 2]
+
+    lay128 = D.gather_layout(off, world, plan_bytes=128, cfg_bytes=8)
+    blk = torch.zeros(lay128.blk, dtype=torch.uint8, device="cuda")
+    res = B.BatchResult(blk[lay128.ps:lay128.ps + 8 * m].view(-1, 8), blk[:lay128.ps].view(-1, 128), k, m, CFG_TINY)
+    gat = torch.empty(world * lay128.blk, dtype=torch.uint8, device="cuda")
+    ms_compute = timed(lambda: B.plan_batch(dt, *d, cfg_format=CFG_TINY, out=res))
+    ms_nccl = timed(lambda: dist.all_gather_into_tensor(gat, blk))
+    lay = D.gather_layout(off, world, plan_bytes=64, cfg_bytes=8)
+    pg = D.PeerGather(lay, n_slots=2)
+    state = {"i": 0}
+
+    def fused():
+        slot = state["i"] % 2
+        state["i"] += 1
+        B.plan_batch(dt, *d, cfg_format=CFG_TINY, out=pg.local(slot, CFG_TINY), mirror=pg.mirror(slot))
+        pg.wait(slot, release=True)
+
+    fused()
+    ms_fused = timed(fused)
+    torch.cuda.synchronize()
+    pg.check()
+    last = (state["i"] - 1) % 2
+    ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), *ins, threads=max(1, (os.cpu_count() or 1) // world))
+    mine = digest(tiny_config(ocfg).tobytes(), oplan.tobytes())
+    every = [None] * world
+    dist.all_gather_object(every, mine)
+    cfg, plan = pg.records(last)
+    ok = all(digest(cfg[sa:sb].tobytes(), plan[a:b].tobytes()) == every[r]
+             for r, ((a, b), (sa, sb)) in enumerate(zip(lay.spans, lay.svc_spans)))
+    ok = dist_all(dist, torch, world, ok)
+    pg.close()
+    ms_compute, ms_nccl, ms_fused = dist_max(dist, torch, world, [ms_compute, ms_nccl, ms_fused])
+    return {"workload": f"C4 generator (seed 1), 10^6 scenarios x 11 services sharded over {world} GPUs (strong)",
+            "scenarios": n, "scenarios_per_gpu": k, "value": n / (ms_fused / 1000.0), "unit": UNIT,
+            "ms_fused_plan_and_gather": ms_fused, "ms_compute_only": ms_compute,
+            "ms_nccl_allgather_only": ms_nccl,
+            "gathered_bytes_per_scenario": {"fused": 64 + 8 * 11, "nccl": 128 + 8 * 11},
+            "value_compute_plus_nccl": n / ((ms_compute + ms_nccl) / 1000.0),
+            "parity_gathered": ok, "timing": "median of 5 after a barrier, CUDA events, max over ranks"}
+
+
+def sweep_measure(args, torch, dist, world, rank, N, B, W, hbm, peak_src):
+    """C3 configurator sweep (K1, the HBM-roofline kernel).  N > 1: the 10^4
+    workloads shard contiguously (each rank generates and sweeps only its
+    tables), then ONE all-gather of the 32-B config records; every rank
+    checks the gathered records of every shard (digests vs the oracle on a
+    sample of each shard)."""
+    import oracle
+    from paper_2409_14447_b200 import distributed as D
     from paper_2409_14447_b200.tables import pack_dense
     nw = args.sweep_workloads
+    a, b = D.shard_bounds(nw, rank, world)
     t0 = time.perf_counter()
-    dth = W.dense_tables(nw, seed=3)
+    dth = W.dense_tables(b - a, seed=3, first=a)
     gen_s = time.perf_counter() - t0
     pt = pack_dense(dth)
     dt = N.DeviceTables(pt, build_index=False)
-    q_table = N.to_device(np.arange(nw, dtype=np.int32))
+    nl = b - a
+    q_table = N.to_device(np.arange(nl, dtype=np.int32))
     q_rate = N.to_device(dth.rate)
     q_bound = N.to_device(dth.slo / 2.0)
-    out = B.configure_sweep(dt, q_table, q_rate, q_bound)
+    max_l = max(y - x for x, y in (D.shard_bounds(nw, r, world) for r in range(world)))
+    out = torch.zeros((max_l, 32), dtype=torch.uint8, device="cuda")
+    B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
     steps = max(10, min(args.steps, 50))
     for _ in range(5):
         B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     s = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    with ClockSampler(local) as clk:
-        for i in range(steps):
-            ev[i][0].record(s)
-            B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
-            ev[i][1].record(s)
-        torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    for i in range(steps):
+        ev[i][0].record(s)
+        B.configure_sweep(dt, q_table, q_rate, q_bound, out=out)
+        ev[i][1].record(s)
+    torch.cuda.synchronize()
+    ms = sum(x.elapsed_time(y) for x, y in ev) / steps
     points = pt.n_points
-    alg = points * 16 + nw * (4 + 8 + 8) + nw * 32
+    alg = points * 16 + nl * (4 + 8 + 8) + nl * 32
     achieved = alg / (ms / 1000.0) / 1e9
-    import oracle
-    recs = N.records_to_numpy(out, nw, N.CONFIG_DTYPE)
-    k = min(nw, 1000)
+    k = min(nl, 1000)
+    recs = N.records_to_numpy(out, nl, N.CONFIG_DTYPE)
     orec = oracle.configure_batch(pt, np.arange(k), dth.rate[:k], dth.slo[:k] / 2.0)
-    return {"workload": "C3: 10^4 dense tables (5 sizes x batch 1-128 x procs 1-8), 1 query each",
-            "workloads": nw, "points": points, "ms_per_launch": ms, "value": nw / (ms / 1000.0),
+    local_ok = bool(recs[:k].tobytes() == orec.tobytes())
+    line = {"workload": "C3: 10^4 dense tables (5 sizes x batch 1-128 x procs 1-8), 1 query each",
+            "workloads": nw, "points": points, "ms_per_launch": ms, "value": nw / (ms / 1000.0) if world == 1 else None,
             "unit": "workloads/s", "points_per_s": points / (ms / 1000.0),
             "roofline": {"bound": "hbm", "kernel": "configure_sweep_kernel", "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("configure_sweep_kernel"),
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg},
-            "parity_vs_oracle_first_1000": bool(recs[:k].tobytes() == orec.tobytes()),
-            "l2": "no flush: the 760 MB of profile points per launch exceed the 126 MB L2",
-            "generation_s": gen_s, "clocks": clk.summary()}
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": alg},
+            "parity_vs_oracle_first_1000": local_ok,
+            "l2": "no flush: the profile points per launch exceed the 126 MB L2",
+            "generation_s": gen_s}
+    if world == 1:
+        return line
+    # one all-gather of the config records (padded to the largest shard)
+    gat = torch.empty((world * max_l, 32), dtype=torch.uint8, device="cuda")
+    gts = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        dist.barrier()
+        x, y = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x.record(s)
+        dist.all_gather_into_tensor(gat, out)
+        y.record(s)
+        torch.cuda.synchronize()
+        gts.append(x.elapsed_time(y))
+    ms_g = sorted(gts)[2]
+    mine = hashlib.sha256(recs[:k].tobytes()).hexdigest() if local_ok else "local-mismatch"
+    every = [None] * world
+    dist.all_gather_object(every, mine)
+    rows = gat.view(world, max_l, 32).cpu().numpy()
+    ok = all(hashlib.sha256(rows[r, :min(1000, y - x)].tobytes()).hexdigest() == every[r]
+             for r, (x, y) in enumerate(D.shard_bounds(nw, r2, world) for r2 in range(world)))
+    ok = dist_all(dist, torch, world, ok)
+    ms_max, ms_g, frac_min = dist_max(dist, torch, world, [ms, ms_g, -achieved / hbm])
+    line.update({"value": nw / ((ms_max + ms_g) / 1000.0), "ms_sweep_max_over_ranks": ms_max,
+                 "ms_allgather_config_records": ms_g, "workloads_per_gpu": nl,
+                 "roofline_frac_min_over_ranks": -frac_min, "parity_gathered_sample": ok,
+                 "note": "value = all workloads / (slowest rank's sweep + one NCCL all-gather of 32-B records)"})
+    return line
 
 
 if __name__ == "__main__":

@@ -215,42 +215,73 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index,
                      void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
                      void* stream);
 
+/* Output-slot ticket of an overlapped launch.  A caller that keeps several
+ * launches in flight rotates their outputs over slots; each slot owns two
+ * u32 words of device memory (d_words, zeroed before first use: the epoch of
+ * the slot's last completed launch, and a CTA counter).  Every CTA of a
+ * launch waits, before its first store, until d_words[0] == prev_epoch (the
+ * slot's previous launch has completed); the launch's last CTA publishes
+ * `epoch` there.  So launches into one slot never overlap, however many
+ * grids are in flight, and consecutive slots still overlap freely.  A wait
+ * longer than 60 s (environment PARVA_TICKET_TIMEOUT_MS overrides) stores
+ * PARVA_LAUNCH_ERROR into *d_err (if non-NULL) and the CTA stores nothing
+ * (no hang). */
+typedef struct {
+  uint32_t* d_words;     /* [2] per slot, device memory                      */
+  uint32_t prev_epoch;   /* epoch of the slot's previous launch, 0 = first   */
+  uint32_t epoch;        /* this launch's epoch: nonzero, != prev_epoch      */
+  int32_t* d_err;        /* optional error word (device)                     */
+} parva_slot_ticket;
+
 /* parva_plan_batch as a programmatic dependent launch: it may start while
  * the previous call on `stream` is still planning its last scenarios (its
  * CTAs take SM slots as the predecessor's retire), so back-to-back batches
- * leave no idle tail.  The caller guarantees that no call still in flight
- * writes anything this call reads or writes (rotate output buffers). */
+ * leave no idle tail.  `ticket` (required) serializes launches that share
+ * an output slot: d_cfg / d_plan belong to the ticket's slot.  Inputs must
+ * stay unmodified until the launch completes. */
 int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* index,
                                 int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,
                                 const int32_t* d_svc_table, const double* d_svc_rate,
                                 const double* d_svc_bound, int32_t optimize, int32_t threshold,
                                 void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
-                                void* stream);
+                                const parva_slot_ticket* ticket, void* stream);
 
-/* Fused all-gather for the sharded device path (one process per GPU):
- * parva_plan_batch that also stores every plan / config record into this
- * rank's slot of every rank's gathered block over peer memory (NVLink P2P
- * stores from inside K2, tile by tile, so the transfer overlaps the
- * planning), then, after
- * a system-scope fence, stores `epoch` into this rank's flag word on every
- * rank.  plan[m] / cfg[m]: where this rank's records go on rank m (device
- * pointers valid in this process: parva_ipc_open of rank m's block plus the
- * slot offset; m = this rank is the local block).  d_done: a zeroed u32 the
- * launch uses as its CTA counter (one per launch in flight).  overlap: launch
- * as a programmatic dependent launch (parva_plan_batch_overlapped).
- * parva_gather_wait makes `stream` wait until every rank's flag word in
- * d_flags (this rank's flag array) has reached `epoch` (status set to
- * PARVA_LAUNCH_ERROR after timeout_ns instead of waiting forever).
- * Replaces plan_services per scenario plus the NCCL all-gather of the
- * per-scenario plans. */
+/* Fused all-gather for the sharded device path (one process per GPU,
+ * SURVEY §8e; replaces plan_services per scenario plus the NCCL all-gather
+ * of the per-scenario plans).  Every rank owns one gathered buffer with
+ * n_slots slots; slot s holds every rank's [plan | config | overflow]
+ * sections and, in a header, a flag row (rank r's last landed epoch of the
+ * slot) and an ack row (rank r's last released epoch of the slot).
+ * parva_plan_batch_fused plans this rank's shard and, tile by tile while the
+ * other CTAs keep planning, stores the tile's records into this rank's
+ * sections of the slot on every rank (NVLink P2P stores into buffers mapped
+ * by CUDA IPC).  With plan_bytes == 64 the records are 64-byte plan records
+ * (the 128-byte record truncated to 56 payload bytes; a scenario whose
+ * payload does not fit has status PARVA_SPILLED and its full record at the
+ * same index of the overflow section) -- 152 B per C2 scenario on the wire
+ * instead of 216.  Before its first store every CTA waits for the slot's
+ * ticket (this rank's previous launch into the slot has completed) and for
+ * every rank's release of the slot's previous epoch (d_acks[m] >=
+ * ticket.prev_epoch); after a system-scope fence the last CTA stores the
+ * epoch into this rank's flag word of the slot on every rank.  The call is
+ * rejected (PARVA_BAD_INPUT) when the records would not fit the sections
+ * (n_scenarios * plan_bytes > plan_capacity, n_services * config record
+ * bytes > cfg_capacity, or n_scenarios * 128 > spill_capacity). */
 typedef struct {
-  int32_t n;
-  int32_t overlap;
-  void* plan[8];
-  void* cfg[8];
-  uint32_t* flag[8];
-  uint32_t* d_done;
-  uint32_t epoch;
+  int32_t n;               /* ranks, 1..8                                      */
+  int32_t overlap;         /* launch as a programmatic dependent launch        */
+  void* plan[8];           /* this rank's plan section of the slot on rank m  */
+  void* cfg[8];            /* its config section                               */
+  void* spill[8];          /* its overflow section (plan_bytes == 64)          */
+  uint32_t* flag[8];       /* this rank's flag word of the slot on rank m      */
+  const uint32_t* d_acks;  /* the slot's ack row in this rank's buffer [n]     */
+  void* d_spill;           /* local overflow records (plan_bytes == 64)        */
+  int64_t plan_capacity;   /* bytes of one rank's plan section                 */
+  int64_t cfg_capacity;    /* bytes of one rank's config section               */
+  int64_t spill_capacity;  /* bytes of one rank's overflow section             */
+  int32_t plan_bytes;      /* 128, or 64 (overflow section used)               */
+  int32_t reserved;
+  parva_slot_ticket ticket;
 } parva_mirror;
 int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
                            int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,
@@ -258,8 +289,26 @@ int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
                            const double* d_svc_bound, int32_t optimize, int32_t threshold,
                            void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
                            const parva_mirror* mirror, void* stream);
-int parva_gather_wait(const uint32_t* d_flags, int32_t n, uint32_t epoch, int64_t timeout_ns,
+
+/* Consumer side of one slot: make `stream` wait until every rank's flag word
+ * in d_flags equals `epoch` exactly (an epoch that was already overwritten
+ * is an error, never stale data), then, if `release`, store `epoch` into
+ * this rank's ack word of the slot on every rank (ack[m]) so producers may
+ * reuse the slot -- release only when nothing later on the stream reads the
+ * slot, else call parva_gather_release after the last reader.  A wait
+ * longer than timeout_ns stores PARVA_LAUNCH_ERROR into *d_status and
+ * releases nothing (producers then time out too: no hang).  pdl: launch as
+ * a programmatic dependent launch (it may start while the previous kernel
+ * on the stream runs; a later launch still waits for it to finish). */
+typedef struct {
+  int32_t n;               /* ranks, 1..8                                      */
+  int32_t pdl;
+  const uint32_t* d_flags; /* the slot's flag row in this rank's buffer [n]   */
+  uint32_t* ack[8];        /* this rank's ack word of the slot on rank m      */
+} parva_gather_slot;
+int parva_gather_wait(const parva_gather_slot* slot, uint32_t epoch, int32_t release, int64_t timeout_ns,
                       int32_t* d_status, void* stream);
+int parva_gather_release(const parva_gather_slot* slot, uint32_t epoch, void* stream);
 /* CUDA IPC plumbing for the gathered blocks: an exportable zeroed device
  * allocation, its handle (parva_ipc_handle_bytes() bytes), and the mapping
  * of a peer's handle into this process (peer access enabled lazily). */
@@ -359,6 +408,15 @@ int64_t parva_stream_bytes(int32_t n_scenarios, const int32_t* h_scen_off, int32
 int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const uint16_t* h_table,
                           const double* h_rate, const double* h_bound, int32_t chunk_scen,
                           void* h_block, int64_t capacity);
+
+/* parva_stream_pack from the plain arrays a caller of parva_plan_host holds
+ * (int32 table ids; ids outside [0, 65535) become 0xFFFF, i.e. no table:
+ * PARVA_BAD_INPUT for that service), on up to n_threads host threads (0 =
+ * all; PARVA_PACK_THREADS caps the pool).  Returns the bytes written, or -1
+ * (bad offsets, capacity too small). */
+int64_t parva_stream_pack_arrays(int32_t n_scenarios, const int32_t* h_scen_off, const int32_t* h_table,
+                                 const double* h_rate, const double* h_bound, int32_t chunk_scen,
+                                 void* h_block, int64_t capacity, int32_t n_threads);
 
 /* Zero-copy host entry (the end-to-end path; one batch, one launch).  The
  * input block (streamed layout, parva_stream_pack) and the output block

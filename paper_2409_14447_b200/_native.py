@@ -74,21 +74,36 @@ class SimResult(C.Structure):
 EXPORTS = (
     "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
     "parva_plan_batch", "parva_plan_batch_overlapped", "parva_plan_batch_fused", "parva_gather_wait",
+    "parva_gather_release",
     "parva_ipc_alloc", "parva_ipc_free", "parva_ipc_handle_bytes", "parva_ipc_handle", "parva_ipc_open",
     "parva_ipc_close", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",
     "parva_match_demand_lists", "parva_propose_small_batch", "parva_packed_layout",
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
-    "parva_stream_pack", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
+    "parva_stream_pack", "parva_stream_pack_arrays", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
     "parva_simulate", "parva_sim_seed_states", "parva_sim_log1p", "parva_sim_exponential",
 )
+
+
+class SlotTicket(C.Structure):
+    """parva_slot_ticket (include/parva_b200.h): serializes overlapped launches
+    that share an output slot."""
+    _fields_ = [("d_words", C.c_void_p), ("prev_epoch", C.c_uint32), ("epoch", C.c_uint32), ("d_err", C.c_void_p)]
 
 
 class Mirror(C.Structure):
     """parva_mirror (include/parva_b200.h): the fused all-gather's destinations."""
     _fields_ = [("n", C.c_int32), ("overlap", C.c_int32), ("plan", C.c_void_p * 8), ("cfg", C.c_void_p * 8),
-                ("flag", C.c_void_p * 8), ("d_done", C.c_void_p), ("epoch", C.c_uint32)]
+                ("spill", C.c_void_p * 8), ("flag", C.c_void_p * 8), ("d_acks", C.c_void_p),
+                ("d_spill", C.c_void_p), ("plan_capacity", C.c_int64), ("cfg_capacity", C.c_int64),
+                ("spill_capacity", C.c_int64), ("plan_bytes", C.c_int32), ("reserved", C.c_int32),
+                ("ticket", SlotTicket)]
+
+
+class GatherSlot(C.Structure):
+    """parva_gather_slot (include/parva_b200.h): the consumer side of one slot."""
+    _fields_ = [("n", C.c_int32), ("pdl", C.c_int32), ("d_flags", C.c_void_p), ("ack", C.c_void_p * 8)]
 
 
 def lib_path():
@@ -121,6 +136,7 @@ def load_library(build_if_missing: bool = True):
             _LIB.parva_plan_host_mapped_scratch.restype = C.c_size_t
             _LIB.parva_stream_bytes.restype = C.c_int64
             _LIB.parva_stream_pack.restype = C.c_int64
+            _LIB.parva_stream_pack_arrays.restype = C.c_int64
         return _LIB
 
 

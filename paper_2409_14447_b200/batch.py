@@ -46,30 +46,75 @@ def configure_sweep(dt: N.DeviceTables, q_table, q_rate, q_bound, out=None, stre
 
 @dataclass
 class BatchResult:
-    cfg: object            # device uint8 [n_services, 32] (full) or [n_services, 16] (compact)
-    plan: object           # device uint8 [n_scenarios, 128]
+    cfg: object            # device uint8 config records (32, 16 or 8 bytes each, cfg_format)
+    plan: object           # device uint8 plan records: 128 bytes each, or 64 with `spill`
     n_scenarios: int
     n_services: int
     cfg_format: int = CFG_FULL
+    spill: object = None   # 64-byte records: full records of spilled scenarios (same index, 128 B each)
 
     def host(self):
+        """(config records, 128-byte plan records) on the host."""
         cfg = N.records_to_numpy(self.cfg, self.n_services, _CFG_DT[self.cfg_format])
-        plan = N.records_to_numpy(self.plan, self.n_scenarios, PLAN_DTYPE)
+        if self.spill is None:
+            return cfg, N.records_to_numpy(self.plan, self.n_scenarios, PLAN_DTYPE)
+        p64 = N.records_to_numpy(self.plan, self.n_scenarios, PLAN64_DTYPE)
+        plan = np.zeros(self.n_scenarios, dtype=PLAN_DTYPE)
+        plan.view(np.uint8).reshape(-1, 128)[:, :64] = p64.view(np.uint8).reshape(-1, 64)
+        sp = np.nonzero(p64["status"] == SPILLED)[0]
+        if len(sp):
+            plan[sp] = N.records_to_numpy(self.spill, self.n_scenarios, PLAN_DTYPE)[sp]
         return cfg, plan
+
+
+class SlotRing:
+    """Output slots of overlapped launches (parva_slot_ticket): `n_slots`
+    slots, each with two device words (the epoch of its last completed
+    launch, a CTA counter).  ticket(slot) is the ticket of the next launch
+    into `slot`: its CTAs store nothing until the slot's previous launch has
+    completed, so overlapped launches that share a slot never overlap each
+    other -- safe by construction, however many grids are in flight."""
+
+    def __init__(self, n_slots: int):
+        torch = N.require_cuda()
+        if n_slots < 1:
+            raise ValueError("n_slots must be >= 1")
+        self.n_slots = int(n_slots)
+        self.words = torch.zeros(2 * self.n_slots, dtype=torch.int32, device="cuda")
+        self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.last = [0] * self.n_slots
+        self.epoch = 0
+
+    def ticket(self, slot: int) -> N.SlotTicket:
+        self.epoch = self.epoch % 0xFFFFFFFF + 1
+        t = N.SlotTicket(self.words.data_ptr() + 8 * slot, self.last[slot], self.epoch, self.err.data_ptr())
+        self.last[slot] = self.epoch
+        return t
+
+    def check(self):
+        """Raise if a ticket wait timed out (the launch stored nothing)."""
+        if int(self.err.item()) != 0:
+            raise RuntimeError("overlapped launch: a slot ticket wait timed out (its records were not written)")
 
 
 def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, optimize: bool = True,
                threshold: int = 4, cfg_format: int = CFG_FULL, stream=None,
-               out: BatchResult | None = None, overlap: bool = False, mirror=None) -> BatchResult:
+               out: BatchResult | None = None, overlap: bool = False, ticket: N.SlotTicket | None = None,
+               mirror=None) -> BatchResult:
     """Plan independent scenarios; scenario k owns services [scen_off[k], scen_off[k+1]).
 
     overlap=True launches the kernel as a programmatic dependent launch
     (parva_plan_batch_overlapped): it may start while the previous planning
-    call on the stream is still running, so `out` must not be written or
-    read by a call still in flight.  mirror (an N.Mirror, e.g. from
-    distributed.PeerGather.mirror) adds the fused all-gather
-    (parva_plan_batch_fused)."""
+    call on the stream is still running.  It needs the `ticket` of `out`'s
+    slot (SlotRing.ticket): launches into one slot are serialized on the
+    device.  mirror (an N.Mirror, from distributed.PeerGather.mirror) adds
+    the fused all-gather (parva_plan_batch_fused); it carries its own ticket."""
     torch = N.require_cuda()
+    if overlap and mirror is None and ticket is None:
+        raise ValueError("overlap=True needs the slot ticket of `out` (SlotRing.ticket)")
+    if mirror is not None and dt.index_struct is None:
+        raise ValueError("the fused all-gather needs tables small enough for the shared-memory index "
+                         "(parva_plan_batch_preconfigured has no peer stores)")
     dev = lambda a, f: a if isinstance(a, torch.Tensor) else N.to_device(f(a))  # noqa: E731
     scen_off = dev(scen_off, _i32)
     svc_table = dev(svc_table, _i32)
@@ -80,8 +125,9 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     if dt.index_struct is None:
         cfg_format = CFG_FULL
     if out is None:
+        plan_dt = PLAN64_DTYPE if mirror is not None and mirror.plan_bytes == 64 else PLAN_DTYPE
         out = BatchResult(N.empty_records(n_svc, _CFG_DT[cfg_format]),
-                          N.empty_records(n_scen, PLAN_DTYPE), n_scen, n_svc, cfg_format)
+                          N.empty_records(n_scen, plan_dt), n_scen, n_svc, cfg_format)
     s = N.stream_handle(stream)
     L = N.lib()
     if dt.index_struct is not None:
@@ -90,8 +136,10 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
                 C.c_int32(int(threshold)), N.ptr(out.cfg), C.c_int32(out.cfg_format), N.ptr(out.plan))
         if mirror is not None:
             rc = L.parva_plan_batch_fused(*args, C.byref(mirror), s)
+        elif overlap:
+            rc = L.parva_plan_batch_overlapped(*args, C.byref(ticket), s)
         else:
-            rc = (L.parva_plan_batch_overlapped if overlap else L.parva_plan_batch)(*args, s)
+            rc = L.parva_plan_batch(*args, s)
         N.check(rc, "parva_plan_batch")
     else:
         configure_sweep(dt, svc_table, svc_rate, svc_bound, out=out.cfg, stream=stream)
@@ -360,23 +408,26 @@ class PackedHostBatch:
 
 # ------------------------------------------------------------ mapped host
 class MappedHostBatch:
-    """A batch for the zero-copy host entry parva_plan_host_mapped (the
+    """Batches for the zero-copy host entry parva_plan_host_mapped (the
     end-to-end path).
 
-    One pinned input block in the streamed layout (a chunk table, then one
-    packed block per `chunk_scen` consecutive scenarios; packed by
-    parva_stream_pack) and one pinned output block (plan records, config
-    records, and for 64-byte plan records an overflow area of full records).
-    Inside one kernel, loader warps stream the input block over PCIe in
-    order while the other warps plan each scenario as soon as its chunk has
-    landed and write its records straight into the output block; `run` is
-    one launch plus a stream synchronize.
+    Per slot one pinned input block in the streamed layout (a chunk table,
+    then one packed block per `chunk_scen` consecutive scenarios) and one
+    pinned output block (plan records, config records, and for 64-byte plan
+    records an overflow area of full records).  fill() packs a caller's
+    plain arrays (scenario offsets, int32 table ids, rates, bounds -- any
+    host memory) into a slot's input block on the library's host threads
+    (parva_stream_pack_arrays).  Inside one kernel, loader warps stream the
+    input block over PCIe in order while the other warps plan each scenario
+    as soon as its chunk has landed and write its records straight into the
+    output block; `run` is one launch plus a stream synchronize.
 
-    depth > 1 keeps that many calls in flight (one scratch and one output
-    block per slot): `submit(dt, slot)` enqueues a call without waiting,
-    `wait(slot)` spins on its completion word; consecutive submits on a
-    stream overlap (the next call's input stream starts while the previous
-    call finishes planning)."""
+    depth > 1 keeps that many calls in flight (one input block, scratch and
+    output block per slot): `submit(dt, slot)` enqueues a call without
+    waiting, `wait(slot)` spins on its completion word; consecutive submits
+    on a stream overlap (the next call's input stream starts while the
+    previous call finishes planning).  Every batch must have the offsets'
+    shape the object was built with (same scenario and service counts)."""
 
     def __init__(self, scen_off, svc_table, svc_rate, svc_bound, cfg_format: int = CFG_TINY, plan_bytes: int = 64,
                  chunk_scen: int = 32, depth: int = 1):
@@ -388,22 +439,33 @@ class MappedHostBatch:
         self.layout = ChunkLayout()
         N.check(L.parva_mapped_layout(C.c_int32(self.n_scen), C.c_int32(self.n_svc), C.c_int32(cfg_format),
                                       C.c_int32(plan_bytes), C.byref(self.layout)), "parva_mapped_layout")
-        self._off32 = np.ascontiguousarray(scen_off - scen_off[0], dtype=np.int32)
-        self.in_bytes = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(self._off32), C.c_int32(chunk_scen)))
-        self.in_capacity = self.in_bytes   # upper bound; fill() sets in_bytes to the packed size
-        if self.in_bytes < 0:
+        off32 = np.ascontiguousarray(scen_off - scen_off[0], dtype=np.int32)
+        cap = int(L.parva_stream_bytes(C.c_int32(self.n_scen), N.np_ptr(off32), C.c_int32(chunk_scen)))
+        if cap < 0:
             raise ValueError("invalid scenario offsets")
         if depth < 1:
             raise ValueError("depth must be >= 1")
         self.depth = depth
-        self.h_in = torch.zeros(max(self.in_bytes, 256), dtype=torch.uint8).pin_memory()
+        self.in_capacity = cap              # upper bound; fill() records each slot's packed size
+        self.in_sizes = [cap] * depth
+        self.h_ins = [torch.zeros(max(cap, 256), dtype=torch.uint8).pin_memory() for _ in range(depth)]
         self.h_outs = [torch.zeros(max(self.layout.out_bytes, 256), dtype=torch.uint8).pin_memory()
                        for _ in range(depth)]
-        self.scratch_bytes = int(L.parva_plan_host_mapped_scratch(C.c_int64(self.in_bytes)))
+        self.scratch_bytes = int(L.parva_plan_host_mapped_scratch(C.c_int64(cap)))
         self.scratches = [torch.empty(self.scratch_bytes, dtype=torch.uint8, device="cuda") for _ in range(depth)]
         self._tickets = [0] * depth
         self._ticket = C.c_uint64(0)
-        self.fill(scen_off, svc_table, svc_rate, svc_bound)
+        self._args = {}
+        for slot in range(depth):
+            self.fill(scen_off, svc_table, svc_rate, svc_bound, slot=slot)
+
+    @property
+    def h_in(self):
+        return self.h_ins[0]
+
+    @property
+    def in_bytes(self):
+        return self.in_sizes[0]
 
     @property
     def h_out(self):
@@ -413,44 +475,56 @@ class MappedHostBatch:
     def scratch(self):
         return self.scratches[0]
 
-    def fill(self, scen_off, svc_table, svc_rate, svc_bound):
-        scen_off = np.asarray(scen_off, dtype=np.int64)
-        sa, sb = int(scen_off[0]), int(scen_off[-1])
-        off32 = np.ascontiguousarray(scen_off - sa, dtype=np.int32)
-        tab = np.ascontiguousarray(np.asarray(svc_table)[sa:sb], dtype=np.uint16)
-        rate = np.ascontiguousarray(np.asarray(svc_rate)[sa:sb], dtype=np.float64)
-        bound = np.ascontiguousarray(np.asarray(svc_bound)[sa:sb], dtype=np.float64)
-        n = N.lib().parva_stream_pack(C.c_int32(self.n_scen), N.np_ptr(off32), N.np_ptr(tab), N.np_ptr(rate),
-                                      N.np_ptr(bound), C.c_int32(self.chunk_scen), C.c_void_p(self.h_in.data_ptr()),
-                                      C.c_int64(self.in_capacity))
+    def fill(self, scen_off, svc_table, svc_rate, svc_bound, slot: int = 0, threads: int = 0):
+        """Pack a batch into `slot`'s input block (the slot's previous call
+        must have completed: wait(slot))."""
+        if self._tickets[slot]:
+            raise RuntimeError("fill(): the slot's previous call is still in flight (wait(slot) first)")
+        scen_off = np.asarray(scen_off)
+        sa = int(scen_off[0])
+        if sa != 0 or scen_off.dtype != np.int32:
+            scen_off = np.ascontiguousarray(scen_off - sa, dtype=np.int32)
+        sb = sa + int(scen_off[-1])
+
+        def arr(x, dt):
+            x = np.asarray(x)
+            if sa or len(x) != sb - sa:
+                x = x[sa:sb]
+            return x if x.dtype == dt and x.flags.c_contiguous else np.ascontiguousarray(x, dtype=dt)
+
+        tab, rate, bound = arr(svc_table, np.int32), arr(svc_rate, np.float64), arr(svc_bound, np.float64)
+        if len(scen_off) - 1 != self.n_scen or int(scen_off[-1]) != self.n_svc:
+            raise ValueError("batch shape differs from the one this MappedHostBatch was built for")
+        n = N.lib().parva_stream_pack_arrays(C.c_int32(self.n_scen), N.np_ptr(scen_off), N.np_ptr(tab),
+                                             N.np_ptr(rate), N.np_ptr(bound), C.c_int32(self.chunk_scen),
+                                             C.c_void_p(self.h_ins[slot].data_ptr()), C.c_int64(self.in_capacity),
+                                             C.c_int32(threads))
         if n < 0:
-            raise ValueError("parva_stream_pack failed (offsets changed shape?)")
-        self.in_bytes = int(n)          # chunks that repeat one table-id sequence store it once
-        self._args = {}
+            raise ValueError("parva_stream_pack_arrays failed (offsets not non-decreasing?)")
+        self.in_sizes[slot] = int(n)    # chunks that repeat one table-id sequence store it once
 
     def _call_args(self, dt, optimize, threshold, stream, slot):
         sh = N.stream_handle(stream)
-        key = (id(dt), bool(optimize), int(threshold), sh.value, slot)
-        hit = self._args.get(key) if hasattr(self, "_args") else None
-        if hit is None:   # the argument tuple is built once per (tables, options, stream, slot)
+        key = (id(dt), bool(optimize), int(threshold), sh.value, slot, self.in_sizes[slot])
+        hit = self._args.get(key)
+        if hit is None:   # the argument tuple is built once per (tables, options, stream, slot, size)
             args = (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen), C.c_int32(self.n_svc),
-                    C.c_void_p(self.h_in.data_ptr()), C.c_int64(self.in_bytes),
+                    C.c_void_p(self.h_ins[slot].data_ptr()), C.c_int64(self.in_sizes[slot]),
                     C.c_void_p(self.h_outs[slot].data_ptr()), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
                     C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes), N.ptr(self.scratches[slot]),
                     C.c_size_t(self.scratch_bytes), sh)
-            self._args = getattr(self, "_args", {})
             self._args[key] = (args, dt)
             return args
         return hit[0]
 
-    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None):
-        """One synchronous call on slot 0."""
-        self.wait(0)
-        N.check(N.lib().parva_plan_host_mapped(*self._call_args(dt, optimize, threshold, stream, 0)),
+    def run(self, dt: N.DeviceTables, optimize: bool = True, threshold: int = 4, stream=None, slot: int = 0):
+        """One synchronous call on `slot`."""
+        self.wait(slot)
+        N.check(N.lib().parva_plan_host_mapped(*self._call_args(dt, optimize, threshold, stream, slot)),
                 "parva_plan_host_mapped")
 
     def submit(self, dt: N.DeviceTables, slot: int = 0, optimize: bool = True, threshold: int = 4, stream=None):
-        """Enqueue a call writing into slot `slot`'s output block; returns at once."""
+        """Enqueue a call on `slot` (its input block -> its output block); returns at once."""
         N.check(N.lib().parva_plan_host_mapped_submit(*self._call_args(dt, optimize, threshold, stream, slot),
                                                       C.byref(self._ticket)), "parva_plan_host_mapped_submit")
         self._tickets[slot] = self._ticket.value
@@ -467,8 +541,7 @@ class MappedHostBatch:
             for s in range(self.depth):
                 self.wait(s)
             L = N.lib()
-            L.parva_forget_block(C.c_void_p(self.h_in.data_ptr()))
-            for h in self.h_outs:
+            for h in self.h_ins + self.h_outs:
                 L.parva_forget_block(C.c_void_p(h.data_ptr()))
             for d in self.scratches:
                 L.parva_forget_block(C.c_void_p(d.data_ptr()))
@@ -477,8 +550,8 @@ class MappedHostBatch:
 
     @property
     def h2d_bytes(self) -> int:
-        """Bytes the kernel streams from the host input block per call."""
-        return self.in_bytes
+        """Bytes the kernel streams from the host input block per call (mean over slots)."""
+        return int(sum(self.in_sizes) / len(self.in_sizes))
 
     @property
     def d2h_bytes(self) -> int:

@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -45,22 +48,51 @@ int parva_configure_sweep(const parva_tables* tables, int32_t n_queries, const i
                                        (cudaStream_t)stream);
 }
 
+static int64_t cfg_record_bytes(int cfg_format) {
+  return cfg_format == PARVA_CFG_TINY ? 8 : cfg_format == PARVA_CFG_COMPACT ? 16 : 32;
+}
+
 static int plan_batch_impl(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                            int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
                            const double* d_svc_bound, int32_t optimize, int32_t threshold, void* d_cfg,
                            int cfg_format, parva_plan_record* d_plan, int cfg_given, cudaStream_t stream,
-                           int pdl = 0, const parva_mirror* mirror = nullptr) {
+                           int pdl = 0, const parva_slot_ticket* ticket = nullptr,
+                           const parva_mirror* mirror = nullptr) {
   parva::PlanArgs A;
   A.pdl = pdl;
+  A.plan_bytes = 128;
+  A.spill_cap = 0;
+  A.spill_count = nullptr;
+  A.spill = nullptr;
+  if (ticket) {
+    static long long s_timeout_ms = -1;   // PARVA_TICKET_TIMEOUT_MS (tests), default 60 s
+    if (s_timeout_ms < 0) {
+      const char* e = std::getenv("PARVA_TICKET_TIMEOUT_MS");
+      s_timeout_ms = e ? std::max(1ll, std::atoll(e)) : 60000ll;
+    }
+    A.ticket_timeout_ns = (unsigned long long)s_timeout_ms * 1000000ull;
+    A.slot_words = ticket->d_words;
+    A.slot_prev = ticket->prev_epoch;
+    A.slot_epoch = ticket->epoch;
+    A.err_word = ticket->d_err;
+  }
   if (mirror) {
     A.n_mirror = mirror->n;
     for (int m = 0; m < mirror->n; m++) {
       A.mirror_plan[m] = (uint8_t*)mirror->plan[m];
       A.mirror_cfg[m] = (uint8_t*)mirror->cfg[m];
+      A.mirror_spill[m] = (uint8_t*)mirror->spill[m];
       A.peer_flag[m] = mirror->flag[m];
     }
-    A.done_ctas = mirror->d_done;
-    A.flag_epoch = mirror->epoch;
+    A.ack_row = mirror->d_acks;
+    if (mirror->plan_bytes == 64) {
+      // 64-byte records; a spilled scenario's full record at the same index
+      // of the overflow area (local, then mirrored)
+      A.plan_bytes = 64;
+      A.spill = (uint8_t*)mirror->d_spill;
+      A.spill_cap = n_scenarios;
+      A.spill_direct = 1;
+    }
   }
   A.pts = tables->d_pts;
   A.idx_lat = index ? index->d_lat_sorted : nullptr;
@@ -89,11 +121,11 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.cfg = d_cfg;
   A.cfg_format = cfg_format;
   A.plan = d_plan;
-  A.plan_bytes = 128;
-  A.spill_cap = 0;
-  A.spill_count = nullptr;
-  A.spill = nullptr;
   return parva::launch_plan_batch(A, stream);
+}
+
+static bool ticket_ok(const parva_slot_ticket* t) {
+  return t && t->d_words && t->epoch != 0 && t->epoch != t->prev_epoch;
 }
 
 int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
@@ -108,22 +140,23 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32
 
 // parva_plan_batch as a programmatic dependent launch: it may start while the
 // previous overlapped call on the stream is still finishing (its CTAs take
-// SM slots as the predecessor's retire).  The caller guarantees that no call
-// still in flight writes what this one reads or writes.
+// SM slots as the predecessor's retire); the slot ticket serializes the
+// launches that share an output slot.
 int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                                 int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table,
                                 const double* d_svc_rate, const double* d_svc_bound, int32_t optimize,
                                 int32_t threshold, void* d_cfg, int32_t cfg_format, parva_plan_record* d_plan,
-                                void* stream) {
-  if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan) return PARVA_BAD_INPUT;
+                                const parva_slot_ticket* ticket, void* stream) {
+  if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan || !ticket_ok(ticket)) return PARVA_BAD_INPUT;
   if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
+  if (n_scenarios == 0) return PARVA_BAD_INPUT;   // nothing would complete the ticket
   return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
-                         optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream, 1);
+                         optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream, 1, ticket);
 }
 
-// parva_plan_batch with a fused all-gather: every record is also stored into
-// this rank's slot of each rank's gathered block (peer memory), and the last
-// CTA stores `epoch` into this rank's flag word on every rank.
+// parva_plan_batch with a fused all-gather: every tile's records are also
+// stored into this rank's sections of the slot on each rank (peer memory),
+// and the last CTA stores the epoch into this rank's flag word on every rank.
 int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                            int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table,
                            const double* d_svc_rate, const double* d_svc_bound, int32_t optimize, int32_t threshold,
@@ -131,13 +164,23 @@ int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
                            void* stream) {
   if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan || !mirror) return PARVA_BAD_INPUT;
   if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
-  if (mirror->n < 1 || mirror->n > parva::kMaxMirror || !mirror->d_done) return PARVA_BAD_INPUT;
-  for (int m = 0; m < mirror->n; m++)
-    if (!mirror->plan[m] || !mirror->cfg[m] || !mirror->flag[m]) return PARVA_BAD_INPUT;
+  if (mirror->n < 1 || mirror->n > parva::kMaxMirror || !mirror->d_acks || !ticket_ok(&mirror->ticket))
+    return PARVA_BAD_INPUT;
+  if (mirror->plan_bytes != 128 && mirror->plan_bytes != 64) return PARVA_BAD_INPUT;
   if (n_scenarios == 0) return PARVA_BAD_INPUT;   // nothing would publish the epoch
+  // the records must fit this rank's sections (the kernel copies whole
+  // record ranges into them)
+  if (int64_t(n_scenarios) * mirror->plan_bytes > mirror->plan_capacity ||
+      int64_t(n_services) * cfg_record_bytes(cfg_format) > mirror->cfg_capacity)
+    return PARVA_BAD_INPUT;
+  if (mirror->plan_bytes == 64 && (!mirror->d_spill || int64_t(n_scenarios) * 128 > mirror->spill_capacity))
+    return PARVA_BAD_INPUT;
+  for (int m = 0; m < mirror->n; m++)
+    if (!mirror->plan[m] || !mirror->cfg[m] || !mirror->flag[m] || (mirror->plan_bytes == 64 && !mirror->spill[m]))
+      return PARVA_BAD_INPUT;
   return plan_batch_impl(tables, index, n_scenarios, n_services, d_scen_off, d_svc_table, d_svc_rate, d_svc_bound,
                          optimize, threshold, d_cfg, cfg_format, d_plan, 0, (cudaStream_t)stream,
-                         mirror->overlap ? 1 : 0, mirror);
+                         mirror->overlap ? 1 : 0, &mirror->ticket, mirror);
 }
 
 // Same as parva_plan_batch but the config records in d_cfg were produced by
@@ -545,6 +588,174 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
     off += blk_bytes;
   }
   return off;
+}
+
+// ------------------------------------------------------------ host pack pool
+// A small persistent pool of host threads for parva_stream_pack_arrays: the
+// caller's thread takes part, workers sleep on a condition variable between
+// calls (no OpenMP runtime next to torch's).
+namespace {
+class PackPool {
+ public:
+  explicit PackPool(int n) {
+    for (int i = 0; i < n; i++) th_.emplace_back([this] { worker(); });
+  }
+  ~PackPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+  // fn(task) for task in [0, n_tasks), on up to `width` threads (caller included)
+  void run(int n_tasks, int width, const std::function<void(int)>& fn) {
+    std::unique_lock<std::mutex> call(call_mu_);   // one call at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &fn;
+      n_tasks_ = n_tasks;
+      next_.store(0);
+      remaining_.store(n_tasks);
+      width_ = std::max(0, width - 1);
+      taken_ = 0;
+      gen_++;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return remaining_.load() == 0 && active_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void drain() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= n_tasks_) return;
+      (*job_)(i);
+      remaining_.fetch_sub(1);
+    }
+  }
+  void worker() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (taken_ >= width_) continue;   // enough threads on this call
+        taken_++;
+        active_++;
+      }
+      drain();
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        active_--;
+      }
+      done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_tasks_ = 0, width_ = 0, active_ = 0, taken_ = 0;
+  std::atomic<int> next_{0}, remaining_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+PackPool& pack_pool() {
+  static PackPool pool([] {
+    const char* e = std::getenv("PARVA_PACK_THREADS");
+    int n = e ? std::atoi(e) : (int)std::thread::hardware_concurrency();
+    return std::max(0, std::min(n, 64) - 1);
+  }());
+  return pool;
+}
+}  // namespace
+
+// Streamed input block from plain arrays (int32 table ids), multi-threaded:
+// pass 1 sizes every chunk (template detection), a prefix sum places them,
+// pass 2 writes the header and the chunk blocks.  Table ids outside
+// [0, 65535) are stored as 0xFFFF (no table: the kernel reports
+// PARVA_BAD_INPUT for the service, as for any id >= n_tables).
+int64_t parva_stream_pack_arrays(int32_t n_scenarios, const int32_t* h_scen_off, const int32_t* h_table,
+                                 const double* h_rate, const double* h_bound, int32_t chunk_scen, void* h_block,
+                                 int64_t capacity, int32_t n_threads) {
+  if (n_scenarios < 0 || !h_scen_off || chunk_scen < 1 || !h_block || capacity < 16) return -1;
+  if (n_scenarios > 0 && (!h_table || !h_rate || !h_bound || h_scen_off[0] != 0)) return -1;
+  const int32_t n_ch = n_scenarios == 0 ? 0 : (n_scenarios + chunk_scen - 1) / chunk_scen;
+  PackPool& pool = pack_pool();
+  const int width = n_threads > 0 ? std::min(n_threads, pool.size()) : pool.size();
+  constexpr int kChunksPerTask = 4;
+  const int n_tasks = (n_ch + kChunksPerTask - 1) / kChunksPerTask;
+  std::vector<int64_t> blk(n_ch + 1, 0);
+  std::vector<int32_t> tmpl(n_ch, 0);
+  std::atomic<int> bad{0};
+  // pass 1: offsets valid, template?, block bytes
+  pool.run(n_tasks, width, [&](int task) {
+    for (int32_t c = task * kChunksPerTask; c < std::min(n_ch, (task + 1) * kChunksPerTask); c++) {
+      const int32_t a = c * chunk_scen, b = std::min(n_scenarios, a + chunk_scen);
+      for (int32_t k = a; k < b; k++)
+        if (h_scen_off[k + 1] < h_scen_off[k]) { bad.store(1); return; }
+      const int32_t sa = h_scen_off[a], sb = h_scen_off[b];
+      const int32_t t0 = h_scen_off[a + 1] - sa;
+      bool tm = t0 > 0 && b - a > 1;
+      for (int32_t k = a + 1; tm && k < b; k++) {
+        const int32_t ka = h_scen_off[k];
+        tm = h_scen_off[k + 1] - ka == t0 && std::memcmp(h_table + ka, h_table + sa, size_t(t0) * 4) == 0;
+      }
+      const int64_t m = sb - sa;
+      const int64_t rate_at = tm ? 0 : ((int64_t)(b - a + 1) * 4 + 15) & ~int64_t(15);
+      const int64_t table_at = rate_at + m * 16;
+      tmpl[c] = tm ? t0 : 0;
+      blk[c + 1] = (table_at + (tm ? t0 : m) * 2 + 15) & ~int64_t(15);
+    }
+  });
+  if (bad.load()) return -1;
+  const int64_t head = parva_stream_header_bytes(n_ch);
+  blk[0] = head;
+  for (int32_t c = 0; c < n_ch; c++) blk[c + 1] += blk[c];   // blk[c] = offset of chunk c
+  const int64_t total = blk[n_ch];
+  if (total > capacity) return -1;
+  uint8_t* out = (uint8_t*)h_block;
+  std::memset(out, 0, (size_t)head);
+  reinterpret_cast<int32_t*>(out)[0] = n_ch;
+  reinterpret_cast<int32_t*>(out)[1] = chunk_scen;
+  parva_stream_chunk* tab = reinterpret_cast<parva_stream_chunk*>(out + 16);
+  // pass 2: chunk table entries and blocks
+  pool.run(n_tasks, width, [&](int task) {
+    for (int32_t c = task * kChunksPerTask; c < std::min(n_ch, (task + 1) * kChunksPerTask); c++) {
+      const int32_t a = c * chunk_scen, b = std::min(n_scenarios, a + chunk_scen);
+      const int32_t sa = h_scen_off[a], sb = h_scen_off[b];
+      const int64_t m = sb - sa;
+      const bool tm = tmpl[c] > 0;
+      tab[c].scen_lo = a; tab[c].svc_lo = sa; tab[c].k = b - a; tab[c].m = (int32_t)m; tab[c].offset = blk[c];
+      tab[c].tmpl = tmpl[c]; tab[c].reserved = 0;
+      uint8_t* p = out + blk[c];
+      const int64_t rate_at = tm ? 0 : ((int64_t)(b - a + 1) * 4 + 15) & ~int64_t(15);
+      if (!tm) {
+        int32_t* so = reinterpret_cast<int32_t*>(p);
+        for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
+        std::memset(p + int64_t(b - a + 1) * 4, 0, size_t(rate_at - int64_t(b - a + 1) * 4));
+      }
+      std::memcpy(p + rate_at, h_rate + sa, size_t(m) * 8);
+      std::memcpy(p + rate_at + m * 8, h_bound + sa, size_t(m) * 8);
+      uint16_t* t16 = reinterpret_cast<uint16_t*>(p + rate_at + m * 16);
+      const int64_t nt = tm ? tmpl[c] : m;
+      for (int64_t i = 0; i < nt; i++) {
+        const int32_t v = h_table[sa + i];
+        t16[i] = (v < 0 || v >= 65535) ? (uint16_t)0xFFFF : (uint16_t)v;
+      }
+      const int64_t end = rate_at + m * 16 + nt * 2;
+      std::memset(p + end, 0, size_t(blk[c + 1] - blk[c] - end));
+    }
+  });
+  return total;
 }
 
 // scratch head: work counters, slice flags

@@ -58,17 +58,31 @@ struct PlanArgs {
   // streamed call on the stream is still finishing its last scenarios
   uint32_t* done_word = nullptr;
   int pdl = 0;
-  // fused all-gather (device path): every plan / config record is also
-  // stored at mirror_plan[m] / mirror_cfg[m] (the same record index), i.e.
-  // into this rank's slot of every rank's gathered block over peer memory;
-  // the last CTA (done_ctas, self-resetting) then stores flag_epoch into
-  // peer_flag[m] (this rank's flag word on rank m) after a system fence
+  // slot ticket (overlapped and fused launches; parva_slot_ticket): before
+  // its first store every CTA waits until slot_words[0] == slot_prev, i.e.
+  // the previous launch into the same output slot has completed; the last
+  // CTA of the grid (counter slot_words[1], reset before publishing) stores
+  // slot_epoch into slot_words[0].  A wait that times out stores
+  // PARVA_LAUNCH_ERROR into *err_word and the CTA exits without storing.
+  uint32_t* slot_words = nullptr;
+  uint32_t slot_prev = 0, slot_epoch = 0;
+  int32_t* err_word = nullptr;
+  unsigned long long ticket_timeout_ns = 60ull * 1000 * 1000 * 1000;   // PARVA_TICKET_TIMEOUT_MS
+  // fused all-gather (device path): each tile's plan / config records (and,
+  // for 64-byte plan records, the full records of spilled scenarios) are
+  // also stored at mirror_plan[m] / mirror_cfg[m] / mirror_spill[m] (the same
+  // record index), i.e. into this rank's part of slot s on every rank over
+  // peer memory.  Before storing, the CTAs also wait until every rank has
+  // released the slot's previous epoch (ack_row[m] >= slot_prev, written by
+  // rank m's parva_gather_wait).  The last CTA stores slot_epoch into
+  // peer_flag[m] (this rank's flag word of slot s on rank m) after a
+  // system-scope fence.
   int n_mirror = 0;
   uint8_t* mirror_plan[kMaxMirror] = {};
   uint8_t* mirror_cfg[kMaxMirror] = {};
+  uint8_t* mirror_spill[kMaxMirror] = {};
   uint32_t* peer_flag[kMaxMirror] = {};
-  uint32_t* done_ctas = nullptr;
-  uint32_t flag_epoch = 0;
+  const uint32_t* ack_row = nullptr;
 };
 
 #ifndef PARVA_STREAM_SLICE

@@ -99,6 +99,46 @@ __device__ __forceinline__ double unallocated(int total, int n) {
   return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
 }
 
+// ------------------------------------------------------------ slot tickets
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One thread per CTA, before the CTA's first store: the slot's previous
+// launch has completed (its last CTA published slot_prev) and, for the fused
+// all-gather, every rank has released the slot's previous epoch.  Launches
+// into one slot are therefore serialized however many overlapped grids are
+// in flight.  No deadlock: a programmatic dependent launch starts only after
+// every CTA of its predecessor has started, so every earlier grid is
+// resident or finished.  Returns false after the timeout (error recorded).
+__device__ __noinline__ bool ticket_wait(const uint32_t* words, uint32_t prev, const uint32_t* acks, int n_acks,
+                                         unsigned long long timeout_ns, int32_t* err) {
+  const unsigned long long t0 = global_ns();
+  for (unsigned ns = 32;; ns = ns < 1024 ? 2 * ns : ns) {
+    bool ok = ld_acquire_gpu_u32(words) == prev;
+    if (ok && acks && prev)
+      for (int m = 0; m < n_acks && ok; m++) ok = (int32_t)(ld_acquire_sys_u32(acks + m) - prev) >= 0;
+    if (ok) return true;
+    if (global_ns() - t0 > timeout_ns) {
+      if (err) atomicExch(err, (int32_t)PARVA_LAUNCH_ERROR);
+      return false;
+    }
+    __nanosleep(ns);
+  }
+}
+
 // configure one service from the index: for each size class, count = number
 // of points with lat < bound (binary search over the latency-sorted
 // segment), winner = prefix argmax at count-1.  The five searches advance in
@@ -871,8 +911,21 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
       for (int m = 0; m < A.n_mirror; m++) {
         uint4* pd = reinterpret_cast<uint4*>(A.mirror_plan[m] + p0);
         uint2* cd = reinterpret_cast<uint2*>(A.mirror_cfg[m] + c0);
+        if (pd == ps) continue;   // this rank's own part of the slot is the launch's output
         for (size_t x = tid; x < pn; x += PB_THREADS) pd[x] = ps[x];
         for (size_t x = tid; x < cn; x += PB_THREADS) cd[x] = cs[x];
+      }
+      if (A.plan_bytes == 64) {
+        // 64-byte records: a spilled scenario's full record (overflow area,
+        // same index) follows it; one warp per scenario of the tile
+        for (int j = tid >> 5; j < n_tile; j += PB_WARPS) {
+          const size_t kk = (size_t)(S.scen_base + k + j);
+          if (reinterpret_cast<const uint8_t*>(A.plan)[kk * 64] == PARVA_SPILLED && lane < 8) {
+            const uint4 v = reinterpret_cast<const uint4*>(A.spill + kk * 128)[lane];
+            for (int m = 0; m < A.n_mirror; m++)
+              if (A.mirror_spill[m] != A.spill) reinterpret_cast<uint4*>(A.mirror_spill[m] + kk * 128)[lane] = v;
+          }
+        }
       }
     }
     k += n_tile;
@@ -888,30 +941,45 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
   __shared__ uint64_t bar;
-  // an overlapped successor (parva_plan_batch_overlapped: disjoint buffers by
-  // contract) may take SM slots as this grid's CTAs retire
+  __shared__ int s_go;
+  // an overlapped successor (parva_plan_batch_overlapped / _fused) may take
+  // SM slots as this grid's CTAs retire; the slot ticket keeps it from
+  // storing into an output slot a launch still in flight writes
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   PHASE(0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0)
+    s_go = !A.slot_words ||
+           ticket_wait(A.slot_words, A.slot_prev, A.ack_row, A.n_mirror, A.ticket_timeout_ns, A.err_word);
+  // (a barrier of its own: sharing load_index's costs K2 ~9 registers of spill)
+  __syncthreads();
+  if (!s_go) return;   // timed out: store nothing
   const IndexView V = load_index(A, smem_raw + kWarpArea * PB_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
   PHASE(1);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // this CTA's contiguous block of scenarios
   const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
   const int k = blockIdx.x * per;
   const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
   run_tiles<kMirror>(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
   PHASE(3);
-  if (kMirror) {
-    // fused all-gather completion: every thread's peer stores are fenced
-    // before its CTA counts itself done; the last CTA publishes the epoch
-    // into this rank's flag word on every rank
-    __threadfence_system();
+  if (A.slot_words) {
+    // completion: every thread's stores (peer stores at system scope) are
+    // fenced before its CTA counts itself done; the last CTA resets the
+    // counter, publishes the epoch into this rank's flag word of the slot
+    // on every rank (fused), then completes the slot's ticket
+    if (kMirror) __threadfence_system();
+    else __threadfence();
     __syncthreads();
-    if (tid == 0 && atomicAdd(A.done_ctas, 1u) == gridDim.x - 1) {
-      atomicExch(A.done_ctas, 0u);
-      __threadfence_system();
-      for (int m = 0; m < A.n_mirror; m++)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.peer_flag[m]), "r"(A.flag_epoch) : "memory");
+    if (tid == 0 && atomicAdd(&A.slot_words[1], 1u) == gridDim.x - 1) {
+      atomicExch(&A.slot_words[1], 0u);
+      if (kMirror) {
+        __threadfence_system();
+        for (int m = 0; m < A.n_mirror; m++)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.peer_flag[m]), "r"(A.slot_epoch) : "memory");
+      } else {
+        __threadfence();
+      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.slot_words), "r"(A.slot_epoch) : "memory");
     }
   }
 }

@@ -126,23 +126,80 @@ def plan_sharded(scen_off, svc_table, svc_rate, svc_bound, plan_fn, group=None, 
 
 
 # --------------------------------------------------- fused all-gather (peer memory)
+@dataclass
+class GatherLayout:
+    """Per-rank part of a gathered slot: [plan section | config section |
+    overflow section], each padded to the largest shard (16-byte aligned).
+    plan_bytes 64: 64-byte plan records, a spilled scenario's full 128-byte
+    record at the same index of the overflow section; 128: no overflow."""
+    plan_bytes: int
+    cfg_bytes: int
+    ps: int
+    cs: int
+    os: int
+    blk: int
+    spans: list          # scenario span [a, b) of every rank
+    svc_spans: list      # service span [sa, sb) of every rank
+
+
+def gather_layout(scen_off, world: int, plan_bytes: int = 64, cfg_bytes: int = 8) -> GatherLayout:
+    if plan_bytes not in (64, 128):
+        raise ValueError("plan_bytes must be 64 or 128")
+    n_scen = len(scen_off) - 1
+    spans = [shard_bounds(n_scen, r, world) for r in range(world)]
+    svc = [(int(scen_off[a]), int(scen_off[b])) for a, b in spans]
+    max_s = max(max(b - a for a, b in spans), 1)
+    max_v = max(max(b - a for a, b in svc), 1)
+    ps = (max_s * plan_bytes + 15) & ~15
+    cs = (max_v * cfg_bytes + 15) & ~15
+    os_ = max_s * 128 if plan_bytes == 64 else 0
+    return GatherLayout(plan_bytes, cfg_bytes, ps, cs, os_, ps + cs + os_, spans, svc)
+
+
+def decode_gathered(rows: np.ndarray, lay: GatherLayout):
+    """(config records [N_svc] (uint8 rows of cfg_bytes), 128-byte plan
+    records [N_scen]) in global order from a gathered slot (uint8 [world,
+    blk]); spilled 64-byte records are restored from the overflow section."""
+    from .records import PLAN64_DTYPE, PLAN_DTYPE, SPILLED
+    plans, cfgs = [], []
+    for r, ((a, b), (sa, sb)) in enumerate(zip(lay.spans, lay.svc_spans)):
+        k = b - a
+        row = rows[r]
+        if lay.plan_bytes == 128:
+            plan = row[:k * 128].view(PLAN_DTYPE).copy()
+        else:
+            p64 = row[:k * 64].view(PLAN64_DTYPE)
+            plan = np.zeros(k, dtype=PLAN_DTYPE)
+            plan.view(np.uint8).reshape(-1, 128)[:, :64] = p64.view(np.uint8).reshape(-1, 64)
+            sp = np.nonzero(p64["status"] == SPILLED)[0]
+            if len(sp):
+                full = row[lay.ps + lay.cs:lay.ps + lay.cs + 128 * k].view(PLAN_DTYPE)
+                plan[sp] = full[sp]
+        plans.append(plan)
+        cfgs.append(row[lay.ps:lay.ps + (sb - sa) * lay.cfg_bytes].reshape(-1, lay.cfg_bytes).copy())
+    return np.concatenate(cfgs), np.concatenate(plans)
+
+
 class PeerGather:
-    """Gathered blocks in peer memory for the fused all-gather.
+    """Gathered slots in peer memory for the fused all-gather.
 
-    Every rank allocates one exportable device buffer: a flag array (one u32
-    per source rank) followed by `n_slots` gathered blocks of world x blk
-    bytes (the packed_block layout, rank r's block at r * blk).  The CUDA IPC
-    handles are exchanged with one all_gather_object, every process maps its
-    peers' buffers, and K2 (parva_plan_batch_fused) stores each record into
-    this rank's block of slot s on every rank while it plans, then raises its
-    flag word on every rank to the launch's epoch.  wait(epoch) makes the
-    stream wait until every rank's records of that epoch have landed here.
-    One process per GPU (peers on other GPUs of the NVLink domain; the tests
-    also run two processes on one GPU)."""
+    Every rank allocates one exportable device buffer: a header (per slot a
+    flag row -- rank r's last landed epoch -- an ack row -- rank r's last
+    released epoch -- and the slot's ticket words), then `n_slots` slots of
+    world x layout.blk bytes (rank r's part at r * blk).  The CUDA IPC
+    handles are exchanged with one all_gather_object and every process maps
+    its peers' buffers.  A launch into slot s (mirror(s), then
+    batch.plan_batch(..., out=local(s), mirror=...)) plans this rank's shard
+    straight into its own part of slot s and stores each tile's records into
+    its part of slot s on every rank (K2, parva_plan_batch_fused); its CTAs
+    first wait until every rank released the slot's previous epoch.
+    wait(s) makes the stream wait until every rank's records of the slot's
+    last epoch have landed here and releases the slot.  All ranks must call
+    mirror() in the same order (the epochs agree).  One process per GPU
+    (peers on other GPUs of the NVLink domain; the tests also run several
+    processes on one GPU)."""
 
-    FLAG_BYTES = 256
-
-    def __init__(self, blk_bytes: int, n_slots: int = 3, group=None):
+    def __init__(self, layout: GatherLayout, n_slots: int = 3, group=None):
         import ctypes as C
         import torch
         import torch.distributed as dist
@@ -151,9 +208,13 @@ class PeerGather:
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         if self.world > 8:
             raise ValueError("the fused all-gather spans at most 8 ranks (one NVLink domain)")
-        self.blk, self.n_slots = int(blk_bytes), int(n_slots)
+        if len(layout.spans) != self.world:
+            raise ValueError("layout was built for another world size")
+        self.layout, self.n_slots = layout, int(n_slots)
+        self.blk = layout.blk
         self.slot_bytes = self.world * self.blk
-        size = self.FLAG_BYTES + self.n_slots * self.slot_bytes
+        self.head = (72 * self.n_slots + 255) & ~255
+        size = self.head + self.n_slots * self.slot_bytes
         p = C.c_void_p()
         N.check(L.parva_ipc_alloc(C.c_size_t(size), C.byref(p)), "parva_ipc_alloc")
         self.base = p.value
@@ -171,46 +232,101 @@ class PeerGather:
             N.check(L.parva_ipc_open((C.c_uint8 * hb).from_buffer_copy(hm), C.byref(q)), "parva_ipc_open")
             self.peers.append(q.value)
             self.opened.append(q.value)
-        self.done = torch.zeros(self.n_slots, dtype=torch.int32, device="cuda")
-        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.status = torch.zeros(2, dtype=torch.int32, device="cuda")   # [0] gather waits, [1] tickets
         self.epoch = 0
+        self.last = [0] * self.n_slots
         dist.barrier(group=group)
 
-    def slot_view(self, slot: int):
-        """This process's gathered block of `slot` as a uint8 tensor view
-        (world x blk), for reading the results."""
-        n = self.slot_bytes
-        return _device_view(self.base + self.FLAG_BYTES + slot * n, n)
+    # header addresses
+    def _flag(self, base, slot, r):
+        return base + 4 * (8 * slot + r)
 
-    def mirror(self, slot: int, ps: int, overlap: bool = False):
-        """parva_mirror for a launch into `slot` (next epoch): this rank's
-        plan / config sections on every rank."""
-        import ctypes as C
-        self.epoch += 1
+    def _ack(self, base, slot, r):
+        return base + 32 * self.n_slots + 4 * (8 * slot + r)
+
+    def _part(self, base, slot, r):
+        return base + self.head + slot * self.slot_bytes + r * self.blk
+
+    def slot_view(self, slot: int):
+        """This process's gathered slot as a uint8 tensor view (world x blk)."""
+        return _device_view(self._part(self.base, slot, 0), self.slot_bytes)
+
+    def local(self, slot: int, cfg_format: int):
+        """This rank's part of its own slot as the launch's output (a
+        batch.BatchResult over the plan / config / overflow sections)."""
+        from .batch import BatchResult
+        lay = self.layout
+        a, b = lay.spans[self.rank]
+        sa, sb = lay.svc_spans[self.rank]
+        part = self._part(self.base, slot, self.rank)
+        if cfg_format != {8: 2, 16: 1, 32: 0}[lay.cfg_bytes]:
+            raise ValueError("cfg_format does not match the layout's config record width")
+        plan = _device_view(part, lay.ps).view(-1, lay.plan_bytes)
+        cfg = _device_view(part + lay.ps, lay.cs)[:(sb - sa) * lay.cfg_bytes].view(-1, lay.cfg_bytes)
+        spill = _device_view(part + lay.ps + lay.cs, lay.os).view(-1, 128) if lay.os else None
+        return BatchResult(cfg, plan, b - a, sb - sa, cfg_format, spill)
+
+    def mirror(self, slot: int, overlap: bool = False):
+        """parva_mirror of the next launch into `slot` (the next epoch): this
+        rank's sections of the slot on every rank, the slot's ack row and
+        ticket."""
+        lay = self.layout
+        self.epoch = self.epoch % 0xFFFFFFFF + 1
         m = N.Mirror()
         m.n = self.world
         m.overlap = 1 if overlap else 0
-        off = self.FLAG_BYTES + slot * self.slot_bytes + self.rank * self.blk
         for r, b in enumerate(self.peers):
-            m.plan[r] = b + off
-            m.cfg[r] = b + off + ps
-            m.flag[r] = b + 4 * self.rank
-        m.d_done = self.done.data_ptr() + 4 * slot
-        m.epoch = self.epoch
+            part = self._part(b, slot, self.rank)
+            m.plan[r] = part
+            m.cfg[r] = part + lay.ps
+            m.spill[r] = part + lay.ps + lay.cs if lay.os else None
+            m.flag[r] = self._flag(b, slot, self.rank)
+        m.d_acks = self._ack(self.base, slot, 0)
+        m.d_spill = self._part(self.base, slot, self.rank) + lay.ps + lay.cs if lay.os else None
+        m.plan_capacity, m.cfg_capacity, m.spill_capacity = lay.ps, lay.cs, lay.os
+        m.plan_bytes = lay.plan_bytes
+        m.ticket = N.SlotTicket(self.base + 64 * self.n_slots + 8 * slot, self.last[slot], self.epoch,
+                                self.status.data_ptr() + 4)
+        self.last[slot] = self.epoch
         return m
 
-    def wait(self, epoch: int | None = None, timeout_s: float = 60.0, stream=None):
-        """Stream-ordered wait until every rank's flag reached `epoch` (default:
-        the last launch's); raises later via check() if a peer timed out."""
+    def gather_slot(self, slot: int, pdl: bool = False):
+        g = N.GatherSlot()
+        g.n, g.pdl = self.world, 1 if pdl else 0
+        g.d_flags = self._flag(self.base, slot, 0)
+        for r, b in enumerate(self.peers):
+            g.ack[r] = self._ack(b, slot, self.rank)
+        return g
+
+    def wait(self, slot: int, release: bool = True, pdl: bool = False, timeout_s: float = 60.0, stream=None,
+             gslot=None):
+        """Stream-ordered: wait until every rank's records of the slot's last
+        epoch have landed here; release=True also releases the slot to every
+        producer (nothing later on the stream may read it -- else call
+        release() after the reader).  A timeout is reported by check()."""
         import ctypes as C
-        e = self.epoch if epoch is None else int(epoch)
-        N.check(N.lib().parva_gather_wait(C.c_void_p(self.base), C.c_int32(self.world), C.c_uint32(e),
+        g = gslot if gslot is not None else self.gather_slot(slot, pdl)
+        N.check(N.lib().parva_gather_wait(C.byref(g), C.c_uint32(self.last[slot]), C.c_int32(int(release)),
                                           C.c_int64(int(timeout_s * 1e9)), N.ptr(self.status),
                                           N.stream_handle(stream)), "parva_gather_wait")
 
+    def release(self, slot: int, stream=None):
+        import ctypes as C
+        g = self.gather_slot(slot)
+        N.check(N.lib().parva_gather_release(C.byref(g), C.c_uint32(self.last[slot]), N.stream_handle(stream)),
+                "parva_gather_release")
+
+    def records(self, slot: int):
+        """(config records, 128-byte plan records) of every rank in global order, from this process's copy."""
+        rows = self.slot_view(slot).view(self.world, self.blk).cpu().numpy()
+        return decode_gathered(rows, self.layout)
+
     def check(self):
-        if int(self.status.item()) != 0:
+        st = self.status.cpu().tolist()
+        if st[0] != 0:
             raise RuntimeError("fused all-gather: a peer's records did not arrive (timeout)")
+        if st[1] != 0:
+            raise RuntimeError("fused all-gather: a slot was not released in time (its launch stored nothing)")
 
     def close(self):
         import ctypes as C

@@ -98,9 +98,38 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
     dummy = C.c_void_p(16)
     assert L.parva_plan_batch_fused(None, None, 0, 0, None, None, None, None, 1, 4, None, 2, None,
                                     C.byref(m), None) == BAD
+    # a well-formed mirror whose sections are too small for the records
+    # (the copy would run past the config section into the next
+    # rank's part): rejected before any launch
+    tab, idx = N.ParvaTables(), N.ParvaIndex()
+    m = N.Mirror()
+    m.n, m.plan_bytes = 1, 128
+    m.plan[0] = m.cfg[0] = m.flag[0] = m.d_acks = 16
+    m.ticket = N.SlotTicket(16, 0, 1, None)
+    m.plan_capacity, m.cfg_capacity = 10 * 128, 110 * 8
+    args = (C.byref(tab), C.byref(idx), 10, 110, dummy, dummy, dummy, dummy, 1, 4, dummy)
+    assert L.parva_plan_batch_fused(*args, 0, dummy, C.byref(m), None) == BAD     # 32-B records > 8-B section
+    m.plan_capacity = 9 * 128
+    assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # plan section too small
+    m.plan_capacity, m.plan_bytes = 10 * 128, 64
+    assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # 64-B records need overflow
+    m.plan_bytes = 128
+    m.ticket = N.SlotTicket(16, 1, 1, None)
+    assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # epoch == prev_epoch
+    # overlapped launches need a ticket
+    assert L.parva_plan_batch_overlapped(*args, 2, dummy, None, None) == BAD
+    t = N.SlotTicket(None, 0, 1, None)
+    assert L.parva_plan_batch_overlapped(*args, 2, dummy, C.byref(t), None) == BAD
+    g = N.GatherSlot()
+    g.n = 1
     assert L.parva_gather_wait(None, 1, 1, 0, None, None) == BAD
-    assert L.parva_gather_wait(dummy, 0, 1, 0, dummy, None) == BAD
-    assert L.parva_gather_wait(dummy, 9, 1, 0, dummy, None) == BAD
+    assert L.parva_gather_wait(C.byref(g), 1, 1, 0, dummy, None) == BAD            # no flag row
+    g.d_flags = 16
+    assert L.parva_gather_wait(C.byref(g), 0, 0, 0, dummy, None) == BAD            # epoch 0
+    assert L.parva_gather_wait(C.byref(g), 1, 1, 0, dummy, None) == BAD            # release without ack words
+    g.n = 9
+    assert L.parva_gather_wait(C.byref(g), 1, 0, 0, dummy, None) == BAD
+    assert L.parva_gather_release(None, 1, None) == BAD
     assert L.parva_ipc_handle(None, None) == BAD
     assert L.parva_ipc_open(None, None) == BAD
     assert L.parva_ipc_alloc(C.c_size_t(0), C.byref(C.c_void_p())) == BAD
@@ -203,3 +232,44 @@ def test_deployment_map_json_round_trip():
     with pytest.raises(P.ValidationError):
         P.DeploymentMap.from_json('{"gpus":[{"id":0,"segments":[{"service":"a","instance_size":2,'
                                   '"batch_size":1,"process_count":1,"start_slot":5,"throughput_rps":1.0}]}]}')
+
+
+def test_stream_pack_arrays_matches_the_u16_pack():
+    """parva_stream_pack_arrays (plain int32 arrays, host thread pool) writes
+    exactly the block parva_stream_pack writes from u16 table ids; ids
+    outside [0, 65535) become 0xFFFF; bad offsets / capacity give -1."""
+    import ctypes as C
+    from paper_2409_14447_b200 import workloads as W
+    L = N.load_library()
+    fx = W.load_fixtures()
+    sb = W.scenario_batch(fx, 3_000, seed=4)
+    n, M = sb.rate.shape
+    rng = np.random.default_rng(9)
+    cnt = rng.integers(0, 30, 2_000)
+    cases = [(np.arange(n + 1, dtype=np.int32) * M, np.tile(np.arange(M, dtype=np.int32), n),
+              sb.rate.ravel().copy(), sb.bound.ravel().copy()),
+             (np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32),
+              rng.integers(-3, 70_000, int(cnt.sum())).astype(np.int32),
+              rng.random(int(cnt.sum())), rng.random(int(cnt.sum())))]
+    for off, tab, rate, bound in cases:
+        k = len(off) - 1
+        for chunk in (1, 7, 32):
+            cap = int(L.parva_stream_bytes(C.c_int32(k), N.np_ptr(off), C.c_int32(chunk)))
+            t16 = np.where((tab < 0) | (tab >= 65535), 65535, tab).astype(np.uint16)
+            a = np.zeros(cap, np.uint8)
+            na = L.parva_stream_pack(C.c_int32(k), N.np_ptr(off), N.np_ptr(t16), N.np_ptr(rate), N.np_ptr(bound),
+                                     C.c_int32(chunk), N.np_ptr(a), C.c_int64(cap))
+            for threads in (1, 3, 0):
+                b = np.full(cap, 0xCD, np.uint8)
+                nb = L.parva_stream_pack_arrays(C.c_int32(k), N.np_ptr(off), N.np_ptr(tab), N.np_ptr(rate),
+                                                N.np_ptr(bound), C.c_int32(chunk), N.np_ptr(b), C.c_int64(cap),
+                                                C.c_int32(threads))
+                assert na == nb > 0 and a[:na].tobytes() == b[:nb].tobytes(), (k, chunk, threads)
+            assert L.parva_stream_pack_arrays(C.c_int32(k), N.np_ptr(off), N.np_ptr(tab), N.np_ptr(rate),
+                                              N.np_ptr(bound), C.c_int32(chunk), N.np_ptr(b),
+                                              C.c_int64(na - 16), C.c_int32(0)) == -1
+    bad = np.array([0, 5, 3, 8], dtype=np.int32)
+    z = np.zeros(8)
+    buf = np.zeros(4096, np.uint8)
+    assert L.parva_stream_pack_arrays(C.c_int32(3), N.np_ptr(bad), N.np_ptr(np.zeros(8, np.int32)), N.np_ptr(z),
+                                      N.np_ptr(z), C.c_int32(2), N.np_ptr(buf), C.c_int64(4096), C.c_int32(0)) == -1

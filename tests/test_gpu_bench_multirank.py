@@ -28,12 +28,15 @@ def test_bench_two_ranks(gather):
     env = dict(os.environ, PARVA_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "bench.py"),
-           "--gpus", "2", "--steps", "5", "--warmup", "3", "--no-cpu", "--no-extra", "--no-sweep",
+           "--gpus", "2", "--steps", "5", "--warmup", "3", "--no-cpu", "--no-extra", "--sweep-workloads", "500",
            "--gather", gather]
     r = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["gather"] == gather
-    assert line["parity_vs_oracle_first_2000"] is True
-    assert line["e2e"]["plan_records_equal_device_path"] is True
-    assert line["value"] > 0 and line["gpu_launches"] == 5
+    sw = line["configurator_sweep"]      # sharded C3: one all-gather of config records
+    assert sw["parity_vs_oracle_first_1000"] is True and sw["parity_gathered_sample"] is True
+    par = line["parity_timed_steps"]
+    assert par["equal"] is True and par["steps_checked"] == 5 and par["ranks"] == 2
+    assert line["e2e"]["records_equal_oracle_last_steps"] is True
+    assert line["value"] > 0 and line["gpu_launches"] == 5 * (2 if gather == "fused" else 1)

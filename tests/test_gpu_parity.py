@@ -237,14 +237,20 @@ def test_plan_batch_overlapped_back_to_back(fx):
     outs = [B.BatchResult(N.empty_records(big[1], TINY_DTYPE), N.empty_records(big[0], PLAN_DTYPE), big[0], big[1],
                           CFG_TINY) for _ in range(3)]
     last = {}
+    ring = B.SlotRing(3)
     for i in range(24):
         b, r = (5 * i + 1) % 6, i % 3
         o = outs[r]
         k, m = int(ins[b][0].shape[0]) - 1, int(ins[b][1].shape[0])
         view = B.BatchResult(o.cfg[:m], o.plan[:k], k, m, CFG_TINY)
-        B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view, overlap=(i != 11))
+        if i == 11:
+            torch.cuda.synchronize()     # a plain launch: every earlier launch into the slot is done
+            B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view)
+        else:
+            B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view, overlap=True, ticket=ring.ticket(r))
         last[r] = (b, view)
     torch.cuda.synchronize()
+    ring.check()
     for r, (b, view) in last.items():
         cfg, plan = view.host()
         assert plan.tobytes() == exp[b][1], (r, b)
@@ -732,3 +738,41 @@ def test_mapped_entry_rejects_pageable_memory(fx):
     mb.run(dt)              # and the pinned path still works afterwards
     ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off, tab, sb.rate.ravel(), sb.bound.ravel())
     assert mb.outputs()[1].tobytes() == oplan.tobytes()
+
+
+def test_host_entry_mapped_pack_every_step(fx):
+    """The e2e pipeline of bench.py: every step packs a different batch of
+    plain host arrays into its slot's pinned block (parva_stream_pack_arrays)
+    and submits it, 3 calls in flight; every step's records == oracle."""
+    from paper_2409_14447_b200.records import tiny_config
+    dt = N.device_tables_for(fx.tables)
+    pt = pack_tables(fx.tables)
+    batches = []
+    for seed in range(60, 66):
+        sb = W.scenario_batch(fx, 4_000, seed=seed)
+        k, M = sb.rate.shape
+        off = np.arange(k + 1, dtype=np.int32) * M
+        tab = np.tile(np.arange(M, dtype=np.int32), k)
+        batches.append((off, tab, sb.rate.ravel().copy(), sb.bound.ravel().copy()))
+    exp = []
+    for b in batches:
+        ocfg, oplan = oracle.plan_batch_records(pt, *b)
+        exp.append((tiny_config(ocfg).tobytes(), oplan.tobytes()))
+    D = 3
+    mb = B.MappedHostBatch(*batches[0], cfg_format=2, plan_bytes=64, depth=D)
+    inflight = {}
+    for i in range(20):
+        slot = i % D
+        if slot in inflight:
+            mb.wait(slot)
+            cfg, plan = mb.outputs(slot)
+            j = inflight.pop(slot)
+            assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0], (i, j)
+        j = (7 * i) % len(batches)
+        mb.fill(*batches[j], slot=slot)
+        mb.submit(dt, slot)
+        inflight[slot] = j
+    for slot, j in inflight.items():
+        mb.wait(slot)
+        cfg, plan = mb.outputs(slot)
+        assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0], j

@@ -1,0 +1,124 @@
+#!/usr/bin/env python3
+"""Time the reference itself (`migplan`, pure Python, installed unmodified
+into baseline/_ref by `pip install --no-deps --target baseline/_ref`) on the
+bench's workloads, on this host's cores.  Used by bench.py's cpu_baseline
+leg; prints one JSON object.
+
+    python tools/ref_python_bench.py c2 --n 2000 --procs 1
+    python tools/ref_python_bench.py c5
+
+Timed region per scenario = the reference's own (pipeline.py:95-103):
+configure_service for every service, relocate_segments, optimize_allocation;
+tables are prepared once outside it (pipeline.py:94).  C2 inputs come from
+the same generator as the GPU arm (seed 0); an infeasible
+scenario raises InfeasibleSLOError inside configure, as in plan_services.
+--procs > 1: a fork Pool over strided scenario chunks, wall time of the pool.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[1]
+REF = REPO / "baseline" / "_ref"
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REF))
+
+import migplan  # noqa: E402  (the reference, unmodified)
+from migplan import allocator as RA  # noqa: E402
+from migplan import configurator as RC  # noqa: E402
+from migplan import pipeline as RP  # noqa: E402
+
+from paper_2409_14447_b200 import workloads as W  # noqa: E402  (input generator only)
+
+_STATE = {}
+
+
+def ref_tables(fx):
+    tables = {}
+    for m, t in fx.tables.items():
+        pts = tuple(migplan.ProfilePoint(m, p.instance_size, p.batch_size, p.process_count, p.throughput, p.latency,
+                                         p.memory_required) for p in t.points)
+        tables[m] = migplan.ProfileTable(m, pts)
+    return RP.prepare_tables(tables, RP.PlanOptions())
+
+
+def plan_one(services, prepared):
+    """configure -> relocate -> optimize, as plan_services' timed region."""
+    configured = [RC.configure_service(s, prepared[s.model_id]) for s in services]
+    dmap = RA.relocate_segments(configured)
+    return RA.optimize_allocation(dmap, configured, threshold=4)
+
+
+def _c2_chunk(args):
+    lo, hi, step = args
+    sb, prepared = _STATE["sb"], _STATE["prepared"]
+    done = infeasible = 0
+    t0 = time.perf_counter()
+    for k in range(lo, hi, step):
+        services = [RC.make_service(f"{m}", m, float(sb.rate[k, j]), float(sb.slo[k, j]))
+                    for j, m in enumerate(sb.models)]
+        try:
+            plan_one(services, prepared)
+        except migplan.InfeasibleSLOError:
+            infeasible += 1
+        done += 1
+    return done, infeasible, time.perf_counter() - t0
+
+
+def run_c2(n, procs):
+    fx = W.load_fixtures()
+    _STATE["prepared"] = ref_tables(fx)
+    _STATE["sb"] = W.scenario_batch(fx, n, seed=0)
+    if procs <= 1:
+        done, inf, el = _c2_chunk((0, n, 1))
+    else:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            pool.map(_c2_chunk, [(r, min(n, 64 * procs), procs) for r in range(procs)])   # warm the workers
+            t0 = time.perf_counter()
+            parts = pool.map(_c2_chunk, [(r, n, procs) for r in range(procs)])
+            el = time.perf_counter() - t0
+        done, inf = sum(p[0] for p in parts), sum(p[1] for p in parts)
+    return {"config": "C2", "scenarios": done, "infeasible": inf, "seconds": el, "scenarios_per_s": done / el,
+            "procs": procs}
+
+
+def run_c5():
+    fx = W.load_fixtures()
+    prepared = ref_tables(fx)
+    rates = W.c5_rates()
+    services = [RC.make_service(f"d121#{i}", W.C5_MODEL, float(r), W.C5_SLO) for i, r in enumerate(rates)]
+    t0 = time.perf_counter()
+    configured = [RC.configure_service(s, prepared[s.model_id]) for s in services]
+    t1 = time.perf_counter()
+    dmap = RA.relocate_segments(configured)
+    t2 = time.perf_counter()
+    unopt = dmap.gpu_count
+    out = RA.optimize_allocation(dmap, configured, threshold=4)
+    t3 = time.perf_counter()
+    return {"config": "C5", "services": len(services), "gpus_before_optimize": unopt, "gpus": out.gpu_count,
+            "configure_s": t1 - t0, "relocate_s": t2 - t1, "optimize_s": t3 - t2, "seconds": t3 - t0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=["c2", "c5"])
+    ap.add_argument("--n", type=int, default=2000)
+    ap.add_argument("--procs", type=int, default=1)
+    a = ap.parse_args()
+    res = run_c2(a.n, a.procs) if a.config == "c2" else run_c5()
+    res["python"] = sys.version.split()[0]
+    res["reference"] = "migplan (baseline/_ref, unmodified)"
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    main()
