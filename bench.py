@@ -433,7 +433,7 @@ def main():
                 m = peer.mirror(s, overlap=True)
                 out.append((s, a + (C.byref(m), sh), m))
             else:
-                t = ring.ticket(s)
+                t = ring.ticket(s, n)
                 out.append((s, a + (C.byref(t), sh), t))
         return out
 

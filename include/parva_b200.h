@@ -79,6 +79,7 @@ typedef struct {
   const int32_t* d_seg_count; /* [n_tables * 5]                    */
   int32_t n_tables;
   int64_t n_points;
+  int32_t max_seg_points;     /* max of seg_count (PARVA_CFG_TINY needs <= 254) */
 } parva_tables;
 
 /* Raw (unprepared) tables, same grouping: every point of the source
@@ -130,7 +131,8 @@ typedef struct {
 } parva_config_compact;
 
 /* 8-byte tiny config record, for tables with at most 254 points per
- * (table, size): best[c] = 255 if absent; opt_last = opt | last << 4 (15 =
+ * (table, size) -- every entry rejects PARVA_CFG_TINY with PARVA_BAD_INPUT
+ * when tables->max_seg_points > 254: best[c] = 255 if absent; opt_last = opt | last << 4 (15 =
  * none); status_flags = status | 0x80 if count > 255 (count saturates at
  * 255 -- more than 224 segments cannot fit the fast path anyway). */
 typedef struct {
@@ -216,21 +218,20 @@ int parva_plan_batch(const parva_tables* tables, const parva_index* index,
                      void* stream);
 
 /* Output-slot ticket of an overlapped launch.  A caller that keeps several
- * launches in flight rotates their outputs over slots; each slot owns two
- * u32 words of device memory (d_words, zeroed before first use: the epoch of
- * the slot's last completed launch, and a CTA counter).  Every CTA of a
- * launch waits, before its first store, until d_words[0] == prev_epoch (the
- * slot's previous launch has completed); the launch's last CTA publishes
- * `epoch` there.  So launches into one slot never overlap, however many
- * grids are in flight, and consecutive slots still overlap freely.  A wait
- * longer than 60 s (environment PARVA_TICKET_TIMEOUT_MS overrides) stores
- * PARVA_LAUNCH_ERROR into *d_err (if non-NULL) and the CTA stores nothing
- * (no hang). */
+ * launches in flight rotates their outputs over slots; each slot owns a u64
+ * completion counter in device memory (zeroed before first use) to which
+ * every CTA of a launch into the slot adds its scenario count after its last
+ * store (one release reduction).  Before its first store every CTA waits
+ * until the counter has reached wait_count -- the scenarios of all earlier
+ * launches into the slot -- so launches into one slot never overlap, however
+ * many grids are in flight, while consecutive slots still overlap freely.  A
+ * wait longer than 60 s (environment PARVA_TICKET_TIMEOUT_MS overrides)
+ * stores PARVA_LAUNCH_ERROR into *d_err (if non-NULL) and the CTA stores
+ * nothing (no hang). */
 typedef struct {
-  uint32_t* d_words;     /* [2] per slot, device memory                      */
-  uint32_t prev_epoch;   /* epoch of the slot's previous launch, 0 = first   */
-  uint32_t epoch;        /* this launch's epoch: nonzero, != prev_epoch      */
-  int32_t* d_err;        /* optional error word (device)                     */
+  unsigned long long* d_count;     /* the slot's completion counter (device)         */
+  unsigned long long wait_count;   /* scenarios of the earlier launches into the slot */
+  int32_t* d_err;                  /* optional error word (device)                   */
 } parva_slot_ticket;
 
 /* parva_plan_batch as a programmatic dependent launch: it may start while
@@ -260,9 +261,9 @@ int parva_plan_batch_overlapped(const parva_tables* tables, const parva_index* i
  * payload does not fit has status PARVA_SPILLED and its full record at the
  * same index of the overflow section) -- 152 B per C2 scenario on the wire
  * instead of 216.  Before its first store every CTA waits for the slot's
- * ticket (this rank's previous launch into the slot has completed) and for
+ * ticket (this rank's earlier launches into the slot have completed) and for
  * every rank's release of the slot's previous epoch (d_acks[m] >=
- * ticket.prev_epoch); after a system-scope fence the last CTA stores the
+ * prev_epoch); after a system-scope fence the last CTA (d_done) stores the
  * epoch into this rank's flag word of the slot on every rank.  The call is
  * rejected (PARVA_BAD_INPUT) when the records would not fit the sections
  * (n_scenarios * plan_bytes > plan_capacity, n_services * config record
@@ -275,13 +276,16 @@ typedef struct {
   void* spill[8];          /* its overflow section (plan_bytes == 64)          */
   uint32_t* flag[8];       /* this rank's flag word of the slot on rank m      */
   const uint32_t* d_acks;  /* the slot's ack row in this rank's buffer [n]     */
+  uint32_t* d_done;        /* the slot's CTA counter (device, zeroed; self-resetting) */
   void* d_spill;           /* local overflow records (plan_bytes == 64)        */
   int64_t plan_capacity;   /* bytes of one rank's plan section                 */
   int64_t cfg_capacity;    /* bytes of one rank's config section               */
   int64_t spill_capacity;  /* bytes of one rank's overflow section             */
   int32_t plan_bytes;      /* 128, or 64 (overflow section used)               */
+  uint32_t epoch;          /* this launch's epoch (nonzero), published in the flags */
+  uint32_t prev_epoch;     /* the slot's previous epoch (0: first use)         */
   int32_t reserved;
-  parva_slot_ticket ticket;
+  parva_slot_ticket ticket;/* this rank's launches into the slot              */
 } parva_mirror;
 int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
                            int32_t n_scenarios, int32_t n_services, const int32_t* d_scen_off,

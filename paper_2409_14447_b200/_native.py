@@ -26,7 +26,8 @@ _LOCK = threading.Lock()
 
 class ParvaTables(C.Structure):
     _fields_ = [("d_pts", C.c_void_p), ("d_seg_start", C.c_void_p),
-                ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32), ("n_points", C.c_int64)]
+                ("d_seg_count", C.c_void_p), ("n_tables", C.c_int32), ("n_points", C.c_int64),
+                ("max_seg_points", C.c_int32)]
 
 
 class ParvaRawTables(C.Structure):
@@ -89,16 +90,16 @@ EXPORTS = (
 class SlotTicket(C.Structure):
     """parva_slot_ticket (include/parva_b200.h): serializes overlapped launches
     that share an output slot."""
-    _fields_ = [("d_words", C.c_void_p), ("prev_epoch", C.c_uint32), ("epoch", C.c_uint32), ("d_err", C.c_void_p)]
+    _fields_ = [("d_count", C.c_void_p), ("wait_count", C.c_uint64), ("d_err", C.c_void_p)]
 
 
 class Mirror(C.Structure):
     """parva_mirror (include/parva_b200.h): the fused all-gather's destinations."""
     _fields_ = [("n", C.c_int32), ("overlap", C.c_int32), ("plan", C.c_void_p * 8), ("cfg", C.c_void_p * 8),
-                ("spill", C.c_void_p * 8), ("flag", C.c_void_p * 8), ("d_acks", C.c_void_p),
+                ("spill", C.c_void_p * 8), ("flag", C.c_void_p * 8), ("d_acks", C.c_void_p), ("d_done", C.c_void_p),
                 ("d_spill", C.c_void_p), ("plan_capacity", C.c_int64), ("cfg_capacity", C.c_int64),
-                ("spill_capacity", C.c_int64), ("plan_bytes", C.c_int32), ("reserved", C.c_int32),
-                ("ticket", SlotTicket)]
+                ("spill_capacity", C.c_int64), ("plan_bytes", C.c_int32), ("epoch", C.c_uint32),
+                ("prev_epoch", C.c_uint32), ("reserved", C.c_int32), ("ticket", SlotTicket)]
 
 
 class GatherSlot(C.Structure):
@@ -246,8 +247,9 @@ class DeviceTables:
     def _finish(self, build_index: bool):
         import torch
         packed = self.packed
+        self.max_seg_points = int(packed.seg_count.max(initial=0))
         self.struct = ParvaTables(self.pts.data_ptr(), self.seg_start.data_ptr(),
-                                  self.seg_count.data_ptr(), packed.n_tables, packed.n_points)
+                                  self.seg_count.data_ptr(), packed.n_tables, packed.n_points, self.max_seg_points)
         self.index = None
         self.index_struct = None
         if build_index and packed.n_points and int(packed.seg_count.max(initial=0)) <= 4096:

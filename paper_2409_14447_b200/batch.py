@@ -69,26 +69,24 @@ class BatchResult:
 
 class SlotRing:
     """Output slots of overlapped launches (parva_slot_ticket): `n_slots`
-    slots, each with two device words (the epoch of its last completed
-    launch, a CTA counter).  ticket(slot) is the ticket of the next launch
-    into `slot`: its CTAs store nothing until the slot's previous launch has
-    completed, so overlapped launches that share a slot never overlap each
-    other -- safe by construction, however many grids are in flight."""
+    slots, each with a u64 completion counter on the device.  ticket(slot,
+    n_scenarios) is the ticket of the next launch into `slot`: its CTAs
+    store nothing until every scenario of the slot's earlier launches is
+    done, so overlapped launches that share a slot never overlap each other
+    -- safe by construction, however many grids are in flight."""
 
     def __init__(self, n_slots: int):
         torch = N.require_cuda()
         if n_slots < 1:
             raise ValueError("n_slots must be >= 1")
         self.n_slots = int(n_slots)
-        self.words = torch.zeros(2 * self.n_slots, dtype=torch.int32, device="cuda")
+        self.counts = torch.zeros(self.n_slots, dtype=torch.int64, device="cuda")
         self.err = torch.zeros(1, dtype=torch.int32, device="cuda")
-        self.last = [0] * self.n_slots
-        self.epoch = 0
+        self.issued = [0] * self.n_slots       # scenarios launched into each slot so far
 
-    def ticket(self, slot: int) -> N.SlotTicket:
-        self.epoch = self.epoch % 0xFFFFFFFF + 1
-        t = N.SlotTicket(self.words.data_ptr() + 8 * slot, self.last[slot], self.epoch, self.err.data_ptr())
-        self.last[slot] = self.epoch
+    def ticket(self, slot: int, n_scenarios: int) -> N.SlotTicket:
+        t = N.SlotTicket(self.counts.data_ptr() + 8 * slot, self.issued[slot], self.err.data_ptr())
+        self.issued[slot] += int(n_scenarios)
         return t
 
     def check(self):
@@ -108,7 +106,8 @@ def plan_batch(dt: N.DeviceTables, scen_off, svc_table, svc_rate, svc_bound, opt
     call on the stream is still running.  It needs the `ticket` of `out`'s
     slot (SlotRing.ticket): launches into one slot are serialized on the
     device.  mirror (an N.Mirror, from distributed.PeerGather.mirror) adds
-    the fused all-gather (parva_plan_batch_fused); it carries its own ticket."""
+    the fused all-gather (parva_plan_batch_fused); it carries its own ticket.
+    A ticket is issued for exactly one launch of its n_scenarios."""
     torch = N.require_cuda()
     if overlap and mirror is None and ticket is None:
         raise ValueError("overlap=True needs the slot ticket of `out` (SlotRing.ticket)")

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <thread>
@@ -71,9 +72,8 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
       s_timeout_ms = e ? std::max(1ll, std::atoll(e)) : 60000ll;
     }
     A.ticket_timeout_ns = (unsigned long long)s_timeout_ms * 1000000ull;
-    A.slot_words = ticket->d_words;
-    A.slot_prev = ticket->prev_epoch;
-    A.slot_epoch = ticket->epoch;
+    A.slot_count = (unsigned long long*)ticket->d_count;
+    A.slot_wait = ticket->wait_count;
     A.err_word = ticket->d_err;
   }
   if (mirror) {
@@ -85,6 +85,9 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
       A.peer_flag[m] = mirror->flag[m];
     }
     A.ack_row = mirror->d_acks;
+    A.ack_prev = mirror->prev_epoch;
+    A.flag_epoch = mirror->epoch;
+    A.done_ctas = mirror->d_done;
     if (mirror->plan_bytes == 64) {
       // 64-byte records; a spilled scenario's full record at the same index
       // of the overflow area (local, then mirrored)
@@ -102,6 +105,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   A.seg_count = tables->d_seg_count;
   A.n_tables = tables->n_tables;
   A.n_points = tables->n_points;
+  A.max_seg_points = tables->max_seg_points;
   A.n_scen = n_scenarios;
   A.n_svc = n_services;
   A.scen_off = d_scen_off;
@@ -124,9 +128,7 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   return parva::launch_plan_batch(A, stream);
 }
 
-static bool ticket_ok(const parva_slot_ticket* t) {
-  return t && t->d_words && t->epoch != 0 && t->epoch != t->prev_epoch;
-}
+static bool ticket_ok(const parva_slot_ticket* t) { return t && t->d_count; }
 
 int parva_plan_batch(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
                      int32_t n_services, const int32_t* d_scen_off, const int32_t* d_svc_table, const double* d_svc_rate,
@@ -164,7 +166,8 @@ int parva_plan_batch_fused(const parva_tables* tables, const parva_index* index,
                            void* stream) {
   if (!tables || !index || n_scenarios < 0 || !d_cfg || !d_plan || !mirror) return PARVA_BAD_INPUT;
   if (cfg_format < PARVA_CFG_FULL || cfg_format > PARVA_CFG_TINY) return PARVA_BAD_INPUT;
-  if (mirror->n < 1 || mirror->n > parva::kMaxMirror || !mirror->d_acks || !ticket_ok(&mirror->ticket))
+  if (mirror->n < 1 || mirror->n > parva::kMaxMirror || !mirror->d_acks || !mirror->d_done ||
+      !ticket_ok(&mirror->ticket) || mirror->epoch == 0 || mirror->epoch == mirror->prev_epoch)
     return PARVA_BAD_INPUT;
   if (mirror->plan_bytes != 128 && mirror->plan_bytes != 64) return PARVA_BAD_INPUT;
   if (n_scenarios == 0) return PARVA_BAD_INPUT;   // nothing would publish the epoch
@@ -310,7 +313,8 @@ int parva_plan_host(const parva_tables* tables, const parva_index* index, int32_
       parva::PlanArgs A;
       A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
       A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
-      A.n_points = tables->n_points; A.n_scen = b - a; A.n_svc = sb - sa; A.scen_off = d_off + a; A.svc_table = d_tab;
+      A.n_points = tables->n_points; A.max_seg_points = tables->max_seg_points;
+      A.n_scen = b - a; A.n_svc = sb - sa; A.scen_off = d_off + a; A.svc_table = d_tab;
       A.svc_table16 = nullptr;
       A.svc_rate = d_rate; A.svc_bound = d_bound; A.optimize = optimize; A.threshold = threshold;
       A.cfg_given = 0; A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit; A.cfg = d_cfg;
@@ -462,7 +466,8 @@ int parva_plan_host_packed(const parva_tables* tables, const parva_index* index,
         parva::PlanArgs A;
         A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
         A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
-        A.n_points = tables->n_points; A.n_scen = h_k[c]; A.n_svc = h_m[c];
+        A.n_points = tables->n_points; A.max_seg_points = tables->max_seg_points;
+        A.n_scen = h_k[c]; A.n_svc = h_m[c];
         A.scen_off = (const int32_t*)(d_in[c] + L[c].in_scen_off);
         A.svc_table = nullptr; A.svc_table16 = (const uint16_t*)(d_in[c] + L[c].in_table);
         A.svc_rate = (const double*)(d_in[c] + L[c].in_rate);
@@ -595,15 +600,24 @@ int64_t parva_stream_pack(int32_t n_scenarios, const int32_t* h_scen_off, const 
 // caller's thread takes part, workers sleep on a condition variable between
 // calls (no OpenMP runtime next to torch's).
 namespace {
+// Workers spin (pause) for a while after each call before sleeping on a
+// condition variable: a pipelined caller packs a batch every ~50-100 us, and
+// a futex wake-up of every worker per call cost ~55 us on the B200 host.
+// A call's parameters live in one of two job records (by generation); a
+// worker registers in the record (active) before re-checking that the
+// generation is still current, so a call never returns -- and its record is
+// never rewritten -- while a worker still reads it.
 class PackPool {
  public:
   explicit PackPool(int n) {
+    const char* e = std::getenv("PARVA_PACK_SPIN_US");
+    spin_us_ = e ? std::max(0, std::atoi(e)) : 2000;
     for (int i = 0; i < n; i++) th_.emplace_back([this] { worker(); });
   }
   ~PackPool() {
+    stop_.store(true);
     {
       std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
     }
     cv_.notify_all();
     for (auto& t : th_) t.join();
@@ -611,61 +625,71 @@ class PackPool {
   int size() const { return (int)th_.size() + 1; }
   // fn(task) for task in [0, n_tasks), on up to `width` threads (caller included)
   void run(int n_tasks, int width, const std::function<void(int)>& fn) {
-    std::unique_lock<std::mutex> call(call_mu_);   // one call at a time
-    {
+    std::lock_guard<std::mutex> call(call_mu_);   // one call at a time
+    const uint64_t g = gen_.load() + 1;
+    Job& J = jobs_[g & 1];
+    while (J.active.load() != 0) spin_pause();      // (a stale worker of generation g - 2 leaving)
+    J.fn = &fn;
+    J.n_tasks = n_tasks;
+    J.width = std::max(0, width - 1);
+    J.next.store(0);
+    J.taken.store(0);
+    J.remaining.store(n_tasks);
+    gen_.store(g);
+    if (sleepers_.load() > 0) {
       std::lock_guard<std::mutex> lk(mu_);
-      job_ = &fn;
-      n_tasks_ = n_tasks;
-      next_.store(0);
-      remaining_.store(n_tasks);
-      width_ = std::max(0, width - 1);
-      taken_ = 0;
-      gen_++;
+      cv_.notify_all();
     }
-    cv_.notify_all();
-    drain();
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [this] { return remaining_.load() == 0 && active_ == 0; });
-    job_ = nullptr;
+    drain(J);
+    while (J.remaining.load() != 0 || J.active.load() != 0) spin_pause();
   }
 
  private:
-  void drain() {
+  struct Job {
+    const std::function<void(int)>* fn = nullptr;
+    int n_tasks = 0, width = 0;
+    std::atomic<int> next{0}, taken{0}, remaining{0}, active{0};
+  };
+  static void spin_pause() { __builtin_ia32_pause(); }
+  static void drain(Job& J) {
     for (;;) {
-      const int i = next_.fetch_add(1);
-      if (i >= n_tasks_) return;
-      (*job_)(i);
-      remaining_.fetch_sub(1);
+      const int i = J.next.fetch_add(1);
+      if (i >= J.n_tasks) return;
+      (*J.fn)(i);
+      J.remaining.fetch_sub(1);
     }
   }
   void worker() {
     uint64_t seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
-        if (taken_ >= width_) continue;   // enough threads on this call
-        taken_++;
-        active_++;
+      const auto t0 = std::chrono::steady_clock::now();
+      uint64_t g;
+      for (int k = 0; (g = gen_.load()) == seen && !stop_.load(); k++) {
+        spin_pause();
+        if ((k & 255) == 255 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) {
+          std::unique_lock<std::mutex> lk(mu_);
+          sleepers_.fetch_add(1);
+          cv_.wait(lk, [&] { return gen_.load() != seen || stop_.load(); });
+          sleepers_.fetch_sub(1);
+        }
       }
-      drain();
-      {
-        std::lock_guard<std::mutex> lk(mu_);
-        active_--;
-      }
-      done_cv_.notify_all();
+      if (stop_.load()) return;
+      seen = g;
+      Job& J = jobs_[g & 1];
+      J.active.fetch_add(1);
+      if (gen_.load() == g && J.taken.fetch_add(1) < J.width) drain(J);
+      J.active.fetch_sub(1);
     }
   }
   std::vector<std::thread> th_;
   std::mutex mu_, call_mu_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(int)>* job_ = nullptr;
-  int n_tasks_ = 0, width_ = 0, active_ = 0, taken_ = 0;
-  std::atomic<int> next_{0}, remaining_{0};
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::condition_variable cv_;
+  Job jobs_[2];
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> sleepers_{0};
+  std::atomic<bool> stop_{false};
+  int spin_us_ = 2000;
 };
 
 PackPool& pack_pool() {
@@ -935,7 +959,8 @@ static int plan_host_mapped(const parva_tables* tables, const parva_index* index
     parva::PlanArgs A;
     A.pts = tables->d_pts; A.idx_lat = index->d_lat_sorted; A.idx_best = index->d_best; A.idx_tp = index->d_tp;
     A.seg_start = tables->d_seg_start; A.seg_count = tables->d_seg_count; A.n_tables = tables->n_tables;
-    A.n_points = tables->n_points; A.n_scen = n_scenarios; A.n_svc = n_services;
+    A.n_points = tables->n_points; A.max_seg_points = tables->max_seg_points;
+    A.n_scen = n_scenarios; A.n_svc = n_services;
     A.scen_off = nullptr; A.svc_table = nullptr; A.svc_table16 = nullptr; A.svc_rate = nullptr; A.svc_bound = nullptr;
     A.optimize = optimize; A.threshold = threshold; A.cfg_given = 0;
     A.smem_index = tables->n_points * 18 <= (int64_t)kSmemIndexLimit;

@@ -19,6 +19,7 @@ struct PlanArgs {
   const int32_t* seg_count;
   int n_tables;
   int64_t n_points;
+  int max_seg_points = -1;       // tables->max_seg_points (PARVA_CFG_TINY needs <= 254)
   int n_scen;
   int n_svc;                     // services [scen_off[0], scen_off[0] + n_svc)
   const int32_t* scen_off;
@@ -58,14 +59,15 @@ struct PlanArgs {
   // streamed call on the stream is still finishing its last scenarios
   uint32_t* done_word = nullptr;
   int pdl = 0;
-  // slot ticket (overlapped and fused launches; parva_slot_ticket): before
-  // its first store every CTA waits until slot_words[0] == slot_prev, i.e.
-  // the previous launch into the same output slot has completed; the last
-  // CTA of the grid (counter slot_words[1], reset before publishing) stores
-  // slot_epoch into slot_words[0].  A wait that times out stores
-  // PARVA_LAUNCH_ERROR into *err_word and the CTA exits without storing.
-  uint32_t* slot_words = nullptr;
-  uint32_t slot_prev = 0, slot_epoch = 0;
+  // slot ticket (overlapped and fused launches; parva_slot_ticket): every
+  // CTA adds its scenario count to the slot's completion counter
+  // (*slot_count, one fire-and-forget release reduction after its last
+  // store); before its first store, thread 0 waits until the counter has
+  // reached slot_wait -- every scenario of the slot's earlier launches is
+  // done.  A wait that times out stores PARVA_LAUNCH_ERROR into *err_word
+  // and the CTA exits without storing.
+  unsigned long long* slot_count = nullptr;
+  unsigned long long slot_wait = 0;
   int32_t* err_word = nullptr;
   unsigned long long ticket_timeout_ns = 60ull * 1000 * 1000 * 1000;   // PARVA_TICKET_TIMEOUT_MS
   // fused all-gather (device path): each tile's plan / config records (and,
@@ -73,16 +75,18 @@ struct PlanArgs {
   // also stored at mirror_plan[m] / mirror_cfg[m] / mirror_spill[m] (the same
   // record index), i.e. into this rank's part of slot s on every rank over
   // peer memory.  Before storing, the CTAs also wait until every rank has
-  // released the slot's previous epoch (ack_row[m] >= slot_prev, written by
-  // rank m's parva_gather_wait).  The last CTA stores slot_epoch into
-  // peer_flag[m] (this rank's flag word of slot s on rank m) after a
-  // system-scope fence.
+  // released the slot's previous epoch (ack_row[m] >= ack_prev, written by
+  // rank m's parva_gather_wait).  The last CTA (counter *done_ctas, reset
+  // before publishing) stores flag_epoch into peer_flag[m] (this rank's flag
+  // word of slot s on rank m) after a system-scope fence.
   int n_mirror = 0;
   uint8_t* mirror_plan[kMaxMirror] = {};
   uint8_t* mirror_cfg[kMaxMirror] = {};
   uint8_t* mirror_spill[kMaxMirror] = {};
   uint32_t* peer_flag[kMaxMirror] = {};
   const uint32_t* ack_row = nullptr;
+  uint32_t ack_prev = 0, flag_epoch = 0;
+  uint32_t* done_ctas = nullptr;
 };
 
 #ifndef PARVA_STREAM_SLICE

@@ -116,20 +116,31 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// One thread per CTA, before the CTA's first store: the slot's previous
-// launch has completed (its last CTA published slot_prev) and, for the fused
-// all-gather, every rank has released the slot's previous epoch.  Launches
-// into one slot are therefore serialized however many overlapped grids are
-// in flight.  No deadlock: a programmatic dependent launch starts only after
-// every CTA of its predecessor has started, so every earlier grid is
-// resident or finished.  Returns false after the timeout (error recorded).
-__device__ __noinline__ bool ticket_wait(const uint32_t* words, uint32_t prev, const uint32_t* acks, int n_acks,
+// One thread per CTA, before the CTA's first store: every scenario of the
+// slot's earlier launches is done (completion counter >= wait) and, for the
+// fused all-gather, every rank has released the slot's previous epoch.
+// Launches into one slot are therefore serialized however many overlapped
+// grids are in flight.  No deadlock: a programmatic dependent launch starts
+// only after every CTA of its predecessor has started, so every earlier grid
+// is resident or finished.  Returns false after the timeout (error recorded).
+__device__ __noinline__ bool ticket_wait(const unsigned long long* count, unsigned long long wait,
+                                         const uint32_t* acks, int n_acks, uint32_t ack_prev,
                                          unsigned long long timeout_ns, int32_t* err) {
+  // relaxed polls: nothing the earlier launches wrote is read, only
+  // overwritten, and no store is issued before the poll has returned.  (An
+  // acquire at gpu scope invalidates the SM's L1 -- and with it the index
+  // the SM's overlapped CTAs read through L1: +2 us per C2 step.)
   const unsigned long long t0 = global_ns();
   for (unsigned ns = 32;; ns = ns < 1024 ? 2 * ns : ns) {
-    bool ok = ld_acquire_gpu_u32(words) == prev;
-    if (ok && acks && prev)
-      for (int m = 0; m < n_acks && ok; m++) ok = (int32_t)(ld_acquire_sys_u32(acks + m) - prev) >= 0;
+    unsigned long long c;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(count) : "memory");
+    bool ok = c >= wait;
+    if (ok && acks && ack_prev)
+      for (int m = 0; m < n_acks && ok; m++) {
+        uint32_t a;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(a) : "l"(acks + m) : "memory");
+        ok = (int32_t)(a - ack_prev) >= 0;
+      }
     if (ok) return true;
     if (global_ns() - t0 > timeout_ns) {
       if (err) atomicExch(err, (int32_t)PARVA_LAUNCH_ERROR);
@@ -454,6 +465,7 @@ struct alignas(16) TileSmem {
   int32_t next;                           // next tile scenario to plan (half-warp pass)
   int32_t next_over;                      // next overflow entry (full-warp pass)
   int32_t n_over;
+  int32_t go;                             // slot ticket granted (first tile)
   int16_t over[PB_THREADS];               // tile scenarios beyond a half-warp's width
 };
 
@@ -818,13 +830,17 @@ __device__ __forceinline__ uint64_t src_service(const PlanArgs& A, const IndexVi
 // threads configure a tile's services into shared memory, then the warps
 // plan its scenarios (taken from a shared counter, so uneven scenarios
 // balance inside the CTA).  All threads of the CTA call it.
+// With a slot ticket (A.slot_count), thread 0 waits for it while the first
+// tile's offsets load, before the tile barrier (no store precedes it);
+// returns false (nothing stored) if the wait timed out.
 template <bool kMirror>
-__device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, uint8_t* area,
+__device__ __forceinline__ bool run_tiles(const PlanArgs& A, const IndexView& V, TileSmem& T, uint8_t* area,
                                           const TileSrc& S, int k, const int k1, int tid, int lane) {
 #ifdef PARVA_PHASE_TIMING
   int dbg_n = 0;
   bool dbg_first = true;
 #endif
+  bool first = true;
   while (k < k1) {
     // tile = the longest run of scenarios from k with <= kTileSvc services
     // (at least one scenario; offsets are non-decreasing)
@@ -833,8 +849,19 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
     const int off_e = e <= k1 ? src_ld(S.off + e, S.cg) : 0;
     const bool fits = e <= k1 && (tid == 0 || off_e - a0 <= kTileSvc);
     if (e <= k1) T.off[tid + 1] = off_e;
-    if (tid == 0) { T.off[0] = a0; T.next = 0; T.next_over = 0; T.n_over = 0; }
+    if (tid == 0) {
+      T.off[0] = a0; T.next = 0; T.next_over = 0; T.n_over = 0;
+#if !defined(PARVA_AB_NO_TICKET) && !defined(PARVA_AB_NO_WAIT)   // (A/B builds only: tools/k2_ab.py)
+      if (first && A.slot_count)
+        T.go = ticket_wait(A.slot_count, A.slot_wait, A.ack_row, A.n_mirror, A.ack_prev, A.ticket_timeout_ns,
+                           A.err_word);
+#endif
+    }
     const int n_tile = __syncthreads_count(fits);
+    if (first) {
+      first = false;
+      if (A.slot_count && !T.go) return false;   // timed out: store nothing
+    }
     const int a_end = T.off[n_tile];
 
     // configure the tile's services
@@ -930,6 +957,7 @@ __device__ __forceinline__ void run_tiles(const PlanArgs& A, const IndexView& V,
     }
     k += n_tile;
   }
+  return true;
 }
 
 #ifndef PARVA_TILE_MINB
@@ -941,47 +969,42 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   extern __shared__ __align__(16) uint8_t smem_raw[];
   TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
   __shared__ uint64_t bar;
-  __shared__ int s_go;
   // an overlapped successor (parva_plan_batch_overlapped / _fused) may take
   // SM slots as this grid's CTAs retire; the slot ticket keeps it from
   // storing into an output slot a launch still in flight writes
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   PHASE(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0)
-    s_go = !A.slot_words ||
-           ticket_wait(A.slot_words, A.slot_prev, A.ack_row, A.n_mirror, A.ticket_timeout_ns, A.err_word);
-  // (a barrier of its own: sharing load_index's costs K2 ~9 registers of spill)
-  __syncthreads();
-  if (!s_go) return;   // timed out: store nothing
+  if (tid == 0) T.go = 1;
   const IndexView V = load_index(A, smem_raw + kWarpArea * PB_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
   PHASE(1);
   // this CTA's contiguous block of scenarios
   const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
-  const int k = blockIdx.x * per;
+  const int k = blockIdx.x * per, k1 = min(A.n_scen, k + per);
   const TileSrc S{A.scen_off, A.svc_table16, A.svc_table, A.svc_rate, A.svc_bound, 0, 0, false};
-  run_tiles<kMirror>(A, V, T, smem_raw + kWarpArea * warp, S, k, min(A.n_scen, k + per), tid, lane);
+  if (!run_tiles<kMirror>(A, V, T, smem_raw + kWarpArea * warp, S, k, k1, tid, lane)) return;
   PHASE(3);
-  if (A.slot_words) {
-    // completion: every thread's stores (peer stores at system scope) are
-    // fenced before its CTA counts itself done; the last CTA resets the
-    // counter, publishes the epoch into this rank's flag word of the slot
-    // on every rank (fused), then completes the slot's ticket
+#if !defined(PARVA_AB_NO_TICKET) && !defined(PARVA_AB_NO_DONE)
+  if (A.slot_count) {
+    // completion: the CTA's stores are ordered before thread 0's release
+    // reduction (barrier; a release is cumulative over what the barrier
+    // made visible to thread 0; peer stores: every thread fences at system
+    // scope first).  Fused: the last CTA resets the CTA counter and publishes
+    // the epoch into this rank's flag word of the slot on every rank.
     if (kMirror) __threadfence_system();
-    else __threadfence();
     __syncthreads();
-    if (tid == 0 && atomicAdd(&A.slot_words[1], 1u) == gridDim.x - 1) {
-      atomicExch(&A.slot_words[1], 0u);
-      if (kMirror) {
+    if (tid == 0) {
+      if (kMirror && atomicAdd(A.done_ctas, 1u) == gridDim.x - 1) {
+        atomicExch(A.done_ctas, 0u);
         __threadfence_system();
         for (int m = 0; m < A.n_mirror; m++)
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.peer_flag[m]), "r"(A.slot_epoch) : "memory");
-      } else {
-        __threadfence();
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.peer_flag[m]), "r"(A.flag_epoch) : "memory");
       }
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.slot_words), "r"(A.slot_epoch) : "memory");
+      const unsigned long long mine = k1 > k ? (unsigned long long)(k1 - k) : 0ull;
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(A.slot_count), "l"(mine) : "memory");
     }
   }
+#endif
 }
 
 // K2, warp-autonomous form: every half warp takes scenarios one at a time
@@ -1322,6 +1345,9 @@ int plan_batch_grid(const PlanArgs& A) {
 }
 
 int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
+  // the tiny record stores point positions in a byte (255 = absent)
+  if (A.cfg_format == PARVA_CFG_TINY && !A.cfg_given && (A.max_seg_points < 0 || A.max_seg_points > 254))
+    return PARVA_BAD_INPUT;
   if (A.n_scen <= 0) return PARVA_OK;
   if (A.stream_src && !A.work) return PARVA_BAD_INPUT;
   LaunchCfg L;

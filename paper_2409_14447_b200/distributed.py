@@ -213,7 +213,7 @@ class PeerGather:
         self.layout, self.n_slots = layout, int(n_slots)
         self.blk = layout.blk
         self.slot_bytes = self.world * self.blk
-        self.head = (72 * self.n_slots + 255) & ~255
+        self.head = (80 * self.n_slots + 255) & ~255   # flags, acks (8 u32 each), CTA counter + u64 count
         size = self.head + self.n_slots * self.slot_bytes
         p = C.c_void_p()
         N.check(L.parva_ipc_alloc(C.c_size_t(size), C.byref(p)), "parva_ipc_alloc")
@@ -235,6 +235,7 @@ class PeerGather:
         self.status = torch.zeros(2, dtype=torch.int32, device="cuda")   # [0] gather waits, [1] tickets
         self.epoch = 0
         self.last = [0] * self.n_slots
+        self.issued = [0] * self.n_slots
         dist.barrier(group=group)
 
     # header addresses
@@ -282,11 +283,16 @@ class PeerGather:
             m.spill[r] = part + lay.ps + lay.cs if lay.os else None
             m.flag[r] = self._flag(b, slot, self.rank)
         m.d_acks = self._ack(self.base, slot, 0)
+        m.d_done = self.base + 64 * self.n_slots + 4 * slot
         m.d_spill = self._part(self.base, slot, self.rank) + lay.ps + lay.cs if lay.os else None
         m.plan_capacity, m.cfg_capacity, m.spill_capacity = lay.ps, lay.cs, lay.os
         m.plan_bytes = lay.plan_bytes
-        m.ticket = N.SlotTicket(self.base + 64 * self.n_slots + 8 * slot, self.last[slot], self.epoch,
-                                self.status.data_ptr() + 4)
+        m.epoch, m.prev_epoch = self.epoch, self.last[slot]
+        a, b = lay.spans[self.rank]
+        cnt = self.base + 64 * self.n_slots + 4 * self.n_slots
+        cnt = (cnt + 7) & ~7
+        m.ticket = N.SlotTicket(cnt + 8 * slot, self.issued[slot], self.status.data_ptr() + 4)
+        self.issued[slot] += b - a
         self.last[slot] = self.epoch
         return m
 

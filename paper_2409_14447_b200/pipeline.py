@@ -116,63 +116,160 @@ def _decode_general(services: list[Service], g, out) -> DeploymentMap:
     return DeploymentMap(gpus=gpus, freed_rate=freed, diagnostics=diags)
 
 
+class _BatchRecords:
+    """The records of one plan_many call, shared by its lazy results: config
+    records (numpy), plan records, and the general kernel's outputs for the
+    scenarios it re-planned."""
+
+    __slots__ = ("pt", "off", "tab", "cfg", "plan", "general")
+
+    def __init__(self, pt, off, tab, cfg, plan, general):
+        self.pt, self.off, self.tab, self.cfg, self.plan, self.general = pt, off, tab, cfg, plan, general
+
+    def decode(self, k: int, ss) -> tuple[list[Service], DeploymentMap]:
+        a = int(self.off[k])
+        recs = self.cfg[a:a + len(ss)].tolist()
+        configured = [service_from_record(s, self.pt, self.tab[a + i], recs[i]) for i, s in enumerate(ss)]
+        if k in self.general:
+            g, go = self.general[k]
+            dmap = _decode_general(configured, g, go)
+            if go.fallback:
+                dmap.diagnostics = [format_diag(DIAG_REGRESSED, -1, None)]
+        else:
+            dmap = _decode_record(configured, self.plan[k])
+        return configured, dmap
+
+
+class LazyPlanResult(PlanResult):
+    """A PlanResult of plan_many whose configured services and deployment map
+    are built from the batch's records on first access (the scenario-level
+    fields -- gpu_count, unoptimized_gpu_count -- come straight from the plan
+    record).  It is a PlanResult in every other respect: same fields,
+    equality, repr, summary()."""
+
+    def __init__(self, scenario_name="", services=None, deployment=None, planning_ms=0.0, unoptimized_gpu_count=0,
+                 *, _src=None, _k=0, _ss=None, _n_gpus=0):
+        self.scenario_name = scenario_name
+        self.planning_ms = planning_ms
+        self.unoptimized_gpu_count = unoptimized_gpu_count
+        self._src, self._k, self._ss, self._n_gpus = _src, _k, _ss, _n_gpus
+        self._dec = None if _src is not None else [services, deployment]
+
+    def _decoded(self):
+        if self._dec is None:
+            self._dec = list(self._src.decode(self._k, self._ss))
+            self._src = self._ss = None
+        return self._dec
+
+    @property
+    def services(self) -> list[Service]:
+        return self._decoded()[0]
+
+    @services.setter
+    def services(self, v):
+        self._decoded()[0] = v
+
+    @property
+    def deployment(self) -> DeploymentMap:
+        return self._decoded()[1]
+
+    @deployment.setter
+    def deployment(self, v):
+        self._decoded()[1] = v
+
+    @property
+    def gpu_count(self) -> int:
+        return self._n_gpus if self._dec is None else self._dec[1].gpu_count
+
+    def __eq__(self, other):
+        if not isinstance(other, PlanResult):
+            return NotImplemented
+        f = lambda r: (r.scenario_name, r.services, r.deployment, r.planning_ms, r.unoptimized_gpu_count)  # noqa: E731
+        return f(self) == f(other)
+
+    __hash__ = None
+
+
+def _first_errors(cfg, plan, off, general) -> dict:
+    """Scenario -> index of its first non-OK config record (input order), or
+    -1 when every service is OK but the plan record failed (vectorized)."""
+    st = cfg["status"]
+    bad = np.flatnonzero(st != OK)
+    out = {}
+    if len(bad):
+        ks = np.searchsorted(off, bad, side="right") - 1
+        first = np.ones(len(bad), dtype=bool)
+        first[1:] = ks[1:] != ks[:-1]
+        out = {int(k): int(i) for k, i in zip(ks[first], bad[first])}
+    for k in np.flatnonzero(plan["status"] != OK).tolist():
+        if k not in out and k not in general:
+            out[k] = -1
+    return out
+
+
 def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, ProfileTable],
               options: PlanOptions = PlanOptions(), names: Sequence[str] | None = None,
               raise_errors: bool = False) -> list:
     """Plan independent service sets in one fused launch.
 
-    Returns one PlanResult per set, or the exception the reference would
-    raise for that set (raised instead when raise_errors)."""
+    Returns one PlanResult per set (a LazyPlanResult: its services and
+    deployment are decoded from the records on first access), or the
+    exception the reference would raise for that set (raised instead when
+    raise_errors)."""
     dt = N.device_tables_for(tables, options.memory_map, options.single_process)
     pt = dt.packed
     idx = pt.index_of()
-    off = np.zeros(len(service_sets) + 1, dtype=np.int32)
-    tab, rate, bound = [], [], []
-    for k, ss in enumerate(service_sets):
-        for s in ss:
-            tab.append(idx.get(s.model_id, -1)); rate.append(s.request_rate); bound.append(s.internal_latency)
-        off[k + 1] = len(tab)
+    n = len(service_sets)
+    counts = np.fromiter((len(ss) for ss in service_sets), dtype=np.int64, count=n)
+    off = np.zeros(n + 1, dtype=np.int32)
+    np.cumsum(counts, out=off[1:])
+    flat = [s for ss in service_sets for s in ss]
+    tab = np.fromiter((idx.get(s.model_id, -1) for s in flat), dtype=np.int32, count=len(flat))
+    rate = np.fromiter((s.request_rate for s in flat), dtype=np.float64, count=len(flat))
+    bound = np.fromiter((s.internal_latency for s in flat), dtype=np.float64, count=len(flat))
     torch = N.require_cuda()
     t0 = time.perf_counter()
-    res = plan_batch(dt, off, np.asarray(tab, dtype=np.int32), np.asarray(rate), np.asarray(bound),
-                     optimize=options.optimize, threshold=options.threshold)
+    res = plan_batch(dt, off, tab, rate, bound, optimize=options.optimize, threshold=options.threshold)
     cfg, plan = res.host()
-    general = resolve_capacity(pt, off, np.asarray(tab, dtype=np.int32), cfg, plan, options.optimize,
-                               options.threshold)
+    general = resolve_capacity(pt, off, tab, cfg, plan, options.optimize, options.threshold)
     torch.cuda.synchronize()
     elapsed_ms = (time.perf_counter() - t0) * 1000.0
+    errors = _first_errors(cfg, plan, off, general)
+    src = _BatchRecords(pt, off, tab.tolist(), cfg, plan, general)
+    n_gpus = plan["n_gpus"].tolist()
+    unopt = plan["n_gpus_unopt"].tolist()
     out = []
-    cfg_t = cfg.tolist()                   # records as tuples: plain attribute-free access below
     for k, ss in enumerate(service_sets):
-        a = int(off[k])
-        try:
-            configured = []
-            for i, s in enumerate(ss):
-                rec = cfg_t[a + i]
-                if rec[3] == BAD_INPUT:
-                    raise KeyError(s.model_id)
-                raise_for_record(s, rec)
-                configured.append(service_from_record(s, pt, tab[a + i], rec))
-            rec = plan[k]
-            if k in general:
-                g, go = general[k]
-                if go.status != OK:
-                    raise MigplanError(f"device planner status {go.status}")
-                dmap = _decode_general(configured, g, go)
-                unopt = go.n_gpus_unopt
-                if go.fallback:
-                    dmap.diagnostics = [format_diag(DIAG_REGRESSED, -1, None)]
-            else:
-                if int(rec["status"]) != OK:
-                    raise MigplanError(f"device planner status {int(rec['status'])}")
-                dmap = _decode_record(configured, rec)
-                unopt = int(rec["n_gpus_unopt"])
-            out.append(PlanResult(scenario_name=(names[k] if names else ""), services=configured,
-                                  deployment=dmap, planning_ms=elapsed_ms, unoptimized_gpu_count=unopt))
-        except (MigplanError, KeyError, OverflowError) as exc:
-            if raise_errors:
-                raise
-            out.append(exc)
+        name = names[k] if names else ""
+        if k in errors:
+            try:
+                i = errors[k]
+                if i < 0:
+                    raise MigplanError(f"device planner status {int(plan[k]['status'])}")
+                a = int(off[k])
+                rec = cfg[i]
+                if int(rec["status"]) == BAD_INPUT:
+                    raise KeyError(ss[i - a].model_id)
+                raise_for_record(ss[i - a], rec)
+                raise MigplanError(f"device planner status {int(rec['status'])}")
+            except (MigplanError, KeyError, OverflowError) as exc:
+                if raise_errors:
+                    raise
+                out.append(exc)
+            continue
+        if k in general:
+            g, go = general[k]
+            if go.status != OK:
+                exc = MigplanError(f"device planner status {go.status}")
+                if raise_errors:
+                    raise exc
+                out.append(exc)
+                continue
+            out.append(LazyPlanResult(name, planning_ms=elapsed_ms, unoptimized_gpu_count=int(go.n_gpus_unopt),
+                                      _src=src, _k=k, _ss=ss, _n_gpus=int(len(go.gpu_id))))
+            continue
+        out.append(LazyPlanResult(name, planning_ms=elapsed_ms, unoptimized_gpu_count=unopt[k], _src=src, _k=k,
+                                  _ss=ss, _n_gpus=n_gpus[k]))
     return out
 
 

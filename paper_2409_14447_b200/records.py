@@ -87,7 +87,11 @@ def format_diag(reason: int, gpu_id: int, name: str | None) -> str:
 
 
 def tiny_config(full: np.ndarray) -> np.ndarray:
-    """Full 32-byte config records -> 8-byte tiny records (parva_config_tiny)."""
+    """Full 32-byte config records -> 8-byte tiny records (parva_config_tiny).
+    A point position >= 255 does not fit the byte (the device entries reject
+    PARVA_CFG_TINY for such tables): ValueError."""
+    if full.shape[0] and int(full["best"].max(initial=-1)) >= 255:
+        raise ValueError("tiny config records hold point positions < 255 (a table has > 254 points per size)")
     out = np.zeros(full.shape[0], dtype=TINY_DTYPE)
     out["best"] = np.where(full["best"] < 0, 255, full["best"]).astype(np.uint8)
     opt = np.where(full["opt_sc"] < 0, 15, full["opt_sc"]).astype(np.uint8)

@@ -104,8 +104,9 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
     tab, idx = N.ParvaTables(), N.ParvaIndex()
     m = N.Mirror()
     m.n, m.plan_bytes = 1, 128
-    m.plan[0] = m.cfg[0] = m.flag[0] = m.d_acks = 16
-    m.ticket = N.SlotTicket(16, 0, 1, None)
+    m.plan[0] = m.cfg[0] = m.flag[0] = m.d_acks = m.d_done = 16
+    m.epoch = 1
+    m.ticket = N.SlotTicket(16, 0, None)
     m.plan_capacity, m.cfg_capacity = 10 * 128, 110 * 8
     args = (C.byref(tab), C.byref(idx), 10, 110, dummy, dummy, dummy, dummy, 1, 4, dummy)
     assert L.parva_plan_batch_fused(*args, 0, dummy, C.byref(m), None) == BAD     # 32-B records > 8-B section
@@ -114,11 +115,13 @@ def test_c_abi_rejects_bad_arguments_before_touching_the_device():
     m.plan_capacity, m.plan_bytes = 10 * 128, 64
     assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # 64-B records need overflow
     m.plan_bytes = 128
-    m.ticket = N.SlotTicket(16, 1, 1, None)
+    m.prev_epoch = 1
     assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # epoch == prev_epoch
+    m.prev_epoch, m.d_done = 0, None
+    assert L.parva_plan_batch_fused(*args, 2, dummy, C.byref(m), None) == BAD     # no CTA counter
     # overlapped launches need a ticket
     assert L.parva_plan_batch_overlapped(*args, 2, dummy, None, None) == BAD
-    t = N.SlotTicket(None, 0, 1, None)
+    t = N.SlotTicket(None, 0, None)
     assert L.parva_plan_batch_overlapped(*args, 2, dummy, C.byref(t), None) == BAD
     g = N.GatherSlot()
     g.n = 1

@@ -247,7 +247,7 @@ def test_plan_batch_overlapped_back_to_back(fx):
             torch.cuda.synchronize()     # a plain launch: every earlier launch into the slot is done
             B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view)
         else:
-            B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view, overlap=True, ticket=ring.ticket(r))
+            B.plan_batch(dt, *ins[b], cfg_format=CFG_TINY, out=view, overlap=True, ticket=ring.ticket(r, k))
         last[r] = (b, view)
     torch.cuda.synchronize()
     ring.check()
@@ -776,3 +776,25 @@ def test_host_entry_mapped_pack_every_step(fx):
         mb.wait(slot)
         cfg, plan = mb.outputs(slot)
         assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0], j
+
+
+def test_tiny_records_rejected_for_tables_over_254_points():
+    """ADVICE r1: the 8-byte config record stores a point position in a byte;
+    tables with more than 254 points in one (table, size) segment make every
+    entry reject PARVA_CFG_TINY (the device planner itself is exact there:
+    the full records equal the oracle's)."""
+    from paper_2409_14447_b200.tables import pack_dense
+    dth = W.dense_tables(6, seed=3)
+    pt = pack_dense(dth)
+    assert int(pt.seg_count.max()) > 254
+    dt = N.DeviceTables(pt)
+    off = np.array([0, 3, 6], dtype=np.int32)
+    tab = np.arange(6, dtype=np.int32)
+    rate, bound = dth.rate, dth.slo / 2.0
+    with pytest.raises(Exception, match="parva_plan_batch"):
+        B.plan_batch(dt, off, tab, rate, bound, cfg_format=CFG_TINY)
+    with pytest.raises(Exception):
+        B.MappedHostBatch(off, tab, rate, bound, cfg_format=CFG_TINY).run(dt)
+    cfg, plan = B.plan_batch(dt, off, tab, rate, bound).host()
+    ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
+    assert cfg.tobytes() == ocfg.tobytes() and plan.tobytes() == oplan.tobytes()

@@ -49,12 +49,12 @@ def test_slow_first_launch_then_queued_launches_into_the_same_slots():
     d_big = [N.to_device(a) for a in big]
     d_small = [[N.to_device(a) for a in s] for s in small]
     torch.cuda.synchronize()
-    B.plan_batch(dt, *d_big, cfg_format=CFG_TINY, out=outs[0], overlap=True, ticket=ring.ticket(0))
+    B.plan_batch(dt, *d_big, cfg_format=CFG_TINY, out=outs[0], overlap=True, ticket=ring.ticket(0, nb))
     for j in range(6):
         r = (j + 1) % 2
         k, m = len(small[j][0]) - 1, int(small[j][0][-1])
         view = B.BatchResult(outs[r].cfg[:m], outs[r].plan[:k], k, m, CFG_TINY)
-        B.plan_batch(dt, *d_small[j], cfg_format=CFG_TINY, out=view, overlap=True, ticket=ring.ticket(r))
+        B.plan_batch(dt, *d_small[j], cfg_format=CFG_TINY, out=view, overlap=True, ticket=ring.ticket(r, k))
     torch.cuda.synchronize()
     ring.check()
     bc, bp = oracle.plan_batch_records(pt, *big)
@@ -82,18 +82,18 @@ tab = np.tile(np.arange(11, dtype=np.int32), 500)
 out = B.BatchResult(N.empty_records(5500, TINY_DTYPE), N.empty_records(500, PLAN_DTYPE), 500, 5500, CFG_TINY)
 out.plan.fill_(0xAB)
 ring = B.SlotRing(1)
-bad = N.SlotTicket(ring.words.data_ptr(), 7, 8, ring.err.data_ptr())   # epoch 7 never completes
+bad = N.SlotTicket(ring.counts.data_ptr(), 7, ring.err.data_ptr())   # 7 scenarios never complete
 B.plan_batch(dt, off, tab, sb.rate.ravel(), sb.bound.ravel(), cfg_format=CFG_TINY, out=out, overlap=True, ticket=bad)
 torch.cuda.synchronize()
 assert int(ring.err.item()) == 7, ring.err            # PARVA_LAUNCH_ERROR
 assert bool((out.plan == 0xAB).all()), "a timed-out launch stored records"
-assert int(ring.words[0].item()) == 0                  # the slot's ticket did not advance
+assert int(ring.counts[0].item()) == 0                 # the slot's counter did not advance
 ring.err.zero_()
 B.plan_batch(dt, off, tab, sb.rate.ravel(), sb.bound.ravel(), cfg_format=CFG_TINY, out=out, overlap=True,
-             ticket=ring.ticket(0))
+             ticket=ring.ticket(0, 500))
 torch.cuda.synchronize()
 ring.check()
-assert int(ring.words[0].item()) == ring.last[0]
+assert int(ring.counts[0].item()) == 500
 print("ok")
 """
 

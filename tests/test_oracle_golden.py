@@ -275,3 +275,57 @@ def test_sim_oracle_vs_reference_reports():
         obj["metrics"] = {"internal_slack": S.internal_slack(rep.activity) if rep.activity.segments else None,
                           "slo_compliance": S.slo_compliance(rep)}
         assert json.loads(json.dumps(obj)) == case["report"], (case["scenario"], case["arrivals"], case["seed"])
+
+
+def test_plan_many_lazy_results_decode_to_reference_plans(fx, monkeypatch):
+    """plan_many's lazy results (LazyPlanResult) and its vectorized error
+    path, with the oracle standing in for the device (CPU): every one of the
+    first 3000 C2 scenarios decodes to the reference's digest; gpu_count is
+    answered from the record before any decode; results compare equal to the
+    eagerly decoded PlanResult."""
+    import types
+    import paper_2409_14447_b200 as P
+    from paper_2409_14447_b200 import _native as Nm
+    from paper_2409_14447_b200 import pipeline as PL
+    from paper_2409_14447_b200.records import CONFIG_DTYPE, PLAN_DTYPE
+    g = golden("c2_digests.json")
+    n = 3000
+    sb = W.scenario_batch(fx, n, seed=g["seed"])
+    pt = pack_tables(fx.tables)
+
+    def fake_plan_batch(dt, off, tab, rate, bound, optimize=True, threshold=4, **kw):
+        cfg, plan = oracle.plan_batch_records(pt, off, tab, rate, bound, optimize=optimize, threshold=threshold)
+        return types.SimpleNamespace(host=lambda: (cfg.view(CONFIG_DTYPE), plan.view(PLAN_DTYPE)))
+
+    monkeypatch.setattr(PL, "plan_batch", fake_plan_batch)
+    monkeypatch.setattr(PL, "resolve_capacity", lambda *a, **k: {})
+    monkeypatch.setattr(Nm, "device_tables_for", lambda *a, **k: types.SimpleNamespace(packed=pt))
+    monkeypatch.setattr(Nm, "require_cuda", lambda: types.SimpleNamespace(
+        cuda=types.SimpleNamespace(synchronize=lambda: None)))
+    sets = [[P.make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]
+            for k in range(n)]
+    res = P.plan_many(sets, fx.tables)
+    n_err = 0
+    for k, r in enumerate(res):
+        if isinstance(r, Exception):
+            n_err += 1
+            got = canon.error(r)
+        else:
+            assert isinstance(r, PL.PlanResult) and r._dec is None
+            cnt = r.gpu_count                     # from the record, no decode
+            assert r._dec is None
+            got = canon.plan(r)
+            assert r.gpu_count == cnt == r.deployment.gpu_count
+        assert canon.digest(got) == g["digests"][k], k
+    assert n_err == 30
+    # a lazy result equals the eager one and survives dataclasses.replace / summary
+    import dataclasses
+    k = next(i for i, r in enumerate(res) if not isinstance(r, Exception))
+    lazy = P.plan_many([sets[k]], fx.tables)[0]
+    eager = PL.PlanResult(lazy.scenario_name, lazy.services, lazy.deployment, lazy.planning_ms,
+                          lazy.unoptimized_gpu_count)
+    assert lazy == eager
+    assert dataclasses.replace(lazy, scenario_name="x").deployment.to_json() == eager.deployment.to_json()
+    assert lazy.summary() == eager.summary()
+    with pytest.raises(P.InfeasibleSLOError):
+        P.plan_services(sets[next(i for i, r in enumerate(res) if isinstance(r, Exception))], fx.tables)
