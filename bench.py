@@ -290,7 +290,8 @@ def run_reference(args, rank, world):
             "data": "synthetic (C2 generator; the repo arm's resident batches in the same order: batch 0 = seed 0, "
                     "batch p = seed 1000 + p)",
             "config": {"workload": "C2: 11 fixture workloads x 10^4 synthetic SLO/rate scenarios per GPU",
-                       "scenarios_per_gpu": n, "input_batches": P},
+                       "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n,
+                       "input_batches": P, "optimize": True, "threshold": 4},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                              "cpu_model": lscpu_model(),
                              "sample": f"one full C2 batch ({n} scenarios) per step on {threads} host threads; "
@@ -394,27 +395,6 @@ def main():
     # records survive for the parity check; a slot's ticket serializes the
     # launches that share it
     S = args.slots if args.slots > 0 else max(3, min(args.steps, 64))
-    gather_mode = "none" if world == 1 else args.gather
-    peer = None
-    if gather_mode == "fused":
-        try:
-            lay = D.gather_layout(g_off, world, plan_bytes=64, cfg_bytes=8)
-            peer = D.PeerGather(lay, n_slots=S)
-        except Exception as exc:  # noqa: BLE001 -- no peer access: the NCCL collective instead
-            print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
-            gather_mode = "nccl"
-    if peer is None:
-        lay = D.gather_layout(g_off, world, plan_bytes=128, cfg_bytes=8)   # = packed_block's layout
-        blocks = [torch.zeros(lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
-        results = [B.BatchResult(bk[lay.ps:lay.ps + 8 * n_svc_local].view(-1, 8),
-                                 bk[:lay.ps].view(-1, 128), n, n_svc_local, CFG_TINY) for bk in blocks]
-        ring = B.SlotRing(S)
-        gathered = ([torch.empty(world * lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
-                    if world > 1 else None)
-        works = [None] * S
-    else:
-        results = [peer.local(s, CFG_TINY) for s in range(S)]
-        gslots = [peer.gather_slot(s, pdl=True) for s in range(S)]
 
     def base_args(p, res):
         d_off, d_tab, d_rate, d_bound = batches[p]
@@ -422,65 +402,116 @@ def main():
                 N.ptr(d_off), N.ptr(d_tab), N.ptr(d_rate), N.ptr(d_bound), C.c_int32(1), C.c_int32(4),
                 N.ptr(res.cfg), C.c_int32(CFG_TINY), N.ptr(res.plan))
 
-    def prepare(c0, c1):
-        """C-ABI arguments of calls [c0, c1) (slot c % S, batch c % P), built
-        before the timed region (tickets and mirrors carry sequential epochs)."""
-        out = []
-        for c in range(c0, c1):
-            s = c % S
-            a = base_args(c % P, results[s])
-            if peer is not None:
-                m = peer.mirror(s, overlap=True)
-                out.append((s, a + (C.byref(m), sh), m))
-            else:
-                t = ring.ticket(s, n)
+    class Steps:
+        """The sharded step: an overlapped K2 launch into output slot c % S
+        (batch c % P), then the gather -- fused (K2's own peer stores + one
+        exact-epoch wait/release, step c - lag), NCCL (one async all-gather of
+        the slot), or none (N = 1)."""
+
+        def __init__(self, mode):
+            self.mode, self.peer, self.unwaited = mode, None, []
+            if mode == "fused":
+                self.lay = D.gather_layout(g_off, world, plan_bytes=64, cfg_bytes=8)
+                self.peer = D.PeerGather(self.lay, n_slots=S)
+                self.results = [self.peer.local(s, CFG_TINY) for s in range(S)]
+                self.gslots = [self.peer.gather_slot(s, pdl=True) for s in range(S)]
+                return
+            lay = self.lay = D.gather_layout(g_off, world, plan_bytes=128, cfg_bytes=8)   # = packed_block's
+            self.blocks = [torch.zeros(lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
+            self.results = [B.BatchResult(bk[lay.ps:lay.ps + 8 * n_svc_local].view(-1, 8),
+                                          bk[:lay.ps].view(-1, 128), n, n_svc_local, CFG_TINY) for bk in self.blocks]
+            self.ring = B.SlotRing(S)
+            self.gathered = ([torch.empty(world * lay.blk, dtype=torch.uint8, device="cuda") for _ in range(S)]
+                             if world > 1 else None)
+            self.works = [None] * S
+
+        def prepare(self, c0, c1):
+            """C-ABI arguments of calls [c0, c1), built before the timed
+            region (tickets and mirrors carry sequential epochs)."""
+            out = []
+            for c in range(c0, c1):
+                s = c % S
+                a = base_args(c % P, self.results[s])
+                t = self.peer.mirror(s, overlap=True) if self.peer is not None else self.ring.ticket(s, n)
                 out.append((s, a + (C.byref(t), sh), t))
-        return out
+            return out
 
-    unwaited = []
+        def launch(self, item, timeout_s=60.0):
+            s, a, _keep = item
+            if self.peer is not None:
+                N.check(L.parva_plan_batch_fused(*a), "parva_plan_batch_fused")
+                self.unwaited.append(s)
+                while len(self.unwaited) > args.lag:
+                    w = self.unwaited.pop(0)
+                    self.peer.wait(w, release=True, pdl=True, gslot=self.gslots[w], timeout_s=timeout_s)
+                return
+            if self.works[s] is not None:
+                self.works[s].wait()     # the slot's previous all-gather has read it (a stream wait under NCCL)
+                self.works[s] = None
+            N.check(L.parva_plan_batch_overlapped(*a), "parva_plan_batch_overlapped")
+            if world > 1:
+                self.works[s] = dist.all_gather_into_tensor(self.gathered[s], self.blocks[s], async_op=True)
 
-    def launch(item):
-        s, a, _keep = item
-        if peer is not None:
-            N.check(L.parva_plan_batch_fused(*a), "parva_plan_batch_fused")
-            unwaited.append(s)
-            while len(unwaited) > args.lag:
-                w = unwaited.pop(0)
-                peer.wait(w, release=True, pdl=True, gslot=gslots[w])
-            return
-        if works[s] is not None:
-            works[s].wait()              # the slot's previous all-gather has read it (a stream wait under NCCL)
-            works[s] = None
-        N.check(L.parva_plan_batch_overlapped(*a), "parva_plan_batch_overlapped")
-        if world > 1:
-            works[s] = dist.all_gather_into_tensor(gathered[s], blocks[s], async_op=True)
+        def drain(self, timeout_s=60.0):
+            if self.peer is not None:
+                while self.unwaited:
+                    s = self.unwaited.pop(0)
+                    self.peer.wait(s, release=True, pdl=True, gslot=self.gslots[s], timeout_s=timeout_s)
+                return
+            for s in range(S):
+                if self.works[s] is not None:
+                    self.works[s].wait()
+                    self.works[s] = None
 
-    def drain():
-        if peer is not None:
-            while unwaited:
-                s = unwaited.pop(0)
-                peer.wait(s, release=True, pdl=True, gslot=gslots[s])
-            return
-        for s in range(S):
-            if works[s] is not None:
-                works[s].wait()
-                works[s] = None
+        def healthy(self):
+            if self.peer is not None:
+                return int(self.peer.status.abs().sum().item()) == 0
+            return int(self.ring.err.item()) == 0
+
+        def check(self):
+            if self.peer is not None:
+                self.peer.check()
+            else:
+                self.ring.check()
+
+        def rows(self, s):
+            v = self.peer.slot_view(s) if self.peer is not None else self.gathered[s]
+            return v.view(world, self.lay.blk).cpu().numpy()
+
+        def close(self):
+            if self.peer is not None:
+                self.peer.close()
+                self.peer = None
+
+    gather_mode = "none" if world == 1 else args.gather
+    st = None
+    if gather_mode == "fused":
+        try:
+            st = Steps("fused")
+        except Exception as exc:  # noqa: BLE001 -- no peer access: the NCCL collective instead
+            print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
+            gather_mode = "nccl"
+    if st is None:
+        st = Steps(gather_mode)
 
     # ---- warm-up, then the timed steps
     if world > 1:
         dist.barrier()                   # every rank's inputs are resident before anyone waits on flags
-    for item in prepare(0, args.warmup):
-        launch(item)
-    drain()
+    for item in st.prepare(0, args.warmup):
+        st.launch(item, timeout_s=10.0)
+    st.drain(timeout_s=10.0)
     torch.cuda.synchronize()
-    if peer is not None:
-        # did every rank's warm-up records arrive?  If not (no working peer
-        # writes on this box), fail loudly rather than time a broken path
-        ok = dist_all(dist, torch, world, int(peer.status.abs().sum().item()) == 0)
-        if not ok:
-            raise RuntimeError("fused all-gather: peer records did not arrive in the warm-up "
-                               "(run with --gather nccl on a box without peer access)")
-    timed = prepare(args.warmup, args.warmup + args.steps)
+    if gather_mode == "fused" and not dist_all(dist, torch, world, st.healthy()):
+        # no working peer stores on this box: time the NCCL collective instead
+        print("fused all-gather: peer records did not arrive in the warm-up; using NCCL", file=sys.stderr)
+        st.close()
+        gather_mode = "nccl"
+        st = Steps("nccl")
+        for item in st.prepare(0, args.warmup):
+            st.launch(item)
+        st.drain()
+        torch.cuda.synchronize()
+    timed = st.prepare(args.warmup, args.warmup + args.steps)
     if world > 1:
         dist.barrier()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -488,15 +519,12 @@ def main():
     clk.begin()
     t_start.record(stream)
     for item in timed:
-        launch(item)
-    drain()
+        st.launch(item)
+    st.drain()
     t_stop.record(stream)
     torch.cuda.synchronize()
     step_ms = t_start.elapsed_time(t_stop)
-    if peer is not None:
-        peer.check()
-    else:
-        ring.check()
+    st.check()
 
     # ---- parity of every timed step that survives in its slot: every rank
     # checks its copy of every rank's records against the oracle (digests of
@@ -523,15 +551,11 @@ def main():
     for c in checked:
         s, p = c % S, c % P
         if world == 1:
-            cfg, plan = results[s].host()
+            cfg, plan = st.results[s].host()
             ok = ok and digest(cfg.tobytes(), plan.tobytes()) == every[0][p]
             continue
-        if peer is not None:
-            rows = peer.slot_view(s).view(world, lay.blk).cpu().numpy()
-        else:
-            rows = gathered[s].view(world, lay.blk).cpu().numpy()
-        cfg, plan = D.decode_gathered(rows, lay)
-        for r, ((a, b), (sa, sb)) in enumerate(zip(lay.spans, lay.svc_spans)):
+        cfg, plan = D.decode_gathered(st.rows(s), st.lay)
+        for r, ((a, b), (sa, sb)) in enumerate(zip(st.lay.spans, st.lay.svc_spans)):
             ok = ok and digest(cfg[sa:sb].tobytes(), plan[a:b].tobytes()) == every[r][p]
     parity = dist_all(dist, torch, world, ok)
     parity_info = {"equal": parity, "steps_checked": len(checked), "ranks": world,
@@ -610,8 +634,7 @@ def main():
     line["roofline"]["issue"] = issue_roofline("plan_batch_kernel", kern_s, clk_summary.get("sm_mhz"))
     line["roofline"]["issue_overlapped"] = issue_roofline("plan_batch_kernel", step_ms / 1000.0 / args.steps,
                                                           clk_summary.get("sm_mhz"))
-    if peer is not None:
-        peer.close()
+    st.close()
 
     if not args.no_e2e:
         line["e2e"] = e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_global, pt)

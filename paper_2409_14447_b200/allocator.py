@@ -133,13 +133,21 @@ class DeploymentMap:
 
 
 # ---------------------------------------------------- general-problem glue
+# Deliberate deviation: the reference accepts repeated
+# service ids -- optimize_allocation then proposes from the last service of
+# an id and merges their freed_rate entries (allocator.py:377-404) -- while
+# the device planners keep one ledger entry per service.  Rather than return
+# a silently different plan, every planning entry rejects repeated ids.
+DUPLICATE_IDS = "service ids must be unique (the device planners keep one freed_rate entry per service)"
+
+
 class _Builder:
     """Flattens (map, services) into the general kernel's catalogue form."""
 
     def __init__(self, services: Sequence[Service]):
         ids = [s.id for s in services]
         if len(set(ids)) != len(ids):
-            raise ValidationError("service ids must be unique")
+            raise ValidationError(DUPLICATE_IDS)
         self.services = list(services)
         self.names = list(ids)
         self.name_idx = {n: i for i, n in enumerate(ids)}

@@ -17,10 +17,10 @@ from typing import Mapping, Optional, Sequence
 import numpy as np
 
 from . import _native as N
-from .allocator import DEFAULT_OPTIMIZATION_THRESHOLD, DeploymentMap
+from .allocator import DEFAULT_OPTIMIZATION_THRESHOLD, DUPLICATE_IDS, DeploymentMap
 from .batch import plan_batch, resolve_capacity
 from .configurator import Service, raise_for_record, service_from_record
-from .errors import MigplanError
+from .errors import MigplanError, ValidationError
 from .evaluation import DEFAULT_SMS_PER_GPC, allocated_fraction, external_fragmentation
 from .mig import INSTANCE_SIZES, GpuState, Placement
 from .profiles import DEFAULT_MEMORY_MAP, ProfileTable, filter_feasible
@@ -235,6 +235,9 @@ def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, Pr
     torch.cuda.synchronize()
     elapsed_ms = (time.perf_counter() - t0) * 1000.0
     errors = _first_errors(cfg, plan, off, general)
+    for k, ss in enumerate(service_sets):             # repeated ids: rejected (see allocator.DUPLICATE_IDS)
+        if len(ss) > 1 and len({s.id for s in ss}) != len(ss) and k not in errors:
+            errors[k] = -2
     src = _BatchRecords(pt, off, tab.tolist(), cfg, plan, general)
     n_gpus = plan["n_gpus"].tolist()
     unopt = plan["n_gpus_unopt"].tolist()
@@ -244,6 +247,8 @@ def plan_many(service_sets: Sequence[Sequence[Service]], tables: Mapping[str, Pr
         if k in errors:
             try:
                 i = errors[k]
+                if i == -2:
+                    raise ValidationError(DUPLICATE_IDS)
                 if i < 0:
                     raise MigplanError(f"device planner status {int(plan[k]['status'])}")
                 a = int(off[k])

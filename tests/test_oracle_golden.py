@@ -329,3 +329,7 @@ def test_plan_many_lazy_results_decode_to_reference_plans(fx, monkeypatch):
     assert lazy.summary() == eager.summary()
     with pytest.raises(P.InfeasibleSLOError):
         P.plan_services(sets[next(i for i, r in enumerate(res) if isinstance(r, Exception))], fx.tables)
+    # repeated service ids: rejected (a documented deviation)
+    dup = [dataclasses.replace(s, id="same") for s in sets[k][:3]]
+    got = P.plan_many([sets[k], dup], fx.tables)
+    assert isinstance(got[1], P.ValidationError) and not isinstance(got[0], Exception)
