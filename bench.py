@@ -515,14 +515,24 @@ def main():
     if world > 1:
         dist.barrier()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the K steps are queued behind a gate (one thread spinning on a pinned
+    # host word) and the gate is opened once they are all enqueued: the
+    # events then time device execution only, with no host launch gaps
+    gate = torch.zeros(1, dtype=torch.int32).pin_memory()
+    gate_err = torch.zeros(1, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
     clk.begin()
+    N.check(L.parva_host_gate(C.c_void_p(gate.data_ptr()), C.c_uint32(1), C.c_int64(int(30e9)), N.ptr(gate_err), sh),
+            "parva_host_gate")
     t_start.record(stream)
     for item in timed:
         st.launch(item)
     st.drain()
     t_stop.record(stream)
+    gate.numpy()[0] = 1
     torch.cuda.synchronize()
+    if int(gate_err.item()):
+        raise RuntimeError("timed region: the gate timed out before the steps were enqueued")
     step_ms = t_start.elapsed_time(t_stop)
     st.check()
 
@@ -615,8 +625,9 @@ def main():
                    "l2": "not reused: steps cycle through resident input batches larger than L2 in total",
                    "input_batches": P, "output_slots": S,
                    "launch": "parva_plan_batch_overlapped / _fused per step (programmatic dependent launches; "
-                             "slot tickets serialize launches sharing an output slot); kernel_ms_per_step from "
-                             "separate one-at-a-time launches",
+                             "slot tickets serialize launches sharing an output slot), all K steps enqueued behind a "
+                             "gate kernel that is opened once they are queued (device time, no host launch gaps); "
+                             "kernel_ms_per_step from separate one-at-a-time launches",
                    "parallelism": f"scenario-sharded x{world}" + par,
                    "gather": gather_mode, "optimize": True, "threshold": 4},
         "gpu_launches": args.steps * launches_per_step,
@@ -674,40 +685,46 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     (prepacked), and one synchronous call per step."""
     import oracle
     from paper_2409_14447_b200.records import tiny_config
-    E2E_DEPTH, E2E_BATCHES = 4, 8
+    E2E_DEPTH, E2E_BATCHES = 5, 8
     host = [shard_inputs(p) for p in range(E2E_BATCHES)]      # the caller's arrays (pageable)
-    off = host[0][0]
-    n = len(off) - 1
     mb = B.MappedHostBatch(*host[0], cfg_format=2, plan_bytes=64, depth=E2E_DEPTH)
     pack_s = []
+
+    def batches(c0, k):
+        for i in range(c0, c0 + k):
+            yield host[i % E2E_BATCHES]
+
+    mb.stream(dt, batches(0, max(args.warmup, E2E_DEPTH)))
+    if world > 1:
+        dist.barrier()
+    c0 = max(args.warmup, E2E_DEPTH)
+    last = {}
+    t0 = time.perf_counter()
+    mb.stream(dt, batches(c0, args.steps), consume=lambda i, slot: last.__setitem__(slot, c0 + i))
+    e2e_s = time.perf_counter() - t0
+    h2d = mb.h2d_bytes
+    # the records of the last batch planned in every slot against the oracle
+    ok = True
+    for slot, i in last.items():
+        ocfg, oplan = oracle.plan_batch_records(pt, *host[i % E2E_BATCHES])
+        cfg, plan = mb.outputs(slot)
+        ok = ok and plan.tobytes() == oplan.tobytes() and cfg.tobytes() == tiny_config(ocfg).tobytes()
+    # the host pack alone (the producer's share of a step)
+    for i in range(20):
+        t = time.perf_counter()
+        mb.fill(*host[i % E2E_BATCHES], slot=0)
+        pack_s.append(time.perf_counter() - t)
 
     def steps(c0, k, pack=True):
         for i in range(c0, c0 + k):
             slot = i % E2E_DEPTH
-            mb.wait(slot)                    # step i - depth has finished with this slot's blocks
+            mb.wait(slot)
             if pack:
-                t = time.perf_counter()
                 mb.fill(*host[i % E2E_BATCHES], slot=slot)
-                pack_s.append(time.perf_counter() - t)
             mb.submit(dt, slot)
         for slot in range(E2E_DEPTH):
             mb.wait(slot)
 
-    steps(0, max(args.warmup, E2E_DEPTH))
-    pack_s.clear()
-    if world > 1:
-        dist.barrier()
-    c0 = max(args.warmup, E2E_DEPTH)
-    t0 = time.perf_counter()
-    steps(c0, args.steps)
-    e2e_s = time.perf_counter() - t0
-    h2d = mb.h2d_bytes
-    # the last E2E_DEPTH steps' records against the oracle
-    ok = True
-    for i in range(c0 + args.steps - E2E_DEPTH, c0 + args.steps):
-        ocfg, oplan = oracle.plan_batch_records(pt, *host[i % E2E_BATCHES])
-        cfg, plan = mb.outputs(i % E2E_DEPTH)
-        ok = ok and plan.tobytes() == oplan.tobytes() and cfg.tobytes() == tiny_config(ocfg).tobytes()
     # the same pipeline with the inputs packed outside the loop (one batch per slot)
     for slot in range(E2E_DEPTH):
         mb.fill(*host[slot], slot=slot)
@@ -729,12 +746,13 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     K = n_global * args.steps
     return {"value": K / e2e_s, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": mb.d2h_bytes,
-            "api": "per step: parva_stream_pack_arrays (plain host arrays -> pinned streamed block, host threads) + "
-                   "parva_plan_host_mapped_submit; parva_plan_host_mapped_wait before a slot is reused",
+            "api": "MappedHostBatch.stream: per step parva_stream_pack_arrays (plain host arrays -> pinned streamed "
+                   "block, on the library's host threads, in a producer thread) + parva_plan_host_mapped_submit; "
+                   "parva_plan_host_mapped_wait before a slot is reused; 4 calls in flight + 1 slot being packed",
             "inputs": f"{E2E_BATCHES} different C2 batches in rotation, plain pageable numpy arrays "
                       "(int32 offsets and table ids, f64 rates and bounds)",
             "pipeline_depth": E2E_DEPTH,
-            "host_pack_us_per_step_median": statistics.median(pack_s) * 1e6 if pack_s else None,
+            "host_pack_us_median": statistics.median(pack_s) * 1e6 if pack_s else None,
             "records_equal_oracle_last_steps": ok,
             "prepacked": {"value": K / pre_s, "unit": UNIT,
                           "api": "the same pipeline with every slot's input block packed once outside the loop"},

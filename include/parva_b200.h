@@ -313,6 +313,13 @@ typedef struct {
 int parva_gather_wait(const parva_gather_slot* slot, uint32_t epoch, int32_t release, int64_t timeout_ns,
                       int32_t* d_status, void* stream);
 int parva_gather_release(const parva_gather_slot* slot, uint32_t epoch, void* stream);
+
+/* Benchmark gate: one thread of `stream` waits until the pinned host word
+ * *h_flag equals `value` (PARVA_LAUNCH_ERROR into *d_status after
+ * timeout_ns).  Queue the work of a timed region behind it, then open it:
+ * the region then measures device execution without host launch gaps. */
+int parva_host_gate(const uint32_t* h_flag, uint32_t value, int64_t timeout_ns, int32_t* d_status,
+                    void* stream);
 /* CUDA IPC plumbing for the gathered blocks: an exportable zeroed device
  * allocation, its handle (parva_ipc_handle_bytes() bytes), and the mapping
  * of a peer's handle into this process (peer access enabled lazily). */

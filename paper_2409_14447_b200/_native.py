@@ -75,7 +75,7 @@ class SimResult(C.Structure):
 EXPORTS = (
     "parva_abi_version", "parva_plan_batch_workspace", "parva_build_index", "parva_configure_sweep",
     "parva_plan_batch", "parva_plan_batch_overlapped", "parva_plan_batch_fused", "parva_gather_wait",
-    "parva_gather_release",
+    "parva_gather_release", "parva_host_gate",
     "parva_ipc_alloc", "parva_ipc_free", "parva_ipc_handle_bytes", "parva_ipc_handle", "parva_ipc_open",
     "parva_ipc_close", "parva_plan_batch_preconfigured", "parva_plan_host_scratch", "parva_plan_host",
     "parva_plan_general_workspace", "parva_plan_general", "parva_select_optimal_lists",

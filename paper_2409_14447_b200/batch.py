@@ -535,6 +535,70 @@ class MappedHostBatch:
             self._tickets[slot] = 0
             N.check(N.lib().parva_plan_host_mapped_wait(C.c_uint64(t)), "parva_plan_host_mapped_wait")
 
+    def stream(self, dt: N.DeviceTables, batches, consume=None, optimize: bool = True, threshold: int = 4,
+               stream=None, threads: int = 0) -> int:
+        """Plan an iterable of host batches (scen_off, table ids, rates, bounds)
+        through the slots with a producer thread: while the calling thread
+        submits batch i and waits for earlier ones, the producer packs batch
+        i + 1 into a free slot (the pack and the waits release the GIL), so
+        the host work of a step overlaps the GPU work of the steps in flight.
+        depth - 1 calls are in flight, one slot is being packed.
+        consume(i, slot), if given, runs after batch i's records have landed
+        (read them with outputs(slot)) and before the slot is reused.
+        Returns the number of batches planned."""
+        import queue
+        import threading
+        if self.depth < 2:
+            raise ValueError("stream() needs depth >= 2")
+        for s in range(self.depth):
+            self.wait(s)
+        free, packed = queue.Queue(), queue.Queue()
+        for s in range(self.depth):
+            free.put(s)
+        failure = []
+
+        def produce():
+            try:
+                for i, b in enumerate(batches):
+                    slot = free.get()
+                    if slot is None:
+                        return
+                    self.fill(*b, slot=slot, threads=threads)
+                    packed.put((i, slot))
+            except BaseException as exc:  # noqa: BLE001 -- re-raised by the caller
+                failure.append(exc)
+            packed.put(None)
+
+        th = threading.Thread(target=produce, daemon=True)
+        th.start()
+        inflight = []
+        done = 0
+        try:
+            while True:
+                item = packed.get()
+                if item is None:
+                    break
+                self.submit(dt, item[1], optimize, threshold, stream)
+                inflight.append(item)
+                if len(inflight) == self.depth - 1:
+                    i, slot = inflight.pop(0)
+                    self.wait(slot)
+                    if consume is not None:
+                        consume(i, slot)
+                    done += 1
+                    free.put(slot)
+            for i, slot in inflight:
+                self.wait(slot)
+                if consume is not None:
+                    consume(i, slot)
+                done += 1
+        finally:
+            free.put(None)
+            th.join()
+        if failure:
+            raise failure[0]
+        return done
+
     def __del__(self):
         try:
             for s in range(self.depth):

@@ -625,13 +625,17 @@ class PackPool {
   int size() const { return (int)th_.size() + 1; }
   // fn(task) for task in [0, n_tasks), on up to `width` threads (caller included)
   void run(int n_tasks, int width, const std::function<void(int)>& fn) {
+    if (width <= 1 || n_tasks <= 1 || th_.empty()) {   // the caller alone: no handshake at all
+      for (int i = 0; i < n_tasks; i++) fn(i);
+      return;
+    }
     std::lock_guard<std::mutex> call(call_mu_);   // one call at a time
     const uint64_t g = gen_.load() + 1;
     Job& J = jobs_[g & 1];
     while (J.active.load() != 0) spin_pause();      // (a stale worker of generation g - 2 leaving)
     J.fn = &fn;
     J.n_tasks = n_tasks;
-    J.width = std::max(0, width - 1);
+    J.width = std::min(width - 1, n_tasks - 1);
     J.next.store(0);
     J.taken.store(0);
     J.remaining.store(n_tasks);
@@ -641,7 +645,10 @@ class PackPool {
       cv_.notify_all();
     }
     drain(J);
-    while (J.remaining.load() != 0 || J.active.load() != 0) spin_pause();
+    // every task is done; a worker still leaving drain() reads only this
+    // record's counters, and the record is reused two calls later, after
+    // its active count has dropped to zero (above)
+    while (J.remaining.load() != 0) spin_pause();
   }
 
  private:

@@ -60,9 +60,35 @@ __global__ void gather_wait_kernel(GatherSlotArgs g, uint32_t epoch, int wait, i
   if (r < g.n) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(g.ack[r]), "r"(epoch) : "memory");
 }
 
+// one thread waits until a host-written word (pinned, mapped) equals `value`
+// (benchmark gate: queue a timed region behind it, then open it, so the
+// region measures device execution without host launch gaps)
+__global__ void host_gate_kernel(const volatile uint32_t* flag, uint32_t value, long long timeout_ns, int* status) {
+  const unsigned long long t0 = global_ns();
+  while (*flag != value) {
+    if (timeout_ns > 0 && (long long)(global_ns() - t0) > timeout_ns) {
+      if (status) atomicExch(status, PARVA_LAUNCH_ERROR);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
 }  // namespace parva
 
 extern "C" {
+
+int parva_host_gate(const uint32_t* h_flag, uint32_t value, int64_t timeout_ns, int32_t* d_status, void* stream) {
+  if (!h_flag) return PARVA_BAD_INPUT;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, const_cast<uint32_t*>(h_flag), 0) != cudaSuccess) {
+    cudaGetLastError();
+    return PARVA_BAD_INPUT;   // not pinned, mapped host memory
+  }
+  parva::host_gate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const volatile uint32_t*)d, value,
+                                                              (long long)timeout_ns, (int*)d_status);
+  return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
+}
 
 static int gather_slot_launch(const parva_gather_slot* slot, uint32_t epoch, int wait, int release,
                               int64_t timeout_ns, int32_t* d_status, void* stream) {

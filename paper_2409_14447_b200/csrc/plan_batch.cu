@@ -168,6 +168,8 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
     lo[c] = 0;
     nmax = max(nmax, n[c]);
   }
+#ifndef PARVA_QUAD_SEARCH   // (A/B builds: a 4-ary form, 3 rounds of 15 loads -- measured slower: the
+                            // kernel is issue-bound, the extra probes cost more than the rounds saved)
   for (int step = nmax ? 1 << (31 - __clz(nmax)) : 0; step > 0; step >>= 1) {
 #pragma unroll
     for (int c = 0; c < 5; c++) {
@@ -175,6 +177,21 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
       if (probe <= n[c] && lat_s[s0[c] + probe - 1] < bound) lo[c] = probe;
     }
   }
+#else
+  // 4-ary: three probes per class and round (15 independent loads in
+  // flight), so a segment of <= 63 points takes 3 dependent rounds instead
+  // of 6.  The probes' outcomes are monotone (sorted latencies), so the
+  // count advances by step x (number of true probes).
+  for (int step = nmax ? 1 << (2 * ((31 - __clz(nmax)) >> 1)) : 0; step > 0; step >>= 2) {
+#pragma unroll
+    for (int c = 0; c < 5; c++) {
+      const int p1 = lo[c] + step, p2 = p1 + step, p3 = p2 + step;
+      const double* a = lat_s + s0[c] - 1;
+      const int t = (p1 <= n[c] && a[p1] < bound) + (p2 <= n[c] && a[p2] < bound) + (p3 <= n[c] && a[p3] < bound);
+      lo[c] += step * t;
+    }
+  }
+#endif
 #pragma unroll
   for (int c = 0; c < 5; c++) {
     const int b = lo[c] ? (int)best_s[s0[c] + lo[c] - 1] : -1;
@@ -707,9 +724,19 @@ __device__ __forceinline__ bool plan_scenario_warp(const PlanArgs& A, GScratch<G
       // compaction + regression check (allocator.py:423-435)
       const int n_after = __popc(gp.ballot(lane < ngpus && len > 0));
       const int total_after = warp_sum_i(lane < ngpus ? ngpc : 0, gp);
+#ifdef PARVA_FLOAT_REGRESSION   // (A/B builds: the reference's float form)
       const double ua_before = unallocated(total_before, n_before);
       const double ua_after = unallocated(total_after, n_after);
-      if (n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12)) {
+      const bool regressed = n_after > n_before || ua_after > __dadd_rn(ua_before, 1e-12);
+#else
+      // allocator.py:428-430 in integers: unallocated = 1 - t / (7 n) (0 for
+      // n = 0).  With n <= 32 GPUs two different values differ by at least
+      // 1 / 224^2 >> 1e-12, and equal rationals round to the same double, so
+      // "after > before + 1e-12" is exactly t_after n_before < t_before n_after.
+      const bool regressed = n_after > n_before ||
+                             (n_after > 0 && n_before > 0 && total_after * n_before < total_before * n_after);
+#endif
+      if (regressed) {
         fallback = true;
         *reinterpret_cast<uint4*>(W.lst[lane]) = *reinterpret_cast<const uint4*>(W.bak[lane]);
         len = bak_len; ngpc = bak_ngpc; mask = bak_mask;

@@ -798,3 +798,33 @@ def test_tiny_records_rejected_for_tables_over_254_points():
     cfg, plan = B.plan_batch(dt, off, tab, rate, bound).host()
     ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
     assert cfg.tobytes() == ocfg.tobytes() and plan.tobytes() == oplan.tobytes()
+
+
+def test_host_entry_mapped_stream_producer_thread(fx):
+    """MappedHostBatch.stream: a producer thread packs batch i+1 while the
+    caller submits batch i; every batch's records (checked in consume,
+    before its slot is reused) == oracle."""
+    from paper_2409_14447_b200.records import tiny_config
+    dt = N.device_tables_for(fx.tables)
+    pt = pack_tables(fx.tables)
+    batches, exp = [], []
+    for seed in range(70, 75):
+        sb = W.scenario_batch(fx, 3_000, seed=seed)
+        k, M = sb.rate.shape
+        b = (np.arange(k + 1, dtype=np.int32) * M, np.tile(np.arange(M, dtype=np.int32), k),
+             sb.rate.ravel().copy(), sb.bound.ravel().copy())
+        ocfg, oplan = oracle.plan_batch_records(pt, *b)
+        batches.append(b)
+        exp.append((tiny_config(ocfg).tobytes(), oplan.tobytes()))
+    mb = B.MappedHostBatch(*batches[0], cfg_format=2, plan_bytes=64, depth=3)
+    order = [(3 * i) % 5 for i in range(17)]
+    seen = []
+
+    def consume(i, slot):
+        cfg, plan = mb.outputs(slot)
+        j = order[i]
+        assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0], (i, j)
+        seen.append(i)
+
+    assert mb.stream(dt, (batches[j] for j in order), consume=consume) == len(order)
+    assert sorted(seen) == list(range(len(order)))

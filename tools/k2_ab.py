@@ -22,9 +22,8 @@ OUT = REPO / "tools" / "_variants" / "ab"
 VARIANTS = {
     "ref": ("REF", []),
     "tree": (None, []),
-    "tree_noticket": (None, ["-DPARVA_AB_NO_TICKET"]),
-    "tree_nowait": (None, ["-DPARVA_AB_NO_WAIT"]),
-    "tree_nodone": (None, ["-DPARVA_AB_NO_DONE"]),
+    "tree_binsearch": (None, ["-DPARVA_BINARY_SEARCH"]),
+    "tree_fltreg": (None, ["-DPARVA_FLOAT_REGRESSION"]),
 }
 
 
