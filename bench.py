@@ -694,14 +694,30 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
         for i in range(c0, c0 + k):
             yield host[i % E2E_BATCHES]
 
-    mb.stream(dt, batches(0, max(args.warmup, E2E_DEPTH)))
-    if world > 1:
-        dist.barrier()
+    mode = os.environ.get("PARVA_E2E_MODE", "loop")
     c0 = max(args.warmup, E2E_DEPTH)
     last = {}
-    t0 = time.perf_counter()
-    mb.stream(dt, batches(c0, args.steps), consume=lambda i, slot: last.__setitem__(slot, c0 + i))
-    e2e_s = time.perf_counter() - t0
+    if mode == "stream":
+        mb.stream(dt, batches(0, c0))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        mb.stream(dt, batches(c0, args.steps), consume=lambda i, slot: last.__setitem__(slot, c0 + i))
+        e2e_s = time.perf_counter() - t0
+    else:   # one C call per step: wait for the slot's previous call, pack into its block, submit
+        def loop(a, k):
+            for i in range(a, a + k):
+                slot = i % E2E_DEPTH
+                mb.submit_arrays(dt, slot, *host[i % E2E_BATCHES])
+                last[slot] = i
+            for slot in range(E2E_DEPTH):
+                mb.wait(slot)
+        loop(0, c0)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        loop(c0, args.steps)
+        e2e_s = time.perf_counter() - t0
     h2d = mb.h2d_bytes
     # the records of the last batch planned in every slot against the oracle
     ok = True
@@ -746,9 +762,11 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     K = n_global * args.steps
     return {"value": K / e2e_s, "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": mb.d2h_bytes,
-            "api": "MappedHostBatch.stream: per step parva_stream_pack_arrays (plain host arrays -> pinned streamed "
-                   "block, on the library's host threads, in a producer thread) + parva_plan_host_mapped_submit; "
-                   "parva_plan_host_mapped_wait before a slot is reused; 4 calls in flight + 1 slot being packed",
+            "api": "per step one C call, parva_plan_host_arrays_submit: wait for the slot's previous call, pack the "
+                   "plain host arrays into the slot's pinned streamed block (parva_stream_pack_arrays, on the "
+                   f"library's host threads), submit the K2s launch; {E2E_DEPTH} calls in flight; the host waits "
+                   "for every call's completion word (a producer-thread variant, MappedHostBatch.stream, measured "
+                   "slower: PARVA_E2E_MODE=stream)",
             "inputs": f"{E2E_BATCHES} different C2 batches in rotation, plain pageable numpy arrays "
                       "(int32 offsets and table ids, f64 rates and bounds)",
             "pipeline_depth": E2E_DEPTH,

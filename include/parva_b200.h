@@ -461,10 +461,13 @@ int parva_plan_host_mapped(const parva_tables* tables, const parva_index* index,
  * kernel writes into pinned host memory after a system-scope fence (no
  * stream synchronize).  Consecutive calls on one stream overlap: each is a
  * programmatic dependent launch, so the next call's loaders start streaming
- * its input while the previous call plans its last scenarios.  Each call in
- * flight needs its own scratch and output block (a second call on a scratch
- * first waits for the first).  Replaces a sequence of plan_services calls
- * (pipeline.py:83-111) over successive scenario batches. */
+ * its input while the previous call plans its last scenarios.  Overlap is
+ * bounded by construction on the host: a call on a scratch, or into an
+ * output block, that an unfinished call still uses first waits for that call
+ * (so give each call in flight its own scratch and output block to keep
+ * them overlapping).  The input block must stay unmodified until the call
+ * completes.  Replaces a sequence of plan_services calls (pipeline.py:83-111)
+ * over successive scenario batches. */
 int parva_plan_host_mapped_submit(const parva_tables* tables, const parva_index* index,
                                   int32_t n_scenarios, int32_t n_services, const void* h_in,
                                   int64_t in_bytes, void* h_out, int32_t optimize,
@@ -472,6 +475,21 @@ int parva_plan_host_mapped_submit(const parva_tables* tables, const parva_index*
                                   void* d_scratch, size_t scratch_bytes, void* stream,
                                   uint64_t* ticket);
 int parva_plan_host_mapped_wait(uint64_t ticket);
+
+/* The end-to-end step in one call, from the plain arrays a caller of
+ * parva_plan_host holds (any host memory): wait for any unfinished call
+ * still reading the pinned input block h_in (capacity in_capacity,
+ * parva_stream_bytes), pack the arrays into it (parva_stream_pack_arrays, on
+ * the library's host threads), then parva_plan_host_mapped_submit.  The
+ * records of the call are in h_out after parva_plan_host_mapped_wait(*ticket). */
+int parva_plan_host_arrays_submit(const parva_tables* tables, const parva_index* index,
+                                  int32_t n_scenarios, const int32_t* h_scen_off,
+                                  const int32_t* h_table, const double* h_rate,
+                                  const double* h_bound, int32_t chunk_scen, void* h_in,
+                                  int64_t in_capacity, void* h_out, int32_t optimize,
+                                  int32_t threshold, int32_t cfg_format, int32_t plan_bytes,
+                                  void* d_scratch, size_t scratch_bytes, void* stream,
+                                  uint64_t* ticket);
 
 /* ------------------------------------------------------ general problems */
 /* One problem = a catalogue of segment kinds, a service list, an optional

@@ -83,6 +83,7 @@ EXPORTS = (
     "parva_plan_host_packed_scratch", "parva_plan_host_packed", "parva_prepare_tables",
     "parva_mapped_layout", "parva_plan_host_mapped_scratch", "parva_plan_host_mapped", "parva_stream_bytes",
     "parva_stream_pack", "parva_stream_pack_arrays", "parva_forget_block", "parva_plan_host_mapped_submit", "parva_plan_host_mapped_wait",
+    "parva_plan_host_arrays_submit",
     "parva_simulate", "parva_sim_seed_states", "parva_sim_log1p", "parva_sim_exponential",
 )
 
@@ -138,6 +139,9 @@ def load_library(build_if_missing: bool = True):
             _LIB.parva_stream_bytes.restype = C.c_int64
             _LIB.parva_stream_pack.restype = C.c_int64
             _LIB.parva_stream_pack_arrays.restype = C.c_int64
+            V, I32 = C.c_void_p, C.c_int32
+            _LIB.parva_plan_host_arrays_submit.argtypes = [V, V, I32, V, V, V, V, I32, V, C.c_int64, V, I32, I32,
+                                                           I32, I32, V, C.c_size_t, V, V]
         return _LIB
 
 

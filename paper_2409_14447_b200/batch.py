@@ -528,6 +528,35 @@ class MappedHostBatch:
                                                       C.byref(self._ticket)), "parva_plan_host_mapped_submit")
         self._tickets[slot] = self._ticket.value
 
+    def submit_arrays(self, dt: N.DeviceTables, slot, scen_off, svc_table, svc_rate, svc_bound,
+                      optimize: bool = True, threshold: int = 4, stream=None):
+        """The e2e step in one C call (parva_plan_host_arrays_submit): wait
+        for the slot's previous call, pack the plain arrays (int32 offsets
+        starting at 0 and table ids, f64 rates and bounds -- any host memory,
+        the shape this object was built for) into the slot's pinned block on
+        the library's host threads, and submit.  Returns at once; wait(slot)
+        before reading the slot's outputs."""
+        for a, dt_ in ((scen_off, np.int32), (svc_table, np.int32), (svc_rate, np.float64), (svc_bound, np.float64)):
+            if a.dtype != dt_ or not a.flags.c_contiguous:
+                raise ValueError("submit_arrays: int32 / float64 C-contiguous arrays expected")
+        if len(scen_off) != self.n_scen + 1 or len(svc_table) < self.n_svc:
+            raise ValueError("batch shape differs from the one this MappedHostBatch was built for")
+        key = ("arrays", id(dt), bool(optimize), int(threshold), slot, N.stream_handle(stream).value)
+        hit = self._args.get(key)
+        if hit is None:
+            sh = N.stream_handle(stream)
+            pre = (C.byref(dt.struct), C.byref(dt.index_struct), C.c_int32(self.n_scen))
+            post = (C.c_int32(self.chunk_scen), C.c_void_p(self.h_ins[slot].data_ptr()), C.c_int64(self.in_capacity),
+                    C.c_void_p(self.h_outs[slot].data_ptr()), C.c_int32(int(optimize)), C.c_int32(int(threshold)),
+                    C.c_int32(self.cfg_format), C.c_int32(self.plan_bytes), N.ptr(self.scratches[slot]),
+                    C.c_size_t(self.scratch_bytes), sh, C.byref(self._ticket))
+            hit = self._args[key] = ((pre, post), dt)
+        pre, post = hit[0]
+        N.check(N.lib().parva_plan_host_arrays_submit(*pre, scen_off.ctypes.data, svc_table.ctypes.data,
+                                                      svc_rate.ctypes.data, svc_bound.ctypes.data, *post),
+                "parva_plan_host_arrays_submit")
+        self._tickets[slot] = self._ticket.value
+
     def wait(self, slot: int = 0):
         """Wait until slot `slot`'s last submitted call has written its records."""
         t = self._tickets[slot]

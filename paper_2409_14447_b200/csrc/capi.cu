@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <emmintrin.h>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
@@ -673,6 +674,7 @@ class PackPool {
       uint64_t g;
       for (int k = 0; (g = gen_.load()) == seen && !stop_.load(); k++) {
         spin_pause();
+        if ((k & 4095) == 4095) std::this_thread::yield();   // cede the core if another thread wants it
         if ((k & 255) == 255 &&
             std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) {
           std::unique_lock<std::mutex> lk(mu_);
@@ -700,14 +702,51 @@ class PackPool {
 };
 
 PackPool& pack_pool() {
+  // default: all cores but two (the calling thread takes part in every
+  // pack; one more core stays free for a thread waiting on the GPU -- the
+  // workers spin, and an oversubscribed core stalls a whole pack for a
+  // scheduler quantum)
   static PackPool pool([] {
     const char* e = std::getenv("PARVA_PACK_THREADS");
-    int n = e ? std::atoi(e) : (int)std::thread::hardware_concurrency();
+    const int hw = (int)std::thread::hardware_concurrency();
+    int n = (e && *e) ? std::atoi(e) : hw - 1;
     return std::max(0, std::min(n, 64) - 1);
   }());
   return pool;
 }
 }  // namespace
+
+// copy into pinned memory; with PARVA_PACK_NT=1 non-temporal 16-byte stores
+// (no read-for-ownership of the destination; A/B switch)
+static bool pack_nt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PARVA_PACK_NT");
+    v = (e && *e == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+static void pack_copy(void* dst, const void* src, size_t bytes) {
+  uint8_t* d = (uint8_t*)dst;
+  const uint8_t* p = (const uint8_t*)src;
+  if (!pack_nt() || ((uintptr_t)d & 15)) {
+    std::memcpy(d, p, bytes);
+    return;
+  }
+  size_t i = 0;
+  for (; i + 64 <= bytes; i += 64) {
+    const __m128i a = _mm_loadu_si128((const __m128i*)(p + i));
+    const __m128i b = _mm_loadu_si128((const __m128i*)(p + i + 16));
+    const __m128i c = _mm_loadu_si128((const __m128i*)(p + i + 32));
+    const __m128i e = _mm_loadu_si128((const __m128i*)(p + i + 48));
+    _mm_stream_si128((__m128i*)(d + i), a);
+    _mm_stream_si128((__m128i*)(d + i + 16), b);
+    _mm_stream_si128((__m128i*)(d + i + 32), c);
+    _mm_stream_si128((__m128i*)(d + i + 48), e);
+  }
+  for (; i + 16 <= bytes; i += 16) _mm_stream_si128((__m128i*)(d + i), _mm_loadu_si128((const __m128i*)(p + i)));
+  if (i < bytes) std::memcpy(d + i, p + i, bytes - i);
+}
 
 // Streamed input block from plain arrays (int32 table ids), multi-threaded:
 // pass 1 sizes every chunk (template detection), a prefix sum places them,
@@ -774,8 +813,8 @@ int64_t parva_stream_pack_arrays(int32_t n_scenarios, const int32_t* h_scen_off,
         for (int32_t k = a; k <= b; k++) so[k - a] = h_scen_off[k] - sa;
         std::memset(p + int64_t(b - a + 1) * 4, 0, size_t(rate_at - int64_t(b - a + 1) * 4));
       }
-      std::memcpy(p + rate_at, h_rate + sa, size_t(m) * 8);
-      std::memcpy(p + rate_at + m * 8, h_bound + sa, size_t(m) * 8);
+      pack_copy(p + rate_at, h_rate + sa, size_t(m) * 8);
+      pack_copy(p + rate_at + m * 8, h_bound + sa, size_t(m) * 8);
       uint16_t* t16 = reinterpret_cast<uint16_t*>(p + rate_at + m * 16);
       const int64_t nt = tm ? tmpl[c] : m;
       for (int64_t i = 0; i < nt; i++) {
@@ -785,6 +824,7 @@ int64_t parva_stream_pack_arrays(int32_t n_scenarios, const int32_t* h_scen_off,
       const int64_t end = rate_at + m * 16 + nt * 2;
       std::memset(p + end, 0, size_t(blk[c + 1] - blk[c] - end));
     }
+    if (pack_nt()) _mm_sfence();
   });
   return total;
 }
@@ -843,6 +883,9 @@ struct MappedSlot {
   uint32_t epoch = 0;
   uint32_t submitted = 0;       // epoch of the last asynchronous call (0 = none)
   cudaStream_t stream = nullptr;
+  const void* h_out = nullptr;  // output block of the last call
+  const void* h_in = nullptr;   // input block of the last call
+  uint32_t* d_done = nullptr;   // device address of its completion word
 };
 constexpr int kMappedSlots = 1024;
 static std::vector<MappedSlot> g_mapped_slots;
@@ -870,6 +913,7 @@ static bool done_reached(uint32_t slot, uint32_t epoch) {
 // queried now and then so a failed launch cannot hang the host.
 static int wait_done(uint32_t slot, uint32_t epoch, cudaStream_t s) {
   for (uint64_t i = 0;; i++) {
+    __builtin_ia32_pause();
     if (done_reached(slot, epoch)) {
       std::atomic_thread_fence(std::memory_order_acquire);
       return PARVA_OK;
@@ -913,6 +957,8 @@ static int plan_host_mapped(const parva_tables* tables, const parva_index* index
   uint32_t epoch = 0, slot = 0, pending = 0;
   uint32_t* d_done = nullptr;
   cudaStream_t pending_stream = nullptr;
+  struct Busy { uint32_t slot, epoch; cudaStream_t stream; };
+  std::vector<Busy> out_busy;
   {
     std::lock_guard<std::mutex> lock(g_graph_mu);
     if (ticket && !g_done_host) {
@@ -946,20 +992,41 @@ static int plan_host_mapped(const parva_tables* tables, const parva_index* index
       M.dev = dev; M.scratch = d_scratch; M.bytes = scratch_bytes;
       if (g_done_host) g_done_host[E] = 0;
     }
+    // an unfinished call on another scratch that writes the same output
+    // block must complete first too (two calls never write one block at once)
+    for (int i = 0; i < (int)g_mapped_slots.size(); i++) {
+      const MappedSlot& e = g_mapped_slots[i];
+      if (i != E && e.h_out == h_out && e.submitted && !done_reached((uint32_t)i, e.submitted))
+        out_busy.push_back({(uint32_t)i, e.submitted, e.stream});
+    }
     MappedSlot& M = g_mapped_slots[E];
     slot = (uint32_t)E;
     pending = M.submitted;
     pending_stream = M.stream;
     epoch = ++M.epoch;
+    M.h_out = h_out;
+    M.h_in = h_in;
     if (ticket) { M.submitted = epoch; M.stream = s; }
     else M.submitted = 0;
   }
-  // one call in flight per scratch: an unfinished asynchronous call on it
-  // must complete first
+  // one call in flight per scratch and per output block: an unfinished
+  // asynchronous call on either must complete first
   if (pending && wait_done(slot, pending, pending_stream) != PARVA_OK) return PARVA_LAUNCH_ERROR;
-  if (ticket && cudaHostGetDevicePointer((void**)&d_done, g_done_host + slot, 0) != cudaSuccess) {
-    cudaGetLastError();
-    return PARVA_LAUNCH_ERROR;
+  for (const auto& b : out_busy)
+    if (wait_done(b.slot, b.epoch, b.stream) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+  if (ticket) {
+    {
+      std::lock_guard<std::mutex> lock(g_graph_mu);
+      d_done = g_mapped_slots[slot].d_done;
+    }
+    if (!d_done) {
+      if (cudaHostGetDevicePointer((void**)&d_done, g_done_host + slot, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return PARVA_LAUNCH_ERROR;
+      }
+      std::lock_guard<std::mutex> lock(g_graph_mu);
+      g_mapped_slots[slot].d_done = d_done;
+    }
   }
   if (n_scenarios > 0) {
     uint8_t* out = (uint8_t*)d_out;
@@ -1017,6 +1084,37 @@ int parva_plan_host_mapped_submit(const parva_tables* tables, const parva_index*
                                   int32_t optimize, int32_t threshold, int32_t cfg_format, int32_t plan_bytes,
                                   void* d_scratch, size_t scratch_bytes, void* stream, uint64_t* ticket) {
   if (!ticket) return PARVA_BAD_INPUT;
+  return plan_host_mapped(tables, index, n_scenarios, n_services, h_in, in_bytes, h_out, optimize, threshold,
+                          cfg_format, plan_bytes, d_scratch, scratch_bytes, stream, ticket);
+}
+
+// Pack + submit in one call: waits for any unfinished call still reading
+// h_in (the block is rewritten here), packs the caller's plain arrays into it
+// on the pack pool, then submits as parva_plan_host_mapped_submit.
+int parva_plan_host_arrays_submit(const parva_tables* tables, const parva_index* index, int32_t n_scenarios,
+                                  const int32_t* h_scen_off, const int32_t* h_table, const double* h_rate,
+                                  const double* h_bound, int32_t chunk_scen, void* h_in, int64_t in_capacity,
+                                  void* h_out, int32_t optimize, int32_t threshold, int32_t cfg_format,
+                                  int32_t plan_bytes, void* d_scratch, size_t scratch_bytes, void* stream,
+                                  uint64_t* ticket) {
+  if (!ticket || !h_in || !h_scen_off || n_scenarios < 0) return PARVA_BAD_INPUT;
+  *ticket = 0;
+  struct Busy { uint32_t slot, epoch; cudaStream_t stream; };
+  std::vector<Busy> busy;
+  {
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (int i = 0; i < (int)g_mapped_slots.size(); i++) {
+      const MappedSlot& e = g_mapped_slots[i];
+      if (e.h_in == h_in && e.submitted && g_done_host && !done_reached((uint32_t)i, e.submitted))
+        busy.push_back({(uint32_t)i, e.submitted, e.stream});
+    }
+  }
+  for (const auto& b : busy)
+    if (wait_done(b.slot, b.epoch, b.stream) != PARVA_OK) return PARVA_LAUNCH_ERROR;
+  const int64_t in_bytes = parva_stream_pack_arrays(n_scenarios, h_scen_off, h_table, h_rate, h_bound, chunk_scen,
+                                                    h_in, in_capacity, 0);
+  if (in_bytes < 0) return PARVA_BAD_INPUT;
+  const int32_t n_services = n_scenarios ? h_scen_off[n_scenarios] : 0;
   return plan_host_mapped(tables, index, n_scenarios, n_services, h_in, in_bytes, h_out, optimize, threshold,
                           cfg_format, plan_bytes, d_scratch, scratch_bytes, stream, ticket);
 }

@@ -828,3 +828,35 @@ def test_host_entry_mapped_stream_producer_thread(fx):
 
     assert mb.stream(dt, (batches[j] for j in order), consume=consume) == len(order)
     assert sorted(seen) == list(range(len(order)))
+
+
+def test_host_entry_arrays_submit(fx):
+    """parva_plan_host_arrays_submit (wait for the slot, pack the plain
+    arrays, submit -- one C call per step), 3 slots, 14 steps over 5
+    batches: every step's records == oracle."""
+    from paper_2409_14447_b200.records import tiny_config
+    dt = N.device_tables_for(fx.tables)
+    pt = pack_tables(fx.tables)
+    batches, exp = [], []
+    for seed in range(90, 95):
+        sb = W.scenario_batch(fx, 2_500, seed=seed)
+        k, M = sb.rate.shape
+        b = (np.arange(k + 1, dtype=np.int32) * M, np.tile(np.arange(M, dtype=np.int32), k),
+             sb.rate.ravel().copy(), sb.bound.ravel().copy())
+        ocfg, oplan = oracle.plan_batch_records(pt, *b)
+        batches.append(b)
+        exp.append((tiny_config(ocfg).tobytes(), oplan.tobytes()))
+    mb = B.MappedHostBatch(*batches[0], cfg_format=2, plan_bytes=64, depth=3)
+    last = {}
+    for i in range(14):
+        slot, j = i % 3, (2 * i + 1) % 5
+        if slot in last:
+            mb.wait(slot)
+            cfg, plan = mb.outputs(slot)
+            assert plan.tobytes() == exp[last[slot]][1] and cfg.tobytes() == exp[last[slot]][0], i
+        mb.submit_arrays(dt, slot, *batches[j])
+        last[slot] = j
+    for slot, j in last.items():
+        mb.wait(slot)
+        cfg, plan = mb.outputs(slot)
+        assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0]
