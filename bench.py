@@ -335,6 +335,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 / simulator side measurements")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end host-entry measurement")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="enqueue the timed steps without the host gate (needed under ncu, which serializes "
+                         "launches: the gate kernel would never see its word written)")
     ap.add_argument("--sweep-workloads", type=int, default=10_000)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -518,12 +521,16 @@ def main():
     # the K steps are queued behind a gate (one thread spinning on a pinned
     # host word) and the gate is opened once they are all enqueued: the
     # events then time device execution only, with no host launch gaps
+    # a host-blocking collective (gloo copies CUDA tensors to the host) would
+    # wait behind the gate forever: no gate for the gloo test path either
+    use_gate = not args.no_gate and not (world > 1 and gather_mode == "nccl" and backend != "nccl")
     gate = torch.zeros(1, dtype=torch.int32).pin_memory()
     gate_err = torch.zeros(1, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
     clk.begin()
-    N.check(L.parva_host_gate(C.c_void_p(gate.data_ptr()), C.c_uint32(1), C.c_int64(int(30e9)), N.ptr(gate_err), sh),
-            "parva_host_gate")
+    if use_gate:
+        N.check(L.parva_host_gate(C.c_void_p(gate.data_ptr()), C.c_uint32(1), C.c_int64(int(30e9)), N.ptr(gate_err),
+                                  sh), "parva_host_gate")
     t_start.record(stream)
     for item in timed:
         st.launch(item)
@@ -624,13 +631,15 @@ def main():
                    "scenarios_per_gpu": n, "services_per_scenario": 11, "global_batch": n_global,
                    "l2": "not reused: steps cycle through resident input batches larger than L2 in total",
                    "input_batches": P, "output_slots": S,
-                   "launch": "parva_plan_batch_overlapped / _fused per step (programmatic dependent launches; "
-                             "slot tickets serialize launches sharing an output slot), all K steps enqueued behind a "
-                             "gate kernel that is opened once they are queued (device time, no host launch gaps); "
-                             "kernel_ms_per_step from separate one-at-a-time launches",
+                   "launch": ("parva_plan_batch_overlapped / _fused per step (programmatic dependent launches; "
+                              "slot tickets serialize launches sharing an output slot), "
+                              + ("all K steps enqueued behind a gate kernel that is opened once they are queued "
+                                 "(device time, no host launch gaps); " if use_gate
+                                 else "no gate (host launch gaps included); ")
+                              + "kernel_ms_per_step from separate one-at-a-time launches"),
                    "parallelism": f"scenario-sharded x{world}" + par,
                    "gather": gather_mode, "optimize": True, "threshold": 4},
-        "gpu_launches": args.steps * launches_per_step,
+        "gpu_launches": args.steps * launches_per_step + (1 if use_gate else 0),
         "kernel_ms_per_step": kern_ms / args.steps,
         "roofline": {"bound": "hbm", "kernel": "plan_batch_kernel (fused configure + relocate + optimize)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

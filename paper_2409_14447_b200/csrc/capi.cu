@@ -123,6 +123,9 @@ static int plan_batch_impl(const parva_tables* tables, const parva_index* index,
   // SM's CTAs (measured: 22.6 -> 21.3 us per overlapped C2 step; a single
   // launch is faster with the staged copy, 31.7 vs 35 us)
   A.smem_index = !cfg_given && !pdl && tables->n_points * 18 <= (int64_t)kSmemIndexLimit;
+#ifdef PARVA_NO_SMEM_INDEX   // (A/B builds: small CTAs read the index through L1)
+  A.smem_index = 0;
+#endif
   A.cfg = d_cfg;
   A.cfg_format = cfg_format;
   A.plan = d_plan;

@@ -100,7 +100,10 @@ constexpr double kCountLimit = 1099511627776.0;  // 2^40 segments per service
 // per-size-class best throughputs (tp[c] > 0 iff size class c present).
 // Fills opt_sc, last_sc, count, coverage, status of a config record.  Only
 // constant indices into tp[] (after unrolling), so it stays in registers.
-__device__ inline void match_demand(const double tp[5], double rate, parva_config_record& r) {
+// with_coverage = false skips Service.coverage (for the record formats that
+// do not carry it: compact and tiny).
+__device__ inline void match_demand(const double tp[5], double rate, parva_config_record& r,
+                                    bool with_coverage = true) {
   int o = -1;
   double topt = 0.0;
 #pragma unroll
@@ -144,7 +147,7 @@ __device__ inline void match_demand(const double tp[5], double rate, parva_confi
   }
   r.last_sc = (int8_t)last;
   r.count = count;
-  r.coverage = coverage_sum(topt, count, last >= 0, tlast);
+  r.coverage = with_coverage ? coverage_sum(topt, count, last >= 0, tlast) : 0.0;
   r.status = PARVA_OK;
 }
 

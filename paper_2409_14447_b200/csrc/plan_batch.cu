@@ -44,6 +44,12 @@ namespace parva {
 #endif
 constexpr int PB_WARPS = PARVA_PB_WARPS;
 constexpr int PB_THREADS = PB_WARPS * 32;
+// the tile kernel's CTA shape (K2, device-resident batches)
+#ifndef PARVA_TK_WARPS
+#define PARVA_TK_WARPS PARVA_PB_WARPS
+#endif
+constexpr int TK_WARPS = PARVA_TK_WARPS;
+constexpr int TK_THREADS = TK_WARPS * 32;
 // Per-group scratch of the warp planner; G lanes = G GPUs at most.  The
 // refill queues hold G*7 segments: more than the other G-1 GPUs' 7(G-1)
 // slots cannot fit anyway (the drain then needs a new GPU).
@@ -154,16 +160,17 @@ __device__ __noinline__ bool ticket_wait(const unsigned long long* count, unsign
 // of points with lat < bound (binary search over the latency-sorted
 // segment), winner = prefix argmax at count-1.  The five searches advance in
 // lockstep (branch-free power-of-two steps) so their loads overlap.
+template <typename SegT>
 __device__ __forceinline__ void configure_indexed(const double* lat_s, const uint16_t* best_s,
-                                                  const double* tp, int tp_stride, const int* seg_s,
+                                                  const double* tp, int tp_stride, const SegT* seg_s,
                                                   const int* seg_n, int t, double bound,
                                                   double rate, parva_config_record& r,
-                                                  double tpc[5]) {
+                                                  double tpc[5], bool with_coverage = true) {
   int s0[5], n[5], lo[5];
   int nmax = 0;
 #pragma unroll
   for (int c = 0; c < 5; c++) {
-    s0[c] = seg_s[t * 5 + c];
+    s0[c] = (int)seg_s[t * 5 + c];
     n[c] = seg_n[t * 5 + c];
     lo[c] = 0;
     nmax = max(nmax, n[c]);
@@ -198,7 +205,7 @@ __device__ __forceinline__ void configure_indexed(const double* lat_s, const uin
     r.best[c] = (int16_t)b;
     tpc[c] = b >= 0 ? tp[(s0[c] + b) * tp_stride] : 0.0;
   }
-  match_demand(tpc, rate, r);
+  match_demand(tpc, rate, r, with_coverage);
   if (r.status == PARVA_INFEASIBLE_SLO) r.opt_sc = -1;
 }
 
@@ -478,12 +485,12 @@ __device__ unsigned long long g_warp_wait[1024][PB_WARPS][4];
 struct alignas(16) TileSmem {
   double tp[kTileSvc * 5];                // best tp per (tile service, size class); 0 = absent
   uint64_t meta[kTileSvc];                // count | opt << 48 | last << 52 | status << 56 (15 = none)
-  int32_t off[PB_THREADS + 1];            // tile scenario offsets (absolute service index)
+  int32_t off[TK_THREADS + 1];            // tile scenario offsets (absolute service index)
   int32_t next;                           // next tile scenario to plan (half-warp pass)
   int32_t next_over;                      // next overflow entry (full-warp pass)
   int32_t n_over;
   int32_t go;                             // slot ticket granted (first tile)
-  int16_t over[PB_THREADS];               // tile scenarios beyond a half-warp's width
+  int16_t over[TK_THREADS];               // tile scenarios beyond a half-warp's width
 };
 
 __device__ __forceinline__ uint64_t pack_meta(int opt, int last, int status, long long count) {
@@ -502,7 +509,8 @@ __device__ __forceinline__ uint64_t svc_configure(const PlanArgs& A, const Index
     for (int c = 0; c < 5; c++) { r.best[c] = -1; tpc[c] = 0.0; }
     r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
   } else {
-    configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, bound, rate, r, tpc);
+    configure_indexed(V.lat, V.best, V.tp, V.tp_stride, V.seg_s, V.seg_n, t, bound, rate, r, tpc,
+                      A.cfg_format == PARVA_CFG_FULL);
   }
   store_config(A, out_i, r);
   return pack_meta(r.opt_sc, r.last_sc, r.status, r.count);
@@ -892,7 +900,7 @@ __device__ __forceinline__ bool run_tiles(const PlanArgs& A, const IndexView& V,
     const int a_end = T.off[n_tile];
 
     // configure the tile's services
-    for (int i = a0 + tid; i < a_end; i += PB_THREADS) {
+    for (int i = a0 + tid; i < a_end; i += TK_THREADS) {
       double tpc[5];
       const uint64_t m = src_service(A, V, S, i, tpc);
       const int li = i - a0;
@@ -966,13 +974,13 @@ __device__ __forceinline__ bool run_tiles(const PlanArgs& A, const IndexView& V,
         uint4* pd = reinterpret_cast<uint4*>(A.mirror_plan[m] + p0);
         uint2* cd = reinterpret_cast<uint2*>(A.mirror_cfg[m] + c0);
         if (pd == ps) continue;   // this rank's own part of the slot is the launch's output
-        for (size_t x = tid; x < pn; x += PB_THREADS) pd[x] = ps[x];
-        for (size_t x = tid; x < cn; x += PB_THREADS) cd[x] = cs[x];
+        for (size_t x = tid; x < pn; x += TK_THREADS) pd[x] = ps[x];
+        for (size_t x = tid; x < cn; x += TK_THREADS) cd[x] = cs[x];
       }
       if (A.plan_bytes == 64) {
         // 64-byte records: a spilled scenario's full record (overflow area,
         // same index) follows it; one warp per scenario of the tile
-        for (int j = tid >> 5; j < n_tile; j += PB_WARPS) {
+        for (int j = tid >> 5; j < n_tile; j += TK_WARPS) {
           const size_t kk = (size_t)(S.scen_base + k + j);
           if (reinterpret_cast<const uint8_t*>(A.plan)[kk * 64] == PARVA_SPILLED && lane < 8) {
             const uint4 v = reinterpret_cast<const uint4*>(A.spill + kk * 128)[lane];
@@ -992,9 +1000,9 @@ __device__ __forceinline__ bool run_tiles(const PlanArgs& A, const IndexView& V,
 #endif
 // kMirror: the fused all-gather instantiation (parva_plan_batch_fused)
 template <bool kMirror>
-__global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
+__global__ void __launch_bounds__(TK_THREADS, PARVA_TILE_MINB) plan_batch_kernel(PlanArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * PB_WARPS);
+  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw + kWarpArea * TK_WARPS);
   __shared__ uint64_t bar;
   // an overlapped successor (parva_plan_batch_overlapped / _fused) may take
   // SM slots as this grid's CTAs retire; the slot ticket keeps it from
@@ -1003,7 +1011,7 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_TILE_MINB) plan_batch_kernel
   PHASE(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) T.go = 1;
-  const IndexView V = load_index(A, smem_raw + kWarpArea * PB_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
+  const IndexView V = load_index(A, smem_raw + kWarpArea * TK_WARPS + sizeof(TileSmem), !A.cfg_given, &bar);
   PHASE(1);
   // this CTA's contiguous block of scenarios
   const int per = (A.n_scen + gridDim.x - 1) / gridDim.x;
@@ -1301,6 +1309,8 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
   }
 }
 
+#include "plan_thread.cuh"
+
 size_t index_smem_bytes(int n_tables, int64_t n_points, bool smem_index, bool lat_best) {
   size_t b = (size_t(n_tables) * 5 * 8 + 15) & ~size_t(15);
   if (smem_index) {
@@ -1315,33 +1325,52 @@ struct LaunchCfg {
   size_t smem;
 };
 
-// device-resident batches: the tile kernel (configure a tile with every
-// thread, then plan); streamed batches: the warp-autonomous kernel
+// device-resident batches: the thread-per-scenario kernel (PARVA_K2_THREAD,
+// default) or the tile kernel (configure a tile with every thread, then
+// plan with lane groups); K1's config records given: the tile kernel;
+// streamed batches: the warp-autonomous kernel
+#ifndef PARVA_K2_THREAD
+#define PARVA_K2_THREAD 1
+#endif
 static bool warp_mode(const PlanArgs& A) { return A.stream_src != nullptr; }
+static bool thread_mode(const PlanArgs& A) { return PARVA_K2_THREAD && !warp_mode(A) && !A.cfg_given; }
+
+struct KernelSel {
+  const void* fn;
+  int kind, threads, per_cta;   // per_cta: scenarios one CTA takes per pass (grid sizing)
+};
+
+static KernelSel plan_kernel(const PlanArgs& A) {
+  if (warp_mode(A)) return {(const void*)plan_warp_kernel, 1, PB_THREADS, PB_WARPS};
+  const bool mir = A.n_mirror > 0;
+  if (thread_mode(A))
+    return {mir ? (const void*)plan_thread_kernel<true> : (const void*)plan_thread_kernel<false>, mir ? 4 : 3,
+            TH_THREADS, 32 * TH_WARPS};
+  return {mir ? (const void*)plan_batch_kernel<true> : (const void*)plan_batch_kernel<false>, mir ? 2 : 0,
+          TK_THREADS, TK_WARPS};
+}
 
 static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
   const bool wm = warp_mode(A);
-  const bool mir = !wm && A.n_mirror > 0;
-  const void* fn = wm ? (const void*)plan_warp_kernel
-                      : mir ? (const void*)plan_batch_kernel<true> : (const void*)plan_batch_kernel<false>;
-  const int kind = wm ? 1 : mir ? 2 : 0;
-  const size_t smem = (wm ? (kWarpArea + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
-                          : kWarpArea * PB_WARPS + sizeof(TileSmem)) +
-                      index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
+  const KernelSel K = plan_kernel(A);
+  const size_t smem = K.kind >= 3 ? sizeof(ThWarp) * TH_WARPS
+                                  : (wm ? (kWarpArea + sizeof(WarpSvc)) * PB_WARPS + size_t(kLoaderBufs) * kStreamSlice
+                                        : kWarpArea * TK_WARPS + sizeof(TileSmem)) +
+                                        index_smem_bytes(A.n_tables, A.n_points, A.smem_index, !A.cfg_given);
   // per-device caches: smem attribute set, occupancy for the smem size used
   struct DevCfg { size_t conf, occ; int n_sm, per; };
-  static DevCfg s_cfg[kMaxDevices][3];
+  static DevCfg s_cfg[kMaxDevices][5];
   int dev = 0;
   cudaGetDevice(&dev);
-  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][kind];
+  DevCfg& D = s_cfg[dev & (kMaxDevices - 1)][K.kind];
   if (smem > D.conf) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(K.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
     D.conf = smem;
   }
   if (!D.n_sm) cudaDeviceGetAttribute(&D.n_sm, cudaDevAttrMultiProcessorCount, dev);
   if (smem != D.occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per, fn, PB_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&D.per, K.fn, K.threads, smem);
     D.occ = smem;
   }
   if (D.per < 1) return false;
@@ -1358,7 +1387,7 @@ static bool plan_launch_config(const PlanArgs& A, LaunchCfg* L) {
     }
     if (s_env > 0) per = std::min(per, s_env);
   }
-  int g = (A.n_scen + PB_WARPS - 1) / PB_WARPS;
+  int g = (A.n_scen + K.per_cta - 1) / K.per_cta;
   if (wm) g = std::max(g, A.n_loaders);
   if (g > D.n_sm * per) g = D.n_sm * per;
   L->grid = g < 1 ? 1 : g;
@@ -1393,23 +1422,20 @@ int launch_plan_batch(const PlanArgs& A, cudaStream_t stream) {
     cfg.attrs = at;
     cfg.numAttrs = A.pdl ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, plan_warp_kernel, B) != cudaSuccess) return PARVA_LAUNCH_ERROR;
-  } else if (A.pdl) {
+  } else {
+    const KernelSel K = plan_kernel(A);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(L.grid);
-    cfg.blockDim = dim3(PB_THREADS);
+    cfg.blockDim = dim3(K.threads);
     cfg.dynamicSmemBytes = L.smem;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t e = A.n_mirror ? cudaLaunchKernelEx(&cfg, plan_batch_kernel<true>, A)
-                                     : cudaLaunchKernelEx(&cfg, plan_batch_kernel<false>, A);
-    if (e != cudaSuccess) return PARVA_LAUNCH_ERROR;
-  } else {
-    if (A.n_mirror) plan_batch_kernel<true><<<L.grid, PB_THREADS, L.smem, stream>>>(A);
-    else plan_batch_kernel<false><<<L.grid, PB_THREADS, L.smem, stream>>>(A);
+    cfg.numAttrs = A.pdl ? 1 : 0;
+    void* args[] = {const_cast<PlanArgs*>(&A)};
+    if (cudaLaunchKernelExC(&cfg, K.fn, args) != cudaSuccess) return PARVA_LAUNCH_ERROR;
   }
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
 }
@@ -1421,10 +1447,10 @@ int add_plan_batch_node(cudaGraph_t g, const PlanArgs& A, const cudaGraphNode_t*
   PlanArgs copy = A;
   void* args[] = {&copy};
   cudaKernelNodeParams p = {};
-  p.func = warp_mode(A) ? (void*)plan_warp_kernel
-                         : A.n_mirror ? (void*)plan_batch_kernel<true> : (void*)plan_batch_kernel<false>;
+  const KernelSel K = plan_kernel(A);
+  p.func = const_cast<void*>(K.fn);
   p.gridDim = dim3(L.grid);
-  p.blockDim = dim3(PB_THREADS);
+  p.blockDim = dim3(K.threads);
   p.sharedMemBytes = (unsigned)L.smem;
   p.kernelParams = args;
   return cudaGraphAddKernelNode(node, g, deps, ndeps, &p) == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;

@@ -10,11 +10,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench exit $?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2>gpurun_out/${TAG}_bench_ref.err; echo "ref exit $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
-  python bench.py --steps 5 --warmup 3 --no-cpu --no-extra > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1; echo "ncu launches exit $?"
+  python bench.py --steps 5 --warmup 3 --no-cpu --no-extra --no-gate > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1; echo "ncu launches exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'plan_batch_kernel' \
-  -c 1 -f -o gpurun_out/${TAG}_full_k2 python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-sweep > gpurun_out/${TAG}_ncu_full_k2.log 2>&1; echo "ncu k2 exit $?"
+  -c 1 -f -o gpurun_out/${TAG}_full_k2 python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-gate --no-sweep > gpurun_out/${TAG}_ncu_full_k2.log 2>&1; echo "ncu k2 exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'plan_warp_kernel' \
-  -c 1 -f -o gpurun_out/${TAG}_full_k2s python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-sweep > gpurun_out/${TAG}_ncu_full_k2s.log 2>&1; echo "ncu k2s exit $?"
+  -c 1 -f -o gpurun_out/${TAG}_full_k2s python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-gate --no-sweep > gpurun_out/${TAG}_ncu_full_k2s.log 2>&1; echo "ncu k2s exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'configure_sweep_kernel' \
-  -c 1 -f -o gpurun_out/${TAG}_full_k1 python bench.py --steps 3 --warmup 3 --no-cpu --no-extra > gpurun_out/${TAG}_ncu_full_k1.log 2>&1; echo "ncu k1 exit $?"
+  -c 1 -f -o gpurun_out/${TAG}_full_k1 python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-gate > gpurun_out/${TAG}_ncu_full_k1.log 2>&1; echo "ncu k1 exit $?"
 ls gpurun_out | grep ${TAG}

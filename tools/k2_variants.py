@@ -23,12 +23,12 @@ def variants():
     """name -> (patch list, extra flags).  A patch file holds OLD/NEW blocks
     separated by lines '<<<<' / '====' / '>>>>'.  "head" is the committed
     csrc/ (git HEAD), "base" the working tree."""
-    vs = {"head": (["HEAD"], []), "base": ([], [])}
+    vs = {"base": ([], [])} if os.environ.get("K2_NO_HEAD") else {"head": (["HEAD"], []), "base": ([], [])}
     for w, mb in ():   # launch-shape variants, e.g. ((17, 2), (12, 3), (24, 1))
         vs[f"w{w}_b{mb}"] = ([], [f"-DPARVA_PB_WARPS={w}", f"-DPARVA_PB_MINB={mb}"])
     # flag variants, e.g. ("-DPARVA_PB_WARPS=12", "-DPARVA_TILE_MINB=3", "-DPARVA_TILE_SVC=256"),
     # ("-DPARVA_STREAM_SLICE=16384",), ("-DPARVA_NO_OUT",) (K2s without its record writes)
-    for flags in ():
+    for flags in (tuple(f.split()) for f in os.environ.get("K2_FLAGS", "").split(",") if f):
         vs["_".join(f[8:].replace("=", "") for f in flags)] = ([], list(flags))
     if PATCH_DIR.exists():
         for f in sorted(PATCH_DIR.glob("*.patch")):
@@ -76,8 +76,8 @@ def build():
         inc = str(REPO / "include")
         cmd = [b.NVCC, *b.FLAGS, *flags, "-o", str(lib), *[str(d / s) for s in sources], "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        i = r.stderr.find("_ZN5parva17plan_batch_kernel")
-        print(name, r.returncode, r.stderr[i:i + 300].split("\n")[1:2], r.stderr[:300] if r.returncode else "")
+        i = r.stderr.find(os.environ.get("K2_FN", "_ZN5parva18plan_thread_kernelILb0"))
+        print(name, r.returncode, r.stderr[i:i + 400].split("\n")[1:4], r.stderr[:300] if r.returncode else "")
 
 
 def run():
@@ -121,19 +121,41 @@ def run():
         if not hasattr(run, "_batches"):
             run._batches = [c2_inputs(fx, 10_000, 0 if p == 0 else 1000 + p) for p in range(16)]
         dbat = [[N.to_device(a) for a in bt] for bt in run._batches]
-        outs = [B.plan_batch(dt, *dbat[0]) for _ in range(3)]
+        outs = [B.plan_batch(dt, *dbat[0]) for _ in range(16)]
+        ring = B.SlotRing(16)
+        gate = torch.zeros(1, dtype=torch.int32).pin_memory()
+        gerr = torch.zeros(1, dtype=torch.int32, device="cuda")
+        sh = N.stream_handle(s)
         for rep in range(2):
-            for i in range(200 if rep else 20):
-                if i == 0 and rep:
-                    torch.cuda.synchronize()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(s)
-                B.plan_batch(dt, *dbat[i % 16], out=outs[i % 3], overlap=True)
-            if rep:
-                b.record(s)
+            torch.cuda.synchronize()
+            gate.zero_()
+            lib.parva_host_gate(C.c_void_p(gate.data_ptr()), C.c_uint32(1), C.c_int64(int(30e9)), N.ptr(gerr), sh)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for i in range(200):
+                B.plan_batch(dt, *dbat[i % 16], out=outs[i % 16], overlap=True, ticket=ring.ticket(i % 16, 10_000))
+            b.record(s)
+            gate.numpy()[0] = 1
         torch.cuda.synchronize()
+        ring.check()
         ov = a.elapsed_time(b) * 1e3 / 200
-        ok_ov = outs[199 % 3].host()[1].tobytes() == B.plan_batch(dt, *dbat[199 % 16]).host()[1].tobytes()
+        ok_ov = outs[199 % 16].host()[1].tobytes() == B.plan_batch(dt, *dbat[199 % 16]).host()[1].tobytes()
+        # C4-like: 2 x 10^5 scenarios in one launch (many tiles per CTA)
+        if not hasattr(run, "_c4"):
+            run._c4 = [N.to_device(a) for a in c2_inputs(fx, 200_000, 1)]
+        r4 = B.plan_batch(dt, *run._c4)
+        t4 = []
+        for i in range(6):
+            a4, b4 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a4.record(s)
+            B.plan_batch(dt, *run._c4, out=r4)
+            b4.record(s)
+            torch.cuda.synchronize()
+            t4.append(a4.elapsed_time(b4) * 1e3 / 20)
+        p4 = r4.host()[1]
+        if not hasattr(run, "_c4ref"):
+            run._c4ref = p4.tobytes()
+        ok4 = p4.tobytes() == run._c4ref
         mb = B.MappedHostBatch(off, tab, rate, bound, cfg_format=2, plan_bytes=64, depth=4)
         for k in range(2):
             if k:
@@ -147,7 +169,7 @@ def run():
         e2e = (time.perf_counter() - t0) / 300 * 1e6
         ok = got.tobytes() == ref.tobytes() and mb.outputs(0)[1].tobytes() == ref.tobytes() and ok_ov
         print(f"{name:24s}: device K2 p50 {np.median(ts):6.1f} us  min {min(ts):6.1f}  overlapped {ov:6.1f} us/step"
-              f"  e2e(depth 4) {e2e:6.1f} us  ok {ok}")
+              f"  c4 {np.median(t4):6.1f} us/10^4  e2e(depth 4) {e2e:6.1f} us  ok {ok} {ok4}")
 
 
 if __name__ == "__main__":
