@@ -477,19 +477,73 @@ __device__ __forceinline__ int th_emit(const PlanArgs& A, ThWarp& P, const ThLed
   return A.plan_bytes == 64 && need > 64 - 8;
 }
 
-// configure one service through the global index (segment starts as i64)
-// and store its config record at index i
-__device__ __forceinline__ void th_configure(const PlanArgs& A, const double* tp, int tp_stride, int t, double rate,
-                                             double bound, int64_t i, parva_config_record& r, double tpc[5]) {
-  if (t < 0 || t >= A.n_tables) {
+// configure K services at once through the global index (segment starts
+// as i64): the 5 K binary searches advance in lockstep, so a lane keeps 5 K
+// independent loads in flight per step (configurator.py:93-124 via the
+// prefix-argmax index, then select_optimal_segment + match_demand); stores
+// each config record at its index.  valid[j] = false: service j is absent.
+template <int K>
+__device__ __forceinline__ void th_configure_k(const PlanArgs& A, const double* tp, int tp_stride, const int t[K],
+                                               const double rate[K], const double bound[K], const int64_t i[K],
+                                               const bool valid[K], parva_config_record r[K]) {
+  int s0[K * 5], n[K * 5], lo[K * 5];
+  int nmax = 0;
 #pragma unroll
-    for (int c = 0; c < 5; c++) { r.best[c] = -1; tpc[c] = 0.0; }
-    r.opt_sc = -1; r.last_sc = -1; r.status = PARVA_BAD_INPUT;
-  } else {
-    configure_indexed(A.idx_lat, A.idx_best, tp, tp_stride, A.seg_start, A.seg_count, t, bound, rate, r, tpc,
-                      A.cfg_format == PARVA_CFG_FULL);
+  for (int j = 0; j < K; j++) {
+    const bool ok = valid[j] && t[j] >= 0 && t[j] < A.n_tables;
+#pragma unroll
+    for (int c = 0; c < 5; c++) {
+      s0[j * 5 + c] = ok ? (int)A.seg_start[t[j] * 5 + c] : 0;
+      n[j * 5 + c] = ok ? A.seg_count[t[j] * 5 + c] : 0;
+      lo[j * 5 + c] = 0;
+      nmax = max(nmax, n[j * 5 + c]);
+    }
   }
-  store_config(A, i, r);
+  for (int step = nmax ? 1 << (31 - __clz(nmax)) : 0; step > 0; step >>= 1) {
+#pragma unroll
+    for (int q = 0; q < K * 5; q++) {
+      const int probe = lo[q] + step;
+      if (probe <= n[q] && A.idx_lat[s0[q] + probe - 1] < bound[q / 5]) lo[q] = probe;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    if (!valid[j]) continue;
+    double tpc[5];
+    r[j] = parva_config_record{};
+    if (t[j] < 0 || t[j] >= A.n_tables) {
+#pragma unroll
+      for (int c = 0; c < 5; c++) r[j].best[c] = -1;
+      r[j].opt_sc = -1; r[j].last_sc = -1; r[j].status = PARVA_BAD_INPUT;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 5; c++) {
+        const int q = j * 5 + c;
+        const int b = lo[q] ? (int)A.idx_best[s0[q] + lo[q] - 1] : -1;
+        r[j].best[c] = (int16_t)b;
+        tpc[c] = b >= 0 ? tp[(s0[q] + b) * tp_stride] : 0.0;
+      }
+      match_demand(tpc, rate[j], r[j], A.cfg_format == PARVA_CFG_FULL);
+      if (r[j].status == PARVA_INFEASIBLE_SLO) r[j].opt_sc = -1;
+    }
+    store_config(A, i[j], r[j]);
+  }
+}
+
+__device__ __forceinline__ int th_table(const PlanArgs& A, int64_t i) {
+  return A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
+}
+
+// the planner's view of a configured service (chunk-local index li)
+__device__ __forceinline__ void th_stage(ThWarp& P, int li, int t, const parva_config_record& r) {
+  if (li >= kThSvc) return;
+  const long long cn = r.count < 0 ? 0 : r.count > 255 ? 255 : r.count;
+  P.u.svc.meta[li] = (uint32_t)cn | (uint32_t)(r.opt_sc < 0 ? 15 : r.opt_sc) << 8 |
+                     (uint32_t)(r.last_sc < 0 ? 15 : r.last_sc) << 12 | (uint32_t)(r.status & 0xFF) << 16;
+  uint16_t* b = P.u.svc.best[li];
+#pragma unroll
+  for (int c = 0; c < 5; c++) b[c] = (uint16_t)r.best[c];
+  b[5] = (uint16_t)t;
 }
 
 // K2, thread-per-scenario form.  kMirror: the fused all-gather (each chunk's
@@ -551,22 +605,18 @@ __global__ void __launch_bounds__(TH_THREADS, PARVA_TH_MINB) plan_thread_kernel(
         for (int64_t o = (int64_t)lane * 128; o < nb[r] + 128; o += 32 * 128)
           asm volatile("prefetch.global.L1 [%0];" ::"l"(rg[r] + o));
     }
-    // ---- configure the chunk's services (lane-strided, coalesced)
-    for (int i = a_base + lane; i < a_end; i += 32) {
-      const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
-      parva_config_record r = {};
-      double tpc[5];
-      th_configure(A, tp, tp_stride, t, A.svc_rate[i], A.svc_bound[i], i, r, tpc);
-      const int li = i - a_base;
-      if (li < kThSvc) {
-        const long long cn = r.count < 0 ? 0 : r.count > 255 ? 255 : r.count;
-        P.u.svc.meta[li] = (uint32_t)cn | (uint32_t)(r.opt_sc < 0 ? 15 : r.opt_sc) << 8 |
-                           (uint32_t)(r.last_sc < 0 ? 15 : r.last_sc) << 12 | (uint32_t)(r.status & 0xFF) << 16;
-        uint16_t* b = P.u.svc.best[li];
-#pragma unroll
-        for (int c = 0; c < 5; c++) b[c] = (uint16_t)r.best[c];
-        b[5] = (uint16_t)t;
-      }
+    // ---- configure the chunk's services (lane-strided, coalesced; two
+    // services per lane at a time)
+    for (int i = a_base + lane; i < a_end; i += 64) {
+      const int64_t ii[2] = {i, i + 32};
+      const bool v[2] = {true, i + 32 < a_end};
+      const int tt[2] = {th_table(A, i), v[1] ? th_table(A, i + 32) : 0};
+      const double rr[2] = {A.svc_rate[i], v[1] ? A.svc_rate[i + 32] : 0.0};
+      const double bb[2] = {A.svc_bound[i], v[1] ? A.svc_bound[i + 32] : 0.0};
+      parva_config_record r[2];
+      th_configure_k<2>(A, tp, tp_stride, tt, rr, bb, ii, v, r);
+      th_stage(P, i - a_base, tt[0], r[0]);
+      if (v[1]) th_stage(P, i + 32 - a_base, tt[1], r[1]);
     }
     __syncwarp();
     // ---- plan: thread j takes scenario k0 + j
@@ -621,14 +671,21 @@ __global__ void __launch_bounds__(TH_THREADS, PARVA_TH_MINB) plan_thread_kernel(
       const int j = __ffs(m) - 1, k = k0 + j;
       const int a = A.scen_off[k], n = A.scen_off[k + 1] - a;
       if (n > 0 && n <= PARVA_PLAN_MAX_SERVICES && lane < n) {
-        const int i = a + lane;
-        const int t = A.svc_table16 ? (int)A.svc_table16[i] : A.svc_table[i];
-        parva_config_record r = {};
+        const int64_t ii[1] = {a + lane};
+        const bool v[1] = {true};
+        const int tt[1] = {th_table(A, a + lane)};
+        const double rr[1] = {A.svc_rate[a + lane]}, bb[1] = {A.svc_bound[a + lane]};
+        parva_config_record r[1];
+        th_configure_k<1>(A, tp, tp_stride, tt, rr, bb, ii, v, r);
         double tpc[5];
-        th_configure(A, tp, tp_stride, t, A.svc_rate[i], A.svc_bound[i], i, r, tpc);
+#pragma unroll
+        for (int c = 0; c < 5; c++) {
+          const int b = r[0].best[c];
+          tpc[c] = (b >= 0 && r[0].status != PARVA_BAD_INPUT) ? tp[(A.seg_start[tt[0] * 5 + c] + b) * tp_stride] : 0.0;
+        }
 #pragma unroll
         for (int c = 0; c < 5; c++) P.u.w.s.tp[lane * 5 + c] = tpc[c];
-        P.u.w.s.meta[lane] = pack_meta(r.opt_sc, r.last_sc, r.status, r.count);
+        P.u.w.s.meta[lane] = pack_meta(r[0].opt_sc, r[0].last_sc, r[0].status, r[0].count);
       }
       __syncwarp();
       plan_scenario_warp<32>(A, P.u.w.g, k, n, P.u.w.s.tp, P.u.w.s.meta, n >= 0, lane, Grp<32>{0xffffffffu, 0});

@@ -11,7 +11,7 @@ timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2>gpurun_out/${TAG}_bench_ref.err; echo "ref exit $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 5 --warmup 3 --no-cpu --no-extra --no-gate > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1; echo "ncu launches exit $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'plan_batch_kernel' \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'plan_thread_kernel' \
   -c 1 -f -o gpurun_out/${TAG}_full_k2 python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-gate --no-sweep > gpurun_out/${TAG}_ncu_full_k2.log 2>&1; echo "ncu k2 exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'plan_warp_kernel' \
   -c 1 -f -o gpurun_out/${TAG}_full_k2s python bench.py --steps 3 --warmup 3 --no-cpu --no-extra --no-gate --no-sweep > gpurun_out/${TAG}_ncu_full_k2s.log 2>&1; echo "ncu k2s exit $?"
