@@ -205,13 +205,14 @@ class GeneralOutput:
 def plan_general(g: GeneralInput, stream=None) -> GeneralOutput:
     torch = N.require_cuda()
     n_names = max(len(g.names), 1)
-    total_new = sum(int(c) for c in g.svc_count) + sum(1 for x in g.svc_last if x >= 0) if g.relocate else 0
+    total_new = (int(np.asarray(g.svc_count, dtype=np.int64).sum()) +
+                 int((np.asarray(g.svc_last, dtype=np.int64) >= 0).sum())) if g.relocate else 0
     gpu_cap = len(g.gpu_id) + total_new + 1
     place_cap = gpu_cap * 7
     diag_cap = gpu_cap + 1
 
     def d(a, dt, n=1):
-        arr = np.asarray(a if len(a) else [0] * n, dtype=dt)
+        arr = np.asarray(a, dtype=dt) if len(a) else np.zeros(n, dtype=dt)
         return N.to_device(arr)
 
     cat_size = d(g.cat_size, np.uint8); cat_tp = d(g.cat_tp, np.float64); cat_name = d(g.cat_name, np.int32)
@@ -258,23 +259,29 @@ def plan_general(g: GeneralInput, stream=None) -> GeneralOutput:
 
 
 def general_from_configs(pt: PackedTables, svc_table, cfg, optimize: bool, threshold: int) -> GeneralInput:
-    """General problem for one scenario from its config records (CAPACITY path)."""
+    """General problem for one scenario from its config records (CAPACITY path).
+
+    Vectorized: the catalogue is every (service, size class) with a best
+    point, in service-major order (the order the reference enqueues them)."""
     n = len(svc_table)
-    g = GeneralInput(names=list(range(n)), n_services=n, relocate=True, optimize=optimize, threshold=threshold)
-    memo: dict = {}
-    for s in range(n):
-        t = int(svc_table[s]); r = cfg[s]
-        cats = [-1] * 5
-        for c in range(5):
-            if r["best"][c] >= 0:
-                cats[c] = g.add_cat((1, 2, 3, 4, 7)[c], float(pt.tp[pt.point(t, c, int(r["best"][c]))]), s, memo,
-                                    (s, c))
-        g.svc_t1.append(cats[0]); g.svc_t2.append(cats[1])
-        g.svc_opt.append(cats[int(r["opt_sc"])] if r["opt_sc"] >= 0 else -1)
-        g.svc_count.append(int(r["count"]))
-        g.svc_last.append(cats[int(r["last_sc"])] if r["last_sc"] >= 0 else -1)
-        g.svc_rate.append(0.0)
-    return g
+    t = np.asarray(svc_table, dtype=np.int64)
+    best = np.asarray(cfg["best"], dtype=np.int64).reshape(n, 5)
+    valid = best >= 0
+    cat = np.where(valid, np.cumsum(valid.ravel()).reshape(n, 5) - 1, -1)
+    s_idx, c_idx = np.nonzero(valid)
+    pts = pt.seg_start.astype(np.int64)[t[s_idx] * 5 + c_idx] + best[s_idx, c_idx]
+    sizes = np.array((1, 2, 3, 4, 7), dtype=np.uint8)
+    rows = np.arange(n)
+    opt = np.asarray(cfg["opt_sc"], dtype=np.int64)
+    last = np.asarray(cfg["last_sc"], dtype=np.int64)
+    return GeneralInput(
+        names=list(range(n)), n_services=n, relocate=True, optimize=optimize, threshold=threshold,
+        cat_size=sizes[c_idx], cat_tp=np.asarray(pt.tp, dtype=np.float64)[pts], cat_name=s_idx.astype(np.int32),
+        svc_t1=cat[:, 0].astype(np.int32), svc_t2=cat[:, 1].astype(np.int32),
+        svc_opt=np.where(opt >= 0, cat[rows, np.maximum(opt, 0)], -1).astype(np.int32),
+        svc_count=np.asarray(cfg["count"], dtype=np.int64),
+        svc_last=np.where(last >= 0, cat[rows, np.maximum(last, 0)], -1).astype(np.int32),
+        svc_rate=np.zeros(n), cat_key=list(zip(s_idx.tolist(), c_idx.tolist())))
 
 
 def resolve_capacity(pt: PackedTables, scen_off, svc_table, cfg, plan, optimize=True, threshold=4) -> dict:

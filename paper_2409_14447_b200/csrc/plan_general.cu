@@ -13,6 +13,9 @@
 // whole-dict snapshot (allocator.py:387,418-419): same observable ledger,
 // O(touched) instead of O(services) per GPU.
 #include <cuda_runtime.h>
+#ifdef PARVA_KG_PROF
+#include <cstdio>
+#endif
 
 #include "parva_common.cuh"
 #include "parva_kernels.cuh"
@@ -409,6 +412,12 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
     int32_t next = (int32_t)w.hdr[3];
     int64_t nd = 0;
     int64_t idx = G0 - 1;
+#ifdef PARVA_KG_PROF   // phase cycle counters of the serial chain (probe builds only)
+    long long kp[6] = {0, 0, 0, 0, 0, 0}, kn_drain = 0, kn_place = 0, kt = clock64();
+#define KG_MARK(i) do { const long long c_ = clock64(); kp[i] += c_ - kt; kt = c_; } while (0)
+#else
+#define KG_MARK(i) do { } while (0)
+#endif
     while (true) {
       // next drain candidate at or below idx
       int64_t index = -1;
@@ -420,6 +429,7 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
         idx -= 32;
       }
       if (index < 0) break;
+      KG_MARK(0);
       idx = index - 1;
       const int nl = S.Ln[index];
       // the drained list and what it needs, one entry per lane
@@ -435,6 +445,7 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
           (void)lv;
         }
       }
+      KG_MARK(1);
       int32_t lg_name = -1, lg_ord = 0;   // lane k logs the k-th ledger change
       double lg_val = 0.0;
       double st_v = 0.0;                  // lane 0 staging of the log entry
@@ -475,6 +486,7 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
         }
         if (lane == k) { my_k2 = k2; my_k1 = k1; }
       }
+      KG_MARK(2);
       int64_t nu = 0;
       int32_t my_undo = 0;   // undo entry nu lives in lane nu (first 32), then in w.undo
       if (fail < 0) {
@@ -490,7 +502,9 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
               const long long cnt = __shfl_sync(0xffffffffu, c ? my_k2 : my_k1, k);
               const int cat = __shfl_sync(0xffffffffu, c ? e_t2 : e_t1, k);
               for (long long r = 0; r < cnt; r++) {
+                KG_MARK(3);
                 const int64_t g = S.first_fit(c, index, lane);
+                KG_MARK(5);
                 if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
                 const uint32_t m8 = S.M[g];
                 const int st = find_start(m8 & 0x7Fu, c);
@@ -526,6 +540,10 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
           }
         }
       }
+      KG_MARK(3);
+#ifdef PARVA_KG_PROF
+      kn_drain++; kn_place += nu;
+#endif
       if (fail >= 0) {
         if (rot != nl) {   // allocator.py:415-417: the removed ones are re-appended
           int src = lane + rot;
@@ -554,7 +572,14 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
         S.set_bits(index, lane);
       }
       __syncwarp();
+      KG_MARK(4);
     }
+#ifdef PARVA_KG_PROF
+    if (lane == 0)
+      printf("KGPROF drains %lld placements %lld cycles: search %lld lists %lld ledger+propose %lld place %lld "
+             "finish %lld (first_fit %lld)\n", kn_drain, kn_place, kp[0], kp[1], kp[2], kp[3], kp[4], kp[5]);
+#endif
+#undef KG_MARK
     if (lane == 0) s_nd = nd;
   }
   __syncthreads();
