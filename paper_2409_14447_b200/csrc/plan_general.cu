@@ -291,66 +291,254 @@ __device__ inline double unalloc_g(int64_t total, int64_t n) {
   return __dsub_rn(1.0, __ddiv_rn((double)total, (double)(7 * n)));
 }
 
-// Optimize (allocator.py:362-443) as a warp-cooperative serial chain.  GPU
-// state (8-bit mask + list length) and the per-size accepts bitmaps sit in
-// shared memory when they fit (up to ~85k GPUs), else in global memory.  Warp
-// 0 walks the chain: the next drain candidate (0 < num_gpcs <= threshold) is
-// found 32 GPUs per ballot, first-fit is a ballot over the summary bitmap
-// then one word, proposals stay in lane registers as (kind, count) runs,
-// undo entries carry (gpu, class, slot) so a rollback reads no lists, and the
-// freed_rate ledger rolls back from a per-lane log.
+// Optimize (allocator.py:362-443) as a serial chain walked by warp 0 in
+// lock step: every lane executes the same scalar chain on the same values
+// (shared-memory reads are broadcasts, same-address stores coalesce), so the
+// chain needs no shuffles, no per-step warp barriers and no divergence;
+// the warp's lanes only split the loads of a drained list and the proposal
+// search (propose_small_warp).  GPU state (8-bit mask + list length) and the
+// accepts bitmaps of size classes 1 and 2 -- the only sizes a proposal has
+// -- sit in shared memory when they fit (~110k GPUs), else in global memory.
+// The next drain candidate (0 < num_gpcs <= threshold) is found 8 GPUs per
+// load; first-fit starts at a per-class hint (summary words below it are
+// zero) and reads the summary bitmap, then one word (cursor-free first fit,
+// SURVEY App. B #2); undo entries carry (gpu, class, slot) so a rollback
+// reads no lists; the freed_rate ledger rolls back from a log.
 constexpr int OPT_THREADS = 512;
+constexpr int kChainUndo = 256;   // undo entries kept in shared memory (the rest in w.undo)
 
 struct OptState {
   uint8_t* M;        // mask | flag, per GPU
   uint8_t* Ln;       // list length, per GPU
-  uint64_t* A;       // accepts bitmaps [5][words]
-  uint64_t* Sm;      // summary bitmaps [5][swords]: bit = word of A nonzero
+  uint64_t* A;       // accepts bitmaps [2][words] (size classes 0, 1)
+  uint64_t* Sm;      // summary bitmaps [2][swords]: bit = word of A nonzero
   int64_t words, swords, G;
+  int64_t hint[2];   // summary words below hint[c] are zero
 
-  __device__ void set_bits(int64_t g, int lane) {
-    const uint32_t m = M[g] & 0x7Fu;
-    const int64_t k = g >> 6;
-    const uint64_t bit = 1ull << (g & 63);
-    if (lane < 5) {
-      const int c = lane;
-      const bool acc = find_start(m, c) >= 0;
-      uint64_t* a = &A[c * words + k];
-      const uint64_t nv = acc ? (*a | bit) : (*a & ~bit);
-      *a = nv;
-      uint64_t* sw = &Sm[c * swords + (k >> 6)];
-      const uint64_t sb = 1ull << (k & 63);
-      *sw = nv ? (*sw | sb) : (*sw & ~sb);
-    }
-    __syncwarp();
+  // GPU g's byte is now m: its accepts bits and the summaries
+  __device__ __forceinline__ void set_bits(int64_t g, uint32_t m) {
+    m &= 0x7Fu;
+    const int64_t k = g >> 6, sw = k >> 6;
+    const uint64_t bit = 1ull << (g & 63), sb = 1ull << (k & 63);
+    const bool acc0 = m != 0x7Fu;                                                     // find_start(m, 0) >= 0
+    const bool acc1 = (m & 0x03u) == 0 || (m & 0x0Cu) == 0 || (m & 0x30u) == 0;        // find_start(m, 1) >= 0
+    const uint64_t a0 = A[k], a1 = A[words + k], s0 = Sm[sw], s1 = Sm[swords + sw];
+    const uint64_t n0 = acc0 ? (a0 | bit) : (a0 & ~bit), n1 = acc1 ? (a1 | bit) : (a1 & ~bit);
+    A[k] = n0;
+    A[words + k] = n1;
+    Sm[sw] = n0 ? (s0 | sb) : (s0 & ~sb);
+    Sm[swords + sw] = n1 ? (s1 | sb) : (s1 & ~sb);
+    if (n0 && sw < hint[0]) hint[0] = sw;
+    if (n1 && sw < hint[1]) hint[1] = sw;
   }
 
-  // first GPU in list order accepting class c, skipping `excl` (warp-wide):
-  // ballot over summary words, then the first nonzero bitmap word
-  __device__ int64_t first_fit(int c, int64_t excl, int lane) {
-    const uint64_t* a = &A[c * words];
-    const uint64_t* sm = &Sm[c * swords];
-    const int64_t ew = excl >= 0 ? excl >> 6 : -1;
-    const uint64_t ebit = excl >= 0 ? 1ull << (excl & 63) : 0ull;
-    for (int64_t base = 0; base < swords; base += 32) {
-      const uint64_t v = base + lane < swords ? sm[base + lane] : 0ull;
-      unsigned b = __ballot_sync(0xffffffffu, v != 0ull);
-      while (b) {
-        const int src = __ffs(b) - 1;
-        b &= b - 1;
-        uint64_t vs = __shfl_sync(0xffffffffu, v, src);
-        while (vs) {
-          const int64_t wi = (base + src) * 64 + __ffsll((long long)vs) - 1;
-          vs &= vs - 1;
-          uint64_t word = a[wi];
-          if (wi == ew) word &= ~ebit;
-          if (word) return wi * 64 + __ffsll((long long)word) - 1;
-        }
+  // first GPU in list order accepting class c (0 or 1), skipping `excl`
+  __device__ __forceinline__ int64_t first_fit(int c, int64_t excl) {
+    const uint64_t* a = A + c * words;
+    const uint64_t* sm = Sm + c * swords;
+    const int64_t ew = excl >> 6;
+    const uint64_t ebit = 1ull << (excl & 63);
+    for (int64_t sw = hint[c]; sw < swords; sw++) {
+      uint64_t v = sm[sw];
+      if (!v) {
+        if (sw == hint[c]) hint[c] = sw + 1;
+        continue;
+      }
+      while (v) {
+        const int64_t wi = sw * 64 + __ffsll((long long)v) - 1;
+        v &= v - 1;
+        uint64_t word = a[wi];
+        if (wi == ew) word &= ~ebit;
+        if (word) return wi * 64 + __ffsll((long long)word) - 1;
+      }
+    }
+    return -1;
+  }
+
+  // highest GPU <= idx with 0 < num_gpcs <= thr, 8 GPUs per load
+  __device__ __forceinline__ int64_t prev_candidate(int64_t idx, int thr) const {
+    for (int64_t w8 = idx >> 3; w8 >= 0; w8--) {
+      const uint64_t x = reinterpret_cast<const uint64_t*>(M)[w8];
+      if (!x) continue;
+#pragma unroll
+      for (int b = 7; b >= 0; b--) {
+        const uint32_t m = (uint32_t)(x >> (8 * b)) & 0xFFu;
+        const int ng = __popc(m & 0x7Fu) - (int)(m >> 7);
+        if (w8 * 8 + b <= idx && ng > 0 && ng <= thr) return w8 * 8 + b;
       }
     }
     return -1;
   }
 };
+
+// the drained list and the chain's logs (shared memory, warp 0)
+struct ChainSmem {
+  CatExt ext[8];
+  int32_t cat[8];
+  uint8_t slot[8];
+  long long k2[8], k1[8];
+  int32_t lg_name[8], lg_ord[8];
+  double lg_val[8];
+  double lv[8];      // staged ledger entries of the drained services (lane k: entry k)
+  int32_t lo[8];
+  int32_t undo[kChainUndo];
+};
+
+// kSmem: GPU state and bitmaps in shared memory (dsm / sm_summary), so the
+// compiler emits shared-memory accesses instead of generic ones
+template <bool kSmem>
+__device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, const parva_general_result& R,
+                                             const GenWs& w, int64_t G0, int lane, ChainSmem& C, uint8_t* dsm,
+                                             uint64_t* sm_summary) {
+  OptState S;
+  const int64_t gpad = (G0 + 15) & ~int64_t(15);
+  S.words = (G0 + 63) / 64;
+  S.swords = (S.words + 63) / 64;
+  S.G = G0;
+  S.M = kSmem ? dsm : w.mask;
+  S.Ln = kSmem ? dsm + gpad : w.len;
+  S.A = kSmem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
+  S.Sm = kSmem ? sm_summary : w.summary;
+  S.hint[0] = S.hint[1] = 0;
+  int32_t next = (int32_t)w.hdr[3];
+  int64_t nd = 0;
+  int64_t idx = G0 - 1;
+#ifdef PARVA_KG_PROF   // phase cycle counters of the serial chain (probe builds only)
+  long long kp[6] = {0, 0, 0, 0, 0, 0}, kn_drain = 0, kn_place = 0, kt = clock64();
+#define KG_MARK(i) do { const long long c_ = clock64(); kp[i] += c_ - kt; kt = c_; } while (0)
+#else
+#define KG_MARK(i) do { } while (0)
+#endif
+  while (true) {
+    const int64_t index = S.prev_candidate(idx, P.threshold);
+    if (index < 0) break;
+    KG_MARK(0);
+    idx = index - 1;
+    const int nl = S.Ln[index];
+    if (lane < nl) {            // lane k stages entry k of the drained list
+      const int cat = w.lcat[index * 7 + lane];
+      C.cat[lane] = cat;
+      C.slot[lane] = w.lslot[index * 7 + lane];
+      const CatExt X = w.ext[cat];
+      C.ext[lane] = X;
+      if (X.name < P.n_services) {   // the ledger entries, loaded in parallel
+        C.lv[lane] = R.d_ledger_val[X.name];
+        C.lo[lane] = R.d_ledger_order[X.name];
+      }
+    }
+    __syncwarp();
+    KG_MARK(1);
+    const int32_t sv_next = next;
+    int fail = -1, rot = nl, nlog = 0;
+    int64_t fname = -1;
+    for (int k = 0; k < nl; k++) {   // allocator.py:392-405, in order
+      const CatExt X = C.ext[k];
+      if (X.name >= P.n_services) { fail = PARVA_DIAG_UNKNOWN_SERVICE; fname = X.name; rot = k; break; }
+      const int s = X.name;
+      const double ov = C.lv[k];
+      const int32_t oo = C.lo[k];
+      const double f = oo == 0 ? __dadd_rn(0.0, X.tp) : __dadd_rn(ov, X.tp);
+      const int32_t no = oo == 0 ? ++next : oo;
+      if (oo == 0) R.d_ledger_order[s] = no;
+      R.d_ledger_val[s] = f;
+      C.lg_name[k] = s; C.lg_val[k] = ov; C.lg_ord[k] = oo;
+      nlog = k + 1;
+      long long k2, k1;
+      if (!propose_small_warp(X.tp1, X.tp2, f, k2, k1, lane)) {
+        fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break;
+      }
+      double v = f;
+      for (long long j = 0; j < k2; j++) v = __dsub_rn(v, X.tp2);
+      for (long long j = 0; j < k1; j++) v = __dsub_rn(v, X.tp1);
+      R.d_ledger_val[s] = v;
+      C.k2[k] = k2; C.k1[k] = k1;
+      for (int j = k + 1; j < nl; j++)   // a later entry of the same service sees this update
+        if (C.ext[j].name == s) { C.lv[j] = v; C.lo[j] = no; }
+    }
+    KG_MARK(2);
+    int64_t nu = 0;
+    if (fail < 0) {
+      long long tot = 0;
+      for (int k = 0; k < nl; k++) tot += C.k2[k] + C.k1[k];
+      if (tot > w.qcap) fail = PARVA_DIAG_NEED_NEW_GPU;   // more GPCs than any map can free
+      else {
+        // proposals queue (allocator.py:403-405, drained by size): every size-2
+        // kind in drain order, then every size-1 kind; first fit without new GPUs
+        for (int c = 1; c >= 0 && fail < 0; c--) {
+          for (int k = 0; k < nl && fail < 0; k++) {
+            const long long cnt = c ? C.k2[k] : C.k1[k];
+            const int cat = c ? C.ext[k].c2 : C.ext[k].c1;
+            for (long long r = 0; r < cnt; r++) {
+              KG_MARK(3);
+              const int64_t g = S.first_fit(c, index);
+              KG_MARK(5);
+              if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
+              const uint32_t m8 = S.M[g];
+              const int st = find_start(m8 & 0x7Fu, c);
+              const int ln = S.Ln[g];
+              const uint32_t nm = m8 | footprint(c, st);
+              S.M[g] = (uint8_t)nm;
+              S.Ln[g] = (uint8_t)(ln + 1);
+              w.lcat[g * 7 + ln] = cat;
+              w.lslot[g * 7 + ln] = (uint8_t)st;
+              const int32_t u = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
+              if (nu < kChainUndo) C.undo[nu] = u; else w.undo[nu] = u;
+              nu++;
+              S.set_bits(g, nm);
+            }
+          }
+        }
+        if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
+          for (int64_t j = nu - 1; j >= 0; j--) {
+            const int32_t u = j < kChainUndo ? C.undo[j] : w.undo[j];
+            const int64_t g = u >> 4;
+            const int c = (u >> 3) & 1, st = u & 7;
+            const uint32_t nm = S.M[g] & ~footprint(c, st);
+            S.M[g] = (uint8_t)nm;
+            S.Ln[g] = (uint8_t)(S.Ln[g] - 1);
+            S.set_bits(g, nm);
+          }
+        }
+      }
+    }
+    KG_MARK(3);
+#ifdef PARVA_KG_PROF
+    kn_drain++; kn_place += nu;
+#endif
+    if (fail >= 0) {
+      if (rot != nl && lane < nl) {   // allocator.py:415-417: the removed ones are re-appended
+        int src = lane + rot;
+        if (src >= nl) src -= nl;
+        w.lcat[index * 7 + lane] = C.cat[src];
+        w.lslot[index * 7 + lane] = C.slot[src];
+      }
+      for (int k = nlog - 1; k >= 0; k--) {   // ledger rollback in reverse log order
+        R.d_ledger_val[C.lg_name[k]] = C.lg_val[k];
+        R.d_ledger_order[C.lg_name[k]] = C.lg_ord[k];
+      }
+      next = sv_next;
+      if (nd < R.diag_cap) {
+        R.d_diag[3 * nd] = fail;
+        R.d_diag[3 * nd + 1] = w.id[index];
+        R.d_diag[3 * nd + 2] = fname;
+      }
+      nd++;
+    } else {
+      S.M[index] = 0;
+      S.Ln[index] = 0;
+      S.set_bits(index, 0u);
+    }
+    __syncwarp();                 // C is restaged by the next drain
+    KG_MARK(4);
+  }
+#ifdef PARVA_KG_PROF
+  if (lane == 0)
+    printf("KGPROF drains %lld placements %lld cycles: search %lld lists %lld ledger+propose %lld place %lld "
+           "finish %lld (first_fit %lld)\n", kn_drain, kn_place, kp[0], kp[1], kp[2], kp[3], kp[4], kp[5]);
+#endif
+#undef KG_MARK
+  return nd;
+}
 
 __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general_problem P, parva_general_result R,
                                                                    uint8_t* ws_base, int64_t cap, int64_t qcap,
@@ -359,10 +547,14 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   __shared__ int64_t sh[33];
   __shared__ int s_fallback, s_status;
   __shared__ int64_t s_nd;
-  __shared__ uint64_t sm_summary[5 * 64];
+  __shared__ uint64_t sm_summary[2 * 64];
+  __shared__ ChainSmem chain;
   GenWs w;
   gen_layout(cap, qcap, P.n_services, P.n_cat, ws_base, &w);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef PARVA_KG_PROF
+  const long long kt0 = clock64();
+#endif
   const int64_t G0 = w.hdr[0];
   int status = (int)w.hdr[2];
   const bool in_smem = G0 <= smem_gpus;
@@ -377,21 +569,22 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   S.words = words;
   S.swords = swords;
   S.G = G0;
+  S.hint[0] = S.hint[1] = 0;
   if (in_smem)
     for (int64_t g = tid; g < G0; g += blockDim.x) { S.M[g] = w.mask[g]; S.Ln[g] = w.len[g]; }
   __syncthreads();
   for (int64_t k = tid; k < words; k += blockDim.x) {
-    uint64_t b[5] = {0, 0, 0, 0, 0};
+    uint64_t b[2] = {0, 0};
     for (int j = 0; j < 64 && k * 64 + j < G0; j++) {
       const uint32_t m = S.M[k * 64 + j] & 0x7Fu;
 #pragma unroll
-      for (int c = 0; c < 5; c++) if (find_start(m, c) >= 0) b[c] |= 1ull << j;
+      for (int c = 0; c < 2; c++) if (find_start(m, c) >= 0) b[c] |= 1ull << j;
     }
 #pragma unroll
-    for (int c = 0; c < 5; c++) S.A[c * words + k] = b[c];
+    for (int c = 0; c < 2; c++) S.A[c * words + k] = b[c];
   }
   __syncthreads();
-  for (int64_t k = tid; k < 5 * swords; k += blockDim.x) {
+  for (int64_t k = tid; k < 2 * swords; k += blockDim.x) {
     const int c = (int)(k / swords);
     const int64_t sw = k % swords;
     uint64_t v = 0;
@@ -408,183 +601,20 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   if (tid == 0) { s_fallback = 0; s_status = status; s_nd = 0; }
   __syncthreads();
 
+#ifdef PARVA_KG_PROF
+  const long long kt1 = clock64();
+#endif
   if (run && warp == 0) {
-    int32_t next = (int32_t)w.hdr[3];
-    int64_t nd = 0;
-    int64_t idx = G0 - 1;
-#ifdef PARVA_KG_PROF   // phase cycle counters of the serial chain (probe builds only)
-    long long kp[6] = {0, 0, 0, 0, 0, 0}, kn_drain = 0, kn_place = 0, kt = clock64();
-#define KG_MARK(i) do { const long long c_ = clock64(); kp[i] += c_ - kt; kt = c_; } while (0)
-#else
-#define KG_MARK(i) do { } while (0)
-#endif
-    while (true) {
-      // next drain candidate at or below idx
-      int64_t index = -1;
-      while (idx >= 0) {
-        const int64_t g = idx - lane;
-        const int ng = g >= 0 ? gpcs8(S.M[g]) : 0;
-        const unsigned b = __ballot_sync(0xffffffffu, ng > 0 && ng <= P.threshold);
-        if (b) { index = idx - (__ffs(b) - 1); break; }
-        idx -= 32;
-      }
-      if (index < 0) break;
-      KG_MARK(0);
-      idx = index - 1;
-      const int nl = S.Ln[index];
-      // the drained list and what it needs, one entry per lane
-      int e_cat = 0, e_slot = 0, e_name = 0, e_t1 = -1, e_t2 = -1;
-      double e_tp = 0.0, tp1s = 0.0, tp2s = 0.0;
-      if (lane < nl) {
-        e_cat = w.lcat[index * 7 + lane];
-        e_slot = w.lslot[index * 7 + lane];
-        const CatExt X = w.ext[e_cat];
-        e_name = X.name; e_tp = X.tp; e_t1 = X.c1; e_t2 = X.c2; tp1s = X.tp1; tp2s = X.tp2;
-        if (e_name < P.n_services) {   // warm L1 with this service's ledger entry
-          volatile double lv = R.d_ledger_val[e_name];
-          (void)lv;
-        }
-      }
-      KG_MARK(1);
-      int32_t lg_name = -1, lg_ord = 0;   // lane k logs the k-th ledger change
-      double lg_val = 0.0;
-      double st_v = 0.0;                  // lane 0 staging of the log entry
-      int32_t st_o = 0;
-      const int32_t sv_next = next;
-      long long my_k2 = 0, my_k1 = 0;   // lane k: proposals of the k-th drained placement
-      int fail = -1, rot = nl;
-      int64_t fname = -1;
-      for (int k = 0; k < nl; k++) {
-        const int name = __shfl_sync(0xffffffffu, e_name, k);
-        if (name >= P.n_services) { fail = PARVA_DIAG_UNKNOWN_SERVICE; fname = name; rot = k; break; }
-        const int s = name;
-        const double tpp = __shfl_sync(0xffffffffu, e_tp, k);
-        const int c1 = __shfl_sync(0xffffffffu, e_t1, k), c2 = __shfl_sync(0xffffffffu, e_t2, k);
-        const double t1 = __shfl_sync(0xffffffffu, tp1s, k), t2 = __shfl_sync(0xffffffffu, tp2s, k);
-        double f = 0.0;
-        if (lane == 0) {
-          const double ov = R.d_ledger_val[s];
-          const int32_t oo = R.d_ledger_order[s];
-          f = oo == 0 ? __dadd_rn(0.0, tpp) : __dadd_rn(ov, tpp);
-          if (oo == 0) R.d_ledger_order[s] = ++next;
-          R.d_ledger_val[s] = f;
-          st_v = ov; st_o = oo;
-        }
-        // move lane 0's staged log entry to lane k (k < nl <= 7)
-        const double mv = __shfl_sync(0xffffffffu, st_v, 0);
-        const int32_t mo = __shfl_sync(0xffffffffu, st_o, 0);
-        if (lane == k) { lg_name = s; lg_val = mv; lg_ord = mo; }
-        next = __shfl_sync(0xffffffffu, next, 0);
-        f = __shfl_sync(0xffffffffu, f, 0);
-        long long k2, k1;
-        if (!propose_small_warp(t1, t2, f, k2, k1, lane)) { fail = PARVA_DIAG_SMALL_UNAVAILABLE; fname = s; rot = k + 1; break; }
-        if (lane == 0) {
-          double v = f;
-          for (long long j = 0; j < k2; j++) v = __dsub_rn(v, t2);
-          for (long long j = 0; j < k1; j++) v = __dsub_rn(v, t1);
-          R.d_ledger_val[s] = v;
-        }
-        if (lane == k) { my_k2 = k2; my_k1 = k1; }
-      }
-      KG_MARK(2);
-      int64_t nu = 0;
-      int32_t my_undo = 0;   // undo entry nu lives in lane nu (first 32), then in w.undo
-      if (fail < 0) {
-        long long tot = my_k2 + my_k1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (tot > w.qcap) fail = PARVA_DIAG_NEED_NEW_GPU;   // more GPCs than any map can free
-        else {
-          // proposals queue (allocator.py:403-405, drained by size): every size-2
-          // kind in drain order, then every size-1 kind
-          for (int c = 1; c >= 0 && fail < 0; c--) {
-            for (int k = 0; k < nl && fail < 0; k++) {
-              const long long cnt = __shfl_sync(0xffffffffu, c ? my_k2 : my_k1, k);
-              const int cat = __shfl_sync(0xffffffffu, c ? e_t2 : e_t1, k);
-              for (long long r = 0; r < cnt; r++) {
-                KG_MARK(3);
-                const int64_t g = S.first_fit(c, index, lane);
-                KG_MARK(5);
-                if (g < 0) { fail = PARVA_DIAG_NEED_NEW_GPU; break; }
-                const uint32_t m8 = S.M[g];
-                const int st = find_start(m8 & 0x7Fu, c);
-                const int ln = S.Ln[g];
-                const int32_t u = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
-                if (lane == 0) {
-                  S.M[g] = (uint8_t)(m8 | footprint(c, st));
-                  S.Ln[g] = (uint8_t)(ln + 1);
-                  w.lcat[g * 7 + ln] = cat;
-                  w.lslot[g * 7 + ln] = (uint8_t)st;
-                  if (nu >= 32) w.undo[nu] = u;
-                }
-                if (nu < 32 && lane == nu) my_undo = u;
-                __syncwarp();
-                nu++;
-                S.set_bits(g, lane);
-              }
-            }
-          }
-          if (fail >= 0) {  // all-or-nothing undo (allocator.py:272-277)
-            __threadfence_block();
-            for (int64_t j = nu - 1; j >= 0; j--) {
-              const int32_t u = j < 32 ? __shfl_sync(0xffffffffu, my_undo, (int)j) : w.undo[j];
-              const int64_t g = u >> 4;
-              const int c = (u >> 3) & 1, st = u & 7;
-              if (lane == 0) {
-                S.M[g] = (uint8_t)(S.M[g] & ~footprint(c, st));
-                S.Ln[g] = (uint8_t)(S.Ln[g] - 1);
-              }
-              __syncwarp();
-              S.set_bits(g, lane);
-            }
-          }
-        }
-      }
-      KG_MARK(3);
-#ifdef PARVA_KG_PROF
-      kn_drain++; kn_place += nu;
-#endif
-      if (fail >= 0) {
-        if (rot != nl) {   // allocator.py:415-417: the removed ones are re-appended
-          int src = lane + rot;
-          if (src >= nl) src -= nl;
-          const int nc = __shfl_sync(0xffffffffu, e_cat, src & 31);
-          const int ns = __shfl_sync(0xffffffffu, e_slot, src & 31);
-          if (lane < nl) { w.lcat[index * 7 + lane] = nc; w.lslot[index * 7 + lane] = (uint8_t)ns; }
-        }
-        // ledger rollback in reverse log order
-        for (int k = nl - 1; k >= 0; k--) {
-          const int32_t nm = __shfl_sync(0xffffffffu, lg_name, k);
-          const double v = __shfl_sync(0xffffffffu, lg_val, k);
-          const int32_t o = __shfl_sync(0xffffffffu, lg_ord, k);
-          if (nm >= 0 && lane == 0) { R.d_ledger_val[nm] = v; R.d_ledger_order[nm] = o; }
-        }
-        next = sv_next;
-        if (lane == 0 && nd < R.diag_cap) {
-          R.d_diag[3 * nd] = fail;
-          R.d_diag[3 * nd + 1] = w.id[index];
-          R.d_diag[3 * nd + 2] = fname;
-        }
-        nd++;
-      } else {
-        if (lane == 0) { S.M[index] = 0; S.Ln[index] = 0; }
-        __syncwarp();
-        S.set_bits(index, lane);
-      }
-      __syncwarp();
-      KG_MARK(4);
-    }
-#ifdef PARVA_KG_PROF
-    if (lane == 0)
-      printf("KGPROF drains %lld placements %lld cycles: search %lld lists %lld ledger+propose %lld place %lld "
-             "finish %lld (first_fit %lld)\n", kn_drain, kn_place, kp[0], kp[1], kp[2], kp[3], kp[4], kp[5]);
-#endif
-#undef KG_MARK
+    const int64_t nd = (in_smem && swords <= 64) ? opt_chain<true>(P, R, w, G0, lane, chain, dsm, sm_summary)
+                                                 : opt_chain<false>(P, R, w, G0, lane, chain, dsm, sm_summary);
     if (lane == 0) s_nd = nd;
   }
   __syncthreads();
 
   // ---- compaction + regression check (allocator.py:423-435), parallel
+#ifdef PARVA_KG_PROF
+  const long long kt2 = clock64();
+#endif
   int64_t nd = s_nd;
   if (run) {
     const int64_t n_after = block_scan(G0, [&](int64_t g) -> int64_t { return S.Ln[g] ? 1 : 0; }, w.gpu_pos, sh);
@@ -670,6 +700,9 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
     R.d_counts[3] = (int32_t)G0;
     *R.d_fallback = s_fallback;
     *R.d_status = status;
+#ifdef PARVA_KG_PROF
+    printf("KGPROF kernel cycles: prologue %lld chain %lld epilogue %lld\n", kt1 - kt0, kt2 - kt1, clock64() - kt2);
+#endif
   }
 }
 
@@ -682,7 +715,7 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
   const int64_t cap = r->gpu_cap;
   if (general_workspace(p, cap) > ws_bytes) return PARVA_BAD_INPUT;
   gen_prepare_kernel<<<1, 1024, 0, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8);
-  // shared-memory state when it fits: 2 B per GPU + 5 bitmap bits per GPU
+  // shared-memory state when it fits: 2 B per GPU + 2 bitmap bits per GPU
   static int s_smem[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
@@ -694,9 +727,9 @@ int launch_plan_general(const parva_general_problem* p, parva_general_result* r,
     smem_max -= (int)fa.sharedSizeBytes + 256;   // static shared memory of the kernel
     cudaFuncSetAttribute(plan_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
   }
-  // largest G with 2 * pad16(G) + 40 * ceil(G / 64) <= smem_max
-  int64_t smem_gpus = (int64_t)smem_max * 8 / 21;
-  while (smem_gpus > 0 && 2 * ((smem_gpus + 15) & ~int64_t(15)) + 40 * ((smem_gpus + 63) / 64) > smem_max) smem_gpus--;
+  // largest G with 2 * pad16(G) + 16 * ceil(G / 64) <= smem_max
+  int64_t smem_gpus = (int64_t)smem_max * 4 / 9;
+  while (smem_gpus > 0 && 2 * ((smem_gpus + 15) & ~int64_t(15)) + 16 * ((smem_gpus + 63) / 64) > smem_max) smem_gpus--;
   const size_t smem = (size_t)smem_max;
   plan_general_kernel<<<1, OPT_THREADS, smem, stream>>>(*p, *r, (uint8_t*)ws, cap, cap * 7 + 8, smem_gpus);
   return cudaGetLastError() == cudaSuccess ? PARVA_OK : PARVA_LAUNCH_ERROR;
