@@ -704,6 +704,9 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     import oracle
     from paper_2409_14447_b200.records import tiny_config
     E2E_DEPTH, E2E_BATCHES = 5, 8
+    # a throughput over at least 100 steps: a 20-step run would mostly time
+    # the pipeline's fill and drain (5 calls in flight)
+    steps = max(args.steps, 100)
     host = [shard_inputs(p) for p in range(E2E_BATCHES)]      # the caller's arrays (pageable)
     mb = B.MappedHostBatch(*host[0], cfg_format=2, plan_bytes=64, depth=E2E_DEPTH)
     pack_s = []
@@ -720,7 +723,7 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        mb.stream(dt, batches(c0, args.steps), consume=lambda i, slot: last.__setitem__(slot, c0 + i))
+        mb.stream(dt, batches(c0, steps), consume=lambda i, slot: last.__setitem__(slot, c0 + i))
         e2e_s = time.perf_counter() - t0
     else:   # one C call per step: wait for the slot's previous call, pack into its block, submit
         def loop(a, k):
@@ -734,7 +737,7 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        loop(c0, args.steps)
+        loop(c0, steps)
         e2e_s = time.perf_counter() - t0
     h2d = mb.h2d_bytes
     # the records of the last batch planned in every slot against the oracle
@@ -749,7 +752,7 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
         mb.fill(*host[i % E2E_BATCHES], slot=0)
         pack_s.append(time.perf_counter() - t)
 
-    def steps(c0, k, pack=True):
+    def run_steps(c0, k, pack=True):
         for i in range(c0, c0 + k):
             slot = i % E2E_DEPTH
             mb.wait(slot)
@@ -762,23 +765,25 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     # the same pipeline with the inputs packed outside the loop (one batch per slot)
     for slot in range(E2E_DEPTH):
         mb.fill(*host[slot], slot=slot)
-    steps(0, args.warmup, pack=False)
+    run_steps(0, args.warmup, pack=False)
     t0 = time.perf_counter()
-    steps(0, args.steps, pack=False)
+    run_steps(0, steps, pack=False)
     pre_s = time.perf_counter() - t0
     # one synchronous call per step (pack + launch + stream synchronize)
     for i in range(args.warmup):
         mb.fill(*host[i % E2E_BATCHES], slot=0)
         mb.run(dt)
     t0 = time.perf_counter()
-    for i in range(args.steps):
+    for i in range(steps):
         mb.fill(*host[i % E2E_BATCHES], slot=0)
         mb.run(dt)
     sync_s = time.perf_counter() - t0
+    floor_us = pcie_floor_us(torch, mb.h2d_bytes, mb.d2h_bytes)
     ok = dist_all(dist, torch, world, ok)
     e2e_s, pre_s, sync_s = dist_max(dist, torch, world, [e2e_s, pre_s, sync_s])
-    K = n_global * args.steps
-    return {"value": K / e2e_s, "unit": UNIT,
+    K = n_global * steps
+    step_us = e2e_s / steps * 1e6
+    return {"value": K / e2e_s, "unit": UNIT, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": mb.d2h_bytes,
             "api": "per step one C call, parva_plan_host_arrays_submit: wait for the slot's previous call, pack the "
                    "plain host arrays into the slot's pinned streamed block (parva_stream_pack_arrays, on the "
@@ -789,11 +794,44 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
                       "(int32 offsets and table ids, f64 rates and bounds)",
             "pipeline_depth": E2E_DEPTH,
             "host_pack_us_median": statistics.median(pack_s) * 1e6 if pack_s else None,
+            "pcie_roofline": {"bound": "pcie", "step_us": step_us, "floor_us": floor_us, "frac": floor_us / step_us,
+                              "floor": "the same H2D + D2H bytes per step as plain copy-engine copies from/to "
+                                       "pinned memory (cudaMemcpyAsync, H2D and D2H on their own streams, 3 steps "
+                                       "in flight), no planning: the bus time a step cannot go below"},
             "records_equal_oracle_last_steps": ok,
             "prepacked": {"value": K / pre_s, "unit": UNIT,
                           "api": "the same pipeline with every slot's input block packed once outside the loop"},
             "synchronous": {"value": K / sync_s, "unit": UNIT,
                             "api": "pack + parva_plan_host_mapped (one launch + stream synchronize) per step"}}
+
+
+def pcie_floor_us(torch, h2d_bytes, d2h_bytes, depth=3, steps=200):
+    """us per step for copy-engine copies of a step's H2D + D2H bytes alone
+    (pinned host memory; each step's H2D then D2H on its slot's stream)."""
+    streams = [torch.cuda.Stream() for _ in range(depth)]
+    hin = [torch.empty(h2d_bytes, dtype=torch.uint8).pin_memory() for _ in range(depth)]
+    hout = [torch.empty(d2h_bytes, dtype=torch.uint8).pin_memory() for _ in range(depth)]
+    din = [torch.empty(h2d_bytes, dtype=torch.uint8, device="cuda") for _ in range(depth)]
+    dout = [torch.empty(d2h_bytes, dtype=torch.uint8, device="cuda") for _ in range(depth)]
+    ev = [None] * depth
+
+    def step(i):
+        k = i % depth
+        if ev[k] is not None:
+            ev[k].synchronize()
+        with torch.cuda.stream(streams[k]):
+            din[k].copy_(hin[k], non_blocking=True)
+            hout[k].copy_(dout[k], non_blocking=True)
+            ev[k] = torch.cuda.Event()
+            ev[k].record(streams[k])
+    for i in range(3 * depth):
+        step(i)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        step(i)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / steps * 1e6
 
 
 def sim_measure(torch, fx, runs=256, horizon=10.0):
