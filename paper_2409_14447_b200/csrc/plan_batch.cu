@@ -16,11 +16,13 @@
 //     equivalent to the reference's cursors); the
 //     freed_rate ledger lives in lane = service registers, snapshot/restore
 //     is a register copy.
-// Two kernels: plan_batch_kernel (device-resident batches, tile by tile;
-// the <true> instantiation also copies each tile's records into every
-// rank's gathered block over peer memory) and plan_warp_kernel (the
-// zero-copy entry: loader CTAs stream the input over PCIe with TMA while
-// the other warps plan).  Scenarios beyond the 128-byte record's limits
+// Three kernels: plan_thread_kernel (plan_thread.cuh; device-resident
+// batches, the default: one thread per scenario; the <true> instantiation
+// also copies each chunk's records into every rank's gathered block over
+// peer memory), plan_batch_kernel (the tile kernel: lane groups per
+// scenario; used when K1's config records are given, i.e. for tables too
+// large for the index) and plan_warp_kernel (the zero-copy entry: loader
+// CTAs stream the input over PCIe with TMA while the other warps plan).  Scenarios beyond the 128-byte record's limits
 // report PARVA_CAPACITY and are re-planned by the general kernel
 // (plan_general.cu).
 #include <cuda_runtime.h>
