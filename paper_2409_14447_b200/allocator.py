@@ -108,7 +108,10 @@ class DeploymentMap:
             for p in sorted(gpu.placements, key=lambda p: p.start_slot)]} for gpu in self.gpus]}
 
     def to_json(self) -> str:
-        return json.dumps(self.to_json_obj(), indent=2) + "\n"
+        """json.dumps(self.to_json_obj(), indent=2) + "\\n", byte for byte
+        (the reference's to_json), written directly: one string template per
+        segment, each distinct placement formatted once."""
+        return _map_json(self.gpus)
 
     @classmethod
     def from_json(cls, text: str) -> "DeploymentMap":
@@ -130,6 +133,46 @@ class DeploymentMap:
         dmap = cls(gpus=gpus)
         dmap.validate()
         return dmap
+
+
+_INF = (float("inf"), float("-inf"))
+
+
+def _json_scalar(x) -> str:
+    """json.dumps of one scalar: ints by int.__repr__, finite floats by
+    float.__repr__ (what json's encoder does), anything else through json."""
+    t = type(x)
+    if t is int:
+        return int.__repr__(x)
+    if t is float and x == x and x not in _INF:
+        return float.__repr__(x)
+    return json.dumps(x)
+
+
+_SEGMENT_JSON = ('        {{\n          "service": {},\n          "instance_size": {},\n          "batch_size": {},\n'
+                 '          "process_count": {},\n          "start_slot": {},\n          "throughput_rps": {}\n        }}')
+
+
+def _map_json(gpus) -> str:
+    if not gpus:
+        return '{\n  "gpus": []\n}\n'
+    ids: dict = {}
+    fmt, js = _SEGMENT_JSON.format, _json_scalar
+
+    def seg(p):
+        sid = ids.get(p.service_id)
+        if sid is None:
+            sid = ids[p.service_id] = json.dumps(p.service_id)
+        return fmt(sid, js(p.instance_size), js(p.batch_size), js(p.process_count), js(p.start_slot), js(p.throughput))
+
+    parts = []
+    for gpu in gpus:
+        pl = gpu.placements
+        if len(pl) > 1:
+            pl = sorted(pl, key=lambda p: p.start_slot)
+        head = '    {\n      "id": ' + js(gpu.id) + ',\n      "segments": '
+        parts.append(head + ("[\n" + ",\n".join([seg(p) for p in pl]) + "\n      ]\n    }" if pl else "[]\n    }"))
+    return '{\n  "gpus": [\n' + ",\n".join(parts) + '\n  ]\n}\n'
 
 
 # ---------------------------------------------------- general-problem glue

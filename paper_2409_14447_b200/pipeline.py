@@ -101,17 +101,33 @@ def _decode_record(services: list[Service], rec) -> DeploymentMap:
 
 
 def _decode_general(services: list[Service], g, out) -> DeploymentMap:
+    """DeploymentMap from the general kernel's outputs (GPU ids, placement
+    lists as catalogue indices + start slots, ledger, diagnostics)."""
+    cat_key = g.cat_key
+    proto: dict = {}          # catalogue entry -> (service id, triplet fields)
+    by_size: dict = {}        # service -> {instance size: triplet}
+
+    def kind(cat):
+        v = proto.get(cat)
+        if v is None:
+            s, c = cat_key[cat]
+            d = by_size.get(s)
+            if d is None:
+                d = by_size[s] = {x.instance_size: x for x in services[s].best_triplets}
+            t = d[INSTANCE_SIZES[c]]
+            v = proto[cat] = (services[s].id, t.instance_size, t.batch_size, t.process_count, t.throughput)
+        return v
+
+    pl_cat, pl_slot, pl_off = out.pl_cat.tolist(), out.pl_slot.tolist(), out.pl_off.tolist()
     gpus = []
-    for k in range(len(out.gpu_id)):
-        gs = GpuState(id=int(out.gpu_id[k]))
-        for j in range(int(out.pl_off[k]), int(out.pl_off[k + 1])):
-            s, c = g.cat_key[int(out.pl_cat[j])]
-            t = {INSTANCE_SIZES.index(x.instance_size): x for x in services[s].best_triplets}[c]
-            gs.placements.append(Placement(services[s].id, t.instance_size, t.batch_size, t.process_count,
-                                           t.throughput, int(out.pl_slot[j])))
-        gpus.append(gs)
-    ranks = sorted((int(out.ledger_order[s]), s) for s in range(len(services)) if out.ledger_order[s])
-    freed = {services[s].id: float(out.ledger_val[s]) for _, s in ranks}
+    for k, gid in enumerate(out.gpu_id.tolist()):
+        gpus.append(GpuState(id=gid, placements=[Placement(*kind(pl_cat[j]), pl_slot[j])
+                                                 for j in range(pl_off[k], pl_off[k + 1])]))
+    order = out.ledger_order
+    live = np.flatnonzero(order[:len(services)])
+    ranks = live[np.argsort(order[live], kind="stable")].tolist()
+    vals = out.ledger_val
+    freed = {services[s].id: float(vals[s]) for s in ranks}
     diags = [format_diag(r, gid, services[n].id if n >= 0 else None) for r, gid, n in out.diags]
     return DeploymentMap(gpus=gpus, freed_rate=freed, diagnostics=diags)
 

@@ -276,3 +276,28 @@ def test_stream_pack_arrays_matches_the_u16_pack():
     buf = np.zeros(4096, np.uint8)
     assert L.parva_stream_pack_arrays(C.c_int32(3), N.np_ptr(bad), N.np_ptr(np.zeros(8, np.int32)), N.np_ptr(z),
                                       N.np_ptr(z), C.c_int32(2), N.np_ptr(buf), C.c_int64(4096), C.c_int32(0)) == -1
+
+
+def test_deployment_json_matches_json_dumps():
+    """DeploymentMap.to_json writes the reference's json.dumps(indent=2)
+    text directly; byte-equal on random maps (escapes, non-finite floats,
+    ints, empty lists, slot order)."""
+    import json
+    import random
+
+    from paper_2409_14447_b200.allocator import DeploymentMap
+    from paper_2409_14447_b200.mig import GpuState, Placement
+    rng = random.Random(7)
+    for trial in range(400):
+        gpus = []
+        for g in range(rng.randint(0, 6)):
+            gs = GpuState(id=rng.choice([g, 7 * g, -3, 10 ** 12]))
+            for _ in range(rng.randint(0, 4)):
+                tp = rng.choice([1.5, 0.1 + 0.2, 1e-300, 123456789.123, float("inf"), float("nan"), 3.0, 1e22,
+                                 5e-324, -0.0, 7])
+                sid = rng.choice(["a", "d121#3", 'q"uo\\te', "ünï", "tab\t", ""])
+                gs.placements.append(Placement(sid, rng.choice([1, 2, 3, 4, 7]), rng.randint(1, 128),
+                                               rng.randint(1, 8), tp, rng.randint(0, 6)))
+            gpus.append(gs)
+        d = DeploymentMap(gpus=gpus)
+        assert d.to_json() == json.dumps(d.to_json_obj(), indent=2) + "\n", trial
