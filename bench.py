@@ -930,8 +930,23 @@ def c4_measure(torch, N, B, W, fx, dt, local):
         torch.cuda.synchronize()
         times.append(a.elapsed_time(b))
     ms = sorted(times)[len(times) // 2]
-    return {"workload": "C4 generator (seed 1), 10^6 scenarios x 11 services, one GPU", "ms_per_launch": ms,
+    line = {"workload": "C4 generator (seed 1), 10^6 scenarios x 11 services, one GPU", "ms_per_launch": ms,
             "value": n / (ms / 1000.0), "unit": UNIT, "l2": "inputs 17.6 MB + outputs 480 MB exceed L2 reuse"}
+    # the first 10^4 scenarios on the CPU: the port's time (one thread) and a parity check of those records
+    import oracle
+    from paper_2409_14447_b200.tables import pack_tables
+    k = 10_000
+    cfg = N.records_to_numpy(res.cfg, 11 * k, N.CONFIG_DTYPE)
+    plan = N.records_to_numpy(res.plan, k, B.PLAN_DTYPE)
+    tc = time.perf_counter()
+    ocfg, oplan = oracle.plan_batch_records(pack_tables(fx.tables), off[:k + 1], tab[:11 * k], rate[:11 * k],
+                                            bound[:11 * k], threads=1)
+    port_s = time.perf_counter() - tc
+    line["parity_vs_oracle_first_10000"] = bool(cfg[:11 * k].tobytes() == ocfg.tobytes() and
+                                                plan[:k].tobytes() == oplan.tobytes())
+    line["cpu"] = {"port_1core": {"scenarios": k, "seconds": port_s, "value": k / port_s, "unit": UNIT,
+                                  "extrapolated_s_for_10^6": port_s * n / k}}
+    return line
 
 
 def c4_sharded_measure(torch, dist, world, rank, N, B, D, fx, dt, reps=5):
@@ -1049,8 +1064,11 @@ def sweep_measure(args, torch, dist, world, rank, N, B, W, hbm, peak_src):
     achieved = alg / (ms / 1000.0) / 1e9
     k = min(nl, 1000)
     recs = N.records_to_numpy(out, nl, N.CONFIG_DTYPE)
-    orec = oracle.configure_batch(pt, np.arange(k), dth.rate[:k], dth.slo[:k] / 2.0)
+    tc = time.perf_counter()
+    orec = oracle.configure_batch(pt, np.arange(k), dth.rate[:k], dth.slo[:k] / 2.0, threads=1)
+    port_s = time.perf_counter() - tc
     local_ok = bool(recs[:k].tobytes() == orec.tobytes())
+    port_points = int(np.asarray(pt.seg_count)[:5 * k].sum())
     line = {"workload": "C3: 10^4 dense tables (5 sizes x batch 1-128 x procs 1-8), 1 query each",
             "workloads": nw, "points": points, "ms_per_launch": ms, "value": nw / (ms / 1000.0) if world == 1 else None,
             "unit": "workloads/s", "points_per_s": points / (ms / 1000.0),
@@ -1059,8 +1077,15 @@ def sweep_measure(args, torch, dist, world, rank, N, B, W, hbm, peak_src):
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": alg},
             "parity_vs_oracle_first_1000": local_ok,
             "l2": "no flush: the profile points per launch exceed the 126 MB L2",
-            "generation_s": gen_s}
+            "generation_s": gen_s,
+            "cpu": {"port_1core": {"workloads": k, "points": port_points, "seconds": port_s,
+                                   "workloads_per_s": k / port_s, "points_per_s": port_points / port_s,
+                                   "what": "oracle/migplan_oracle.c configure for the first workloads, one thread"}}}
     if world == 1:
+        if not args.no_cpu:
+            r = ref_python("c3", "--n", 200)
+            if r:
+                line["cpu"]["reference_python_1core"] = r
         return line
     # one all-gather of the config records (padded to the largest shard)
     gat = torch.empty((world * max_l, 32), dtype=torch.uint8, device="cuda")

@@ -5,6 +5,7 @@ bench's workloads, on this host's cores.  Used by bench.py's cpu_baseline
 leg; prints one JSON object.
 
     python tools/ref_python_bench.py c2 --n 2000 --procs 1
+    python tools/ref_python_bench.py c3 --n 200
     python tools/ref_python_bench.py c5
 
 Timed region per scenario = the reference's own (pipeline.py:95-103):
@@ -107,13 +108,42 @@ def run_c5():
             "configure_s": t1 - t0, "relocate_s": t2 - t1, "optimize_s": t3 - t2, "seconds": t3 - t0}
 
 
+def run_c3(n):
+    """configure_service (configurator.py:189-191) for the first n C3
+    workloads, one query each; ProfileTables built outside the timer."""
+    INSTANCE_SIZES = (1, 2, 3, 4, 7)
+    dth = W.dense_tables(n, seed=3)
+    tables = []
+    for w in range(n):
+        pts = []
+        for c, size in enumerate(INSTANCE_SIZES):
+            a = int(dth.seg_start[w * 5 + c])
+            for i in range(a, a + int(dth.seg_count[w * 5 + c])):
+                pts.append(migplan.ProfilePoint(f"w{w:05d}", size, int(dth.batch[i]), int(dth.procs[i]),
+                                                float(dth.tp[i]), float(dth.lat[i])))
+        tables.append(migplan.ProfileTable(f"w{w:05d}", tuple(pts)))
+    services = [RC.make_service(f"w{w:05d}", f"w{w:05d}", float(dth.rate[w]), float(dth.slo[w])) for w in range(n)]
+    done = infeasible = 0
+    t0 = time.perf_counter()
+    for s, t in zip(services, tables):
+        try:
+            RC.configure_service(s, t)
+        except migplan.MigplanError:
+            infeasible += 1
+        done += 1
+    el = time.perf_counter() - t0
+    points = int(dth.seg_count.sum())
+    return {"config": "C3", "workloads": done, "infeasible_or_uncoverable": infeasible, "points": points,
+            "seconds": el, "workloads_per_s": done / el, "points_per_s": points / el, "procs": 1}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=["c2", "c5"])
+    ap.add_argument("config", choices=["c2", "c3", "c5"])
     ap.add_argument("--n", type=int, default=2000)
     ap.add_argument("--procs", type=int, default=1)
     a = ap.parse_args()
-    res = run_c2(a.n, a.procs) if a.config == "c2" else run_c5()
+    res = run_c2(a.n, a.procs) if a.config == "c2" else run_c3(a.n) if a.config == "c3" else run_c5()
     res["python"] = sys.version.split()[0]
     res["reference"] = "migplan (baseline/_ref, unmodified)"
     print(json.dumps(res), flush=True)
