@@ -216,8 +216,19 @@ __device__ inline bool propose_small_warp(double tp1, double tp2, double freed, 
       } else ok = false;
     }
     long long g, cn, nk;
-    // warp-uniform choice (the reductions are collective)
-    if (packed && __all_sync(0xffffffffu, !ok || 2 * k2 + k1 < (1ll << 21))) {
+    // warp-uniform choice (the reductions are collective).  Small fields:
+    // key = gpcs << 20 | count << 10 | (1023 - k2) in 32 bits, one redux.
+    if (__all_sync(0xffffffffu, !ok || (2 * k2 + k1 < 4095 && k2 + k1 < 1024 && k2 < 1024))) {
+      const unsigned key = ok ? (unsigned)(2 * k2 + k1) << 20 | (unsigned)(k2 + k1) << 10 | (unsigned)(1023 - k2)
+                              : 0xFFFFFFFFu;
+      const unsigned m = __reduce_min_sync(0xffffffffu, key);
+      if (m == 0xFFFFFFFFu) { g = cn = nk = LLONG_MAX; }
+      else {
+        g = (long long)(m >> 20);
+        cn = (long long)((m >> 10) & 1023u);
+        nk = (long long)(m & 1023u) - 1023;
+      }
+    } else if (packed && __all_sync(0xffffffffu, !ok || 2 * k2 + k1 < (1ll << 21))) {
       unsigned long long key = ok ? ((unsigned long long)(2 * k2 + k1) << 42) |
                                         ((unsigned long long)(k2 + k1) << 21) |
                                         (unsigned long long)((1ll << 21) - 1 - k2)
