@@ -6,8 +6,8 @@
 //
 // Relocation runs as parallel per-size-class phases (gen_prepare_kernel).  The
 // optimize pass is a serial dependency chain walked by one
-// warp; first-fit is a two-level "accepts" bitmap search (summary ballot,
-// then word) instead of the reference's O(M) scans and O(M) _next_id
+// warp; first-fit is an "accepts" bitmap search from a lazily advanced
+// start word instead of the reference's O(M) scans and O(M) _next_id
 // (allocator.py:204-281), which is what makes the 10^5-segment case (C5)
 // cheap.  Ledger rollback uses an undo log instead of the reference's
 // whole-dict snapshot (allocator.py:387,418-419): same observable ledger,
@@ -48,7 +48,6 @@ struct GenWs {
   int32_t* undo;    // [qcap]
   double* after;    // [n_services]
   uint8_t* seen;    // [n_services]
-  uint64_t* summary;// [5 * swords] (global fallback of the summary bitmaps)
   int64_t* svc_pos; // [n_services + 1] relocation queue offsets of one size class
   int64_t* gpu_pos; // [cap + 1] cumulative capacity of one size class
   int64_t* gpu_pos2;// [cap + 1] second scan buffer
@@ -70,7 +69,6 @@ __host__ __device__ inline size_t gen_layout(int64_t cap, int64_t qcap, int n_se
   t.b_id = (int64_t*)take(cap * 8); t.b_mask = take(cap); t.b_len = take(cap); t.b_ngpc = take(cap);
   t.b_lcat = (int32_t*)take(cap * 7 * 4); t.b_lslot = take(cap * 7);
   t.acc = (uint64_t*)take(5 * words * 8);
-  t.summary = (uint64_t*)take(5 * ((words + 63) / 64 + 1) * 8);
   t.q = (int32_t*)take(qcap * 4); t.q1 = (int32_t*)take(qcap * 4); t.undo = (int32_t*)take(qcap * 4);
   t.after = (double*)take((size_t)(n_services + 1) * 8); t.seen = take(n_services + 1);
   t.svc_pos = (int64_t*)take((size_t)(n_services + 2) * 8); t.gpu_pos = (int64_t*)take((size_t)(cap + 2) * 8);
@@ -300,9 +298,10 @@ __device__ inline double unalloc_g(int64_t total, int64_t n) {
 // accepts bitmaps of size classes 1 and 2 -- the only sizes a proposal has
 // -- sit in shared memory when they fit (~110k GPUs), else in global memory.
 // The next drain candidate (0 < num_gpcs <= threshold) is found 8 GPUs per
-// load; first-fit starts at a per-class hint (summary words below it are
-// zero) and reads the summary bitmap, then one word (cursor-free first fit,
-// SURVEY App. B #2); undo entries carry (gpu, class, slot) so a rollback
+// load (SWAR per-byte popcount); first fit is the first nonzero accepts word
+// at or after a per-class start word that moves past zero words once and
+// back only when a GPU below it starts accepting (cursor-free first fit,
+// same choice as a scan from GPU 0); undo entries carry (gpu, class, slot) so a rollback
 // reads no lists; the freed_rate ledger rolls back from a log.
 constexpr int OPT_THREADS = 512;
 constexpr int kChainUndo = 256;   // undo entries kept in shared memory (the rest in w.undo)
@@ -311,61 +310,55 @@ struct OptState {
   uint8_t* M;        // mask | flag, per GPU
   uint8_t* Ln;       // list length, per GPU
   uint64_t* A;       // accepts bitmaps [2][words] (size classes 0, 1)
-  uint64_t* Sm;      // summary bitmaps [2][swords]: bit = word of A nonzero
-  int64_t words, swords, G;
-  int64_t hint[2];   // summary words below hint[c] are zero
+  int64_t words, G;
+  int64_t lw[2];     // accepts words below lw[c] are zero (first-fit starts there)
 
-  // GPU g's byte is now m: its accepts bits and the summaries
+  // GPU g's byte is now m: its accepts bits and the start words
   __device__ __forceinline__ void set_bits(int64_t g, uint32_t m) {
     m &= 0x7Fu;
-    const int64_t k = g >> 6, sw = k >> 6;
-    const uint64_t bit = 1ull << (g & 63), sb = 1ull << (k & 63);
+    const int64_t k = g >> 6;
+    const uint64_t bit = 1ull << (g & 63);
     const bool acc0 = m != 0x7Fu;                                                     // find_start(m, 0) >= 0
     const bool acc1 = (m & 0x03u) == 0 || (m & 0x0Cu) == 0 || (m & 0x30u) == 0;        // find_start(m, 1) >= 0
-    const uint64_t a0 = A[k], a1 = A[words + k], s0 = Sm[sw], s1 = Sm[swords + sw];
-    const uint64_t n0 = acc0 ? (a0 | bit) : (a0 & ~bit), n1 = acc1 ? (a1 | bit) : (a1 & ~bit);
-    A[k] = n0;
-    A[words + k] = n1;
-    Sm[sw] = n0 ? (s0 | sb) : (s0 & ~sb);
-    Sm[swords + sw] = n1 ? (s1 | sb) : (s1 & ~sb);
-    if (n0 && sw < hint[0]) hint[0] = sw;
-    if (n1 && sw < hint[1]) hint[1] = sw;
+    const uint64_t a0 = A[k], a1 = A[words + k];
+    A[k] = acc0 ? (a0 | bit) : (a0 & ~bit);
+    A[words + k] = acc1 ? (a1 | bit) : (a1 & ~bit);
+    if (acc0 && k < lw[0]) lw[0] = k;
+    if (acc1 && k < lw[1]) lw[1] = k;
   }
 
-  // first GPU in list order accepting class c (0 or 1), skipping `excl`
+  // first GPU in list order accepting class c (0 or 1), skipping `excl`:
+  // the first nonzero accepts word at or after lw[c] (zero words are passed
+  // once: lw only moves back when a GPU below it starts accepting)
   __device__ __forceinline__ int64_t first_fit(int c, int64_t excl) {
     const uint64_t* a = A + c * words;
-    const uint64_t* sm = Sm + c * swords;
     const int64_t ew = excl >> 6;
     const uint64_t ebit = 1ull << (excl & 63);
-    for (int64_t sw = hint[c]; sw < swords; sw++) {
-      uint64_t v = sm[sw];
-      if (!v) {
-        if (sw == hint[c]) hint[c] = sw + 1;
-        continue;
-      }
-      while (v) {
-        const int64_t wi = sw * 64 + __ffsll((long long)v) - 1;
-        v &= v - 1;
-        uint64_t word = a[wi];
-        if (wi == ew) word &= ~ebit;
-        if (word) return wi * 64 + __ffsll((long long)word) - 1;
-      }
+    for (int64_t k = lw[c]; k < words; k++) {
+      const uint64_t word = a[k];
+      const uint64_t v = k == ew ? word & ~ebit : word;
+      if (v) return k * 64 + __ffsll((long long)v) - 1;
+      if (!word && k == lw[c]) lw[c] = k + 1;
     }
     return -1;
   }
 
-  // highest GPU <= idx with 0 < num_gpcs <= thr, 8 GPUs per load
+  // highest GPU <= idx with 0 < num_gpcs <= thr: 8 GPUs per load, tested
+  // at once (per-byte popcount of the 7 slot bits minus the size-3@0 flag)
   __device__ __forceinline__ int64_t prev_candidate(int64_t idx, int thr) const {
-    for (int64_t w8 = idx >> 3; w8 >= 0; w8--) {
+    if (thr <= 0 || idx < 0) return -1;
+    const uint64_t lo7 = 0x7F7F7F7F7F7F7F7Full, b1 = 0x0101010101010101ull;
+    const uint64_t up = thr >= 7 ? 0ull : (uint64_t)(0x80 - thr - 1) * b1;   // + up sets bit 7 iff gpcs > thr
+    uint64_t keep = (idx & 7) == 7 ? ~0ull : (1ull << (8 * ((idx & 7) + 1))) - 1;   // bytes <= idx
+    for (int64_t w8 = idx >> 3; w8 >= 0; w8--, keep = ~0ull) {
       const uint64_t x = reinterpret_cast<const uint64_t*>(M)[w8];
-      if (!x) continue;
-#pragma unroll
-      for (int b = 7; b >= 0; b--) {
-        const uint32_t m = (uint32_t)(x >> (8 * b)) & 0xFFu;
-        const int ng = __popc(m & 0x7Fu) - (int)(m >> 7);
-        if (w8 * 8 + b <= idx && ng > 0 && ng <= thr) return w8 * 8 + b;
-      }
+      uint64_t v = x & lo7;
+      v = v - ((v >> 1) & 0x5555555555555555ull);
+      v = (v & 0x3333333333333333ull) + ((v >> 2) & 0x3333333333333333ull);
+      v = (v + (v >> 4)) & 0x0F0F0F0F0F0F0F0Full;
+      const uint64_t g = v - ((x >> 7) & b1);                   // gpcs per byte, 0..7 (the flag implies >= 4 cells)
+      const uint64_t hit = (g + lo7) & ~(thr >= 7 ? 0ull : (g + up)) & (b1 << 7) & keep;
+      if (hit) return w8 * 8 + ((63 - __clzll((long long)hit)) >> 3);
     }
     return -1;
   }
@@ -384,22 +377,19 @@ struct ChainSmem {
   int32_t undo[kChainUndo];
 };
 
-// kSmem: GPU state and bitmaps in shared memory (dsm / sm_summary), so the
+// kSmem: GPU state and bitmaps in shared memory (dsm), so the
 // compiler emits shared-memory accesses instead of generic ones
 template <bool kSmem>
 __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, const parva_general_result& R,
-                                             const GenWs& w, int64_t G0, int lane, ChainSmem& C, uint8_t* dsm,
-                                             uint64_t* sm_summary) {
+                                             const GenWs& w, int64_t G0, int lane, ChainSmem& C, uint8_t* dsm) {
   OptState S;
   const int64_t gpad = (G0 + 15) & ~int64_t(15);
   S.words = (G0 + 63) / 64;
-  S.swords = (S.words + 63) / 64;
   S.G = G0;
   S.M = kSmem ? dsm : w.mask;
   S.Ln = kSmem ? dsm + gpad : w.len;
   S.A = kSmem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
-  S.Sm = kSmem ? sm_summary : w.summary;
-  S.hint[0] = S.hint[1] = 0;
+  S.lw[0] = S.lw[1] = 0;
   int32_t next = (int32_t)w.hdr[3];
   int64_t nd = 0;
   int64_t idx = G0 - 1;
@@ -547,7 +537,6 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   __shared__ int64_t sh[33];
   __shared__ int s_fallback, s_status;
   __shared__ int64_t s_nd;
-  __shared__ uint64_t sm_summary[2 * 64];
   __shared__ ChainSmem chain;
   GenWs w;
   gen_layout(cap, qcap, P.n_services, P.n_cat, ws_base, &w);
@@ -559,17 +548,14 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   int status = (int)w.hdr[2];
   const bool in_smem = G0 <= smem_gpus;
   const int64_t words = (G0 + 63) / 64;
-  const int64_t swords = (words + 63) / 64;
   const int64_t gpad = (G0 + 15) & ~int64_t(15);
   OptState S;
   S.M = in_smem ? dsm : w.mask;
   S.Ln = in_smem ? dsm + gpad : w.len;
   S.A = in_smem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
-  S.Sm = (in_smem && swords <= 64) ? sm_summary : w.summary;
   S.words = words;
-  S.swords = swords;
   S.G = G0;
-  S.hint[0] = S.hint[1] = 0;
+  S.lw[0] = S.lw[1] = 0;
   if (in_smem)
     for (int64_t g = tid; g < G0; g += blockDim.x) { S.M[g] = w.mask[g]; S.Ln[g] = w.len[g]; }
   __syncthreads();
@@ -582,15 +568,6 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
     }
 #pragma unroll
     for (int c = 0; c < 2; c++) S.A[c * words + k] = b[c];
-  }
-  __syncthreads();
-  for (int64_t k = tid; k < 2 * swords; k += blockDim.x) {
-    const int c = (int)(k / swords);
-    const int64_t sw = k % swords;
-    uint64_t v = 0;
-    for (int j = 0; j < 64 && sw * 64 + j < words; j++)
-      if (S.A[c * words + sw * 64 + j]) v |= 1ull << j;
-    S.Sm[k] = v;
   }
   const bool run = P.optimize && status == PARVA_OK;
   if (run)
@@ -605,8 +582,8 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
   const long long kt1 = clock64();
 #endif
   if (run && warp == 0) {
-    const int64_t nd = (in_smem && swords <= 64) ? opt_chain<true>(P, R, w, G0, lane, chain, dsm, sm_summary)
-                                                 : opt_chain<false>(P, R, w, G0, lane, chain, dsm, sm_summary);
+    const int64_t nd = in_smem ? opt_chain<true>(P, R, w, G0, lane, chain, dsm)
+                               : opt_chain<false>(P, R, w, G0, lane, chain, dsm);
     if (lane == 0) s_nd = nd;
   }
   __syncthreads();

@@ -67,11 +67,12 @@ def build():
                 elif f.name in sources:
                     sources.remove(f.name)
             patches = []
-        pb = d / "plan_batch.cu"
-        src = pb.read_text()
-        for p in patches:
-            src = apply(src, p)
-        pb.write_text(src)
+        for p in patches:                    # each block applies to the csrc file that holds its OLD text
+            for block in p.read_text().split("<<<<\n")[1:]:
+                old, rest = block.split("====\n", 1)
+                hit = [f for f in sorted(d.iterdir()) if f.suffix in (".cu", ".cuh") and old in f.read_text()]
+                assert hit, (p, old[:80])
+                hit[0].write_text(hit[0].read_text().replace(old, rest.split(">>>>\n", 1)[0]))
         lib = OUT / f"libk2_{name}.so"
         inc = str(REPO / "include")
         cmd = [b.NVCC, *b.FLAGS, *flags, "-o", str(lib), *[str(d / s) for s in sources], "-lcudart"]
