@@ -230,11 +230,11 @@ def cpu_baselines(fx, n, min_seconds=10.0):
                      f"oracle/migplan_oracle.c via OpenMP on {threads} threads",
            "port_1core": {"value": v1, "unit": UNIT, "cores": 1,
                           "sample": f"C2 batch repeated {reps1}x ({el1:.1f} s) on one thread"}}
-    r1 = ref_python("c2", "--n", 1500, "--procs", 1)
+    r1 = ref_python("c2", "--n", n, "--procs", 1)
     ra = ref_python("c2", "--n", n, "--procs", threads)
     if r1 is not None:
         out["reference_python_1core"] = {"value": r1.get("scenarios_per_s"), "unit": UNIT, "cores": 1,
-                                         "sample": "first 1500 C2 scenarios (seed 0), configure + relocate + "
+                                         "sample": f"full C2 batch ({n} scenarios, seed 0), configure + relocate + "
                                                    "optimize per scenario (pipeline.py:95-103)", "raw": r1}
         out["reference_python_all_cores"] = {"value": ra.get("scenarios_per_s"), "unit": UNIT, "cores": threads,
                                              "sample": f"full C2 batch ({n} scenarios), fork Pool of {threads} "
@@ -677,10 +677,21 @@ def main():
         if rank == 0:
             line["large_cluster"] = c5_measure(torch, fx)
             line["simulation"] = sim_measure(torch, fx)
+    if not args.no_extra and rank == 0:
+        line["c1_fixtures"] = c1_measure(fx)
     if not args.no_cpu and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baselines(fx, n)
         if "large_cluster" in line:
             line["large_cluster"]["cpu"] = c5_cpu(fx)
+        if "c1_fixtures" in line:
+            r = ref_python("c1")
+            if r:
+                line["c1_fixtures"]["reference_python_1core"] = r
+        if "c4_single_gpu" in line:
+            r = ref_python("c4", "--n", 2000, "--procs", 1)
+            if r:
+                r["extrapolated_s_for_10^6"] = r["seconds"] * 1e6 / r["scenarios"]
+                line["c4_single_gpu"].setdefault("cpu", {})["reference_python_1core"] = r
     clk.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -911,6 +922,29 @@ def c5_measure(torch, fx):
             "gpus_before_optimize": out.n_gpus_unopt, "gpus": int(len(out.gpu_id)),
             "ms_wall_incl_transfers": min(m[0] for m in ms), "ms_stream": min(m[1] for m in ms),
             "note": "CPU times on this host in large_cluster.cpu (cpu leg)"}
+
+
+def c1_measure(fx, reps=20):
+    """C1: the Table IV fixture scenarios S1-S6 through the public API
+    (plan_scenario: one fused launch + decode of every object), wall time per
+    scenario (median of reps), GPU counts checked against the reference's."""
+    import paper_2409_14447_b200 as P
+    want = {"S1": 1, "S2": 2, "S3": 3, "S4": 4, "S5": 8, "S6": 9}     # SURVEY 8c / BASELINE 2
+    out = {}
+    for name, svcs in fx.scenarios.items():
+        sc = P.Scenario(name, tuple(P.scenario.ScenarioService(m, r, l) for m, r, l in svcs))
+        P.plan_scenario(sc, fx.tables)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            res = P.plan_scenario(sc, fx.tables)
+            res.services, res.deployment
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        out[name] = {"ms": ts[len(ts) // 2] * 1e3, "gpus": res.gpu_count,
+                     "gpus_equal_reference": res.gpu_count == want.get(name)}
+    return {"workload": "C1: S1-S6 through plan_scenario (one launch + synchronize + full decode per scenario)",
+            "scenarios": out}
 
 
 def c4_measure(torch, N, B, W, fx, dt, local):

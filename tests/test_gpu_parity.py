@@ -860,3 +860,24 @@ def test_host_entry_arrays_submit(fx):
         mb.wait(slot)
         cfg, plan = mb.outputs(slot)
         assert plan.tobytes() == exp[j][1] and cfg.tobytes() == exp[j][0]
+
+
+def test_plan_many_zero_copy_and_copy_paths(fx):
+    """plan_many below pipeline._ZERO_COPY_MAX scenarios runs K2 straight on
+    pinned host buffers (no copies); above it, on device copies.  Both give
+    the reference's C2 digests (first 1,500 scenarios: one call of 1,000 on
+    the zero-copy path, then 1,500 on the copy path, then single scenarios)."""
+    from paper_2409_14447_b200 import pipeline as PL
+    g = golden("c2_digests.json")
+    n = 1500
+    sb = W.scenario_batch(fx, n, seed=g["seed"])
+    sets = [[P.make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]
+            for k in range(n)]
+    assert 1000 <= PL._ZERO_COPY_MAX < n
+    for lo, hi in ((0, 1000), (0, n)):
+        res = P.plan_many(sets[lo:hi], fx.tables)
+        for k, r in enumerate(res, start=lo):
+            assert canon.digest(_canon_result(r)) == g["digests"][k], (lo, hi, k)
+    for k in (0, 99, 777):
+        r = P.plan_many([sets[k]], fx.tables)[0]
+        assert canon.digest(_canon_result(r)) == g["digests"][k], k

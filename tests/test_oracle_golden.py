@@ -299,7 +299,7 @@ def test_plan_many_lazy_results_decode_to_reference_plans(fx, monkeypatch):
 
     monkeypatch.setattr(PL, "plan_batch", fake_plan_batch)
     monkeypatch.setattr(PL, "resolve_capacity", lambda *a, **k: {})
-    monkeypatch.setattr(Nm, "device_tables_for", lambda *a, **k: types.SimpleNamespace(packed=pt))
+    monkeypatch.setattr(Nm, "device_tables_for", lambda *a, **k: types.SimpleNamespace(packed=pt, index_struct=None))
     monkeypatch.setattr(Nm, "require_cuda", lambda: types.SimpleNamespace(
         cuda=types.SimpleNamespace(synchronize=lambda: None)))
     sets = [[P.make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]

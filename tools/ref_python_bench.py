@@ -5,7 +5,9 @@ bench's workloads, on this host's cores.  Used by bench.py's cpu_baseline
 leg; prints one JSON object.
 
     python tools/ref_python_bench.py c2 --n 2000 --procs 1
+    python tools/ref_python_bench.py c1
     python tools/ref_python_bench.py c3 --n 200
+    python tools/ref_python_bench.py c4 --n 2000     (C4 generator = C2 with seed 1)
     python tools/ref_python_bench.py c5
 
 Timed region per scenario = the reference's own (pipeline.py:95-103):
@@ -72,10 +74,27 @@ def _c2_chunk(args):
     return done, infeasible, time.perf_counter() - t0
 
 
-def run_c2(n, procs):
+def run_c1(reps=20):
+    """S1-S6 (Table IV fixtures), the plan region per scenario, median of reps."""
+    fx = W.load_fixtures()
+    prepared = ref_tables(fx)
+    out = {}
+    for name, svcs in fx.scenarios.items():
+        services = [RC.make_service(f"{m}#{i}", m, float(r), float(l)) for i, (m, r, l) in enumerate(svcs)]
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            res = plan_one(services, prepared)
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        out[name] = {"ms": ts[len(ts) // 2] * 1e3, "gpus": res.gpu_count, "services": len(services)}
+    return {"config": "C1", "scenarios": out, "procs": 1}
+
+
+def run_c2(n, procs, seed=0):
     fx = W.load_fixtures()
     _STATE["prepared"] = ref_tables(fx)
-    _STATE["sb"] = W.scenario_batch(fx, n, seed=0)
+    _STATE["sb"] = W.scenario_batch(fx, n, seed=seed)
     if procs <= 1:
         done, inf, el = _c2_chunk((0, n, 1))
     else:
@@ -87,8 +106,8 @@ def run_c2(n, procs):
             parts = pool.map(_c2_chunk, [(r, n, procs) for r in range(procs)])
             el = time.perf_counter() - t0
         done, inf = sum(p[0] for p in parts), sum(p[1] for p in parts)
-    return {"config": "C2", "scenarios": done, "infeasible": inf, "seconds": el, "scenarios_per_s": done / el,
-            "procs": procs}
+    return {"config": "C2" if seed == 0 else f"C2 generator, seed {seed}", "scenarios": done, "infeasible": inf,
+            "seconds": el, "scenarios_per_s": done / el, "procs": procs}
 
 
 def run_c5():
@@ -139,11 +158,18 @@ def run_c3(n):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("config", choices=["c2", "c3", "c5"])
+    ap.add_argument("config", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n", type=int, default=2000)
     ap.add_argument("--procs", type=int, default=1)
     a = ap.parse_args()
-    res = run_c2(a.n, a.procs) if a.config == "c2" else run_c3(a.n) if a.config == "c3" else run_c5()
+    if a.config == "c1":
+        res = run_c1()
+    elif a.config in ("c2", "c4"):
+        res = run_c2(a.n, a.procs, seed=0 if a.config == "c2" else 1)
+    elif a.config == "c3":
+        res = run_c3(a.n)
+    else:
+        res = run_c5()
     res["python"] = sys.version.split()[0]
     res["reference"] = "migplan (baseline/_ref, unmodified)"
     print(json.dumps(res), flush=True)
