@@ -881,3 +881,20 @@ def test_plan_many_zero_copy_and_copy_paths(fx):
     for k in (0, 99, 777):
         r = P.plan_many([sets[k]], fx.tables)[0]
         assert canon.digest(_canon_result(r)) == g["digests"][k], k
+
+
+def test_general_kernel_global_memory_chain(fx):
+    """A C5-like allocation too large for KG's shared-memory GPU state
+    (> ~110k GPUs before optimize): the optimize chain runs on global memory
+    (opt_chain<false>).  Same deployment map, ledger and diagnostics as the
+    oracle (the C restatement with the reference's cursors)."""
+    from helpers import map_canon
+    rates = W.c5_rates(n=120_000, seed=7)
+    n = len(rates)
+    svcs = [P.make_service(f"d121#{i}", W.C5_MODEL, float(r), W.C5_SLO) for i, r in enumerate(rates)]
+    res = P.plan_services(svcs, fx.tables)
+    pt = pack_tables(fx.tables)
+    t = pt.index_of()[W.C5_MODEL]
+    _, ores = oracle.plan_scenario(pt, np.full(n, t), rates, np.full(n, W.C5_SLO / 2.0), True, 4, gcap=400_000)
+    assert res.unoptimized_gpu_count == ores["unopt"] > 115_000
+    assert canon.dmap(res.deployment) == map_canon(ores, [s.id for s in svcs])
