@@ -898,3 +898,29 @@ def test_general_kernel_global_memory_chain(fx):
     _, ores = oracle.plan_scenario(pt, np.full(n, t), rates, np.full(n, W.C5_SLO / 2.0), True, 4, gcap=400_000)
     assert res.unoptimized_gpu_count == ores["unopt"] > 115_000
     assert canon.dmap(res.deployment) == map_canon(ores, [s.id for s in svcs])
+
+
+@pytest.mark.parametrize("with_index", [False, True])
+def test_plan_batch_dense_tables_vs_oracle(with_index):
+    """Scenarios over the C3 dense tables (up to 1,024 points per size):
+    without the prefix-argmax index K1 configures and the tile kernel plans
+    (parva_plan_batch_preconfigured); with it, the thread kernel searches the
+    index through L1.  Records byte-equal to the oracle's."""
+    dt_h = W.dense_tables(300, seed=3)
+    pt = pack_dense(dt_h)
+    dt = N.DeviceTables(pt, build_index=with_index)
+    assert (dt.index_struct is not None) == with_index
+    rng = np.random.default_rng(11)
+    n = 600
+    sizes = rng.integers(1, 9, n)
+    off = np.zeros(n + 1, dtype=np.int32)
+    off[1:] = np.cumsum(sizes)
+    m = int(off[-1])
+    tab = rng.integers(0, dt_h.n_workloads, m).astype(np.int32)
+    rate = np.exp(rng.uniform(np.log(10.0), np.log(3000.0), m))
+    bound = np.exp(rng.uniform(np.log(20.0), np.log(2000.0), m)) / 2.0
+    cfg, plan = B.plan_batch(dt, off, tab, rate, bound).host()
+    ocfg, oplan = oracle.plan_batch_records(pt, off, tab, rate, bound)
+    assert cfg.tobytes() == ocfg.tobytes()
+    assert plan.tobytes() == oplan.tobytes()
+    assert (plan["status"] == 0).sum() > n // 4          # mostly real plans, not errors
