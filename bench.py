@@ -714,7 +714,7 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     (prepacked), and one synchronous call per step."""
     import oracle
     from paper_2409_14447_b200.records import tiny_config
-    E2E_DEPTH, E2E_BATCHES = 5, 8
+    E2E_DEPTH, E2E_BATCHES = int(os.environ.get("PARVA_E2E_DEPTH", 5)), 8
     # a throughput over at least 300 steps: a 20-step run would mostly time
     # the pipeline's fill and drain (5 calls in flight)
     steps = max(args.steps, 300)
