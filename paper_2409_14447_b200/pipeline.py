@@ -240,7 +240,7 @@ class _PinnedArena:
     def views(self, n: int, m: int):
         torch = N.require_cuda()
         up = lambda x: (x + 255) & ~255  # noqa: E731
-        sizes = [4 * (n + 1), 4 * m, 8 * m, 8 * m, 32 * m, 128 * n]
+        sizes = [4 * (n + 1), 4 * m, 8 * m, 8 * m, 32 * max(m, 1), 128 * max(n, 1)]   # >= 1 record each
         offs, tot = [], 0
         for b in sizes:
             offs.append(tot)
