@@ -107,27 +107,37 @@ def triplet_at(pt, t: int, c: int, j: int) -> Triplet:
     return tr
 
 
-_SERVICE_INIT = Service.__init__
 
 
 def service_from_record(svc: Service, pt, t: int, rec) -> Service:
     """Configured Service from a config record (status must be OK): a numpy
-    record, or the same record as a tuple (records.tolist())."""
+    record, or the same record as a tuple (records.tolist()).  The triplet
+    part (best per size, optimal, last) is shared by every service of table
+    t with the same record positions (Triplets are immutable)."""
     if isinstance(rec, tuple):
         bests, o, l, count = rec[0], rec[1], rec[2], rec[6]
     else:
         bests, o, l, count = rec["best"].tolist(), int(rec["opt_sc"]), int(rec["last_sc"]), int(rec["count"])
-    best = [None] * 5
-    cache, seg = _triplet_cache(pt)
-    for c in range(5):
-        j = bests[c]
-        if j >= 0:
-            tr = cache.get(seg[t * 5 + c] + j)
-            best[c] = tr if tr is not None else triplet_at(pt, t, c, j)
-    out = object.__new__(Service)
-    _SERVICE_INIT(out, svc.id, svc.model_id, svc.request_rate, svc.slo_latency, svc.internal_latency,
-                  tuple(b for b in best if b is not None), best[o] if o >= 0 else None, int(count),
-                  best[l] if l >= 0 else None)
+    d = pt.__dict__
+    kinds = d.get("_service_kinds")
+    if kinds is None:
+        kinds = d["_service_kinds"] = {}
+    key = (t, *bests, o, l)
+    v = kinds.get(key)
+    if v is None:
+        best = [None] * 5
+        cache, seg = _triplet_cache(pt)
+        for c in range(5):
+            j = bests[c]
+            if j >= 0:
+                tr = cache.get(seg[t * 5 + c] + j)
+                best[c] = tr if tr is not None else triplet_at(pt, t, c, j)
+        v = kinds[key] = (tuple([b for b in best if b is not None]), best[o] if o >= 0 else None,
+                          best[l] if l >= 0 else None)
+    out = object.__new__(Service)     # frozen dataclass: fill its __dict__ directly (what __init__ stores)
+    out.__dict__.update(id=svc.id, model_id=svc.model_id, request_rate=svc.request_rate,
+                        slo_latency=svc.slo_latency, internal_latency=svc.internal_latency, best_triplets=v[0],
+                        optimal_segment=v[1], optimal_segment_count=int(count), last_segment=v[2])
     return out
 
 

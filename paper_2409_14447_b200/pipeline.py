@@ -10,6 +10,7 @@ path's record limits are re-planned by the general kernel on the GPU.
 
 from __future__ import annotations
 
+import struct
 import time
 from dataclasses import dataclass, field
 from typing import Mapping, Optional, Sequence
@@ -77,24 +78,39 @@ def prepare_tables(tables: Mapping[str, ProfileTable], options: PlanOptions) -> 
 
 
 def _decode_record(services: list[Service], rec) -> DeploymentMap:
-    """DeploymentMap from a 128-byte plan record (include/parva_b200.h)."""
-    places, diag_codes, ledger = plan_payload(rec)
+    """DeploymentMap from a 128-byte plan record (include/parva_b200.h):
+    `rec` is the record (numpy) or its 128 bytes."""
+    buf = rec.tobytes() if hasattr(rec, "tobytes") else rec
+    n_place, n_diag, n_ledger, flags = buf[4], buf[5], buf[6], buf[7]
+    u16 = struct.unpack_from(f"<{n_place + n_diag}H", buf, 8)
+    off = 8 + ((2 * (n_place + n_diag) + 7) & ~7)
+    vals = struct.unpack_from(f"<{n_ledger}d", buf, off)
+    keys = struct.unpack_from(f"<{n_ledger}H", buf, off + 8 * n_ledger)
     gpus: list[GpuState] = []
-    by_size = [{t.instance_size: t for t in s.best_triplets} for s in services]
-    for v in places:
-        g, cat, slot = unpack_place(v)
-        s, c = divmod(cat, 5)
-        if not gpus or gpus[-1].id != g:
-            gpus.append(GpuState(id=g))
-        t = by_size[s][INSTANCE_SIZES[c]]
-        gpus[-1].placements.append(Placement(services[s].id, t.instance_size, t.batch_size,
-                                             t.process_count, t.throughput, slot))
-    freed = {services[s].id: v for s, v in ledger}
-    if int(rec["flags"]) & FLAG_FALLBACK:
+    kinds: dict = {}
+    new_p = object.__new__
+    cur = None
+    for v in u16[:n_place]:
+        g, cat, slot = v >> 11, (v >> 3) & 0xFF, v & 7
+        if cur is None or cur.id != g:
+            cur = GpuState(id=g)
+            gpus.append(cur)
+        k = kinds.get(cat)
+        if k is None:
+            s, c = divmod(cat, 5)
+            size = INSTANCE_SIZES[c]
+            t = next(x for x in services[s].best_triplets if x.instance_size == size)
+            k = kinds[cat] = (services[s].id, size, t.batch_size, t.process_count, t.throughput)
+        p = new_p(Placement)              # frozen dataclass: fill its __dict__ directly
+        p.__dict__.update(service_id=k[0], instance_size=k[1], batch_size=k[2], process_count=k[3],
+                          throughput=k[4], start_slot=slot)
+        cur.placements.append(p)
+    freed = {services[kk & 0xFF].id: v for kk, v in zip(keys, vals)}
+    if flags & FLAG_FALLBACK:
         diags = [format_diag(DIAG_REGRESSED, -1, None)]
     else:
         diags = []
-        for v in diag_codes:
+        for v in u16[n_place:]:
             g, reason, s = unpack_diag(v)
             diags.append(format_diag(reason, g, services[s].id))
     return DeploymentMap(gpus=gpus, freed_rate=freed, diagnostics=diags)
