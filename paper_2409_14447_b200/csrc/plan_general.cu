@@ -375,26 +375,13 @@ struct ChainSmem {
   double lv[8];      // staged ledger entries of the drained services (lane k: entry k)
   int32_t lo[8];
   int32_t undo[kChainUndo];
-  // warp 1 stages the next drain candidate's list while warp 0 drains
-  struct Stage {
-    int64_t index;     // the GPU staged (-1: none)
-    int32_t nl;
-    int32_t cat[8];
-    uint8_t slot[8];
-    CatExt ext[8];
-    double lv[8];
-    int32_t lo[8];
-  } st[2];
-  int64_t pub_index;   // warp 0 -> warp 1: the GPU being drained (-1: stop)
-  int32_t pub_buf;     // the buffer warp 1 fills
 };
 
-// named barriers between warp 0 (the chain) and warp 1 (the stager)
-__device__ __forceinline__ void chain_bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void chain_bar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
-
+// kSmem: GPU state and bitmaps in shared memory (dsm), so the
+// compiler emits shared-memory accesses instead of generic ones
 template <bool kSmem>
-__device__ __forceinline__ OptState chain_state(const GenWs& w, int64_t G0, uint8_t* dsm) {
+__device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, const parva_general_result& R,
+                                             const GenWs& w, int64_t G0, int lane, ChainSmem& C, uint8_t* dsm) {
   OptState S;
   const int64_t gpad = (G0 + 15) & ~int64_t(15);
   S.words = (G0 + 63) / 64;
@@ -403,53 +390,9 @@ __device__ __forceinline__ OptState chain_state(const GenWs& w, int64_t G0, uint
   S.Ln = kSmem ? dsm + gpad : w.len;
   S.A = kSmem ? reinterpret_cast<uint64_t*>(dsm + 2 * gpad) : w.acc;
   S.lw[0] = S.lw[1] = 0;
-  return S;
-}
-
-// Warp 1: while warp 0 drains GPU `cur`, load the list, catalogue entries
-// and ledger entries of the candidate below it (as things stand: warp 0
-// checks the GPU and its list length before using them, and reloads the
-// ledger entries of services its own drain touched)
-template <bool kSmem>
-__device__ void opt_stager(const parva_general_problem& P, const parva_general_result& R, const GenWs& w,
-                           int64_t G0, int lane, ChainSmem& C, uint8_t* dsm) {
-  const OptState S = chain_state<kSmem>(w, G0, dsm);
-  while (true) {
-    chain_bar_sync(1);
-    const int64_t cur = *reinterpret_cast<volatile int64_t*>(&C.pub_index);
-    if (cur < 0) break;
-    ChainSmem::Stage& B = C.st[*reinterpret_cast<volatile int32_t*>(&C.pub_buf)];
-    const int64_t spec = S.prev_candidate(cur - 1, P.threshold);
-    const int nl = spec >= 0 ? S.Ln[spec] : 0;
-    if (lane < nl) {
-      const int cat = w.lcat[spec * 7 + lane];
-      B.cat[lane] = cat;
-      B.slot[lane] = w.lslot[spec * 7 + lane];
-      const CatExt X = w.ext[cat];
-      B.ext[lane] = X;
-      if (X.name < P.n_services) {
-        B.lv[lane] = R.d_ledger_val[X.name];
-        B.lo[lane] = R.d_ledger_order[X.name];
-      }
-    }
-    if (lane == 0) { B.index = spec; B.nl = nl; }
-    __syncwarp();
-    chain_bar_arrive(2);
-  }
-}
-
-// kSmem: GPU state and bitmaps in shared memory (dsm), so the
-// compiler emits shared-memory accesses instead of generic ones
-template <bool kSmem>
-__device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, const parva_general_result& R,
-                                             const GenWs& w, int64_t G0, int lane, ChainSmem& C, uint8_t* dsm) {
-  OptState S = chain_state<kSmem>(w, G0, dsm);
   int32_t next = (int32_t)w.hdr[3];
   int64_t nd = 0;
-  int64_t index = S.prev_candidate(G0 - 1, P.threshold);
-  int sb = 0;                  // the stage buffer warp 1 filled during the previous drain
-  bool staged = false;
-  int prev_nl = 0;
+  int64_t idx = G0 - 1;
 #ifdef PARVA_KG_PROF   // phase cycle counters of the serial chain (probe builds only)
   long long kp[6] = {0, 0, 0, 0, 0, 0}, kn_drain = 0, kn_place = 0, kt = clock64();
 #define KG_MARK(i) do { const long long c_ = clock64(); kp[i] += c_ - kt; kt = c_; } while (0)
@@ -457,35 +400,12 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
 #define KG_MARK(i) do { } while (0)
 #endif
   while (true) {
-    if (index < 0) {
-      if (lane == 0) C.pub_index = -1;
-      __syncwarp();
-      chain_bar_arrive(1);      // warp 1 stops
-      break;
-    }
+    const int64_t index = S.prev_candidate(idx, P.threshold);
+    if (index < 0) break;
     KG_MARK(0);
+    idx = index - 1;
     const int nl = S.Ln[index];
-    const ChainSmem::Stage& B = C.st[sb];
-    if (staged && B.index == index && B.nl == nl) {
-      // warp 1's copy: entries below the list length never change while the
-      // length is unchanged; reload the ledger entries of services the
-      // previous drain wrote (their staged values may predate the writes)
-      int cat = 0, slot = 0, name = 0;
-      CatExt X;
-      double lv = 0.0;
-      int32_t lo = 0;
-      bool fresh = false;
-      if (lane < nl) {
-        cat = B.cat[lane]; slot = B.slot[lane]; X = B.ext[lane]; lv = B.lv[lane]; lo = B.lo[lane];
-        name = X.name;
-        for (int j = 0; j < prev_nl; j++) fresh |= C.ext[j].name == name;
-      }
-      __syncwarp();
-      if (lane < nl) {
-        if (fresh && name < P.n_services) { lv = R.d_ledger_val[name]; lo = R.d_ledger_order[name]; }
-        C.cat[lane] = cat; C.slot[lane] = (uint8_t)slot; C.ext[lane] = X; C.lv[lane] = lv; C.lo[lane] = lo;
-      }
-    } else if (lane < nl) {     // lane k stages entry k of the drained list
+    if (lane < nl) {            // lane k stages entry k of the drained list
       const int cat = w.lcat[index * 7 + lane];
       C.cat[lane] = cat;
       C.slot[lane] = w.lslot[index * 7 + lane];
@@ -496,9 +416,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
         C.lo[lane] = R.d_ledger_order[X.name];
       }
     }
-    if (lane == 0) { C.pub_index = index; C.pub_buf = sb ^ 1; }
     __syncwarp();
-    chain_bar_arrive(1);        // warp 1 stages the candidate below this one
     KG_MARK(1);
     const int32_t sv_next = next;
     int fail = -1, rot = nl, nlog = 0;
@@ -600,13 +518,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
       S.Ln[index] = 0;
       S.set_bits(index, 0u);
     }
-    const int64_t nxt = S.prev_candidate(index - 1, P.threshold);
     __syncwarp();                 // C is restaged by the next drain
-    chain_bar_sync(2);            // warp 1's staging of the candidate below is complete
-    sb ^= 1;
-    staged = true;
-    prev_nl = nl;
-    index = nxt;
     KG_MARK(4);
   }
 #ifdef PARVA_KG_PROF
@@ -673,9 +585,6 @@ __global__ void __launch_bounds__(OPT_THREADS) plan_general_kernel(parva_general
     const int64_t nd = in_smem ? opt_chain<true>(P, R, w, G0, lane, chain, dsm)
                                : opt_chain<false>(P, R, w, G0, lane, chain, dsm);
     if (lane == 0) s_nd = nd;
-  } else if (run && warp == 1) {
-    if (in_smem) opt_stager<true>(P, R, w, G0, lane, chain, dsm);
-    else opt_stager<false>(P, R, w, G0, lane, chain, dsm);
   }
   __syncthreads();
 
