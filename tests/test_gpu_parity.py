@@ -924,3 +924,32 @@ def test_plan_batch_dense_tables_vs_oracle(with_index):
     assert cfg.tobytes() == ocfg.tobytes()
     assert plan.tobytes() == oplan.tobytes()
     assert (plan["status"] == 0).sum() > n // 4          # mostly real plans, not errors
+
+
+@pytest.mark.parametrize("threshold", [0, 1, 3, 6, 7, 9])
+def test_general_kernel_thresholds_vs_oracle(fx, threshold):
+    """KG's optimize chain across drain thresholds (0: nothing drains; >= 7:
+    every non-empty GPU is a candidate) on a C5-like allocation with mixed
+    models, against the oracle: maps, ledger and diagnostics equal."""
+    from helpers import map_canon
+    rng = np.random.default_rng(threshold)
+    models = list(fx.models)
+    n = 3000
+    pick = rng.integers(0, len(models), n)
+    svcs, tab, rates, bounds = [], [], [], []
+    pt = pack_tables(fx.tables)
+    idx = pt.index_of()
+    for i in range(n):
+        m = models[pick[i]]
+        lat = [p.latency for p in fx.tables[m].points]
+        slo = float(rng.uniform(2.5 * min(lat), 2.5 * max(lat)))
+        rate = float(rng.uniform(10.0, 3000.0))
+        svcs.append(P.make_service(f"s{i}", m, rate, slo))
+        tab.append(idx[m]); rates.append(rate); bounds.append(slo / 2.0)
+    ocfg, ores = oracle.plan_scenario(pt, np.array(tab), np.array(rates), np.array(bounds), True, threshold,
+                                      gcap=100_000)
+    if (ocfg["status"] != 0).any():
+        pytest.skip("an infeasible service in this draw")
+    res = P.plan_services(svcs, fx.tables, P.PlanOptions(threshold=threshold))
+    assert res.unoptimized_gpu_count == ores["unopt"]
+    assert canon.dmap(res.deployment) == map_canon(ores, [s.id for s in svcs])
