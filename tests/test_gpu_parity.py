@@ -953,3 +953,33 @@ def test_general_kernel_thresholds_vs_oracle(fx, threshold):
     res = P.plan_services(svcs, fx.tables, P.PlanOptions(threshold=threshold))
     assert res.unoptimized_gpu_count == ores["unopt"]
     assert canon.dmap(res.deployment) == map_canon(ores, [s.id for s in svcs])
+
+
+def test_concurrent_planning_threads(fx):
+    """Disjoint runs may execute concurrently: four host
+    threads plan different scenario sets at once through the public API
+    (small calls on the zero-copy path, larger ones on device copies); every
+    result equals the single-threaded one."""
+    import threading
+    g = golden("c2_digests.json")
+    sb = W.scenario_batch(fx, 1600, seed=g["seed"])
+    sets = [[P.make_service(m, m, float(sb.rate[k, j]), float(sb.slo[k, j])) for j, m in enumerate(sb.models)]
+            for k in range(1600)]
+    jobs = [(0, 1), (1, 300), (300, 301), (301, 1600), (5, 6), (6, 1100)]
+    errors = []
+
+    def worker(t):
+        try:
+            for rep in range(3):
+                for a, b in jobs[t::4] if t < 4 else []:
+                    for k, r in enumerate(P.plan_many(sets[a:b], fx.tables), start=a):
+                        if canon.digest(_canon_result(r)) != g["digests"][k]:
+                            errors.append((t, rep, k))
+        except Exception as exc:  # noqa: BLE001
+            errors.append((t, repr(exc)))
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors[:5]
