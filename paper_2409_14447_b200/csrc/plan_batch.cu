@@ -420,7 +420,7 @@ __device__ __forceinline__ IndexView load_index(const PlanArgs& A, uint8_t* base
 // config record store, words assembled in registers (no local copy)
 __device__ __forceinline__ void store_config(const PlanArgs& A, int64_t i, const parva_config_record& r) {
   void* cfg = A.cfg;
-#ifdef PARVA_NO_OUT
+#if defined(PARVA_NO_OUT) || defined(PARVA_NO_CFG_OUT)
   if (A.stream_src) return;   // development probe: PCIe reads without the record writes
 #endif
   const uint32_t b01 = (uint16_t)r.best[0] | (uint32_t)(uint16_t)r.best[1] << 16;
@@ -809,7 +809,7 @@ __device__ __forceinline__ bool plan_scenario_warp(const PlanArgs& A, GScratch<G
   }
   gp.sync();
   uint8_t* dst = reinterpret_cast<uint8_t*>(A.plan) + (size_t)k * A.plan_bytes;
-#ifdef PARVA_NO_OUT
+#if defined(PARVA_NO_OUT) || defined(PARVA_NO_PLAN_OUT)
   if (A.stream_src) { gp.sync(); return true; }
 #endif
   if (status == PARVA_OK && spill && A.spill_direct) {
