@@ -8,6 +8,7 @@
 #include <condition_variable>
 #include <functional>
 #include <thread>
+#include <sched.h>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -709,9 +710,17 @@ PackPool& pack_pool() {
   // pack; one more core stays free for a thread waiting on the GPU -- the
   // workers spin, and an oversubscribed core stalls a whole pack for a
   // scheduler quantum)
+  // cores: this process's CPU affinity; with one process per GPU
+  // (LOCAL_WORLD_SIZE from torchrun) and no launcher pinning, its share
   static PackPool pool([] {
     const char* e = std::getenv("PARVA_PACK_THREADS");
-    const int hw = (int)std::thread::hardware_concurrency();
+    const int all = (int)std::thread::hardware_concurrency();
+    int hw = all;
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0 && CPU_COUNT(&set) > 0) hw = CPU_COUNT(&set);
+    const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+    const int ranks = (lw && *lw) ? std::max(1, std::atoi(lw)) : 1;
+    if (hw >= all && ranks > 1) hw = std::max(1, hw / ranks);
     int n = (e && *e) ? std::atoi(e) : hw - 1;
     return std::max(0, std::min(n, 64) - 1);
   }());
