@@ -1262,19 +1262,19 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
     const Grp<16> gh{0xFFFFu << (16 * h), 16 * h};
     GScratch<16>& Wh = reinterpret_cast<GScratch<16>*>(area)[h];
     GSvc<16>& Sh = reinterpret_cast<GSvc<16>*>(&wsvc[warp])[h];
-    volatile int* stop = &stop_flag[warp];
+    int* stop = &stop_flag[warp];       // cross-half signal: shared-memory atomics (no plain racing accesses)
     ChunkCursor C, Cw;
     bool out = false;                                  // this half saw the tickets run out
     for (;;) {
       int pend = -1;
-      while (!out && !*stop) {
+      while (!out && !atomicAdd(stop, 0)) {
         int j = 0;
         if (hl == 0) j = (int)atomicAdd(&A.work[0], 1u);
         j = gh.shfl(j, 0);
         if (j >= A.n_scen) { out = true; break; }
         if (!stream_plan_one<16>(A, V, Wh, Sh, C, j, n_ch, ch_scen, hl, gh)) {
           pend = j;
-          if (hl == 0) *stop = 1;
+          if (hl == 0) atomicExch(stop, 1);
         }
       }
       __syncwarp();
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(PB_THREADS, PARVA_PB_MINB) plan_warp_kernel(Pl
       if (p1 >= 0)
         stream_plan_one<32>(A, V, *reinterpret_cast<GScratch<32>*>(area), wsvc[warp], Cw, p1, n_ch, ch_scen, lane, gw);
       if (__all_sync(0xffffffffu, out)) break;
-      if (lane == 0) *stop = 0;
+      if (lane == 0) atomicExch(stop, 0);
       __syncwarp();
     }
   }

@@ -292,7 +292,9 @@ __device__ inline double unalloc_g(int64_t total, int64_t n) {
 // Optimize (allocator.py:362-443) as a serial chain walked by warp 0 in
 // lock step: every lane executes the same scalar chain on the same values
 // (shared-memory reads are broadcasts, same-address stores coalesce), so the
-// chain needs no shuffles, no per-step warp barriers and no divergence;
+// chain needs no shuffles and no divergence; a __syncwarp separates every
+// read of shared state from the lanes' identical writes of it (the chain
+// does not rely on lock-step execution: compute-sanitizer racecheck clean);
 // the warp's lanes only split the loads of a drained list and the proposal
 // search (propose_small_warp).  GPU state (8-bit mask + list length) and the
 // accepts bitmaps of size classes 1 and 2 -- the only sizes a proposal has
@@ -321,10 +323,12 @@ struct OptState {
     const bool acc0 = m != 0x7Fu;                                                     // find_start(m, 0) >= 0
     const bool acc1 = (m & 0x03u) == 0 || (m & 0x0Cu) == 0 || (m & 0x30u) == 0;        // find_start(m, 1) >= 0
     const uint64_t a0 = A[k], a1 = A[words + k];
+    __syncwarp();   // every lane has read the words before any lane writes them
     A[k] = acc0 ? (a0 | bit) : (a0 & ~bit);
     A[words + k] = acc1 ? (a1 | bit) : (a1 & ~bit);
     if (acc0 && k < lw[0]) lw[0] = k;
     if (acc1 && k < lw[1]) lw[1] = k;
+    __syncwarp();   // the lanes wrote the same words: ordered before any lane reads them again
   }
 
   // first GPU in list order accepting class c (0 or 1), skipping `excl`:
@@ -444,6 +448,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
       C.k2[k] = k2; C.k1[k] = k1;
       for (int j = k + 1; j < nl; j++)   // a later entry of the same service sees this update
         if (C.ext[j].name == s) { C.lv[j] = v; C.lo[j] = no; }
+      __syncwarp();
     }
     KG_MARK(2);
     int64_t nu = 0;
@@ -467,6 +472,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
               const int st = find_start(m8 & 0x7Fu, c);
               const int ln = S.Ln[g];
               const uint32_t nm = m8 | footprint(c, st);
+              __syncwarp();             // every lane has read the GPU's state before any lane updates it
               S.M[g] = (uint8_t)nm;
               S.Ln[g] = (uint8_t)(ln + 1);
               w.lcat[g * 7 + ln] = cat;
@@ -474,6 +480,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
               const int32_t u = (int32_t)(g << 4 | c << 3 | st);   // g < 2^27
               if (nu < kChainUndo) C.undo[nu] = u; else w.undo[nu] = u;
               nu++;
+              __syncwarp();
               S.set_bits(g, nm);
             }
           }
@@ -484,8 +491,10 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
             const int64_t g = u >> 4;
             const int c = (u >> 3) & 1, st = u & 7;
             const uint32_t nm = S.M[g] & ~footprint(c, st);
+            const int ln = S.Ln[g];
+            __syncwarp();
             S.M[g] = (uint8_t)nm;
-            S.Ln[g] = (uint8_t)(S.Ln[g] - 1);
+            S.Ln[g] = (uint8_t)(ln - 1);
             S.set_bits(g, nm);
           }
         }
@@ -502,6 +511,7 @@ __device__ __forceinline__ int64_t opt_chain(const parva_general_problem& P, con
         w.lcat[index * 7 + lane] = C.cat[src];
         w.lslot[index * 7 + lane] = C.slot[src];
       }
+      __syncwarp();                 // (the loop above may have left before its barrier)
       for (int k = nlog - 1; k >= 0; k--) {   // ledger rollback in reverse log order
         R.d_ledger_val[C.lg_name[k]] = C.lg_val[k];
         R.d_ledger_order[C.lg_name[k]] = C.lg_ord[k];
