@@ -714,7 +714,8 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     (prepacked), and one synchronous call per step."""
     import oracle
     from paper_2409_14447_b200.records import tiny_config
-    E2E_DEPTH, E2E_BATCHES = int(os.environ.get("PARVA_E2E_DEPTH", 5)), 8
+    E2E_DEPTH, E2E_BATCHES, E2E_SPANS = int(os.environ.get("PARVA_E2E_DEPTH", 5)), 8, 5
+    span_s = []
     # a throughput over at least 300 steps: a 20-step run would mostly time
     # the pipeline's fill and drain (5 calls in flight)
     steps = max(args.steps, 300)
@@ -747,9 +748,14 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
         loop(0, c0)
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
-        loop(c0, steps)
-        e2e_s = time.perf_counter() - t0
+        # E2E_SPANS spans of `steps` steps each (the pipeline drains between
+        # spans); the median span is the value: one host scheduling hiccup of
+        # a few ms inside a ~15 ms span would otherwise move it by 10-20%
+        for r in range(E2E_SPANS):
+            t0 = time.perf_counter()
+            loop(c0 + r * steps, steps)
+            span_s.append(time.perf_counter() - t0)
+        e2e_s = statistics.median(span_s)
     h2d = mb.h2d_bytes
     # the records of the last batch planned in every slot against the oracle
     ok = True
@@ -796,6 +802,8 @@ def e2e_measure(args, torch, dist, world, N, B, fx, dt, shard_inputs, P, n_globa
     step_us = e2e_s / steps * 1e6
     floor_us = max(mb.h2d_bytes / p_h2d, mb.d2h_bytes / p_d2h, (mb.h2d_bytes + mb.d2h_bytes) / p_bi) / 1e3
     return {"value": K / e2e_s, "unit": UNIT, "steps": steps,
+            "spans": {"n": len(span_s), "steps_each": steps, "value_per_span": [n_global * steps / x for x in span_s],
+                      "value": "the median span"} if span_s else None,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": mb.d2h_bytes,
             "api": "per step one C call, parva_plan_host_arrays_submit: wait for the slot's previous call, pack the "
                    "plain host arrays into the slot's pinned streamed block (parva_stream_pack_arrays, on the "
