@@ -244,6 +244,7 @@ struct WarpArrivals {
 
   // 32 more draws -> the gaps they complete, in order (warp-collective)
   __device__ __noinline__ void refill(SimWarp& W) {
+    __syncwarp();                  // every lane's reads of the old samples precede the overwrite
     cnt = 0;
     head = 0;
     do {
@@ -291,6 +292,7 @@ struct WarpArrivals {
   // per-chunk cumsum plus the previous chunk's last time (a sequential
   // chain), or the grid i * step; false once the horizon is reached
   __device__ __noinline__ bool fill(SimWarp& W) {
+    __syncwarp();                  // every lane's reads of the old times precede the overwrite
     th = tn = 0;
     while (!done && tn == 0) {
       if (kind == 1) {
