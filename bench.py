@@ -21,9 +21,11 @@ all-gather of the packed 128-byte records instead.  After the timed region
 every rank checks its gathered copy of every timed step against the CPU
 oracle (digests of each rank's own shard, exchanged once).
 
-Also reported: e2e through the C-ABI host entry, the C3 configurator sweep
-(the HBM-roofline kernel; sharded across ranks at N > 1 with one all-gather
-of config records), C4 (10^6 scenarios; sharded at N > 1), C5, the batched
+Also reported: e2e through the C-ABI host entry from plain host arrays
+(median of five 300-step spans, with the PCIe floor of its bytes), the C3
+configurator sweep (the HBM-roofline kernel; sharded across ranks at N > 1
+with one all-gather of config records), C4 (10^6 scenarios; sharded at
+N > 1), C5, C1 (the fixture scenarios through the public API), the batched
 simulator, and the CPU baselines (the C oracle = a port of the reference,
 and the reference's own Python planner when baseline/_ref is installed).
 """
