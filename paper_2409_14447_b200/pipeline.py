@@ -135,10 +135,19 @@ def _decode_general(services: list[Service], g, out) -> DeploymentMap:
         return v
 
     pl_cat, pl_slot, pl_off = out.pl_cat.tolist(), out.pl_slot.tolist(), out.pl_off.tolist()
+    new_o = object.__new__
+    _fields = ("service_id", "instance_size", "batch_size", "process_count", "throughput", "start_slot")
+
+    def placement(cat, slot):       # frozen dataclass: fill its __dict__ directly (what __init__ stores)
+        p = new_o(Placement)
+        p.__dict__.update(zip(_fields, (*kind(cat), slot)))
+        return p
+
     gpus = []
     for k, gid in enumerate(out.gpu_id.tolist()):
-        gpus.append(GpuState(id=gid, placements=[Placement(*kind(pl_cat[j]), pl_slot[j])
-                                                 for j in range(pl_off[k], pl_off[k + 1])]))
+        g = new_o(GpuState)
+        g.__dict__.update(id=gid, placements=[placement(pl_cat[j], pl_slot[j]) for j in range(pl_off[k], pl_off[k + 1])])
+        gpus.append(g)
     order = out.ledger_order
     live = np.flatnonzero(order[:len(services)])
     ranks = live[np.argsort(order[live], kind="stable")].tolist()
